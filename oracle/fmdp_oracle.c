@@ -1,0 +1,544 @@
+/*
+ * fmdp_oracle.c -- plain, slow, obviously-correct CPU oracle of the FastMDP-GPU
+ * hot path (arXiv 2008.03518).  TEST INFRASTRUCTURE ONLY (see fmdp_oracle.h).
+ *
+ * Style: direct loops in the order of the paper's algorithms, fp64 for values,
+ * int64 for every distance predicate, libm pow/sqrt.  No blocking, no fusion, no
+ * min-distance identity, no culling: every (projected state, peak) pair is
+ * evaluated as Algs 4, 6, 7 state it.
+ *
+ * Build: gcc -O2 -ffp-contract=off -fno-fast-math -fPIC -shared -o liboracle.so fmdp_oracle.c -lm
+ */
+#include "fmdp_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------- */
+/* Parameter conversion to integer units (R23: u-quantised world).  */
+/* ------------------------------------------------------------------------- */
+
+/* x / u must be an integer (all scenario lengths are multiples of u). */
+static int to_units(double x, double u, int64_t* out) {
+  double r = x / u;
+  double n = rint(r);
+  if (!(fabs(r - n) <= 1e-9 * (1.0 + fabs(r)))) return ORC_E_ARG;
+  *out = (int64_t)n;
+  return ORC_OK;
+}
+
+typedef struct conv {
+  int64_t step_u;                 /* v0*dt/u                          */
+  int64_t k_tau[ORC_MAX_TAU];     /* tau/dt substeps (Table PK)   */
+  int64_t R_tau[ORC_MAX_TAU];     /* 300+10 tau metres -> units         */
+  int64_t R_max;
+  int64_t zdeck_u, cap_u, sep_u;
+} conv;
+
+static int convert(const orc_params* p, conv* c) {
+  if (!p || p->u_m <= 0 || p->dt_s <= 0 || p->W < 1 || p->HL < 8 || (p->HL % 8) != 0) return ORC_E_ARG;
+  if (p->n_turn < 1 || p->n_turn > ORC_MAX_TURN || p->n_climb < 1 || p->n_climb > ORC_MAX_CLIMB) return ORC_E_ARG;
+  if (p->n_tau < 0 || p->n_tau > ORC_MAX_TAU) return ORC_E_ARG;
+  if (to_units(p->speed_mps * p->dt_s, p->u_m, &c->step_u)) return ORC_E_ARG;
+  c->R_max = 0;
+  for (int i = 0; i < p->n_tau; ++i) {
+    double k = p->tau_s[i] / p->dt_s;
+    if (fabs(k - rint(k)) > 1e-9) return ORC_E_ARG;
+    c->k_tau[i] = (int64_t)rint(k);
+    if (to_units(p->tau_radius_m[i], p->u_m, &c->R_tau[i]) || c->R_tau[i] <= 0) return ORC_E_ARG;
+    if (c->R_tau[i] > c->R_max) c->R_max = c->R_tau[i];
+  }
+  if (to_units(p->deck_alt_m, p->u_m, &c->zdeck_u)) return ORC_E_ARG;
+  if (to_units(p->capture_m, p->u_m, &c->cap_u)) return ORC_E_ARG;
+  if (to_units(p->sep_m, p->u_m, &c->sep_u)) return ORC_E_ARG;
+  return ORC_OK;
+}
+
+int orc_check_params(const orc_params* p) {
+  conv c;
+  return convert(p, &c);
+}
+
+/* ------------------------------------------------------------------------- */
+/* Heading lattice (R14: dynamics deferred by the paper).     */
+/* D[psi] = L*(cos, sin)(2*pi*psi/HL) rounded, defined on the first octant and */
+/* reflected / rotated so the lattice is exactly symmetric.                    */
+/* ------------------------------------------------------------------------- */
+int orc_tables(const orc_params* p, int32_t* DX, int32_t* DY) {
+  conv c;
+  if (convert(p, &c)) return ORC_E_ARG;
+  const int HL = p->HL, Q = HL / 4, O = HL / 8;
+  const double L = (double)c.step_u;
+  for (int psi = 0; psi < HL; ++psi) {
+    int quad = psi / Q, r = psi % Q;
+    double a, b;  /* first-quadrant vector at lattice angle r */
+    if (r <= O) {
+      a = rint(L * cos(2.0 * M_PI * r / HL));
+      b = rint(L * sin(2.0 * M_PI * r / HL));
+    } else {
+      int m = Q - r; /* reflect about 45 degrees */
+      a = rint(L * sin(2.0 * M_PI * m / HL));
+      b = rint(L * cos(2.0 * M_PI * m / HL));
+    }
+    int32_t x, y;
+    switch (quad) {
+      case 0: x = (int32_t)a;  y = (int32_t)b;  break;
+      case 1: x = (int32_t)-b; y = (int32_t)a;  break;
+      case 2: x = (int32_t)-a; y = (int32_t)-b; break;
+      default: x = (int32_t)b; y = (int32_t)-a; break;
+    }
+    DX[psi] = x;
+    DY[psi] = y;
+  }
+  return ORC_OK;
+}
+
+static int32_t pmod(int64_t a, int32_t m) {
+  int64_t r = a % m;
+  return (int32_t)(r < 0 ? r + m : r);
+}
+
+/* Lattice heading nearest to the bearing src -> dst (R21). */
+int32_t orc_initial_heading(const orc_params* p, const int32_t src[3], const int32_t dst[3]) {
+  double dx = (double)dst[0] - (double)src[0];
+  double dy = (double)dst[1] - (double)src[1];
+  double a = atan2(dy, dx) * (double)p->HL / (2.0 * M_PI);
+  return pmod((int64_t)rint(a), p->HL);
+}
+
+/* ------------------------------------------------------------------------- */
+/* Build Peaks (Alg 2; Table PK): five wells per intruder at   */
+/* p + v*tau, radius 300 + 10 tau metres; v per substep (reading R11).         */
+/* ------------------------------------------------------------------------- */
+int orc_build_wells(const orc_params* p, const int32_t pos[3], const int32_t vel[3],
+                    int32_t* centers, int64_t* radius_u) {
+  conv c;
+  if (convert(p, &c)) return ORC_E_ARG;
+  for (int i = 0; i < p->n_tau; ++i) {
+    for (int d = 0; d < 3; ++d) centers[3 * i + d] = (int32_t)(pos[d] + c.k_tau[i] * (int64_t)vel[d]);
+    radius_u[i] = c.R_tau[i];
+  }
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Forward projection (Alg 3): the action (turn h, climb c) is held  */
+/* for W substeps; psi_t = psi_{t-1} + h, q_t = q_{t-1} + (DX,DY)[psi_t] + c.  */
+/* Action index a = i_turn * n_climb + i_climb.                                */
+/* ------------------------------------------------------------------------- */
+int orc_project(const orc_params* p, const int32_t q[3], int32_t psi, int32_t* states, int32_t* psi_out) {
+  int32_t* DX = (int32_t*)malloc(sizeof(int32_t) * p->HL);
+  int32_t* DY = (int32_t*)malloc(sizeof(int32_t) * p->HL);
+  if (!DX || !DY) { free(DX); free(DY); return ORC_E_NOMEM; }
+  if (orc_tables(p, DX, DY)) { free(DX); free(DY); return ORC_E_ARG; }
+  const int W = p->W;
+  for (int it = 0; it < p->n_turn; ++it) {
+    for (int ic = 0; ic < p->n_climb; ++ic) {
+      int a = it * p->n_climb + ic;
+      int64_t x = q[0], y = q[1], z = q[2];
+      int32_t h = psi;
+      for (int t = 1; t <= W; ++t) {
+        h = pmod((int64_t)h + p->turn_steps[it], p->HL);
+        x += DX[h];
+        y += DY[h];
+        z += p->climb_units[ic];
+        int idx = a * W + (t - 1);
+        states[3 * idx + 0] = (int32_t)x;
+        states[3 * idx + 1] = (int32_t)y;
+        states[3 * idx + 2] = (int32_t)z;
+        if (psi_out) psi_out[idx] = h;
+      }
+    }
+  }
+  free(DX);
+  free(DY);
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Peak values.                                                                */
+/* ------------------------------------------------------------------------- */
+static int64_t d2_of(const int32_t a[3], const int32_t b[3]) {
+  int64_t dx = (int64_t)a[0] - b[0], dy = (int64_t)a[1] - b[1], dz = (int64_t)a[2] - b[2];
+  return dx * dx + dy * dy + dz * dz;
+}
+
+/* Alg 4: V = |r| * gamma^d, d the Euclidean distance in metres (R10). */
+double orc_goal_value(const orc_params* p, int64_t d2) {
+  double d = p->u_m * sqrt((double)d2);
+  return fabs(p->goal_r) * pow(p->goal_gamma, d);
+}
+
+/* Algs 6/7 P:657-668: in = d < R; V = in * |r| * gamma^d (R12: exact d^2 < R^2). */
+double orc_well_value(double r, double gamma, double u_m, int64_t d2, int64_t R_u) {
+  int in = d2 < R_u * R_u;
+  if (!in) return 0.0;
+  double d = u_m * sqrt((double)d2);
+  return fabs(r) * pow(gamma, d);
+}
+
+/* Alg 1 P:207-210 with the projected altitude (R6) and z_deck in metres (R7). */
+double orc_deck_penalty(const orc_params* p, int32_t z) {
+  conv c;
+  if (convert(p, &c)) return NAN;
+  if ((int64_t)z < c.zdeck_u) return p->deck_scale - p->u_m * (double)z;
+  return 0.0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Accepted-plan store (Sec. V: "a simple table in memory").             */
+/* ------------------------------------------------------------------------- */
+struct orc_store {
+  int32_t n, cap;
+  int64_t* t0;
+  int32_t* len;
+  int32_t** states;
+};
+
+orc_store* orc_store_new(void) {
+  orc_store* s = (orc_store*)calloc(1, sizeof(orc_store));
+  return s;
+}
+
+void orc_store_free(orc_store* s) {
+  if (!s) return;
+  for (int i = 0; i < s->n; ++i) free(s->states[i]);
+  free(s->t0);
+  free(s->len);
+  free(s->states);
+  free(s);
+}
+
+int orc_store_add(orc_store* s, int64_t t0, int32_t n, const int32_t* states) {
+  if (!s || n < 1 || !states || t0 < 0) return ORC_E_ARG;
+  if (s->n == s->cap) {
+    int32_t nc = s->cap ? 2 * s->cap : 64;
+    int64_t* a = (int64_t*)realloc(s->t0, sizeof(int64_t) * nc);
+    if (!a) return ORC_E_NOMEM;
+    s->t0 = a;
+    int32_t* b = (int32_t*)realloc(s->len, sizeof(int32_t) * nc);
+    if (!b) return ORC_E_NOMEM;
+    s->len = b;
+    int32_t** c = (int32_t**)realloc(s->states, sizeof(int32_t*) * nc);
+    if (!c) return ORC_E_NOMEM;
+    s->states = c;
+    s->cap = nc;
+  }
+  int32_t* copy = (int32_t*)malloc(sizeof(int32_t) * 3 * (size_t)n);
+  if (!copy) return ORC_E_NOMEM;
+  memcpy(copy, states, sizeof(int32_t) * 3 * (size_t)n);
+  s->t0[s->n] = t0;
+  s->len[s->n] = n;
+  s->states[s->n] = copy;
+  s->n += 1;
+  return ORC_OK;
+}
+
+int32_t orc_store_count(const orc_store* s) { return s ? s->n : 0; }
+
+/* Intruder position and linear velocity at row K (reading R11): the stored
+ * state, and the forward difference to the next stored state (the last state
+ * repeats the previous difference; a single-state plan has v = 0).
+ * Returns 1 if the plan is active at K, else 0. */
+int orc_store_sample(const orc_store* s, int32_t plan, int64_t K, int32_t pos[3], int32_t vel[3]) {
+  if (!s || plan < 0 || plan >= s->n) return 0;
+  int64_t i = K - s->t0[plan];
+  int32_t n = s->len[plan];
+  if (i < 0 || i >= n) return 0;
+  const int32_t* st = s->states[plan];
+  for (int d = 0; d < 3; ++d) pos[d] = st[3 * i + d];
+  if (n == 1) {
+    vel[0] = vel[1] = vel[2] = 0;
+  } else if (i < n - 1) {
+    for (int d = 0; d < 3; ++d) vel[d] = st[3 * (i + 1) + d] - st[3 * i + d];
+  } else {
+    for (int d = 0; d < 3; ++d) vel[d] = st[3 * i + d] - st[3 * (i - 1) + d];
+  }
+  return 1;
+}
+
+/* Min d^2 from q to any plan active at row K, saturated at R_max^2 (Sec IV.I; R15, R20). */
+static int64_t nearest_d2(const orc_store* S, const int32_t q[3], int64_t K, int64_t sat) {
+  int64_t best = sat;
+  for (int32_t j = 0; j < orc_store_count(S); ++j) {
+    int32_t pos[3], vel[3];
+    if (!orc_store_sample(S, j, K, pos, vel)) continue;
+    int64_t d2 = d2_of(q, pos);
+    if (d2 < best) best = d2;
+  }
+  return best;
+}
+
+/* Terrain collision (R16): below z = 0 or below the height raster cell. */
+static int terrain_collision(const orc_terrain* T, const int32_t q[3]) {
+  if (q[2] < 0) return 1;
+  if (!T || T->nx <= 0 || T->ny <= 0 || !T->height) return 0;
+  int64_t rx = (int64_t)q[0] - T->x0, ry = (int64_t)q[1] - T->y0;
+  if (rx < 0 || ry < 0) return 0;
+  int64_t ix = rx / T->cell, iy = ry / T->cell;
+  if (ix >= T->nx || iy >= T->ny) return 0;
+  return q[2] < T->height[iy * (int64_t)T->nx + ix];
+}
+
+/* ------------------------------------------------------------------------- */
+/* One decision step: Algs 2-9 in the order of Fig 3a.             */
+/* ------------------------------------------------------------------------- */
+int orc_eval_step(const orc_params* p, const orc_terrain* T, const orc_store* S,
+                  const int32_t q[3], int32_t psi, const int32_t g[3], int64_t K, orc_step_out* out) {
+  conv c;
+  if (convert(p, &c) || !out) return ORC_E_ARG;
+  const int A = p->n_turn * p->n_climb, W = p->W, AW = A * W;
+  int32_t* proj = (int32_t*)malloc(sizeof(int32_t) * 3 * AW);
+  int32_t* ppsi = (int32_t*)malloc(sizeof(int32_t) * AW);
+  double* vpos = (double*)malloc(sizeof(double) * AW);
+  double* vint = (double*)malloc(sizeof(double) * AW);
+  double* vter = (double*)malloc(sizeof(double) * AW);
+  double* valt = (double*)malloc(sizeof(double) * AW);
+  double* v = (double*)malloc(sizeof(double) * AW);
+  double* scale = (double*)malloc(sizeof(double) * AW);
+  double* vstar = (double*)malloc(sizeof(double) * A);
+  double* vsc = (double*)malloc(sizeof(double) * A);
+  int rc = ORC_OK;
+  if (!proj || !ppsi || !vpos || !vint || !vter || !valt || !v || !scale || !vstar || !vsc) {
+    rc = ORC_E_NOMEM;
+    goto done;
+  }
+
+  /* Forward project (Alg 3). */
+  if ((rc = orc_project(p, q, psi, proj, ppsi))) goto done;
+
+  /* Process positive rewards (Alg 4): P+ = { goal } (Alg 2, Table PK, R8). */
+  for (int i = 0; i < AW; ++i) {
+    vpos[i] = 0.0;
+    double V = orc_goal_value(p, d2_of(&proj[3 * i], g));
+    if (V > vpos[i]) vpos[i] = V;  /* "Save max value" P:583-584 (single peak) */
+  }
+
+  /* Process negative terrain rewards (Alg 6). */
+  for (int i = 0; i < AW; ++i) {
+    vter[i] = 0.0;
+    for (int w = 0; T && w < T->n_wells; ++w) {
+      double V = orc_well_value(p->terr_r, p->terr_gamma, p->u_m, d2_of(&proj[3 * i], &T->center[3 * w]),
+                                (int64_t)T->radius[w]);
+      if (V > vter[i]) vter[i] = V;
+    }
+  }
+
+  /* Process negative intruder rewards (Alg 7): five wells per plan active at row K. */
+  for (int i = 0; i < AW; ++i) vint[i] = 0.0;
+  for (int32_t j = 0; j < orc_store_count(S); ++j) {
+    int32_t pos[3], vel[3], cen[3 * ORC_MAX_TAU];
+    int64_t rad[ORC_MAX_TAU];
+    if (!orc_store_sample(S, j, K, pos, vel)) continue;
+    orc_build_wells(p, pos, vel, cen, rad);  /* Alg 2 */
+    for (int tau = 0; tau < p->n_tau; ++tau) {
+      for (int i = 0; i < AW; ++i) {
+        double V = orc_well_value(p->intr_r, p->intr_gamma, p->u_m, d2_of(&proj[3 * i], &cen[3 * tau]), rad[tau]);
+        if (V > vint[i]) vint[i] = V;
+      }
+    }
+  }
+
+  /* Hard deck (Alg 1; Alg 8). */
+  for (int i = 0; i < AW; ++i) valt[i] = orc_deck_penalty(p, proj[3 * i + 2]);
+
+  /* Compute value (Alg 8): V = V+ - max(V-, V^T, V^I) - V_alt; V- is empty
+   * for a single requesting aircraft (Table DS P:397 with N = 1). */
+  for (int a = 0; a < A; ++a) {
+    double vmax = p->vmax_init_zero ? 0.0 : -INFINITY;  /* P:736 vs R2 */
+    double best_t = -INFINITY, best_sc = 0.0;
+    for (int t = 0; t < W; ++t) {
+      int i = a * W + t;
+      double neg = vter[i] > vint[i] ? vter[i] : vint[i];
+      v[i] = vpos[i] - neg - valt[i];
+      scale[i] = vpos[i] + neg + valt[i];
+      if (v[i] > vmax) vmax = v[i];
+      if (v[i] > best_t) { best_t = v[i]; best_sc = scale[i]; }
+    }
+    vstar[a] = vmax;
+    vsc[a] = best_sc;
+  }
+
+  /* Select best action (Alg 9), lowest index on ties (R13). */
+  int a1 = 0;
+  for (int a = 1; a < A; ++a)
+    if (vstar[a] > vstar[a1]) a1 = a;
+  int a2 = -1;
+  for (int a = 0; a < A; ++a) {
+    if (a == a1) continue;
+    if (a2 < 0 || vstar[a] > vstar[a2]) a2 = a;
+  }
+  out->a_star = a1;
+  out->a_second = a2;
+  out->gap = a2 >= 0 ? vstar[a1] - vstar[a2] : INFINITY;
+  out->near_tie = a2 >= 0 && out->gap < p->near_tie_rel * vsc[a1];
+
+  /* Conflict of every action's first substep (Delta_1, Alg 1) against row K+1 (R20). */
+  if (out->conf_d2) {
+    for (int a = 0; a < A; ++a)
+      out->conf_d2[a] = nearest_d2(S, &proj[3 * (a * W + 0)], K + 1, c.R_max * c.R_max);
+  }
+
+  if (out->v_pos) memcpy(out->v_pos, vpos, sizeof(double) * AW);
+  if (out->v_int) memcpy(out->v_int, vint, sizeof(double) * AW);
+  if (out->v_ter) memcpy(out->v_ter, vter, sizeof(double) * AW);
+  if (out->v_alt) memcpy(out->v_alt, valt, sizeof(double) * AW);
+  if (out->v) memcpy(out->v, v, sizeof(double) * AW);
+  if (out->scale) memcpy(out->scale, scale, sizeof(double) * AW);
+  if (out->vstar) memcpy(out->vstar, vstar, sizeof(double) * A);
+  if (out->vstar_scale) memcpy(out->vstar_scale, vsc, sizeof(double) * A);
+  if (out->proj) memcpy(out->proj, proj, sizeof(int32_t) * 3 * AW);
+  if (out->proj_psi) memcpy(out->proj_psi, ppsi, sizeof(int32_t) * AW);
+
+done:
+  free(proj); free(ppsi); free(vpos); free(vint); free(vter); free(valt);
+  free(v); free(scale); free(vstar); free(vsc);
+  return rc;
+}
+
+/* ------------------------------------------------------------------------- */
+/* One PDFP request (Fig 3a loop P:272-289; Sec. V).              */
+/* ------------------------------------------------------------------------- */
+int orc_schedule(const orc_params* p, const orc_terrain* T, const orc_store* S,
+                 const int32_t src[3], const int32_t dst[3], int64_t t0, int32_t cap,
+                 int32_t* traj, int32_t* heading, int32_t* astar, orc_result* res) {
+  conv c;
+  if (convert(p, &c) || !traj || !heading || !res || cap < 1 || t0 < 0) return ORC_E_ARG;
+  const int A = p->n_turn * p->n_climb, W = p->W;
+  const int64_t sat = c.R_max * c.R_max, sep2 = c.sep_u * c.sep_u, cap2 = c.cap_u * c.cap_u;
+  int32_t q[3] = {src[0], src[1], src[2]};
+  int32_t psi = orc_initial_heading(p, src, dst);
+  int64_t K = t0;
+  int32_t k = 0;
+  memset(res, 0, sizeof(*res));
+  res->fail_step = -1;
+  res->min_sep_d2 = sat;
+  memcpy(&traj[0], q, sizeof(q));
+  heading[0] = psi;
+
+  /* Initial terminal tests at the departure row. */
+  int64_t n0 = nearest_d2(S, q, K, sat);
+  if (n0 < res->min_sep_d2) res->min_sep_d2 = n0;
+  if (n0 < sep2) { res->status = ORC_REJ_CONFLICT; res->fail_step = 0; res->n_states = 1; return ORC_OK; }
+  if (terrain_collision(T, q)) { res->status = ORC_REJ_TERRAIN; res->fail_step = 0; res->n_states = 1; return ORC_OK; }
+  if (d2_of(q, dst) < cap2) { res->status = ORC_ACCEPTED; res->n_states = 1; return ORC_OK; }
+
+  int32_t* proj = (int32_t*)malloc(sizeof(int32_t) * 3 * A * W);
+  int32_t* ppsi = (int32_t*)malloc(sizeof(int32_t) * A * W);
+  if (!proj || !ppsi) { free(proj); free(ppsi); return ORC_E_NOMEM; }
+  int rc = ORC_OK;
+  for (;;) {
+    if (k + 1 >= cap) { rc = ORC_E_RANGE; break; }
+    orc_step_out o;
+    memset(&o, 0, sizeof(o));
+    o.proj = proj;
+    o.proj_psi = ppsi;
+    if ((rc = orc_eval_step(p, T, S, q, psi, dst, K, &o))) break;
+    if (o.near_tie) res->n_near_ties += 1;
+    if (astar) astar[k] = o.a_star;
+    /* s_{t+1} <- Delta_1[a*] (Alg 1; R5). */
+    int i1 = o.a_star * W + 0;
+    q[0] = proj[3 * i1 + 0]; q[1] = proj[3 * i1 + 1]; q[2] = proj[3 * i1 + 2];
+    psi = ppsi[i1];
+    k += 1;
+    K += 1;
+    memcpy(&traj[3 * k], q, sizeof(q));
+    heading[k] = psi;
+    /* Determine terminal state (Sec IV.I), priority order R15/R16/R20. */
+    int64_t nd = nearest_d2(S, q, K, sat);
+    if (nd < res->min_sep_d2) res->min_sep_d2 = nd;
+    if (nd < sep2) { res->status = ORC_REJ_CONFLICT; res->fail_step = k; break; }
+    if (terrain_collision(T, q)) { res->status = ORC_REJ_TERRAIN; res->fail_step = k; break; }
+    if (d2_of(q, dst) < cap2) { res->status = ORC_ACCEPTED; break; }
+    if (k >= p->max_steps) { res->status = ORC_REJ_TIMEOUT; res->fail_step = k; break; }
+  }
+  res->n_states = k + 1;
+  free(proj);
+  free(ppsi);
+  return rc;
+}
+
+/* Strict FCFS: requests in array order, each against the
+ * store including every plan accepted before it (R-a10). */
+int orc_schedule_batch(const orc_params* p, const orc_terrain* T, orc_store* S, int32_t n,
+                       const int32_t* src, const int32_t* dst, const int64_t* t0, int32_t cap,
+                       int32_t* traj, int32_t* heading, int32_t* astar, orc_result* res) {
+  for (int32_t i = 0; i < n; ++i) {
+    int32_t* tr = traj + (size_t)3 * cap * i;
+    int32_t* hd = heading + (size_t)cap * i;
+    int32_t* as = astar ? astar + (size_t)cap * i : NULL;
+    int rc = orc_schedule(p, T, S, &src[3 * i], &dst[3 * i], t0[i], cap, tr, hd, as, &res[i]);
+    if (rc) return rc;
+    if (res[i].status == ORC_ACCEPTED) {
+      rc = orc_store_add(S, t0[i], res[i].n_states, tr);
+      if (rc) return rc;
+    }
+  }
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Lockstep replay of an externally produced trajectory (parity protocol).     */
+/* At every step the oracle recomputes V*, a*; a different action is accepted  */
+/* only at a near-tie of the oracle's own values; the transition and every    */
+/* terminal verdict must be reproduced exactly.                               */
+/* ------------------------------------------------------------------------- */
+int orc_replay(const orc_params* p, const orc_terrain* T, const orc_store* S,
+               const int32_t src[3], const int32_t dst[3], int64_t t0,
+               int32_t n, const int32_t* traj, const int32_t* heading, const int32_t* astar,
+               int32_t status, orc_replay_stats* st) {
+  conv c;
+  if (convert(p, &c) || !st || n < 1) return ORC_E_ARG;
+  memset(st, 0, sizeof(*st));
+  st->first_fail_step = -1;
+  const int A = p->n_turn * p->n_climb, W = p->W;
+  const int64_t sat = c.R_max * c.R_max, sep2 = c.sep_u * c.sep_u, cap2 = c.cap_u * c.cap_u;
+#define FAIL(k_) do { st->n_fail++; if (st->first_fail_step < 0) st->first_fail_step = (k_); } while (0)
+  if (traj[0] != src[0] || traj[1] != src[1] || traj[2] != src[2]) FAIL(0);
+  if (heading[0] != orc_initial_heading(p, src, dst)) FAIL(0);
+  double* vstar = (double*)malloc(sizeof(double) * A);
+  double* vsc = (double*)malloc(sizeof(double) * A);
+  int32_t* proj = (int32_t*)malloc(sizeof(int32_t) * 3 * A * W);
+  int32_t* ppsi = (int32_t*)malloc(sizeof(int32_t) * A * W);
+  if (!vstar || !vsc || !proj || !ppsi) { free(vstar); free(vsc); free(proj); free(ppsi); return ORC_E_NOMEM; }
+  for (int32_t k = 0; k < n; ++k) {
+    const int32_t* q = &traj[3 * k];
+    int64_t K = t0 + k;
+    /* Terminal verdict at state k. */
+    int verdict = -1;
+    int64_t nd = nearest_d2(S, q, K, sat);
+    if (nd < sep2) verdict = ORC_REJ_CONFLICT;
+    else if (terrain_collision(T, q)) verdict = ORC_REJ_TERRAIN;
+    else if (d2_of(q, dst) < cap2) verdict = ORC_ACCEPTED;
+    else if (k >= p->max_steps) verdict = ORC_REJ_TIMEOUT;
+    if (k == n - 1) {
+      if (verdict != status) FAIL(k);
+      break;
+    }
+    if (verdict >= 0) { FAIL(k); break; }
+    orc_step_out o;
+    memset(&o, 0, sizeof(o));
+    o.vstar = vstar;
+    o.vstar_scale = vsc;
+    o.proj = proj;
+    o.proj_psi = ppsi;
+    if (orc_eval_step(p, T, S, q, heading[k], dst, K, &o)) { FAIL(k); break; }
+    st->n_steps_checked++;
+    if (o.near_tie) st->n_near_ties++;
+    int ag = astar ? astar[k] : o.a_star;
+    if (ag < 0 || ag >= A) { FAIL(k); break; }
+    if (ag != o.a_star) {
+      if (vstar[o.a_star] - vstar[ag] < p->near_tie_rel * vsc[o.a_star]) st->n_divergent++;
+      else FAIL(k);
+    }
+    int i1 = ag * W;
+    const int32_t* q1 = &traj[3 * (k + 1)];
+    if (q1[0] != proj[3 * i1] || q1[1] != proj[3 * i1 + 1] || q1[2] != proj[3 * i1 + 2] ||
+        heading[k + 1] != ppsi[i1])
+      FAIL(k);
+  }
+#undef FAIL
+  free(vstar); free(vsc); free(proj); free(ppsi);
+  return ORC_OK;
+}
