@@ -1,0 +1,234 @@
+/*
+ * fmdp.h -- C ABI of the B200-native FastMDP-GPU hot path (arXiv 2008.03518).
+ *
+ * Paper passages are cited as P:n = line n of the paper source; the readings
+ * of ambiguous passages (R1..R23) are listed in DESIGN.md "Readings".
+ *
+ * Model (one request = one aircraft, N = 1):
+ *   At every 0.1 s step k of the requesting aircraft's trajectory (Fig 3a loop P:272-289)
+ *   every action a = (turn, climb) is projected W substeps ahead (Alg 3) and
+ *   each projected state s_{a,t} is valued with Alg 8:
+ *       V(a,t) = V+(a,t) - max(V^T(a,t), V^I(a,t)) - V_alt(a,t)
+ *       V+  = 200 * .999^d(goal)                     (Alg 4, Table PK)
+ *       V^I = max over accepted plans j active at the step's time row and
+ *             tau in {-5,0,5,10,15} s of [d < 300+10 tau] 1000 * .97^d
+ *             around p_j + v_j tau                   (Alg 7, Table PK)
+ *       V^T = max over terrain wells of [d < R] 1000 * .99^d   (Alg 6, Table PK)
+ *       V_alt = 1000 - z if z < deck else 0          (Alg 1, R6/R7)
+ *   V*(a) = max_t V(a,t) (Alg 8), a* = argmax (Alg 9, lowest index on ties),
+ *   the aircraft advances one substep along a* (Alg 1), and the terminal state is
+ *   determined (Sec IV.I): separation conflict with any accepted plan (exact),
+ *   terrain, goal capture, timeout.  An accepted trajectory is appended to the plan store
+ *   (Sec V) and constrains every later request (first-come-first-served).
+ *
+ * Units: positions are integers in units of airspace.u_m metres (2^-6 m by default,
+ *   R23); fmdp_vec3 arguments are metres and are quantised with llrint(x / u_m)
+ *   (round half to even).  Time is an integer step index ("clock row") of dt seconds.
+ *
+ * Conventions (all functions):
+ *   - Every function returns fmdp_status (0 = OK, < 0 = error) and never throws.
+ *   - A REJECTION IS NOT AN ERROR: fmdp_schedule returns FMDP_OK with
+ *     res->status != FMDP_ACCEPTED ("otherwise an error is reported" is the
+ *     request-level status, not an API failure).
+ *   - The context owns all device memory; input arrays are copied before return and may
+ *     be freed by the caller; output buffers are caller-allocated with a capacity; a
+ *     too-small buffer yields FMDP_E_BUFFER and the required size in *n / n_states.
+ *   - One context = one FCFS sequence; calls on one context must be serialised by the
+ *     caller.  Different contexts are independent.
+ *   - Results are deterministic and bit-identical across runs, batch speculation and
+ *     launch configuration (every reduction on the path is an exact min/max).
+ *   - The library requires an sm_100a device; without one fmdp_create fails with
+ *     FMDP_E_NODEV.  There is no CPU fallback.
+ */
+#ifndef FMDP_H
+#define FMDP_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FMDP_ABI_VERSION 1
+
+typedef struct fmdp_ctx fmdp_ctx; /* opaque; owns device memory, plan store, scratch */
+typedef int32_t fmdp_status;
+
+enum {
+  FMDP_OK = 0,
+  FMDP_E_ARG = -1,       /* invalid argument / scenario                                 */
+  FMDP_E_NOMEM = -2,     /* host or device allocation failed                            */
+  FMDP_E_CUDA = -3,      /* CUDA runtime error (fmdp_last_error has the text)           */
+  FMDP_E_CAPACITY = -4,  /* a time row would exceed airspace.row_capacity               */
+  FMDP_E_DUPLICATE = -5, /* reserved (plan ids are assigned by the library)             */
+  FMDP_E_BUFFER = -6,    /* output buffer too small; required size returned             */
+  FMDP_E_RANGE = -7,     /* position outside the airspace / 2^24-unit span, or a plan   */
+                         /* running past horizon_steps, or |velocity| beyond packing    */
+  FMDP_E_NODEV = -8,     /* no sm_100 device                                            */
+  FMDP_E_INTERNAL = -99
+};
+
+/* Request status (fmdp_result.status). */
+enum { FMDP_ACCEPTED = 0, FMDP_REJ_CONFLICT = 1, FMDP_REJ_TERRAIN = 2, FMDP_REJ_TIMEOUT = 3 };
+
+typedef struct { double x, y, z; } fmdp_vec3;   /* metres, local ENU                      */
+typedef struct { int32_t x, y, z; } fmdp_qpos;  /* integer units of u_m                   */
+
+/* Scenario.  Defaults (DESIGN.md Appendix A) are filled by fmdp_airspace_default(). */
+typedef struct fmdp_airspace {
+  uint32_t abi_version;            /* = FMDP_ABI_VERSION                                */
+  fmdp_vec3 lo, hi;                /* airspace bounds, metres; span < 2^24 units         */
+  double u_m;                      /* metres per position unit (2^-6)                    */
+  double dt;                       /* substep, 0.1 s                             */
+  int32_t window;                  /* W = 10 look-ahead substeps                 */
+  double speed;                    /* constant ground speed v0, m/s; v0*dt/u integral    */
+  int32_t heading_lattice;         /* H_L headings, divisible by 8 (R14)                 */
+  int32_t n_turn;                  /* <= 32                                              */
+  const int32_t* turn_steps;       /* lattice steps per substep, ascending               */
+  int32_t n_climb;                 /* 1, 3 or 5                                          */
+  const int32_t* climb_units;      /* z units per substep, ascending                     */
+  double goal_r, goal_gamma;       /* 200, 0.999 (Table PK, R8)                    */
+  double intr_r, intr_gamma;       /* 1000, 0.97 (Table PK)                        */
+  int32_t n_tau;                   /* <= 5                                               */
+  const double* tau_s;             /* {-5,0,5,10,15} s; tau/dt integral (R9)             */
+  const double* tau_radius_m;      /* 300 + 10 tau m; multiples of u; max < 1024 m       */
+  double terr_r, terr_gamma;       /* 1000, 0.99 (Table PK)                        */
+  double deck_alt_m, deck_scale;   /* 30 m, 1000 (Alg 1, R7)                   */
+  double capture_radius_m;         /* goal capture, 100 m (R16)                          */
+  double sep_min_m;                /* separation minimum, 150 m (R15)                    */
+  int32_t max_steps;               /* timeout                                            */
+  int32_t vmax_init_zero;          /* 0: V_max <- -inf (R2, default); 1: literal P:736   */
+  double near_tie_rel;             /* 1e-4: near-tie threshold for logging               */
+  int64_t horizon_steps;           /* number of time rows in the plan store              */
+  int32_t row_capacity;            /* plan slots per time row (multiple of 4)            */
+} fmdp_airspace;
+
+/* Terrain: manually placed wells (Table PK) and a ground-height raster used only
+ * for the terrain-collision verdict (R16).  All integer units. */
+typedef struct fmdp_terrain {
+  int32_t n_wells;
+  const fmdp_qpos* center;         /* [n_wells]                                          */
+  const int32_t* radius_u;         /* [n_wells]                                          */
+  int32_t nx, ny;                  /* raster cells (0 = no raster)                       */
+  int32_t x0_u, y0_u, cell_u;      /* raster origin and cell size                        */
+  const int32_t* height_u;         /* [ny][nx] ground height                             */
+} fmdp_terrain;
+
+/* Device / launch configuration (NULL = current device, default stream, cudaMalloc). */
+typedef struct fmdp_devices {
+  int32_t device;                                   /* CUDA ordinal                      */
+  void* stream;                                     /* cudaStream_t or NULL              */
+  void* (*alloc)(size_t bytes, void* user);         /* optional device allocator         */
+  void (*release)(void* ptr, void* user);
+  void* user;
+} fmdp_devices;
+
+typedef struct fmdp_launch {
+  int32_t cluster_size;   /* CTAs cooperating on one trajectory (1..16), 0 = auto        */
+  int32_t max_walkers;    /* concurrent trajectories in a batch round, 0 = auto          */
+  int32_t threads;        /* threads per CTA, 0 = auto                                   */
+} fmdp_launch;
+
+typedef struct fmdp_request {
+  uint64_t aircraft_id;
+  fmdp_vec3 src, dst;      /* metres                                                     */
+  int64_t t0_step;         /* departure clock row                                        */
+} fmdp_request;
+
+typedef struct fmdp_result {
+  int32_t status;          /* FMDP_ACCEPTED / FMDP_REJ_*                                 */
+  uint32_t plan_id;        /* valid if ACCEPTED                                          */
+  int32_t n_states;        /* trajectory length (states 0..n-1 at rows t0..t0+n-1)       */
+  int32_t fail_step;       /* step of the rejecting verdict, -1 if accepted              */
+  double min_sep_m;        /* min distance to any accepted plan along the trajectory,    */
+                           /* saturated at the largest well radius (450 m)               */
+  int32_t n_near_ties;     /* steps whose top-2 V* gap < near_tie_rel * term scale       */
+  int32_t n_exact;         /* (state,tau) minima resolved by the exact fallback          */
+} fmdp_result;
+
+/* Per-call counters of the last schedule / schedule_batch call. */
+typedef struct fmdp_stats {
+  int64_t steps;           /* decision steps executed on the device (incl. re-runs)      */
+  int64_t pair_evals;      /* (projected state, well) pairs evaluated in the hot loop    */
+  int32_t rounds;          /* speculative FCFS rounds                                     */
+  int32_t reruns;          /* trajectories re-run after influence by an earlier commit   */
+  int32_t cluster_size;
+  int32_t walkers;
+  int32_t kernels;         /* kernel launches                                             */
+  double device_ms;        /* sum of walk-kernel device time (CUDA events)                */
+} fmdp_stats;
+
+/* Fill *a with the defaults of DESIGN.md Appendix A (the arrays point to static storage). */
+void fmdp_airspace_default(fmdp_airspace* a);
+
+/* Create a context on one device.  Copies airspace and terrain (wells to device,
+ * raster to device).  Errors: E_ARG (invalid scenario), E_NODEV, E_NOMEM, E_CUDA. */
+fmdp_status fmdp_create(const fmdp_airspace* airspace, const fmdp_terrain* terrain,
+                        const fmdp_devices* devs, fmdp_ctx** out);
+void fmdp_destroy(fmdp_ctx* ctx);
+
+/* Launch tuning (NULL resets to auto). */
+fmdp_status fmdp_set_launch(fmdp_ctx* ctx, const fmdp_launch* launch);
+
+/* Import an externally produced plan: n >= 1 states at rows t0..t0+n-1.
+ * Velocities are the forward differences (R11) and must fit the packed store record
+ * (|vx|,|vy| <= 1023, |vz| <= 511 units/step) else E_RANGE.  Rows past horizon ->
+ * E_RANGE; full rows -> E_CAPACITY (nothing is stored).  *plan_id receives the id. */
+fmdp_status fmdp_add_plan(fmdp_ctx* ctx, uint64_t aircraft_id, int64_t t0_step, int32_t n,
+                          const fmdp_qpos* states, int32_t flags, uint32_t* plan_id);
+
+/* Bulk import of n_plans plans in order (ids first_id..first_id+n_plans-1); states are
+ * concatenated.  aircraft_ids may be NULL.  All-or-nothing. */
+fmdp_status fmdp_add_plans(fmdp_ctx* ctx, int32_t n_plans, const uint64_t* aircraft_ids,
+                           const int64_t* t0_steps, const int32_t* n_states,
+                           const fmdp_qpos* states, uint32_t* first_id);
+
+/* Schedule one request against every accepted plan (Sec V) and append it on
+ * acceptance.  traj receives n_states states (cap traj_cap; E_BUFFER if smaller than
+ * max_steps + 1).  Request errors: src == dst, outside the airspace -> E_ARG / E_RANGE;
+ * t0 + max_steps + 1 >= horizon -> E_RANGE. */
+fmdp_status fmdp_schedule(fmdp_ctx* ctx, uint64_t aircraft_id, fmdp_vec3 src, fmdp_vec3 dst,
+                          int64_t t0_step, fmdp_result* res, fmdp_qpos* traj, int32_t traj_cap);
+
+/* First-come-first-served batch: results identical to calling fmdp_schedule on each
+ * request in array order.  Default implementation: speculative rounds against a store
+ * snapshot + exact influence test + in-order commit.
+ * flags: FMDP_BATCH_SEQUENTIAL forces the plain loop.
+ * traj: n * traj_cap_each states (may be NULL to skip trajectory output). */
+#define FMDP_BATCH_SEQUENTIAL 1
+fmdp_status fmdp_schedule_batch(fmdp_ctx* ctx, const fmdp_request* reqs, int32_t n,
+                                fmdp_result* res, fmdp_qpos* traj, int32_t traj_cap_each,
+                                int32_t flags);
+
+/* Per-step log of the last trajectory of request `index` of the last schedule /
+ * schedule_batch call: action a*_k, heading psi_k, and near-tie flag per step (k < n).
+ * Any pointer may be NULL. */
+fmdp_status fmdp_get_steplog(fmdp_ctx* ctx, int32_t index, int32_t* astar, int32_t* heading,
+                             int32_t* near_tie, int32_t cap, int32_t* n);
+
+fmdp_status fmdp_get_plan(fmdp_ctx* ctx, uint32_t plan_id, int64_t* t0_step, fmdp_qpos* buf,
+                          int32_t cap, int32_t* n);
+fmdp_status fmdp_num_plans(const fmdp_ctx* ctx, uint32_t* n);
+
+/* Remove every plan with id >= n_plans (restores the store of an earlier moment). */
+fmdp_status fmdp_truncate(fmdp_ctx* ctx, uint32_t n_plans);
+
+/* One decision step at (pos, heading) for goal `goal` at clock row `clock_step`, run by
+ * the same device code as fmdp_schedule (parity / debug hook; V mirrors Table DS "V",
+ * P:405).  Outputs (host pointers, any may be NULL except vstar):
+ *   vstar[A], v_at[A*W], scale_at[A*W] (V+ + max(V^T,V^I) + V_alt), conflict[A] (1 if
+ *   Delta_1(a) is within sep of a plan at row clock+1), min_d2[A+1] (saturated min d^2 of
+ *   Delta_1(a) to row clock+1; entry A: pos to row clock), *a_star. */
+fmdp_status fmdp_eval_step(fmdp_ctx* ctx, fmdp_qpos pos, int32_t heading, fmdp_qpos goal,
+                           int64_t clock_step, double* vstar, double* v_at, double* scale_at,
+                           int32_t* conflict, int64_t* min_d2, int32_t* a_star);
+
+fmdp_status fmdp_get_stats(const fmdp_ctx* ctx, fmdp_stats* out);
+int32_t fmdp_num_actions(const fmdp_ctx* ctx);
+const char* fmdp_strerror(fmdp_status s);
+const char* fmdp_last_error(const fmdp_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FMDP_H */

@@ -1,0 +1,143 @@
+// fmdp_dev.h -- device data layout shared by the host library (fmdp_host.cu) and the
+// kernels (fmdp_walk.cu).  Product code; independent of oracle/.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fmdp {
+
+constexpr int NTAU = 5;         // intruder wells per plan (Table PK: "5 rewards")
+constexpr int MAX_TURN = 32;
+constexpr int MAX_CLIMB = 5;
+constexpr int MAX_W = 16;
+constexpr int MAX_AW = 1024;    // projected states per step (A*W)
+constexpr int AMB_MAX = 64;     // ambiguous (state, tau) minima handled per step
+constexpr int TC_MAX = 128;     // terrain-well candidates per step
+
+// Scenario + store in integer units, passed by value to the kernels.
+struct World {
+  int32_t A, W, n_turn, n_climb, HL;
+  int32_t turn[MAX_TURN];
+  int32_t climb[MAX_CLIMB];
+  int32_t k_tau[NTAU];          // tau / dt substeps (padding taus: k = 0, R2 = 0)
+  int64_t R2_tau[NTAU];         // exact R_tau^2, units^2
+  float R2lo[NTAU], R2hi[NTAU]; // FP32 filter band R^2 (1 -/+ 2^-20)
+  int32_t R_max;                // max tau radius, units (< 2^15)
+  uint32_t sat_d2;              // R_max^2: saturation of separation minima
+  uint32_t sep2;                // separation minimum^2
+  int64_t cap2;                 // goal capture radius^2
+  int32_t reach_u;              // bound on |s_{a,t} - q| over all projected states
+  double goal_r, goal_l2g;      // goal peak: |r|, log2(gamma) * u  (fp64)
+  float intr_r, intr_l2g;       // intruder wells: |r|, log2(gamma) * u (FP32 ex2)
+  float terr_r, terr_l2g;       // terrain wells
+  int32_t zdeck_u;
+  double deck_scale, u_m;
+  int32_t max_steps, vmax_init_zero;
+  double near_tie_rel;
+  // accepted-plan store: rows[K] = { x[cap], y[cap], z[cap], vpack[cap] } (int32 SoA)
+  int64_t horizon;
+  int32_t row_cap;
+  const int32_t* rows;
+  const int32_t* counts;        // active slots per row
+  // terrain
+  int32_t n_tw;
+  const int4* tw;               // x, y, z, R (units)
+  int32_t nx, ny, x0, y0, cell;
+  const int32_t* height;        // [ny][nx] units
+  const int2* dxy;              // heading lattice table [HL]
+};
+
+struct Req {
+  int32_t src[3];
+  int32_t dst[3];
+  int32_t psi0;
+  int32_t start_k;              // resume step (0 = fresh request)
+  int64_t t0;
+  int32_t slot;                 // output slot
+  int32_t pad;
+};
+
+struct Out {
+  int32_t status, n_states, fail_step, n_near_ties;
+  int32_t n_exact, steps_run;
+  uint32_t min_sep_d2;
+  int32_t pad;
+};
+
+struct WalkArgs {
+  const Req* reqs;
+  int32_t n_reqs;
+  int32_t* queue;               // dynamic request counter (zeroed before launch)
+  Out* out;                     // [slot]
+  int32_t* traj;                // [slot][cap][3]
+  int32_t* heading;             // [slot][cap]
+  int32_t* astar;               // [slot][cap]
+  uint32_t* stepd2;             // [slot][cap] saturated nearest-plan d^2 of state k
+  int8_t* ntie;                 // [slot][cap]
+  int32_t cap;
+  int32_t eval;                 // 1: evaluate one step (debug outputs), no advance
+  double* dbg_vstar;            // [A]
+  double* dbg_v;                // [A*W]
+  double* dbg_s;                // [A*W]
+  uint32_t* dbg_conf;           // [A+1]
+  int32_t* dbg_astar;           // [1]
+  unsigned long long* pairs;    // hot-loop pair counter (stats)
+};
+
+// Shared-memory carve-up, identical on host (size) and device (offsets).
+struct Layout {
+  int HL, CH, NT, C, NCOL, A, AW, RED, RAWW;
+  size_t o_dxy, o_raw, o_cen, o_red, o_pos, o_fix, o_sfix, o_vT, o_mI, o_vstar, o_vsc, o_conf, o_confg,
+      o_amb, o_tc, o_bar, o_ctl, total;
+  __host__ __device__ static size_t al(size_t x) { return (x + 15) & ~size_t(15); }
+  __host__ __device__ void build(int hl, int ch, int nt, int c, int ncol, int a, int aw) {
+    HL = hl; CH = ch; NT = nt; C = c; NCOL = ncol; A = a; AW = aw;
+    RED = NCOL * C * NTAU + A + 1;
+    RAWW = CH + 8;                      // words per SoA array in one raw row buffer
+    size_t o = 0;
+    o_dxy = o;  o = al(o + sizeof(int2) * HL);
+    o_raw = o;  o = al(o + sizeof(int32_t) * 4 * RAWW * 3);
+    size_t cen = sizeof(float) * 16 * CH;
+    size_t part = sizeof(float) * (size_t)NT * C * NTAU;
+    o_cen = o;  o = al(o + (cen > part ? cen : part));
+    o_red = o;  o = al(o + sizeof(uint32_t) * 3 * RED);
+    o_pos = o;  o = al(o + sizeof(int4) * AW);
+    o_fix = o;  o = al(o + sizeof(double) * AW);
+    o_sfix = o; o = al(o + sizeof(double) * AW);
+    o_vT = o;   o = al(o + sizeof(float) * AW);
+    o_mI = o;   o = al(o + sizeof(float) * AW);
+    o_vstar = o; o = al(o + sizeof(double) * A);
+    o_vsc = o;  o = al(o + sizeof(double) * A);
+    o_conf = o; o = al(o + sizeof(uint32_t) * (A + 1));
+    o_confg = o; o = al(o + sizeof(uint32_t) * (A + 1));
+    o_amb = o;  o = al(o + sizeof(int32_t) * AMB_MAX);
+    o_tc = o;   o = al(o + sizeof(int32_t) * TC_MAX);
+    o_bar = o;  o = al(o + sizeof(uint64_t) * 4);
+    o_ctl = o;  o = al(o + 256);
+    total = o;
+  }
+};
+
+struct AppendPlan {
+  int64_t t0;
+  int32_t n;
+  int32_t pad;
+  const int32_t* states;        // device [n][3]
+  const int32_t* slots;         // device [n] row slot of state i
+};
+
+struct InflPair {
+  int32_t i, j;                 // request slot i, plan from slot j
+};
+
+// Kernel launchers (fmdp_walk.cu).
+cudaError_t launch_walk(const World& w, const WalkArgs& a, int n_climb, int cluster, int n_clusters,
+                        int threads, int chunk, cudaStream_t s);
+cudaError_t walk_max_clusters(const World& w, int n_climb, int cluster, int threads, int chunk, int* out);
+size_t walk_smem_bytes(const World& w, int n_climb, int threads, int chunk);
+cudaError_t launch_append(int32_t* rows, int32_t row_cap, int64_t horizon, const AppendPlan* plans, int n_plans,
+                          int max_n, cudaStream_t s);
+cudaError_t launch_influence(const int32_t* traj, int32_t cap, const int32_t* n_states, const int64_t* t0,
+                             const InflPair* pairs, int n_pairs, int64_t bound2, int32_t* kfirst, cudaStream_t s);
+
+}  // namespace fmdp

@@ -1,0 +1,1039 @@
+// fmdp_host.cu -- C ABI (include/fmdp.h) of the B200 FastMDP-GPU hot path: context,
+// scenario validation and quantisation, the device plan store ([time row][slot] SoA),
+// and the first-come-first-served driver (sequential and speculative rounds).
+// Every step of the path runs in the kernels of fmdp_walk.cu; this file only validates,
+// allocates, launches and copies.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/fmdp.h"
+#include "fmdp_dev.h"
+
+using fmdp::AppendPlan;
+using fmdp::InflPair;
+using fmdp::Out;
+using fmdp::Req;
+using fmdp::World;
+
+namespace {
+struct PlanRec {
+  uint64_t aircraft;
+  int64_t t0;
+  std::vector<int32_t> states;  // n*3
+};
+}  // namespace
+
+struct fmdp_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  void* (*alloc)(size_t, void*) = nullptr;
+  void (*release)(void*, void*) = nullptr;
+  void* user = nullptr;
+  std::vector<void*> allocs;
+
+  fmdp_airspace air{};
+  std::vector<int32_t> turn, climb;
+  std::vector<double> tau_s, tau_r;
+  World w{};
+  int A = 0, W = 0, C = 0;
+  int64_t lo_u[3]{}, hi_u[3]{};
+  int64_t bound2 = 0;
+
+  std::vector<int32_t> counts;  // host mirror of the per-row slot counts (authoritative)
+  std::vector<PlanRec> plans;
+  int32_t* d_rows = nullptr;
+  int32_t* d_counts = nullptr;
+  int4* d_tw = nullptr;
+  int32_t* d_height = nullptr;
+  int2* d_dxy = nullptr;
+
+  // per-request scratch (grown on demand)
+  int slots_cap = 0;
+  int32_t cap_states = 0;
+  Req* d_reqs = nullptr;
+  Out* d_out = nullptr;
+  int32_t *d_traj = nullptr, *d_heading = nullptr, *d_astar = nullptr;
+  uint32_t* d_stepd2 = nullptr;
+  int8_t* d_ntie = nullptr;
+  int32_t* d_queue = nullptr;
+  int32_t* d_nstates = nullptr;
+  int64_t* d_t0s = nullptr;
+  unsigned long long* d_pairctr = nullptr;
+  InflPair* d_pairs = nullptr;
+  int32_t* d_kfirst = nullptr;
+  int pairs_cap = 0;
+  AppendPlan* d_app = nullptr;
+  int app_cap = 0;
+  int32_t* d_up = nullptr;  // upload scratch (states / slots)
+  size_t up_cap = 0;
+  double *d_dbg_vstar = nullptr, *d_dbg_v = nullptr, *d_dbg_s = nullptr;
+  uint32_t* d_dbg_conf = nullptr;
+  int32_t* d_dbg_astar = nullptr;
+
+  std::vector<Out> h_out;
+  int last_n = 0;
+  fmdp_launch launch{};
+  fmdp_stats stats{};
+  std::string err;
+  int num_sms = 0;
+  int mc_cache[17] = {0};
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace {
+
+const char* kStatusText[] = {"ok", "invalid argument", "out of memory", "CUDA error", "row capacity exceeded",
+                             "duplicate", "buffer too small", "out of range", "no sm_100 device"};
+
+fmdp_status fail(fmdp_ctx* c, fmdp_status s, const std::string& msg) {
+  if (c) c->err = msg;
+  return s;
+}
+
+#define CK(call)                                                                                   \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess) return fail(ctx, FMDP_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+void* dalloc(fmdp_ctx* ctx, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  void* p = nullptr;
+  if (ctx->alloc) {
+    p = ctx->alloc(bytes, ctx->user);
+  } else if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    p = nullptr;
+  }
+  if (p) ctx->allocs.push_back(p);
+  return p;
+}
+
+void dfree(fmdp_ctx* ctx, void* p) {
+  if (!p) return;
+  auto it = std::find(ctx->allocs.begin(), ctx->allocs.end(), p);
+  if (it != ctx->allocs.end()) ctx->allocs.erase(it);
+  if (ctx->release) ctx->release(p, ctx->user);
+  else cudaFree(p);
+}
+
+template <class T>
+fmdp_status grow(fmdp_ctx* ctx, T*& p, size_t n) {
+  dfree(ctx, p);
+  p = static_cast<T*>(dalloc(ctx, sizeof(T) * n));
+  return p ? FMDP_OK : fail(ctx, FMDP_E_NOMEM, "device allocation failed");
+}
+
+bool integral(double r, int64_t* out) {
+  double n = std::rint(r);
+  if (!(std::fabs(r - n) <= 1e-9 * (1.0 + std::fabs(r)))) return false;
+  *out = (int64_t)n;
+  return true;
+}
+
+// Heading lattice (R14): first-octant rounding of L*(cos, sin), reflected and rotated so the
+// table is exactly symmetric.  Independent implementation of the DESIGN.md definition.
+void build_lattice(int HL, int64_t L, std::vector<int2>& t) {
+  t.resize(HL);
+  const int Q = HL / 4, O = HL / 8;
+  for (int psi = 0; psi < HL; ++psi) {
+    const int quad = psi / Q, r = psi % Q;
+    double cx, sy;
+    if (r <= O) {
+      cx = std::rint((double)L * std::cos(2.0 * M_PI * r / HL));
+      sy = std::rint((double)L * std::sin(2.0 * M_PI * r / HL));
+    } else {
+      const int m = Q - r;
+      cx = std::rint((double)L * std::sin(2.0 * M_PI * m / HL));
+      sy = std::rint((double)L * std::cos(2.0 * M_PI * m / HL));
+    }
+    const int a = (int)cx, b = (int)sy;
+    switch (quad) {
+      case 0: t[psi] = make_int2(a, b); break;
+      case 1: t[psi] = make_int2(-b, a); break;
+      case 2: t[psi] = make_int2(-a, -b); break;
+      default: t[psi] = make_int2(b, -a); break;
+    }
+  }
+}
+
+fmdp_status quantize(fmdp_ctx* ctx, const fmdp_vec3& v, int32_t q[3]) {
+  const double m[3] = {v.x, v.y, v.z};
+  for (int d = 0; d < 3; ++d) {
+    const double x = m[d] / ctx->air.u_m;
+    if (!std::isfinite(x)) return fail(ctx, FMDP_E_ARG, "non-finite coordinate");
+    const long long r = std::llrint(x);
+    if (r < ctx->lo_u[d] || r > ctx->hi_u[d]) return fail(ctx, FMDP_E_RANGE, "position outside the airspace");
+    q[d] = (int32_t)r;
+  }
+  return FMDP_OK;
+}
+
+int32_t initial_heading(const fmdp_ctx* ctx, const int32_t s[3], const int32_t g[3]) {
+  const double a = std::atan2((double)g[1] - (double)s[1], (double)g[0] - (double)s[0]) * ctx->w.HL / (2.0 * M_PI);
+  long long h = std::llrint(a) % ctx->w.HL;
+  if (h < 0) h += ctx->w.HL;
+  return (int32_t)h;
+}
+
+fmdp_status ensure_slots(fmdp_ctx* ctx, int n) {
+  if (n <= ctx->slots_cap) return FMDP_OK;
+  const int m = std::max(n, 2 * ctx->slots_cap);
+  const size_t cap = (size_t)ctx->cap_states;
+  fmdp_status s;
+  if ((s = grow(ctx, ctx->d_reqs, m)) || (s = grow(ctx, ctx->d_out, m)) || (s = grow(ctx, ctx->d_traj, 3 * cap * m)) ||
+      (s = grow(ctx, ctx->d_heading, cap * m)) || (s = grow(ctx, ctx->d_astar, cap * m)) ||
+      (s = grow(ctx, ctx->d_stepd2, cap * m)) || (s = grow(ctx, ctx->d_ntie, cap * m)) ||
+      (s = grow(ctx, ctx->d_nstates, m)) || (s = grow(ctx, ctx->d_t0s, m)))
+    return s;
+  ctx->slots_cap = m;
+  ctx->h_out.resize(m);
+  return FMDP_OK;
+}
+
+fmdp_status ensure_up(fmdp_ctx* ctx, size_t words) {
+  if (words <= ctx->up_cap) return FMDP_OK;
+  const size_t m = std::max(words, 2 * ctx->up_cap);
+  fmdp_status s = grow(ctx, ctx->d_up, m);
+  if (s) return s;
+  ctx->up_cap = m;
+  return FMDP_OK;
+}
+
+int threads_for(const fmdp_ctx* ctx) {
+  if (ctx->launch.threads > 0) return ctx->launch.threads;
+  const int ncol = ctx->w.n_turn * ctx->w.W;
+  const int group = (ncol + 31) & ~31;
+  int ng = std::max(1, 512 / group);
+  int nt = ng * group;
+  while (nt < ctx->A) nt += group;  // one conflict thread per action at least
+  return nt;
+}
+
+constexpr int kChunk = 512;
+
+int max_clusters(fmdp_ctx* ctx, int G) {
+  if (ctx->mc_cache[G]) return ctx->mc_cache[G];
+  int n = 0;
+  if (fmdp::walk_max_clusters(ctx->w, ctx->C, G, threads_for(ctx), kChunk, &n) != cudaSuccess || n < 0) n = 0;
+  cudaGetLastError();
+  ctx->mc_cache[G] = n;
+  return n;
+}
+
+// Cluster size for a round of n_run trajectories: the G minimising
+// waves(G) * (per-step work / G + per-step sync overhead), among sizes that can run.
+void choose_launch(fmdp_ctx* ctx, int n_run, int* G_out, int* nc_out) {
+  int best_G = 1;
+  double best = 1e300;
+  double plans = 0;
+  {
+    int64_t tot = 0, nz = 0;
+    for (int32_t c : ctx->counts)
+      if (c) { tot += c; ++nz; }
+    plans = nz ? (double)tot / nz : 0.0;
+  }
+  const double work = plans * fmdp::NTAU * ctx->A * ctx->W / 24.0 + 4000.0;  // cycles on one SM
+  const int sizes[] = {16, 8, 4, 2, 1};
+  for (int G : sizes) {
+    if (ctx->launch.cluster_size && G != ctx->launch.cluster_size) continue;
+    const int mc = max_clusters(ctx, G);
+    if (mc <= 0) continue;
+    int conc = std::min(mc, n_run);
+    if (ctx->launch.max_walkers > 0) conc = std::min(conc, ctx->launch.max_walkers);
+    const double waves = std::ceil((double)n_run / conc);
+    const double t = waves * (work / G + 2500.0 + 300.0 * G);
+    if (t < best) {
+      best = t;
+      best_G = G;
+    }
+  }
+  int mc = std::max(1, max_clusters(ctx, best_G));
+  int conc = std::min(mc, n_run);
+  if (ctx->launch.max_walkers > 0) conc = std::min(conc, ctx->launch.max_walkers);
+  *G_out = best_G;
+  *nc_out = std::max(1, conc);
+}
+
+fmdp_status run_walk(fmdp_ctx* ctx, const std::vector<Req>& run, bool eval) {
+  if (run.empty()) return FMDP_OK;
+  CK(cudaMemcpyAsync(ctx->d_reqs, run.data(), sizeof(Req) * run.size(), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemsetAsync(ctx->d_queue, 0, sizeof(int32_t), ctx->stream));
+  fmdp::WalkArgs a{};
+  a.reqs = ctx->d_reqs;
+  a.n_reqs = (int32_t)run.size();
+  a.queue = ctx->d_queue;
+  a.out = ctx->d_out;
+  a.traj = ctx->d_traj;
+  a.heading = ctx->d_heading;
+  a.astar = ctx->d_astar;
+  a.stepd2 = ctx->d_stepd2;
+  a.ntie = ctx->d_ntie;
+  a.cap = ctx->cap_states;
+  a.eval = eval ? 1 : 0;
+  a.dbg_vstar = ctx->d_dbg_vstar;
+  a.dbg_v = ctx->d_dbg_v;
+  a.dbg_s = ctx->d_dbg_s;
+  a.dbg_conf = ctx->d_dbg_conf;
+  a.dbg_astar = ctx->d_dbg_astar;
+  a.pairs = ctx->d_pairctr;
+  int G = 1, nc = 1;
+  choose_launch(ctx, (int)run.size(), &G, &nc);
+  ctx->stats.cluster_size = G;
+  ctx->stats.walkers = std::max(ctx->stats.walkers, nc);
+  CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  CK(fmdp::launch_walk(ctx->w, a, ctx->C, G, nc, threads_for(ctx), kChunk, ctx->stream));
+  CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  CK(cudaEventSynchronize(ctx->ev1));
+  CK(cudaGetLastError());
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  ctx->stats.device_ms += ms;
+  ctx->stats.kernels += 1;
+  return FMDP_OK;
+}
+
+fmdp_status fetch_out(fmdp_ctx* ctx, int n) {
+  CK(cudaMemcpyAsync(ctx->h_out.data(), ctx->d_out, sizeof(Out) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return FMDP_OK;
+}
+
+// Append plans (already validated: rows in horizon, capacity checked by the caller) whose
+// states are on the device.  Slots come from the host mirror, in plan order.
+fmdp_status append_device(fmdp_ctx* ctx, const std::vector<int64_t>& t0, const std::vector<int32_t>& n,
+                          const std::vector<const int32_t*>& d_states) {
+  const int np = (int)t0.size();
+  if (np == 0) return FMDP_OK;
+  size_t tot = 0;
+  int maxn = 0;
+  for (int i = 0; i < np; ++i) {
+    tot += n[i];
+    maxn = std::max(maxn, n[i]);
+  }
+  std::vector<int32_t> slots(tot);
+  size_t o = 0;
+  for (int i = 0; i < np; ++i)
+    for (int s = 0; s < n[i]; ++s) slots[o++] = ctx->counts[t0[i] + s]++;
+  fmdp_status st = ensure_up(ctx, tot);
+  if (st) return st;
+  if (np > ctx->app_cap) {
+    if ((st = grow(ctx, ctx->d_app, np))) return st;
+    ctx->app_cap = np;
+  }
+  std::vector<AppendPlan> ap(np);
+  o = 0;
+  for (int i = 0; i < np; ++i) {
+    ap[i].t0 = t0[i];
+    ap[i].n = n[i];
+    ap[i].pad = 0;
+    ap[i].states = d_states[i];
+    ap[i].slots = ctx->d_up + o;
+    o += n[i];
+  }
+  CK(cudaMemcpyAsync(ctx->d_up, slots.data(), sizeof(int32_t) * tot, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->d_app, ap.data(), sizeof(AppendPlan) * np, cudaMemcpyHostToDevice, ctx->stream));
+  CK(fmdp::launch_append(ctx->d_rows, ctx->w.row_cap, ctx->w.horizon, ctx->d_app, np, maxn, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->d_counts, ctx->counts.data(), sizeof(int32_t) * ctx->counts.size(), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->stats.kernels += 1;
+  return FMDP_OK;
+}
+
+bool rows_fit(const fmdp_ctx* ctx, const std::vector<int64_t>& t0, const std::vector<int32_t>& n) {
+  std::vector<int32_t> extra;
+  int64_t lo = INT64_MAX, hi = -1;
+  for (size_t i = 0; i < t0.size(); ++i) {
+    lo = std::min(lo, t0[i]);
+    hi = std::max(hi, t0[i] + n[i]);
+  }
+  if (hi < 0) return true;
+  extra.assign((size_t)(hi - lo), 0);
+  for (size_t i = 0; i < t0.size(); ++i)
+    for (int s = 0; s < n[i]; ++s)
+      if (ctx->counts[t0[i] + s] + ++extra[t0[i] + s - lo] > ctx->w.row_cap) return false;
+  return true;
+}
+
+// Commit accepted slots (in order): host plan records + device append.
+fmdp_status commit_slots(fmdp_ctx* ctx, const std::vector<int>& slots, const std::vector<Req>& base,
+                         const std::vector<uint64_t>& aircraft, std::vector<uint32_t>& plan_id) {
+  if (slots.empty()) return FMDP_OK;
+  std::vector<int64_t> t0;
+  std::vector<int32_t> n;
+  std::vector<const int32_t*> ds;
+  for (int s : slots) {
+    t0.push_back(base[s].t0);
+    n.push_back(ctx->h_out[s].n_states);
+    ds.push_back(ctx->d_traj + (size_t)s * ctx->cap_states * 3);
+  }
+  if (!rows_fit(ctx, t0, n)) return fail(ctx, FMDP_E_CAPACITY, "time row capacity exceeded on commit");
+  for (size_t i = 0; i < slots.size(); ++i) {
+    PlanRec p;
+    p.aircraft = aircraft[slots[i]];
+    p.t0 = t0[i];
+    p.states.resize((size_t)3 * n[i]);
+    CK(cudaMemcpyAsync(p.states.data(), ds[i], sizeof(int32_t) * 3 * n[i], cudaMemcpyDeviceToHost, ctx->stream));
+    plan_id[slots[i]] = (uint32_t)ctx->plans.size();
+    ctx->plans.push_back(std::move(p));
+  }
+  return append_device(ctx, t0, n, ds);
+}
+
+fmdp_status influence(fmdp_ctx* ctx, const std::vector<InflPair>& pairs, std::vector<int32_t>& kf) {
+  kf.assign(pairs.size(), INT_MAX);
+  if (pairs.empty()) return FMDP_OK;
+  if ((int)pairs.size() > ctx->pairs_cap) {
+    fmdp_status s;
+    if ((s = grow(ctx, ctx->d_pairs, pairs.size())) || (s = grow(ctx, ctx->d_kfirst, pairs.size()))) return s;
+    ctx->pairs_cap = (int)pairs.size();
+  }
+  CK(cudaMemcpyAsync(ctx->d_pairs, pairs.data(), sizeof(InflPair) * pairs.size(), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(fmdp::launch_influence(ctx->d_traj, ctx->cap_states, ctx->d_nstates, ctx->d_t0s, ctx->d_pairs, (int)pairs.size(),
+                            ctx->bound2, ctx->d_kfirst, ctx->stream));
+  CK(cudaMemcpyAsync(kf.data(), ctx->d_kfirst, sizeof(int32_t) * pairs.size(), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->stats.kernels += 1;
+  return FMDP_OK;
+}
+
+fmdp_status prepare_requests(fmdp_ctx* ctx, const fmdp_request* reqs, int n, std::vector<Req>& base) {
+  base.resize(n);
+  for (int i = 0; i < n; ++i) {
+    Req& r = base[i];
+    std::memset(&r, 0, sizeof(r));
+    fmdp_status s;
+    if ((s = quantize(ctx, reqs[i].src, r.src)) || (s = quantize(ctx, reqs[i].dst, r.dst))) return s;
+    if (r.src[0] == r.dst[0] && r.src[1] == r.dst[1] && r.src[2] == r.dst[2])
+      return fail(ctx, FMDP_E_ARG, "source equals destination");
+    if (reqs[i].t0_step < 0 || reqs[i].t0_step + ctx->w.max_steps + 2 > ctx->w.horizon)
+      return fail(ctx, FMDP_E_RANGE, "t0 + max_steps + 1 must lie inside the store horizon");
+    r.t0 = reqs[i].t0_step;
+    r.psi0 = initial_heading(ctx, r.src, r.dst);
+    r.start_k = 0;
+    r.slot = i;
+  }
+  return FMDP_OK;
+}
+
+fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_result* res, fmdp_qpos* traj,
+                          int32_t traj_cap_each, int32_t flags) {
+  if (!ctx || (n > 0 && (!reqs || !res)) || n < 0) return fail(ctx, FMDP_E_ARG, "null argument");
+  if (traj && traj_cap_each < ctx->w.max_steps + 1)
+    return fail(ctx, FMDP_E_BUFFER, "traj_cap must be >= max_steps + 1");
+  std::memset(&ctx->stats, 0, sizeof(ctx->stats));
+  if (n == 0) return FMDP_OK;
+  std::vector<Req> base;
+  fmdp_status st = prepare_requests(ctx, reqs, n, base);
+  if (st) return st;
+  if ((st = ensure_slots(ctx, n))) return st;
+  std::vector<uint64_t> aircraft(n);
+  for (int i = 0; i < n; ++i) aircraft[i] = reqs[i].aircraft_id;
+  std::vector<uint32_t> plan_id(n, 0xffffffffu);
+  CK(cudaMemsetAsync(ctx->d_pairctr, 0, sizeof(unsigned long long), ctx->stream));
+  std::vector<int64_t> t0s(n);
+  for (int i = 0; i < n; ++i) t0s[i] = base[i].t0;
+  CK(cudaMemcpyAsync(ctx->d_t0s, t0s.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+
+  int runs = 0;
+  if (flags & FMDP_BATCH_SEQUENTIAL) {
+    for (int i = 0; i < n; ++i) {
+      if ((st = run_walk(ctx, {base[i]}, false))) return st;
+      ++runs;
+      ctx->stats.rounds += 1;
+      if ((st = fetch_out(ctx, n))) return st;
+      if (ctx->h_out[i].status == FMDP_ACCEPTED && (st = commit_slots(ctx, {i}, base, aircraft, plan_id))) return st;
+    }
+  } else {
+    // Speculative FCFS rounds (DESIGN.md a10): run every not-yet-valid request against the
+    // current store, then commit in array order while no plan committed after a request's
+    // run could have influenced it; an influenced request resumes from its first
+    // influenced step in the next round.  Identical to the sequential loop.
+    std::vector<char> valid(n, 0);
+    std::vector<int> start(n, 0);
+    std::vector<size_t> version(n, 0);
+    std::vector<int> committed;  // slots committed during this call, in order
+    int c = 0;
+    while (c < n) {
+      std::vector<Req> run;
+      for (int i = c; i < n; ++i)
+        if (!valid[i]) {
+          Req r = base[i];
+          r.start_k = start[i];
+          run.push_back(r);
+        }
+      if ((st = run_walk(ctx, run, false))) return st;
+      runs += (int)run.size();
+      ctx->stats.rounds += 1;
+      for (const Req& r : run) {
+        valid[r.slot] = 1;
+        version[r.slot] = ctx->plans.size();
+      }
+      if ((st = fetch_out(ctx, n))) return st;
+      std::vector<int32_t> ns(n);
+      for (int i = 0; i < n; ++i) ns[i] = ctx->h_out[i].n_states;
+      CK(cudaMemcpyAsync(ctx->d_nstates, ns.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+      // influence pairs (i, j): j committed after i's run, or j < i accepted in this round's walk
+      std::vector<InflPair> pairs;
+      for (int i = c; i < n; ++i) {
+        if (!valid[i]) continue;
+        for (int j : committed)
+          if (plan_id[j] >= version[i]) pairs.push_back({i, j});
+        for (int j = c; j < i; ++j)
+          if (valid[j] && ctx->h_out[j].status == FMDP_ACCEPTED) pairs.push_back({i, j});
+      }
+      std::vector<int32_t> kf;
+      if ((st = influence(ctx, pairs, kf))) return st;
+      std::vector<int> newly;
+      auto kfirst_of = [&](int i, bool only_newly) {
+        int best = INT_MAX;
+        for (size_t p = 0; p < pairs.size(); ++p) {
+          if (pairs[p].i != i || kf[p] == INT_MAX) continue;
+          const int j = pairs[p].j;
+          const bool in_new = std::find(newly.begin(), newly.end(), j) != newly.end();
+          const bool in_old = !only_newly && plan_id[j] != 0xffffffffu && plan_id[j] >= version[i];
+          if (in_new || in_old) best = std::min(best, kf[p]);
+        }
+        return best;
+      };
+      while (c < n && valid[c]) {
+        const int k1 = kfirst_of(c, false);
+        if (k1 != INT_MAX) {
+          valid[c] = 0;
+          start[c] = k1;
+          break;
+        }
+        if (ctx->h_out[c].status == FMDP_ACCEPTED) newly.push_back(c);
+        ++c;
+      }
+      if ((st = commit_slots(ctx, newly, base, aircraft, plan_id))) return st;
+      committed.insert(committed.end(), newly.begin(), newly.end());
+      for (int i = c + 1; i < n; ++i) {
+        if (!valid[i]) continue;
+        const int k1 = kfirst_of(i, true);
+        if (k1 != INT_MAX) {
+          valid[i] = 0;
+          start[i] = k1;
+        }
+      }
+    }
+  }
+  ctx->stats.reruns = runs - n;
+  if ((st = fetch_out(ctx, n))) return st;
+  unsigned long long pc = 0;
+  CK(cudaMemcpy(&pc, ctx->d_pairctr, sizeof(pc), cudaMemcpyDeviceToHost));
+  ctx->stats.pair_evals = (int64_t)pc;
+  for (int i = 0; i < n; ++i) {
+    const Out& o = ctx->h_out[i];
+    res[i].status = o.status;
+    res[i].plan_id = plan_id[i];
+    res[i].n_states = o.n_states;
+    res[i].fail_step = o.fail_step;
+    res[i].min_sep_m = std::sqrt((double)o.min_sep_d2) * ctx->air.u_m;
+    res[i].n_near_ties = o.n_near_ties;
+    res[i].n_exact = o.n_exact;
+    ctx->stats.steps += o.steps_run;
+  }
+  if (traj) {
+    for (int i = 0; i < n; ++i) {
+      CK(cudaMemcpyAsync(traj + (size_t)i * traj_cap_each, ctx->d_traj + (size_t)i * ctx->cap_states * 3,
+                         sizeof(fmdp_qpos) * ctx->h_out[i].n_states, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  ctx->last_n = n;
+  return FMDP_OK;
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+extern "C" {
+
+void fmdp_airspace_default(fmdp_airspace* a) {
+  static const int32_t turns[9] = {-8, -6, -4, -2, 0, 2, 4, 6, 8};
+  static const int32_t climbs[3] = {-16, 0, 16};
+  static const double taus[5] = {-5.0, 0.0, 5.0, 10.0, 15.0};
+  static const double radii[5] = {250.0, 300.0, 350.0, 400.0, 450.0};
+  std::memset(a, 0, sizeof(*a));
+  a->abi_version = FMDP_ABI_VERSION;
+  a->lo = {-8000.0, -8000.0, 0.0};
+  a->hi = {8000.0, 8000.0, 1500.0};
+  a->u_m = 1.0 / 64.0;
+  a->dt = 0.1;
+  a->window = 10;
+  a->speed = 50.0;
+  a->heading_lattice = 1440;
+  a->n_turn = 9;
+  a->turn_steps = turns;
+  a->n_climb = 3;
+  a->climb_units = climbs;
+  a->goal_r = 200.0;
+  a->goal_gamma = 0.999;
+  a->intr_r = 1000.0;
+  a->intr_gamma = 0.97;
+  a->n_tau = 5;
+  a->tau_s = taus;
+  a->tau_radius_m = radii;
+  a->terr_r = 1000.0;
+  a->terr_gamma = 0.99;
+  a->deck_alt_m = 30.0;
+  a->deck_scale = 1000.0;
+  a->capture_radius_m = 100.0;
+  a->sep_min_m = 150.0;
+  a->max_steps = 4000;
+  a->vmax_init_zero = 0;
+  a->near_tie_rel = 1e-4;
+  a->horizon_steps = 8192;
+  a->row_capacity = 4096;
+}
+
+const char* fmdp_strerror(fmdp_status s) {
+  if (s == FMDP_E_INTERNAL) return "internal error";
+  const int i = -s;
+  if (i >= 0 && i < (int)(sizeof(kStatusText) / sizeof(kStatusText[0]))) return kStatusText[i];
+  return "unknown status";
+}
+
+const char* fmdp_last_error(const fmdp_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int32_t fmdp_num_actions(const fmdp_ctx* ctx) { return ctx ? ctx->A : 0; }
+
+fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const fmdp_devices* devs,
+                        fmdp_ctx** out) {
+  if (!air || !out) return FMDP_E_ARG;
+  *out = nullptr;
+  if (air->abi_version != FMDP_ABI_VERSION) return FMDP_E_ARG;
+  fmdp_ctx* ctx = new (std::nothrow) fmdp_ctx();
+  if (!ctx) return FMDP_E_NOMEM;
+  auto bad = [&](fmdp_status s, const char* m) {
+    std::fprintf(stderr, "fmdp_create: %s\n", m);
+    delete ctx;
+    return s;
+  };
+  const fmdp_airspace& a = *air;
+  if (!(a.u_m > 0) || !(a.dt > 0) || a.window < 1 || a.window > fmdp::MAX_W) return bad(FMDP_E_ARG, "u/dt/window");
+  if (a.heading_lattice < 8 || a.heading_lattice % 8) return bad(FMDP_E_ARG, "heading_lattice % 8");
+  if (a.n_turn < 1 || a.n_turn > fmdp::MAX_TURN || !a.turn_steps) return bad(FMDP_E_ARG, "turns");
+  if (!(a.n_climb == 1 || a.n_climb == 3 || a.n_climb == 5) || !a.climb_units) return bad(FMDP_E_ARG, "climbs");
+  if (a.n_tau < 1 || a.n_tau > fmdp::NTAU || !a.tau_s || !a.tau_radius_m) return bad(FMDP_E_ARG, "tau");
+  const int A = a.n_turn * a.n_climb;
+  if (A * a.window > fmdp::MAX_AW) return bad(FMDP_E_ARG, "A*W too large");
+  int64_t step_u;
+  if (!integral(a.speed * a.dt / a.u_m, &step_u) || step_u <= 0 || step_u > 1000) return bad(FMDP_E_ARG, "speed");
+  for (int i = 0; i < a.n_climb; ++i)
+    if (std::abs(a.climb_units[i]) > 100) return bad(FMDP_E_ARG, "climb rate");
+  int64_t zdeck, capu, sepu;
+  if (!integral(a.deck_alt_m / a.u_m, &zdeck) || !integral(a.capture_radius_m / a.u_m, &capu) ||
+      !integral(a.sep_min_m / a.u_m, &sepu) || capu <= 0 || sepu <= 0)
+    return bad(FMDP_E_ARG, "deck/capture/sep must be multiples of u");
+  if (a.horizon_steps < 4 || a.row_capacity < 4 || a.row_capacity % 4) return bad(FMDP_E_ARG, "store geometry");
+  if (a.max_steps < 1) return bad(FMDP_E_ARG, "max_steps");
+
+  ctx->air = a;
+  ctx->turn.assign(a.turn_steps, a.turn_steps + a.n_turn);
+  ctx->climb.assign(a.climb_units, a.climb_units + a.n_climb);
+  ctx->tau_s.assign(a.tau_s, a.tau_s + a.n_tau);
+  ctx->tau_r.assign(a.tau_radius_m, a.tau_radius_m + a.n_tau);
+  ctx->air.turn_steps = ctx->turn.data();
+  ctx->air.climb_units = ctx->climb.data();
+  ctx->air.tau_s = ctx->tau_s.data();
+  ctx->air.tau_radius_m = ctx->tau_r.data();
+  ctx->A = A;
+  ctx->W = a.window;
+  ctx->C = a.n_climb;
+  const double lo[3] = {a.lo.x, a.lo.y, a.lo.z}, hi[3] = {a.hi.x, a.hi.y, a.hi.z};
+  for (int d = 0; d < 3; ++d) {
+    ctx->lo_u[d] = std::llrint(lo[d] / a.u_m);
+    ctx->hi_u[d] = std::llrint(hi[d] / a.u_m);
+    if (ctx->hi_u[d] <= ctx->lo_u[d] || ctx->hi_u[d] - ctx->lo_u[d] >= (1LL << 24))
+      return bad(FMDP_E_RANGE, "airspace span must be positive and < 2^24 units");
+  }
+
+  // device
+  int dev = devs ? devs->device : -1;
+  if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) return bad(FMDP_E_NODEV, "no CUDA device");
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return bad(FMDP_E_NODEV, "no CUDA device");
+  }
+  if (prop.major != 10) return bad(FMDP_E_NODEV, "libfmdp is built for sm_100a only");
+  if (cudaSetDevice(dev) != cudaSuccess) return bad(FMDP_E_NODEV, "cudaSetDevice failed");
+  ctx->device = dev;
+  ctx->num_sms = prop.multiProcessorCount;
+  if (devs) {
+    ctx->alloc = devs->alloc;
+    ctx->release = devs->release;
+    ctx->user = devs->user;
+    ctx->stream = (cudaStream_t)devs->stream;
+  }
+  if (!ctx->stream) {
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess)
+      return bad(FMDP_E_CUDA, "stream");
+    ctx->own_stream = true;
+  }
+  cudaEventCreate(&ctx->ev0);
+  cudaEventCreate(&ctx->ev1);
+
+  World& w = ctx->w;
+  std::memset(&w, 0, sizeof(w));
+  w.A = A;
+  w.W = a.window;
+  w.n_turn = a.n_turn;
+  w.n_climb = a.n_climb;
+  w.HL = a.heading_lattice;
+  for (int i = 0; i < a.n_turn; ++i) w.turn[i] = a.turn_steps[i];
+  for (int i = 0; i < a.n_climb; ++i) w.climb[i] = a.climb_units[i];
+  int64_t Rmax = 0;
+  for (int i = 0; i < fmdp::NTAU; ++i) {
+    if (i < a.n_tau) {
+      int64_t k, R;
+      if (!integral(a.tau_s[i] / a.dt, &k) || !integral(a.tau_radius_m[i] / a.u_m, &R) || R <= 0)
+        return bad(FMDP_E_ARG, "tau/dt and radii/u must be integral");
+      w.k_tau[i] = (int32_t)k;
+      w.R2_tau[i] = R * R;
+      const double d = std::ldexp(1.0, -20);
+      w.R2lo[i] = (float)((double)(R * R) * (1.0 - d));
+      w.R2hi[i] = (float)((double)(R * R) * (1.0 + d));
+      Rmax = std::max(Rmax, R);
+    } else {
+      w.k_tau[i] = 0;
+      w.R2_tau[i] = 0;
+      w.R2lo[i] = -1.f;
+      w.R2hi[i] = -1.f;
+    }
+  }
+  if (Rmax >= 32768) return bad(FMDP_E_ARG, "well radius must be < 2^15 units");
+  if (sepu >= Rmax) return bad(FMDP_E_ARG, "separation minimum must be below the largest well radius");
+  w.R_max = (int32_t)Rmax;
+  w.sat_d2 = (uint32_t)(Rmax * Rmax);
+  w.sep2 = (uint32_t)(sepu * sepu);
+  w.cap2 = capu * capu;
+  w.goal_r = std::fabs(a.goal_r);
+  w.goal_l2g = std::log2(a.goal_gamma) * a.u_m;
+  w.intr_r = (float)std::fabs(a.intr_r);
+  w.intr_l2g = (float)(std::log2(a.intr_gamma) * a.u_m);
+  w.terr_r = (float)std::fabs(a.terr_r);
+  w.terr_l2g = (float)(std::log2(a.terr_gamma) * a.u_m);
+  w.zdeck_u = (int32_t)zdeck;
+  w.deck_scale = a.deck_scale;
+  w.u_m = a.u_m;
+  w.max_steps = a.max_steps;
+  w.vmax_init_zero = a.vmax_init_zero;
+  w.near_tie_rel = a.near_tie_rel;
+  w.horizon = a.horizon_steps;
+  w.row_cap = a.row_capacity;
+
+  std::vector<int2> lat;
+  build_lattice(w.HL, step_u, lat);
+  double maxd = 0;
+  for (const int2& d : lat) maxd = std::max(maxd, std::sqrt((double)d.x * d.x + (double)d.y * d.y));
+  int maxc = 0;
+  for (int c : ctx->climb) maxc = std::max(maxc, std::abs(c));
+  w.reach_u = (int32_t)(a.window * ((int64_t)std::ceil(maxd) + maxc) + 1);
+  int kmax = 0;
+  for (int i = 0; i < a.n_tau; ++i) kmax = std::max(kmax, std::abs(w.k_tau[i]));
+  const int64_t vdyn = (int64_t)std::ceil(std::sqrt(maxd * maxd + (double)maxc * maxc));
+  const int64_t B = Rmax + w.reach_u + (int64_t)kmax * vdyn + 2;
+  ctx->bound2 = B * B;
+
+  // device memory
+  const size_t row_words = (size_t)4 * w.row_cap;
+  ctx->d_rows = (int32_t*)dalloc(ctx, sizeof(int32_t) * row_words * (size_t)w.horizon);
+  ctx->d_counts = (int32_t*)dalloc(ctx, sizeof(int32_t) * (size_t)w.horizon);
+  ctx->d_dxy = (int2*)dalloc(ctx, sizeof(int2) * w.HL);
+  ctx->d_queue = (int32_t*)dalloc(ctx, sizeof(int32_t) * 4);
+  ctx->d_pairctr = (unsigned long long*)dalloc(ctx, sizeof(unsigned long long));
+  ctx->d_dbg_vstar = (double*)dalloc(ctx, sizeof(double) * A);
+  ctx->d_dbg_v = (double*)dalloc(ctx, sizeof(double) * A * a.window);
+  ctx->d_dbg_s = (double*)dalloc(ctx, sizeof(double) * A * a.window);
+  ctx->d_dbg_conf = (uint32_t*)dalloc(ctx, sizeof(uint32_t) * (A + 1));
+  ctx->d_dbg_astar = (int32_t*)dalloc(ctx, sizeof(int32_t) * 4);
+  if (!ctx->d_rows || !ctx->d_counts || !ctx->d_dxy || !ctx->d_queue || !ctx->d_pairctr || !ctx->d_dbg_vstar ||
+      !ctx->d_dbg_v || !ctx->d_dbg_s || !ctx->d_dbg_conf || !ctx->d_dbg_astar) {
+    fmdp_destroy(ctx);
+    return FMDP_E_NOMEM;
+  }
+  cudaMemset(ctx->d_rows, 0, sizeof(int32_t) * row_words * (size_t)w.horizon);
+  cudaMemset(ctx->d_counts, 0, sizeof(int32_t) * (size_t)w.horizon);
+  cudaMemcpy(ctx->d_dxy, lat.data(), sizeof(int2) * w.HL, cudaMemcpyHostToDevice);
+  ctx->counts.assign((size_t)w.horizon, 0);
+  w.rows = ctx->d_rows;
+  w.counts = ctx->d_counts;
+  w.dxy = ctx->d_dxy;
+
+  if (ter && ter->n_wells > 0) {
+    if (!ter->center || !ter->radius_u) {
+      fmdp_destroy(ctx);
+      return FMDP_E_ARG;
+    }
+    std::vector<int4> tw(ter->n_wells);
+    for (int i = 0; i < ter->n_wells; ++i)
+      tw[i] = make_int4(ter->center[i].x, ter->center[i].y, ter->center[i].z, ter->radius_u[i]);
+    ctx->d_tw = (int4*)dalloc(ctx, sizeof(int4) * tw.size());
+    if (!ctx->d_tw) {
+      fmdp_destroy(ctx);
+      return FMDP_E_NOMEM;
+    }
+    cudaMemcpy(ctx->d_tw, tw.data(), sizeof(int4) * tw.size(), cudaMemcpyHostToDevice);
+    w.n_tw = ter->n_wells;
+    w.tw = ctx->d_tw;
+  }
+  if (ter && ter->nx > 0 && ter->ny > 0) {
+    if (!ter->height_u || ter->cell_u <= 0) {
+      fmdp_destroy(ctx);
+      return FMDP_E_ARG;
+    }
+    const size_t nh = (size_t)ter->nx * ter->ny;
+    ctx->d_height = (int32_t*)dalloc(ctx, sizeof(int32_t) * nh);
+    if (!ctx->d_height) {
+      fmdp_destroy(ctx);
+      return FMDP_E_NOMEM;
+    }
+    cudaMemcpy(ctx->d_height, ter->height_u, sizeof(int32_t) * nh, cudaMemcpyHostToDevice);
+    w.nx = ter->nx;
+    w.ny = ter->ny;
+    w.x0 = ter->x0_u;
+    w.y0 = ter->y0_u;
+    w.cell = ter->cell_u;
+    w.height = ctx->d_height;
+  }
+  ctx->cap_states = a.max_steps + 2;
+  if (fmdp::walk_smem_bytes(w, ctx->C, threads_for(ctx), kChunk) > 227 * 1024) {
+    fmdp_destroy(ctx);
+    return FMDP_E_ARG;
+  }
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    fmdp_destroy(ctx);
+    return FMDP_E_CUDA;
+  }
+  *out = ctx;
+  return FMDP_OK;
+}
+
+void fmdp_destroy(fmdp_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  std::vector<void*> a = ctx->allocs;
+  for (void* p : a) dfree(ctx, p);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+fmdp_status fmdp_set_launch(fmdp_ctx* ctx, const fmdp_launch* l) {
+  if (!ctx) return FMDP_E_ARG;
+  fmdp_launch n{};
+  if (l) n = *l;
+  if (n.cluster_size < 0 || n.cluster_size > 16 || (n.cluster_size & (n.cluster_size - 1)))
+    return fail(ctx, FMDP_E_ARG, "cluster_size must be 0 or a power of two <= 16");
+  if (n.threads && (n.threads % 32 || n.threads > 512 || n.threads < ctx->A))
+    return fail(ctx, FMDP_E_ARG, "threads must be a multiple of 32 in [A, 512]");
+  if (n.threads) {
+    const int ncol = ctx->w.n_turn * ctx->w.W, group = (ncol + 31) & ~31;
+    if (n.threads % group) return fail(ctx, FMDP_E_ARG, "threads must be a multiple of the column group");
+  }
+  ctx->launch = n;
+  std::memset(ctx->mc_cache, 0, sizeof(ctx->mc_cache));
+  if (fmdp::walk_smem_bytes(ctx->w, ctx->C, threads_for(ctx), kChunk) > 227 * 1024)
+    return fail(ctx, FMDP_E_ARG, "shared memory");
+  return FMDP_OK;
+}
+
+fmdp_status fmdp_add_plans(fmdp_ctx* ctx, int32_t n_plans, const uint64_t* aircraft_ids, const int64_t* t0_steps,
+                           const int32_t* n_states, const fmdp_qpos* states, uint32_t* first_id) {
+  if (!ctx || n_plans < 0 || (n_plans > 0 && (!t0_steps || !n_states || !states)))
+    return fail(ctx, FMDP_E_ARG, "null argument");
+  if (first_id) *first_id = (uint32_t)ctx->plans.size();
+  if (n_plans == 0) return FMDP_OK;
+  std::vector<int64_t> t0(n_plans);
+  std::vector<int32_t> n(n_plans);
+  size_t tot = 0;
+  const int64_t margin = 1LL << 20;
+  for (int i = 0; i < n_plans; ++i) {
+    t0[i] = t0_steps[i];
+    n[i] = n_states[i];
+    if (n[i] < 1) return fail(ctx, FMDP_E_ARG, "plan with no states");
+    if (t0[i] < 0 || t0[i] + n[i] > ctx->w.horizon) return fail(ctx, FMDP_E_RANGE, "plan rows outside horizon");
+    const fmdp_qpos* s = states + tot;
+    for (int k = 0; k < n[i]; ++k) {
+      const int32_t p[3] = {s[k].x, s[k].y, s[k].z};
+      for (int d = 0; d < 3; ++d)
+        if (p[d] < ctx->lo_u[d] - margin || p[d] > ctx->hi_u[d] + margin)
+          return fail(ctx, FMDP_E_RANGE, "plan state far outside the airspace");
+      if (k + 1 < n[i]) {
+        const int64_t vx = (int64_t)s[k + 1].x - s[k].x, vy = (int64_t)s[k + 1].y - s[k].y,
+                      vz = (int64_t)s[k + 1].z - s[k].z;
+        if (vx < -1024 || vx > 1023 || vy < -1024 || vy > 1023 || vz < -512 || vz > 511)
+          return fail(ctx, FMDP_E_RANGE, "plan velocity beyond the packed store record");
+      }
+    }
+    tot += n[i];
+  }
+  if (!rows_fit(ctx, t0, n)) return fail(ctx, FMDP_E_CAPACITY, "time row capacity exceeded");
+  // upload in chunks of whole plans
+  const size_t kMaxWords = (size_t)48 << 20;
+  size_t off = 0;
+  int p0 = 0;
+  while (p0 < n_plans) {
+    size_t words = 0;
+    int p1 = p0;
+    while (p1 < n_plans && (p1 == p0 || words + 3 * (size_t)n[p1] <= kMaxWords)) words += 3 * (size_t)n[p1++];
+    fmdp_status st = ensure_up(ctx, words + (words / 3));
+    if (st) return st;
+    // states first, then slots (append_device writes slots at d_up, so place states after)
+    int32_t* d_states = nullptr;
+    {
+      // reserve: slots [0, words/3), states [words/3, words/3 + words)
+      d_states = ctx->d_up + words / 3;
+      CK(cudaMemcpyAsync(d_states, states + off, sizeof(int32_t) * words, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    std::vector<int64_t> ct0(t0.begin() + p0, t0.begin() + p1);
+    std::vector<int32_t> cn(n.begin() + p0, n.begin() + p1);
+    std::vector<const int32_t*> ds;
+    size_t o = 0;
+    for (int i = p0; i < p1; ++i) {
+      ds.push_back(d_states + o);
+      o += 3 * (size_t)n[i];
+    }
+    st = append_device(ctx, ct0, cn, ds);
+    if (st) return st;
+    for (int i = p0; i < p1; ++i) {
+      PlanRec r;
+      r.aircraft = aircraft_ids ? aircraft_ids[i] : 0;
+      r.t0 = t0[i];
+      const int32_t* src = reinterpret_cast<const int32_t*>(states + off);
+      r.states.assign(src, src + 3 * (size_t)n[i]);
+      off += n[i];
+      ctx->plans.push_back(std::move(r));
+    }
+    p0 = p1;
+  }
+  return FMDP_OK;
+}
+
+fmdp_status fmdp_add_plan(fmdp_ctx* ctx, uint64_t aircraft_id, int64_t t0_step, int32_t n, const fmdp_qpos* states,
+                          int32_t flags, uint32_t* plan_id) {
+  (void)flags;
+  return fmdp_add_plans(ctx, 1, &aircraft_id, &t0_step, &n, states, plan_id);
+}
+
+fmdp_status fmdp_schedule(fmdp_ctx* ctx, uint64_t aircraft_id, fmdp_vec3 src, fmdp_vec3 dst, int64_t t0_step,
+                          fmdp_result* res, fmdp_qpos* traj, int32_t traj_cap) {
+  fmdp_request r;
+  r.aircraft_id = aircraft_id;
+  r.src = src;
+  r.dst = dst;
+  r.t0_step = t0_step;
+  return schedule_many(ctx, &r, 1, res, traj, traj_cap, FMDP_BATCH_SEQUENTIAL);
+}
+
+fmdp_status fmdp_schedule_batch(fmdp_ctx* ctx, const fmdp_request* reqs, int32_t n, fmdp_result* res,
+                                fmdp_qpos* traj, int32_t traj_cap_each, int32_t flags) {
+  return schedule_many(ctx, reqs, n, res, traj, traj_cap_each, flags);
+}
+
+fmdp_status fmdp_get_steplog(fmdp_ctx* ctx, int32_t index, int32_t* astar, int32_t* heading, int32_t* near_tie,
+                             int32_t cap, int32_t* n) {
+  if (!ctx || index < 0 || index >= ctx->last_n) return fail(ctx, FMDP_E_ARG, "no such request in the last call");
+  const int ns = ctx->h_out[index].n_states;
+  if (n) *n = ns;
+  if (cap < ns) return FMDP_E_BUFFER;
+  const size_t b = (size_t)index * ctx->cap_states;
+  if (astar) CK(cudaMemcpy(astar, ctx->d_astar + b, sizeof(int32_t) * ns, cudaMemcpyDeviceToHost));
+  if (heading) CK(cudaMemcpy(heading, ctx->d_heading + b, sizeof(int32_t) * ns, cudaMemcpyDeviceToHost));
+  if (near_tie) {
+    std::vector<int8_t> t(ns);
+    CK(cudaMemcpy(t.data(), ctx->d_ntie + b, ns, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < ns; ++i) near_tie[i] = t[i];
+  }
+  return FMDP_OK;
+}
+
+fmdp_status fmdp_get_plan(fmdp_ctx* ctx, uint32_t plan_id, int64_t* t0_step, fmdp_qpos* buf, int32_t cap, int32_t* n) {
+  if (!ctx || plan_id >= ctx->plans.size()) return fail(ctx, FMDP_E_ARG, "no such plan");
+  const PlanRec& p = ctx->plans[plan_id];
+  const int32_t ns = (int32_t)(p.states.size() / 3);
+  if (n) *n = ns;
+  if (t0_step) *t0_step = p.t0;
+  if (!buf) return FMDP_OK;
+  if (cap < ns) return FMDP_E_BUFFER;
+  std::memcpy(buf, p.states.data(), sizeof(int32_t) * p.states.size());
+  return FMDP_OK;
+}
+
+fmdp_status fmdp_num_plans(const fmdp_ctx* ctx, uint32_t* n) {
+  if (!ctx || !n) return FMDP_E_ARG;
+  *n = (uint32_t)ctx->plans.size();
+  return FMDP_OK;
+}
+
+fmdp_status fmdp_truncate(fmdp_ctx* ctx, uint32_t n_plans) {
+  if (!ctx) return FMDP_E_ARG;
+  if (n_plans >= ctx->plans.size()) return FMDP_OK;
+  // later plans occupy the top slots of each of their rows (appends are in id order)
+  for (size_t i = n_plans; i < ctx->plans.size(); ++i) {
+    const PlanRec& p = ctx->plans[i];
+    const int64_t ns = (int64_t)(p.states.size() / 3);
+    for (int64_t k = 0; k < ns; ++k) ctx->counts[p.t0 + k] -= 1;
+  }
+  ctx->plans.resize(n_plans);
+  CK(cudaMemcpyAsync(ctx->d_counts, ctx->counts.data(), sizeof(int32_t) * ctx->counts.size(), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return FMDP_OK;
+}
+
+fmdp_status fmdp_eval_step(fmdp_ctx* ctx, fmdp_qpos pos, int32_t heading, fmdp_qpos goal, int64_t clock_step,
+                           double* vstar, double* v_at, double* scale_at, int32_t* conflict, int64_t* min_d2,
+                           int32_t* a_star) {
+  if (!ctx || !vstar) return fail(ctx, FMDP_E_ARG, "null argument");
+  if (clock_step < 0 || clock_step + 1 >= ctx->w.horizon) return fail(ctx, FMDP_E_RANGE, "clock outside horizon");
+  if (heading < 0 || heading >= ctx->w.HL) return fail(ctx, FMDP_E_ARG, "heading outside the lattice");
+  fmdp_status st = ensure_slots(ctx, 1);
+  if (st) return st;
+  Req r;
+  std::memset(&r, 0, sizeof(r));
+  r.src[0] = pos.x; r.src[1] = pos.y; r.src[2] = pos.z;
+  r.dst[0] = goal.x; r.dst[1] = goal.y; r.dst[2] = goal.z;
+  r.psi0 = heading;
+  r.t0 = clock_step;
+  r.slot = 0;
+  if ((st = run_walk(ctx, {r}, true))) return st;
+  const int A = ctx->A, AW = A * ctx->W;
+  std::vector<uint32_t> conf(A + 1);
+  int32_t as = 0;
+  CK(cudaMemcpy(vstar, ctx->d_dbg_vstar, sizeof(double) * A, cudaMemcpyDeviceToHost));
+  if (v_at) CK(cudaMemcpy(v_at, ctx->d_dbg_v, sizeof(double) * AW, cudaMemcpyDeviceToHost));
+  if (scale_at) CK(cudaMemcpy(scale_at, ctx->d_dbg_s, sizeof(double) * AW, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(conf.data(), ctx->d_dbg_conf, sizeof(uint32_t) * (A + 1), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&as, ctx->d_dbg_astar, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (conflict)
+    for (int a = 0; a < A; ++a) conflict[a] = conf[a] < ctx->w.sep2 ? 1 : 0;
+  if (min_d2)
+    for (int a = 0; a <= A; ++a) min_d2[a] = conf[a];
+  if (a_star) *a_star = as;
+  return FMDP_OK;
+}
+
+fmdp_status fmdp_get_stats(const fmdp_ctx* ctx, fmdp_stats* out) {
+  if (!ctx || !out) return FMDP_E_ARG;
+  *out = ctx->stats;
+  return FMDP_OK;
+}
+
+}  // extern "C"

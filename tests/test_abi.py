@@ -1,0 +1,63 @@
+"""C-ABI library: builds for sm_100a, loads, exports every symbol include/fmdp.h declares,
+and fails loudly (no CPU fallback) when no sm_100 device is present."""
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "fmdp.h")
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(fmdp_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_library_builds_and_exports_header_symbols():
+    from paper_2008_03518_b200.build import build
+    lib = build()
+    out = subprocess.run(["nm", "-D", "--defined-only", lib], capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (fmdp_\w+)", out))
+    want = declared_symbols()
+    assert len(want) >= 15
+    missing = [s for s in want if s not in exported]
+    assert not missing, f"declared but not exported: {missing}"
+    from paper_2008_03518_b200 import fmdp
+    assert set(fmdp.EXPORTS) <= exported
+    L = fmdp.lib()
+    for s in want:
+        assert hasattr(L, s)
+
+
+def test_sass_is_sm100a_and_uses_bulk_copy():
+    from paper_2008_03518_b200.build import build
+    lib = build()
+    out = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True, check=True).stdout
+    assert "sm_100a" in out
+    assert "UBLKCP" in out            # cp.async.bulk (TMA bulk copy) staging of the plan rows
+    assert "FMNMX" in out and "FFMA" in out
+
+
+def test_strerror_and_no_cpu_fallback():
+    from paper_2008_03518_b200 import fmdp
+    L = fmdp.lib()
+    assert L.fmdp_strerror(-8).decode() == "no sm_100 device"
+    assert L.fmdp_strerror(0).decode() == "ok"
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    import fmdp_synth as fs
+    with pytest.raises(fmdp.FmdpError, match="no sm_100 device"):
+        fmdp.FMDP(fs.Airspace(), torch_alloc=False)
+
+
+def test_product_package_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2008_03518_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"#.*|//.*", "", txt).lower().replace("no cpu fallback", ""), f
