@@ -235,7 +235,8 @@ def random_small(seed: int, n_plans: int = 40, n_requests: int = 4, half_m: floa
     request band so that wells, exact-boundary cases and conflicts all occur."""
     rng = np.random.default_rng(seed)
     a = Airspace(max_steps=max_steps, lo_m=(-half_m, -half_m, z_m[0]), hi_m=(half_m, half_m, z_m[1]),
-                 horizon_steps=int(rows + max_steps + 8), row_capacity=max(64, n_plans + n_requests + 8))
+                 horizon_steps=int(rows + max_steps + 8),
+                 row_capacity=(max(64, n_plans + n_requests + 8) + 3) // 4 * 4)
     a = a.replace(**air)
     terrain = (manhattan_terrain(rng, n_buildings, core_half_m=min(1000.0, half_m), raster_half_m=half_m)
                if n_buildings else Terrain())

@@ -127,6 +127,7 @@ typedef struct fmdp_launch {
   int32_t cluster_size;   /* CTAs cooperating on one trajectory (1..16), 0 = auto        */
   int32_t max_walkers;    /* concurrent trajectories in a batch round, 0 = auto          */
   int32_t threads;        /* threads per CTA, 0 = auto                                   */
+  int32_t profile;        /* 1: accumulate per-phase cycles of CTA 0 (fmdp_stats)        */
 } fmdp_launch;
 
 typedef struct fmdp_request {
@@ -156,6 +157,9 @@ typedef struct fmdp_stats {
   int32_t walkers;
   int32_t kernels;         /* kernel launches                                             */
   double device_ms;        /* sum of walk-kernel device time (CUDA events)                */
+  int64_t phase_cycles[10]; /* profile=1: CTA-0 cycles per phase: projection, goal/terrain, */
+                           /* row wait, hot loop, stage, reduce-scatter, barrier 1,         */
+                           /* owner epilogue, barrier 2, decide                             */
 } fmdp_stats;
 
 /* Fill *a with the defaults of DESIGN.md Appendix A (the arrays point to static storage). */
@@ -217,8 +221,9 @@ fmdp_status fmdp_truncate(fmdp_ctx* ctx, uint32_t n_plans);
  * the same device code as fmdp_schedule (parity / debug hook; V mirrors Table DS "V",
  * P:405).  Outputs (host pointers, any may be NULL except vstar):
  *   vstar[A], v_at[A*W], scale_at[A*W] (V+ + max(V^T,V^I) + V_alt), conflict[A] (1 if
- *   Delta_1(a) is within sep of a plan at row clock+1), min_d2[A+1] (saturated min d^2 of
- *   Delta_1(a) to row clock+1; entry A: pos to row clock), *a_star. */
+ *   Delta_1(a) is within sep of a plan at row clock+1, i.e. choosing a would end the
+ *   request with a separation conflict at the next step), min_d2[A+1] (saturated min d^2
+ *   of Delta_1(a) to row clock+1; entry A: pos to row clock), *a_star. */
 fmdp_status fmdp_eval_step(fmdp_ctx* ctx, fmdp_qpos pos, int32_t heading, fmdp_qpos goal,
                            int64_t clock_step, double* vstar, double* v_at, double* scale_at,
                            int32_t* conflict, int64_t* min_d2, int32_t* a_star);

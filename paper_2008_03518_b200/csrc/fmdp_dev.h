@@ -13,6 +13,8 @@ constexpr int MAX_W = 16;
 constexpr int MAX_AW = 1024;    // projected states per step (A*W)
 constexpr int AMB_MAX = 64;     // ambiguous (state, tau) minima handled per step
 constexpr int TC_MAX = 128;     // terrain-well candidates per step
+constexpr int TW_SMEM = 512;    // terrain wells cached in shared memory (more: read from L2)
+constexpr int N_PHASES = 10;    // walk-kernel phase accounting (fmdp_stats.phase_cycles)
 
 // Scenario + store in integer units, passed by value to the kernels.
 struct World {
@@ -82,25 +84,29 @@ struct WalkArgs {
   uint32_t* dbg_conf;           // [A+1]
   int32_t* dbg_astar;           // [1]
   unsigned long long* pairs;    // hot-loop pair counter (stats)
+  unsigned long long* prof;     // [PH_N] per-phase cycles of rank 0 (nullptr = off)
 };
 
 // Shared-memory carve-up, identical on host (size) and device (offsets).
+//   BLK: per-action block of the reduce-scatter = W*NTAU (state, tau) minima, padded to float4.
 struct Layout {
-  int HL, CH, NT, C, NCOL, A, AW, RED, RAWW;
-  size_t o_dxy, o_raw, o_cen, o_red, o_pos, o_fix, o_sfix, o_vT, o_mI, o_vstar, o_vsc, o_conf, o_confg,
-      o_amb, o_tc, o_bar, o_ctl, total;
+  int HL, CH, NT, C, NCOL, A, AW, G, BLK, NOWN, RAWW;
+  size_t o_dxy, o_tw, o_raw, o_cen, o_stage, o_recv, o_pos, o_fix, o_sfix, o_vT, o_mI, o_vstar, o_vsc, o_conf,
+      o_confg, o_flags, o_stay, o_amb, o_tc, o_bar, o_ctl, total;
   __host__ __device__ static size_t al(size_t x) { return (x + 15) & ~size_t(15); }
-  __host__ __device__ void build(int hl, int ch, int nt, int c, int ncol, int a, int aw) {
-    HL = hl; CH = ch; NT = nt; C = c; NCOL = ncol; A = a; AW = aw;
-    RED = NCOL * C * NTAU + A + 1;
+  __host__ __device__ void build(int hl, int ch, int nt, int c, int ncol, int a, int aw, int g) {
+    HL = hl; CH = ch; NT = nt; C = c; NCOL = ncol; A = a; AW = aw; G = g;
+    BLK = ((AW / A) * NTAU + 3) & ~3;
+    NOWN = (A + G - 1) / G;             // max actions owned by one CTA
     RAWW = CH + 8;                      // words per SoA array in one raw row buffer
     size_t o = 0;
     o_dxy = o;  o = al(o + sizeof(int2) * HL);
+    o_tw = o;   o = al(o + sizeof(int4) * TW_SMEM);
     o_raw = o;  o = al(o + sizeof(int32_t) * 4 * RAWW * 3);
     size_t cen = sizeof(float) * 16 * CH;
-    size_t part = sizeof(float) * (size_t)NT * C * NTAU;
-    o_cen = o;  o = al(o + (cen > part ? cen : part));
-    o_red = o;  o = al(o + sizeof(uint32_t) * 3 * RED);
+    o_cen = o;  o = al(o + cen);
+    o_stage = o; o = al(o + sizeof(float) * (size_t)A * BLK);
+    o_recv = o; o = al(o + sizeof(float) * 2 * (size_t)G * NOWN * BLK);
     o_pos = o;  o = al(o + sizeof(int4) * AW);
     o_fix = o;  o = al(o + sizeof(double) * AW);
     o_sfix = o; o = al(o + sizeof(double) * AW);
@@ -110,6 +116,8 @@ struct Layout {
     o_vsc = o;  o = al(o + sizeof(double) * A);
     o_conf = o; o = al(o + sizeof(uint32_t) * (A + 1));
     o_confg = o; o = al(o + sizeof(uint32_t) * (A + 1));
+    o_flags = o; o = al(o + sizeof(int32_t) * A);
+    o_stay = o; o = al(o + sizeof(uint32_t) * 2);
     o_amb = o;  o = al(o + sizeof(int32_t) * AMB_MAX);
     o_tc = o;   o = al(o + sizeof(int32_t) * TC_MAX);
     o_bar = o;  o = al(o + sizeof(uint64_t) * 4);
@@ -133,8 +141,11 @@ struct InflPair {
 // Kernel launchers (fmdp_walk.cu).
 cudaError_t launch_walk(const World& w, const WalkArgs& a, int n_climb, int cluster, int n_clusters,
                         int threads, int chunk, cudaStream_t s);
+// Hot-loop thread mapping: warps of 32/ngw columns x ngw plan groups; threads = 32*warps.
+int walk_groups_per_warp(int ncol, int max_threads);
+int walk_threads(int ncol, int max_threads);
 cudaError_t walk_max_clusters(const World& w, int n_climb, int cluster, int threads, int chunk, int* out);
-size_t walk_smem_bytes(const World& w, int n_climb, int threads, int chunk);
+size_t walk_smem_bytes(const World& w, int n_climb, int threads, int chunk, int cluster);
 cudaError_t launch_append(int32_t* rows, int32_t row_cap, int64_t horizon, const AppendPlan* plans, int n_plans,
                           int max_n, cudaStream_t s);
 cudaError_t launch_influence(const int32_t* traj, int32_t cap, const int32_t* n_states, const int64_t* t0,

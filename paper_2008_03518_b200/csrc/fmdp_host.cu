@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -68,6 +69,7 @@ struct fmdp_ctx {
   int32_t* d_nstates = nullptr;
   int64_t* d_t0s = nullptr;
   unsigned long long* d_pairctr = nullptr;
+  unsigned long long* d_prof = nullptr;
   InflPair* d_pairs = nullptr;
   int32_t* d_kfirst = nullptr;
   int pairs_cap = 0;
@@ -209,13 +211,8 @@ fmdp_status ensure_up(fmdp_ctx* ctx, size_t words) {
 }
 
 int threads_for(const fmdp_ctx* ctx) {
-  if (ctx->launch.threads > 0) return ctx->launch.threads;
-  const int ncol = ctx->w.n_turn * ctx->w.W;
-  const int group = (ncol + 31) & ~31;
-  int ng = std::max(1, 512 / group);
-  int nt = ng * group;
-  while (nt < ctx->A) nt += group;  // one conflict thread per action at least
-  return nt;
+  const int tmax = ctx->C == 1 ? 512 : 384;  // kernel __launch_bounds__
+  return fmdp::walk_threads(ctx->w.n_turn * ctx->w.W, tmax);
 }
 
 constexpr int kChunk = 512;
@@ -261,6 +258,9 @@ void choose_launch(fmdp_ctx* ctx, int n_run, int* G_out, int* nc_out) {
   if (ctx->launch.max_walkers > 0) conc = std::min(conc, ctx->launch.max_walkers);
   *G_out = best_G;
   *nc_out = std::max(1, conc);
+  if (std::getenv("FMDP_DEBUG"))
+    std::fprintf(stderr, "fmdp: n_run=%d plans/row=%.0f -> G=%d clusters=%d (max active %d)\n", n_run, plans, best_G,
+                 *nc_out, mc);
 }
 
 fmdp_status run_walk(fmdp_ctx* ctx, const std::vector<Req>& run, bool eval) {
@@ -285,6 +285,7 @@ fmdp_status run_walk(fmdp_ctx* ctx, const std::vector<Req>& run, bool eval) {
   a.dbg_conf = ctx->d_dbg_conf;
   a.dbg_astar = ctx->d_dbg_astar;
   a.pairs = ctx->d_pairctr;
+  a.prof = ctx->launch.profile ? ctx->d_prof : nullptr;
   int G = 1, nc = 1;
   choose_launch(ctx, (int)run.size(), &G, &nc);
   ctx->stats.cluster_size = G;
@@ -441,6 +442,7 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
   for (int i = 0; i < n; ++i) aircraft[i] = reqs[i].aircraft_id;
   std::vector<uint32_t> plan_id(n, 0xffffffffu);
   CK(cudaMemsetAsync(ctx->d_pairctr, 0, sizeof(unsigned long long), ctx->stream));
+  CK(cudaMemsetAsync(ctx->d_prof, 0, sizeof(unsigned long long) * fmdp::N_PHASES, ctx->stream));
   std::vector<int64_t> t0s(n);
   for (int i = 0; i < n; ++i) t0s[i] = base[i].t0;
   CK(cudaMemcpyAsync(ctx->d_t0s, t0s.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, ctx->stream));
@@ -533,6 +535,11 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
   unsigned long long pc = 0;
   CK(cudaMemcpy(&pc, ctx->d_pairctr, sizeof(pc), cudaMemcpyDeviceToHost));
   ctx->stats.pair_evals = (int64_t)pc;
+  if (ctx->launch.profile) {
+    unsigned long long ph[fmdp::N_PHASES];
+    CK(cudaMemcpy(ph, ctx->d_prof, sizeof(ph), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < fmdp::N_PHASES; ++i) ctx->stats.phase_cycles[i] = (int64_t)ph[i];
+  }
   for (int i = 0; i < n; ++i) {
     const Out& o = ctx->h_out[i];
     res[i].status = o.status;
@@ -625,6 +632,8 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   if (!(a.u_m > 0) || !(a.dt > 0) || a.window < 1 || a.window > fmdp::MAX_W) return bad(FMDP_E_ARG, "u/dt/window");
   if (a.heading_lattice < 8 || a.heading_lattice % 8) return bad(FMDP_E_ARG, "heading_lattice % 8");
   if (a.n_turn < 1 || a.n_turn > fmdp::MAX_TURN || !a.turn_steps) return bad(FMDP_E_ARG, "turns");
+  for (int i = 0; i < a.n_turn; ++i)
+    if (std::abs(a.turn_steps[i]) >= a.heading_lattice) return bad(FMDP_E_ARG, "turn step beyond the lattice");
   if (!(a.n_climb == 1 || a.n_climb == 3 || a.n_climb == 5) || !a.climb_units) return bad(FMDP_E_ARG, "climbs");
   if (a.n_tau < 1 || a.n_tau > fmdp::NTAU || !a.tau_s || !a.tau_radius_m) return bad(FMDP_E_ARG, "tau");
   const int A = a.n_turn * a.n_climb;
@@ -755,12 +764,13 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   ctx->d_dxy = (int2*)dalloc(ctx, sizeof(int2) * w.HL);
   ctx->d_queue = (int32_t*)dalloc(ctx, sizeof(int32_t) * 4);
   ctx->d_pairctr = (unsigned long long*)dalloc(ctx, sizeof(unsigned long long));
+  ctx->d_prof = (unsigned long long*)dalloc(ctx, sizeof(unsigned long long) * fmdp::N_PHASES);
   ctx->d_dbg_vstar = (double*)dalloc(ctx, sizeof(double) * A);
   ctx->d_dbg_v = (double*)dalloc(ctx, sizeof(double) * A * a.window);
   ctx->d_dbg_s = (double*)dalloc(ctx, sizeof(double) * A * a.window);
   ctx->d_dbg_conf = (uint32_t*)dalloc(ctx, sizeof(uint32_t) * (A + 1));
   ctx->d_dbg_astar = (int32_t*)dalloc(ctx, sizeof(int32_t) * 4);
-  if (!ctx->d_rows || !ctx->d_counts || !ctx->d_dxy || !ctx->d_queue || !ctx->d_pairctr || !ctx->d_dbg_vstar ||
+  if (!ctx->d_rows || !ctx->d_counts || !ctx->d_dxy || !ctx->d_queue || !ctx->d_pairctr || !ctx->d_prof || !ctx->d_dbg_vstar ||
       !ctx->d_dbg_v || !ctx->d_dbg_s || !ctx->d_dbg_conf || !ctx->d_dbg_astar) {
     fmdp_destroy(ctx);
     return FMDP_E_NOMEM;
@@ -810,7 +820,7 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
     w.height = ctx->d_height;
   }
   ctx->cap_states = a.max_steps + 2;
-  if (fmdp::walk_smem_bytes(w, ctx->C, threads_for(ctx), kChunk) > 227 * 1024) {
+  if (threads_for(ctx) > (ctx->C == 1 ? 512 : 384) || fmdp::walk_smem_bytes(w, ctx->C, threads_for(ctx), kChunk, 16) > 227 * 1024) {
     fmdp_destroy(ctx);
     return FMDP_E_ARG;
   }
@@ -841,15 +851,11 @@ fmdp_status fmdp_set_launch(fmdp_ctx* ctx, const fmdp_launch* l) {
   if (l) n = *l;
   if (n.cluster_size < 0 || n.cluster_size > 16 || (n.cluster_size & (n.cluster_size - 1)))
     return fail(ctx, FMDP_E_ARG, "cluster_size must be 0 or a power of two <= 16");
-  if (n.threads && (n.threads % 32 || n.threads > 512 || n.threads < ctx->A))
-    return fail(ctx, FMDP_E_ARG, "threads must be a multiple of 32 in [A, 512]");
-  if (n.threads) {
-    const int ncol = ctx->w.n_turn * ctx->w.W, group = (ncol + 31) & ~31;
-    if (n.threads % group) return fail(ctx, FMDP_E_ARG, "threads must be a multiple of the column group");
-  }
+  if (n.threads && n.threads != threads_for(ctx))
+    return fail(ctx, FMDP_E_ARG, "threads is derived from the action lattice; pass 0");
   ctx->launch = n;
   std::memset(ctx->mc_cache, 0, sizeof(ctx->mc_cache));
-  if (fmdp::walk_smem_bytes(ctx->w, ctx->C, threads_for(ctx), kChunk) > 227 * 1024)
+  if (fmdp::walk_smem_bytes(ctx->w, ctx->C, threads_for(ctx), kChunk, 1) > 227 * 1024)
     return fail(ctx, FMDP_E_ARG, "shared memory");
   return FMDP_OK;
 }

@@ -84,9 +84,10 @@ struct Ctl {
   int32_t psi;
   int32_t k;
   int32_t done;
+  int32_t fin;        // state k is terminal by terrain / goal / timeout (only its separation test remains)
+  int32_t fl;         // terrain (1) / goal (2) flags of state k
   int32_t namb;
   int32_t ntc;
-  int32_t a_star;
   int32_t n_near;
   int32_t n_exact;
   int32_t status;
@@ -97,19 +98,19 @@ struct Ctl {
   int32_t sl_lo[3], sl_n[3], sl_off[3];
 };
 
-// Row K's slice for this CTA: slots [lo, lo+n); the first CH of them are staged in the ring
-// buffer K % 3 starting at word offset `off`.
-__device__ __forceinline__ void issue_row(const World& w, int64_t K, unsigned rank, unsigned G, int CH,
+// Stage row K's slice for this CTA (slots [lo, lo+n) of n_row active slots): the first CH
+// plans go to ring buffer K % 3 with cp.async.bulk (TMA bulk copy), completion on its
+// mbarrier.  Called by one thread.
+__device__ __forceinline__ void issue_row(const World& w, int64_t K, int n_row, unsigned rank, unsigned G, int CH,
                                           int32_t* raw, int RAWW, uint64_t* bars, Ctl* ctl) {
   const int b = (int)(K % 3);
-  int n = (K >= 0 && K < w.horizon) ? __ldg(&w.counts[K]) : 0;
-  int lo = (int)(((int64_t)n * rank) / G), hi = (int)(((int64_t)n * (rank + 1)) / G);
-  int e = min(hi, lo + CH);
-  int lo4 = lo & ~3, e4 = (e + 3) & ~3;
+  const int lo = (int)(((int64_t)n_row * rank) / G), hi = (int)(((int64_t)n_row * (rank + 1)) / G);
+  const int e = min(hi, lo + CH);
+  const int lo4 = lo & ~3, e4 = (e + 3) & ~3;
   ctl->sl_lo[b] = lo;
   ctl->sl_n[b] = hi - lo;
   ctl->sl_off[b] = lo - lo4;
-  uint32_t bytes = (e > lo) ? (uint32_t)(e4 - lo4) * 4u : 0u;
+  const uint32_t bytes = (e > lo) ? (uint32_t)(e4 - lo4) * 4u : 0u;
   fence_proxy_async();
   mbar_arrive_tx(&bars[b], 4u * bytes);
   if (bytes) {
@@ -120,41 +121,51 @@ __device__ __forceinline__ void issue_row(const World& w, int64_t K, unsigned ra
   }
 }
 
-// Argmax with the lowest index on ties (Alg 9, R13), warp-wide.
-__device__ __forceinline__ void warp_argmax(double v, int i, double& bv, int& bi) {
-  bv = v;
-  bi = i;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-    int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (ov > bv || (ov == bv && oi < bi)) {
-      bv = ov;
-      bi = oi;
-    }
-  }
+__device__ __forceinline__ int row_count(const World& w, int64_t K) {
+  return (K >= 0 && K < w.horizon) ? __ldg(&w.counts[K]) : 0;
 }
 
+// Top-2 merge for the argmax (Alg 9): order by value, then lowest index (R13).
+__device__ __forceinline__ bool better(double v, int i, double bv, int bi) { return v > bv || (v == bv && i < bi); }
+
+// Terrain collision height under (x, y) (R16): INT_MIN outside the raster.
+__device__ __forceinline__ int ground_height(const World& w, int x, int y) {
+  if (w.nx <= 0) return INT_MIN;
+  const int64_t rx = (int64_t)x - w.x0, ry = (int64_t)y - w.y0;
+  if (rx < 0 || ry < 0) return INT_MIN;
+  const int64_t ix = rx / w.cell, iy = ry / w.cell;
+  if (ix >= w.nx || iy >= w.ny) return INT_MIN;
+  return __ldg(&w.height[iy * (int64_t)w.nx + ix]);
+}
+
+// Per-phase cycle accounting (rank 0, thread 0), enabled when args.prof != nullptr.
+enum Phase { PH_PROJ, PH_FIX, PH_WAIT, PH_HOT, PH_STAGE, PH_SCATTER, PH_BAR1, PH_OWNER, PH_BAR2, PH_DECIDE, PH_N };
+
 template <int C>
-__global__ void __launch_bounds__(512, 1) walk_kernel(const World w, const WalkArgs args, const int CH) {
+__global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
+    walk_kernel(const World w, const WalkArgs args, const int CH, const int NGW) {
   cg::cluster_group cluster = cg::this_cluster();
   const unsigned rank = cluster.block_rank();
   const unsigned G = cluster.num_blocks();
-  const int tid = threadIdx.x, NT = blockDim.x;
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int W = w.W, A = w.A, AW = A * W;
   const int NCOL = w.n_turn * W;
-  const int GROUP = (NCOL + 31) & ~31;
-  const int NG = NT / GROUP;
-  const int grp = tid / GROUP, col = tid % GROUP;
-  const int RS = NT / A;  // conflict threads per action
+  // hot-loop mapping: each warp = CPW columns x NGW plan groups; the lanes of one group
+  // (a multiple of 8) read the same well record -> shared-memory broadcast
+  const int CPW = 32 / NGW;
+  const int col = warp * CPW + (lane % CPW), grp = lane / CPW;
+  // actions owned by this CTA (reduce-scatter target and epilogue): a = rank + oa*G
+  const int n_own = (A > (int)rank) ? (A - (int)rank + (int)G - 1) / (int)G : 0;
 
   Layout L;
-  L.build(w.HL, CH, NT, C, NCOL, A, AW);
+  L.build(w.HL, CH, NT, C, NCOL, A, AW, (int)G);
   extern __shared__ __align__(16) unsigned char smem[];
   int2* s_dxy = reinterpret_cast<int2*>(smem + L.o_dxy);
+  int4* s_tw = reinterpret_cast<int4*>(smem + L.o_tw);
   int32_t* s_raw = reinterpret_cast<int32_t*>(smem + L.o_raw);
   float* s_cen = reinterpret_cast<float*>(smem + L.o_cen);
-  uint32_t* s_red = reinterpret_cast<uint32_t*>(smem + L.o_red);
+  float* s_stage = reinterpret_cast<float*>(smem + L.o_stage);
+  float* s_recv = reinterpret_cast<float*>(smem + L.o_recv);
   int4* s_pos = reinterpret_cast<int4*>(smem + L.o_pos);
   double* s_fix = reinterpret_cast<double*>(smem + L.o_fix);
   double* s_sfix = reinterpret_cast<double*>(smem + L.o_sfix);
@@ -163,15 +174,30 @@ __global__ void __launch_bounds__(512, 1) walk_kernel(const World w, const WalkA
   double* s_vstar = reinterpret_cast<double*>(smem + L.o_vstar);
   double* s_vsc = reinterpret_cast<double*>(smem + L.o_vsc);
   uint32_t* s_conf = reinterpret_cast<uint32_t*>(smem + L.o_conf);
-  uint32_t* s_confg = reinterpret_cast<uint32_t*>(smem + L.o_confg);
+  int32_t* s_flags = reinterpret_cast<int32_t*>(smem + L.o_flags);
+  uint32_t* s_stay = reinterpret_cast<uint32_t*>(smem + L.o_stay);
   int32_t* s_amb = reinterpret_cast<int32_t*>(smem + L.o_amb);
   int32_t* s_tc = reinterpret_cast<int32_t*>(smem + L.o_tc);
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + L.o_bar);
   Ctl* ctl = reinterpret_cast<Ctl*>(smem + L.o_ctl);
-  const int RED = L.RED, RAWW = L.RAWW;
-  const int NHOT = NCOL * C * NTAU;
+  const int RAWW = L.RAWW, BLK = L.BLK, NOWN = L.NOWN;
+  const int4* tw = (w.n_tw <= TW_SMEM) ? s_tw : w.tw;
+
+  const bool prof = args.prof != nullptr && rank == 0 && tid == 0;
+  unsigned long long pacc[PH_N];
+#pragma unroll
+  for (int i = 0; i < PH_N; ++i) pacc[i] = 0;
+  long long tmark = 0;
+#define FMDP_MARK(ph)                               \
+  if (prof) {                                       \
+    const long long now_ = clock64();               \
+    pacc[ph] += (unsigned long long)(now_ - tmark); \
+    tmark = now_;                                   \
+  }
 
   for (int i = tid; i < w.HL; i += NT) s_dxy[i] = w.dxy[i];
+  if (w.n_tw <= TW_SMEM)
+    for (int i = tid; i < w.n_tw; i += NT) s_tw[i] = w.tw[i];
   if (tid == 0) {
     for (int b = 0; b < 3; ++b) mbar_init(&s_bar[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -179,6 +205,7 @@ __global__ void __launch_bounds__(512, 1) walk_kernel(const World w, const WalkA
   __syncthreads();
   uint32_t par = 0;      // next wait parity per ring buffer (bit b)
   uint32_t pending = 0;  // ring buffers issued and not yet waited
+  int cnt2 = 0;          // (tid 0) active count of row K+2, loaded one step ahead
 
   for (;;) {
     // ------------------------------------------------------------ next request
@@ -192,17 +219,27 @@ __global__ void __launch_bounds__(512, 1) walk_kernel(const World w, const WalkA
     const Req rq = args.reqs[r];
     const size_t sbase = (size_t)rq.slot * args.cap;
     if (tid == 0) {
-      int k0 = rq.start_k;
+      const int k0 = rq.start_k;
+      int q0[3], p0;
       if (k0 == 0) {
-        ctl->q[0] = rq.src[0]; ctl->q[1] = rq.src[1]; ctl->q[2] = rq.src[2];
-        ctl->psi = rq.psi0;
+        q0[0] = rq.src[0]; q0[1] = rq.src[1]; q0[2] = rq.src[2];
+        p0 = rq.psi0;
       } else {
         const int32_t* tq = args.traj + 3 * (sbase + k0);
-        ctl->q[0] = tq[0]; ctl->q[1] = tq[1]; ctl->q[2] = tq[2];
-        ctl->psi = args.heading[sbase + k0];
+        q0[0] = tq[0]; q0[1] = tq[1]; q0[2] = tq[2];
+        p0 = args.heading[sbase + k0];
       }
+      ctl->q[0] = q0[0]; ctl->q[1] = q0[1]; ctl->q[2] = q0[2];
+      ctl->psi = p0;
       ctl->k = k0;
       ctl->done = 0;
+      // terminal flags of the starting state (terrain, goal; timeout cannot apply: k0 < max_steps)
+      {
+        const int h = ground_height(w, q0[0], q0[1]);
+        const int64_t gx = (int64_t)q0[0] - rq.dst[0], gy = (int64_t)q0[1] - rq.dst[1], gz = (int64_t)q0[2] - rq.dst[2];
+        ctl->fl = ((q0[2] < 0 || q0[2] < h) ? 1 : 0) | ((gx * gx + gy * gy + gz * gz < w.cap2) ? 2 : 0);
+        ctl->fin = (!args.eval && ctl->fl) ? 1 : 0;
+      }
       ctl->n_near = 0;
       ctl->n_exact = 0;
       ctl->status = 0;
@@ -212,8 +249,10 @@ __global__ void __launch_bounds__(512, 1) walk_kernel(const World w, const WalkA
       if (rank == 0 && k0 > 0 && !args.eval) {  // resume: aggregates of the kept prefix
         int nn = 0;
         uint32_t ms = w.sat_d2;
-        for (int kk = 0; kk < k0; ++kk) nn += args.ntie[sbase + kk];
-        for (int kk = 0; kk <= k0; ++kk) ms = min(ms, args.stepd2[sbase + kk]);
+        for (int kk = 0; kk < k0; ++kk) {
+          nn += args.ntie[sbase + kk];
+          ms = min(ms, args.stepd2[sbase + kk]);
+        }
         ctl->n_near = nn;
         ctl->min_sep = ms;
       }
@@ -222,57 +261,61 @@ __global__ void __launch_bounds__(512, 1) walk_kernel(const World w, const WalkA
         tq[0] = rq.src[0]; tq[1] = rq.src[1]; tq[2] = rq.src[2];
         args.heading[sbase] = rq.psi0;
       }
+      const int64_t K0 = rq.t0 + k0;
+      const int n0 = row_count(w, K0), n1 = row_count(w, K0 + 1);
+      cnt2 = row_count(w, K0 + 2);
+      issue_row(w, K0, n0, rank, G, CH, s_raw, RAWW, s_bar, ctl);
+      issue_row(w, K0 + 1, n1, rank, G, CH, s_raw, RAWW, s_bar, ctl);
+      s_stay[0] = w.sat_d2;
+      s_stay[1] = w.sat_d2;
     }
-    if (rank == 0)
-      for (int i = tid; i < 3 * RED; i += NT) s_red[i] = 0xffffffffu;
-    __syncthreads();
     {
-      const int64_t K0 = rq.t0 + ctl->k;
-      if (tid == 0) {
-        issue_row(w, K0, rank, G, CH, s_raw, RAWW, s_bar, ctl);
-        issue_row(w, K0 + 1, rank, G, CH, s_raw, RAWW, s_bar, ctl);
-      }
+      const int64_t K0 = rq.t0 + rq.start_k;
       pending |= (1u << (K0 % 3)) | (1u << ((K0 + 1) % 3));
     }
     cluster.sync();
 
     // ------------------------------------------------------------ step loop
     for (;;) {
+      if (prof) tmark = clock64();
       const int k = ctl->k;
       const int64_t K = rq.t0 + k;
       const int qx = ctl->q[0], qy = ctl->q[1], qz = ctl->q[2], psi = ctl->psi;
-      const int bK = (int)(K % 3), bK1 = (int)((K + 1) % 3), bK2 = (int)((K + 2) % 3);
-      if (rank == 0)  // reset the reduction buffer of step k+1 (last read in step k-2)
-        for (int i = tid; i < RED; i += NT) s_red[((k + 1) % 3) * RED + i] = 0xffffffffu;
-      if (!args.eval && tid == 0) issue_row(w, K + 2, rank, G, CH, s_raw, RAWW, s_bar, ctl);
-      if (!args.eval) pending |= 1u << bK2;
+      const bool fin = ctl->fin != 0;  // only the separation test of state k remains
+      const int bK = (int)(K % 3), bK2 = (int)((K + 2) % 3);
       if (tid == 0) {
+        if (!args.eval && !fin) {
+          issue_row(w, K + 2, cnt2, rank, G, CH, s_raw, RAWW, s_bar, ctl);
+          cnt2 = row_count(w, K + 3);  // consumed next step: latency hidden by this step
+        }
         ctl->namb = 0;
         ctl->ntc = 0;
+        s_stay[(k + 1) & 1] = w.sat_d2;  // written remotely in step k+1 (after both barriers of k)
       }
-      for (int a = tid; a <= A; a += NT) s_conf[a] = w.sat_d2;
+      if (!args.eval && !fin) pending |= 1u << bK2;
       __syncthreads();
 
-      // ---- a5 candidates: terrain wells that can reach any projected state (exact cull)
-      for (int i = tid; i < w.n_tw; i += NT) {
-        int4 t = __ldg(&w.tw[i]);
-        int64_t dx = t.x - qx, dy = t.y - qy, dz = t.z - qz;
-        int64_t rr = (int64_t)t.w + w.reach_u;
-        if (dx * dx + dy * dy + dz * dz < rr * rr) {
-          int slot = atomicAdd(&ctl->ntc, 1);
-          if (slot < TC_MAX) s_tc[slot] = i;
-        }
-      }
-      // ---- a2 forward projection: thread (grp, col) -> column (turn it, substep t)
       float sx = 0.f, sy = 0.f, sz[C];
-      {
+      int hgt = INT_MIN, x1 = 0, y1 = 0;  // ground under Delta_1 (t = 1 columns, group 0)
+      if (!fin) {
+        // ---- a5 candidates: terrain wells that can reach any projected state (exact cull)
+        for (int i = tid; i < w.n_tw; i += NT) {
+          const int4 t = tw[i];
+          const int64_t dx = t.x - qx, dy = t.y - qy, dz = t.z - qz;
+          const int64_t rr = (int64_t)t.w + w.reach_u;
+          if (dx * dx + dy * dy + dz * dz < rr * rr) {
+            const int slot = atomicAdd(&ctl->ntc, 1);
+            if (slot < TC_MAX) s_tc[slot] = i;
+          }
+        }
+        // ---- a2 forward projection (Alg 3): column (turn it, substep t) on the integer lattice
         const int it = min(col / W, w.n_turn - 1), t = col % W + 1;
         const int h = w.turn[it];
         int x = qx, y = qy, ps = psi;
         for (int s = 1; s <= t; ++s) {
           ps += h;
-          ps = (ps % w.HL + w.HL) % w.HL;
-          int2 d = s_dxy[ps];
+          ps = ps >= w.HL ? ps - w.HL : (ps < 0 ? ps + w.HL : ps);
+          const int2 d = s_dxy[ps];
           x += d.x;
           y += d.y;
         }
@@ -282,43 +325,39 @@ __global__ void __launch_bounds__(512, 1) walk_kernel(const World w, const WalkA
         for (int c = 0; c < C; ++c) sz[c] = (float)(w.climb[c] * t);
         if (grp == 0 && col < NCOL) {
 #pragma unroll
-          for (int c = 0; c < C; ++c) {
-            const int a = it * C + c;
-            s_pos[a * W + (t - 1)] = make_int4(x, y, qz + w.climb[c] * t, ps);
+          for (int c = 0; c < C; ++c) s_pos[(it * C + c) * W + (t - 1)] = make_int4(x, y, qz + w.climb[c] * t, ps);
+          if (t == 1) {  // raster load issued now, consumed after the hot loop
+            hgt = ground_height(w, x, y);
+            x1 = x;
+            y1 = y;
           }
         }
-      }
-      __syncthreads();
-      const int ntc = ctl->ntc;
-
-      // ---- a3 goal (fp64), deck, a5 terrain (exact predicate, FP32 ex2 value)
-      for (int st = tid; st < AW; st += NT) {
-        const int4 p = s_pos[st];
-        const int64_t gx = (int64_t)p.x - rq.dst[0], gy = (int64_t)p.y - rq.dst[1], gz = (int64_t)p.z - rq.dst[2];
-        const double vpos = w.goal_r * exp2(w.goal_l2g * sqrt((double)(gx * gx + gy * gy + gz * gz)));
-        const double valt = (p.z < w.zdeck_u) ? (w.deck_scale - w.u_m * (double)p.z) : 0.0;
-        int64_t mT = INT64_MAX;
-        if (ntc <= TC_MAX) {
-          for (int c = 0; c < ntc; ++c) {
-            int4 t = __ldg(&w.tw[s_tc[c]]);
-            int64_t dx = p.x - t.x, dy = p.y - t.y, dz = p.z - t.z;
-            int64_t d2 = dx * dx + dy * dy + dz * dz;
-            if (d2 < (int64_t)t.w * t.w && d2 < mT) mT = d2;
+        __syncthreads();
+        FMDP_MARK(PH_PROJ)
+        // ---- a3 goal (fp64), deck, a5 terrain (exact predicate, FP32 ex2 value): owned states
+        const int ntc = ctl->ntc;
+        for (int i = tid; i < n_own * W; i += NT) {
+          const int st = ((int)rank + (i / W) * (int)G) * W + i % W;
+          const int4 p = s_pos[st];
+          const int64_t gx = (int64_t)p.x - rq.dst[0], gy = (int64_t)p.y - rq.dst[1], gz = (int64_t)p.z - rq.dst[2];
+          const double vpos = w.goal_r * exp2(w.goal_l2g * sqrt((double)(gx * gx + gy * gy + gz * gz)));
+          const double valt = (p.z < w.zdeck_u) ? (w.deck_scale - w.u_m * (double)p.z) : 0.0;
+          int64_t mT = INT64_MAX;
+          const int nt = ntc <= TC_MAX ? ntc : w.n_tw;
+          for (int c = 0; c < nt; ++c) {
+            const int4 t4 = tw[ntc <= TC_MAX ? s_tc[c] : c];
+            const int64_t dx = p.x - t4.x, dy = p.y - t4.y, dz = p.z - t4.z;
+            const int64_t d2 = dx * dx + dy * dy + dz * dz;
+            if (d2 < (int64_t)t4.w * t4.w && d2 < mT) mT = d2;
           }
-        } else {
-          for (int c = 0; c < w.n_tw; ++c) {
-            int4 t = __ldg(&w.tw[c]);
-            int64_t dx = p.x - t.x, dy = p.y - t.y, dz = p.z - t.z;
-            int64_t d2 = dx * dx + dy * dy + dz * dz;
-            if (d2 < (int64_t)t.w * t.w && d2 < mT) mT = d2;
-          }
+          s_vT[st] = (mT != INT64_MAX) ? w.terr_r * ex2_approx(w.terr_l2g * sqrtf((float)mT)) : 0.f;
+          s_fix[st] = vpos - valt;
+          s_sfix[st] = vpos + valt;
         }
-        s_vT[st] = (mT != INT64_MAX) ? w.terr_r * ex2_approx(w.terr_l2g * sqrtf((float)mT)) : 0.f;
-        s_fix[st] = vpos - valt;
-        s_sfix[st] = vpos + valt;
+        FMDP_MARK(PH_FIX)
       }
 
-      // ---- a1 + a4: wells of row K, hot loop
+      // ---- a1 + a4: stage row K, wells, hot loop; exact nearest-plan distance of q ("stay")
       float m[C][NTAU];
 #pragma unroll
       for (int c = 0; c < C; ++c)
@@ -329,6 +368,7 @@ __global__ void __launch_bounds__(512, 1) walk_kernel(const World w, const WalkA
         par ^= 1u << bK;
         pending &= ~(1u << bK);
       }
+      FMDP_MARK(PH_WAIT)
       uint32_t stay = w.sat_d2;
       {
         const int lo = ctl->sl_lo[bK], n = ctl->sl_n[bK];
@@ -344,9 +384,10 @@ __global__ void __launch_bounds__(512, 1) walk_kernel(const World w, const WalkA
           }
           for (int j = tid; j < nc; j += NT) {
             const int rx = X[j] - qx, ry = Y[j] - qy, rz = Z[j] - qz;
+            stay = min(stay, clamp_d2(rx, ry, rz, w.R_max, w.sat_d2));
+            if (fin) continue;
             const uint32_t pv = (uint32_t)V[j];
             const int vx = sext(pv, 11), vy = sext(pv >> 11, 11), vz = sext(pv >> 22, 10);
-            stay = min(stay, clamp_d2(rx, ry, rz, w.R_max, w.sat_d2));
             float4* c4 = reinterpret_cast<float4*>(s_cen + 16 * j);
             float cc[16];
 #pragma unroll
@@ -361,19 +402,20 @@ __global__ void __launch_bounds__(512, 1) walk_kernel(const World w, const WalkA
             c4[2] = make_float4(cc[8], cc[9], cc[10], cc[11]);
             c4[3] = make_float4(cc[12], cc[13], cc[14], cc[15]);
           }
+          if (fin) continue;
           __syncthreads();
           const float4* cen4 = reinterpret_cast<const float4*>(s_cen);
-#define FMDP_WELL(T, CX, CY, CZ)                          \
-  {                                                       \
-    const float dx = sx - (CX), dy = sy - (CY);           \
-    const float hh = fmaf(dy, dy, dx * dx);               \
-    _Pragma("unroll") for (int cc_ = 0; cc_ < C; ++cc_) { \
-      const float dz = sz[cc_] - (CZ);                    \
-      m[cc_][T] = fminf(m[cc_][T], fmaf(dz, dz, hh));     \
-    }                                                     \
+#define FMDP_WELL(T, CX, CY, CZ)                            \
+  {                                                         \
+    const float dx = sx - (CX), dy = sy - (CY);             \
+    const float hh = fmaf(dy, dy, dx * dx);                 \
+    _Pragma("unroll") for (int cc_ = 0; cc_ < C; ++cc_) {   \
+      const float dz = sz[cc_] - (CZ);                      \
+      m[cc_][T] = fminf(m[cc_][T], fmaf(dz, dz, hh));       \
+    }                                                       \
   }
 #pragma unroll 2
-          for (int j = grp; j < nc; j += NG) {
+          for (int j = grp; j < nc; j += NGW) {
             const float4 e0 = cen4[4 * j + 0], e1 = cen4[4 * j + 1], e2 = cen4[4 * j + 2], e3 = cen4[4 * j + 3];
             FMDP_WELL(0, e0.x, e0.y, e0.z)
             FMDP_WELL(1, e0.w, e1.x, e1.y)
@@ -384,197 +426,224 @@ __global__ void __launch_bounds__(512, 1) walk_kernel(const World w, const WalkA
 #undef FMDP_WELL
           __syncthreads();
         }
-        if (tid == 0 && args.pairs) atomicAdd(args.pairs, (unsigned long long)n * NTAU * AW);
+        if (!fin && tid == 0 && args.pairs) atomicAdd(args.pairs, (unsigned long long)n * NTAU * AW);
       }
-      if (stay < w.sat_d2) atomicMin(&s_conf[A], stay);
+      // stay: slice minimum of |q - p(K)|^2 -> every CTA (terminal separation test, Sec IV.I)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) stay = min(stay, __shfl_xor_sync(0xffffffffu, stay, o));
+      if (lane == 0 && stay < w.sat_d2)
+        for (unsigned b = 0; b < G; ++b) atomicMin(cluster.map_shared_rank(&s_stay[k & 1], b), stay);
+      FMDP_MARK(PH_HOT)
 
-      // ---- a8 fused separation check: Delta_1(a) vs this CTA's slice of row K+1
-      if (pending & (1u << bK1)) {
-        mbar_wait(&s_bar[bK1], (par >> bK1) & 1u);
-        par ^= 1u << bK1;
-        pending &= ~(1u << bK1);
-      }
-      {
-        const int lo = ctl->sl_lo[bK1], n = ctl->sl_n[bK1];
-        const int a = tid / RS, rr = tid % RS;
-        if (a < A) {
-          const int4 p1 = s_pos[a * W + 0];
-          const int ax = p1.x - qx, ay = p1.y - qy, az = p1.z - qz;
-          uint32_t cm = w.sat_d2;
-          const int32_t* b = s_raw + (size_t)bK1 * 4 * RAWW + ctl->sl_off[bK1];
-          const int32_t* rowg = w.rows + (size_t)(K + 1) * 4 * w.row_cap + lo;
-          for (int j = rr; j < n; j += RS) {
-            int px, py, pz;
-            if (j < CH) {
-              px = b[j]; py = b[RAWW + j]; pz = b[2 * RAWW + j];
-            } else {
-              px = rowg[j]; py = rowg[w.row_cap + j]; pz = rowg[2 * w.row_cap + j];
-            }
-            cm = min(cm, clamp_d2(px - qx - ax, py - qy - ay, pz - qz - az, w.R_max, w.sat_d2));
+      if (!fin) {
+        // terrain / goal flags of every action's Delta_1 (the candidate next state)
+        if (grp == 0 && col < NCOL && col % W == 0) {
+          const int it = col / W;
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            const int z = qz + w.climb[c];
+            const int64_t gx = (int64_t)x1 - rq.dst[0], gy = (int64_t)y1 - rq.dst[1], gz = (int64_t)z - rq.dst[2];
+            s_flags[it * C + c] = ((z < 0 || z < hgt) ? 1 : 0) | ((gx * gx + gy * gy + gz * gz < w.cap2) ? 2 : 0);
           }
-          if (cm < w.sat_d2) atomicMin(&s_conf[a], cm);
         }
-      }
-
-      // ---- cross-CTA reduction into CTA 0 (distributed shared memory)
-      float* s_part = s_cen;  // reuse: [grp][col][c][tau]
+        // group minimum inside the warp, then per-action blocks [t][tau] in s_stage
 #pragma unroll
-      for (int c = 0; c < C; ++c)
+        for (int c = 0; c < C; ++c)
 #pragma unroll
-        for (int t = 0; t < NTAU; ++t) s_part[((size_t)(grp * GROUP + col) * C + c) * NTAU + t] = m[c][t];
-      __syncthreads();
-      {
-        uint32_t* red = cluster.map_shared_rank(s_red + (k % 3) * RED, 0);
-        for (int i = tid; i < NHOT; i += NT) {
-          const int cl = i / (C * NTAU), rem = i % (C * NTAU);
-          float mm = s_part[(size_t)cl * C * NTAU + rem];
-          for (int g2 = 1; g2 < NG; ++g2) mm = fminf(mm, s_part[((size_t)(g2 * GROUP + cl)) * C * NTAU + rem]);
-          atomicMin(&red[i], __float_as_uint(mm));
+          for (int t = 0; t < NTAU; ++t)
+            for (int o = CPW; o < 32; o <<= 1) m[c][t] = fminf(m[c][t], __shfl_xor_sync(0xffffffffu, m[c][t], o));
+        if (grp == 0 && col < NCOL) {
+          const int it = col / W, t1 = col % W;
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+#pragma unroll
+            for (int t = 0; t < NTAU; ++t) s_stage[(it * C + c) * BLK + t1 * NTAU + t] = m[c][t];
         }
-        for (int a = tid; a <= A; a += NT) atomicMin(&red[NHOT + a], s_conf[a]);
+        FMDP_MARK(PH_STAGE)
+        __syncthreads();
+        // reduce-scatter: float4 DSMEM stores of each action block into slot [rank] of its owner
+        {
+          const int par_off = (k & 1) * (int)G * NOWN * BLK;
+          const int nv = BLK / 4;
+          for (int i = tid; i < A * nv; i += NT) {
+            const int a = i / nv, e = i % nv;
+            float4* dst = reinterpret_cast<float4*>(cluster.map_shared_rank(s_recv, a % (int)G) + par_off +
+                                                    ((int)rank * NOWN + a / (int)G) * BLK);
+            dst[e] = reinterpret_cast<const float4*>(s_stage + a * BLK)[e];
+          }
+        }
+        FMDP_MARK(PH_SCATTER)
       }
       cluster.sync();
+      FMDP_MARK(PH_BAR1)
 
-      // ---- epilogue (every CTA, identical inputs -> identical decisions)
-      const uint32_t* redg = cluster.map_shared_rank(s_red + (k % 3) * RED, 0);
-      for (int a = tid; a <= A; a += NT) s_confg[a] = redg[NHOT + a];
-      for (int st = tid; st < AW; st += NT) {
-        const int a = st / W, t1 = st % W, it = a / C, c = a % C;
-        const int base = ((it * W + t1) * C + c) * NTAU;
-        float mi = FLT_MAX;
+      if (!fin) {
+        // ---- owner epilogue (half-warp per owned action, lane = substep): reduce the G
+        //      partial blocks, exact in/out, values (Alg 8), V*(a)
+        const float* rcv = s_recv + (k & 1) * (int)G * NOWN * BLK;
+        const int hw = tid >> 4, hl = tid & 15;
+        const int n_hw = NT >> 4;
+        for (int oa0 = 0; oa0 < NOWN; oa0 += n_hw) {  // uniform trip count across the CTA
+          const int oa = oa0 + hw;
+          const bool act = oa < n_own && hl < W;
+          const int a = (int)rank + oa * (int)G;
+          const int st = a * W + hl;
+          float mi = FLT_MAX;
+          int amb = 0;
+          if (act) {
 #pragma unroll
-        for (int t = 0; t < NTAU; ++t) {
-          const float M = __uint_as_float(redg[base + t]);
-          if (M < w.R2lo[t]) {
-            mi = fminf(mi, M);
-          } else if (M <= w.R2hi[t]) {  // inside the 2^-20 band: decide exactly below
-            const int idx = atomicAdd(&ctl->namb, 1);
-            if (idx < AMB_MAX) s_amb[idx] = st * NTAU + t;
+            for (int t = 0; t < NTAU; ++t) {
+              float M = FLT_MAX;
+              for (int b = 0; b < (int)G; ++b) M = fminf(M, rcv[(b * NOWN + oa) * BLK + hl * NTAU + t]);
+              if (M < w.R2lo[t]) {
+                mi = fminf(mi, M);
+              } else if (M <= w.R2hi[t]) {  // inside the 2^-20 band: decided exactly below
+                amb = 1;
+                const int idx = atomicAdd(&ctl->namb, 1);
+                if (idx < AMB_MAX) s_amb[idx] = st * NTAU + t;
+              }
+            }
+            s_mI[st] = mi;
+          }
+          if (__syncthreads_or(amb)) {
+            // Exact fallback: min over the WHOLE row K of the int64 d^2 for each flagged
+            // (state, tau); each CTA resolves its own states (rare).
+            const int namb = ctl->namb;
+            const int nK = row_count(w, K);
+            const int32_t* rowg = w.rows + (size_t)K * 4 * w.row_cap;
+            const int nitems = namb <= AMB_MAX ? namb : n_hw * W * NTAU;
+            for (int it2 = 0; it2 < nitems; ++it2) {
+              int item;
+              if (namb <= AMB_MAX) {
+                item = s_amb[it2];
+              } else {  // overflow: walk every owned (state, tau) of this pass, re-test the band
+                const int oa2 = oa0 + it2 / (W * NTAU), rem = it2 % (W * NTAU), l2 = rem / NTAU, t = rem % NTAU;
+                if (oa2 >= n_own) continue;
+                float M = FLT_MAX;
+                for (int b = 0; b < (int)G; ++b) M = fminf(M, rcv[(b * NOWN + oa2) * BLK + l2 * NTAU + t]);
+                if (!(M >= w.R2lo[t] && M <= w.R2hi[t])) continue;
+                item = (((int)rank + oa2 * (int)G) * W + l2) * NTAU + t;
+              }
+              const int sti = item / NTAU, t = item % NTAU;
+              if (tid == 0) ctl->xmin = ULLONG_MAX;
+              __syncthreads();
+              const int4 p = s_pos[sti];
+              unsigned long long best = ULLONG_MAX;
+              for (int j = tid; j < nK; j += NT) {
+                const uint32_t pv = (uint32_t)rowg[3 * w.row_cap + j];
+                const int64_t cx = rowg[j] + (int64_t)w.k_tau[t] * sext(pv, 11);
+                const int64_t cy = rowg[w.row_cap + j] + (int64_t)w.k_tau[t] * sext(pv >> 11, 11);
+                const int64_t cz = rowg[2 * w.row_cap + j] + (int64_t)w.k_tau[t] * sext(pv >> 22, 10);
+                const int64_t dx = p.x - cx, dy = p.y - cy, dz = p.z - cz;
+                best = min(best, (unsigned long long)(dx * dx + dy * dy + dz * dz));
+              }
+              for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+              if (lane == 0 && best != ULLONG_MAX) atomicMin(&ctl->xmin, best);
+              __syncthreads();
+              if (tid == 0) {
+                const unsigned long long x = ctl->xmin;
+                if ((int64_t)x < w.R2_tau[t]) s_mI[sti] = fminf(s_mI[sti], (float)x);
+                atomicAdd(&ctl->n_exact, 1);
+              }
+              __syncthreads();
+            }
+            if (tid == 0) ctl->namb = 0;
+            if (act) mi = s_mI[st];
+            __syncthreads();
+          }
+          // a6 values
+          double v = -INFINITY, sc = 0.0;
+          if (act) {
+            const float vI = (mi < FLT_MAX) ? w.intr_r * ex2_approx(w.intr_l2g * sqrtf(mi)) : 0.f;
+            const double neg = (double)fmaxf(vI, s_vT[st]);
+            v = s_fix[st] - neg;
+            sc = s_sfix[st] + neg;
+            if (args.eval) {
+              args.dbg_v[st] = v;
+              args.dbg_s[st] = sc;
+            }
+          }
+          // V*(a) = max(init, max_t V), term scale at the first maximising t: half-warp shuffles
+          double bv = v, bs = sc;
+          int bt = act ? hl : 99;
+#pragma unroll
+          for (int o = 8; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o, 16);
+            const double os = __shfl_xor_sync(0xffffffffu, bs, o, 16);
+            const int ot = __shfl_xor_sync(0xffffffffu, bt, o, 16);
+            if (ov > bv || (ov == bv && ot < bt)) {
+              bv = ov;
+              bs = os;
+              bt = ot;
+            }
+          }
+          if (oa < n_own && hl < (int)G) {  // broadcast V*(a) and S(a) to CTA hl
+            const double vstar = w.vmax_init_zero ? fmax(0.0, bv) : bv;
+            cluster.map_shared_rank(s_vstar, hl)[a] = vstar;
+            cluster.map_shared_rank(s_vsc, hl)[a] = bs;
+            if (args.eval && hl == 0) args.dbg_vstar[a] = vstar;
           }
         }
-        s_mI[st] = mi;
+        if (tid == 0 && ctl->n_exact && rank != 0) {
+          atomicAdd(&cluster.map_shared_rank(ctl, 0)->n_exact, ctl->n_exact);
+          ctl->n_exact = 0;
+        }
+        FMDP_MARK(PH_OWNER)
+        cluster.sync();
+        FMDP_MARK(PH_BAR2)
       }
-      __syncthreads();
-      const int namb = ctl->namb;
-      if (namb > 0) {
-        // Exact fallback: min over the WHOLE row K of the int64 d^2 for (state, tau); rare.
-        const int nK = (K < w.horizon) ? __ldg(&w.counts[K]) : 0;
-        const int32_t* rowg = w.rows + (size_t)K * 4 * w.row_cap;
-        const int nitems = namb <= AMB_MAX ? namb : AW * NTAU;
-        for (int it2 = 0; it2 < nitems; ++it2) {
-          const int item = namb <= AMB_MAX ? s_amb[it2] : it2;
-          const int st = item / NTAU, t = item % NTAU;
-          if (namb > AMB_MAX) {  // overflow: re-test this item's filter verdict
-            const int a = st / W, t1 = st % W, it = a / C, c = a % C;
-            const float M = __uint_as_float(redg[((it * W + t1) * C + c) * NTAU + t]);
-            if (!(M >= w.R2lo[t] && M <= w.R2hi[t])) continue;
+
+      // ---- a7/a8 (every CTA, identical inputs -> identical decisions)
+      if (warp == 0) {
+        double v1 = -INFINITY, v2 = -INFINITY;  // a7: top-2 (lowest index on ties)
+        int a1 = INT_MAX, a2 = INT_MAX;
+        if (!fin) {
+          for (int a = lane; a < A; a += 32) {
+            const double v = s_vstar[a];
+            if (better(v, a, v1, a1)) {
+              v2 = v1; a2 = a1; v1 = v; a1 = a;
+            } else if (better(v, a, v2, a2)) {
+              v2 = v; a2 = a;
+            }
           }
-          if (tid == 0) ctl->xmin = ULLONG_MAX;
-          __syncthreads();
-          const int4 p = s_pos[st];
-          unsigned long long best = ULLONG_MAX;
-          for (int j = tid; j < nK; j += NT) {
-            const uint32_t pv = (uint32_t)rowg[3 * w.row_cap + j];
-            const int64_t cx = rowg[j] + (int64_t)w.k_tau[t] * sext(pv, 11);
-            const int64_t cy = rowg[w.row_cap + j] + (int64_t)w.k_tau[t] * sext(pv >> 11, 11);
-            const int64_t cz = rowg[2 * w.row_cap + j] + (int64_t)w.k_tau[t] * sext(pv >> 22, 10);
-            const int64_t dx = p.x - cx, dy = p.y - cy, dz = p.z - cz;
-            best = min(best, (unsigned long long)(dx * dx + dy * dy + dz * dz));
-          }
-          if (best != ULLONG_MAX) atomicMin(&ctl->xmin, best);
-          __syncthreads();
-          if (tid == 0) {
-            const unsigned long long x = ctl->xmin;
-            if ((int64_t)x < w.R2_tau[t]) s_mI[st] = fminf(s_mI[st], (float)x);
-            ctl->n_exact += 1;
-          }
-          __syncthreads();
-        }
-      }
-      // a6: V = V+ - max(V^T, V^I) - V_alt (Alg 8), term scale S
-      for (int st = tid; st < AW; st += NT) {
-        const float mi = s_mI[st];
-        const float vI = (mi < FLT_MAX) ? w.intr_r * ex2_approx(w.intr_l2g * sqrtf(mi)) : 0.f;
-        const double neg = (double)fmaxf(vI, s_vT[st]);
-        const double fx = s_fix[st], sf = s_sfix[st];
-        s_fix[st] = fx - neg;
-        s_sfix[st] = sf + neg;
-      }
-      __syncthreads();
-      for (int a = tid; a < A; a += NT) {  // V*(a) = max(init, max_t V(a,t))
-        double vmax = w.vmax_init_zero ? 0.0 : -INFINITY, bt = -INFINITY, bs = 0.0;
-        for (int t = 0; t < W; ++t) {
-          const double v = s_fix[a * W + t];
-          if (v > vmax) vmax = v;
-          if (v > bt) {
-            bt = v;
-            bs = s_sfix[a * W + t];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const double ov1 = __shfl_xor_sync(0xffffffffu, v1, o), ov2 = __shfl_xor_sync(0xffffffffu, v2, o);
+            const int oa1 = __shfl_xor_sync(0xffffffffu, a1, o), oa2 = __shfl_xor_sync(0xffffffffu, a2, o);
+            if (better(ov1, oa1, v1, a1)) {
+              if (better(v1, a1, ov2, oa2)) { v2 = v1; a2 = a1; } else { v2 = ov2; a2 = oa2; }
+              v1 = ov1; a1 = oa1;
+            } else if (better(ov1, oa1, v2, a2)) {
+              v2 = ov1; a2 = oa1;
+            }
           }
         }
-        s_vstar[a] = vmax;
-        s_vsc[a] = bs;
-      }
-      __syncthreads();
-      if (tid < 32) {  // a7: argmax (lowest index on ties) and runner-up
-        double bv = -INFINITY;
-        int bi = INT_MAX;
-        for (int a = tid; a < A; a += 32) {
-          const double v = s_vstar[a];
-          if (v > bv || (v == bv && a < bi)) { bv = v; bi = a; }
-        }
-        double v1;
-        int a1;
-        warp_argmax(bv, bi, v1, a1);
-        double cv = -INFINITY;
-        int ci = INT_MAX;
-        for (int a = tid; a < A; a += 32) {
-          if (a == a1) continue;
-          const double v = s_vstar[a];
-          if (v > cv || (v == cv && a < ci)) { cv = v; ci = a; }
-        }
-        double v2;
-        int a2;
-        warp_argmax(cv, ci, v2, a2);
-        if (tid == 0) {
-          const bool near = (A > 1) && (v1 - v2 < w.near_tie_rel * s_vsc[a1]);
+        if (lane == 0) {
+          const uint32_t c0 = s_stay[k & 1];
           if (args.eval) {
             if (rank == 0) {
-              for (int a = 0; a < A; ++a) args.dbg_vstar[a] = s_vstar[a];
-              for (int a = 0; a <= A; ++a) args.dbg_conf[a] = s_confg[a];
+              args.dbg_conf[A] = c0;
               args.dbg_astar[0] = a1;
             }
             ctl->done = 1;
           } else {
-            const size_t sb = sbase;
-            bool decided = false;
-            if (k == 0) {  // departure-row terminal tests before the first decision
-              const uint32_t c0 = s_confg[A];
-              ctl->min_sep = min(ctl->min_sep, c0);
-              if (rank == 0) args.stepd2[sb] = c0;
-              int st = -1;
-              const bool below = (qz < 0) || ([&] {
-                                   if (w.nx <= 0) return false;
-                                   const int64_t rx = (int64_t)qx - w.x0, ry = (int64_t)qy - w.y0;
-                                   if (rx < 0 || ry < 0) return false;
-                                   const int64_t ix = rx / w.cell, iy = ry / w.cell;
-                                   if (ix >= w.nx || iy >= w.ny) return false;
-                                   return qz < __ldg(&w.height[iy * (int64_t)w.nx + ix]);
-                                 }());
-              const int64_t gx = (int64_t)qx - rq.dst[0], gy = (int64_t)qy - rq.dst[1], gz = (int64_t)qz - rq.dst[2];
-              if (c0 < w.sep2) st = 1;
-              else if (below) st = 2;
-              else if (gx * gx + gy * gy + gz * gz < w.cap2) st = 0;
-              if (st >= 0) {
-                ctl->status = st;
-                ctl->fail_step = st == 0 ? -1 : 0;
-                ctl->done = 1;
-                decided = true;
-              }
-            }
-            if (!decided) {
+            ctl->min_sep = min(ctl->min_sep, c0);
+            if (rank == 0) args.stepd2[sbase + k] = c0;
+            // Determine terminal state of state k (Sec IV.I): conflict, terrain, goal, timeout
+            int st = -1;
+            if (c0 < w.sep2) st = 1;
+            else if (ctl->fl & 1) st = 2;
+            else if (ctl->fl & 2) st = 0;
+            else if (k >= w.max_steps) st = 3;
+            if (st >= 0) {
+              ctl->status = st;
+              ctl->fail_step = st == 0 ? -1 : k;
+              ctl->done = 1;
+            } else {
+              const bool near = (A > 1) && (v1 - v2 < w.near_tie_rel * s_vsc[a1]);
               if (rank == 0) {
-                args.astar[sb + k] = a1;
-                args.ntie[sb + k] = near ? 1 : 0;
+                args.astar[sbase + k] = a1;
+                args.ntie[sbase + k] = near ? 1 : 0;
               }
               ctl->n_near += near ? 1 : 0;
               const int4 p1 = s_pos[a1 * W + 0];  // s_{t+1} <- Delta_1[a*] (Alg 1)
@@ -583,50 +652,42 @@ __global__ void __launch_bounds__(512, 1) walk_kernel(const World w, const WalkA
               ctl->psi = p1.w;
               ctl->k = k1;
               ctl->steps_run += 1;
-              const uint32_t c1 = s_confg[a1];
-              ctl->min_sep = min(ctl->min_sep, c1);
+              ctl->fl = s_flags[a1];
+              ctl->fin = (ctl->fl != 0 || k1 >= w.max_steps) ? 1 : 0;
               if (rank == 0) {
-                int32_t* tq = args.traj + 3 * (sb + k1);
+                int32_t* tq = args.traj + 3 * (sbase + k1);
                 tq[0] = p1.x; tq[1] = p1.y; tq[2] = p1.z;
-                args.heading[sb + k1] = p1.w;
-                args.stepd2[sb + k1] = c1;
-              }
-              // Determine terminal state (Sec IV.I), priority: conflict, terrain, goal, timeout
-              const bool below = (p1.z < 0) || ([&] {
-                                   if (w.nx <= 0) return false;
-                                   const int64_t rx = (int64_t)p1.x - w.x0, ry = (int64_t)p1.y - w.y0;
-                                   if (rx < 0 || ry < 0) return false;
-                                   const int64_t ix = rx / w.cell, iy = ry / w.cell;
-                                   if (ix >= w.nx || iy >= w.ny) return false;
-                                   return p1.z < __ldg(&w.height[iy * (int64_t)w.nx + ix]);
-                                 }());
-              const int64_t gx = (int64_t)p1.x - rq.dst[0], gy = (int64_t)p1.y - rq.dst[1],
-                            gz = (int64_t)p1.z - rq.dst[2];
-              int st = -1;
-              if (c1 < w.sep2) st = 1;
-              else if (below) st = 2;
-              else if (gx * gx + gy * gy + gz * gz < w.cap2) st = 0;
-              else if (k1 >= w.max_steps) st = 3;
-              if (st >= 0) {
-                ctl->status = st;
-                ctl->fail_step = st == 0 ? -1 : k1;
-                ctl->done = 1;
+                args.heading[sbase + k1] = p1.w;
               }
             }
           }
         }
       }
-      if (args.eval && rank == 0) {
-        for (int i = tid; i < AW; i += NT) {
-          args.dbg_v[i] = s_fix[i];
-          args.dbg_s[i] = s_sfix[i];
-        }
-      }
       __syncthreads();
+      FMDP_MARK(PH_DECIDE)
       if (ctl->done) break;
     }
 
+    // eval only: separation minimum of every action's Delta_1 vs the whole row K+1 (debug hook)
+    if (args.eval && rank == 0) {
+      for (int a = tid; a < A; a += NT) s_conf[a] = w.sat_d2;
+      __syncthreads();
+      const int64_t K1 = rq.t0 + 1;
+      const int n1 = row_count(w, K1);
+      const int32_t* rowg = w.rows + (size_t)K1 * 4 * w.row_cap;
+      for (int i = tid; i < A * n1; i += NT) {
+        const int a = i / n1, j = i % n1;
+        const int4 p1 = s_pos[a * W];
+        const uint32_t d = clamp_d2(rowg[j] - p1.x, rowg[w.row_cap + j] - p1.y, rowg[2 * w.row_cap + j] - p1.z,
+                                    w.R_max, w.sat_d2);
+        if (d < w.sat_d2) atomicMin(&s_conf[a], d);
+      }
+      __syncthreads();
+      for (int a = tid; a < A; a += NT) args.dbg_conf[a] = s_conf[a];
+    }
+
     // ------------------------------------------------------------ request epilogue
+    cluster.sync();  // n_exact contributions of every CTA have landed in rank 0
     if (rank == 0 && tid == 0 && !args.eval) {
       Out o;
       o.status = ctl->status;
@@ -649,6 +710,10 @@ __global__ void __launch_bounds__(512, 1) walk_kernel(const World w, const WalkA
     pending = 0;
     __syncthreads();
   }
+  if (prof) {
+    for (int i = 0; i < PH_N; ++i) atomicAdd(&args.prof[i], pacc[i]);
+  }
+#undef FMDP_MARK
 }
 
 // ----------------------------------------------------------------------------- append / influence
@@ -677,8 +742,9 @@ __global__ void append_kernel(int32_t* rows, int32_t cap, int64_t horizon, const
   }
 }
 
-// First decision step of request i whose computation could see plan j (|q_i(k) - p_j(K')|
-// < bound for K' in {K, K+1}); INT_MAX if none.  Conservative and exact (DESIGN.md a10).
+// First step k of request i whose computation could see plan j: step k reads only row
+// K = t0_i + k (wells around the projected states, and the exact separation test of state
+// k), so it is unaffected unless |q_i(k) - p_j(K)| < bound (DESIGN.md a10).  INT_MAX if none.
 __global__ void influence_kernel(const int32_t* traj, int32_t cap, const int32_t* n_states, const int64_t* t0,
                                  const InflPair* pairs, int64_t bound2, int32_t* kfirst) {
   __shared__ int32_t best;
@@ -687,33 +753,37 @@ __global__ void influence_kernel(const int32_t* traj, int32_t cap, const int32_t
   __syncthreads();
   const int ni = n_states[pr.i], nj = n_states[pr.j];
   const int64_t ti = t0[pr.i], tj = t0[pr.j];
-  const int kmax = ni > 1 ? ni - 1 : 1;  // decisions 0..n-2 (state 0 check included in k = 0)
   const int32_t* qi = traj + (size_t)pr.i * cap * 3;
   const int32_t* pj = traj + (size_t)pr.j * cap * 3;
-  for (int k = threadIdx.x; k < kmax; k += blockDim.x) {
+  // only rows where both are present can interact
+  const int64_t k_lo = max((int64_t)0, tj - ti), k_hi = min((int64_t)ni, tj + nj - ti);
+  for (int64_t k = k_lo + threadIdx.x; k < k_hi; k += blockDim.x) {
     if (k >= best) break;
-    const int64_t K = ti + k;
-#pragma unroll
-    for (int d = 0; d < 2; ++d) {
-      const int64_t idx = K + d - tj;
-      if (idx < 0 || idx >= nj) continue;
-      const int64_t dx = qi[3 * k] - pj[3 * idx], dy = qi[3 * k + 1] - pj[3 * idx + 1], dz = qi[3 * k + 2] - pj[3 * idx + 2];
-      if (dx * dx + dy * dy + dz * dz < bound2) {
-        atomicMin(&best, k);
-        break;
-      }
-    }
+    const int64_t idx = ti + k - tj;
+    const int64_t dx = qi[3 * k] - pj[3 * idx], dy = qi[3 * k + 1] - pj[3 * idx + 1], dz = qi[3 * k + 2] - pj[3 * idx + 2];
+    if (dx * dx + dy * dy + dz * dz < bound2) atomicMin(&best, (int32_t)k);
   }
   __syncthreads();
   if (threadIdx.x == 0) kfirst[blockIdx.x] = best;
 }
 
 // ----------------------------------------------------------------------------- launchers
+int walk_groups_per_warp(int ncol, int max_threads) {
+  for (int ngw = 4; ngw > 1; ngw >>= 1)
+    if (32 * ((ncol + 32 / ngw - 1) / (32 / ngw)) <= max_threads) return ngw;
+  return 1;
+}
+
+int walk_threads(int ncol, int max_threads) {
+  const int cpw = 32 / walk_groups_per_warp(ncol, max_threads);
+  return 32 * ((ncol + cpw - 1) / cpw);
+}
+
 template <int C>
 static cudaError_t launch_walk_t(const World& w, const WalkArgs& a, int cluster, int n_clusters, int threads,
                                  int chunk, cudaStream_t s) {
   Layout L;
-  L.build(w.HL, chunk, threads, C, w.n_turn * w.W, w.A, w.A * w.W);
+  L.build(w.HL, chunk, threads, C, w.n_turn * w.W, w.A, w.A * w.W, cluster);
   cudaError_t e = cudaFuncSetAttribute(walk_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
   if (cluster > 8) {
@@ -732,13 +802,14 @@ static cudaError_t launch_walk_t(const World& w, const WalkArgs& a, int cluster,
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, walk_kernel<C>, w, a, chunk);
+  const int ngw = walk_groups_per_warp(w.n_turn * w.W, threads);
+  return cudaLaunchKernelEx(&cfg, walk_kernel<C>, w, a, chunk, ngw);
 }
 
 template <int C>
 static cudaError_t max_clusters_t(const World& w, int cluster, int threads, int chunk, int* out) {
   Layout L;
-  L.build(w.HL, chunk, threads, C, w.n_turn * w.W, w.A, w.A * w.W);
+  L.build(w.HL, chunk, threads, C, w.n_turn * w.W, w.A, w.A * w.W, cluster);
   cudaError_t e = cudaFuncSetAttribute(walk_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
   if (cluster > 8) {
@@ -778,9 +849,9 @@ cudaError_t walk_max_clusters(const World& w, int n_climb, int cluster, int thre
   }
 }
 
-size_t walk_smem_bytes(const World& w, int n_climb, int threads, int chunk) {
+size_t walk_smem_bytes(const World& w, int n_climb, int threads, int chunk, int cluster) {
   Layout L;
-  L.build(w.HL, chunk, threads, n_climb, w.n_turn * w.W, w.A, w.A * w.W);
+  L.build(w.HL, chunk, threads, n_climb, w.n_turn * w.W, w.A, w.A * w.W, cluster);
   return L.total;
 }
 

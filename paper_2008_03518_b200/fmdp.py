@@ -65,7 +65,8 @@ class Devices(C.Structure):
 
 
 class Launch(C.Structure):
-    _fields_ = [("cluster_size", C.c_int32), ("max_walkers", C.c_int32), ("threads", C.c_int32)]
+    _fields_ = [("cluster_size", C.c_int32), ("max_walkers", C.c_int32), ("threads", C.c_int32),
+                ("profile", C.c_int32)]
 
 
 class Request(C.Structure):
@@ -80,7 +81,10 @@ class Result(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("steps", C.c_int64), ("pair_evals", C.c_int64), ("rounds", C.c_int32), ("reruns", C.c_int32),
                 ("cluster_size", C.c_int32), ("walkers", C.c_int32), ("kernels", C.c_int32),
-                ("device_ms", C.c_double)]
+                ("device_ms", C.c_double), ("phase_cycles", C.c_int64 * 10)]
+
+PHASES = ("projection", "goal_terrain", "row_wait", "hot_loop", "stage", "reduce_scatter", "barrier1",
+          "owner_epilogue", "barrier2", "decide")
 
 
 EXPORTS = ["fmdp_airspace_default", "fmdp_create", "fmdp_destroy", "fmdp_set_launch", "fmdp_add_plan",
@@ -201,7 +205,10 @@ class FMDP:
                 return int(torch.cuda.caching_allocator_alloc(int(nbytes), device=dev, stream=tstream))
 
             def _release(ptr, user):
-                torch.cuda.caching_allocator_delete(int(ptr))
+                try:
+                    torch.cuda.caching_allocator_delete(int(ptr))
+                except Exception:  # interpreter shutdown: torch already torn down
+                    pass
 
             self._alloc_cb, self._release_cb = ALLOC_FN(_alloc), RELEASE_FN(_release)
             d.alloc, d.release = self._alloc_cb, self._release_cb
@@ -234,8 +241,8 @@ class FMDP:
     def __exit__(self, *exc):
         self.close()
 
-    def set_launch(self, cluster_size=0, max_walkers=0, threads=0):
-        l = Launch(cluster_size, max_walkers, threads)
+    def set_launch(self, cluster_size=0, max_walkers=0, threads=0, profile=0):
+        l = Launch(cluster_size, max_walkers, threads, profile)
         self._check(self.L.fmdp_set_launch(self.ctx, C.byref(l)), "fmdp_set_launch")
 
     # ------------------------------------------------------------------ store
@@ -342,4 +349,6 @@ class FMDP:
     def stats(self) -> dict:
         st = Stats()
         self._check(self.L.fmdp_get_stats(self.ctx, C.byref(st)), "fmdp_get_stats")
-        return {k: getattr(st, k) for k, _ in Stats._fields_}
+        out = {k: getattr(st, k) for k, _ in Stats._fields_ if k != "phase_cycles"}
+        out["phase_cycles"] = {p: int(st.phase_cycles[i]) for i, p in enumerate(PHASES)}
+        return out

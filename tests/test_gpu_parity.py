@@ -78,18 +78,25 @@ def test_eval_step_identical_across_cluster_sizes(F):
         check_step(o, orc.eval_step(q, psi, g, K))
 
 
-def _sum_of_two_squares(n):
+def _sum_of_squares(n):
+    """(a, b, c) with a^2 + b^2 + c^2 = n (brute force, largest a first)."""
     a = int(np.sqrt(n))
     while a > 0:
-        b2 = n - a * a
-        b = int(round(np.sqrt(b2)))
-        if b * b == b2:
-            return a, b
+        r = n - a * a
+        b = int(np.sqrt(r))
+        while b >= 0:
+            c2 = r - b * b
+            c = int(round(np.sqrt(c2)))
+            if c * c == c2:
+                return a, b, c
+            b -= 1
+            if b < int(np.sqrt(r)) - 64:
+                break
         a -= 1
     return None
 
 
-@pytest.mark.parametrize("delta", [-1, 0, 1])
+@pytest.mark.parametrize("delta", [-2, 0, 1])   # R^2-1 = 7 mod 8 is no sum of 3 squares
 def test_exact_radius_boundary(F, delta):
     """Well exactly at / one unit^2 inside / outside R for a projected state: the FP32 filter
     lands in its band and the exact fallback must reproduce the oracle's strict d < R."""
@@ -98,9 +105,9 @@ def test_exact_radius_boundary(F, delta):
     q = np.array([0, 0, 200 * U], np.int32)
     s = q + np.array([320 * 10, 0, 0])                   # straight-level, t = W
     R = 450 * U
-    ab = _sum_of_two_squares(R * R + delta)
-    assert ab is not None
-    p = s + np.array([ab[0], ab[1], 0])
+    abc = _sum_of_squares(R * R + delta)
+    assert abc is not None
+    p = s + np.array(abc)
     plan = np.repeat(p[None], 40, axis=0).astype(np.int32)   # stationary: all 5 wells at p
     sc = fs.Scenario(air, fs.Terrain(), [(0, plan)], q[None], q[None], np.zeros(1, np.int64))
     orc = O.for_scenario(sc)
