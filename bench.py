@@ -1,0 +1,294 @@
+#!/usr/bin/env python
+"""Benchmark of the FastMDP-GPU hot path on BASELINE.json configs[1].
+
+One "step" = one first-come-first-served batch of 100 requests scheduled against the
+3000-plan store with terrain (all rows of SURVEY §8(a): wells, projection, goal, hot loop,
+terrain, combine, argmax, advance, separation, append, FCFS speculation).  The store is
+restored (fmdp_truncate) and L2 is flushed between steps, outside the timed region.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+N > 1 (torchrun, one process per GPU): every rank schedules an independent replica batch
+("independent parallel instances") -> weak scaling, value = all ranks' requests / max
+time over ranks.  --impl reference times the oracle (oracle/, fp64 C) on host cores on a
+bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FCFS requests scheduled/sec and ms/request vs #accepted plans, 1/2/4/8 B200"
+WORKLOAD = ("configs[1]: batch of 100 FCFS requests against 3000 accepted plans with a 256-well terrain "
+            "grid, 16x16 km dense urban airspace, 9 headings x 3 climbs, W=10")
+OPS_PER_PAIR = 13.0 / 3.0  # hot-loop instructions per (state, well) pair at 3 climbs
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="native", choices=["native", "reference"])
+    p.add_argument("--seed", type=int, default=2)
+    p.add_argument("--cpu-sample-s", type=float, default=15.0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the timed region runs."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_baseline(sc, budget_s: float):
+    """The oracle as it stands (fp64 C, one core): FCFS requests of the same batch, in order,
+    until the time budget is spent."""
+    from oracle import oracle as O
+    orc = O.for_scenario(sc)
+    t0 = time.perf_counter()
+    done = states = 0
+    while done < sc.n_requests and time.perf_counter() - t0 < budget_s:
+        r = orc.schedule(sc.src[done], sc.dst[done], int(sc.t0[done]))
+        states += r.n_states
+        done += 1
+    dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": "requests/s", "cores": 1, "kind": "oracle",
+            "sample": f"first {done} of {sc.n_requests} requests of the same FCFS batch ({states} states) "
+                      f"in {dt:.1f} s, single thread"}
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    import fmdp_synth as fs
+    from oracle import oracle as O
+    sc = fs.config_c2(seed=args.seed)
+    n_req = 1  # bounded sample per step: the first request of the batch against the initial store
+    times, states = [], 0
+    for i in range(args.warmup + args.steps):
+        orc = O.for_scenario(sc)
+        t0 = time.perf_counter()
+        r = orc.schedule(sc.src[0], sc.dst[0], int(sc.t0[0]))
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+            states += r.n_states
+    tot = sum(times)
+    value = n_req * args.steps / tot
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "requests/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": WORKLOAD, "sample": "first request of the batch per step"},
+            "cpu_baseline": {"value": value, "unit": "requests/s", "cores": 1, "kind": "oracle",
+                             "sample": f"first request of the configs[1] batch ({states // max(1, args.steps)} "
+                                       f"states) per step, fp64 C oracle, single thread"},
+            "e2e": {"value": value, "unit": "requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_native(args):
+    rank, world, local = dist_env()
+    import numpy as np
+    import torch
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import fmdp_synth as fs
+    from paper_2008_03518_b200.fmdp import FMDP, Request, Result
+
+    sc = fs.config_c2(seed=args.seed + 1000 * rank)  # replica r: its own seeded batch and store
+    stream = torch.cuda.Stream(device=local)
+    ctx = FMDP(sc.airspace, sc.terrain, device=local, stream=stream)
+    ctx.add_plans(sc.plans)
+    n0 = ctx.num_plans()
+    reqs = ctx.make_requests(sc.src, sc.dst, sc.t0)
+    n = len(reqs)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def one(want_traj):
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            res = ctx.schedule_batch(None, None, None, want_traj=want_traj, reqs=reqs)
+            ev1.record(stream)
+        ev1.synchronize()
+        return res, ev0.elapsed_time(ev1)
+
+    def reset():
+        ctx.truncate(n0)
+        flush.zero_()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        one(False)
+        reset()
+    # ---- value: device-resident store and requests, trajectories left on the device
+    times, st_all, res_last = [], [], None
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            res, ms = one(False)
+            st_all.append(ctx.stats())
+            times.append(ms)
+            res_last = res
+            reset()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    # ---- e2e: through the public API with host requests, trajectories and results copied back
+    e2e_times, d2h = [], 0
+    for _ in range(max(1, args.steps)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res, ms = one(True)
+        e2e_times.append(ms)
+        d2h = sum(r.n_states for r in res) * 12 + n * C_RESULT_BYTES
+        reset()
+    h2d = n * C_REQUEST_BYTES
+
+    tot_ms = max_over_ranks(sum(times), world)
+    e2e_ms = max_over_ranks(sum(e2e_times), world)
+    total_req = sum_over_ranks(n * args.steps, world)
+    value = total_req / (tot_ms / 1e3)
+    e2e_value = sum_over_ranks(n * len(e2e_times), world) / (e2e_ms / 1e3)
+    stats = st_all[-1]
+    walk_ms = sum(s["device_ms"] for s in st_all)
+    pairs = sum(s["pair_evals"] for s in st_all)
+    launches = sum(s["kernels"] for s in st_all)
+    acc = sum(r.accepted for r in res_last)
+    states = sum(r.n_states for r in res_last)
+    steps_dev = sum(s["steps"] for s in st_all)
+    clocks = clk.summary()
+    peak_clock = 1965.0
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        peak_clock = float(mp.get("sm_max_mhz", peak_clock))
+    except Exception:
+        pass
+    peak_tops = 148 * 128 * peak_clock * 1e6 / 1e12
+    achieved_tops = pairs * OPS_PER_PAIR / (walk_ms / 1e3) / 1e12 if walk_ms > 0 else 0.0
+    if rank != 0:
+        return 0
+    line = {
+        "metric": METRIC, "value": value, "unit": "requests/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "plans": len(sc.plans), "requests": n, "terrain_wells": int(len(sc.terrain.radius)),
+                   "actions": sc.airspace.n_actions, "W": sc.airspace.W, "l2": "flushed between steps (256 MB write)",
+                   "parallelism": f"replicas{world}" if world > 1 else "single-gpu"},
+        "ms_per_request": tot_ms / args.steps / n,
+        "requests_accepted": acc, "states_per_request": states / n, "device_steps_per_batch": steps_dev / args.steps,
+        "action_plan_evals_per_s": pairs / 5.0 / sc.airspace.W / (tot_ms / 1e3) * world,
+        "pair_evals_per_s": pairs / (tot_ms / 1e3) * world,
+        "rounds": stats["rounds"], "reruns": stats["reruns"],
+        "roofline": {"bound": "alu", "achieved": achieved_tops, "peak": peak_tops, "unit": "Top/s",
+                     "frac": achieved_tops / peak_tops, "traffic": None,
+                     "kernel": "walk_kernel<3>", "ops_per_pair": OPS_PER_PAIR,
+                     "peak_basis": f"148 SM x 128 lanes x {peak_clock:.0f} MHz (MEASURED_PEAKS sm_max_mhz)"},
+        "e2e": {"value": e2e_value, "unit": "requests/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(sc, args.cpu_sample_s)
+    print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+C_REQUEST_BYTES = 64  # sizeof(fmdp_request): u64 + 2 x 3 doubles + i64
+C_RESULT_BYTES = 32   # sizeof(fmdp_result)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_native(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

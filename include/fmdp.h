@@ -128,6 +128,7 @@ typedef struct fmdp_launch {
   int32_t max_walkers;    /* concurrent trajectories in a batch round, 0 = auto          */
   int32_t threads;        /* threads per CTA, 0 = auto                                   */
   int32_t profile;        /* 1: accumulate per-phase cycles of CTA 0 (fmdp_stats)        */
+  int32_t step_budget;    /* batch: decision steps per trajectory per launch slice, 0 = 256 */
 } fmdp_launch;
 
 typedef struct fmdp_request {
@@ -151,8 +152,9 @@ typedef struct fmdp_result {
 typedef struct fmdp_stats {
   int64_t steps;           /* decision steps executed on the device (incl. re-runs)      */
   int64_t pair_evals;      /* (projected state, well) pairs evaluated in the hot loop    */
-  int32_t rounds;          /* speculative FCFS rounds                                     */
-  int32_t reruns;          /* trajectories re-run after influence by an earlier commit   */
+  int32_t rounds;          /* walk launches (speculative FCFS slices)                      */
+  int32_t reruns;          /* rollbacks: trajectories resumed from an earlier step after an */
+                           /* earlier request's commit could influence them               */
   int32_t cluster_size;
   int32_t walkers;
   int32_t kernels;         /* kernel launches                                             */

@@ -60,7 +60,7 @@ struct Req {
 };
 
 struct Out {
-  int32_t status, n_states, fail_step, n_near_ties;
+  int32_t status, n_states, fail_step, n_near_ties;  // status -1: paused (resume at n_states-1)
   int32_t n_exact, steps_run;
   uint32_t min_sep_d2;
   int32_t pad;
@@ -78,6 +78,7 @@ struct WalkArgs {
   int8_t* ntie;                 // [slot][cap]
   int32_t cap;
   int32_t eval;                 // 1: evaluate one step (debug outputs), no advance
+  int32_t budget;               // decision steps per request in this launch (then pause, status -1)
   double* dbg_vstar;            // [A]
   double* dbg_v;                // [A*W]
   double* dbg_s;                // [A*W]

@@ -238,7 +238,9 @@ void choose_launch(fmdp_ctx* ctx, int n_run, int* G_out, int* nc_out) {
       if (c) { tot += c; ++nz; }
     plans = nz ? (double)tot / nz : 0.0;
   }
-  const double work = plans * fmdp::NTAU * ctx->A * ctx->W / 24.0 + 4000.0;  // cycles on one SM
+  // per-step cycles of one walker: hot loop (~21 pairs/clk/SM, measured) / G + per-step
+  // overhead (projection, reductions, two cluster barriers, decision; measured ~16k cycles)
+  const double work = plans * fmdp::NTAU * ctx->A * ctx->W / 21.0;
   const int sizes[] = {16, 8, 4, 2, 1};
   for (int G : sizes) {
     if (ctx->launch.cluster_size && G != ctx->launch.cluster_size) continue;
@@ -247,7 +249,7 @@ void choose_launch(fmdp_ctx* ctx, int n_run, int* G_out, int* nc_out) {
     int conc = std::min(mc, n_run);
     if (ctx->launch.max_walkers > 0) conc = std::min(conc, ctx->launch.max_walkers);
     const double waves = std::ceil((double)n_run / conc);
-    const double t = waves * (work / G + 2500.0 + 300.0 * G);
+    const double t = waves * (work / G + 16000.0 + 300.0 * G);
     if (t < best) {
       best = t;
       best_G = G;
@@ -263,7 +265,7 @@ void choose_launch(fmdp_ctx* ctx, int n_run, int* G_out, int* nc_out) {
                  *nc_out, mc);
 }
 
-fmdp_status run_walk(fmdp_ctx* ctx, const std::vector<Req>& run, bool eval) {
+fmdp_status run_walk(fmdp_ctx* ctx, const std::vector<Req>& run, bool eval, int budget = INT_MAX) {
   if (run.empty()) return FMDP_OK;
   CK(cudaMemcpyAsync(ctx->d_reqs, run.data(), sizeof(Req) * run.size(), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemsetAsync(ctx->d_queue, 0, sizeof(int32_t), ctx->stream));
@@ -279,6 +281,7 @@ fmdp_status run_walk(fmdp_ctx* ctx, const std::vector<Req>& run, bool eval) {
   a.ntie = ctx->d_ntie;
   a.cap = ctx->cap_states;
   a.eval = eval ? 1 : 0;
+  a.budget = budget;
   a.dbg_vstar = ctx->d_dbg_vstar;
   a.dbg_v = ctx->d_dbg_v;
   a.dbg_s = ctx->d_dbg_s;
@@ -299,6 +302,7 @@ fmdp_status run_walk(fmdp_ctx* ctx, const std::vector<Req>& run, bool eval) {
   CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
   ctx->stats.device_ms += ms;
   ctx->stats.kernels += 1;
+  if (std::getenv("FMDP_DEBUG")) std::fprintf(stderr, "fmdp: walk n=%zu G=%d clusters=%d %.3f ms\n", run.size(), G, nc, ms);
   return FMDP_OK;
 }
 
@@ -454,81 +458,88 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
       ++runs;
       ctx->stats.rounds += 1;
       if ((st = fetch_out(ctx, n))) return st;
+      ctx->stats.steps += ctx->h_out[i].steps_run;
       if (ctx->h_out[i].status == FMDP_ACCEPTED && (st = commit_slots(ctx, {i}, base, aircraft, plan_id))) return st;
     }
   } else {
-    // Speculative FCFS rounds (DESIGN.md a10): run every not-yet-valid request against the
-    // current store, then commit in array order while no plan committed after a request's
-    // run could have influenced it; an influenced request resumes from its first
-    // influenced step in the next round.  Identical to the sequential loop.
-    std::vector<char> valid(n, 0);
-    std::vector<int> start(n, 0);
-    std::vector<size_t> version(n, 0);
-    std::vector<int> committed;  // slots committed during this call, in order
+    // Speculative FCFS in time slices (DESIGN.md a10).  Invariant at the top of every
+    // slice: the steps already computed for every pending request are consistent with the
+    // current store.  A slice advances every unfinished request by at most `budget` steps
+    // (cluster size re-chosen for the shrinking count), then commits the finished FCFS prefix
+    // and rolls back any pending request whose computed steps could see a newly committed
+    // plan to its first influenced step.  Result: identical to the sequential loop.
+    const int budget = ctx->launch.step_budget > 0 ? ctx->launch.step_budget : 256;
+    std::vector<char> fin(n, 0);
+    std::vector<int> kdone(n, 0);
+    int rollbacks = 0;
     int c = 0;
     while (c < n) {
       std::vector<Req> run;
       for (int i = c; i < n; ++i)
-        if (!valid[i]) {
+        if (!fin[i]) {
           Req r = base[i];
-          r.start_k = start[i];
+          r.start_k = kdone[i];
           run.push_back(r);
         }
-      if ((st = run_walk(ctx, run, false))) return st;
-      runs += (int)run.size();
-      ctx->stats.rounds += 1;
-      for (const Req& r : run) {
-        valid[r.slot] = 1;
-        version[r.slot] = ctx->plans.size();
+      if (!run.empty()) {
+        if ((st = run_walk(ctx, run, false, budget))) return st;
+        runs += (int)run.size();
+        ctx->stats.rounds += 1;
       }
       if ((st = fetch_out(ctx, n))) return st;
+      for (const Req& r : run) {
+        const Out& o = ctx->h_out[r.slot];
+        ctx->stats.steps += o.steps_run;
+        if (o.status < 0) kdone[r.slot] = o.n_states - 1;
+        else fin[r.slot] = 1;
+      }
+      // influence of every finished, accepted request j on every later pending request i
+      std::vector<InflPair> pairs;
       std::vector<int32_t> ns(n);
       for (int i = 0; i < n; ++i) ns[i] = ctx->h_out[i].n_states;
-      CK(cudaMemcpyAsync(ctx->d_nstates, ns.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
-      // influence pairs (i, j): j committed after i's run, or j < i accepted in this round's walk
-      std::vector<InflPair> pairs;
-      for (int i = c; i < n; ++i) {
-        if (!valid[i]) continue;
-        for (int j : committed)
-          if (plan_id[j] >= version[i]) pairs.push_back({i, j});
+      for (int i = c + 1; i < n; ++i)
         for (int j = c; j < i; ++j)
-          if (valid[j] && ctx->h_out[j].status == FMDP_ACCEPTED) pairs.push_back({i, j});
-      }
+          if (fin[j] && ctx->h_out[j].status == FMDP_ACCEPTED) pairs.push_back({i, j});
       std::vector<int32_t> kf;
-      if ((st = influence(ctx, pairs, kf))) return st;
+      if (!pairs.empty()) {
+        CK(cudaMemcpyAsync(ctx->d_nstates, ns.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+        if ((st = influence(ctx, pairs, kf))) return st;
+      }
       std::vector<int> newly;
-      auto kfirst_of = [&](int i, bool only_newly) {
+      auto first_influence = [&](int i) {
         int best = INT_MAX;
-        for (size_t p = 0; p < pairs.size(); ++p) {
-          if (pairs[p].i != i || kf[p] == INT_MAX) continue;
-          const int j = pairs[p].j;
-          const bool in_new = std::find(newly.begin(), newly.end(), j) != newly.end();
-          const bool in_old = !only_newly && plan_id[j] != 0xffffffffu && plan_id[j] >= version[i];
-          if (in_new || in_old) best = std::min(best, kf[p]);
-        }
+        for (size_t p = 0; p < pairs.size(); ++p)
+          if (pairs[p].i == i && kf[p] != INT_MAX &&
+              std::find(newly.begin(), newly.end(), pairs[p].j) != newly.end())
+            best = std::min(best, kf[p]);
         return best;
       };
-      while (c < n && valid[c]) {
-        const int k1 = kfirst_of(c, false);
+      while (c < n && fin[c]) {
+        const int k1 = first_influence(c);
         if (k1 != INT_MAX) {
-          valid[c] = 0;
-          start[c] = k1;
+          fin[c] = 0;
+          kdone[c] = k1;
+          ++rollbacks;
           break;
         }
         if (ctx->h_out[c].status == FMDP_ACCEPTED) newly.push_back(c);
         ++c;
       }
       if ((st = commit_slots(ctx, newly, base, aircraft, plan_id))) return st;
-      committed.insert(committed.end(), newly.begin(), newly.end());
-      for (int i = c + 1; i < n; ++i) {
-        if (!valid[i]) continue;
-        const int k1 = kfirst_of(i, true);
-        if (k1 != INT_MAX) {
-          valid[i] = 0;
-          start[i] = k1;
+      for (int i = c; i < n; ++i) {  // includes the unfinished head c
+        const int k1 = first_influence(i);
+        if (k1 == INT_MAX) continue;
+        if (fin[i]) {
+          fin[i] = 0;
+          kdone[i] = k1;
+          ++rollbacks;
+        } else if (k1 < kdone[i]) {
+          kdone[i] = k1;
+          ++rollbacks;
         }
       }
     }
+    runs = n + rollbacks;
   }
   ctx->stats.reruns = runs - n;
   if ((st = fetch_out(ctx, n))) return st;
@@ -549,7 +560,6 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
     res[i].min_sep_m = std::sqrt((double)o.min_sep_d2) * ctx->air.u_m;
     res[i].n_near_ties = o.n_near_ties;
     res[i].n_exact = o.n_exact;
-    ctx->stats.steps += o.steps_run;
   }
   if (traj) {
     for (int i = 0; i < n; ++i) {

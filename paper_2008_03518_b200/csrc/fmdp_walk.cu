@@ -67,6 +67,35 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+// Packed FP32 pairs (sm_100: FADD2 / FMUL2 / FFMA2) and the 3-input minimum (FMNMX3).
+typedef unsigned long long f2;
+__device__ __forceinline__ f2 pk2(float lo, float hi) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  f2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+  f2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  f2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ float min3(float a, f2 p) {
+  float lo, hi, r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(p));
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(lo), "f"(hi));
+  return r;
+}
+
 __device__ __forceinline__ int sext(uint32_t v, int bits) { return (int)(v << (32 - bits)) >> (32 - bits); }
 
 // exact squared distance, saturated at sat (= R_max^2 < 2^30): valid because any component
@@ -296,6 +325,9 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       __syncthreads();
 
       float sx = 0.f, sy = 0.f, sz[C];
+      f2 sx2 = 0, sy2 = 0, sz2[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) sz2[c] = 0;
       int hgt = INT_MIN, x1 = 0, y1 = 0;  // ground under Delta_1 (t = 1 columns, group 0)
       if (!fin) {
         // ---- a5 candidates: terrain wells that can reach any projected state (exact cull)
@@ -323,6 +355,10 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         sy = (float)(y - qy);
 #pragma unroll
         for (int c = 0; c < C; ++c) sz[c] = (float)(w.climb[c] * t);
+        sx2 = pk2(sx, sx);
+        sy2 = pk2(sy, sy);
+#pragma unroll
+        for (int c = 0; c < C; ++c) sz2[c] = pk2(sz[c], sz[c]);
         if (grp == 0 && col < NCOL) {
 #pragma unroll
           for (int c = 0; c < C; ++c) s_pos[(it * C + c) * W + (t - 1)] = make_int4(x, y, qz + w.climb[c] * t, ps);
@@ -388,42 +424,48 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
             if (fin) continue;
             const uint32_t pv = (uint32_t)V[j];
             const int vx = sext(pv, 11), vy = sext(pv >> 11, 11), vz = sext(pv >> 22, 10);
-            float4* c4 = reinterpret_cast<float4*>(s_cen + 16 * j);
-            float cc[16];
+            // plan pair layout: [pair][tau][x_j, x_j', y_j, y_j', z_j, z_j'] (+2 pad), negated
+            // offsets so that s - c is one packed add; exact integers < 2^24 (R23)
+            float* cp = s_cen + 32 * (j >> 1) + (j & 1);
 #pragma unroll
             for (int t = 0; t < NTAU; ++t) {
-              cc[3 * t + 0] = (float)(rx + w.k_tau[t] * vx);
-              cc[3 * t + 1] = (float)(ry + w.k_tau[t] * vy);
-              cc[3 * t + 2] = (float)(rz + w.k_tau[t] * vz);
+              cp[6 * t + 0] = (float)(-(rx + w.k_tau[t] * vx));
+              cp[6 * t + 2] = (float)(-(ry + w.k_tau[t] * vy));
+              cp[6 * t + 4] = (float)(-(rz + w.k_tau[t] * vz));
             }
-            cc[15] = 0.f;
-            c4[0] = make_float4(cc[0], cc[1], cc[2], cc[3]);
-            c4[1] = make_float4(cc[4], cc[5], cc[6], cc[7]);
-            c4[2] = make_float4(cc[8], cc[9], cc[10], cc[11]);
-            c4[3] = make_float4(cc[12], cc[13], cc[14], cc[15]);
+          }
+          if (!fin && (nc & 1) && tid == 0) {  // odd tail: the partner slot is a well at infinity
+            float* cp = s_cen + 32 * (nc >> 1) + 1;
+#pragma unroll
+            for (int t = 0; t < NTAU; ++t) cp[6 * t + 0] = cp[6 * t + 2] = cp[6 * t + 4] = 3.0e18f;
           }
           if (fin) continue;
           __syncthreads();
-          const float4* cen4 = reinterpret_cast<const float4*>(s_cen);
-#define FMDP_WELL(T, CX, CY, CZ)                            \
-  {                                                         \
-    const float dx = sx - (CX), dy = sy - (CY);             \
-    const float hh = fmaf(dy, dy, dx * dx);                 \
-    _Pragma("unroll") for (int cc_ = 0; cc_ < C; ++cc_) {   \
-      const float dz = sz[cc_] - (CZ);                      \
-      m[cc_][T] = fminf(m[cc_][T], fmaf(dz, dz, hh));       \
-    }                                                       \
+          const ulonglong2* cen2 = reinterpret_cast<const ulonglong2*>(s_cen);
+          // (state, well) pair: |s - c|^2 = (dx^2 + dy^2) + dz^2, the horizontal part shared by
+          // the C climbs; two plans per packed instruction, FMNMX3 folds both into the minimum
+#define FMDP_WELL2(T, X, Y, Z)                                \
+  {                                                           \
+    const f2 dx = add2(sx2, (X)), dy = add2(sy2, (Y));        \
+    const f2 hh = fma2(dy, dy, mul2(dx, dx));                 \
+    _Pragma("unroll") for (int cc_ = 0; cc_ < C; ++cc_) {     \
+      const f2 dz = add2(sz2[cc_], (Z));                      \
+      m[cc_][T] = min3(m[cc_][T], fma2(dz, dz, hh));          \
+    }                                                         \
   }
-#pragma unroll 2
-          for (int j = grp; j < nc; j += NGW) {
-            const float4 e0 = cen4[4 * j + 0], e1 = cen4[4 * j + 1], e2 = cen4[4 * j + 2], e3 = cen4[4 * j + 3];
-            FMDP_WELL(0, e0.x, e0.y, e0.z)
-            FMDP_WELL(1, e0.w, e1.x, e1.y)
-            FMDP_WELL(2, e1.z, e1.w, e2.x)
-            FMDP_WELL(3, e2.y, e2.z, e2.w)
-            FMDP_WELL(4, e3.x, e3.y, e3.z)
+          const int np = (nc + 1) >> 1;
+          for (int pp = grp; pp < np; pp += NGW) {
+            const ulonglong2* c8 = cen2 + 8 * pp;
+            const ulonglong2 e0 = c8[0], e1 = c8[1], e2 = c8[2], e3 = c8[3], e4 = c8[4], e5 = c8[5], e6 = c8[6],
+                             e7 = c8[7];
+            FMDP_WELL2(0, e0.x, e0.y, e1.x)
+            FMDP_WELL2(1, e1.y, e2.x, e2.y)
+            FMDP_WELL2(2, e3.x, e3.y, e4.x)
+            FMDP_WELL2(3, e4.y, e5.x, e5.y)
+            FMDP_WELL2(4, e6.x, e6.y, e7.x)
+            (void)e7;
           }
-#undef FMDP_WELL
+#undef FMDP_WELL2
           __syncthreads();
         }
         if (!fin && tid == 0 && args.pairs) atomicAdd(args.pairs, (unsigned long long)n * NTAU * AW);
@@ -481,6 +523,24 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         // ---- owner epilogue (half-warp per owned action, lane = substep): reduce the G
         //      partial blocks, exact in/out, values (Alg 8), V*(a)
         const float* rcv = s_recv + (k & 1) * (int)G * NOWN * BLK;
+        // (1) global minimum of every owned (state, tau) over the G partial blocks, all threads
+        float* s_min = s_stage;  // free after barrier 1: [oa][t*NTAU + tau]
+        {
+          const int WT = W * NTAU;
+          for (int e = tid; e < n_own * WT; e += NT) {
+            const int oa = e / WT, rem = e - oa * WT;
+            const float* src = rcv + oa * BLK + rem;
+            float M0 = FLT_MAX, M1 = FLT_MAX;
+            int b = 0;
+            for (; b + 1 < (int)G; b += 2) {
+              M0 = fminf(M0, src[b * NOWN * BLK]);
+              M1 = fminf(M1, src[(b + 1) * NOWN * BLK]);
+            }
+            if (b < (int)G) M0 = fminf(M0, src[b * NOWN * BLK]);
+            s_min[e] = fminf(M0, M1);
+          }
+        }
+        __syncthreads();
         const int hw = tid >> 4, hl = tid & 15;
         const int n_hw = NT >> 4;
         for (int oa0 = 0; oa0 < NOWN; oa0 += n_hw) {  // uniform trip count across the CTA
@@ -493,8 +553,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           if (act) {
 #pragma unroll
             for (int t = 0; t < NTAU; ++t) {
-              float M = FLT_MAX;
-              for (int b = 0; b < (int)G; ++b) M = fminf(M, rcv[(b * NOWN + oa) * BLK + hl * NTAU + t]);
+              const float M = s_min[oa * W * NTAU + hl * NTAU + t];
               if (M < w.R2lo[t]) {
                 mi = fminf(mi, M);
               } else if (M <= w.R2hi[t]) {  // inside the 2^-20 band: decided exactly below
@@ -519,8 +578,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
               } else {  // overflow: walk every owned (state, tau) of this pass, re-test the band
                 const int oa2 = oa0 + it2 / (W * NTAU), rem = it2 % (W * NTAU), l2 = rem / NTAU, t = rem % NTAU;
                 if (oa2 >= n_own) continue;
-                float M = FLT_MAX;
-                for (int b = 0; b < (int)G; ++b) M = fminf(M, rcv[(b * NOWN + oa2) * BLK + l2 * NTAU + t]);
+                const float M = s_min[oa2 * W * NTAU + l2 * NTAU + t];
                 if (!(M >= w.R2lo[t] && M <= w.R2hi[t])) continue;
                 item = (((int)rank + oa2 * (int)G) * W + l2) * NTAU + t;
               }
@@ -598,6 +656,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         double v1 = -INFINITY, v2 = -INFINITY;  // a7: top-2 (lowest index on ties)
         int a1 = INT_MAX, a2 = INT_MAX;
         if (!fin) {
+          // lane l scans a = l, l+32, ... in increasing order; merge lanes with shuffles
           for (int a = lane; a < A; a += 32) {
             const double v = s_vstar[a];
             if (better(v, a, v1, a1)) {
@@ -606,8 +665,10 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
               v2 = v; a2 = a;
             }
           }
+          const int span = A < 32 ? A : 32;  // lanes >= span hold nothing
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) {
+            if (o >= span) continue;  // uniform: skip rounds that only merge empty lanes
             const double ov1 = __shfl_xor_sync(0xffffffffu, v1, o), ov2 = __shfl_xor_sync(0xffffffffu, v2, o);
             const int oa1 = __shfl_xor_sync(0xffffffffu, a1, o), oa2 = __shfl_xor_sync(0xffffffffu, a2, o);
             if (better(ov1, oa1, v1, a1)) {
@@ -658,6 +719,10 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
                 int32_t* tq = args.traj + 3 * (sbase + k1);
                 tq[0] = p1.x; tq[1] = p1.y; tq[2] = p1.z;
                 args.heading[sbase + k1] = p1.w;
+              }
+              if (k1 - rq.start_k >= args.budget) {  // step budget spent: pause at state k1
+                ctl->status = -1;
+                ctl->done = 1;
               }
             }
           }

@@ -66,7 +66,7 @@ class Devices(C.Structure):
 
 class Launch(C.Structure):
     _fields_ = [("cluster_size", C.c_int32), ("max_walkers", C.c_int32), ("threads", C.c_int32),
-                ("profile", C.c_int32)]
+                ("profile", C.c_int32), ("step_budget", C.c_int32)]
 
 
 class Request(C.Structure):
@@ -241,8 +241,8 @@ class FMDP:
     def __exit__(self, *exc):
         self.close()
 
-    def set_launch(self, cluster_size=0, max_walkers=0, threads=0, profile=0):
-        l = Launch(cluster_size, max_walkers, threads, profile)
+    def set_launch(self, cluster_size=0, max_walkers=0, threads=0, profile=0, step_budget=0):
+        l = Launch(cluster_size, max_walkers, threads, profile, step_budget)
         self._check(self.L.fmdp_set_launch(self.ctx, C.byref(l)), "fmdp_set_launch")
 
     # ------------------------------------------------------------------ store

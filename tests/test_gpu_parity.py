@@ -164,14 +164,15 @@ def _replay_fcfs(sc, results, gpu_ctx):
 
 def test_batch_speculative_equals_sequential_and_oracle(F):
     sc = fs.random_small(41, n_plans=60, n_requests=10, half_m=1200.0, n_buildings=20, max_steps=500, t0_max=60)
-    a = ctx_for(F, sc)
-    spec = a.schedule_batch(sc.src, sc.dst, sc.t0)
-    st = a.stats()
     b = ctx_for(F, sc)
     seq = b.schedule_batch(sc.src, sc.dst, sc.t0, sequential=True)
-    for x, y in zip(spec, seq):
-        assert x.status == y.status and x.n_states == y.n_states and (x.traj == y.traj).all()
-        assert x.plan_id == y.plan_id and x.min_sep_m == y.min_sep_m
+    for budget in (0, 7):  # default slices and tiny slices (many pauses, resumes, rollbacks)
+        a = ctx_for(F, sc, step_budget=budget)
+        spec = a.schedule_batch(sc.src, sc.dst, sc.t0)
+        st = a.stats()
+        for x, y in zip(spec, seq):
+            assert x.status == y.status and x.n_states == y.n_states and (x.traj == y.traj).all()
+            assert x.plan_id == y.plan_id and x.min_sep_m == y.min_sep_m and x.n_near_ties == y.n_near_ties
     assert a.num_plans() == b.num_plans()
     for pid in range(len(sc.plans), a.num_plans()):
         ta, sa = a.get_plan(pid)
