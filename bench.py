@@ -30,7 +30,7 @@ sys.path.insert(0, ROOT)
 METRIC = "FCFS requests scheduled/sec and ms/request vs #accepted plans, 1/2/4/8 B200"
 WORKLOAD = ("configs[1]: batch of 100 FCFS requests against 3000 accepted plans with a 256-well terrain "
             "grid, 16x16 km dense urban airspace, 9 headings x 3 climbs, W=10")
-OPS_PER_PAIR = 13.0 / 3.0  # hot-loop instructions per (state, well) pair at 3 climbs
+OPS_PER_PAIR = 10.0 / 3.0  # FP32 lane-ops per (state, well) pair at 3 climbs
 
 
 def parse():
@@ -264,7 +264,7 @@ def run_native(args):
         "roofline": {"bound": "alu", "achieved": achieved_tops, "peak": peak_tops, "unit": "Top/s",
                      "frac": achieved_tops / peak_tops, "traffic": None,
                      "kernel": "walk_kernel<3>", "ops_per_pair": OPS_PER_PAIR,
-                     "peak_basis": f"148 SM x 128 lanes x {peak_clock:.0f} MHz (MEASURED_PEAKS sm_max_mhz)"},
+                     "peak_basis": f"FP32 pipe: 148 SM x 128 lanes x {peak_clock:.0f} MHz (MEASURED_PEAKS sm_max_mhz)"},
         "e2e": {"value": e2e_value, "unit": "requests/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
         "clocks": clocks,
