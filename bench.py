@@ -246,6 +246,11 @@ def run_native(args):
     except Exception:
         pass
     peak_tops = 148 * 128 * peak_clock * 1e6 / 1e12
+    traffic = None
+    try:  # dram read+write bytes per walk launch from the committed ncu --set full capture
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))["per_launch_bytes"]
+    except Exception:
+        pass
     achieved_tops = pairs * OPS_PER_PAIR / (walk_ms / 1e3) / 1e12 if walk_ms > 0 else 0.0
     if rank != 0:
         return 0
@@ -262,7 +267,8 @@ def run_native(args):
         "pair_evals_per_s": pairs / (tot_ms / 1e3) * world,
         "rounds": stats["rounds"], "reruns": stats["reruns"],
         "roofline": {"bound": "alu", "achieved": achieved_tops, "peak": peak_tops, "unit": "Top/s",
-                     "frac": achieved_tops / peak_tops, "traffic": None,
+                     "frac": achieved_tops / peak_tops, "traffic": traffic,
+                     "traffic_source": "profiles/r01_traffic.json (ncu --set full, bytes per walk launch)",
                      "kernel": "walk_kernel<3>", "ops_per_pair": OPS_PER_PAIR,
                      "peak_basis": f"FP32 pipe: 148 SM x 128 lanes x {peak_clock:.0f} MHz (MEASURED_PEAKS sm_max_mhz)"},
         "e2e": {"value": e2e_value, "unit": "requests/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
