@@ -159,7 +159,7 @@ typedef struct fmdp_stats {
   int32_t walkers;
   int32_t kernels;         /* kernel launches                                             */
   double device_ms;        /* sum of walk-kernel device time (CUDA events)                */
-  int64_t phase_cycles[10]; /* profile=1: CTA-0 cycles per phase: projection, goal/terrain, */
+  int64_t phase_cycles[16]; /* profile=1: CTA-0 cycles per phase: projection, goal/terrain, */
                            /* row wait, hot loop, stage, reduce-scatter, barrier 1,         */
                            /* owner epilogue, barrier 2, decide                             */
 } fmdp_stats;

@@ -14,7 +14,8 @@ constexpr int MAX_AW = 1024;    // projected states per step (A*W)
 constexpr int AMB_MAX = 64;     // ambiguous (state, tau) minima handled per step
 constexpr int TC_MAX = 128;     // terrain-well candidates per step
 constexpr int TW_SMEM = 512;    // terrain wells cached in shared memory (more: read from L2)
-constexpr int N_PHASES = 10;    // walk-kernel phase accounting (fmdp_stats.phase_cycles)
+constexpr int N_PHASES = 16;
+constexpr int PAIR_STRIDE = 36;  // floats per plan-pair record (30 used): 16B-aligned, 2-way banks    // walk-kernel phase accounting (fmdp_stats.phase_cycles)
 
 // Scenario + store in integer units, passed by value to the kernels.
 struct World {
@@ -29,6 +30,7 @@ struct World {
   uint32_t sep2;                // separation minimum^2
   int64_t cap2;                 // goal capture radius^2
   int32_t reach_u;              // bound on |s_{a,t} - q| over all projected states
+  int32_t step_reach_u;         // bound on |Delta_1(a) - q| (one substep)
   double goal_r, goal_l2g;      // goal peak: |r|, log2(gamma) * u  (fp64)
   float intr_r, intr_l2g;       // intruder wells: |r|, log2(gamma) * u (FP32 ex2)
   float terr_r, terr_l2g;       // terrain wells
@@ -45,6 +47,7 @@ struct World {
   int32_t n_tw;
   const int4* tw;               // x, y, z, R (units)
   int32_t nx, ny, x0, y0, cell;
+  uint64_t cell_magic;          // ceil(2^40 / cell): exact floor division for offsets < 2^25
   const int32_t* height;        // [ny][nx] units
   const int2* dxy;              // heading lattice table [HL]
 };
@@ -104,11 +107,11 @@ struct Layout {
     o_dxy = o;  o = al(o + sizeof(int2) * HL);
     o_tw = o;   o = al(o + sizeof(int4) * TW_SMEM);
     o_raw = o;  o = al(o + sizeof(int32_t) * 4 * RAWW * 3);
-    size_t cen = sizeof(float) * 16 * CH;
+    size_t cen = sizeof(float) * PAIR_STRIDE * ((CH + 1) / 2);  // plan-pair well records
     o_cen = o;  o = al(o + cen);
     o_stage = o; o = al(o + sizeof(float) * (size_t)A * BLK);
     o_recv = o; o = al(o + sizeof(float) * 2 * (size_t)G * NOWN * BLK);
-    o_pos = o;  o = al(o + sizeof(int4) * AW);
+    o_pos = o;  o = al(o + sizeof(int4) * 2 * AW);   // double-buffered by step parity
     o_fix = o;  o = al(o + sizeof(double) * AW);
     o_sfix = o; o = al(o + sizeof(double) * AW);
     o_vT = o;   o = al(o + sizeof(float) * AW);
@@ -120,9 +123,9 @@ struct Layout {
     o_flags = o; o = al(o + sizeof(int32_t) * A);
     o_stay = o; o = al(o + sizeof(uint32_t) * 2);
     o_amb = o;  o = al(o + sizeof(int32_t) * AMB_MAX);
-    o_tc = o;   o = al(o + sizeof(int32_t) * TC_MAX);
+    o_tc = o;   o = al(o + sizeof(int32_t) * 2 * TC_MAX);  // candidate lists, by step parity
     o_bar = o;  o = al(o + sizeof(uint64_t) * 4);
-    o_ctl = o;  o = al(o + 256);
+    o_ctl = o;  o = al(o + 512);
     total = o;
   }
 };

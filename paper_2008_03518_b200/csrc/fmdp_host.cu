@@ -761,6 +761,7 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   int maxc = 0;
   for (int c : ctx->climb) maxc = std::max(maxc, std::abs(c));
   w.reach_u = (int32_t)(a.window * ((int64_t)std::ceil(maxd) + maxc) + 1);
+  w.step_reach_u = (int32_t)((int64_t)std::ceil(maxd) + maxc + 1);
   int kmax = 0;
   for (int i = 0; i < a.n_tau; ++i) kmax = std::max(kmax, std::abs(w.k_tau[i]));
   const int64_t vdyn = (int64_t)std::ceil(std::sqrt(maxd * maxd + (double)maxc * maxc));
@@ -827,6 +828,7 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
     w.x0 = ter->x0_u;
     w.y0 = ter->y0_u;
     w.cell = ter->cell_u;
+    w.cell_magic = ((1ULL << 40) + (uint64_t)ter->cell_u - 1) / (uint64_t)ter->cell_u;
     w.height = ctx->d_height;
   }
   ctx->cap_states = a.max_steps + 2;

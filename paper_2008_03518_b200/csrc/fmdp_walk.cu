@@ -107,33 +107,28 @@ __device__ __forceinline__ uint32_t clamp_d2(int dx, int dy, int dz, int rmax, u
   return min(d2, sat);
 }
 
+// Per-step shared control block.  Counters used inside a step are double-buffered by step
+// parity so that no CTA barrier is needed at a step boundary.
 struct Ctl {
   int32_t req;
-  int32_t q[3];
-  int32_t psi;
-  int32_t k;
-  int32_t done;
-  int32_t fin;        // state k is terminal by terrain / goal / timeout (only its separation test remains)
-  int32_t fl;         // terrain (1) / goal (2) flags of state k
-  int32_t namb;
-  int32_t ntc;
-  int32_t n_near;
-  int32_t n_exact;
-  int32_t status;
-  int32_t fail_step;
-  uint32_t min_sep;
-  int32_t steps_run;
+  int32_t fl0;                // terrain (1) / goal (2) flags of the starting state
+  int32_t ntc[2];             // terrain candidate list length, by step parity
+  int32_t namb[2];            // ambiguous (state, tau) count, by step parity
+  uint32_t stay_local[2];     // this CTA's slice minimum of |q - p(K)|^2, by step parity
+  int32_t n_exact;            // exact-fallback count (rank 0 accumulates the cluster's)
+  int32_t pad;
   unsigned long long xmin;
   int32_t sl_lo[3], sl_n[3], sl_off[3];
+  int32_t hgt[MAX_TURN];      // ground height under Delta_1 of every turn (cp.async target)
 };
 
 // Stage row K's slice for this CTA (slots [lo, lo+n) of n_row active slots): the first CH
 // plans go to ring buffer K % 3 with cp.async.bulk (TMA bulk copy), completion on its
 // mbarrier.  Called by one thread.
-__device__ __forceinline__ void issue_row(const World& w, int64_t K, int n_row, unsigned rank, unsigned G, int CH,
+__device__ __forceinline__ void issue_row(const World& w, int64_t K, int n_row, unsigned rank, unsigned lgG, int CH,
                                           int32_t* raw, int RAWW, uint64_t* bars, Ctl* ctl) {
   const int b = (int)(K % 3);
-  const int lo = (int)(((int64_t)n_row * rank) / G), hi = (int)(((int64_t)n_row * (rank + 1)) / G);
+  const int lo = (int)(((uint32_t)n_row * rank) >> lgG), hi = (int)(((uint32_t)n_row * (rank + 1)) >> lgG);
   const int e = min(hi, lo + CH);
   const int lo4 = lo & ~3, e4 = (e + 3) & ~3;
   ctl->sl_lo[b] = lo;
@@ -157,18 +152,29 @@ __device__ __forceinline__ int row_count(const World& w, int64_t K) {
 // Top-2 merge for the argmax (Alg 9): order by value, then lowest index (R13).
 __device__ __forceinline__ bool better(double v, int i, double bv, int bi) { return v > bv || (v == bv && i < bi); }
 
-// Terrain collision height under (x, y) (R16): INT_MIN outside the raster.
-__device__ __forceinline__ int ground_height(const World& w, int x, int y) {
-  if (w.nx <= 0) return INT_MIN;
-  const int64_t rx = (int64_t)x - w.x0, ry = (int64_t)y - w.y0;
-  if (rx < 0 || ry < 0) return INT_MIN;
-  const int64_t ix = rx / w.cell, iy = ry / w.cell;
-  if (ix >= w.nx || iy >= w.ny) return INT_MIN;
-  return __ldg(&w.height[iy * (int64_t)w.nx + ix]);
+// Terrain collision height under (x, y) (R16): INT_MIN outside the raster.  32-bit cell
+// arithmetic (positions span < 2^25 units).
+__device__ __forceinline__ const int32_t* ground_cell(const World& w, int x, int y) {
+  if (w.nx <= 0) return nullptr;
+  const int rx = x - w.x0, ry = y - w.y0;
+  if (rx < 0 || ry < 0) return nullptr;
+  const int ix = (int)(((uint64_t)rx * w.cell_magic) >> 40), iy = (int)(((uint64_t)ry * w.cell_magic) >> 40);
+  if (ix >= w.nx || iy >= w.ny) return nullptr;
+  return w.height + (size_t)iy * w.nx + ix;
 }
+__device__ __forceinline__ int ground_height(const World& w, int x, int y) {
+  const int32_t* p = ground_cell(w, x, y);
+  return p ? __ldg(p) : INT_MIN;
+}
+// 4-byte asynchronous global -> shared copy (LDGSTS); completion by cp.async.wait_all.
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // Per-phase cycle accounting (rank 0, thread 0), enabled when args.prof != nullptr.
-enum Phase { PH_PROJ, PH_FIX, PH_WAIT, PH_HOT, PH_STAGE, PH_SCATTER, PH_BAR1, PH_OWNER, PH_BAR2, PH_DECIDE, PH_N };
+enum Phase { PH_PROJ, PH_FIX, PH_WAIT, PH_HOT, PH_STAGE, PH_SCATTER, PH_BAR1, PH_OWNER, PH_BAR2, PH_DECIDE,
+             PH_TOP, PH_SCAN, PH_PLOOP, PH_BUILD, PH_OWN1, PH_ARGMAX, PH_N };
 
 template <int C>
 __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
@@ -176,6 +182,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   cg::cluster_group cluster = cg::this_cluster();
   const unsigned rank = cluster.block_rank();
   const unsigned G = cluster.num_blocks();
+  const unsigned lgG = 31 - __clz(G);  // G is a power of two
   const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int W = w.W, A = w.A, AW = A * W;
   const int NCOL = w.n_turn * W;
@@ -183,6 +190,8 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   // (a multiple of 8) read the same well record -> shared-memory broadcast
   const int CPW = 32 / NGW;
   const int col = warp * CPW + (lane % CPW), grp = lane / CPW;
+  const int col_it = min(col / W, w.n_turn - 1), col_t = col % W + 1;  // this thread's column
+  const int col_h = w.turn[col_it];
   // actions owned by this CTA (reduce-scatter target and epilogue): a = rank + oa*G
   const int n_own = (A > (int)rank) ? (A - (int)rank + (int)G - 1) / (int)G : 0;
 
@@ -195,7 +204,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   float* s_cen = reinterpret_cast<float*>(smem + L.o_cen);
   float* s_stage = reinterpret_cast<float*>(smem + L.o_stage);
   float* s_recv = reinterpret_cast<float*>(smem + L.o_recv);
-  int4* s_pos = reinterpret_cast<int4*>(smem + L.o_pos);
+  int4* s_pos2 = reinterpret_cast<int4*>(smem + L.o_pos);
   double* s_fix = reinterpret_cast<double*>(smem + L.o_fix);
   double* s_sfix = reinterpret_cast<double*>(smem + L.o_sfix);
   float* s_vT = reinterpret_cast<float*>(smem + L.o_vT);
@@ -206,7 +215,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   int32_t* s_flags = reinterpret_cast<int32_t*>(smem + L.o_flags);
   uint32_t* s_stay = reinterpret_cast<uint32_t*>(smem + L.o_stay);
   int32_t* s_amb = reinterpret_cast<int32_t*>(smem + L.o_amb);
-  int32_t* s_tc = reinterpret_cast<int32_t*>(smem + L.o_tc);
+  int32_t* s_tc2 = reinterpret_cast<int32_t*>(smem + L.o_tc);
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + L.o_bar);
   Ctl* ctl = reinterpret_cast<Ctl*>(smem + L.o_ctl);
   const int RAWW = L.RAWW, BLK = L.BLK, NOWN = L.NOWN;
@@ -247,102 +256,104 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
     if (r >= args.n_reqs) break;
     const Req rq = args.reqs[r];
     const size_t sbase = (size_t)rq.slot * args.cap;
+    // walker state, identical in every thread of every CTA of the cluster
+    int k = rq.start_k;
+    int qx, qy, qz, psi;
+    if (k == 0) {
+      qx = rq.src[0]; qy = rq.src[1]; qz = rq.src[2];
+      psi = rq.psi0;
+    } else {
+      const int32_t* tq = args.traj + 3 * (sbase + k);
+      qx = tq[0]; qy = tq[1]; qz = tq[2];
+      psi = args.heading[sbase + k];
+    }
+    // per-request aggregates, kept by thread 0 of rank 0
+    int n_near = 0, steps_run = 0, status = 0, fail_step = -1;
+    uint32_t min_sep = w.sat_d2;
     if (tid == 0) {
-      const int k0 = rq.start_k;
-      int q0[3], p0;
-      if (k0 == 0) {
-        q0[0] = rq.src[0]; q0[1] = rq.src[1]; q0[2] = rq.src[2];
-        p0 = rq.psi0;
-      } else {
-        const int32_t* tq = args.traj + 3 * (sbase + k0);
-        q0[0] = tq[0]; q0[1] = tq[1]; q0[2] = tq[2];
-        p0 = args.heading[sbase + k0];
-      }
-      ctl->q[0] = q0[0]; ctl->q[1] = q0[1]; ctl->q[2] = q0[2];
-      ctl->psi = p0;
-      ctl->k = k0;
-      ctl->done = 0;
-      // terminal flags of the starting state (terrain, goal; timeout cannot apply: k0 < max_steps)
-      {
-        const int h = ground_height(w, q0[0], q0[1]);
-        const int64_t gx = (int64_t)q0[0] - rq.dst[0], gy = (int64_t)q0[1] - rq.dst[1], gz = (int64_t)q0[2] - rq.dst[2];
-        ctl->fl = ((q0[2] < 0 || q0[2] < h) ? 1 : 0) | ((gx * gx + gy * gy + gz * gz < w.cap2) ? 2 : 0);
-        ctl->fin = (!args.eval && ctl->fl) ? 1 : 0;
-      }
-      ctl->n_near = 0;
+      // terminal flags of the starting state (terrain, goal; timeout cannot apply: k < max_steps)
+      const int h = ground_height(w, qx, qy);
+      const int64_t gx = (int64_t)qx - rq.dst[0], gy = (int64_t)qy - rq.dst[1], gz = (int64_t)qz - rq.dst[2];
+      ctl->fl0 = ((qz < 0 || qz < h) ? 1 : 0) | ((gx * gx + gy * gy + gz * gz < w.cap2) ? 2 : 0);
+      ctl->ntc[0] = ctl->ntc[1] = 0;
+      ctl->namb[0] = ctl->namb[1] = 0;
+      ctl->stay_local[0] = ctl->stay_local[1] = w.sat_d2;
       ctl->n_exact = 0;
-      ctl->status = 0;
-      ctl->fail_step = -1;
-      ctl->steps_run = 0;
-      ctl->min_sep = w.sat_d2;
-      if (rank == 0 && k0 > 0 && !args.eval) {  // resume: aggregates of the kept prefix
-        int nn = 0;
-        uint32_t ms = w.sat_d2;
-        for (int kk = 0; kk < k0; ++kk) {
-          nn += args.ntie[sbase + kk];
-          ms = min(ms, args.stepd2[sbase + kk]);
+      if (rank == 0 && k > 0 && !args.eval) {  // resume: aggregates of the kept prefix
+        for (int kk = 0; kk < k; ++kk) {
+          n_near += args.ntie[sbase + kk];
+          min_sep = min(min_sep, args.stepd2[sbase + kk]);
         }
-        ctl->n_near = nn;
-        ctl->min_sep = ms;
       }
-      if (rank == 0 && k0 == 0 && !args.eval) {
+      if (rank == 0 && k == 0 && !args.eval) {
         int32_t* tq = args.traj + 3 * sbase;
         tq[0] = rq.src[0]; tq[1] = rq.src[1]; tq[2] = rq.src[2];
         args.heading[sbase] = rq.psi0;
       }
-      const int64_t K0 = rq.t0 + k0;
+      const int64_t K0 = rq.t0 + k;
       const int n0 = row_count(w, K0), n1 = row_count(w, K0 + 1);
       cnt2 = row_count(w, K0 + 2);
-      issue_row(w, K0, n0, rank, G, CH, s_raw, RAWW, s_bar, ctl);
-      issue_row(w, K0 + 1, n1, rank, G, CH, s_raw, RAWW, s_bar, ctl);
+      issue_row(w, K0, n0, rank, lgG, CH, s_raw, RAWW, s_bar, ctl);
+      issue_row(w, K0 + 1, n1, rank, lgG, CH, s_raw, RAWW, s_bar, ctl);
       s_stay[0] = w.sat_d2;
       s_stay[1] = w.sat_d2;
     }
     {
-      const int64_t K0 = rq.t0 + rq.start_k;
+      const int64_t K0 = rq.t0 + k;
       pending |= (1u << (K0 % 3)) | (1u << ((K0 + 1) % 3));
     }
+    __syncthreads();
+    // terrain candidates for the first step (exact cull: wells that can reach a projected state)
+    for (int i = tid; i < w.n_tw; i += NT) {
+      const int4 t = tw[i];
+      const int64_t dx = t.x - qx, dy = t.y - qy, dz = t.z - qz;
+      const int64_t rr = (int64_t)t.w + w.reach_u;
+      if (dx * dx + dy * dy + dz * dz < rr * rr) {
+        const int slot = atomicAdd(&ctl->ntc[k & 1], 1);
+        if (slot < TC_MAX) s_tc2[(k & 1) * TC_MAX + slot] = i;
+      }
+    }
+    int fl = ctl->fl0;
+    bool fin = !args.eval && fl != 0;  // only the separation test of state k remains
     cluster.sync();
 
     // ------------------------------------------------------------ step loop
     for (;;) {
       if (prof) tmark = clock64();
-      const int k = ctl->k;
       const int64_t K = rq.t0 + k;
-      const int qx = ctl->q[0], qy = ctl->q[1], qz = ctl->q[2], psi = ctl->psi;
-      const bool fin = ctl->fin != 0;  // only the separation test of state k remains
+      const int p = k & 1;
       const int bK = (int)(K % 3), bK2 = (int)((K + 2) % 3);
-      if (tid == 0) {
-        if (!args.eval && !fin) {
-          issue_row(w, K + 2, cnt2, rank, G, CH, s_raw, RAWW, s_bar, ctl);
-          cnt2 = row_count(w, K + 3);  // consumed next step: latency hidden by this step
-        }
-        ctl->namb = 0;
-        ctl->ntc = 0;
-        s_stay[(k + 1) & 1] = w.sat_d2;  // written remotely in step k+1 (after both barriers of k)
+      int4* s_pos = s_pos2 + p * AW;
+      if (tid == 0 && !args.eval && !fin) {
+        issue_row(w, K + 2, cnt2, rank, lgG, CH, s_raw, RAWW, s_bar, ctl);
+        cnt2 = row_count(w, K + 3);  // consumed next step: latency hidden by this step
       }
       if (!args.eval && !fin) pending |= 1u << bK2;
-      __syncthreads();
+      FMDP_MARK(PH_TOP)
 
       float sx = 0.f, sy = 0.f, sz[C];
       f2 sx2 = 0, sy2 = 0, sz2[C];
 #pragma unroll
       for (int c = 0; c < C; ++c) sz2[c] = 0;
-      int hgt = INT_MIN, x1 = 0, y1 = 0;  // ground under Delta_1 (t = 1 columns, group 0)
+      int x1 = 0, y1 = 0;  // Delta_1 of this turn (t = 1 columns, group 0)
       if (!fin) {
-        // ---- a5 candidates: terrain wells that can reach any projected state (exact cull)
-        for (int i = tid; i < w.n_tw; i += NT) {
-          const int4 t = tw[i];
-          const int64_t dx = t.x - qx, dy = t.y - qy, dz = t.z - qz;
-          const int64_t rr = (int64_t)t.w + w.reach_u;
-          if (dx * dx + dy * dy + dz * dz < rr * rr) {
-            const int slot = atomicAdd(&ctl->ntc, 1);
-            if (slot < TC_MAX) s_tc[slot] = i;
+        // ---- a5 candidates for step k+1: radius enlarged by one substep, so the list is an
+        //      exact superset for whichever next state the decision picks
+        {
+          const int64_t grow = (int64_t)w.reach_u + w.step_reach_u;
+          for (int i = tid; i < w.n_tw; i += NT) {
+            const int4 t = tw[i];
+            const int64_t dx = t.x - qx, dy = t.y - qy, dz = t.z - qz;
+            const int64_t rr = (int64_t)t.w + grow;
+            if (dx * dx + dy * dy + dz * dz < rr * rr) {
+              const int slot = atomicAdd(&ctl->ntc[p ^ 1], 1);
+              if (slot < TC_MAX) s_tc2[(p ^ 1) * TC_MAX + slot] = i;
+            }
           }
         }
+        FMDP_MARK(PH_SCAN)
         // ---- a2 forward projection (Alg 3): column (turn it, substep t) on the integer lattice
-        const int it = min(col / W, w.n_turn - 1), t = col % W + 1;
-        const int h = w.turn[it];
+        const int it = col_it, t = col_t, h = col_h;
         int x = qx, y = qy, ps = psi;
         for (int s = 1; s <= t; ++s) {
           ps += h;
@@ -362,27 +373,31 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         if (grp == 0 && col < NCOL) {
 #pragma unroll
           for (int c = 0; c < C; ++c) s_pos[(it * C + c) * W + (t - 1)] = make_int4(x, y, qz + w.climb[c] * t, ps);
-          if (t == 1) {  // raster load issued now, consumed after the hot loop
-            hgt = ground_height(w, x, y);
+          if (t == 1) {  // raster load in flight during the hot loop (LDGSTS), consumed after it
+            const int32_t* cell = ground_cell(w, x, y);
+            if (cell) cp_async4(&ctl->hgt[it], cell);
+            else ctl->hgt[it] = INT_MIN;
             x1 = x;
             y1 = y;
           }
         }
+        FMDP_MARK(PH_PLOOP)
         __syncthreads();
         FMDP_MARK(PH_PROJ)
         // ---- a3 goal (fp64), deck, a5 terrain (exact predicate, FP32 ex2 value): owned states
-        const int ntc = ctl->ntc;
+        const int ntc = ctl->ntc[p];
+        const int32_t* s_tc = s_tc2 + p * TC_MAX;
         for (int i = tid; i < n_own * W; i += NT) {
           const int st = ((int)rank + (i / W) * (int)G) * W + i % W;
-          const int4 p = s_pos[st];
-          const int64_t gx = (int64_t)p.x - rq.dst[0], gy = (int64_t)p.y - rq.dst[1], gz = (int64_t)p.z - rq.dst[2];
-          const double vpos = w.goal_r * exp2(w.goal_l2g * sqrt((double)(gx * gx + gy * gy + gz * gz)));
-          const double valt = (p.z < w.zdeck_u) ? (w.deck_scale - w.u_m * (double)p.z) : 0.0;
+          const int4 q4 = s_pos[st];
+          const double gx = (double)q4.x - rq.dst[0], gy = (double)q4.y - rq.dst[1], gz = (double)q4.z - rq.dst[2];
+          const double vpos = w.goal_r * exp2(w.goal_l2g * sqrt(gx * gx + gy * gy + gz * gz));
+          const double valt = (q4.z < w.zdeck_u) ? (w.deck_scale - w.u_m * (double)q4.z) : 0.0;
           int64_t mT = INT64_MAX;
           const int nt = ntc <= TC_MAX ? ntc : w.n_tw;
           for (int c = 0; c < nt; ++c) {
             const int4 t4 = tw[ntc <= TC_MAX ? s_tc[c] : c];
-            const int64_t dx = p.x - t4.x, dy = p.y - t4.y, dz = p.z - t4.z;
+            const int64_t dx = q4.x - t4.x, dy = q4.y - t4.y, dz = q4.z - t4.z;
             const int64_t d2 = dx * dx + dy * dy + dz * dz;
             if (d2 < (int64_t)t4.w * t4.w && d2 < mT) mT = d2;
           }
@@ -424,9 +439,9 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
             if (fin) continue;
             const uint32_t pv = (uint32_t)V[j];
             const int vx = sext(pv, 11), vy = sext(pv >> 11, 11), vz = sext(pv >> 22, 10);
-            // plan pair layout: [pair][tau][x_j, x_j', y_j, y_j', z_j, z_j'] (+2 pad), negated
+            // plan pair layout: [pair][tau][x_j, x_j', y_j, y_j', z_j, z_j'] (+6 pad), negated
             // offsets so that s - c is one packed add; exact integers < 2^24 (R23)
-            float* cp = s_cen + 32 * (j >> 1) + (j & 1);
+            float* cp = s_cen + PAIR_STRIDE * (j >> 1) + (j & 1);
 #pragma unroll
             for (int t = 0; t < NTAU; ++t) {
               cp[6 * t + 0] = (float)(-(rx + w.k_tau[t] * vx));
@@ -435,11 +450,12 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
             }
           }
           if (!fin && (nc & 1) && tid == 0) {  // odd tail: the partner slot is a well at infinity
-            float* cp = s_cen + 32 * (nc >> 1) + 1;
+            float* cp = s_cen + PAIR_STRIDE * (nc >> 1) + 1;
 #pragma unroll
             for (int t = 0; t < NTAU; ++t) cp[6 * t + 0] = cp[6 * t + 2] = cp[6 * t + 4] = 3.0e18f;
           }
           if (fin) continue;
+          FMDP_MARK(PH_BUILD)
           __syncthreads();
           const ulonglong2* cen2 = reinterpret_cast<const ulonglong2*>(s_cen);
           // (state, well) pair: |s - c|^2 = (dx^2 + dy^2) + dz^2, the horizontal part shared by
@@ -455,7 +471,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   }
           const int np = (nc + 1) >> 1;
           for (int pp = grp; pp < np; pp += NGW) {
-            const ulonglong2* c8 = cen2 + 8 * pp;
+            const ulonglong2* c8 = cen2 + (PAIR_STRIDE / 4) * pp;
             const ulonglong2 e0 = c8[0], e1 = c8[1], e2 = c8[2], e3 = c8[3], e4 = c8[4], e5 = c8[5], e6 = c8[6],
                              e7 = c8[7];
             FMDP_WELL2(0, e0.x, e0.y, e1.x)
@@ -470,17 +486,19 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         }
         if (!fin && tid == 0 && args.pairs) atomicAdd(args.pairs, (unsigned long long)n * NTAU * AW);
       }
-      // stay: slice minimum of |q - p(K)|^2 -> every CTA (terminal separation test, Sec IV.I)
+      if (tid == 0 && !fin) ctl->ntc[p] = 0;  // list of step k consumed (FIX precedes the syncs above)
+      // stay: slice minimum of |q - p(K)|^2 (terminal separation test of state k, Sec IV.I)
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) stay = min(stay, __shfl_xor_sync(0xffffffffu, stay, o));
-      if (lane == 0 && stay < w.sat_d2)
-        for (unsigned b = 0; b < G; ++b) atomicMin(cluster.map_shared_rank(&s_stay[k & 1], b), stay);
+      if (lane == 0 && stay < w.sat_d2) atomicMin(&ctl->stay_local[p], stay);
       FMDP_MARK(PH_HOT)
 
       if (!fin) {
         // terrain / goal flags of every action's Delta_1 (the candidate next state)
         if (grp == 0 && col < NCOL && col % W == 0) {
           const int it = col / W;
+          cp_async_wait_all();
+          const int hgt = ctl->hgt[it];
 #pragma unroll
           for (int c = 0; c < C; ++c) {
             const int z = qz + w.climb[c];
@@ -502,17 +520,24 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
             for (int t = 0; t < NTAU; ++t) s_stage[(it * C + c) * BLK + t1 * NTAU + t] = m[c][t];
         }
         FMDP_MARK(PH_STAGE)
-        __syncthreads();
-        // reduce-scatter: float4 DSMEM stores of each action block into slot [rank] of its owner
-        {
-          const int par_off = (k & 1) * (int)G * NOWN * BLK;
-          const int nv = BLK / 4;
-          for (int i = tid; i < A * nv; i += NT) {
-            const int a = i / nv, e = i % nv;
-            float4* dst = reinterpret_cast<float4*>(cluster.map_shared_rank(s_recv, a % (int)G) + par_off +
-                                                    ((int)rank * NOWN + a / (int)G) * BLK);
-            dst[e] = reinterpret_cast<const float4*>(s_stage + a * BLK)[e];
-          }
+      }
+      __syncthreads();
+      if (tid == 0) {  // step k+1's counters: every warp has left step k-1 (this barrier)
+        ctl->namb[p ^ 1] = 0;
+        ctl->stay_local[p ^ 1] = w.sat_d2;
+        s_stay[p ^ 1] = w.sat_d2;  // written remotely in step k+1, after the cluster barriers of k
+      }
+      // slice separation minimum -> every CTA; reduce-scatter of the per-action blocks
+      if (tid < (int)G && ctl->stay_local[p] < w.sat_d2)
+        atomicMin(cluster.map_shared_rank(&s_stay[p], tid), ctl->stay_local[p]);
+      if (!fin) {
+        const int par_off = p * (int)G * NOWN * BLK;
+        const int nv = BLK / 4;
+        for (int i = tid; i < A * nv; i += NT) {
+          const int a = i / nv, e = i % nv;
+          float4* dst = reinterpret_cast<float4*>(cluster.map_shared_rank(s_recv, a % (int)G) + par_off +
+                                                  ((int)rank * NOWN + a / (int)G) * BLK);
+          dst[e] = reinterpret_cast<const float4*>(s_stage + a * BLK)[e];
         }
         FMDP_MARK(PH_SCATTER)
       }
@@ -520,27 +545,9 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       FMDP_MARK(PH_BAR1)
 
       if (!fin) {
-        // ---- owner epilogue (half-warp per owned action, lane = substep): reduce the G
-        //      partial blocks, exact in/out, values (Alg 8), V*(a)
-        const float* rcv = s_recv + (k & 1) * (int)G * NOWN * BLK;
-        // (1) global minimum of every owned (state, tau) over the G partial blocks, all threads
-        float* s_min = s_stage;  // free after barrier 1: [oa][t*NTAU + tau]
-        {
-          const int WT = W * NTAU;
-          for (int e = tid; e < n_own * WT; e += NT) {
-            const int oa = e / WT, rem = e - oa * WT;
-            const float* src = rcv + oa * BLK + rem;
-            float M0 = FLT_MAX, M1 = FLT_MAX;
-            int b = 0;
-            for (; b + 1 < (int)G; b += 2) {
-              M0 = fminf(M0, src[b * NOWN * BLK]);
-              M1 = fminf(M1, src[(b + 1) * NOWN * BLK]);
-            }
-            if (b < (int)G) M0 = fminf(M0, src[b * NOWN * BLK]);
-            s_min[e] = fminf(M0, M1);
-          }
-        }
-        __syncthreads();
+        // ---- owner epilogue (half-warp per owned action, lane = substep): G-way minimum of
+        //      the partial blocks, exact in/out, values (Alg 8), V*(a)
+        const float* rcv = s_recv + p * (int)G * NOWN * BLK;
         const int hw = tid >> 4, hl = tid & 15;
         const int n_hw = NT >> 4;
         for (int oa0 = 0; oa0 < NOWN; oa0 += n_hw) {  // uniform trip count across the CTA
@@ -551,23 +558,43 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           float mi = FLT_MAX;
           int amb = 0;
           if (act) {
+            const float* src = rcv + oa * BLK + hl * NTAU;
+            const int sstride = NOWN * BLK;
+            float M[NTAU], M1[NTAU], M2[NTAU], M3[NTAU];
+#pragma unroll
+            for (int t = 0; t < NTAU; ++t) M[t] = M1[t] = M2[t] = M3[t] = src[t];
+            int b = 1;
+            for (; b + 3 < (int)G; b += 4) {  // four independent load streams
+#pragma unroll
+              for (int t = 0; t < NTAU; ++t) {
+                M[t] = fminf(M[t], src[b * sstride + t]);
+                M1[t] = fminf(M1[t], src[(b + 1) * sstride + t]);
+                M2[t] = fminf(M2[t], src[(b + 2) * sstride + t]);
+                M3[t] = fminf(M3[t], src[(b + 3) * sstride + t]);
+              }
+            }
+            for (; b < (int)G; ++b)
+#pragma unroll
+              for (int t = 0; t < NTAU; ++t) M[t] = fminf(M[t], src[b * sstride + t]);
+#pragma unroll
+            for (int t = 0; t < NTAU; ++t) M[t] = fminf(fminf(M[t], M1[t]), fminf(M2[t], M3[t]));
 #pragma unroll
             for (int t = 0; t < NTAU; ++t) {
-              const float M = s_min[oa * W * NTAU + hl * NTAU + t];
-              if (M < w.R2lo[t]) {
-                mi = fminf(mi, M);
-              } else if (M <= w.R2hi[t]) {  // inside the 2^-20 band: decided exactly below
+              if (M[t] < w.R2lo[t]) {
+                mi = fminf(mi, M[t]);
+              } else if (M[t] <= w.R2hi[t]) {  // inside the 2^-20 band: decided exactly below
                 amb = 1;
-                const int idx = atomicAdd(&ctl->namb, 1);
+                const int idx = atomicAdd(&ctl->namb[p], 1);
                 if (idx < AMB_MAX) s_amb[idx] = st * NTAU + t;
               }
             }
             s_mI[st] = mi;
           }
+          FMDP_MARK(PH_OWN1)
           if (__syncthreads_or(amb)) {
             // Exact fallback: min over the WHOLE row K of the int64 d^2 for each flagged
             // (state, tau); each CTA resolves its own states (rare).
-            const int namb = ctl->namb;
+            const int namb = ctl->namb[p];
             const int nK = row_count(w, K);
             const int32_t* rowg = w.rows + (size_t)K * 4 * w.row_cap;
             const int nitems = namb <= AMB_MAX ? namb : n_hw * W * NTAU;
@@ -578,21 +605,22 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
               } else {  // overflow: walk every owned (state, tau) of this pass, re-test the band
                 const int oa2 = oa0 + it2 / (W * NTAU), rem = it2 % (W * NTAU), l2 = rem / NTAU, t = rem % NTAU;
                 if (oa2 >= n_own) continue;
-                const float M = s_min[oa2 * W * NTAU + l2 * NTAU + t];
+                float M = FLT_MAX;
+                for (int b = 0; b < (int)G; ++b) M = fminf(M, rcv[(b * NOWN + oa2) * BLK + l2 * NTAU + t]);
                 if (!(M >= w.R2lo[t] && M <= w.R2hi[t])) continue;
                 item = (((int)rank + oa2 * (int)G) * W + l2) * NTAU + t;
               }
               const int sti = item / NTAU, t = item % NTAU;
               if (tid == 0) ctl->xmin = ULLONG_MAX;
               __syncthreads();
-              const int4 p = s_pos[sti];
+              const int4 q4 = s_pos[sti];
               unsigned long long best = ULLONG_MAX;
               for (int j = tid; j < nK; j += NT) {
                 const uint32_t pv = (uint32_t)rowg[3 * w.row_cap + j];
                 const int64_t cx = rowg[j] + (int64_t)w.k_tau[t] * sext(pv, 11);
                 const int64_t cy = rowg[w.row_cap + j] + (int64_t)w.k_tau[t] * sext(pv >> 11, 11);
                 const int64_t cz = rowg[2 * w.row_cap + j] + (int64_t)w.k_tau[t] * sext(pv >> 22, 10);
-                const int64_t dx = p.x - cx, dy = p.y - cy, dz = p.z - cz;
+                const int64_t dx = q4.x - cx, dy = q4.y - cy, dz = q4.z - cz;
                 best = min(best, (unsigned long long)(dx * dx + dy * dy + dz * dz));
               }
               for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
@@ -605,7 +633,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
               }
               __syncthreads();
             }
-            if (tid == 0) ctl->namb = 0;
+            if (tid == 0) ctl->namb[p] = 0;
             if (act) mi = s_mI[st];
             __syncthreads();
           }
@@ -651,12 +679,24 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         FMDP_MARK(PH_BAR2)
       }
 
-      // ---- a7/a8 (every CTA, identical inputs -> identical decisions)
-      if (warp == 0) {
-        double v1 = -INFINITY, v2 = -INFINITY;  // a7: top-2 (lowest index on ties)
-        int a1 = INT_MAX, a2 = INT_MAX;
-        if (!fin) {
-          // lane l scans a = l, l+32, ... in increasing order; merge lanes with shuffles
+      // ---- a7/a8: every warp decides redundantly (identical inputs -> identical decisions),
+      //      so no barrier is needed before the next step
+      double v1 = -INFINITY, v2 = -INFINITY;
+      int a1 = INT_MAX, a2 = INT_MAX;
+      if (!fin) {
+        if (A <= 32) {
+          // rank of action `lane` = number of actions better than it (value, then lower index);
+          // a* has rank 0, the runner-up rank 1 (Alg 9, R13)
+          const double mine = lane < A ? s_vstar[lane] : -INFINITY;
+          int rk = 0;
+          for (int a = 0; a < A; ++a) rk += better(s_vstar[a], a, mine, lane) ? 1 : 0;
+          const unsigned b0 = __ballot_sync(0xffffffffu, lane < A && rk == 0);
+          const unsigned b1 = __ballot_sync(0xffffffffu, lane < A && rk == 1);
+          a1 = __ffs(b0) - 1;
+          a2 = b1 ? __ffs(b1) - 1 : INT_MAX;
+          v1 = s_vstar[a1];
+          v2 = b1 ? s_vstar[a2] : -INFINITY;
+        } else {
           for (int a = lane; a < A; a += 32) {
             const double v = s_vstar[a];
             if (better(v, a, v1, a1)) {
@@ -665,10 +705,8 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
               v2 = v; a2 = a;
             }
           }
-          const int span = A < 32 ? A : 32;  // lanes >= span hold nothing
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) {
-            if (o >= span) continue;  // uniform: skip rounds that only merge empty lanes
             const double ov1 = __shfl_xor_sync(0xffffffffu, v1, o), ov2 = __shfl_xor_sync(0xffffffffu, v2, o);
             const int oa1 = __shfl_xor_sync(0xffffffffu, a1, o), oa2 = __shfl_xor_sync(0xffffffffu, a2, o);
             if (better(ov1, oa1, v1, a1)) {
@@ -679,64 +717,62 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
             }
           }
         }
-        if (lane == 0) {
-          const uint32_t c0 = s_stay[k & 1];
-          if (args.eval) {
-            if (rank == 0) {
-              args.dbg_conf[A] = c0;
-              args.dbg_astar[0] = a1;
-            }
-            ctl->done = 1;
-          } else {
-            ctl->min_sep = min(ctl->min_sep, c0);
-            if (rank == 0) args.stepd2[sbase + k] = c0;
-            // Determine terminal state of state k (Sec IV.I): conflict, terrain, goal, timeout
-            int st = -1;
-            if (c0 < w.sep2) st = 1;
-            else if (ctl->fl & 1) st = 2;
-            else if (ctl->fl & 2) st = 0;
-            else if (k >= w.max_steps) st = 3;
-            if (st >= 0) {
-              ctl->status = st;
-              ctl->fail_step = st == 0 ? -1 : k;
-              ctl->done = 1;
-            } else {
-              const bool near = (A > 1) && (v1 - v2 < w.near_tie_rel * s_vsc[a1]);
-              if (rank == 0) {
-                args.astar[sbase + k] = a1;
-                args.ntie[sbase + k] = near ? 1 : 0;
-              }
-              ctl->n_near += near ? 1 : 0;
-              const int4 p1 = s_pos[a1 * W + 0];  // s_{t+1} <- Delta_1[a*] (Alg 1)
-              const int k1 = k + 1;
-              ctl->q[0] = p1.x; ctl->q[1] = p1.y; ctl->q[2] = p1.z;
-              ctl->psi = p1.w;
-              ctl->k = k1;
-              ctl->steps_run += 1;
-              ctl->fl = s_flags[a1];
-              ctl->fin = (ctl->fl != 0 || k1 >= w.max_steps) ? 1 : 0;
-              if (rank == 0) {
-                int32_t* tq = args.traj + 3 * (sbase + k1);
-                tq[0] = p1.x; tq[1] = p1.y; tq[2] = p1.z;
-                args.heading[sbase + k1] = p1.w;
-              }
-              if (k1 - rq.start_k >= args.budget) {  // step budget spent: pause at state k1
-                ctl->status = -1;
-                ctl->done = 1;
-              }
-            }
+      }
+      FMDP_MARK(PH_ARGMAX)
+      const uint32_t c0 = s_stay[p];
+      bool done = false;
+      if (args.eval) {
+        if (rank == 0 && tid == 0) {
+          args.dbg_conf[A] = c0;
+          args.dbg_astar[0] = a1;
+        }
+        done = true;
+      } else {
+        if (rank == 0 && tid == 0) args.stepd2[sbase + k] = c0;
+        min_sep = min(min_sep, c0);
+        // Determine terminal state of state k (Sec IV.I): conflict, terrain, goal, timeout
+        int st = -1;
+        if (c0 < w.sep2) st = 1;
+        else if (fl & 1) st = 2;
+        else if (fl & 2) st = 0;
+        else if (k >= w.max_steps) st = 3;
+        if (st >= 0) {
+          status = st;
+          fail_step = st == 0 ? -1 : k;
+          done = true;
+        } else {
+          const bool near = (A > 1) && (v1 - v2 < w.near_tie_rel * s_vsc[a1]);
+          const int4 p1 = s_pos[a1 * W + 0];  // s_{t+1} <- Delta_1[a*] (Alg 1)
+          if (rank == 0 && tid == 0) {
+            args.astar[sbase + k] = a1;
+            args.ntie[sbase + k] = near ? 1 : 0;
+            int32_t* tq = args.traj + 3 * (sbase + k + 1);
+            tq[0] = p1.x; tq[1] = p1.y; tq[2] = p1.z;
+            args.heading[sbase + k + 1] = p1.w;
+          }
+          n_near += near ? 1 : 0;
+          steps_run += 1;
+          k += 1;
+          qx = p1.x; qy = p1.y; qz = p1.z;
+          psi = p1.w;
+          fl = s_flags[a1];
+          fin = fl != 0 || k >= w.max_steps;
+          if (k - rq.start_k >= args.budget) {  // step budget spent: pause at state k
+            status = -1;
+            done = true;
           }
         }
       }
-      __syncthreads();
       FMDP_MARK(PH_DECIDE)
-      if (ctl->done) break;
+      if (done) break;
     }
 
     // eval only: separation minimum of every action's Delta_1 vs the whole row K+1 (debug hook)
     if (args.eval && rank == 0) {
+      __syncthreads();
       for (int a = tid; a < A; a += NT) s_conf[a] = w.sat_d2;
       __syncthreads();
+      const int4* s_pos = s_pos2 + (k & 1) * AW;
       const int64_t K1 = rq.t0 + 1;
       const int n1 = row_count(w, K1);
       const int32_t* rowg = w.rows + (size_t)K1 * 4 * w.row_cap;
@@ -755,13 +791,13 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
     cluster.sync();  // n_exact contributions of every CTA have landed in rank 0
     if (rank == 0 && tid == 0 && !args.eval) {
       Out o;
-      o.status = ctl->status;
-      o.n_states = ctl->k + 1;
-      o.fail_step = ctl->fail_step;
-      o.n_near_ties = ctl->n_near;
+      o.status = status;
+      o.n_states = k + 1;
+      o.fail_step = fail_step;
+      o.n_near_ties = n_near;
       o.n_exact = ctl->n_exact;
-      o.steps_run = ctl->steps_run;
-      o.min_sep_d2 = ctl->min_sep;
+      o.steps_run = steps_run;
+      o.min_sep_d2 = min_sep;
       o.pad = 0;
       args.out[rq.slot] = o;
     }

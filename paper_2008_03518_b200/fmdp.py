@@ -81,10 +81,10 @@ class Result(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("steps", C.c_int64), ("pair_evals", C.c_int64), ("rounds", C.c_int32), ("reruns", C.c_int32),
                 ("cluster_size", C.c_int32), ("walkers", C.c_int32), ("kernels", C.c_int32),
-                ("device_ms", C.c_double), ("phase_cycles", C.c_int64 * 10)]
+                ("device_ms", C.c_double), ("phase_cycles", C.c_int64 * 16)]
 
 PHASES = ("projection", "goal_terrain", "row_wait", "hot_loop", "stage", "reduce_scatter", "barrier1",
-          "owner_epilogue", "barrier2", "decide")
+          "owner_epilogue", "barrier2", "decide", "top", "tscan", "proj_loop", "build", "own_classify", "argmax")
 
 
 EXPORTS = ["fmdp_airspace_default", "fmdp_create", "fmdp_destroy", "fmdp_set_launch", "fmdp_add_plan",

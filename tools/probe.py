@@ -10,7 +10,7 @@ ctx = FMDP(sc.airspace, sc.terrain)
 t = time.time(); ctx.add_plans(sc.plans); print('load', round(time.time() - t, 3), flush=True)
 n0 = ctx.num_plans()
 i = 2
-for G in (16, 8, 4, 2, 1):
+for G in (16, 1):
     ctx.set_launch(cluster_size=G, profile=1)
     t = time.time(); r = ctx.schedule(sc.src[i], sc.dst[i], int(sc.t0[i])); dt = time.time() - t
     st = ctx.stats(); ctx.truncate(n0)
