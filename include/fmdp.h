@@ -129,6 +129,8 @@ typedef struct fmdp_launch {
   int32_t threads;        /* threads per CTA, 0 = auto                                   */
   int32_t profile;        /* 1: accumulate per-phase cycles of CTA 0 (fmdp_stats)        */
   int32_t step_budget;    /* batch: decision steps per trajectory per launch slice, 0 = 256 */
+  int32_t cull;           /* 1: SURVEY f1 exact culling -- skip plans none of whose wells can */
+                          /* reach a projected state (outputs bit-identical)               */
 } fmdp_launch;
 
 typedef struct fmdp_request {
@@ -159,7 +161,7 @@ typedef struct fmdp_stats {
   int32_t walkers;
   int32_t kernels;         /* kernel launches                                             */
   double device_ms;        /* sum of walk-kernel device time (CUDA events)                */
-  int64_t phase_cycles[16]; /* profile=1: CTA-0 cycles per phase: projection, goal/terrain, */
+  int64_t phase_cycles[17]; /* profile=1: CTA-0 cycles per phase: projection, goal/terrain, */
                            /* row wait, hot loop, stage, reduce-scatter, barrier 1,         */
                            /* owner epilogue, barrier 2, decide                             */
 } fmdp_stats;

@@ -14,7 +14,7 @@ constexpr int MAX_AW = 1024;    // projected states per step (A*W)
 constexpr int AMB_MAX = 64;     // ambiguous (state, tau) minima handled per step
 constexpr int TC_MAX = 128;     // terrain-well candidates per step
 constexpr int TW_SMEM = 512;    // terrain wells cached in shared memory (more: read from L2)
-constexpr int N_PHASES = 16;
+constexpr int N_PHASES = 17;
 constexpr int PAIR_STRIDE = 36;  // floats per plan-pair record (30 used): 16B-aligned, 2-way banks    // walk-kernel phase accounting (fmdp_stats.phase_cycles)
 
 // Scenario + store in integer units, passed by value to the kernels.
@@ -24,6 +24,9 @@ struct World {
   int32_t climb[MAX_CLIMB];
   int32_t k_tau[NTAU];          // tau / dt substeps (padding taus: k = 0, R2 = 0)
   int64_t R2_tau[NTAU];         // exact R_tau^2, units^2
+  float cull2f_tau[NTAU];       // (R_tau + reach + 1)^2 (1 + 2^-16): conservative FP32 f1 cull threshold
+  int32_t cull_inf;             // R_max + reach + 1: f1 L-inf prefilter radius
+  int32_t k_absmax;             // max |tau/dt|
   float R2lo[NTAU], R2hi[NTAU]; // FP32 filter band R^2 (1 -/+ 2^-20)
   int32_t R_max;                // max tau radius, units (< 2^15)
   uint32_t sat_d2;              // R_max^2: saturation of separation minima
@@ -82,6 +85,7 @@ struct WalkArgs {
   int32_t cap;
   int32_t eval;                 // 1: evaluate one step (debug outputs), no advance
   int32_t budget;               // decision steps per request in this launch (then pause, status -1)
+  int32_t cull;                 // 1: f1 exact culling of plans whose wells cannot reach the states
   double* dbg_vstar;            // [A]
   double* dbg_v;                // [A*W]
   double* dbg_s;                // [A*W]
@@ -94,15 +98,15 @@ struct WalkArgs {
 // Shared-memory carve-up, identical on host (size) and device (offsets).
 //   BLK: per-action block of the reduce-scatter = W*NTAU (state, tau) minima, padded to float4.
 struct Layout {
-  int HL, CH, NT, C, NCOL, A, AW, G, BLK, NOWN, RAWW;
+  int HL, CH, RAWCAP, NT, C, NCOL, A, AW, G, BLK, NOWN, RAWW;
   size_t o_dxy, o_tw, o_raw, o_cen, o_stage, o_recv, o_pos, o_fix, o_sfix, o_vT, o_mI, o_vstar, o_vsc, o_conf,
       o_confg, o_flags, o_stay, o_amb, o_tc, o_bar, o_ctl, total;
   __host__ __device__ static size_t al(size_t x) { return (x + 15) & ~size_t(15); }
-  __host__ __device__ void build(int hl, int ch, int nt, int c, int ncol, int a, int aw, int g) {
-    HL = hl; CH = ch; NT = nt; C = c; NCOL = ncol; A = a; AW = aw; G = g;
+  __host__ __device__ void build(int hl, int ch, int rawcap, int nt, int c, int ncol, int a, int aw, int g) {
+    HL = hl; CH = ch; RAWCAP = rawcap; NT = nt; C = c; NCOL = ncol; A = a; AW = aw; G = g;
     BLK = ((AW / A) * NTAU + 3) & ~3;
     NOWN = (A + G - 1) / G;             // max actions owned by one CTA
-    RAWW = CH + 8;                      // words per SoA array in one raw row buffer
+    RAWW = RAWCAP + 8;                  // words per SoA array in one raw row buffer
     size_t o = 0;
     o_dxy = o;  o = al(o + sizeof(int2) * HL);
     o_tw = o;   o = al(o + sizeof(int4) * TW_SMEM);
@@ -144,12 +148,12 @@ struct InflPair {
 
 // Kernel launchers (fmdp_walk.cu).
 cudaError_t launch_walk(const World& w, const WalkArgs& a, int n_climb, int cluster, int n_clusters,
-                        int threads, int chunk, cudaStream_t s);
+                        int threads, int chunk, int rawcap, cudaStream_t s);
 // Hot-loop thread mapping: warps of 32/ngw columns x ngw plan groups; threads = 32*warps.
 int walk_groups_per_warp(int ncol, int max_threads);
 int walk_threads(int ncol, int max_threads);
-cudaError_t walk_max_clusters(const World& w, int n_climb, int cluster, int threads, int chunk, int* out);
-size_t walk_smem_bytes(const World& w, int n_climb, int threads, int chunk, int cluster);
+cudaError_t walk_max_clusters(const World& w, int n_climb, int cluster, int threads, int chunk, int rawcap, int* out);
+size_t walk_smem_bytes(const World& w, int n_climb, int threads, int chunk, int rawcap, int cluster);
 cudaError_t launch_append(int32_t* rows, int32_t row_cap, int64_t horizon, const AppendPlan* plans, int n_plans,
                           int max_n, cudaStream_t s);
 cudaError_t launch_influence(const int32_t* traj, int32_t cap, const int32_t* n_states, const int64_t* t0,

@@ -215,12 +215,27 @@ int threads_for(const fmdp_ctx* ctx) {
   return fmdp::walk_threads(ctx->w.n_turn * ctx->w.W, tmax);
 }
 
-constexpr int kChunk = 512;
+constexpr int kChunk = 512;      // well records / plans per build pass (brute force)
+constexpr int kCullChunk = 256;  // well records with f1 culling (survivors only)
+// raw plans staged per row buffer: with culling as much of the slice as shared memory allows
+int rawcap_for(const fmdp_ctx* ctx);
+int chunk_for(const fmdp_ctx* ctx) { return ctx->launch.cull ? kCullChunk : kChunk; }
+
+int rawcap_for(const fmdp_ctx* ctx) {
+  if (!ctx->launch.cull) return kChunk;
+  int cap = 3072;
+  while (cap > kCullChunk &&
+         fmdp::walk_smem_bytes(ctx->w, ctx->C, threads_for(ctx), kCullChunk, cap, 16) > 220 * 1024)
+    cap -= 256;
+  return cap;
+}
 
 int max_clusters(fmdp_ctx* ctx, int G) {
   if (ctx->mc_cache[G]) return ctx->mc_cache[G];
   int n = 0;
-  if (fmdp::walk_max_clusters(ctx->w, ctx->C, G, threads_for(ctx), kChunk, &n) != cudaSuccess || n < 0) n = 0;
+  if (fmdp::walk_max_clusters(ctx->w, ctx->C, G, threads_for(ctx), chunk_for(ctx), rawcap_for(ctx), &n) !=
+          cudaSuccess || n < 0)
+    n = 0;
   cudaGetLastError();
   ctx->mc_cache[G] = n;
   return n;
@@ -240,7 +255,8 @@ void choose_launch(fmdp_ctx* ctx, int n_run, int* G_out, int* nc_out) {
   }
   // per-step cycles of one walker: hot loop (~21 pairs/clk/SM, measured) / G + per-step
   // overhead (projection, reductions, two cluster barriers, decision; measured ~16k cycles)
-  const double work = plans * fmdp::NTAU * ctx->A * ctx->W / 21.0;
+  // (with f1 culling the hot loop is a few dozen plans: the build pass over the slice remains)
+  const double work = ctx->launch.cull ? plans * 0.6 : plans * fmdp::NTAU * ctx->A * ctx->W / 21.0;
   const int sizes[] = {16, 8, 4, 2, 1};
   for (int G : sizes) {
     if (ctx->launch.cluster_size && G != ctx->launch.cluster_size) continue;
@@ -282,6 +298,7 @@ fmdp_status run_walk(fmdp_ctx* ctx, const std::vector<Req>& run, bool eval, int 
   a.cap = ctx->cap_states;
   a.eval = eval ? 1 : 0;
   a.budget = budget;
+  a.cull = ctx->launch.cull ? 1 : 0;
   a.dbg_vstar = ctx->d_dbg_vstar;
   a.dbg_v = ctx->d_dbg_v;
   a.dbg_s = ctx->d_dbg_s;
@@ -294,7 +311,7 @@ fmdp_status run_walk(fmdp_ctx* ctx, const std::vector<Req>& run, bool eval, int 
   ctx->stats.cluster_size = G;
   ctx->stats.walkers = std::max(ctx->stats.walkers, nc);
   CK(cudaEventRecord(ctx->ev0, ctx->stream));
-  CK(fmdp::launch_walk(ctx->w, a, ctx->C, G, nc, threads_for(ctx), kChunk, ctx->stream));
+  CK(fmdp::launch_walk(ctx->w, a, ctx->C, G, nc, threads_for(ctx), chunk_for(ctx), rawcap_for(ctx), ctx->stream));
   CK(cudaEventRecord(ctx->ev1, ctx->stream));
   CK(cudaEventSynchronize(ctx->ev1));
   CK(cudaGetLastError());
@@ -762,6 +779,13 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   for (int c : ctx->climb) maxc = std::max(maxc, std::abs(c));
   w.reach_u = (int32_t)(a.window * ((int64_t)std::ceil(maxd) + maxc) + 1);
   w.step_reach_u = (int32_t)((int64_t)std::ceil(maxd) + maxc + 1);
+  w.cull_inf = (int32_t)(Rmax + w.reach_u + 1);
+  w.k_absmax = 0;
+  for (int i = 0; i < a.n_tau; ++i) w.k_absmax = std::max(w.k_absmax, std::abs(w.k_tau[i]));
+  for (int i = 0; i < fmdp::NTAU; ++i) {
+    const double rc = i < a.n_tau ? std::sqrt((double)w.R2_tau[i]) + w.reach_u + 1.0 : -1.0;
+    w.cull2f_tau[i] = i < a.n_tau ? (float)(rc * rc * (1.0 + std::ldexp(1.0, -16))) : -1.0f;
+  }
   int kmax = 0;
   for (int i = 0; i < a.n_tau; ++i) kmax = std::max(kmax, std::abs(w.k_tau[i]));
   const int64_t vdyn = (int64_t)std::ceil(std::sqrt(maxd * maxd + (double)maxc * maxc));
@@ -832,7 +856,7 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
     w.height = ctx->d_height;
   }
   ctx->cap_states = a.max_steps + 2;
-  if (threads_for(ctx) > (ctx->C == 1 ? 512 : 384) || fmdp::walk_smem_bytes(w, ctx->C, threads_for(ctx), kChunk, 16) > 227 * 1024) {
+  if (threads_for(ctx) > (ctx->C == 1 ? 512 : 384) || fmdp::walk_smem_bytes(w, ctx->C, threads_for(ctx), kChunk, kChunk, 16) > 227 * 1024) {
     fmdp_destroy(ctx);
     return FMDP_E_ARG;
   }
@@ -867,7 +891,7 @@ fmdp_status fmdp_set_launch(fmdp_ctx* ctx, const fmdp_launch* l) {
     return fail(ctx, FMDP_E_ARG, "threads is derived from the action lattice; pass 0");
   ctx->launch = n;
   std::memset(ctx->mc_cache, 0, sizeof(ctx->mc_cache));
-  if (fmdp::walk_smem_bytes(ctx->w, ctx->C, threads_for(ctx), kChunk, 1) > 227 * 1024)
+  if (fmdp::walk_smem_bytes(ctx->w, ctx->C, threads_for(ctx), chunk_for(ctx), rawcap_for(ctx), 16) > 227 * 1024)
     return fail(ctx, FMDP_E_ARG, "shared memory");
   return FMDP_OK;
 }

@@ -89,6 +89,11 @@ __device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
   return d;
 }
+__device__ __forceinline__ f2 hi_far(f2 v) {  // replace the high float by a far-away coordinate
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return pk2(lo, 3.0e18f);
+}
 __device__ __forceinline__ float min3(float a, f2 p) {
   float lo, hi, r;
   asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(p));
@@ -101,10 +106,30 @@ __device__ __forceinline__ int sext(uint32_t v, int bits) { return (int)(v << (3
 // exact squared distance, saturated at sat (= R_max^2 < 2^30): valid because any component
 // >= R_max already implies d^2 >= R_max^2.
 __device__ __forceinline__ uint32_t clamp_d2(int dx, int dy, int dz, int rmax, uint32_t sat) {
-  uint32_t ax = (uint32_t)abs(dx), ay = (uint32_t)abs(dy), az = (uint32_t)abs(dz);
-  if (max(ax, max(ay, az)) >= (uint32_t)rmax) return sat;
-  uint32_t d2 = ax * ax + ay * ay + az * az;
-  return min(d2, sat);
+  const uint32_t ax = (uint32_t)abs(dx), ay = (uint32_t)abs(dy), az = (uint32_t)abs(dz);
+  const uint32_t mx = max(ax, max(ay, az));
+  const uint32_t a = min(ax, (uint32_t)rmax), b = min(ay, (uint32_t)rmax), c = min(az, (uint32_t)rmax);
+  const uint32_t d2 = a * a + b * b + c * c;  // < 3 * 2^30: no overflow (branch-free)
+  return mx >= (uint32_t)rmax ? sat : min(d2, sat);
+}
+
+// Order-preserving unsigned key of a double (larger value -> larger key).
+__device__ __forceinline__ unsigned long long dkey(double v) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(v);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+// Lane (in `mask`) holding the maximum key, ties broken by the smallest `idx`, among lanes
+// whose `ok` is set; -1 if none.  32-bit REDUX reductions (sm_80+): max hi, max lo, min idx.
+__device__ __forceinline__ int argmax_key(unsigned mask, bool ok, unsigned long long key, unsigned idx) {
+  const unsigned hi = ok ? (unsigned)(key >> 32) : 0u;
+  const unsigned mhi = __reduce_max_sync(mask, hi);
+  const bool c1 = ok && hi == mhi;
+  const unsigned lo = c1 ? (unsigned)key : 0u;
+  const unsigned mlo = __reduce_max_sync(mask, lo);
+  const bool c2 = c1 && lo == mlo;
+  const unsigned mi = __reduce_min_sync(mask, c2 ? idx : 0xffffffffu);
+  const unsigned win = __ballot_sync(mask, c2 && idx == mi) & mask;
+  return win ? __ffs(win) - 1 : -1;
 }
 
 // Per-step shared control block.  Counters used inside a step are double-buffered by step
@@ -116,7 +141,7 @@ struct Ctl {
   int32_t namb[2];            // ambiguous (state, tau) count, by step parity
   uint32_t stay_local[2];     // this CTA's slice minimum of |q - p(K)|^2, by step parity
   int32_t n_exact;            // exact-fallback count (rank 0 accumulates the cluster's)
-  int32_t pad;
+  int32_t nsurv[4];           // plans kept by the build, by (step parity, chunk parity)
   unsigned long long xmin;
   int32_t sl_lo[3], sl_n[3], sl_off[3];
   int32_t hgt[MAX_TURN];      // ground height under Delta_1 of every turn (cp.async target)
@@ -174,11 +199,11 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 // Per-phase cycle accounting (rank 0, thread 0), enabled when args.prof != nullptr.
 enum Phase { PH_PROJ, PH_FIX, PH_WAIT, PH_HOT, PH_STAGE, PH_SCATTER, PH_BAR1, PH_OWNER, PH_BAR2, PH_DECIDE,
-             PH_TOP, PH_SCAN, PH_PLOOP, PH_BUILD, PH_OWN1, PH_ARGMAX, PH_N };
+             PH_TOP, PH_SCAN, PH_PLOOP, PH_BUILD, PH_OWN1, PH_ARGMAX, PH_FLAGS, PH_N };
 
 template <int C>
 __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
-    walk_kernel(const World w, const WalkArgs args, const int CH, const int NGW) {
+    walk_kernel(const World w, const WalkArgs args, const int CH, const int RAWCAP, const int NGW) {
   cg::cluster_group cluster = cg::this_cluster();
   const unsigned rank = cluster.block_rank();
   const unsigned G = cluster.num_blocks();
@@ -196,7 +221,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   const int n_own = (A > (int)rank) ? (A - (int)rank + (int)G - 1) / (int)G : 0;
 
   Layout L;
-  L.build(w.HL, CH, NT, C, NCOL, A, AW, (int)G);
+  L.build(w.HL, CH, RAWCAP, NT, C, NCOL, A, AW, (int)G);
   extern __shared__ __align__(16) unsigned char smem[];
   int2* s_dxy = reinterpret_cast<int2*>(smem + L.o_dxy);
   int4* s_tw = reinterpret_cast<int4*>(smem + L.o_tw);
@@ -278,6 +303,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       ctl->ntc[0] = ctl->ntc[1] = 0;
       ctl->namb[0] = ctl->namb[1] = 0;
       ctl->stay_local[0] = ctl->stay_local[1] = w.sat_d2;
+      ctl->nsurv[0] = ctl->nsurv[1] = ctl->nsurv[2] = ctl->nsurv[3] = 0;
       ctl->n_exact = 0;
       if (rank == 0 && k > 0 && !args.eval) {  // resume: aggregates of the kept prefix
         for (int kk = 0; kk < k; ++kk) {
@@ -293,8 +319,8 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       const int64_t K0 = rq.t0 + k;
       const int n0 = row_count(w, K0), n1 = row_count(w, K0 + 1);
       cnt2 = row_count(w, K0 + 2);
-      issue_row(w, K0, n0, rank, lgG, CH, s_raw, RAWW, s_bar, ctl);
-      issue_row(w, K0 + 1, n1, rank, lgG, CH, s_raw, RAWW, s_bar, ctl);
+      issue_row(w, K0, n0, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl);
+      issue_row(w, K0 + 1, n1, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl);
       s_stay[0] = w.sat_d2;
       s_stay[1] = w.sat_d2;
     }
@@ -324,9 +350,12 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       const int p = k & 1;
       const int bK = (int)(K % 3), bK2 = (int)((K + 2) % 3);
       int4* s_pos = s_pos2 + p * AW;
-      if (tid == 0 && !args.eval && !fin) {
-        issue_row(w, K + 2, cnt2, rank, lgG, CH, s_raw, RAWW, s_bar, ctl);
-        cnt2 = row_count(w, K + 3);  // consumed next step: latency hidden by this step
+      if (tid == 0) {
+        if (!args.eval && !fin) {
+          issue_row(w, K + 2, cnt2, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl);
+          cnt2 = row_count(w, K + 3);  // consumed next step: latency hidden by this step
+        }
+        ctl->nsurv[((k + 1) & 1) * 2] = 0;  // step k+1, chunk 0 (last used in step k-1)
       }
       if (!args.eval && !fin) pending |= 1u << bK2;
       FMDP_MARK(PH_TOP)
@@ -355,12 +384,23 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         // ---- a2 forward projection (Alg 3): column (turn it, substep t) on the integer lattice
         const int it = col_it, t = col_t, h = col_h;
         int x = qx, y = qy, ps = psi;
-        for (int s = 1; s <= t; ++s) {
-          ps += h;
-          ps = ps >= w.HL ? ps - w.HL : (ps < 0 ? ps + w.HL : ps);
-          const int2 d = s_dxy[ps];
-          x += d.x;
-          y += d.y;
+        {
+          // psi_s = psi + s*h (closed form): the W table loads are independent
+          int ax[MAX_W], ay[MAX_W];
+#pragma unroll
+          for (int s = 1; s <= MAX_W; ++s) {
+            int pss = psi + s * h;
+            pss = pss >= w.HL ? pss - w.HL : (pss < 0 ? pss + w.HL : pss);
+            const int2 d = s <= t ? s_dxy[pss] : make_int2(0, 0);
+            ax[s - 1] = d.x;
+            ay[s - 1] = d.y;
+            if (s == t) ps = pss;
+          }
+#pragma unroll
+          for (int s = 0; s < MAX_W; ++s) {
+            x += ax[s];
+            y += ay[s];
+          }
         }
         sx = (float)(x - qx);
         sy = (float)(y - qy);
@@ -423,43 +463,73 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       uint32_t stay = w.sat_d2;
       {
         const int lo = ctl->sl_lo[bK], n = ctl->sl_n[bK];
-        const int32_t* rowg = w.rows + (size_t)K * 4 * w.row_cap;
-        for (int c0 = 0; c0 < n; c0 += CH) {
-          const int nc = min(CH, n - c0);
-          const int32_t *X, *Y, *Z, *V;
-          if (c0 == 0) {
-            const int32_t* b = s_raw + (size_t)bK * 4 * RAWW + ctl->sl_off[bK];
-            X = b; Y = b + RAWW; Z = b + 2 * RAWW; V = b + 3 * RAWW;
-          } else {
-            X = rowg + lo + c0; Y = X + w.row_cap; Z = Y + w.row_cap; V = Z + w.row_cap;
-          }
-          for (int j = tid; j < nc; j += NT) {
-            const int rx = X[j] - qx, ry = Y[j] - qy, rz = Z[j] - qz;
-            stay = min(stay, clamp_d2(rx, ry, rz, w.R_max, w.sat_d2));
+        // plan j of the CTA slice: the first RAWCAP were staged by TMA, the rest are read from L2
+        const int32_t* rb = s_raw + (size_t)bK * 4 * RAWW + ctl->sl_off[bK];
+        const int32_t* rg = w.rows + (size_t)K * 4 * w.row_cap + lo;
+        const int SC = args.cull ? RAWCAP : CH;  // plans per build pass
+        const ulonglong2* cen2 = reinterpret_cast<const ulonglong2*>(s_cen);
+
+        // Build pass over plans [c0, c0+nc) of the slice: exact nearest-plan distance (stay);
+        // well records of every plan (compact == false: slot = plan) or, with f1 culling, only
+        // of plans one of whose wells can reach a projected state (|q - c_tau| < R_tau + reach +
+        // 1 unit, conservative FP32 test; a culled well is farther than R_tau from every state
+        // by at least one unit, i.e. clearly outside the FP32 band, so the minima that decide
+        // the values are unchanged).  Survivors are compacted, order-free; slot >= CH overflows.
+        auto build = [&](int c0, int nc, bool compact, int* counter) {
+          for (int j0 = 0; j0 < nc; j0 += NT) {
+            const int jj = j0 + tid;
+            const bool valid = jj < nc;
+            const int j = c0 + jj;
+            int rx = 0, ry = 0, rz = 0, vx = 0, vy = 0, vz = 0;
+            if (valid) {
+              uint32_t pv;
+              if (j < RAWCAP) {
+                rx = rb[j] - qx; ry = rb[RAWW + j] - qy; rz = rb[2 * RAWW + j] - qz;
+                pv = (uint32_t)rb[3 * RAWW + j];
+              } else {
+                rx = __ldg(&rg[j]) - qx; ry = __ldg(&rg[w.row_cap + j]) - qy; rz = __ldg(&rg[2 * w.row_cap + j]) - qz;
+                pv = (uint32_t)__ldg(&rg[3 * w.row_cap + j]);
+              }
+              stay = min(stay, clamp_d2(rx, ry, rz, w.R_max, w.sat_d2));
+              vx = sext(pv, 11); vy = sext(pv >> 11, 11); vz = sext(pv >> 22, 10);
+            }
             if (fin) continue;
-            const uint32_t pv = (uint32_t)V[j];
-            const int vx = sext(pv, 11), vy = sext(pv >> 11, 11), vz = sext(pv >> 22, 10);
-            // plan pair layout: [pair][tau][x_j, x_j', y_j, y_j', z_j, z_j'] (+6 pad), negated
-            // offsets so that s - c is one packed add; exact integers < 2^24 (R23)
-            float* cp = s_cen + PAIR_STRIDE * (j >> 1) + (j & 1);
+            bool keep = valid;
+            if (valid && compact) {
+              // exact L-inf prefilter on the whole plan: every well lies within kmax*|v|_inf of p,
+              // so |p - q|_inf - kmax*|v|_inf >= R + reach + 1 culls all five wells
+              const int vinf = max(abs(vx), max(abs(vy), abs(vz)));
+              const int dinf = max(abs(rx), max(abs(ry), abs(rz)));
+              keep = dinf < w.cull_inf + w.k_absmax * vinf;
+            }
+            if (keep && compact) {
+              keep = false;
 #pragma unroll
-            for (int t = 0; t < NTAU; ++t) {
-              cp[6 * t + 0] = (float)(-(rx + w.k_tau[t] * vx));
-              cp[6 * t + 2] = (float)(-(ry + w.k_tau[t] * vy));
-              cp[6 * t + 4] = (float)(-(rz + w.k_tau[t] * vz));
+              for (int t = 0; t < NTAU; ++t) {
+                const float cx = (float)(rx + w.k_tau[t] * vx), cy = (float)(ry + w.k_tau[t] * vy),
+                            cz = (float)(rz + w.k_tau[t] * vz);
+                keep |= fmaf(cz, cz, fmaf(cy, cy, cx * cx)) < w.cull2f_tau[t];
+              }
+            }
+            int slot = jj;
+            if (compact && keep) slot = atomicAdd(counter, 1);  // survivors are rare: no warp round trip
+            if (keep && slot < CH) {
+              // plan pair layout: [pair][tau][x_j, x_j', y_j, y_j', z_j, z_j'] (+6 pad), negated
+              // offsets so that s - c is one packed add; exact integers < 2^24 (R23)
+              float* cp = s_cen + PAIR_STRIDE * (slot >> 1) + (slot & 1);
+#pragma unroll
+              for (int t = 0; t < NTAU; ++t) {
+                cp[6 * t + 0] = (float)(-(rx + w.k_tau[t] * vx));
+                cp[6 * t + 2] = (float)(-(ry + w.k_tau[t] * vy));
+                cp[6 * t + 4] = (float)(-(rz + w.k_tau[t] * vz));
+              }
             }
           }
-          if (!fin && (nc & 1) && tid == 0) {  // odd tail: the partner slot is a well at infinity
-            float* cp = s_cen + PAIR_STRIDE * (nc >> 1) + 1;
-#pragma unroll
-            for (int t = 0; t < NTAU; ++t) cp[6 * t + 0] = cp[6 * t + 2] = cp[6 * t + 4] = 3.0e18f;
-          }
-          if (fin) continue;
-          FMDP_MARK(PH_BUILD)
-          __syncthreads();
-          const ulonglong2* cen2 = reinterpret_cast<const ulonglong2*>(s_cen);
-          // (state, well) pair: |s - c|^2 = (dx^2 + dy^2) + dz^2, the horizontal part shared by
-          // the C climbs; two plans per packed instruction, FMNMX3 folds both into the minimum
+        };
+        // Hot loop over ns well records (two plans per packed instruction).
+        auto hot = [&](int ns) {
+          // (state, well) pair: |s - c|^2 = (dx^2 + dy^2) + dz^2, the horizontal part shared
+          // by the C climbs; FMNMX3 folds both plans of a pair into the running minimum
 #define FMDP_WELL2(T, X, Y, Z)                                \
   {                                                           \
     const f2 dx = add2(sx2, (X)), dy = add2(sy2, (Y));        \
@@ -469,11 +539,16 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       m[cc_][T] = min3(m[cc_][T], fma2(dz, dz, hh));          \
     }                                                         \
   }
-          const int np = (nc + 1) >> 1;
+          const int np = (ns + 1) >> 1;
           for (int pp = grp; pp < np; pp += NGW) {
             const ulonglong2* c8 = cen2 + (PAIR_STRIDE / 4) * pp;
-            const ulonglong2 e0 = c8[0], e1 = c8[1], e2 = c8[2], e3 = c8[3], e4 = c8[4], e5 = c8[5], e6 = c8[6],
-                             e7 = c8[7];
+            ulonglong2 e0 = c8[0], e1 = c8[1], e2 = c8[2], e3 = c8[3], e4 = c8[4], e5 = c8[5], e6 = c8[6], e7 = c8[7];
+            if (2 * pp + 1 == ns) {  // odd tail: the partner slot is a well at infinity
+              e0.x = hi_far(e0.x); e0.y = hi_far(e0.y); e1.x = hi_far(e1.x); e1.y = hi_far(e1.y);
+              e2.x = hi_far(e2.x); e2.y = hi_far(e2.y); e3.x = hi_far(e3.x); e3.y = hi_far(e3.y);
+              e4.x = hi_far(e4.x); e4.y = hi_far(e4.y); e5.x = hi_far(e5.x); e5.y = hi_far(e5.y);
+              e6.x = hi_far(e6.x); e6.y = hi_far(e6.y); e7.x = hi_far(e7.x);
+            }
             FMDP_WELL2(0, e0.x, e0.y, e1.x)
             FMDP_WELL2(1, e1.y, e2.x, e2.y)
             FMDP_WELL2(2, e3.x, e3.y, e4.x)
@@ -482,9 +557,32 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
             (void)e7;
           }
 #undef FMDP_WELL2
+          if (tid == 0 && args.pairs) atomicAdd(args.pairs, (unsigned long long)ns * NTAU * AW);
+        };
+
+        for (int c0 = 0, cidx = 0; c0 < n; c0 += SC, ++cidx) {
+          const int nc = min(SC, n - c0);
+          int* counter = &ctl->nsurv[(k & 1) * 2 + (cidx & 1)];
+          build(c0, nc, args.cull != 0, counter);
+          if (fin) continue;
+          FMDP_MARK(PH_BUILD)
           __syncthreads();
+          const int ns = args.cull ? *counter : nc;
+          if (tid == 0) ctl->nsurv[(k & 1) * 2 + ((cidx + 1) & 1)] = 0;  // next pass's counter
+          if (ns <= CH) {
+            hot(ns);
+            __syncthreads();
+          } else {  // more survivors than well records (rare): exact fallback, uncompacted
+            __syncthreads();
+            for (int m0 = c0; m0 < c0 + nc; m0 += CH) {
+              const int mn = min(CH, c0 + nc - m0);
+              build(m0, mn, false, counter);
+              __syncthreads();
+              hot(mn);
+              __syncthreads();
+            }
+          }
         }
-        if (!fin && tid == 0 && args.pairs) atomicAdd(args.pairs, (unsigned long long)n * NTAU * AW);
       }
       if (tid == 0 && !fin) ctl->ntc[p] = 0;  // list of step k consumed (FIX precedes the syncs above)
       // stay: slice minimum of |q - p(K)|^2 (terminal separation test of state k, Sec IV.I)
@@ -506,12 +604,21 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
             s_flags[it * C + c] = ((z < 0 || z < hgt) ? 1 : 0) | ((gx * gx + gy * gy + gz * gz < w.cap2) ? 2 : 0);
           }
         }
+        FMDP_MARK(PH_FLAGS)
         // group minimum inside the warp, then per-action blocks [t][tau] in s_stage
+        // (rounds over all C*NTAU values are unrolled so the shuffles overlap)
+        if (CPW <= 8) {
 #pragma unroll
-        for (int c = 0; c < C; ++c)
+          for (int c = 0; c < C; ++c)
 #pragma unroll
-          for (int t = 0; t < NTAU; ++t)
-            for (int o = CPW; o < 32; o <<= 1) m[c][t] = fminf(m[c][t], __shfl_xor_sync(0xffffffffu, m[c][t], o));
+            for (int t = 0; t < NTAU; ++t) m[c][t] = fminf(m[c][t], __shfl_xor_sync(0xffffffffu, m[c][t], 8));
+        }
+        if (CPW <= 16) {
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+#pragma unroll
+            for (int t = 0; t < NTAU; ++t) m[c][t] = fminf(m[c][t], __shfl_xor_sync(0xffffffffu, m[c][t], 16));
+        }
         if (grp == 0 && col < NCOL) {
           const int it = col / W, t1 = col % W;
 #pragma unroll
@@ -684,38 +791,29 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       double v1 = -INFINITY, v2 = -INFINITY;
       int a1 = INT_MAX, a2 = INT_MAX;
       if (!fin) {
-        if (A <= 32) {
-          // rank of action `lane` = number of actions better than it (value, then lower index);
-          // a* has rank 0, the runner-up rank 1 (Alg 9, R13)
-          const double mine = lane < A ? s_vstar[lane] : -INFINITY;
-          int rk = 0;
-          for (int a = 0; a < A; ++a) rk += better(s_vstar[a], a, mine, lane) ? 1 : 0;
-          const unsigned b0 = __ballot_sync(0xffffffffu, lane < A && rk == 0);
-          const unsigned b1 = __ballot_sync(0xffffffffu, lane < A && rk == 1);
-          a1 = __ffs(b0) - 1;
-          a2 = b1 ? __ffs(b1) - 1 : INT_MAX;
-          v1 = s_vstar[a1];
-          v2 = b1 ? s_vstar[a2] : -INFINITY;
-        } else {
-          for (int a = lane; a < A; a += 32) {
-            const double v = s_vstar[a];
-            if (better(v, a, v1, a1)) {
-              v2 = v1; a2 = a1; v1 = v; a1 = a;
-            } else if (better(v, a, v2, a2)) {
-              v2 = v; a2 = a;
-            }
+        // a7: top-2 over V* (Alg 9; ties -> lowest index, R13).  Lane l holds its best
+        // and second-best among a = l, l+32, ...; REDUX max over order-preserving keys.
+        double lb1 = -INFINITY, lb2 = -INFINITY;
+        int li1 = INT_MAX, li2 = INT_MAX;
+        for (int a = lane; a < A; a += 32) {
+          const double v = s_vstar[a];
+          if (better(v, a, lb1, li1)) {
+            lb2 = lb1; li2 = li1; lb1 = v; li1 = a;
+          } else if (better(v, a, lb2, li2)) {
+            lb2 = v; li2 = a;
           }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const double ov1 = __shfl_xor_sync(0xffffffffu, v1, o), ov2 = __shfl_xor_sync(0xffffffffu, v2, o);
-            const int oa1 = __shfl_xor_sync(0xffffffffu, a1, o), oa2 = __shfl_xor_sync(0xffffffffu, a2, o);
-            if (better(ov1, oa1, v1, a1)) {
-              if (better(v1, a1, ov2, oa2)) { v2 = v1; a2 = a1; } else { v2 = ov2; a2 = oa2; }
-              v1 = ov1; a1 = oa1;
-            } else if (better(ov1, oa1, v2, a2)) {
-              v2 = ov1; a2 = oa1;
-            }
-          }
+        }
+        const int w1 = argmax_key(0xffffffffu, li1 != INT_MAX, dkey(lb1), (unsigned)li1);
+        a1 = __shfl_sync(0xffffffffu, li1, w1);
+        v1 = __shfl_sync(0xffffffffu, lb1, w1);
+        // runner-up: every lane's best excluding a1
+        const bool own = lane == w1;
+        const double cv = own ? lb2 : lb1;
+        const int ci = own ? li2 : li1;
+        const int w2 = argmax_key(0xffffffffu, ci != INT_MAX, dkey(cv), (unsigned)ci);
+        if (w2 >= 0) {
+          a2 = __shfl_sync(0xffffffffu, ci, w2);
+          v2 = __shfl_sync(0xffffffffu, cv, w2);
         }
       }
       FMDP_MARK(PH_ARGMAX)
@@ -882,9 +980,9 @@ int walk_threads(int ncol, int max_threads) {
 
 template <int C>
 static cudaError_t launch_walk_t(const World& w, const WalkArgs& a, int cluster, int n_clusters, int threads,
-                                 int chunk, cudaStream_t s) {
+                                 int chunk, int rawcap, cudaStream_t s) {
   Layout L;
-  L.build(w.HL, chunk, threads, C, w.n_turn * w.W, w.A, w.A * w.W, cluster);
+  L.build(w.HL, chunk, rawcap, threads, C, w.n_turn * w.W, w.A, w.A * w.W, cluster);
   cudaError_t e = cudaFuncSetAttribute(walk_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
   if (cluster > 8) {
@@ -904,13 +1002,13 @@ static cudaError_t launch_walk_t(const World& w, const WalkArgs& a, int cluster,
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const int ngw = walk_groups_per_warp(w.n_turn * w.W, threads);
-  return cudaLaunchKernelEx(&cfg, walk_kernel<C>, w, a, chunk, ngw);
+  return cudaLaunchKernelEx(&cfg, walk_kernel<C>, w, a, chunk, rawcap, ngw);
 }
 
 template <int C>
-static cudaError_t max_clusters_t(const World& w, int cluster, int threads, int chunk, int* out) {
+static cudaError_t max_clusters_t(const World& w, int cluster, int threads, int chunk, int rawcap, int* out) {
   Layout L;
-  L.build(w.HL, chunk, threads, C, w.n_turn * w.W, w.A, w.A * w.W, cluster);
+  L.build(w.HL, chunk, rawcap, threads, C, w.n_turn * w.W, w.A, w.A * w.W, cluster);
   cudaError_t e = cudaFuncSetAttribute(walk_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
   if (cluster > 8) {
@@ -932,27 +1030,27 @@ static cudaError_t max_clusters_t(const World& w, int cluster, int threads, int 
 }
 
 cudaError_t launch_walk(const World& w, const WalkArgs& a, int n_climb, int cluster, int n_clusters, int threads,
-                        int chunk, cudaStream_t s) {
+                        int chunk, int rawcap, cudaStream_t s) {
   switch (n_climb) {
-    case 1: return launch_walk_t<1>(w, a, cluster, n_clusters, threads, chunk, s);
-    case 3: return launch_walk_t<3>(w, a, cluster, n_clusters, threads, chunk, s);
-    case 5: return launch_walk_t<5>(w, a, cluster, n_clusters, threads, chunk, s);
+    case 1: return launch_walk_t<1>(w, a, cluster, n_clusters, threads, chunk, rawcap, s);
+    case 3: return launch_walk_t<3>(w, a, cluster, n_clusters, threads, chunk, rawcap, s);
+    case 5: return launch_walk_t<5>(w, a, cluster, n_clusters, threads, chunk, rawcap, s);
     default: return cudaErrorInvalidValue;
   }
 }
 
-cudaError_t walk_max_clusters(const World& w, int n_climb, int cluster, int threads, int chunk, int* out) {
+cudaError_t walk_max_clusters(const World& w, int n_climb, int cluster, int threads, int chunk, int rawcap, int* out) {
   switch (n_climb) {
-    case 1: return max_clusters_t<1>(w, cluster, threads, chunk, out);
-    case 3: return max_clusters_t<3>(w, cluster, threads, chunk, out);
-    case 5: return max_clusters_t<5>(w, cluster, threads, chunk, out);
+    case 1: return max_clusters_t<1>(w, cluster, threads, chunk, rawcap, out);
+    case 3: return max_clusters_t<3>(w, cluster, threads, chunk, rawcap, out);
+    case 5: return max_clusters_t<5>(w, cluster, threads, chunk, rawcap, out);
     default: return cudaErrorInvalidValue;
   }
 }
 
-size_t walk_smem_bytes(const World& w, int n_climb, int threads, int chunk, int cluster) {
+size_t walk_smem_bytes(const World& w, int n_climb, int threads, int chunk, int rawcap, int cluster) {
   Layout L;
-  L.build(w.HL, chunk, threads, n_climb, w.n_turn * w.W, w.A, w.A * w.W, cluster);
+  L.build(w.HL, chunk, rawcap, threads, n_climb, w.n_turn * w.W, w.A, w.A * w.W, cluster);
   return L.total;
 }
 

@@ -256,3 +256,37 @@ def test_api_errors(F):
         ctx.add_plans(flood)
     assert ctx.num_plans() == n
     ctx.close()
+
+
+# ----------------------------------------------------------------------------- f1: exact culling
+def test_cull_bit_identical_steps(F):
+    """culling plans none of whose wells can reach a projected state changes no
+    output bit (truncation), at small sizes and at configs[1] size."""
+    for sc, n in ((fs.random_small(51, n_plans=800, half_m=2000.0, n_buildings=30), 12), (fs.config_c2(), 6)):
+        states = fs.random_states(52, sc, n)
+        outs = []
+        for cull in (0, 1):
+            ctx = ctx_for(F, sc, cull=cull)
+            outs.append([ctx.eval_step(q, psi, g, K) for q, psi, g, K in states])
+            st = ctx.stats()
+            ctx.close()
+        for a, b in zip(*outs):
+            assert (a["v"] == b["v"]).all() and (a["vstar"] == b["vstar"]).all()
+            assert (a["min_d2"] == b["min_d2"]).all() and a["a_star"] == b["a_star"]
+
+
+def test_cull_bit_identical_batch(F):
+    sc = fs.random_small(53, n_plans=200, n_requests=10, half_m=1500.0, n_buildings=20, max_steps=500, t0_max=60)
+    res = []
+    for cull in (0, 1):
+        ctx = ctx_for(F, sc, cull=cull, step_budget=32)
+        res.append(ctx.schedule_batch(sc.src, sc.dst, sc.t0))
+        if cull:
+            pairs_cull = ctx.stats()["pair_evals"]
+        else:
+            pairs_full = ctx.stats()["pair_evals"]
+        ctx.close()
+    for x, y in zip(*res):
+        assert x.status == y.status and x.n_states == y.n_states and (x.traj == y.traj).all()
+        assert x.min_sep_m == y.min_sep_m and x.n_near_ties == y.n_near_ties
+    assert pairs_cull < pairs_full
