@@ -139,24 +139,25 @@ def run_reference(args):
     import fmdp_synth as fs
     from oracle import oracle as O
     sc = fs.config_c2(seed=args.seed)
-    n_req = 1  # bounded sample per step: the first request of the batch against the initial store
+    n_req = 2  # bounded sample per step: the first two FCFS requests of the batch (~12 s)
     times, states = [], 0
     for i in range(args.warmup + args.steps):
         orc = O.for_scenario(sc)
+        nr = 1 if i < args.warmup else n_req  # warm-up steps: one request
         t0 = time.perf_counter()
-        r = orc.schedule(sc.src[0], sc.dst[0], int(sc.t0[0]))
+        st = sum(orc.schedule(sc.src[q], sc.dst[q], int(sc.t0[q])).n_states for q in range(nr))
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(dt)
-            states += r.n_states
+            states += st
     tot = sum(times)
     value = n_req * args.steps / tot
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "requests/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": WORKLOAD, "sample": "first request of the batch per step"},
+            "data": "synthetic", "config": {"workload": WORKLOAD, "sample": "first two FCFS requests of the batch per step"},
             "cpu_baseline": {"value": value, "unit": "requests/s", "cores": 1, "kind": "oracle",
-                             "sample": f"first request of the configs[1] batch ({states // max(1, args.steps)} "
+                             "sample": f"first two FCFS requests of the configs[1] batch ({states // max(1, args.steps)} "
                                        f"states) per step, fp64 C oracle, single thread"},
             "e2e": {"value": value, "unit": "requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -197,48 +198,54 @@ def run_native(args):
         flush.zero_()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        one(False)
-        reset()
-    # ---- value: device-resident store and requests, trajectories left on the device
-    times, st_all, res_last = [], [], None
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            res, ms = one(False)
-            st_all.append(ctx.stats())
-            times.append(ms)
-            res_last = res
+    def measure(cull):
+        ctx.set_launch(cull=cull)
+        for _ in range(args.warmup):
+            one(False)
             reset()
-    torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    # ---- e2e: through the public API with host requests, trajectories and results copied back
-    e2e_times, d2h = [], 0
-    for _ in range(max(1, args.steps)):
+        # value: device-resident store and requests, trajectories left on the device
+        times, st_all, res_last = [], [], None
+        if world > 1:
+            torch.distributed.barrier()
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        res, ms = one(True)
-        e2e_times.append(ms)
-        d2h = sum(r.n_states for r in res) * 12 + n * C_RESULT_BYTES
-        reset()
-    h2d = n * C_REQUEST_BYTES
+        with ClockSampler(local) as clk:
+            for _ in range(args.steps):
+                res, ms = one(False)
+                st_all.append(ctx.stats())
+                times.append(ms)
+                res_last = res
+                reset()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        # e2e: through the public API with host requests, trajectories and results copied back
+        e2e_times, d2h = [], 0
+        for _ in range(max(1, args.steps)):
+            torch.cuda.synchronize()
+            res, ms = one(True)
+            e2e_times.append(ms)
+            d2h = sum(r.n_states for r in res) * 12 + n * C_RESULT_BYTES
+            reset()
+        tot_ms = max_over_ranks(sum(times), world)
+        e2e_ms = max_over_ranks(sum(e2e_times), world)
+        return dict(tot_ms=tot_ms, e2e_ms=e2e_ms,
+                    value=sum_over_ranks(n * args.steps, world) / (tot_ms / 1e3),
+                    e2e_value=sum_over_ranks(n * len(e2e_times), world) / (e2e_ms / 1e3), d2h=d2h,
+                    st_all=st_all, res_last=res_last, clocks=clk.summary(),
+                    walk_ms=sum(s["device_ms"] for s in st_all), pairs=sum(s["pair_evals"] for s in st_all),
+                    launches=sum(s["kernels"] for s in st_all), steps_dev=sum(s["steps"] for s in st_all))
 
-    tot_ms = max_over_ranks(sum(times), world)
-    e2e_ms = max_over_ranks(sum(e2e_times), world)
-    total_req = sum_over_ranks(n * args.steps, world)
-    value = total_req / (tot_ms / 1e3)
-    e2e_value = sum_over_ranks(n * len(e2e_times), world) / (e2e_ms / 1e3)
-    stats = st_all[-1]
-    walk_ms = sum(s["device_ms"] for s in st_all)
-    pairs = sum(s["pair_evals"] for s in st_all)
-    launches = sum(s["kernels"] for s in st_all)
+    M = measure(0)       # every (state, well) pair evaluated
+    Mc = measure(1)      # exact culling, bit-identical outputs
+    h2d = n * C_REQUEST_BYTES
+    tot_ms, value, e2e_value, d2h = M["tot_ms"], M["value"], M["e2e_value"], M["d2h"]
+    stats = M["st_all"][-1]
+    walk_ms, pairs, launches, steps_dev = M["walk_ms"], M["pairs"], M["launches"], M["steps_dev"]
+    res_last = M["res_last"]
     acc = sum(r.accepted for r in res_last)
     states = sum(r.n_states for r in res_last)
-    steps_dev = sum(s["steps"] for s in st_all)
-    clocks = clk.summary()
+    clocks = M["clocks"]
+    same = all(a.status == b.status and a.n_states == b.n_states for a, b in zip(M["res_last"], Mc["res_last"]))
     peak_clock = 1965.0
     try:
         mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -274,6 +281,15 @@ def run_native(args):
         "e2e": {"value": e2e_value, "unit": "requests/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
         "clocks": clocks,
+        "f1_cull": {
+            "what": "SURVEY f1 exact culling of plans none of whose wells can reach a projected state; "
+                    "outputs bit-identical (tests/test_gpu_parity.py::test_cull_*)",
+            "value": Mc["value"], "unit": "requests/s", "ms_per_step": Mc["tot_ms"] / args.steps,
+            "e2e": {"value": Mc["e2e_value"], "unit": "requests/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": Mc["d2h"]},
+            "walk_device_ms_per_step": Mc["walk_ms"] / args.steps,
+            "pair_evals_per_step": Mc["pairs"] / args.steps, "gpu_launches": Mc["launches"],
+            "same_results_as_full": same, "clocks": Mc["clocks"]},
     }
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(sc, args.cpu_sample_s)

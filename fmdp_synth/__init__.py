@@ -141,6 +141,35 @@ def reflecting_lines(rng: np.random.Generator, n: int, lo_u, hi_u, rows: Tuple[i
     return plans
 
 
+def reflecting_lines_fast(rng: np.random.Generator, n: int, lo_u, hi_u, rows: Tuple[int, int],
+                          speed_mps=(30.0, 60.0), vz_units=(-16, 16), z_lo_u=None, z_hi_u=None,
+                          chunk: int = 8192) -> List[Tuple[int, np.ndarray]]:
+    """Vectorised reflecting lines (same recipe as reflecting_lines, all active over ``rows``);
+    the returned state arrays are views into one [n, rows, 3] int32 block."""
+    lo_u = np.asarray(lo_u, np.int64)
+    hi_u = np.asarray(hi_u, np.int64)
+    zlo = int(lo_u[2] if z_lo_u is None else z_lo_u)
+    zhi = int(hi_u[2] if z_hi_u is None else z_hi_u)
+    lo3 = np.array([lo_u[0], lo_u[1], zlo], np.int64)
+    hi3 = np.array([hi_u[0], hi_u[1], zhi], np.int64)
+    p0 = np.stack([rng.integers(lo3[d], hi3[d] + 1, size=n) for d in range(3)], axis=1)
+    sp = rng.uniform(*speed_mps, size=n) * 0.1 * U_PER_M
+    th = rng.uniform(0.0, 2.0 * np.pi, size=n)
+    v = np.stack([np.rint(sp * np.cos(th)), np.rint(sp * np.sin(th)),
+                  rng.integers(vz_units[0], vz_units[1] + 1, size=n)], axis=1).astype(np.int64)
+    nk = rows[1] - rows[0]
+    out = np.empty((n, nk, 3), np.int32)
+    K = np.arange(nk, dtype=np.int64)[None, :, None]
+    L = (hi3 - lo3)[None, None, :]
+    for a in range(0, n, chunk):
+        b = min(n, a + chunk)
+        raw = p0[a:b, None, :] + v[a:b, None, :] * K - lo3[None, None, :]
+        y = np.mod(raw, 2 * L)
+        y = np.where(y > L, 2 * L - y, y)
+        out[a:b] = (lo3[None, None, :] + y).astype(np.int32)
+    return [(int(rows[0]), out[j]) for j in range(n)]
+
+
 def manhattan_terrain(rng: np.random.Generator, n_buildings: int, core_half_m: float,
                       raster_half_m: float, pitch_m=100.0, block_m=60.0, cell_m=10.0) -> Terrain:
     """Building wells on a Manhattan grid + a height raster covering the airspace."""
@@ -269,3 +298,45 @@ def random_states(seed: int, sc: Scenario, n: int):
         K = int(rng.integers(0, max(1, a.horizon_steps - a.max_steps - 2)))
         out.append((q.astype(np.int32), psi, g.astype(np.int32), K))
     return out
+
+
+def config_c3(seed: int = 3, n_requests: int = 1000, n_buildings: int = 256) -> Scenario:
+    """configs[2]: 1000 sequential FCFS requests growing the store from 0 to ~1000 plans, the
+    configs[1] city and terrain, pairs 2-6 km apart, t0 U[0,600) (dense overlap)."""
+    rng = np.random.default_rng(seed)
+    a = Airspace(max_steps=4000, lo_m=(-8000.0, -8000.0, 0.0), hi_m=(8000.0, 8000.0, 1500.0),
+                 horizon_steps=8192, row_capacity=1024)
+    terrain = manhattan_terrain(rng, n_buildings, core_half_m=5000.0, raster_half_m=8000.0)
+    pads = vertiports(rng, 200, 5000.0, terrain)
+    src, dst, t0 = request_pairs(rng, pads, n_requests, 2000.0, 6000.0, (0, 600))
+    return Scenario(a, terrain, [], src, dst, t0, name="c3")
+
+
+def config_c4(seed: int = 4, n_plans: int = 100_000, rows: int = 4000, n_requests: int = 10,
+              n_buildings: int = 256) -> Scenario:
+    """configs[3]: 100k plans in 100 x 100 km x [60,1500] m (~6.9 plans/km^3, the configs[1]
+    density), 256 building wells near the request area, 5 km requests."""
+    rng = np.random.default_rng(seed)
+    a = Airspace(max_steps=min(4000, rows - 8), lo_m=(-50000.0, -50000.0, 0.0), hi_m=(50000.0, 50000.0, 1500.0),
+                 horizon_steps=rows + 8, row_capacity=((n_plans + n_requests + 64) + 3) // 4 * 4)
+    terrain = manhattan_terrain(rng, n_buildings, core_half_m=5000.0, raster_half_m=8000.0)
+    lo, hi = m2u(a.lo_m), m2u(a.hi_m)
+    plans = reflecting_lines_fast(rng, n_plans, lo, hi, (0, rows), z_lo_u=int(m2u(60)), z_hi_u=int(m2u(1500)))
+    pads = vertiports(rng, 40, 5000.0, terrain)
+    src, dst, t0 = request_pairs(rng, pads, n_requests, 4500.0, 5500.0, (0, 1))
+    return Scenario(a, terrain, plans, src, dst, t0, name="c4")
+
+
+def config_c5(seed: int = 5, n_plans: int = 1_000_000, rows: int = 3000, n_requests: int = 10) -> Scenario:
+    """configs[4]: 1M plans in 250 x 250 km x [60,2350] m (~7 plans/km^3), widened action set
+    17 headings x 5 climbs (A = 85), 256 terrain wells."""
+    rng = np.random.default_rng(seed)
+    a = Airspace(max_steps=min(4000, rows - 8), lo_m=(-125000.0, -125000.0, 0.0), hi_m=(125000.0, 125000.0, 2350.0),
+                 horizon_steps=rows + 8, row_capacity=((n_plans + n_requests + 64) + 3) // 4 * 4,
+                 turn_steps=tuple(range(-8, 9)), climb_units=(-32, -16, 0, 16, 32))
+    terrain = manhattan_terrain(rng, 256, core_half_m=5000.0, raster_half_m=8000.0)
+    lo, hi = m2u(a.lo_m), m2u(a.hi_m)
+    plans = reflecting_lines_fast(rng, n_plans, lo, hi, (0, rows), z_lo_u=int(m2u(60)), z_hi_u=int(m2u(2350)))
+    pads = vertiports(rng, 40, 5000.0, terrain)
+    src, dst, t0 = request_pairs(rng, pads, n_requests, 4500.0, 5500.0, (0, 1))
+    return Scenario(a, terrain, plans, src, dst, t0, name="c5")

@@ -512,8 +512,8 @@ int orc_replay(const orc_params* p, const orc_terrain* T, const orc_store* S,
     else if (terrain_collision(T, q)) verdict = ORC_REJ_TERRAIN;
     else if (d2_of(q, dst) < cap2) verdict = ORC_ACCEPTED;
     else if (k >= p->max_steps) verdict = ORC_REJ_TIMEOUT;
-    if (k == n - 1) {
-      if (verdict != status) FAIL(k);
+    if (k == n - 1) {  /* status -1: a trajectory prefix, its last state must be non-terminal */
+      if (verdict != (status < 0 ? -1 : status)) FAIL(k);
       break;
     }
     if (verdict >= 0) { FAIL(k); break; }

@@ -124,6 +124,7 @@ int orc_schedule(const orc_params* p, const orc_terrain* T, const orc_store* S,
 int orc_schedule_batch(const orc_params* p, const orc_terrain* T, orc_store* S, int32_t n,
                        const int32_t* src, const int32_t* dst, const int64_t* t0, int32_t cap,
                        int32_t* traj, int32_t* heading, int32_t* astar, orc_result* res);
+/* status -1 replays a prefix (the last given state must not be terminal). */
 int orc_replay(const orc_params* p, const orc_terrain* T, const orc_store* S,
                const int32_t src[3], const int32_t dst[3], int64_t t0,
                int32_t n, const int32_t* traj, const int32_t* heading, const int32_t* astar,

@@ -485,7 +485,8 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
     // (cluster size re-chosen for the shrinking count), then commits the finished FCFS prefix
     // and rolls back any pending request whose computed steps could see a newly committed
     // plan to its first influenced step.  Result: identical to the sequential loop.
-    const int budget = ctx->launch.step_budget > 0 ? ctx->launch.step_budget : 256;
+    // slice budget: measured optimum on configs[1] (tools/sweep_budget.py)
+    const int budget = ctx->launch.step_budget > 0 ? ctx->launch.step_budget : (ctx->launch.cull ? 256 : 128);
     std::vector<char> fin(n, 0);
     std::vector<int> kdone(n, 0);
     int rollbacks = 0;

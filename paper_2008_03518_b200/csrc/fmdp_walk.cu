@@ -919,8 +919,8 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
 // Append accepted plans to the time rows (Sec V: "automatically stored in the database
 // of accepted flight plans").  Slots are assigned by the host in plan-id order.
 __global__ void append_kernel(int32_t* rows, int32_t cap, int64_t horizon, const AppendPlan* plans) {
-  const AppendPlan P = plans[blockIdx.y];
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x) {
+  const AppendPlan P = plans[blockIdx.x];  // one block per plan (grid.x up to 2^31-1 plans)
+  for (int i = threadIdx.x; i < P.n; i += blockDim.x) {
     const int64_t K = P.t0 + i;
     if (K < 0 || K >= horizon) continue;
     const int32_t* s = P.states + 3 * i;
@@ -1057,8 +1057,8 @@ size_t walk_smem_bytes(const World& w, int n_climb, int threads, int chunk, int 
 cudaError_t launch_append(int32_t* rows, int32_t row_cap, int64_t horizon, const AppendPlan* plans, int n_plans,
                           int max_n, cudaStream_t s) {
   if (n_plans <= 0) return cudaSuccess;
-  dim3 grid((max_n + 255) / 256, n_plans, 1);
-  append_kernel<<<grid, 256, 0, s>>>(rows, row_cap, horizon, plans);
+  (void)max_n;
+  append_kernel<<<n_plans, 256, 0, s>>>(rows, row_cap, horizon, plans);
   return cudaGetLastError();
 }
 
