@@ -209,6 +209,24 @@ fmdp_status fmdp_schedule_batch(fmdp_ctx* ctx, const fmdp_request* reqs, int32_t
                                 fmdp_result* res, fmdp_qpos* traj, int32_t traj_cap_each,
                                 int32_t flags);
 
+/* Plan-sharded multi-GPU scheduling, host-stepped reference path.
+ * Every rank holds the same store (plans added identically on all ranks) and evaluates only
+ * its shard of every time row (slots [n*rank/world, n*(rank+1)/world)).  Per decision step
+ * the per-(projected state, tau) minimum squared distances (FP32 bits) and the nearest-plan
+ * distance (uint32) -- A*W*5 + 1 values -- are combined with allreduce_min_u32 (in place,
+ * elementwise MIN over ranks, e.g. ncclAllReduce(ncclMin) / gloo); every rank then takes the
+ * identical decision.  Minima are exact, so results are bit-identical to one GPU.
+ * Collective call: every rank must call it with the same request.  The callback returns 0
+ * on success. */
+typedef struct fmdp_shard {
+  int32_t rank, world;
+  int32_t (*allreduce_min_u32)(uint32_t* host_buf, int32_t count, void* user);
+  void* user;
+} fmdp_shard;
+fmdp_status fmdp_schedule_sharded(fmdp_ctx* ctx, const fmdp_shard* shard, uint64_t aircraft_id, fmdp_vec3 src,
+                                  fmdp_vec3 dst, int64_t t0_step, fmdp_result* res, fmdp_qpos* traj,
+                                  int32_t traj_cap);
+
 /* Per-step log of the last trajectory of request `index` of the last schedule /
  * schedule_batch call: action a*_k, heading psi_k, and near-tie flag per step (k < n).
  * Any pointer may be NULL. */

@@ -86,6 +86,9 @@ struct WalkArgs {
   int32_t eval;                 // 1: evaluate one step (debug outputs), no advance
   int32_t budget;               // decision steps per request in this launch (then pause, status -1)
   int32_t cull;                 // 1: f1 exact culling of plans whose wells cannot reach the states
+  int32_t shard_rank, shard_world;  // plan shard of this GPU; 0, 1 = whole rows
+  int32_t xmode;                // 0 normal; 1 export per-(state,tau) minima + stay; 2 import and decide
+  uint32_t* xbuf;               // [A*W*NTAU + 1] exchange buffer (float bits / stay d^2)
   double* dbg_vstar;            // [A]
   double* dbg_v;                // [A*W]
   double* dbg_s;                // [A*W]

@@ -77,6 +77,8 @@ struct fmdp_ctx {
   int app_cap = 0;
   int32_t* d_up = nullptr;  // upload scratch (states / slots)
   size_t up_cap = 0;
+  uint32_t* d_xbuf = nullptr;  // multi-GPU exchange buffer [A*W*NTAU + 1]
+  int xmode = 0, shard_rank = 0, shard_world = 1;
   double *d_dbg_vstar = nullptr, *d_dbg_v = nullptr, *d_dbg_s = nullptr;
   uint32_t* d_dbg_conf = nullptr;
   int32_t* d_dbg_astar = nullptr;
@@ -299,6 +301,10 @@ fmdp_status run_walk(fmdp_ctx* ctx, const std::vector<Req>& run, bool eval, int 
   a.eval = eval ? 1 : 0;
   a.budget = budget;
   a.cull = ctx->launch.cull ? 1 : 0;
+  a.xmode = ctx->xmode;
+  a.shard_rank = ctx->shard_rank;
+  a.shard_world = ctx->shard_world;
+  a.xbuf = ctx->d_xbuf;
   a.dbg_vstar = ctx->d_dbg_vstar;
   a.dbg_v = ctx->d_dbg_v;
   a.dbg_s = ctx->d_dbg_s;
@@ -806,8 +812,9 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   ctx->d_dbg_s = (double*)dalloc(ctx, sizeof(double) * A * a.window);
   ctx->d_dbg_conf = (uint32_t*)dalloc(ctx, sizeof(uint32_t) * (A + 1));
   ctx->d_dbg_astar = (int32_t*)dalloc(ctx, sizeof(int32_t) * 4);
+  ctx->d_xbuf = (uint32_t*)dalloc(ctx, sizeof(uint32_t) * ((size_t)A * a.window * fmdp::NTAU + 1));
   if (!ctx->d_rows || !ctx->d_counts || !ctx->d_dxy || !ctx->d_queue || !ctx->d_pairctr || !ctx->d_prof || !ctx->d_dbg_vstar ||
-      !ctx->d_dbg_v || !ctx->d_dbg_s || !ctx->d_dbg_conf || !ctx->d_dbg_astar) {
+      !ctx->d_dbg_v || !ctx->d_dbg_s || !ctx->d_dbg_conf || !ctx->d_dbg_astar || !ctx->d_xbuf) {
     fmdp_destroy(ctx);
     return FMDP_E_NOMEM;
   }
@@ -983,6 +990,79 @@ fmdp_status fmdp_schedule(fmdp_ctx* ctx, uint64_t aircraft_id, fmdp_vec3 src, fm
   r.dst = dst;
   r.t0_step = t0_step;
   return schedule_many(ctx, &r, 1, res, traj, traj_cap, FMDP_BATCH_SEQUENTIAL);
+}
+
+fmdp_status fmdp_schedule_sharded(fmdp_ctx* ctx, const fmdp_shard* shard, uint64_t aircraft_id, fmdp_vec3 src,
+                                  fmdp_vec3 dst, int64_t t0_step, fmdp_result* res, fmdp_qpos* traj,
+                                  int32_t traj_cap) {
+  if (!ctx || !shard || !res || !shard->allreduce_min_u32 || shard->world < 1 || shard->rank < 0 ||
+      shard->rank >= shard->world)
+    return fail(ctx, FMDP_E_ARG, "invalid shard description");
+  if (traj && traj_cap < ctx->w.max_steps + 1) return fail(ctx, FMDP_E_BUFFER, "traj_cap must be >= max_steps + 1");
+  std::memset(&ctx->stats, 0, sizeof(ctx->stats));
+  fmdp_request rq;
+  rq.aircraft_id = aircraft_id;
+  rq.src = src;
+  rq.dst = dst;
+  rq.t0_step = t0_step;
+  std::vector<Req> base;
+  fmdp_status st = prepare_requests(ctx, &rq, 1, base);
+  if (st) return st;
+  if ((st = ensure_slots(ctx, 1))) return st;
+  CK(cudaMemsetAsync(ctx->d_pairctr, 0, sizeof(unsigned long long), ctx->stream));
+  const int nx = ctx->A * ctx->W * fmdp::NTAU + 1;
+  std::vector<uint32_t> hbuf(nx);
+  ctx->shard_rank = shard->rank;
+  ctx->shard_world = shard->world;
+  int k = 0;
+  for (;;) {
+    Req r = base[0];
+    r.start_k = k;
+    ctx->xmode = 1;  // this GPU's minima over its plan shard
+    st = run_walk(ctx, {r}, false, 1);
+    if (!st) {
+      CK(cudaMemcpyAsync(hbuf.data(), ctx->d_xbuf, sizeof(uint32_t) * nx, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      if (shard->allreduce_min_u32(hbuf.data(), nx, shard->user) != 0) st = fail(ctx, FMDP_E_INTERNAL, "allreduce failed");
+    }
+    if (!st) {
+      CK(cudaMemcpyAsync(ctx->d_xbuf, hbuf.data(), sizeof(uint32_t) * nx, cudaMemcpyHostToDevice, ctx->stream));
+      ctx->xmode = 2;  // all-reduced minima -> identical decision on every GPU
+      st = run_walk(ctx, {r}, false, 1);
+    }
+    ctx->xmode = 0;
+    if (!st) st = fetch_out(ctx, 1);
+    if (st) {
+      ctx->shard_rank = 0;
+      ctx->shard_world = 1;
+      return st;
+    }
+    ctx->stats.steps += ctx->h_out[0].steps_run;
+    ctx->stats.rounds += 1;
+    if (ctx->h_out[0].status >= 0) break;
+    k = ctx->h_out[0].n_states - 1;
+  }
+  ctx->shard_rank = 0;
+  ctx->shard_world = 1;
+  const Out& o = ctx->h_out[0];
+  std::vector<uint32_t> plan_id(1, 0xffffffffu);
+  std::vector<uint64_t> aircraft(1, aircraft_id);
+  if (o.status == FMDP_ACCEPTED && (st = commit_slots(ctx, {0}, base, aircraft, plan_id))) return st;
+  res->status = o.status;
+  res->plan_id = plan_id[0];
+  res->n_states = o.n_states;
+  res->fail_step = o.fail_step;
+  res->min_sep_m = std::sqrt((double)o.min_sep_d2) * ctx->air.u_m;
+  res->n_near_ties = o.n_near_ties;
+  res->n_exact = o.n_exact;
+  if (traj) {
+    CK(cudaMemcpy(traj, ctx->d_traj, sizeof(fmdp_qpos) * o.n_states, cudaMemcpyDeviceToHost));
+  }
+  unsigned long long pc = 0;
+  CK(cudaMemcpy(&pc, ctx->d_pairctr, sizeof(pc), cudaMemcpyDeviceToHost));
+  ctx->stats.pair_evals = (int64_t)pc;
+  ctx->last_n = 1;
+  return FMDP_OK;
 }
 
 fmdp_status fmdp_schedule_batch(fmdp_ctx* ctx, const fmdp_request* reqs, int32_t n, fmdp_result* res,

@@ -151,9 +151,12 @@ struct Ctl {
 // plans go to ring buffer K % 3 with cp.async.bulk (TMA bulk copy), completion on its
 // mbarrier.  Called by one thread.
 __device__ __forceinline__ void issue_row(const World& w, int64_t K, int n_row, unsigned rank, unsigned lgG, int CH,
-                                          int32_t* raw, int RAWW, uint64_t* bars, Ctl* ctl) {
+                                          int32_t* raw, int RAWW, uint64_t* bars, Ctl* ctl, int srank, int sworld) {
   const int b = (int)(K % 3);
-  const int lo = (int)(((uint32_t)n_row * rank) >> lgG), hi = (int)(((uint32_t)n_row * (rank + 1)) >> lgG);
+  // plan shard of this GPU: slots [s0, s1) of the row, then this CTA's part
+  const int s0 = (int)(((int64_t)n_row * srank) / sworld), s1 = (int)(((int64_t)n_row * (srank + 1)) / sworld);
+  const uint32_t len = (uint32_t)(s1 - s0);
+  const int lo = s0 + (int)((len * rank) >> lgG), hi = s0 + (int)((len * (rank + 1)) >> lgG);
   const int e = min(hi, lo + CH);
   const int lo4 = lo & ~3, e4 = (e + 3) & ~3;
   ctl->sl_lo[b] = lo;
@@ -245,6 +248,9 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   Ctl* ctl = reinterpret_cast<Ctl*>(smem + L.o_ctl);
   const int RAWW = L.RAWW, BLK = L.BLK, NOWN = L.NOWN;
   const int4* tw = (w.n_tw <= TW_SMEM) ? s_tw : w.tw;
+  // plan-sharded multi-GPU step: xmode 1 exports this GPU's per-(state, tau)
+  // minima and nearest-plan distance, xmode 2 imports their all-reduced minimum and decides
+  const int xmode = args.xmode;
 
   const bool prof = args.prof != nullptr && rank == 0 && tid == 0;
   unsigned long long pacc[PH_N];
@@ -319,8 +325,8 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       const int64_t K0 = rq.t0 + k;
       const int n0 = row_count(w, K0), n1 = row_count(w, K0 + 1);
       cnt2 = row_count(w, K0 + 2);
-      issue_row(w, K0, n0, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl);
-      issue_row(w, K0 + 1, n1, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl);
+      issue_row(w, K0, n0, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, args.shard_rank, args.shard_world);
+      issue_row(w, K0 + 1, n1, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, args.shard_rank, args.shard_world);
       s_stay[0] = w.sat_d2;
       s_stay[1] = w.sat_d2;
     }
@@ -352,7 +358,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       int4* s_pos = s_pos2 + p * AW;
       if (tid == 0) {
         if (!args.eval && !fin) {
-          issue_row(w, K + 2, cnt2, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl);
+          issue_row(w, K + 2, cnt2, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, args.shard_rank, args.shard_world);
           cnt2 = row_count(w, K + 3);  // consumed next step: latency hidden by this step
         }
         ctl->nsurv[((k + 1) & 1) * 2] = 0;  // step k+1, chunk 0 (last used in step k-1)
@@ -560,7 +566,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           if (tid == 0 && args.pairs) atomicAdd(args.pairs, (unsigned long long)ns * NTAU * AW);
         };
 
-        for (int c0 = 0, cidx = 0; c0 < n; c0 += SC, ++cidx) {
+        for (int c0 = 0, cidx = 0; xmode != 2 && c0 < n; c0 += SC, ++cidx) {
           const int nc = min(SC, n - c0);
           int* counter = &ctl->nsurv[(k & 1) * 2 + (cidx & 1)];
           build(c0, nc, args.cull != 0, counter);
@@ -635,9 +641,12 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         s_stay[p ^ 1] = w.sat_d2;  // written remotely in step k+1, after the cluster barriers of k
       }
       // slice separation minimum -> every CTA; reduce-scatter of the per-action blocks
-      if (tid < (int)G && ctl->stay_local[p] < w.sat_d2)
+      if (xmode == 2) {
+        if (tid == 0) s_stay[p] = args.xbuf[NTAU * AW];  // all-reduced over the GPUs
+      } else if (tid < (int)G && ctl->stay_local[p] < w.sat_d2) {
         atomicMin(cluster.map_shared_rank(&s_stay[p], tid), ctl->stay_local[p]);
-      if (!fin) {
+      }
+      if (!fin && xmode != 2) {
         const int par_off = p * (int)G * NOWN * BLK;
         const int nv = BLK / 4;
         for (int i = tid; i < A * nv; i += NT) {
@@ -650,6 +659,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       }
       cluster.sync();
       FMDP_MARK(PH_BAR1)
+      if (xmode == 1 && rank == 0 && tid == 0) args.xbuf[NTAU * AW] = s_stay[p];
 
       if (!fin) {
         // ---- owner epilogue (half-warp per owned action, lane = substep): G-way minimum of
@@ -685,6 +695,13 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
               for (int t = 0; t < NTAU; ++t) M[t] = fminf(M[t], src[b * sstride + t]);
 #pragma unroll
             for (int t = 0; t < NTAU; ++t) M[t] = fminf(fminf(M[t], M1[t]), fminf(M2[t], M3[t]));
+            if (xmode == 1) {  // this GPU's minima -> export buffer; the decision waits for import
+#pragma unroll
+              for (int t = 0; t < NTAU; ++t) args.xbuf[st * NTAU + t] = __float_as_uint(M[t]);
+            } else if (xmode == 2) {
+#pragma unroll
+              for (int t = 0; t < NTAU; ++t) M[t] = __uint_as_float(args.xbuf[st * NTAU + t]);
+            }
 #pragma unroll
             for (int t = 0; t < NTAU; ++t) {
               if (M[t] < w.R2lo[t]) {
@@ -819,7 +836,10 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       FMDP_MARK(PH_ARGMAX)
       const uint32_t c0 = s_stay[p];
       bool done = false;
-      if (args.eval) {
+      if (xmode == 1) {  // export step: no decision in this launch
+        status = -1;
+        done = true;
+      } else if (args.eval) {
         if (rank == 0 && tid == 0) {
           args.dbg_conf[A] = c0;
           args.dbg_astar[0] = a1;

@@ -78,6 +78,13 @@ class Result(C.Structure):
                 ("min_sep_m", C.c_double), ("n_near_ties", C.c_int32), ("n_exact", C.c_int32)]
 
 
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int32, C.POINTER(C.c_uint32), C.c_int32, C.c_void_p)
+
+
+class Shard(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("allreduce_min_u32", ALLREDUCE_FN), ("user", C.c_void_p)]
+
+
 class Stats(C.Structure):
     _fields_ = [("steps", C.c_int64), ("pair_evals", C.c_int64), ("rounds", C.c_int32), ("reruns", C.c_int32),
                 ("cluster_size", C.c_int32), ("walkers", C.c_int32), ("kernels", C.c_int32),
@@ -88,7 +95,7 @@ PHASES = ("projection", "goal_terrain", "row_wait", "hot_loop", "stage", "reduce
 
 
 EXPORTS = ["fmdp_airspace_default", "fmdp_create", "fmdp_destroy", "fmdp_set_launch", "fmdp_add_plan",
-           "fmdp_add_plans", "fmdp_schedule", "fmdp_schedule_batch", "fmdp_get_steplog", "fmdp_get_plan",
+           "fmdp_add_plans", "fmdp_schedule", "fmdp_schedule_batch", "fmdp_schedule_sharded", "fmdp_get_steplog", "fmdp_get_plan",
            "fmdp_num_plans", "fmdp_truncate", "fmdp_eval_step", "fmdp_get_stats", "fmdp_num_actions",
            "fmdp_strerror", "fmdp_last_error"]
 
@@ -113,6 +120,8 @@ def lib():
         L.fmdp_add_plans.argtypes = [vp, i32, vp, vp, vp, vp, C.POINTER(C.c_uint32)]
         L.fmdp_schedule.argtypes = [vp, C.c_uint64, Vec3, Vec3, i64, C.POINTER(Result), vp, i32]
         L.fmdp_schedule_batch.argtypes = [vp, vp, i32, vp, vp, i32, i32]
+        L.fmdp_schedule_sharded.argtypes = [vp, C.POINTER(Shard), C.c_uint64, Vec3, Vec3, i64, C.POINTER(Result), vp,
+                                            i32]
         L.fmdp_get_steplog.argtypes = [vp, i32, vp, vp, vp, i32, C.POINTER(i32)]
         L.fmdp_get_plan.argtypes = [vp, C.c_uint32, C.POINTER(i64), vp, i32, C.POINTER(i32)]
         L.fmdp_num_plans.argtypes = [vp, C.POINTER(C.c_uint32)]
@@ -322,6 +331,28 @@ class FMDP:
                     "fmdp_schedule_batch")
         return [self._res(res[i], None if traj is None else traj[i]) for i in range(n)]
 
+    def schedule_sharded(self, src, dst, t0: int, rank: int, world: int, allreduce_min, aircraft_id: int = 0,
+                         want_traj: bool = True) -> ScheduleResult:
+        """Plan-sharded request (SURVEY §8(e)): this rank evaluates its shard of every time row;
+        ``allreduce_min(np.ndarray[uint32])`` must replace the array in place by the elementwise
+        minimum over all ranks (see ``allreduce_min_torch``).  Collective over the ranks."""
+        def _cb(ptr, count, user):
+            try:
+                arr = np.ctypeslib.as_array(ptr, shape=(count,))
+                allreduce_min(arr)
+                return 0
+            except Exception:  # reported as FMDP_E_INTERNAL
+                return 1
+
+        cb = ALLREDUCE_FN(_cb)
+        sh = Shard(rank, world, cb, None)
+        cap = self.max_steps + 1
+        traj = np.zeros((cap, 3), np.int32) if want_traj else None
+        r = Result()
+        self._check(self.L.fmdp_schedule_sharded(self.ctx, C.byref(sh), aircraft_id, self._vec(src), self._vec(dst),
+                                                 int(t0), C.byref(r), _p(traj), cap), "fmdp_schedule_sharded")
+        return self._res(r, traj)
+
     def steplog(self, index: int):
         n = C.c_int32()
         cap = self.max_steps + 2
@@ -352,3 +383,18 @@ class FMDP:
         out = {k: getattr(st, k) for k, _ in Stats._fields_ if k != "phase_cycles"}
         out["phase_cycles"] = {p: int(st.phase_cycles[i]) for i, p in enumerate(PHASES)}
         return out
+
+
+def allreduce_min_torch(group=None, device=None):
+    """Elementwise-MIN all-reduce of a uint32 host array over a torch.distributed group
+    (plumbing for ``schedule_sharded``): NCCL when ``device`` is a CUDA device, else gloo."""
+    import torch
+    import torch.distributed as dist
+
+    def f(arr: np.ndarray):
+        t = torch.from_numpy(arr.astype(np.int64))
+        if device is not None:
+            t = t.to(device)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+        arr[:] = t.cpu().numpy().astype(np.uint32)
+    return f

@@ -1,0 +1,50 @@
+"""Multi-process host logic on CPU (gloo, world size 2): the min-all-reduce adapter used by
+the plan-sharded path and bench.py's max-over-ranks timing."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out_dir):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2008_03518_b200.fmdp import allreduce_min_torch
+    import bench
+    rng = np.random.default_rng(100 + rank)
+    v = rng.integers(0, 2 ** 32, size=1351, dtype=np.uint64).astype(np.uint32)
+    v[0] = 0xFFFFFFFF  # saturated entries survive
+    allreduce_min_torch()(v)
+    t = bench.max_over_ranks(float(rank + 1), world)
+    tot = bench.sum_over_ranks(100.0, world)
+    np.save(os.path.join(out_dir, f"r{rank}.npy"), v)
+    np.save(os.path.join(out_dir, f"t{rank}.npy"), np.array([t, tot]))
+    dist.destroy_process_group()
+
+
+def test_gloo_allreduce_min_and_timing(tmp_path):
+    world = 2
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    vs = [np.random.default_rng(100 + r).integers(0, 2 ** 32, size=1351, dtype=np.uint64).astype(np.uint32)
+          for r in range(world)]
+    for v in vs:
+        v[0] = 0xFFFFFFFF
+    want = np.minimum(vs[0], vs[1])
+    for r in range(world):
+        got = np.load(tmp_path / f"r{r}.npy")
+        assert (got == want).all() and got.dtype == np.uint32
+        t, tot = np.load(tmp_path / f"t{r}.npy")
+        assert t == world and tot == 100.0 * world
