@@ -149,6 +149,13 @@ struct InflPair {
   int32_t i, j;                 // request slot i, plan from slot j
 };
 
+struct InflWells {              // exact-conservative influence criterion (a10)
+  int32_t n_tau;
+  int32_t k_tau[NTAU];
+  int64_t r2[NTAU];             // (R_tau + reach + 1)^2
+  int64_t sat2;                 // R_max^2: separation saturation
+};
+
 // Kernel launchers (fmdp_walk.cu).
 cudaError_t launch_walk(const World& w, const WalkArgs& a, int n_climb, int cluster, int n_clusters,
                         int threads, int chunk, int rawcap, cudaStream_t s);
@@ -160,6 +167,6 @@ size_t walk_smem_bytes(const World& w, int n_climb, int threads, int chunk, int 
 cudaError_t launch_append(int32_t* rows, int32_t row_cap, int64_t horizon, const AppendPlan* plans, int n_plans,
                           int max_n, cudaStream_t s);
 cudaError_t launch_influence(const int32_t* traj, int32_t cap, const int32_t* n_states, const int64_t* t0,
-                             const InflPair* pairs, int n_pairs, int64_t bound2, int32_t* kfirst, cudaStream_t s);
+                             const InflPair* pairs, int n_pairs, const InflWells& iw, int32_t* kfirst, cudaStream_t s);
 
 }  // namespace fmdp

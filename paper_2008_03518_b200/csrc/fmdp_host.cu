@@ -47,7 +47,7 @@ struct fmdp_ctx {
   World w{};
   int A = 0, W = 0, C = 0;
   int64_t lo_u[3]{}, hi_u[3]{};
-  int64_t bound2 = 0;
+  fmdp::InflWells iw{};
 
   std::vector<int32_t> counts;  // host mirror of the per-row slot counts (authoritative)
   std::vector<PlanRec> plans;
@@ -428,7 +428,7 @@ fmdp_status influence(fmdp_ctx* ctx, const std::vector<InflPair>& pairs, std::ve
   CK(cudaMemcpyAsync(ctx->d_pairs, pairs.data(), sizeof(InflPair) * pairs.size(), cudaMemcpyHostToDevice,
                      ctx->stream));
   CK(fmdp::launch_influence(ctx->d_traj, ctx->cap_states, ctx->d_nstates, ctx->d_t0s, ctx->d_pairs, (int)pairs.size(),
-                            ctx->bound2, ctx->d_kfirst, ctx->stream));
+                            ctx->iw, ctx->d_kfirst, ctx->stream));
   CK(cudaMemcpyAsync(kf.data(), ctx->d_kfirst, sizeof(int32_t) * pairs.size(), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->stats.kernels += 1;
@@ -492,7 +492,7 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
     // and rolls back any pending request whose computed steps could see a newly committed
     // plan to its first influenced step.  Result: identical to the sequential loop.
     // slice budget: measured optimum on configs[1] (tools/sweep_budget.py)
-    const int budget = ctx->launch.step_budget > 0 ? ctx->launch.step_budget : (ctx->launch.cull ? 256 : 128);
+    const int budget = ctx->launch.step_budget > 0 ? ctx->launch.step_budget : (ctx->launch.cull ? 512 : 128);
     std::vector<char> fin(n, 0);
     std::vector<int> kdone(n, 0);
     int rollbacks = 0;
@@ -793,11 +793,13 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
     const double rc = i < a.n_tau ? std::sqrt((double)w.R2_tau[i]) + w.reach_u + 1.0 : -1.0;
     w.cull2f_tau[i] = i < a.n_tau ? (float)(rc * rc * (1.0 + std::ldexp(1.0, -16))) : -1.0f;
   }
-  int kmax = 0;
-  for (int i = 0; i < a.n_tau; ++i) kmax = std::max(kmax, std::abs(w.k_tau[i]));
-  const int64_t vdyn = (int64_t)std::ceil(std::sqrt(maxd * maxd + (double)maxc * maxc));
-  const int64_t B = Rmax + w.reach_u + (int64_t)kmax * vdyn + 2;
-  ctx->bound2 = B * B;
+  ctx->iw.n_tau = a.n_tau;
+  for (int i = 0; i < a.n_tau; ++i) {
+    const int64_t R = std::llround(std::sqrt((double)w.R2_tau[i])) + w.reach_u + 1;
+    ctx->iw.k_tau[i] = w.k_tau[i];
+    ctx->iw.r2[i] = R * R;
+  }
+  ctx->iw.sat2 = Rmax * Rmax;
 
   // device memory
   const size_t row_words = (size_t)4 * w.row_cap;

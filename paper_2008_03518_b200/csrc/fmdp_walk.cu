@@ -90,8 +90,8 @@ __device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
   return d;
 }
 __device__ __forceinline__ f2 hi_far(f2 v) {  // replace the high float by a far-away coordinate
-  float lo, hi;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  float lo;
+  asm("mov.b64 {%0, _}, %1;" : "=f"(lo) : "l"(v));
   return pk2(lo, 3.0e18f);
 }
 __device__ __forceinline__ float min3(float a, f2 p) {
@@ -961,11 +961,13 @@ __global__ void append_kernel(int32_t* rows, int32_t cap, int64_t horizon, const
   }
 }
 
-// First step k of request i whose computation could see plan j: step k reads only row
-// K = t0_i + k (wells around the projected states, and the exact separation test of state
-// k), so it is unaffected unless |q_i(k) - p_j(K)| < bound (DESIGN.md a10).  INT_MAX if none.
+// First step k of request i whose computation could see plan j, or INT_MAX.  Step k reads
+// only row K = t0_i + k: plan j can change it only if one of its wells c_tau = p + k_tau v
+// comes within R_tau + reach + 1 of q_i(k) (else it is >= R_tau + 1 from every projected
+// state: clearly outside the FP32 band, the same argument as f1 culling), or if p itself is
+// within the separation saturation radius R_max of q_i(k).  Exact-conservative (DESIGN.md a10).
 __global__ void influence_kernel(const int32_t* traj, int32_t cap, const int32_t* n_states, const int64_t* t0,
-                                 const InflPair* pairs, int64_t bound2, int32_t* kfirst) {
+                                 const InflPair* pairs, InflWells iw, int32_t* kfirst) {
   __shared__ int32_t best;
   const InflPair pr = pairs[blockIdx.x];
   if (threadIdx.x == 0) best = INT_MAX;
@@ -979,8 +981,19 @@ __global__ void influence_kernel(const int32_t* traj, int32_t cap, const int32_t
   for (int64_t k = k_lo + threadIdx.x; k < k_hi; k += blockDim.x) {
     if (k >= best) break;
     const int64_t idx = ti + k - tj;
-    const int64_t dx = qi[3 * k] - pj[3 * idx], dy = qi[3 * k + 1] - pj[3 * idx + 1], dz = qi[3 * k + 2] - pj[3 * idx + 2];
-    if (dx * dx + dy * dy + dz * dz < bound2) atomicMin(&best, (int32_t)k);
+    const int32_t* p = pj + 3 * idx;
+    int64_t vx = 0, vy = 0, vz = 0;  // forward difference (R11)
+    if (nj > 1) {
+      const int32_t* a = idx < nj - 1 ? p : p - 3;
+      vx = a[3] - a[0]; vy = a[4] - a[1]; vz = a[5] - a[2];
+    }
+    const int64_t rx = (int64_t)p[0] - qi[3 * k], ry = (int64_t)p[1] - qi[3 * k + 1], rz = (int64_t)p[2] - qi[3 * k + 2];
+    bool hit = rx * rx + ry * ry + rz * rz < iw.sat2;
+    for (int t = 0; t < iw.n_tau && !hit; ++t) {
+      const int64_t cx = rx + iw.k_tau[t] * vx, cy = ry + iw.k_tau[t] * vy, cz = rz + iw.k_tau[t] * vz;
+      hit = cx * cx + cy * cy + cz * cz < iw.r2[t];
+    }
+    if (hit) atomicMin(&best, (int32_t)k);
   }
   __syncthreads();
   if (threadIdx.x == 0) kfirst[blockIdx.x] = best;
@@ -1083,9 +1096,9 @@ cudaError_t launch_append(int32_t* rows, int32_t row_cap, int64_t horizon, const
 }
 
 cudaError_t launch_influence(const int32_t* traj, int32_t cap, const int32_t* n_states, const int64_t* t0,
-                             const InflPair* pairs, int n_pairs, int64_t bound2, int32_t* kfirst, cudaStream_t s) {
+                             const InflPair* pairs, int n_pairs, const InflWells& iw, int32_t* kfirst, cudaStream_t s) {
   if (n_pairs <= 0) return cudaSuccess;
-  influence_kernel<<<n_pairs, 256, 0, s>>>(traj, cap, n_states, t0, pairs, bound2, kfirst);
+  influence_kernel<<<n_pairs, 256, 0, s>>>(traj, cap, n_states, t0, pairs, iw, kfirst);
   return cudaGetLastError();
 }
 
