@@ -545,22 +545,29 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       m[cc_][T] = min3(m[cc_][T], fma2(dz, dz, hh));          \
     }                                                         \
   }
-          const int np = (ns + 1) >> 1;
-          for (int pp = grp; pp < np; pp += NGW) {
-            const ulonglong2* c8 = cen2 + (PAIR_STRIDE / 4) * pp;
-            ulonglong2 e0 = c8[0], e1 = c8[1], e2 = c8[2], e3 = c8[3], e4 = c8[4], e5 = c8[5], e6 = c8[6], e7 = c8[7];
-            if (2 * pp + 1 == ns) {  // odd tail: the partner slot is a well at infinity
-              e0.x = hi_far(e0.x); e0.y = hi_far(e0.y); e1.x = hi_far(e1.x); e1.y = hi_far(e1.y);
-              e2.x = hi_far(e2.x); e2.y = hi_far(e2.y); e3.x = hi_far(e3.x); e3.y = hi_far(e3.y);
-              e4.x = hi_far(e4.x); e4.y = hi_far(e4.y); e5.x = hi_far(e5.x); e5.y = hi_far(e5.y);
-              e6.x = hi_far(e6.x); e6.y = hi_far(e6.y); e7.x = hi_far(e7.x);
-            }
+          const int npf = ns >> 1;  // full pairs; an odd tail is peeled below
+          const ulonglong2* c8 = cen2 + (PAIR_STRIDE / 4) * grp;
+          for (int pp = grp; pp < npf; pp += NGW, c8 += (PAIR_STRIDE / 4) * NGW) {
+            const ulonglong2 e0 = c8[0], e1 = c8[1], e2 = c8[2], e3 = c8[3], e4 = c8[4], e5 = c8[5], e6 = c8[6],
+                             e7 = c8[7];
             FMDP_WELL2(0, e0.x, e0.y, e1.x)
             FMDP_WELL2(1, e1.y, e2.x, e2.y)
             FMDP_WELL2(2, e3.x, e3.y, e4.x)
             FMDP_WELL2(3, e4.y, e5.x, e5.y)
             FMDP_WELL2(4, e6.x, e6.y, e7.x)
-            (void)e7;
+          }
+          if ((ns & 1) && npf % NGW == grp) {  // odd tail: the partner slot is a well at infinity
+            const ulonglong2* t8 = cen2 + (PAIR_STRIDE / 4) * npf;
+            ulonglong2 e0 = t8[0], e1 = t8[1], e2 = t8[2], e3 = t8[3], e4 = t8[4], e5 = t8[5], e6 = t8[6], e7 = t8[7];
+            e0.x = hi_far(e0.x); e0.y = hi_far(e0.y); e1.x = hi_far(e1.x); e1.y = hi_far(e1.y);
+            e2.x = hi_far(e2.x); e2.y = hi_far(e2.y); e3.x = hi_far(e3.x); e3.y = hi_far(e3.y);
+            e4.x = hi_far(e4.x); e4.y = hi_far(e4.y); e5.x = hi_far(e5.x); e5.y = hi_far(e5.y);
+            e6.x = hi_far(e6.x); e6.y = hi_far(e6.y); e7.x = hi_far(e7.x);
+            FMDP_WELL2(0, e0.x, e0.y, e1.x)
+            FMDP_WELL2(1, e1.y, e2.x, e2.y)
+            FMDP_WELL2(2, e3.x, e3.y, e4.x)
+            FMDP_WELL2(3, e4.y, e5.x, e5.y)
+            FMDP_WELL2(4, e6.x, e6.y, e7.x)
           }
 #undef FMDP_WELL2
           if (tid == 0 && args.pairs) atomicAdd(args.pairs, (unsigned long long)ns * NTAU * AW);

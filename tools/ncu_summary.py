@@ -1,0 +1,96 @@
+"""Summarise gpurun_out ncu captures into profiles/<round>_ncu_summary.md (+ traffic json)."""
+import collections, csv, io, json, subprocess, sys
+
+rnd = sys.argv[1] if len(sys.argv) > 1 else "r01"
+WANT = ['gpu__time_duration.sum', 'launch__grid_size', 'launch__cluster_size', 'launch__block_size',
+        'launch__registers_per_thread', 'dram__bytes_read.sum', 'dram__bytes_write.sum', 'lts__t_bytes.sum',
+        'sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active',
+        'sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active',
+        'sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active',
+        'sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active',
+        'smsp__issue_active.avg.pct_of_peak_sustained_active', 'sm__warps_active.avg.pct_of_peak_sustained_active',
+        'smsp__inst_executed.sum']
+
+
+def raw(rep):
+    out = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
+    rr = list(csv.reader(io.StringIO(out)))
+    return {h: (v, u) for h, u, v in zip(rr[0], rr[1], rr[2])}
+
+
+def source(rep):
+    out = subprocess.run(['ncu', '-i', rep, '--page', 'source', '--csv', '--print-source', 'sass'],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    return rows[1], rows[2:]
+
+
+def stalls(hdr, data, a, b):
+    cols = [c for c in hdr if c.startswith("stall_") and "Not Issued" not in c]
+    s = collections.Counter()
+    for r in data[a:b]:
+        for c in cols:
+            s[c[6:]] += float(r[hdr.index(c)] or 0)
+    t = sum(s.values()) or 1
+    return {k: v / t * 100 for k, v in s.items() if v / t > 0.01}
+
+
+lines = [f"# {rnd} — ncu evidence (B200, sm_100a)\n",
+         "Captures (`ncu --set full --clock-control none --import-source on -k regex:walk_kernel -c 1`):",
+         "- `walk_batch`: first walk launch of the configs[1] FCFS batch (`tools/ncu_batch.py`: 100 requests x",
+         "  128-step slice, one single-CTA walker per request) — the bench's dominant kernel, §8(a) path;",
+         "- `walk_cull2`: one configs[1] request with SURVEY f1 culling on a 2-CTA cluster (`tools/ncu_cull.py 2`).",
+         "Launch list: `ncu --metrics gpu__time_duration.sum --clock-control none` of `python bench.py --steps 1",
+         "--warmup 3 --no-cpu-baseline` (cold-cache, serialised: compare shares, not absolutes).\n"]
+rows = list(csv.reader(open('gpurun_out/launches.csv')))
+hi = [i for i, r in enumerate(rows) if r and r[0] == 'ID'][0]
+hdr = rows[hi]; data = rows[hi + 1:]
+ik, iv, im = hdr.index('Kernel Name'), hdr.index('Metric Value'), hdr.index('Metric Name')
+t = collections.defaultdict(float); n = collections.Counter()
+for r in data:
+    if len(r) <= iv or r[im] != 'gpu__time_duration.sum':
+        continue
+    name = r[ik].split('(')[0].replace('void ', '')
+    t[name] += float(r[iv].replace(',', '')); n[name] += 1
+tot = sum(t.values())
+lines += ["## Launch list of the bench command\n", "| kernel | launches | device time (ms) | share |", "|---|---|---|---|"]
+for k in sorted(t, key=lambda k: -t[k]):
+    lines.append(f"| `{k}` | {n[k]} | {t[k] / 1e6:.2f} | {t[k] / tot * 100:.1f}% |")
+lines.append("")
+traffic = None
+for rep, title in (('walk_batch', 'configs[1] batch slice, 100 walkers x G=1 (full path)'),
+                   ('walk_cull2', 'configs[1] request, f1 culling, G=2')):
+    m = raw(f'gpurun_out/{rep}.ncu-rep')
+    lines += [f"## walk_kernel<3> — {title}\n", "| metric | value |", "|---|---|"]
+    for k in WANT:
+        if k in m:
+            lines.append(f"| `{k}` | {m[k][0]} {m[k][1]} |")
+    if rep == 'walk_batch':
+        rd = float(m['dram__bytes_read.sum'][0].replace(',', '')) * (1e6 if m['dram__bytes_read.sum'][1] == 'Mbyte' else 1e3 if m['dram__bytes_read.sum'][1] == 'Kbyte' else 1e9 if m['dram__bytes_read.sum'][1] == 'Gbyte' else 1)
+        wr = float(m['dram__bytes_write.sum'][0].replace(',', '')) * (1e6 if m['dram__bytes_write.sum'][1] == 'Mbyte' else 1e3 if m['dram__bytes_write.sum'][1] == 'Kbyte' else 1e9 if m['dram__bytes_write.sum'][1] == 'Gbyte' else 1)
+        traffic = dict(kernel="walk_kernel<3>", capture=f"{rnd} walk_batch (tools/ncu_batch.py, first launch)",
+                       dram_bytes_read=int(rd), dram_bytes_write=int(wr), per_launch_bytes=int(rd + wr),
+                       note="DRAM traffic per launch; the kernel is FP32-pipe bound, plan rows are L2-resident")
+    h, d = source(f'gpurun_out/{rep}.ncu-rep')
+    iss = h.index("Warp Stall Sampling (All Samples)"); ie = h.index("Instructions Executed"); isrc = h.index("Source")
+    ex = [float(r[ie] or 0) for r in d]
+    mx = max(ex)
+    hot = [i for i, e in enumerate(ex) if e >= 0.9 * mx]
+    a, b = min(hot), max(hot) + 1
+    ts = sum(float(r[iss] or 0) for r in d)
+    hs = sum(float(r[iss] or 0) for r in d[a:b])
+    st = stalls(h, d, a, b)
+    allst = stalls(h, d, 0, len(d))
+    ops = collections.Counter()
+    for r in d[a:b]:
+        tok = r[isrc].split()
+        op = tok[1] if tok and tok[0].startswith('@') else (tok[0] if tok else '')
+        ops[op.split('.')[0]] += 1
+    lines += ["", f"Most-executed loop: {b - a} SASS instructions, {hs / ts * 100:.1f} % of warp-stall samples; "
+              + "reasons: " + ", ".join(f"{k} {v:.1f}%" for k, v in sorted(st.items(), key=lambda x: -x[1])) + ".",
+              "Instruction mix: " + ", ".join(f"{k} {v}" for k, v in ops.most_common()) + ".",
+              "Whole kernel: " + ", ".join(f"{k} {v:.1f}%" for k, v in sorted(allst.items(), key=lambda x: -x[1])) + ".", ""]
+open(f'profiles/{rnd}_ncu_summary.md', 'w').write("\n".join(lines) + "\n")
+if traffic:
+    json.dump(traffic, open(f'profiles/{rnd}_traffic.json', 'w'), indent=1)
+print("\n".join(lines))
