@@ -235,8 +235,39 @@ def run_native(args):
                     walk_ms=sum(s["device_ms"] for s in st_all), pairs=sum(s["pair_evals"] for s in st_all),
                     launches=sum(s["kernels"] for s in st_all), steps_dev=sum(s["steps"] for s in st_all))
 
+    def measure_departures(n_req=8, delays=tuple(range(0, 400, 50))):
+        # each request tried at len(delays) departures in one call, earliest accepted kept
+        ctx.set_launch(cull=1)
+        sub = [(sc.src[i], sc.dst[i], int(sc.t0[i])) for i in range(n_req)]
+
+        def run():
+            chosen = []
+            with torch.cuda.stream(stream):
+                ev0.record(stream)
+                for s_, d_, t_ in sub:
+                    chosen.append(ctx.schedule_departures(s_, d_, t_, delays, want_traj=False)[1])
+                ev1.record(stream)
+            ev1.synchronize()
+            return chosen, ev0.elapsed_time(ev1)
+        for _ in range(args.warmup):
+            run()
+            reset()
+        times, chosen = [], []
+        for _ in range(args.steps):
+            chosen, ms = run()
+            times.append(ms)
+            reset()
+        tot = max_over_ranks(sum(times), world)
+        return {"what": "SURVEY f3: each request scheduled at 8 candidate departures (t0 + 0..350 steps) in one "
+                        "walk against the same store; the earliest accepted is appended "
+                        "(tests/test_gpu_parity.py::test_departure_candidates)",
+                "value": sum_over_ranks(n_req * args.steps, world) / (tot / 1e3), "unit": "requests/s",
+                "candidates_per_request": len(delays), "requests_per_step": n_req, "cull": 1,
+                "ms_per_request": tot / args.steps / n_req, "chosen_delay_index": chosen}
+
     M = measure(0)       # every (state, well) pair evaluated
     Mc = measure(1)      # exact culling, bit-identical outputs
+    Md = measure_departures()
     h2d = n * C_REQUEST_BYTES
     tot_ms, value, e2e_value, d2h = M["tot_ms"], M["value"], M["e2e_value"], M["d2h"]
     stats = M["st_all"][-1]
@@ -290,6 +321,7 @@ def run_native(args):
             "walk_device_ms_per_step": Mc["walk_ms"] / args.steps,
             "pair_evals_per_step": Mc["pairs"] / args.steps, "gpu_launches": Mc["launches"],
             "same_results_as_full": same, "clocks": Mc["clocks"]},
+        "f3_departures": Md,
     }
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(sc, args.cpu_sample_s)

@@ -227,6 +227,16 @@ fmdp_status fmdp_schedule_sharded(fmdp_ctx* ctx, const fmdp_shard* shard, uint64
                                   fmdp_vec3 dst, int64_t t0_step, fmdp_result* res, fmdp_qpos* traj,
                                   int32_t traj_cap);
 
+/* Departure-time candidates ("recommended take-off time"):
+ * schedule one request for n_delays candidate departures t0_step + delays[i] in parallel, all
+ * against the current store (the candidates are alternatives, they do not see each other);
+ * the accepted candidate with the earliest departure (ties: lowest index) is appended and its
+ * index returned in *chosen (-1 if none).  res[n_delays]; traj: n_delays * traj_cap states or
+ * NULL.  Each res[i] equals fmdp_schedule of that candidate alone (without the append). */
+fmdp_status fmdp_schedule_departures(fmdp_ctx* ctx, uint64_t aircraft_id, fmdp_vec3 src, fmdp_vec3 dst,
+                                     int64_t t0_step, int32_t n_delays, const int64_t* delays, fmdp_result* res,
+                                     fmdp_qpos* traj, int32_t traj_cap, int32_t* chosen);
+
 /* Per-step log of the last trajectory of request `index` of the last schedule /
  * schedule_batch call: action a*_k, heading psi_k, and near-tie flag per step (k < n).
  * Any pointer may be NULL. */

@@ -1067,6 +1067,59 @@ fmdp_status fmdp_schedule_sharded(fmdp_ctx* ctx, const fmdp_shard* shard, uint64
   return FMDP_OK;
 }
 
+fmdp_status fmdp_schedule_departures(fmdp_ctx* ctx, uint64_t aircraft_id, fmdp_vec3 src, fmdp_vec3 dst,
+                                     int64_t t0_step, int32_t n_delays, const int64_t* delays, fmdp_result* res,
+                                     fmdp_qpos* traj, int32_t traj_cap, int32_t* chosen) {
+  if (!ctx || n_delays < 1 || !delays || !res || !chosen) return fail(ctx, FMDP_E_ARG, "null argument");
+  if (traj && traj_cap < ctx->w.max_steps + 1) return fail(ctx, FMDP_E_BUFFER, "traj_cap must be >= max_steps + 1");
+  std::memset(&ctx->stats, 0, sizeof(ctx->stats));
+  *chosen = -1;
+  std::vector<fmdp_request> rq(n_delays);
+  for (int i = 0; i < n_delays; ++i) {
+    rq[i].aircraft_id = aircraft_id;
+    rq[i].src = src;
+    rq[i].dst = dst;
+    rq[i].t0_step = t0_step + delays[i];
+  }
+  std::vector<Req> base;
+  fmdp_status st = prepare_requests(ctx, rq.data(), n_delays, base);
+  if (st) return st;
+  if ((st = ensure_slots(ctx, n_delays))) return st;
+  CK(cudaMemsetAsync(ctx->d_pairctr, 0, sizeof(unsigned long long), ctx->stream));
+  // every candidate against the same store: one walk over all of them, no commits in between
+  if ((st = run_walk(ctx, base, false))) return st;
+  if ((st = fetch_out(ctx, n_delays))) return st;
+  ctx->stats.rounds = 1;
+  int best = -1;
+  for (int i = 0; i < n_delays; ++i) {
+    ctx->stats.steps += ctx->h_out[i].steps_run;
+    if (ctx->h_out[i].status == FMDP_ACCEPTED && (best < 0 || base[i].t0 < base[best].t0)) best = i;
+  }
+  std::vector<uint32_t> plan_id(n_delays, 0xffffffffu);
+  std::vector<uint64_t> aircraft(n_delays, aircraft_id);
+  if (best >= 0 && (st = commit_slots(ctx, {best}, base, aircraft, plan_id))) return st;
+  *chosen = best;
+  for (int i = 0; i < n_delays; ++i) {
+    const Out& o = ctx->h_out[i];
+    res[i].status = o.status;
+    res[i].plan_id = plan_id[i];
+    res[i].n_states = o.n_states;
+    res[i].fail_step = o.fail_step;
+    res[i].min_sep_m = std::sqrt((double)o.min_sep_d2) * ctx->air.u_m;
+    res[i].n_near_ties = o.n_near_ties;
+    res[i].n_exact = o.n_exact;
+    if (traj)
+      CK(cudaMemcpyAsync(traj + (size_t)i * traj_cap, ctx->d_traj + (size_t)i * ctx->cap_states * 3,
+                         sizeof(fmdp_qpos) * o.n_states, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  unsigned long long pc = 0;
+  CK(cudaMemcpy(&pc, ctx->d_pairctr, sizeof(pc), cudaMemcpyDeviceToHost));
+  ctx->stats.pair_evals = (int64_t)pc;
+  ctx->last_n = n_delays;
+  return FMDP_OK;
+}
+
 fmdp_status fmdp_schedule_batch(fmdp_ctx* ctx, const fmdp_request* reqs, int32_t n, fmdp_result* res,
                                 fmdp_qpos* traj, int32_t traj_cap_each, int32_t flags) {
   return schedule_many(ctx, reqs, n, res, traj, traj_cap_each, flags);

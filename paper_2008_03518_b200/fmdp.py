@@ -95,7 +95,8 @@ PHASES = ("projection", "goal_terrain", "row_wait", "hot_loop", "stage", "reduce
 
 
 EXPORTS = ["fmdp_airspace_default", "fmdp_create", "fmdp_destroy", "fmdp_set_launch", "fmdp_add_plan",
-           "fmdp_add_plans", "fmdp_schedule", "fmdp_schedule_batch", "fmdp_schedule_sharded", "fmdp_get_steplog", "fmdp_get_plan",
+           "fmdp_add_plans", "fmdp_schedule", "fmdp_schedule_batch", "fmdp_schedule_sharded",
+           "fmdp_schedule_departures", "fmdp_get_steplog", "fmdp_get_plan",
            "fmdp_num_plans", "fmdp_truncate", "fmdp_eval_step", "fmdp_get_stats", "fmdp_num_actions",
            "fmdp_strerror", "fmdp_last_error"]
 
@@ -120,6 +121,7 @@ def lib():
         L.fmdp_add_plans.argtypes = [vp, i32, vp, vp, vp, vp, C.POINTER(C.c_uint32)]
         L.fmdp_schedule.argtypes = [vp, C.c_uint64, Vec3, Vec3, i64, C.POINTER(Result), vp, i32]
         L.fmdp_schedule_batch.argtypes = [vp, vp, i32, vp, vp, i32, i32]
+        L.fmdp_schedule_departures.argtypes = [vp, C.c_uint64, Vec3, Vec3, i64, i32, vp, vp, vp, i32, C.POINTER(i32)]
         L.fmdp_schedule_sharded.argtypes = [vp, C.POINTER(Shard), C.c_uint64, Vec3, Vec3, i64, C.POINTER(Result), vp,
                                             i32]
         L.fmdp_get_steplog.argtypes = [vp, i32, vp, vp, vp, i32, C.POINTER(i32)]
@@ -352,6 +354,20 @@ class FMDP:
         self._check(self.L.fmdp_schedule_sharded(self.ctx, C.byref(sh), aircraft_id, self._vec(src), self._vec(dst),
                                                  int(t0), C.byref(r), _p(traj), cap), "fmdp_schedule_sharded")
         return self._res(r, traj)
+
+    def schedule_departures(self, src, dst, t0: int, delays, aircraft_id: int = 0, want_traj: bool = True):
+        """SURVEY f3: candidate departures t0 + delays[i] in parallel against the current store;
+        returns (results, chosen index or -1); the chosen candidate is appended."""
+        d = np.ascontiguousarray(delays, np.int64)
+        n = len(d)
+        res = (Result * n)()
+        cap = self.max_steps + 1
+        traj = np.zeros((n, cap, 3), np.int32) if want_traj else None
+        ch = C.c_int32()
+        self._check(self.L.fmdp_schedule_departures(self.ctx, aircraft_id, self._vec(src), self._vec(dst), int(t0), n,
+                                                    _p(d), C.cast(res, C.c_void_p), _p(traj), cap, C.byref(ch)),
+                    "fmdp_schedule_departures")
+        return [self._res(res[i], None if traj is None else traj[i]) for i in range(n)], int(ch.value)
 
     def steplog(self, index: int):
         n = C.c_int32()

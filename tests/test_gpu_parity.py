@@ -290,3 +290,31 @@ def test_cull_bit_identical_batch(F):
         assert x.status == y.status and x.n_states == y.n_states and (x.traj == y.traj).all()
         assert x.min_sep_m == y.min_sep_m and x.n_near_ties == y.n_near_ties
     assert pairs_cull < pairs_full
+
+
+# ----------------------------------------------------------------------------- f3: departure candidates
+def test_departure_candidates(F):
+    """every candidate equals an isolated fmdp_schedule of that departure against
+    the same store; the earliest accepted candidate is the one appended; oracle replay."""
+    sc = fs.random_small(81, n_plans=120, n_requests=1, half_m=1500.0, n_buildings=20, max_steps=500, t0_max=10)
+    delays = [0, 30, 60, 90, 120, 150, 180, 210]
+    ctx = ctx_for(F, sc)
+    n0 = ctx.num_plans()
+    res, chosen = ctx.schedule_departures(sc.src[0], sc.dst[0], int(sc.t0[0]), delays)
+    ref = ctx_for(F, sc)
+    orc = O.for_scenario(sc)
+    for i, d in enumerate(delays):
+        r = ref.schedule(sc.src[0], sc.dst[0], int(sc.t0[0]) + d)
+        ref.truncate(n0)
+        assert r.status == res[i].status and r.n_states == res[i].n_states and (r.traj == res[i].traj).all()
+    acc = [i for i, r in enumerate(res) if r.accepted]
+    assert chosen == (min(acc, key=lambda i: delays[i]) if acc else -1)
+    assert ctx.num_plans() == n0 + (1 if acc else 0)
+    if acc:
+        t0, st = ctx.get_plan(n0)
+        assert t0 == int(sc.t0[0]) + delays[chosen] and (st == res[chosen].traj).all()
+        ast, hd, _ = ctx.steplog(chosen)
+        rp = orc.replay(sc.src[0], sc.dst[0], t0, res[chosen].traj, hd, ast, 0)
+        assert rp.n_fail == 0
+    ctx.close()
+    ref.close()
