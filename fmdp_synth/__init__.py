@@ -340,3 +340,26 @@ def config_c5(seed: int = 5, n_plans: int = 1_000_000, rows: int = 3000, n_reque
     pads = vertiports(rng, 40, 5000.0, terrain)
     src, dst, t0 = request_pairs(rng, pads, n_requests, 4500.0, 5500.0, (0, 1))
     return Scenario(a, terrain, plans, src, dst, t0, name="c5")
+
+
+def cosim_ring(seed: int, n_batch: int, n_plans: int = 100, radius_m: float = 1200.0, half_m: float = 4000.0,
+               z_m: float = 150.0, t0_max: int = 60, rows: int = 1200, max_steps: int = 800, jitter_deg: float = 6.0,
+               **air) -> Scenario:
+    """SURVEY f2 (co-simulated batch, Fig perf2: batch sizes 1-20 against 100 intruders):
+    n_batch aircraft on a ring of radius_m at one altitude, each bound for the (jittered)
+    opposite point, departures U[0, t0_max) steps, so their straight paths cross near the
+    centre; n_plans reflecting-line intruders in the box.  No terrain."""
+    rng = np.random.default_rng(seed)
+    a = Airspace(max_steps=max_steps, lo_m=(-half_m, -half_m, 0.0), hi_m=(half_m, half_m, 2 * z_m + 200.0),
+                 horizon_steps=int(rows + max_steps + t0_max + 8),
+                 row_capacity=(max(64, n_plans + n_batch + 8) + 3) // 4 * 4)
+    a = a.replace(**air)
+    lo, hi = m2u(a.lo_m), m2u(a.hi_m)
+    plans = reflecting_lines(rng, n_plans, lo, hi, (0, rows), z_lo_u=int(m2u(40)), z_hi_u=int(m2u(2 * z_m + 160)))
+    ang = 2 * np.pi * (np.arange(n_batch) + rng.uniform(0, 1)) / max(1, n_batch)
+    jit = np.deg2rad(rng.uniform(-jitter_deg, jitter_deg, n_batch))
+    src = np.stack([radius_m * np.cos(ang), radius_m * np.sin(ang), np.full(n_batch, z_m)], 1)
+    dst = np.stack([radius_m * np.cos(ang + np.pi + jit), radius_m * np.sin(ang + np.pi + jit), np.full(n_batch, z_m)], 1)
+    t0 = rng.integers(0, max(1, t0_max), n_batch).astype(np.int64)
+    return Scenario(a, Terrain(), plans, m2u(src).astype(np.int32), m2u(dst).astype(np.int32), t0,
+                    name=f"cosim{seed}x{n_batch}")

@@ -286,6 +286,12 @@ static int terrain_collision(const orc_terrain* T, const int32_t q[3]) {
 /* ------------------------------------------------------------------------- */
 int orc_eval_step(const orc_params* p, const orc_terrain* T, const orc_store* S,
                   const int32_t q[3], int32_t psi, const int32_t g[3], int64_t K, orc_step_out* out) {
+  return orc_eval_step_peers(p, T, S, q, psi, g, K, 0, NULL, NULL, out);
+}
+
+int orc_eval_step_peers(const orc_params* p, const orc_terrain* T, const orc_store* S,
+                        const int32_t q[3], int32_t psi, const int32_t g[3], int64_t K, int32_t n_peer,
+                        const int32_t* peer_pos, const int32_t* peer_vel, orc_step_out* out) {
   conv c;
   if (convert(p, &c) || !out) return ORC_E_ARG;
   const int A = p->n_turn * p->n_climb, W = p->W, AW = A * W;
@@ -299,8 +305,9 @@ int orc_eval_step(const orc_params* p, const orc_terrain* T, const orc_store* S,
   double* scale = (double*)malloc(sizeof(double) * AW);
   double* vstar = (double*)malloc(sizeof(double) * A);
   double* vsc = (double*)malloc(sizeof(double) * A);
+  double* vneg = (double*)malloc(sizeof(double) * AW);
   int rc = ORC_OK;
-  if (!proj || !ppsi || !vpos || !vint || !vter || !valt || !v || !scale || !vstar || !vsc) {
+  if (!proj || !ppsi || !vpos || !vint || !vter || !valt || !v || !scale || !vstar || !vsc || !vneg) {
     rc = ORC_E_NOMEM;
     goto done;
   }
@@ -340,6 +347,21 @@ int orc_eval_step(const orc_params* p, const orc_terrain* T, const orc_store* S,
     }
   }
 
+  /* Process negative rewards (Alg 5): five wells per batch peer (P^-, Alg 2
+   * P:464-466), same peak parameters as an intruder (Table PK aircraft row). */
+  for (int i = 0; i < AW; ++i) vneg[i] = 0.0;
+  for (int32_t j = 0; j < n_peer; ++j) {
+    int32_t cen[3 * ORC_MAX_TAU];
+    int64_t rad[ORC_MAX_TAU];
+    orc_build_wells(p, &peer_pos[3 * j], &peer_vel[3 * j], cen, rad);
+    for (int tau = 0; tau < p->n_tau; ++tau) {
+      for (int i = 0; i < AW; ++i) {
+        double V = orc_well_value(p->intr_r, p->intr_gamma, p->u_m, d2_of(&proj[3 * i], &cen[3 * tau]), rad[tau]);
+        if (V > vneg[i]) vneg[i] = V;
+      }
+    }
+  }
+
   /* Hard deck (Alg 1; Alg 8). */
   for (int i = 0; i < AW; ++i) valt[i] = orc_deck_penalty(p, proj[3 * i + 2]);
 
@@ -351,6 +373,7 @@ int orc_eval_step(const orc_params* p, const orc_terrain* T, const orc_store* S,
     for (int t = 0; t < W; ++t) {
       int i = a * W + t;
       double neg = vter[i] > vint[i] ? vter[i] : vint[i];
+      if (vneg[i] > neg) neg = vneg[i];
       v[i] = vpos[i] - neg - valt[i];
       scale[i] = vpos[i] + neg + valt[i];
       if (v[i] > vmax) vmax = v[i];
@@ -382,6 +405,7 @@ int orc_eval_step(const orc_params* p, const orc_terrain* T, const orc_store* S,
 
   if (out->v_pos) memcpy(out->v_pos, vpos, sizeof(double) * AW);
   if (out->v_int) memcpy(out->v_int, vint, sizeof(double) * AW);
+  if (out->v_neg) memcpy(out->v_neg, vneg, sizeof(double) * AW);
   if (out->v_ter) memcpy(out->v_ter, vter, sizeof(double) * AW);
   if (out->v_alt) memcpy(out->v_alt, valt, sizeof(double) * AW);
   if (out->v) memcpy(out->v, v, sizeof(double) * AW);
@@ -393,7 +417,7 @@ int orc_eval_step(const orc_params* p, const orc_terrain* T, const orc_store* S,
 
 done:
   free(proj); free(ppsi); free(vpos); free(vint); free(vter); free(valt);
-  free(v); free(scale); free(vstar); free(vsc);
+  free(v); free(scale); free(vstar); free(vsc); free(vneg);
   return rc;
 }
 
@@ -541,4 +565,219 @@ int orc_replay(const orc_params* p, const orc_terrain* T, const orc_store* S,
 #undef FAIL
   free(vstar); free(vsc); free(proj); free(ppsi);
   return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Co-simulated batch.                                             */
+/* ------------------------------------------------------------------------- */
+
+/* Linear velocity of a batch aircraft at its state k ("position and the linear velocity";
+ * DESIGN.md R28): the displacement of its last transition, q(k) - q(k-1); at departure (k = 0)
+ * the initial heading at level flight, (DX, DY)[psi_0], climb 0. */
+static void peer_velocity(const int32_t* DX, const int32_t* DY, const int32_t* traj, const int32_t* heading,
+                          int32_t k, int32_t vel[3]) {
+  if (k == 0) {
+    vel[0] = DX[heading[0]];
+    vel[1] = DY[heading[0]];
+    vel[2] = 0;
+  } else {
+    for (int d = 0; d < 3; ++d) vel[d] = traj[3 * k + d] - traj[3 * (k - 1) + d];
+  }
+}
+
+/* Terminal verdict of a state (Sec IV.I; Table DS "Determine terminal state" N x N):
+ * separation against the store row K and against every other present batch aircraft. */
+static int cosim_verdict(const orc_terrain* T, const orc_store* S, const int32_t q[3], const int32_t dst[3],
+                         int64_t K, int32_t k, int32_t max_steps, int32_t n_peer, const int32_t* peer_pos,
+                         int64_t sat, int64_t sep2, int64_t cap2, int64_t* nd_out) {
+  int64_t nd = nearest_d2(S, q, K, sat);
+  for (int32_t j = 0; j < n_peer; ++j) {
+    int64_t d2 = d2_of(q, &peer_pos[3 * j]);
+    if (d2 < nd) nd = d2;
+  }
+  *nd_out = nd;
+  if (nd < sep2) return ORC_REJ_CONFLICT;
+  if (terrain_collision(T, q)) return ORC_REJ_TERRAIN;
+  if (d2_of(q, dst) < cap2) return ORC_ACCEPTED;
+  if (k >= max_steps) return ORC_REJ_TIMEOUT;
+  return -1;
+}
+
+int orc_cosim(const orc_params* p, const orc_terrain* T, const orc_store* S, int32_t n,
+              const int32_t* src, const int32_t* dst, const int64_t* t0, int32_t cap,
+              int32_t* traj, int32_t* heading, int32_t* astar, orc_result* res) {
+  conv c;
+  if (convert(p, &c) || n < 1 || !src || !dst || !t0 || !traj || !heading || !res || cap < 2) return ORC_E_ARG;
+  const int A = p->n_turn * p->n_climb, W = p->W;
+  const int64_t sat = c.R_max * c.R_max, sep2 = c.sep_u * c.sep_u, cap2 = c.cap_u * c.cap_u;
+  int32_t* DX = (int32_t*)malloc(sizeof(int32_t) * p->HL);
+  int32_t* DY = (int32_t*)malloc(sizeof(int32_t) * p->HL);
+  int32_t* state = (int32_t*)malloc(sizeof(int32_t) * n);     /* -2 waiting, -1 flying, >= 0 verdict */
+  int32_t* kk = (int32_t*)malloc(sizeof(int32_t) * n);
+  int32_t* verdict = (int32_t*)malloc(sizeof(int32_t) * n);
+  int32_t* next = (int32_t*)malloc(sizeof(int32_t) * 4 * n);  /* decided next state + heading */
+  int32_t* ppos = (int32_t*)malloc(sizeof(int32_t) * 3 * n);
+  int32_t* pvel = (int32_t*)malloc(sizeof(int32_t) * 3 * n);
+  int32_t* proj = (int32_t*)malloc(sizeof(int32_t) * 3 * A * W);
+  int32_t* ppsi = (int32_t*)malloc(sizeof(int32_t) * A * W);
+  int rc = ORC_OK;
+  if (!DX || !DY || !state || !kk || !verdict || !next || !ppos || !pvel || !proj || !ppsi) { rc = ORC_E_NOMEM; goto out; }
+  if (orc_tables(p, DX, DY)) { rc = ORC_E_ARG; goto out; }
+  int64_t K = INT64_MAX;
+  for (int32_t i = 0; i < n; ++i) {
+    if (t0[i] < 0) { rc = ORC_E_ARG; goto out; }
+    if (t0[i] < K) K = t0[i];
+    state[i] = -2;
+    memset(&res[i], 0, sizeof(res[i]));
+    res[i].fail_step = -1;
+    res[i].min_sep_d2 = sat;
+  }
+  for (;; ++K) {
+    int32_t waiting = 0;
+    for (int32_t i = 0; i < n; ++i) {  /* departures at clock K */
+      if (state[i] == -2 && t0[i] == K) {
+        int32_t* tr = traj + (size_t)3 * cap * i;
+        int32_t* hd = heading + (size_t)cap * i;
+        memcpy(tr, &src[3 * i], sizeof(int32_t) * 3);
+        hd[0] = orc_initial_heading(p, &src[3 * i], &dst[3 * i]);
+        state[i] = -1;
+        kk[i] = 0;
+      }
+      if (state[i] == -2) waiting++;
+    }
+    int32_t flying = 0;
+    for (int32_t i = 0; i < n; ++i) flying += state[i] == -1;
+    if (!flying && !waiting) break;
+    /* 1) terminal verdicts of every present state at clock K (others' states at K) */
+    for (int32_t i = 0; i < n; ++i) {
+      if (state[i] != -1) continue;
+      int32_t np = 0;
+      for (int32_t j = 0; j < n; ++j)
+        if (j != i && state[j] == -1) { memcpy(&ppos[3 * np], traj + (size_t)3 * cap * j + 3 * kk[j], 12); np++; }
+      int64_t nd;
+      const int32_t* q = traj + (size_t)3 * cap * i + 3 * kk[i];
+      verdict[i] = cosim_verdict(T, S, q, &dst[3 * i], K, kk[i], p->max_steps, np, ppos, sat, sep2, cap2, &nd);
+      if (nd < res[i].min_sep_d2) res[i].min_sep_d2 = nd;
+    }
+    /* 2) decisions of the non-terminal ones, all from the states at clock K (Alg 1) */
+    for (int32_t i = 0; i < n; ++i) {
+      if (state[i] != -1 || verdict[i] >= 0) continue;
+      if (kk[i] + 1 >= cap) { rc = ORC_E_RANGE; goto out; }
+      int32_t np = 0;
+      for (int32_t j = 0; j < n; ++j) {
+        if (j == i || state[j] != -1) continue;
+        const int32_t* trj = traj + (size_t)3 * cap * j;
+        memcpy(&ppos[3 * np], trj + 3 * kk[j], 12);
+        peer_velocity(DX, DY, trj, heading + (size_t)cap * j, kk[j], &pvel[3 * np]);
+        np++;
+      }
+      const int32_t* q = traj + (size_t)3 * cap * i + 3 * kk[i];
+      orc_step_out o;
+      memset(&o, 0, sizeof(o));
+      o.proj = proj;
+      o.proj_psi = ppsi;
+      if ((rc = orc_eval_step_peers(p, T, S, q, heading[(size_t)cap * i + kk[i]], &dst[3 * i], K, np, ppos, pvel, &o)))
+        goto out;
+      if (o.near_tie) res[i].n_near_ties += 1;
+      if (astar) astar[(size_t)cap * i + kk[i]] = o.a_star;
+      const int i1 = o.a_star * W;
+      next[4 * i + 0] = proj[3 * i1 + 0];
+      next[4 * i + 1] = proj[3 * i1 + 1];
+      next[4 * i + 2] = proj[3 * i1 + 2];
+      next[4 * i + 3] = ppsi[i1];
+    }
+    /* 3) apply: terminal aircraft leave, the others move (s_{t+1} <- Delta_1[a*]) */
+    for (int32_t i = 0; i < n; ++i) {
+      if (state[i] != -1) continue;
+      if (verdict[i] >= 0) {
+        state[i] = verdict[i];
+        res[i].status = verdict[i];
+        res[i].n_states = kk[i] + 1;
+        res[i].fail_step = verdict[i] == ORC_ACCEPTED ? -1 : kk[i];
+        continue;
+      }
+      kk[i] += 1;
+      memcpy(traj + (size_t)3 * cap * i + 3 * kk[i], &next[4 * i], 12);
+      heading[(size_t)cap * i + kk[i]] = next[4 * i + 3];
+    }
+  }
+out:
+  free(DX); free(DY); free(state); free(kk); free(verdict); free(next); free(ppos); free(pvel); free(proj); free(ppsi);
+  return rc;
+}
+
+int orc_cosim_replay(const orc_params* p, const orc_terrain* T, const orc_store* S, int32_t n,
+                     const int32_t* src, const int32_t* dst, const int64_t* t0, int32_t cap,
+                     const int32_t* n_states, const int32_t* traj, const int32_t* heading, const int32_t* astar,
+                     const int32_t* status, orc_replay_stats* st) {
+  conv c;
+  if (convert(p, &c) || n < 1 || !st || !n_states || !traj || !heading || !status) return ORC_E_ARG;
+  const int A = p->n_turn * p->n_climb, W = p->W;
+  const int64_t sat = c.R_max * c.R_max, sep2 = c.sep_u * c.sep_u, cap2 = c.cap_u * c.cap_u;
+  int32_t* DX = (int32_t*)malloc(sizeof(int32_t) * p->HL);
+  int32_t* DY = (int32_t*)malloc(sizeof(int32_t) * p->HL);
+  int32_t* ppos = (int32_t*)malloc(sizeof(int32_t) * 3 * n);
+  int32_t* pvel = (int32_t*)malloc(sizeof(int32_t) * 3 * n);
+  double* vstar = (double*)malloc(sizeof(double) * A);
+  double* vsc = (double*)malloc(sizeof(double) * A);
+  int32_t* proj = (int32_t*)malloc(sizeof(int32_t) * 3 * A * W);
+  int32_t* ppsi = (int32_t*)malloc(sizeof(int32_t) * A * W);
+  int rc = ORC_OK;
+  if (!DX || !DY || !ppos || !pvel || !vstar || !vsc || !proj || !ppsi) { rc = ORC_E_NOMEM; goto out; }
+  if (orc_tables(p, DX, DY)) { rc = ORC_E_ARG; goto out; }
+  for (int32_t i = 0; i < n; ++i) {
+    orc_replay_stats* s = &st[i];
+    memset(s, 0, sizeof(*s));
+    s->first_fail_step = -1;
+#define FAIL(k_) do { s->n_fail++; if (s->first_fail_step < 0) s->first_fail_step = (k_); } while (0)
+    const int32_t* tr = traj + (size_t)3 * cap * i;
+    const int32_t* hd = heading + (size_t)cap * i;
+    const int32_t ni = n_states[i];
+    if (ni < 1 || ni > cap) { FAIL(0); continue; }
+    if (tr[0] != src[3 * i] || tr[1] != src[3 * i + 1] || tr[2] != src[3 * i + 2]) FAIL(0);
+    if (hd[0] != orc_initial_heading(p, &src[3 * i], &dst[3 * i])) FAIL(0);
+    for (int32_t k = 0; k < ni; ++k) {
+      const int64_t K = t0[i] + k;
+      int32_t np = 0;  /* peers present at clock K in the given trajectories */
+      for (int32_t j = 0; j < n; ++j) {
+        const int64_t kj = K - t0[j];
+        if (j == i || kj < 0 || kj >= n_states[j]) continue;
+        const int32_t* trj = traj + (size_t)3 * cap * j;
+        memcpy(&ppos[3 * np], trj + 3 * kj, 12);
+        peer_velocity(DX, DY, trj, heading + (size_t)cap * j, (int32_t)kj, &pvel[3 * np]);
+        np++;
+      }
+      const int32_t* q = &tr[3 * k];
+      int64_t nd;
+      const int v = cosim_verdict(T, S, q, &dst[3 * i], K, k, p->max_steps, np, ppos, sat, sep2, cap2, &nd);
+      if (k == ni - 1) {
+        if (v != (status[i] < 0 ? -1 : status[i])) FAIL(k);
+        break;
+      }
+      if (v >= 0) { FAIL(k); break; }
+      orc_step_out o;
+      memset(&o, 0, sizeof(o));
+      o.vstar = vstar;
+      o.vstar_scale = vsc;
+      o.proj = proj;
+      o.proj_psi = ppsi;
+      if (orc_eval_step_peers(p, T, S, q, hd[k], &dst[3 * i], K, np, ppos, pvel, &o)) { FAIL(k); break; }
+      s->n_steps_checked++;
+      if (o.near_tie) s->n_near_ties++;
+      const int ag = astar ? astar[(size_t)cap * i + k] : o.a_star;
+      if (ag < 0 || ag >= A) { FAIL(k); break; }
+      if (ag != o.a_star) {
+        if (vstar[o.a_star] - vstar[ag] < p->near_tie_rel * vsc[o.a_star]) s->n_divergent++;
+        else FAIL(k);
+      }
+      const int i1 = ag * W;
+      const int32_t* q1 = &tr[3 * (k + 1)];
+      if (q1[0] != proj[3 * i1] || q1[1] != proj[3 * i1 + 1] || q1[2] != proj[3 * i1 + 2] || hd[k + 1] != ppsi[i1])
+        FAIL(k);
+    }
+#undef FAIL
+  }
+out:
+  free(DX); free(DY); free(ppos); free(pvel); free(vstar); free(vsc); free(proj); free(ppsi);
+  return rc;
 }

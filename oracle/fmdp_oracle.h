@@ -78,6 +78,7 @@ typedef struct orc_step_out {
   int32_t a_second;  /* runner-up (lowest index among ties)  */
   double gap;        /* V*(a*) - V*(a_second)                */
   int32_t near_tie;  /* gap < near_tie_rel * vstar_scale[a*] */
+  double* v_neg;     /* [A*W] V^- (Alg 5; batch peers) */
 } orc_step_out;
 
 typedef struct orc_result {
@@ -118,12 +119,32 @@ int orc_store_sample(const orc_store* s, int32_t plan, int64_t K, int32_t pos[3]
 
 int orc_eval_step(const orc_params* p, const orc_terrain* T, const orc_store* S,
                   const int32_t q[3], int32_t psi, const int32_t g[3], int64_t K, orc_step_out* out);
+/* Alg 2-9 with batch peers (Alg 5, Table DS P:397 P^-): n_peer other
+ * aircraft of a co-simulated batch at clock K, each with position and linear velocity (per
+ * substep); they add five wells each (Table PK "aircraft" row, like an intruder). */
+int orc_eval_step_peers(const orc_params* p, const orc_terrain* T, const orc_store* S,
+                        const int32_t q[3], int32_t psi, const int32_t g[3], int64_t K, int32_t n_peer,
+                        const int32_t* peer_pos, const int32_t* peer_vel, orc_step_out* out);
 int orc_schedule(const orc_params* p, const orc_terrain* T, const orc_store* S,
                  const int32_t src[3], const int32_t dst[3], int64_t t0, int32_t cap,
                  int32_t* traj, int32_t* heading, int32_t* astar, orc_result* res);
 int orc_schedule_batch(const orc_params* p, const orc_terrain* T, orc_store* S, int32_t n,
                        const int32_t* src, const int32_t* dst, const int64_t* t0, int32_t cap,
                        int32_t* traj, int32_t* heading, int32_t* astar, orc_result* res);
+/* Co-simulated batch (Alg 1 P:151-237 synchronous update, Alg 5, Table DS
+ * "Determine terminal state N x N"): the n aircraft share one clock K; aircraft i is present
+ * at K for t0[i] <= K until its terminal state.  At every clock each present aircraft sees the
+ * others' wells and separation; all decide, then all move.  traj/heading/astar: n blocks of
+ * cap states; res[n].  S is not modified (the caller appends the accepted plans). */
+int orc_cosim(const orc_params* p, const orc_terrain* T, const orc_store* S, int32_t n,
+              const int32_t* src, const int32_t* dst, const int64_t* t0, int32_t cap,
+              int32_t* traj, int32_t* heading, int32_t* astar, orc_result* res);
+/* Lockstep replay of a co-simulated batch: every aircraft's steps and verdicts recomputed with
+ * its peers taken from the given trajectories; st[n]. */
+int orc_cosim_replay(const orc_params* p, const orc_terrain* T, const orc_store* S, int32_t n,
+                     const int32_t* src, const int32_t* dst, const int64_t* t0, int32_t cap,
+                     const int32_t* n_states, const int32_t* traj, const int32_t* heading, const int32_t* astar,
+                     const int32_t* status, orc_replay_stats* st);
 /* status -1 replays a prefix (the last given state must not be terminal). */
 int orc_replay(const orc_params* p, const orc_terrain* T, const orc_store* S,
                const int32_t src[3], const int32_t dst[3], int64_t t0,

@@ -60,7 +60,8 @@ class StepOut(C.Structure):
     _fields_ = [("v_pos", C.c_void_p), ("v_int", C.c_void_p), ("v_ter", C.c_void_p), ("v_alt", C.c_void_p),
                 ("v", C.c_void_p), ("scale", C.c_void_p), ("vstar", C.c_void_p), ("vstar_scale", C.c_void_p),
                 ("conf_d2", C.c_void_p), ("proj", C.c_void_p), ("proj_psi", C.c_void_p),
-                ("a_star", C.c_int32), ("a_second", C.c_int32), ("gap", C.c_double), ("near_tie", C.c_int32)]
+                ("a_star", C.c_int32), ("a_second", C.c_int32), ("gap", C.c_double), ("near_tie", C.c_int32),
+                ("v_neg", C.c_void_p)]
 
 
 class Result(C.Structure):
@@ -99,6 +100,11 @@ def lib():
             L.orc_store_count.restype = i32
             L.orc_store_sample.argtypes = [vp, i32, i64, vp, vp]
             L.orc_eval_step.argtypes = [P, C.POINTER(Terrain), vp, vp, i32, vp, i64, C.POINTER(StepOut)]
+            L.orc_eval_step_peers.argtypes = [P, C.POINTER(Terrain), vp, vp, i32, vp, i64, i32, vp, vp,
+                                              C.POINTER(StepOut)]
+            L.orc_cosim.argtypes = [P, C.POINTER(Terrain), vp, i32, vp, vp, vp, i32, vp, vp, vp, C.POINTER(Result)]
+            L.orc_cosim_replay.argtypes = [P, C.POINTER(Terrain), vp, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp,
+                                           C.POINTER(ReplayStats)]
             L.orc_schedule.argtypes = [P, C.POINTER(Terrain), vp, vp, vp, i64, i32, vp, vp, vp,
                                        C.POINTER(Result)]
             L.orc_schedule_batch.argtypes = [P, C.POINTER(Terrain), vp, i32, vp, vp, vp, i32, vp, vp, vp,
@@ -140,6 +146,7 @@ class StepResult:
     v_int: np.ndarray
     v_ter: np.ndarray
     v_alt: np.ndarray
+    v_neg: np.ndarray
     v: np.ndarray
     scale: np.ndarray
     vstar: np.ndarray
@@ -254,9 +261,10 @@ class Oracle:
         return (pos, vel) if ok else None
 
     # ---- one decision step --------------------------------------------------
-    def eval_step(self, q, psi, goal, K) -> StepResult:
+    def eval_step(self, q, psi, goal, K, peer_pos=None, peer_vel=None) -> StepResult:
+        """Algs 2-9 at clock K; optional batch peers (Alg 5) as [n, 3] pos / vel."""
         A, W = self.A, self.air.W
-        arr = {k: np.zeros(A * W, np.float64) for k in ("v_pos", "v_int", "v_ter", "v_alt", "v", "scale")}
+        arr = {k: np.zeros(A * W, np.float64) for k in ("v_pos", "v_int", "v_ter", "v_alt", "v_neg", "v", "scale")}
         vstar = np.zeros(A, np.float64)
         vsc = np.zeros(A, np.float64)
         conf = np.zeros(A, np.int64)
@@ -268,8 +276,11 @@ class Oracle:
         o.vstar, o.vstar_scale, o.conf_d2, o.proj, o.proj_psi = _ptr(vstar), _ptr(vsc), _ptr(conf), _ptr(proj), _ptr(pps)
         qq = np.ascontiguousarray(q, np.int32)
         gg = np.ascontiguousarray(goal, np.int32)
-        rc = self.L.orc_eval_step(C.byref(self.p), C.byref(self.T), self.S, _ptr(qq), int(psi), _ptr(gg), int(K),
-                                  C.byref(o))
+        npeer = 0 if peer_pos is None else len(peer_pos)
+        pp = np.ascontiguousarray(np.reshape(peer_pos, (-1, 3)) if npeer else np.zeros((0, 3)), np.int32)
+        pv = np.ascontiguousarray(np.reshape(peer_vel, (-1, 3)) if npeer else np.zeros((0, 3)), np.int32)
+        rc = self.L.orc_eval_step_peers(C.byref(self.p), C.byref(self.T), self.S, _ptr(qq), int(psi), _ptr(gg), int(K),
+                                        npeer, _ptr(pp), _ptr(pv), C.byref(o))
         if rc:
             raise RuntimeError(f"orc_eval_step failed ({rc})")
         return StepResult(**{k: v.reshape(A, W) for k, v in arr.items()}, vstar=vstar, vstar_scale=vsc,
@@ -311,6 +322,59 @@ class Oracle:
         if rc:
             raise RuntimeError(f"orc_replay failed ({rc})")
         return st
+
+
+    # ---- co-simulated batch ------------------------------------
+    def cosim(self, src, dst, t0):
+        """Mutually aware batch on one clock (Alg 1 synchronous update, Alg 5); the store is
+        not modified.  Returns one SchedResult per aircraft."""
+        n = len(t0)
+        cap = self.air.max_steps + 2
+        traj = np.zeros((n, cap, 3), np.int32)
+        hd = np.zeros((n, cap), np.int32)
+        ast = np.full((n, cap), -1, np.int32)
+        res = (Result * n)()
+        s = np.ascontiguousarray(src, np.int32).reshape(n, 3)
+        d = np.ascontiguousarray(dst, np.int32).reshape(n, 3)
+        t = np.ascontiguousarray(t0, np.int64)
+        rc = self.L.orc_cosim(C.byref(self.p), C.byref(self.T), self.S, n, _ptr(s), _ptr(d), _ptr(t), cap,
+                              _ptr(traj), _ptr(hd), _ptr(ast), res)
+        if rc:
+            raise RuntimeError(f"orc_cosim failed ({rc})")
+        out = []
+        for i in range(n):
+            r = res[i]
+            m = r.n_states
+            out.append(SchedResult(r.status, m, r.fail_step, r.n_near_ties, r.min_sep_d2, traj[i, :m].copy(),
+                                   hd[i, :m].copy(), ast[i, :max(m - 1, 0)].copy()))
+        return out
+
+    def cosim_replay(self, src, dst, t0, trajs, headings, astars, statuses):
+        """Replay a co-simulated batch produced elsewhere; one ReplayStats per aircraft."""
+        n = len(t0)
+        cap = max(len(x) for x in trajs) + 1
+        traj = np.zeros((n, cap, 3), np.int32)
+        hd = np.zeros((n, cap), np.int32)
+        ast = np.full((n, cap), -1, np.int32)
+        ns = np.zeros(n, np.int32)
+        for i in range(n):
+            m = len(trajs[i])
+            ns[i] = m
+            traj[i, :m] = trajs[i]
+            hd[i, :m] = headings[i]
+            if astars is not None:
+                ast[i, :len(astars[i])] = astars[i]
+        st = (ReplayStats * n)()
+        s = np.ascontiguousarray(src, np.int32).reshape(n, 3)
+        d = np.ascontiguousarray(dst, np.int32).reshape(n, 3)
+        t = np.ascontiguousarray(t0, np.int64)
+        status = np.ascontiguousarray(statuses, np.int32)
+        rc = self.L.orc_cosim_replay(C.byref(self.p), C.byref(self.T), self.S, n, _ptr(s), _ptr(d), _ptr(t), cap,
+                                     _ptr(ns), _ptr(traj), _ptr(hd), None if astars is None else _ptr(ast),
+                                     _ptr(status), st)
+        if rc:
+            raise RuntimeError(f"orc_cosim_replay failed ({rc})")
+        return [st[i] for i in range(n)]
 
 
 def for_scenario(sc, plans=True) -> Oracle:
