@@ -30,7 +30,8 @@ sys.path.insert(0, ROOT)
 METRIC = "FCFS requests scheduled/sec and ms/request vs #accepted plans, 1/2/4/8 B200"
 WORKLOAD = ("configs[1]: batch of 100 FCFS requests against 3000 accepted plans with a 256-well terrain "
             "grid, 16x16 km dense urban airspace, 9 headings x 3 climbs, W=10")
-OPS_PER_PAIR = 10.0 / 3.0  # FP32 lane-ops per (state, well) pair at 3 climbs
+OPS_PER_PAIR = 7.0  # algorithmic FP32 ops per (state, well) pair
+EXEC_OPS_PER_PAIR = 5.0 / 3.0  # FP32 lane-ops the kernel executes per pair at 3 climbs ((2 + C)/C)
 
 
 def parse():
@@ -265,9 +266,45 @@ def run_native(args):
                 "candidates_per_request": len(delays), "requests_per_step": n_req, "cull": 1,
                 "ms_per_request": tot / args.steps / n_req, "chosen_delay_index": chosen}
 
+    def measure_cosim(sizes=(1, 5, 10, 20), n_plans=100):
+        # SURVEY f2 / Fig perf2: co-simulated batches against 100 intruders;
+        # batch cycles/s = clocks / time, total cycles/s = aircraft-steps / time
+        out = []
+        for nb in sizes:
+            cs = fs.cosim_ring(args.seed + 40 + rank, nb, n_plans=n_plans)
+            cctx = FMDP(cs.airspace, cs.terrain, device=local, stream=stream)
+            cctx.add_plans(cs.plans)
+            c0 = cctx.num_plans()
+            creqs = cctx.make_requests(cs.src, cs.dst, cs.t0)
+            times, res = [], None
+            for it in range(args.warmup + args.steps):
+                with torch.cuda.stream(stream):
+                    ev0.record(stream)
+                    res = cctx.schedule_cosim(None, None, None, want_traj=False, reqs=creqs)
+                    ev1.record(stream)
+                ev1.synchronize()
+                if it >= args.warmup:
+                    times.append(ev0.elapsed_time(ev1))
+                cctx.truncate(c0)
+            st = cctx.stats()
+            cctx.close()
+            ms = max_over_ranks(sum(times), world) / len(times)
+            clocks = max(int(cs.t0[i]) + r.n_states for i, r in enumerate(res)) - int(cs.t0.min())
+            steps = sum(r.n_states for r in res)
+            out.append({"batch": nb, "ms_per_batch": ms, "clocks": clocks, "aircraft_steps": steps,
+                        "batch_cycles_per_s": clocks / (ms / 1e3), "total_cycles_per_s": steps / (ms / 1e3),
+                        "accepted": sum(r.accepted for r in res), "cluster_size": st["cluster_size"]})
+        return {"what": "SURVEY f2: co-simulated batches (mutually aware, synchronous clock; Alg 5 peer wells) "
+                        "against 100 intruder plans, the Fig perf2 experiment (tests/test_gpu_cosim.py)",
+                "workload": "fmdp_synth.cosim_ring (ring of aircraft crossing the centre, 8 km box)",
+                "paper_fig_perf2_hz": {"1": 194.5, "5": 48.5, "10": 24.0, "20": 12.2},
+                "paper_note": "paper's GPU, A=1350 actions (context, not the target)",
+                "sizes": out}
+
     M = measure(0)       # every (state, well) pair evaluated
     Mc = measure(1)      # exact culling, bit-identical outputs
     Md = measure_departures()
+    Mco = measure_cosim()
     h2d = n * C_REQUEST_BYTES
     tot_ms, value, e2e_value, d2h = M["tot_ms"], M["value"], M["e2e_value"], M["d2h"]
     stats = M["st_all"][-1]
@@ -290,6 +327,7 @@ def run_native(args):
     except Exception:
         pass
     achieved_tops = pairs * OPS_PER_PAIR / (walk_ms / 1e3) / 1e12 if walk_ms > 0 else 0.0
+    exec_tops = pairs * EXEC_OPS_PER_PAIR / (walk_ms / 1e3) / 1e12 if walk_ms > 0 else 0.0
     if rank != 0:
         return 0
     line = {
@@ -307,7 +345,9 @@ def run_native(args):
         "roofline": {"bound": "alu", "achieved": achieved_tops, "peak": peak_tops, "unit": "Top/s",
                      "frac": achieved_tops / peak_tops, "traffic": traffic,
                      "traffic_source": "profiles/r01_traffic.json (ncu --set full, bytes per walk launch)",
-                     "kernel": "walk_kernel<3>", "ops_per_pair": OPS_PER_PAIR,
+                     "kernel": "walk_kernel<3, false>", "ops_per_pair": OPS_PER_PAIR,
+                     "ops_per_pair_basis": "algorithmic, SURVEY §8(d) d.3 (3 differences, 3 squares/fmas, 1 min)",
+                     "pipe_frac": exec_tops / peak_tops, "exec_ops_per_pair": EXEC_OPS_PER_PAIR,
                      "peak_basis": f"FP32 pipe: 148 SM x 128 lanes x {peak_clock:.0f} MHz (MEASURED_PEAKS sm_max_mhz)"},
         "e2e": {"value": e2e_value, "unit": "requests/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
@@ -322,6 +362,7 @@ def run_native(args):
             "pair_evals_per_step": Mc["pairs"] / args.steps, "gpu_launches": Mc["launches"],
             "same_results_as_full": same, "clocks": Mc["clocks"]},
         "f3_departures": Md,
+        "f2_cosim": Mco,
     }
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(sc, args.cpu_sample_s)

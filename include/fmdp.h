@@ -237,6 +237,22 @@ fmdp_status fmdp_schedule_departures(fmdp_ctx* ctx, uint64_t aircraft_id, fmdp_v
                                      int64_t t0_step, int32_t n_delays, const int64_t* delays, fmdp_result* res,
                                      fmdp_qpos* traj, int32_t traj_cap, int32_t* chosen);
 
+/* Co-simulated batch ("multiple aircraft being co-simulated together with the
+ * same set of accepted flights ... aware of each other"; Alg 1 P:230-235 synchronous update;
+ * Alg 5 P:598-631 and Table DS P:397 P^- wells; Table DS "Determine terminal state" N x N).
+ * The n requests fly on one clock K (request i from K = t0_step until its terminal state): at
+ * every clock each airborne aircraft sees the five wells of every other airborne batch
+ * aircraft (position, and velocity = its last displacement; R28) next to the
+ * accepted plans, all decide from the states at K, then all move.  Two batch aircraft closer
+ * than sep_m at a clock are both rejected for conflict; min_sep_m includes batch peers.
+ * Accepted trajectories (mutually separated) are appended in array order; the store is not
+ * changed during the batch.  All n walkers run concurrently: n <= fmdp_cosim_max(ctx), else
+ * FMDP_E_CAPACITY.  res[n]; traj: n * traj_cap_each states or NULL. */
+fmdp_status fmdp_schedule_cosim(fmdp_ctx* ctx, const fmdp_request* reqs, int32_t n, fmdp_result* res, fmdp_qpos* traj,
+                                int32_t traj_cap_each);
+/* Largest co-simulated batch the device can run (co-resident walkers). */
+int32_t fmdp_cosim_max(fmdp_ctx* ctx);
+
 /* Per-step log of the last trajectory of request `index` of the last schedule /
  * schedule_batch call: action a*_k, heading psi_k, and near-tie flag per step (k < n).
  * Any pointer may be NULL. */

@@ -14,8 +14,8 @@ constexpr int MAX_AW = 1024;    // projected states per step (A*W)
 constexpr int AMB_MAX = 64;     // ambiguous (state, tau) minima handled per step
 constexpr int TC_MAX = 128;     // terrain-well candidates per step
 constexpr int TW_SMEM = 512;    // terrain wells cached in shared memory (more: read from L2)
-constexpr int N_PHASES = 17;
-constexpr int PAIR_STRIDE = 36;  // floats per plan-pair record (30 used): 16B-aligned, 2-way banks    // walk-kernel phase accounting (fmdp_stats.phase_cycles)
+constexpr int N_PHASES = 17;     // walk-kernel phase accounting (fmdp_stats.phase_cycles)
+constexpr int PAIR_STRIDE = 40;  // floats per plan-pair record: per tau (X, X', Y, Y', Z, Z', Q, Q')
 
 // Scenario + store in integer units, passed by value to the kernels.
 struct World {
@@ -27,7 +27,7 @@ struct World {
   float cull2f_tau[NTAU];       // (R_tau + reach + 1)^2 (1 + 2^-16): conservative FP32 f1 cull threshold
   int32_t cull_inf;             // R_max + reach + 1: f1 L-inf prefilter radius
   int32_t k_absmax;             // max |tau/dt|
-  float R2lo[NTAU], R2hi[NTAU]; // FP32 filter band R^2 (1 -/+ 2^-20)
+  float R2lo[NTAU], R2hi[NTAU]; // FP32 filter band R^2 (1 -/+ band_tau), band >= 2^-20 (host: error bound)
   int32_t R_max;                // max tau radius, units (< 2^15)
   uint32_t sat_d2;              // R_max^2: saturation of separation minima
   uint32_t sep2;                // separation minimum^2
@@ -96,6 +96,13 @@ struct WalkArgs {
   int32_t* dbg_astar;           // [1]
   unsigned long long* pairs;    // hot-loop pair counter (stats)
   unsigned long long* prof;     // [PH_N] per-phase cycles of rank 0 (nullptr = off)
+  // co-simulated batch: one cluster per request, all on one clock
+  int32_t cosim;                // 1: batch peers are wells (Alg 5) and separation partners
+  int32_t cs_n;                 // batch size = clusters launched (all co-resident)
+  int64_t cs_k0;                // first clock (min t0)
+  int4* cs_pub;                 // [2][cs_n][2]: {x, y, z, flags}, {vx, vy, vz, 0} by clock parity
+  unsigned* cs_arrive;          // arrivals, one per walker per clock (zeroed before launch)
+  int32_t* cs_err;              // set on a barrier timeout (walkers not co-resident)
 };
 
 // Shared-memory carve-up, identical on host (size) and device (offsets).
@@ -162,7 +169,8 @@ cudaError_t launch_walk(const World& w, const WalkArgs& a, int n_climb, int clus
 // Hot-loop thread mapping: warps of 32/ngw columns x ngw plan groups; threads = 32*warps.
 int walk_groups_per_warp(int ncol, int max_threads);
 int walk_threads(int ncol, int max_threads);
-cudaError_t walk_max_clusters(const World& w, int n_climb, int cluster, int threads, int chunk, int rawcap, int* out);
+cudaError_t walk_max_clusters(const World& w, int n_climb, int cluster, int threads, int chunk, int rawcap, int* out,
+                              bool cosim = false);
 size_t walk_smem_bytes(const World& w, int n_climb, int threads, int chunk, int rawcap, int cluster);
 cudaError_t launch_append(int32_t* rows, int32_t row_cap, int64_t horizon, const AppendPlan* plans, int n_plans,
                           int max_n, cudaStream_t s);

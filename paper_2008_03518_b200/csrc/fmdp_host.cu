@@ -77,6 +77,9 @@ struct fmdp_ctx {
   int app_cap = 0;
   int32_t* d_up = nullptr;  // upload scratch (states / slots)
   size_t up_cap = 0;
+  int4* d_cspub = nullptr;     // co-simulation publish buffer [2][n][2]
+  int32_t* d_csctr = nullptr;  // [0] arrivals, [1] barrier error
+  int cs_cap = 0;
   uint32_t* d_xbuf = nullptr;  // multi-GPU exchange buffer [A*W*NTAU + 1]
   int xmode = 0, shard_rank = 0, shard_world = 1;
   double *d_dbg_vstar = nullptr, *d_dbg_v = nullptr, *d_dbg_s = nullptr;
@@ -90,6 +93,9 @@ struct fmdp_ctx {
   std::string err;
   int num_sms = 0;
   int mc_cache[17] = {0};
+  int mc_cache_cs[17] = {0};
+  double fan_radius_u = 0;             // bound on |s - o| (hot-loop origin), units
+  double band_rel[fmdp::NTAU] = {0};   // FP32 filter band per tau, relative to R^2
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
 
@@ -232,14 +238,15 @@ int rawcap_for(const fmdp_ctx* ctx) {
   return cap;
 }
 
-int max_clusters(fmdp_ctx* ctx, int G) {
-  if (ctx->mc_cache[G]) return ctx->mc_cache[G];
+int max_clusters(fmdp_ctx* ctx, int G, bool cosim = false) {
+  int* cache = cosim ? ctx->mc_cache_cs : ctx->mc_cache;
+  if (cache[G]) return cache[G];
   int n = 0;
-  if (fmdp::walk_max_clusters(ctx->w, ctx->C, G, threads_for(ctx), chunk_for(ctx), rawcap_for(ctx), &n) !=
+  if (fmdp::walk_max_clusters(ctx->w, ctx->C, G, threads_for(ctx), chunk_for(ctx), rawcap_for(ctx), &n, cosim) !=
           cudaSuccess || n < 0)
     n = 0;
   cudaGetLastError();
-  ctx->mc_cache[G] = n;
+  cache[G] = n;
   return n;
 }
 
@@ -283,10 +290,7 @@ void choose_launch(fmdp_ctx* ctx, int n_run, int* G_out, int* nc_out) {
                  *nc_out, mc);
 }
 
-fmdp_status run_walk(fmdp_ctx* ctx, const std::vector<Req>& run, bool eval, int budget = INT_MAX) {
-  if (run.empty()) return FMDP_OK;
-  CK(cudaMemcpyAsync(ctx->d_reqs, run.data(), sizeof(Req) * run.size(), cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemsetAsync(ctx->d_queue, 0, sizeof(int32_t), ctx->stream));
+fmdp::WalkArgs make_args(fmdp_ctx* ctx, const std::vector<Req>& run, bool eval, int budget) {
   fmdp::WalkArgs a{};
   a.reqs = ctx->d_reqs;
   a.n_reqs = (int32_t)run.size();
@@ -312,8 +316,17 @@ fmdp_status run_walk(fmdp_ctx* ctx, const std::vector<Req>& run, bool eval, int 
   a.dbg_astar = ctx->d_dbg_astar;
   a.pairs = ctx->d_pairctr;
   a.prof = ctx->launch.profile ? ctx->d_prof : nullptr;
-  int G = 1, nc = 1;
-  choose_launch(ctx, (int)run.size(), &G, &nc);
+  return a;
+}
+
+// Launch the walker over `run` with cluster size G and nc clusters (G = 0: cost model).
+fmdp_status run_walk(fmdp_ctx* ctx, const std::vector<Req>& run, bool eval, int budget = INT_MAX,
+                     const fmdp::WalkArgs* over = nullptr, int G = 0, int nc = 0) {
+  if (run.empty()) return FMDP_OK;
+  CK(cudaMemcpyAsync(ctx->d_reqs, run.data(), sizeof(Req) * run.size(), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemsetAsync(ctx->d_queue, 0, sizeof(int32_t), ctx->stream));
+  const fmdp::WalkArgs a = over ? *over : make_args(ctx, run, eval, budget);
+  if (G == 0) choose_launch(ctx, (int)run.size(), &G, &nc);
   ctx->stats.cluster_size = G;
   ctx->stats.walkers = std::max(ctx->stats.walkers, nc);
   CK(cudaEventRecord(ctx->ev0, ctx->stream));
@@ -745,16 +758,11 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
       if (!integral(a.tau_s[i] / a.dt, &k) || !integral(a.tau_radius_m[i] / a.u_m, &R) || R <= 0)
         return bad(FMDP_E_ARG, "tau/dt and radii/u must be integral");
       w.k_tau[i] = (int32_t)k;
-      w.R2_tau[i] = R * R;
-      const double d = std::ldexp(1.0, -20);
-      w.R2lo[i] = (float)((double)(R * R) * (1.0 - d));
-      w.R2hi[i] = (float)((double)(R * R) * (1.0 + d));
+      w.R2_tau[i] = R * R;  // FP32 band R2lo/R2hi: set below from the hot loop's error bound
       Rmax = std::max(Rmax, R);
     } else {
       w.k_tau[i] = 0;
       w.R2_tau[i] = 0;
-      w.R2lo[i] = -1.f;
-      w.R2hi[i] = -1.f;
     }
   }
   if (Rmax >= 32768) return bad(FMDP_E_ARG, "well radius must be < 2^15 units");
@@ -787,6 +795,43 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   w.reach_u = (int32_t)(a.window * ((int64_t)std::ceil(maxd) + maxc) + 1);
   w.step_reach_u = (int32_t)((int64_t)std::ceil(maxd) + maxc + 1);
   w.cull_inf = (int32_t)(Rmax + w.reach_u + 1);
+  // Hot-loop filter band.  The kernel evaluates e = Q + 2(s-o).X, X = o - c,
+  // Q = fl(|X|^2), with s - o bounded by S (the fan radius around o = q + (W/2)(DX,DY)[psi],
+  // measured here over every heading, turn and substep, plus the climb).  First-order
+  // rounding error of the computed d^2 = e + |s-o|^2 for d <= R(1 + band):
+  //   u [3 (R+S)^2 + 2((R+S)^2 + 2S(R+S)) + 2R^2 + S^2],  u = 2^-24;
+  // the band is 1.5x that, relative to R^2, and never below 2^-20.
+  {
+    int64_t s2max = 0;
+    const int half = a.window / 2;
+    for (int psi = 0; psi < w.HL; ++psi) {
+      const int64_t ox = (int64_t)half * lat[psi].x, oy = (int64_t)half * lat[psi].y;
+      for (int it = 0; it < a.n_turn; ++it) {
+        int64_t x = 0, y = 0;
+        int ps = psi;
+        for (int t = 1; t <= a.window; ++t) {
+          ps = ((ps + a.turn_steps[it]) % w.HL + w.HL) % w.HL;
+          x += lat[ps].x;
+          y += lat[ps].y;
+          s2max = std::max(s2max, (x - ox) * (x - ox) + (y - oy) * (y - oy));
+        }
+      }
+    }
+    const double S = std::sqrt((double)s2max) + (double)a.window * maxc + 1.0;
+    ctx->fan_radius_u = S;
+    for (int i = 0; i < a.n_tau; ++i) {
+      const double R = std::sqrt((double)w.R2_tau[i]);
+      const double err = 3 * (R + S) * (R + S) + 2 * ((R + S) * (R + S) + 2 * S * (R + S)) + 2 * R * R + S * S;
+      const double band = std::max(std::ldexp(1.0, -20), 1.5 * std::ldexp(err / (R * R), -24));
+      w.R2lo[i] = (float)((R * R) * (1.0 - band));
+      w.R2hi[i] = (float)((R * R) * (1.0 + band));
+      ctx->band_rel[i] = band;
+    }
+    for (int i = a.n_tau; i < fmdp::NTAU; ++i) {
+      w.R2lo[i] = -1.f;
+      w.R2hi[i] = -1.f;
+    }
+  }
   w.k_absmax = 0;
   for (int i = 0; i < a.n_tau; ++i) w.k_absmax = std::max(w.k_absmax, std::abs(w.k_tau[i]));
   for (int i = 0; i < fmdp::NTAU; ++i) {
@@ -901,6 +946,7 @@ fmdp_status fmdp_set_launch(fmdp_ctx* ctx, const fmdp_launch* l) {
     return fail(ctx, FMDP_E_ARG, "threads is derived from the action lattice; pass 0");
   ctx->launch = n;
   std::memset(ctx->mc_cache, 0, sizeof(ctx->mc_cache));
+  std::memset(ctx->mc_cache_cs, 0, sizeof(ctx->mc_cache_cs));
   if (fmdp::walk_smem_bytes(ctx->w, ctx->C, threads_for(ctx), chunk_for(ctx), rawcap_for(ctx), 16) > 227 * 1024)
     return fail(ctx, FMDP_E_ARG, "shared memory");
   return FMDP_OK;
@@ -1067,6 +1113,32 @@ fmdp_status fmdp_schedule_sharded(fmdp_ctx* ctx, const fmdp_shard* shard, uint64
   return FMDP_OK;
 }
 
+// Co-simulated batch: one cluster per request, all resident at once (they wait for
+// each other every clock).  Cluster size: the cost model of choose_launch among the sizes
+// whose co-resident cluster count covers the batch.
+int cosim_cluster_size(fmdp_ctx* ctx, int n) {
+  double plans = 0;
+  {
+    int64_t tot = 0, nz = 0;
+    for (int32_t c : ctx->counts)
+      if (c) { tot += c; ++nz; }
+    plans = nz ? (double)tot / nz : 0.0;
+  }
+  const double work = (ctx->launch.cull ? plans * 0.6 : (plans + n) * fmdp::NTAU * ctx->A * ctx->W / 21.0);
+  int best_G = 0;
+  double best = 1e300;
+  for (int G : {16, 8, 4, 2, 1}) {
+    if (ctx->launch.cluster_size && G != ctx->launch.cluster_size) continue;
+    if (max_clusters(ctx, G, true) < n) continue;
+    const double t = work / G + 16000.0 + 300.0 * G;
+    if (t < best) {
+      best = t;
+      best_G = G;
+    }
+  }
+  return best_G;
+}
+
 fmdp_status fmdp_schedule_departures(fmdp_ctx* ctx, uint64_t aircraft_id, fmdp_vec3 src, fmdp_vec3 dst,
                                      int64_t t0_step, int32_t n_delays, const int64_t* delays, fmdp_result* res,
                                      fmdp_qpos* traj, int32_t traj_cap, int32_t* chosen) {
@@ -1117,6 +1189,79 @@ fmdp_status fmdp_schedule_departures(fmdp_ctx* ctx, uint64_t aircraft_id, fmdp_v
   CK(cudaMemcpy(&pc, ctx->d_pairctr, sizeof(pc), cudaMemcpyDeviceToHost));
   ctx->stats.pair_evals = (int64_t)pc;
   ctx->last_n = n_delays;
+  return FMDP_OK;
+}
+
+int32_t fmdp_cosim_max(fmdp_ctx* ctx) {
+  if (!ctx) return 0;
+  int m = 0;
+  for (int G : {1, 2, 4, 8, 16})
+    if (!ctx->launch.cluster_size || G == ctx->launch.cluster_size) m = std::max(m, max_clusters(ctx, G, true));
+  return m;
+}
+
+fmdp_status fmdp_schedule_cosim(fmdp_ctx* ctx, const fmdp_request* reqs, int32_t n, fmdp_result* res, fmdp_qpos* traj,
+                                int32_t traj_cap_each) {
+  if (!ctx || n < 1 || !reqs || !res) return fail(ctx, FMDP_E_ARG, "null argument");
+  if (traj && traj_cap_each < ctx->w.max_steps + 1) return fail(ctx, FMDP_E_BUFFER, "traj_cap must be >= max_steps + 1");
+  std::memset(&ctx->stats, 0, sizeof(ctx->stats));
+  std::vector<Req> base;
+  fmdp_status st = prepare_requests(ctx, reqs, n, base);
+  if (st) return st;
+  const int G = cosim_cluster_size(ctx, n);
+  if (G == 0)
+    return fail(ctx, FMDP_E_CAPACITY, "co-simulated batch larger than the co-resident walkers (fmdp_cosim_max)");
+  if ((st = ensure_slots(ctx, n))) return st;
+  if (n > ctx->cs_cap) {
+    if ((st = grow(ctx, ctx->d_cspub, (size_t)4 * n)) || (st = grow(ctx, ctx->d_csctr, 2))) return st;
+    ctx->cs_cap = n;
+  }
+  int64_t k0 = INT64_MAX;
+  for (const Req& r : base) k0 = std::min(k0, r.t0);
+  CK(cudaMemsetAsync(ctx->d_csctr, 0, 2 * sizeof(int32_t), ctx->stream));
+  CK(cudaMemsetAsync(ctx->d_cspub, 0, sizeof(int4) * 4 * n, ctx->stream));
+  CK(cudaMemsetAsync(ctx->d_pairctr, 0, sizeof(unsigned long long), ctx->stream));
+  fmdp::WalkArgs a = make_args(ctx, base, false, INT_MAX);
+  a.cosim = 1;
+  a.cs_n = n;
+  a.cs_k0 = k0;
+  a.cs_pub = ctx->d_cspub;
+  a.cs_arrive = reinterpret_cast<unsigned*>(ctx->d_csctr);
+  a.cs_err = ctx->d_csctr + 1;
+  if ((st = run_walk(ctx, base, false, INT_MAX, &a, G, n))) return st;
+  int32_t err = 0;
+  CK(cudaMemcpy(&err, ctx->d_csctr + 1, sizeof(err), cudaMemcpyDeviceToHost));
+  if (err) return fail(ctx, FMDP_E_CUDA, "co-simulation clock barrier timed out (walkers not co-resident)");
+  if ((st = fetch_out(ctx, n))) return st;
+  ctx->stats.rounds = 1;
+  std::vector<int> acc;
+  for (int i = 0; i < n; ++i) {
+    ctx->stats.steps += ctx->h_out[i].steps_run;
+    if (ctx->h_out[i].status == FMDP_ACCEPTED) acc.push_back(i);
+  }
+  // accepted plans are mutually separated (N x N terminal test): append all, in array order
+  std::vector<uint32_t> plan_id(n, 0xffffffffu);
+  std::vector<uint64_t> aircraft(n);
+  for (int i = 0; i < n; ++i) aircraft[i] = reqs[i].aircraft_id;
+  if ((st = commit_slots(ctx, acc, base, aircraft, plan_id))) return st;
+  for (int i = 0; i < n; ++i) {
+    const Out& o = ctx->h_out[i];
+    res[i].status = o.status;
+    res[i].plan_id = plan_id[i];
+    res[i].n_states = o.n_states;
+    res[i].fail_step = o.fail_step;
+    res[i].min_sep_m = std::sqrt((double)o.min_sep_d2) * ctx->air.u_m;
+    res[i].n_near_ties = o.n_near_ties;
+    res[i].n_exact = o.n_exact;
+    if (traj)
+      CK(cudaMemcpyAsync(traj + (size_t)i * traj_cap_each, ctx->d_traj + (size_t)i * ctx->cap_states * 3,
+                         sizeof(fmdp_qpos) * o.n_states, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  unsigned long long pc = 0;
+  CK(cudaMemcpy(&pc, ctx->d_pairctr, sizeof(pc), cudaMemcpyDeviceToHost));
+  ctx->stats.pair_evals = (int64_t)pc;
+  ctx->last_n = n;
   return FMDP_OK;
 }
 

@@ -1,6 +1,6 @@
 // fmdp_walk.cu -- sm_100a kernels of the FastMDP-GPU hot path.
 //
-// walk_kernel<C>: one thread-block CLUSTER of G CTAs walks one request's whole trajectory
+// walk_kernel<C, CS>: one thread-block CLUSTER of G CTAs walks one request's whole trajectory
 // (Fig 3a loop) with no host round trip per step; clusters take requests from
 // a device queue.  Per decision step k (clock row K = t0 + k):
 //   a1  stage the CTA's slice of row K (and prefetch row K+2) with cp.async.bulk (TMA)
@@ -89,10 +89,10 @@ __device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
   return d;
 }
-__device__ __forceinline__ f2 hi_far(f2 v) {  // replace the high float by a far-away coordinate
+__device__ __forceinline__ f2 hi_set(f2 v, float hi) {  // replace the high float
   float lo;
   asm("mov.b64 {%0, _}, %1;" : "=f"(lo) : "l"(v));
-  return pk2(lo, 3.0e18f);
+  return pk2(lo, hi);
 }
 __device__ __forceinline__ float min3(float a, f2 p) {
   float lo, hi, r;
@@ -145,6 +145,7 @@ struct Ctl {
   unsigned long long xmin;
   int32_t sl_lo[3], sl_n[3], sl_off[3];
   int32_t hgt[MAX_TURN];      // ground height under Delta_1 of every turn (cp.async target)
+  int32_t cs_ok;              // scratch of cs_idle
 };
 
 // Stage row K's slice for this CTA (slots [lo, lo+n) of n_row active slots): the first CH
@@ -200,11 +201,125 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// ----------------------------------------------------------------------------- co-simulation clock
+// SURVEY f2 (Alg 1: every aircraft decides from the states at clock K, then all
+// move).  Walker i publishes its state for clock K into cs_pub[K & 1][i] and arrives; a walker
+// reads clock K's entries once all cs_n walkers have arrived.  Two buffers suffice: a walker
+// writes clock K+2 only after passing clock K+1, i.e. after every walker published K+1, which
+// each does after it finished reading clock K.
+enum { CS_ABSENT = 0, CS_PRESENT = 1, CS_FINISHED = 2 };
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __noinline__ void cs_publish_at(int4* e, int x, int y, int z, int flags, int vx, int vy, int vz,
+                                           unsigned* arrive) {
+  __stcg(e, make_int4(x, y, z, flags));
+  __stcg(e + 1, make_int4(vx, vy, vz, 0));
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(arrive) : "memory");
+}
+__device__ __forceinline__ void cs_publish(const WalkArgs& a, int i, int64_t K, int x, int y, int z, int flags, int vx,
+                                           int vy, int vz) {
+  cs_publish_at(a.cs_pub + ((size_t)(K & 1) * a.cs_n + i) * 2, x, y, z, flags, vx, vy, vz, a.cs_arrive);
+}
+// true once every walker has published clock K; false on a timeout (~2 s: the walkers are not
+// all resident) or when another walker timed out.  (Plain pointers: a reference to the kernel
+// parameters would force a local copy of them.)
+__device__ __noinline__ bool cs_wait_until(const unsigned* arrive, int32_t* err, unsigned target) {
+  if (ld_acquire_gpu(arrive) >= target) return true;
+  const long long t0 = clock64();
+  for (;;) {
+    if (ld_acquire_gpu(arrive) >= target) return true;
+    if (*(volatile int32_t*)err) return false;
+    if (clock64() - t0 > (4ll << 30)) {
+      atomicExch(err, 1);
+      return false;
+    }
+  }
+}
+__device__ __forceinline__ bool cs_wait(const WalkArgs& a, int64_t K) {
+  return cs_wait_until(a.cs_arrive, a.cs_err, (unsigned)a.cs_n * (unsigned)(K - a.cs_k0 + 1));
+}
+// Clocks [K0, K1) (or until every walker has finished) on which walker i is not flying:
+// publish flags, keep the clock.  All threads of one CTA; false on a barrier failure.
+__device__ __noinline__ bool cs_idle(int4* pub_all, unsigned* arrive, int32_t* err, int n, int64_t k0, Ctl* ctl, int i,
+                                     int64_t K0, int64_t K1, int flags, bool until_all) {
+  for (int64_t K = K0; until_all || K < K1; ++K) {
+    int4* pub = pub_all + (size_t)(K & 1) * n * 2;
+    if (threadIdx.x == 0) {
+      __stcg(pub + 2 * i, make_int4(0, 0, 0, flags));
+      __stcg(pub + 2 * i + 1, make_int4(0, 0, 0, 0));
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(arrive) : "memory");
+      ctl->cs_ok = cs_wait_until(arrive, err, (unsigned)n * (unsigned)(K - k0 + 1)) ? 1 : 0;
+    }
+    __syncthreads();
+    const bool ok = ctl->cs_ok != 0;
+    bool all = until_all;
+    if (ok && until_all)
+      for (int j = threadIdx.x; j < n; j += blockDim.x) all &= __ldcg(&pub[2 * j]).w == CS_FINISHED;
+    all = __syncthreads_and(all);  // also orders cs_ok's read before the next write
+    if (!ok) return false;
+    if (all) return true;
+  }
+  return true;
+}
+
+struct TauSteps {
+  int k[NTAU];
+};
+// Well records of this CTA's batch peers j = rank + i*G (out of line: keeps the step loop's
+// code small).  Returns the thread's minimum separation d^2 to a present peer (saturated).
+__device__ __noinline__ uint32_t cs_build_peers(const int4* pub, int npr, int rank, int G, int self, int qx, int qy,
+                                                int qz, int ox, int oy, bool records, float* s_cen, int R_max,
+                                                uint32_t sat, TauSteps kt) {
+  uint32_t stay = sat;
+  for (int i = threadIdx.x; i < npr; i += blockDim.x) {
+    const int j = rank + i * G;
+    const int4 e = __ldcg(&pub[2 * j]);
+    const bool on = e.w == CS_PRESENT && j != self;
+    int rx = 0, ry = 0, rz = 0, vx = 0, vy = 0, vz = 0;
+    if (on) {
+      const int4 v = __ldcg(&pub[2 * j + 1]);
+      rx = e.x - qx; ry = e.y - qy; rz = e.z - qz;
+      vx = v.x; vy = v.y; vz = v.z;
+      stay = min(stay, clamp_d2(rx, ry, rz, R_max, sat));
+    }
+    if (records) {
+      float* cp = s_cen + PAIR_STRIDE * (i >> 1) + (i & 1);
+#pragma unroll
+      for (int t = 0; t < NTAU; ++t) {  // absent peer / self: a well at infinity (Q huge, offsets 0)
+        const float X = on ? (float)(ox - (rx + kt.k[t] * vx)) : 0.f;
+        const float Y = on ? (float)(oy - (ry + kt.k[t] * vy)) : 0.f;
+        const float Z = on ? (float)(-(rz + kt.k[t] * vz)) : 0.f;
+        cp[8 * t + 0] = X;
+        cp[8 * t + 2] = Y;
+        cp[8 * t + 4] = Z;
+        cp[8 * t + 6] = on ? fmaf(Z, Z, fmaf(Y, Y, X * X)) : 3.0e18f;
+      }
+    }
+  }
+  return stay;
+}
+// Exact int64 minimum d^2 from q to the tau-well of every present batch peer (this thread's share).
+__device__ __noinline__ unsigned long long cs_exact_peers(const int4* pub, int n, int self, int4 q4, int kt) {
+  unsigned long long best = ULLONG_MAX;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const int4 e = __ldcg(&pub[2 * j]);
+    if (e.w != CS_PRESENT || j == self) continue;
+    const int4 v = __ldcg(&pub[2 * j + 1]);
+    const int64_t dx = q4.x - (e.x + (int64_t)kt * v.x), dy = q4.y - (e.y + (int64_t)kt * v.y),
+                  dz = q4.z - (e.z + (int64_t)kt * v.z);
+    best = min(best, (unsigned long long)(dx * dx + dy * dy + dz * dz));
+  }
+  return best;
+}
+
 // Per-phase cycle accounting (rank 0, thread 0), enabled when args.prof != nullptr.
 enum Phase { PH_PROJ, PH_FIX, PH_WAIT, PH_HOT, PH_STAGE, PH_SCATTER, PH_BAR1, PH_OWNER, PH_BAR2, PH_DECIDE,
              PH_TOP, PH_SCAN, PH_PLOOP, PH_BUILD, PH_OWN1, PH_ARGMAX, PH_FLAGS, PH_N };
 
-template <int C>
+template <int C, bool CS>
 __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
     walk_kernel(const World w, const WalkArgs args, const int CH, const int RAWCAP, const int NGW) {
   cg::cluster_group cluster = cg::this_cluster();
@@ -251,6 +366,9 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   // plan-sharded multi-GPU step: xmode 1 exports this GPU's per-(state, tau)
   // minima and nearest-plan distance, xmode 2 imports their all-reduced minimum and decides
   const int xmode = args.xmode;
+  // SURVEY f2 co-simulated batch: a separate instantiation, so the FCFS walker carries no
+  // co-simulation code at all (measured: any of it on the step path costs ~1.5 %)
+  const int cosim = CS ? 1 : 0;
 
   const bool prof = args.prof != nullptr && rank == 0 && tid == 0;
   unsigned long long pacc[PH_N];
@@ -287,6 +405,12 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
     if (r >= args.n_reqs) break;
     const Req rq = args.reqs[r];
     const size_t sbase = (size_t)rq.slot * args.cap;
+    if (cosim) {  // keep the batch clock until this aircraft departs
+      if (rank == 0 && rq.t0 > args.cs_k0)
+        cs_idle(args.cs_pub, args.cs_arrive, args.cs_err, args.cs_n, args.cs_k0, ctl, r, args.cs_k0, rq.t0, CS_ABSENT,
+                false);
+      cluster.sync();
+    }
     // walker state, identical in every thread of every CTA of the cluster
     int k = rq.start_k;
     int qx, qy, qz, psi;
@@ -321,6 +445,8 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         int32_t* tq = args.traj + 3 * sbase;
         tq[0] = rq.src[0]; tq[1] = rq.src[1]; tq[2] = rq.src[2];
         args.heading[sbase] = rq.psi0;
+        if (cosim)  // departure: level flight along the initial heading (R28)
+          cs_publish(args, r, rq.t0, qx, qy, qz, CS_PRESENT, s_dxy[psi].x, s_dxy[psi].y, 0);
       }
       const int64_t K0 = rq.t0 + k;
       const int n0 = row_count(w, K0), n1 = row_count(w, K0 + 1);
@@ -356,6 +482,8 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       const int p = k & 1;
       const int bK = (int)(K % 3), bK2 = (int)((K + 2) % 3);
       int4* s_pos = s_pos2 + p * AW;
+      // fan origin of this step's projected states (hot-loop formulation)
+      const int ox = (W >> 1) * s_dxy[psi].x, oy = (W >> 1) * s_dxy[psi].y;
       if (tid == 0) {
         if (!args.eval && !fin) {
           issue_row(w, K + 2, cnt2, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, args.shard_rank, args.shard_world);
@@ -408,10 +536,12 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
             y += ay[s];
           }
         }
-        sx = (float)(x - qx);
-        sy = (float)(y - qy);
+        // offsets from the fan origin o = q + (W/2) (DX, DY)[psi], doubled: the hot loop
+        // evaluates |s - c|^2 - |s - o|^2 = Q + 2 (s - o).X with X = o - c, Q = |X|^2
+        sx = (float)(2 * (x - qx - ox));
+        sy = (float)(2 * (y - qy - oy));
 #pragma unroll
-        for (int c = 0; c < C; ++c) sz[c] = (float)(w.climb[c] * t);
+        for (int c = 0; c < C; ++c) sz[c] = (float)(2 * w.climb[c] * t);
         sx2 = pk2(sx, sx);
         sy2 = pk2(sy, sy);
 #pragma unroll
@@ -520,67 +650,101 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
             int slot = jj;
             if (compact && keep) slot = atomicAdd(counter, 1);  // survivors are rare: no warp round trip
             if (keep && slot < CH) {
-              // plan pair layout: [pair][tau][x_j, x_j', y_j, y_j', z_j, z_j'] (+6 pad), negated
-              // offsets so that s - c is one packed add; exact integers < 2^24 (R23)
+              // plan pair layout: [pair][tau][X_j, X_j', Y_j, Y_j', Z_j, Z_j', Q_j, Q_j']: X = o - c
+              // (exact integers < 2^24, R23) and Q = |X|^2 (FP32, DESIGN.md §7 error bound)
               float* cp = s_cen + PAIR_STRIDE * (slot >> 1) + (slot & 1);
 #pragma unroll
               for (int t = 0; t < NTAU; ++t) {
-                cp[6 * t + 0] = (float)(-(rx + w.k_tau[t] * vx));
-                cp[6 * t + 2] = (float)(-(ry + w.k_tau[t] * vy));
-                cp[6 * t + 4] = (float)(-(rz + w.k_tau[t] * vz));
+                const float X = (float)(ox - (rx + w.k_tau[t] * vx));
+                const float Y = (float)(oy - (ry + w.k_tau[t] * vy));
+                const float Z = (float)(-(rz + w.k_tau[t] * vz));
+                cp[8 * t + 0] = X;
+                cp[8 * t + 2] = Y;
+                cp[8 * t + 4] = Z;
+                cp[8 * t + 6] = fmaf(Z, Z, fmaf(Y, Y, X * X));
               }
             }
           }
         };
         // Hot loop over ns well records (two plans per packed instruction).
         auto hot = [&](int ns) {
-          // (state, well) pair: |s - c|^2 = (dx^2 + dy^2) + dz^2, the horizontal part shared
-          // by the C climbs; FMNMX3 folds both plans of a pair into the running minimum
-#define FMDP_WELL2(T, X, Y, Z)                                \
-  {                                                           \
-    const f2 dx = add2(sx2, (X)), dy = add2(sy2, (Y));        \
-    const f2 hh = fma2(dy, dy, mul2(dx, dx));                 \
-    _Pragma("unroll") for (int cc_ = 0; cc_ < C; ++cc_) {     \
-      const f2 dz = add2(sz2[cc_], (Z));                      \
-      m[cc_][T] = min3(m[cc_][T], fma2(dz, dz, hh));          \
-    }                                                         \
+          // (state, well) pair: |s - c|^2 - |s - o|^2 = Q + 2(s-o).X, the horizontal part
+          // shared by the C climbs (2 FFMA2), one FFMA2 per climb; FMNMX3 folds both plans of a
+          // pair into the running minimum (|s - o|^2 is added back by the owner)
+#define FMDP_WELL2(T, XY, ZQ)                                  \
+  {                                                            \
+    const f2 h = fma2(sy2, (XY).y, fma2(sx2, (XY).x, (ZQ).y)); \
+    _Pragma("unroll") for (int cc_ = 0; cc_ < C; ++cc_) {      \
+      m[cc_][T] = min3(m[cc_][T], fma2(sz2[cc_], (ZQ).x, h));  \
+    }                                                          \
   }
           const int npf = ns >> 1;  // full pairs; an odd tail is peeled below
           const ulonglong2* c8 = cen2 + (PAIR_STRIDE / 4) * grp;
           for (int pp = grp; pp < npf; pp += NGW, c8 += (PAIR_STRIDE / 4) * NGW) {
             const ulonglong2 e0 = c8[0], e1 = c8[1], e2 = c8[2], e3 = c8[3], e4 = c8[4], e5 = c8[5], e6 = c8[6],
-                             e7 = c8[7];
-            FMDP_WELL2(0, e0.x, e0.y, e1.x)
-            FMDP_WELL2(1, e1.y, e2.x, e2.y)
-            FMDP_WELL2(2, e3.x, e3.y, e4.x)
-            FMDP_WELL2(3, e4.y, e5.x, e5.y)
-            FMDP_WELL2(4, e6.x, e6.y, e7.x)
+                             e7 = c8[7], e8 = c8[8], e9 = c8[9];
+            FMDP_WELL2(0, e0, e1)
+            FMDP_WELL2(1, e2, e3)
+            FMDP_WELL2(2, e4, e5)
+            FMDP_WELL2(3, e6, e7)
+            FMDP_WELL2(4, e8, e9)
           }
           if ((ns & 1) && npf % NGW == grp) {  // odd tail: the partner slot is a well at infinity
             const ulonglong2* t8 = cen2 + (PAIR_STRIDE / 4) * npf;
-            ulonglong2 e0 = t8[0], e1 = t8[1], e2 = t8[2], e3 = t8[3], e4 = t8[4], e5 = t8[5], e6 = t8[6], e7 = t8[7];
-            e0.x = hi_far(e0.x); e0.y = hi_far(e0.y); e1.x = hi_far(e1.x); e1.y = hi_far(e1.y);
-            e2.x = hi_far(e2.x); e2.y = hi_far(e2.y); e3.x = hi_far(e3.x); e3.y = hi_far(e3.y);
-            e4.x = hi_far(e4.x); e4.y = hi_far(e4.y); e5.x = hi_far(e5.x); e5.y = hi_far(e5.y);
-            e6.x = hi_far(e6.x); e6.y = hi_far(e6.y); e7.x = hi_far(e7.x);
-            FMDP_WELL2(0, e0.x, e0.y, e1.x)
-            FMDP_WELL2(1, e1.y, e2.x, e2.y)
-            FMDP_WELL2(2, e3.x, e3.y, e4.x)
-            FMDP_WELL2(3, e4.y, e5.x, e5.y)
-            FMDP_WELL2(4, e6.x, e6.y, e7.x)
+            ulonglong2 e[10];
+#pragma unroll
+            for (int i = 0; i < 10; ++i) {
+              e[i] = t8[i];
+              if (i & 1) {
+                e[i].x = hi_set(e[i].x, 0.f);
+                e[i].y = hi_set(e[i].y, 3.0e18f);
+              } else {
+                e[i].x = hi_set(e[i].x, 0.f);
+                e[i].y = hi_set(e[i].y, 0.f);
+              }
+            }
+            FMDP_WELL2(0, e[0], e[1])
+            FMDP_WELL2(1, e[2], e[3])
+            FMDP_WELL2(2, e[4], e[5])
+            FMDP_WELL2(3, e[6], e[7])
+            FMDP_WELL2(4, e[8], e[9])
           }
 #undef FMDP_WELL2
           if (tid == 0 && args.pairs) atomicAdd(args.pairs, (unsigned long long)ns * NTAU * AW);
         };
 
-        for (int c0 = 0, cidx = 0; xmode != 2 && c0 < n; c0 += SC, ++cidx) {
-          const int nc = min(SC, n - c0);
+        // batch peers at clock K (Alg 5, P^- of Table DS), five wells each, staged
+        // as one more chunk after the row's (same records, same hot loop); this CTA takes peers
+        // j = rank + i*G.  The clock wait sits after the row's hot loop, overlapping it.
+        auto build_peers = [&]() -> int {
+          // (a failed wait sets cs_err: the host discards the batch; later waits return at once)
+          if (tid == 0) cs_wait(args, K);
+          __syncthreads();
+          const int npr = args.cs_n > (int)rank ? (args.cs_n - (int)rank + (int)G - 1) / (int)G : 0;
+          TauSteps kt;
+#pragma unroll
+          for (int t = 0; t < NTAU; ++t) kt.k[t] = w.k_tau[t];
+          stay = min(stay, cs_build_peers(args.cs_pub + (size_t)(K & 1) * args.cs_n * 2, npr, (int)rank, (int)G, r, qx,
+                                          qy, qz, ox, oy, !fin, s_cen, w.R_max, w.sat_d2, kt));
+          return npr;
+        };
+
+        const int n_chunks = xmode != 2 ? (n + SC - 1) / SC : 0;
+        for (int cidx = 0; cidx < n_chunks + cosim; ++cidx) {
+          const int c0 = cidx * SC;
+          const bool peers = cidx == n_chunks;
           int* counter = &ctl->nsurv[(k & 1) * 2 + (cidx & 1)];
-          build(c0, nc, args.cull != 0, counter);
+          int nc;
+          if (!peers) {
+            nc = min(SC, n - c0);
+            build(c0, nc, args.cull != 0, counter);
+          } else {
+            nc = build_peers();
+          }
           if (fin) continue;
           FMDP_MARK(PH_BUILD)
           __syncthreads();
-          const int ns = args.cull ? *counter : nc;
+          const int ns = (args.cull && !peers) ? *counter : nc;
           if (tid == 0) ctl->nsurv[(k & 1) * 2 + ((cidx + 1) & 1)] = 0;  // next pass's counter
           if (ns <= CH) {
             hot(ns);
@@ -666,6 +830,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       }
       cluster.sync();
       FMDP_MARK(PH_BAR1)
+      // co-simulation barrier failure, as every CTA of the cluster saw it at this step
       if (xmode == 1 && rank == 0 && tid == 0) args.xbuf[NTAU * AW] = s_stay[p];
 
       if (!fin) {
@@ -709,6 +874,13 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
 #pragma unroll
               for (int t = 0; t < NTAU; ++t) M[t] = __uint_as_float(args.xbuf[st * NTAU + t]);
             }
+            {  // |s - o|^2 back in (exact integer < 2^24; one rounding)
+              const int4 q4 = s_pos[st];
+              const int dx = q4.x - qx - ox, dy = q4.y - qy - oy, dz = q4.z - qz;
+              const float s2 = (float)(dx * dx + dy * dy + dz * dz);
+#pragma unroll
+              for (int t = 0; t < NTAU; ++t) M[t] += s2;
+            }
 #pragma unroll
             for (int t = 0; t < NTAU; ++t) {
               if (M[t] < w.R2lo[t]) {
@@ -738,6 +910,12 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
                 if (oa2 >= n_own) continue;
                 float M = FLT_MAX;
                 for (int b = 0; b < (int)G; ++b) M = fminf(M, rcv[(b * NOWN + oa2) * BLK + l2 * NTAU + t]);
+                if (xmode == 2) M = __uint_as_float(args.xbuf[((((int)rank + oa2 * (int)G) * W + l2) * NTAU + t)]);
+                {
+                  const int4 q4 = s_pos[((int)rank + oa2 * (int)G) * W + l2];
+                  const int dx = q4.x - qx - ox, dy = q4.y - qy - oy, dz = q4.z - qz;
+                  M += (float)(dx * dx + dy * dy + dz * dz);
+                }
                 if (!(M >= w.R2lo[t] && M <= w.R2hi[t])) continue;
                 item = (((int)rank + oa2 * (int)G) * W + l2) * NTAU + t;
               }
@@ -754,6 +932,9 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
                 const int64_t dx = q4.x - cx, dy = q4.y - cy, dz = q4.z - cz;
                 best = min(best, (unsigned long long)(dx * dx + dy * dy + dz * dz));
               }
+              if (cosim)  // batch peers of clock K
+                best = min(best, cs_exact_peers(args.cs_pub + (size_t)(K & 1) * args.cs_n * 2, args.cs_n, r, q4,
+                                                w.k_tau[t]));
               for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
               if (lane == 0 && best != ULLONG_MAX) atomicMin(&ctl->xmin, best);
               __syncthreads();
@@ -890,6 +1071,10 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       }
       FMDP_MARK(PH_DECIDE)
       if (done) break;
+      // co-simulation: state of clock K+1 and its velocity, the last displacement
+      // q(k+1) - q(k) = ((DX, DY)[psi_{k+1}], climb of a*) (R28)
+      if (cosim && rank == 0 && tid == 0)
+        cs_publish(args, r, K + 1, qx, qy, qz, CS_PRESENT, s_dxy[psi].x, s_dxy[psi].y, w.climb[a1 % C]);
     }
 
     // eval only: separation minimum of every action's Delta_1 vs the whole row K+1 (debug hook)
@@ -935,6 +1120,9 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
     }
     pending = 0;
     __syncthreads();
+    // co-simulation: this aircraft has left; keep the clock until every walker has
+    if (cosim && rank == 0) cs_idle(args.cs_pub, args.cs_arrive, args.cs_err, args.cs_n, args.cs_k0, ctl, r, rq.t0 + k + 1, 0, CS_FINISHED,
+              true);
   }
   if (prof) {
     for (int i = 0; i < PH_N; ++i) atomicAdd(&args.prof[i], pacc[i]);
@@ -1018,15 +1206,15 @@ int walk_threads(int ncol, int max_threads) {
   return 32 * ((ncol + cpw - 1) / cpw);
 }
 
-template <int C>
+template <int C, bool CS>
 static cudaError_t launch_walk_t(const World& w, const WalkArgs& a, int cluster, int n_clusters, int threads,
                                  int chunk, int rawcap, cudaStream_t s) {
   Layout L;
   L.build(w.HL, chunk, rawcap, threads, C, w.n_turn * w.W, w.A, w.A * w.W, cluster);
-  cudaError_t e = cudaFuncSetAttribute(walk_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+  cudaError_t e = cudaFuncSetAttribute(walk_kernel<C, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
   if (cluster > 8) {
-    e = cudaFuncSetAttribute(walk_kernel<C>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaFuncSetAttribute(walk_kernel<C, CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg = {};
@@ -1042,17 +1230,17 @@ static cudaError_t launch_walk_t(const World& w, const WalkArgs& a, int cluster,
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const int ngw = walk_groups_per_warp(w.n_turn * w.W, threads);
-  return cudaLaunchKernelEx(&cfg, walk_kernel<C>, w, a, chunk, rawcap, ngw);
+  return cudaLaunchKernelEx(&cfg, walk_kernel<C, CS>, w, a, chunk, rawcap, ngw);
 }
 
-template <int C>
+template <int C, bool CS>
 static cudaError_t max_clusters_t(const World& w, int cluster, int threads, int chunk, int rawcap, int* out) {
   Layout L;
   L.build(w.HL, chunk, rawcap, threads, C, w.n_turn * w.W, w.A, w.A * w.W, cluster);
-  cudaError_t e = cudaFuncSetAttribute(walk_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+  cudaError_t e = cudaFuncSetAttribute(walk_kernel<C, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
   if (cluster > 8) {
-    e = cudaFuncSetAttribute(walk_kernel<C>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaFuncSetAttribute(walk_kernel<C, CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg = {};
@@ -1066,24 +1254,32 @@ static cudaError_t max_clusters_t(const World& w, int cluster, int threads, int 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaOccupancyMaxActiveClusters(out, walk_kernel<C>, &cfg);
+  return cudaOccupancyMaxActiveClusters(out, walk_kernel<C, CS>, &cfg);
 }
 
 cudaError_t launch_walk(const World& w, const WalkArgs& a, int n_climb, int cluster, int n_clusters, int threads,
                         int chunk, int rawcap, cudaStream_t s) {
+  const bool cs = a.cosim != 0;
   switch (n_climb) {
-    case 1: return launch_walk_t<1>(w, a, cluster, n_clusters, threads, chunk, rawcap, s);
-    case 3: return launch_walk_t<3>(w, a, cluster, n_clusters, threads, chunk, rawcap, s);
-    case 5: return launch_walk_t<5>(w, a, cluster, n_clusters, threads, chunk, rawcap, s);
+    case 1: return cs ? launch_walk_t<1, true>(w, a, cluster, n_clusters, threads, chunk, rawcap, s)
+                      : launch_walk_t<1, false>(w, a, cluster, n_clusters, threads, chunk, rawcap, s);
+    case 3: return cs ? launch_walk_t<3, true>(w, a, cluster, n_clusters, threads, chunk, rawcap, s)
+                      : launch_walk_t<3, false>(w, a, cluster, n_clusters, threads, chunk, rawcap, s);
+    case 5: return cs ? launch_walk_t<5, true>(w, a, cluster, n_clusters, threads, chunk, rawcap, s)
+                      : launch_walk_t<5, false>(w, a, cluster, n_clusters, threads, chunk, rawcap, s);
     default: return cudaErrorInvalidValue;
   }
 }
 
-cudaError_t walk_max_clusters(const World& w, int n_climb, int cluster, int threads, int chunk, int rawcap, int* out) {
+cudaError_t walk_max_clusters(const World& w, int n_climb, int cluster, int threads, int chunk, int rawcap, int* out,
+                              bool cosim) {
   switch (n_climb) {
-    case 1: return max_clusters_t<1>(w, cluster, threads, chunk, rawcap, out);
-    case 3: return max_clusters_t<3>(w, cluster, threads, chunk, rawcap, out);
-    case 5: return max_clusters_t<5>(w, cluster, threads, chunk, rawcap, out);
+    case 1: return cosim ? max_clusters_t<1, true>(w, cluster, threads, chunk, rawcap, out)
+                         : max_clusters_t<1, false>(w, cluster, threads, chunk, rawcap, out);
+    case 3: return cosim ? max_clusters_t<3, true>(w, cluster, threads, chunk, rawcap, out)
+                         : max_clusters_t<3, false>(w, cluster, threads, chunk, rawcap, out);
+    case 5: return cosim ? max_clusters_t<5, true>(w, cluster, threads, chunk, rawcap, out)
+                         : max_clusters_t<5, false>(w, cluster, threads, chunk, rawcap, out);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -96,7 +96,7 @@ PHASES = ("projection", "goal_terrain", "row_wait", "hot_loop", "stage", "reduce
 
 EXPORTS = ["fmdp_airspace_default", "fmdp_create", "fmdp_destroy", "fmdp_set_launch", "fmdp_add_plan",
            "fmdp_add_plans", "fmdp_schedule", "fmdp_schedule_batch", "fmdp_schedule_sharded",
-           "fmdp_schedule_departures", "fmdp_get_steplog", "fmdp_get_plan",
+           "fmdp_schedule_departures", "fmdp_schedule_cosim", "fmdp_cosim_max", "fmdp_get_steplog", "fmdp_get_plan",
            "fmdp_num_plans", "fmdp_truncate", "fmdp_eval_step", "fmdp_get_stats", "fmdp_num_actions",
            "fmdp_strerror", "fmdp_last_error"]
 
@@ -122,6 +122,9 @@ def lib():
         L.fmdp_schedule.argtypes = [vp, C.c_uint64, Vec3, Vec3, i64, C.POINTER(Result), vp, i32]
         L.fmdp_schedule_batch.argtypes = [vp, vp, i32, vp, vp, i32, i32]
         L.fmdp_schedule_departures.argtypes = [vp, C.c_uint64, Vec3, Vec3, i64, i32, vp, vp, vp, i32, C.POINTER(i32)]
+        L.fmdp_schedule_cosim.argtypes = [vp, vp, i32, vp, vp, i32]
+        L.fmdp_cosim_max.argtypes = [vp]
+        L.fmdp_cosim_max.restype = i32
         L.fmdp_schedule_sharded.argtypes = [vp, C.POINTER(Shard), C.c_uint64, Vec3, Vec3, i64, C.POINTER(Result), vp,
                                             i32]
         L.fmdp_get_steplog.argtypes = [vp, i32, vp, vp, vp, i32, C.POINTER(i32)]
@@ -332,6 +335,21 @@ class FMDP:
                                                _p(traj), cap, BATCH_SEQUENTIAL if sequential else 0),
                     "fmdp_schedule_batch")
         return [self._res(res[i], None if traj is None else traj[i]) for i in range(n)]
+
+    def schedule_cosim(self, src, dst, t0, want_traj: bool = True, reqs=None) -> List[ScheduleResult]:
+        """co-simulated batch (mutually aware, one clock); accepted plans appended in order."""
+        if reqs is None:
+            reqs = self.make_requests(src, dst, t0)
+        n = len(reqs)
+        res = (Result * n)()
+        cap = self.max_steps + 1
+        traj = np.zeros((n, cap, 3), np.int32) if want_traj else None
+        self._check(self.L.fmdp_schedule_cosim(self.ctx, C.cast(reqs, C.c_void_p), n, C.cast(res, C.c_void_p),
+                                               _p(traj), cap), "fmdp_schedule_cosim")
+        return [self._res(res[i], None if traj is None else traj[i]) for i in range(n)]
+
+    def cosim_max(self) -> int:
+        return int(self.L.fmdp_cosim_max(self.ctx))
 
     def schedule_sharded(self, src, dst, t0: int, rank: int, world: int, allreduce_min, aircraft_id: int = 0,
                          want_traj: bool = True) -> ScheduleResult:
