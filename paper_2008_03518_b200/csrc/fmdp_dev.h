@@ -34,7 +34,8 @@ struct World {
   int64_t cap2;                 // goal capture radius^2
   int32_t reach_u;              // bound on |s_{a,t} - q| over all projected states
   int32_t step_reach_u;         // bound on |Delta_1(a) - q| (one substep)
-  double goal_r, goal_l2g;      // goal peak: |r|, log2(gamma) * u  (fp64)
+  double goal_r, goal_l2g;      // goal peak: |r|, log2(gamma) * u
+  float goal_rf, goal_l2gf;     // the same in FP32 (kernel: ex2.approx of exact-offset distances)
   float intr_r, intr_l2g;       // intruder wells: |r|, log2(gamma) * u (FP32 ex2)
   float terr_r, terr_l2g;       // terrain wells
   int32_t zdeck_u;
@@ -62,7 +63,7 @@ struct Req {
   int32_t start_k;              // resume step (0 = fresh request)
   int64_t t0;
   int32_t slot;                 // output slot
-  int32_t pad;
+  int32_t head;                 // 1: the earliest pending FCFS request (never paused; sets *stop when done)
 };
 
 struct Out {
@@ -85,6 +86,8 @@ struct WalkArgs {
   int32_t cap;
   int32_t eval;                 // 1: evaluate one step (debug outputs), no advance
   int32_t budget;               // decision steps per request in this launch (then pause, status -1)
+  int32_t* stop;                // single-wave slices: set by the head request when it finishes; the
+                                // others pause after `budget` steps only once it is set (nullptr: off)
   int32_t cull;                 // 1: f1 exact culling of plans whose wells cannot reach the states
   int32_t shard_rank, shard_world;  // plan shard of this GPU; 0, 1 = whole rows
   int32_t xmode;                // 0 normal; 1 export per-(state,tau) minima + stay; 2 import and decide

@@ -66,6 +66,7 @@ struct fmdp_ctx {
   uint32_t* d_stepd2 = nullptr;
   int8_t* d_ntie = nullptr;
   int32_t* d_queue = nullptr;
+  int32_t* d_stop = nullptr;   // head-finished flag of a single-wave slice
   int32_t* d_nstates = nullptr;
   int64_t* d_t0s = nullptr;
   unsigned long long* d_pairctr = nullptr;
@@ -250,22 +251,28 @@ int max_clusters(fmdp_ctx* ctx, int G, bool cosim = false) {
   return n;
 }
 
-// Cluster size for a round of n_run trajectories: the G minimising
-// waves(G) * (per-step work / G + per-step sync overhead), among sizes that can run.
+// Per-step cycles of one walker with cluster size G over rows of P plans, measured on B200
+// (tools/calib.py: configs[1] 3000 plans and configs[3] 100k plans, G = 1..16, full and f1):
+//   t(G) = 12200 (projection, epilogue, barriers, decision) + P*b/G + 130*G,
+//   b = 2.8 cycles/plan with culling (build pass), 5*A*W/26.5 without (hot loop, ~26.5 pairs/clk/SM).
+double step_cycles(const fmdp_ctx* ctx, double plans, int G) {
+  const double b = ctx->launch.cull ? 2.8 : fmdp::NTAU * ctx->A * ctx->W / 26.5;
+  return 12200.0 + plans * b / G + 130.0 * G;
+}
+
+double mean_plans(const fmdp_ctx* ctx) {
+  int64_t tot = 0, nz = 0;
+  for (int32_t c : ctx->counts)
+    if (c) { tot += c; ++nz; }
+  return nz ? (double)tot / nz : 0.0;
+}
+
+// Cluster size for a round of n_run trajectories: the G minimising waves(G) * t(G) among the
+// sizes that can run.
 void choose_launch(fmdp_ctx* ctx, int n_run, int* G_out, int* nc_out) {
   int best_G = 1;
   double best = 1e300;
-  double plans = 0;
-  {
-    int64_t tot = 0, nz = 0;
-    for (int32_t c : ctx->counts)
-      if (c) { tot += c; ++nz; }
-    plans = nz ? (double)tot / nz : 0.0;
-  }
-  // per-step cycles of one walker: hot loop (~21 pairs/clk/SM, measured) / G + per-step
-  // overhead (projection, reductions, two cluster barriers, decision; measured ~16k cycles)
-  // (with f1 culling the hot loop is a few dozen plans: the build pass over the slice remains)
-  const double work = ctx->launch.cull ? plans * 0.6 : plans * fmdp::NTAU * ctx->A * ctx->W / 21.0;
+  const double plans = mean_plans(ctx);
   const int sizes[] = {16, 8, 4, 2, 1};
   for (int G : sizes) {
     if (ctx->launch.cluster_size && G != ctx->launch.cluster_size) continue;
@@ -274,8 +281,8 @@ void choose_launch(fmdp_ctx* ctx, int n_run, int* G_out, int* nc_out) {
     int conc = std::min(mc, n_run);
     if (ctx->launch.max_walkers > 0) conc = std::min(conc, ctx->launch.max_walkers);
     const double waves = std::ceil((double)n_run / conc);
-    const double t = waves * (work / G + 16000.0 + 300.0 * G);
-    if (t < best) {
+    const double t = waves * step_cycles(ctx, plans, G);
+    if (t < best - 1e-9) {
       best = t;
       best_G = G;
     }
@@ -288,6 +295,23 @@ void choose_launch(fmdp_ctx* ctx, int n_run, int* G_out, int* nc_out) {
   if (std::getenv("FMDP_DEBUG"))
     std::fprintf(stderr, "fmdp: n_run=%d plans/row=%.0f -> G=%d clusters=%d (max active %d)\n", n_run, plans, best_G,
                  *nc_out, mc);
+}
+
+// The cluster size a lone walker would get (fastest per step).
+int solo_cluster_size(fmdp_ctx* ctx) {
+  int best_G = 1;
+  double best = 1e300;
+  const double plans = mean_plans(ctx);
+  for (int G : {16, 8, 4, 2, 1}) {
+    if (ctx->launch.cluster_size && G != ctx->launch.cluster_size) continue;
+    if (max_clusters(ctx, G) <= 0) continue;
+    const double t = step_cycles(ctx, plans, G);
+    if (t < best - 1e-9) {
+      best = t;
+      best_G = G;
+    }
+  }
+  return best_G;
 }
 
 fmdp::WalkArgs make_args(fmdp_ctx* ctx, const std::vector<Req>& run, bool eval, int budget) {
@@ -519,7 +543,20 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
           run.push_back(r);
         }
       if (!run.empty()) {
-        if ((st = run_walk(ctx, run, false, budget))) return st;
+        // A slice whose walkers are all resident at the cluster size a lone walker would use
+        // runs the head (request c: everything before it is committed, so it can never be
+        // rolled back) to completion; the others go on past `budget` until it is done -- their
+        // extra steps cost no wall time and stay valid unless a rollback discards them.
+        int G = 0, nc = 0;
+        choose_launch(ctx, (int)run.size(), &G, &nc);
+        const bool single = nc >= (int)run.size() && G >= solo_cluster_size(ctx);
+        fmdp::WalkArgs a = make_args(ctx, run, false, budget);
+        if (single) {
+          run[0].head = 1;  // run[0] is request c
+          CK(cudaMemsetAsync(ctx->d_stop, 0, sizeof(int32_t), ctx->stream));
+          a.stop = ctx->d_stop;
+        }
+        if ((st = run_walk(ctx, run, false, budget, &a, G, nc))) return st;
         runs += (int)run.size();
         ctx->stats.rounds += 1;
       }
@@ -773,6 +810,8 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   w.cap2 = capu * capu;
   w.goal_r = std::fabs(a.goal_r);
   w.goal_l2g = std::log2(a.goal_gamma) * a.u_m;
+  w.goal_rf = (float)w.goal_r;
+  w.goal_l2gf = (float)w.goal_l2g;
   w.intr_r = (float)std::fabs(a.intr_r);
   w.intr_l2g = (float)(std::log2(a.intr_gamma) * a.u_m);
   w.terr_r = (float)std::fabs(a.terr_r);
@@ -852,6 +891,7 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   ctx->d_counts = (int32_t*)dalloc(ctx, sizeof(int32_t) * (size_t)w.horizon);
   ctx->d_dxy = (int2*)dalloc(ctx, sizeof(int2) * w.HL);
   ctx->d_queue = (int32_t*)dalloc(ctx, sizeof(int32_t) * 4);
+  ctx->d_stop = ctx->d_queue ? ctx->d_queue + 2 : nullptr;
   ctx->d_pairctr = (unsigned long long*)dalloc(ctx, sizeof(unsigned long long));
   ctx->d_prof = (unsigned long long*)dalloc(ctx, sizeof(unsigned long long) * fmdp::N_PHASES);
   ctx->d_dbg_vstar = (double*)dalloc(ctx, sizeof(double) * A);

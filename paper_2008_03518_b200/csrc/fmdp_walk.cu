@@ -146,6 +146,7 @@ struct Ctl {
   int32_t sl_lo[3], sl_n[3], sl_off[3];
   int32_t hgt[MAX_TURN];      // ground height under Delta_1 of every turn (cp.async target)
   int32_t cs_ok;              // scratch of cs_idle
+  int32_t stop[2];            // head-finished flag seen by rank 0 at the top of the step, by parity
 };
 
 // Stage row K's slice for this CTA (slots [lo, lo+n) of n_row active slots): the first CH
@@ -155,7 +156,11 @@ __device__ __forceinline__ void issue_row(const World& w, int64_t K, int n_row, 
                                           int32_t* raw, int RAWW, uint64_t* bars, Ctl* ctl, int srank, int sworld) {
   const int b = (int)(K % 3);
   // plan shard of this GPU: slots [s0, s1) of the row, then this CTA's part
-  const int s0 = (int)(((int64_t)n_row * srank) / sworld), s1 = (int)(((int64_t)n_row * (srank + 1)) / sworld);
+  int s0 = 0, s1 = n_row;  // single GPU: no 64-bit division on the step's critical path
+  if (sworld > 1) {
+    s0 = (int)(((int64_t)n_row * srank) / sworld);
+    s1 = (int)(((int64_t)n_row * (srank + 1)) / sworld);
+  }
   const uint32_t len = (uint32_t)(s1 - s0);
   const int lo = s0 + (int)((len * rank) >> lgG), hi = s0 + (int)((len * (rank + 1)) >> lgG);
   const int e = min(hi, lo + CH);
@@ -490,6 +495,10 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           cnt2 = row_count(w, K + 3);  // consumed next step: latency hidden by this step
         }
         ctl->nsurv[((k + 1) & 1) * 2] = 0;  // step k+1, chunk 0 (last used in step k-1)
+        if (args.stop && rank == 0) {  // one reading for the whole cluster, visible after BAR1
+          const int f = *(volatile int32_t*)args.stop;
+          for (unsigned b = 0; b < G; ++b) cluster.map_shared_rank(&ctl->stop[p], b)[0] = f;
+        }
       }
       if (!args.eval && !fin) pending |= 1u << bK2;
       FMDP_MARK(PH_TOP)
@@ -560,14 +569,15 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         FMDP_MARK(PH_PLOOP)
         __syncthreads();
         FMDP_MARK(PH_PROJ)
-        // ---- a3 goal (fp64), deck, a5 terrain (exact predicate, FP32 ex2 value): owned states
+        // ---- a3 goal (FP32 ex2), deck, a5 terrain (exact predicate, FP32 ex2 value): owned states
         const int ntc = ctl->ntc[p];
         const int32_t* s_tc = s_tc2 + p * TC_MAX;
         for (int i = tid; i < n_own * W; i += NT) {
           const int st = ((int)rank + (i / W) * (int)G) * W + i % W;
           const int4 q4 = s_pos[st];
-          const double gx = (double)q4.x - rq.dst[0], gy = (double)q4.y - rq.dst[1], gz = (double)q4.z - rq.dst[2];
-          const double vpos = w.goal_r * exp2(w.goal_l2g * sqrt(gx * gx + gy * gy + gz * gz));
+          // FP32: exact integer offsets (< 2^24), |rel err| ~ 2^-21 << the 1e-5 S tolerance (R25)
+          const float gx = (float)(q4.x - rq.dst[0]), gy = (float)(q4.y - rq.dst[1]), gz = (float)(q4.z - rq.dst[2]);
+          const double vpos = (double)(w.goal_rf * ex2_approx(w.goal_l2gf * sqrtf(fmaf(gz, gz, fmaf(gy, gy, gx * gx)))));
           const double valt = (q4.z < w.zdeck_u) ? (w.deck_scale - w.u_m * (double)q4.z) : 0.0;
           int64_t mT = INT64_MAX;
           const int nt = ntc <= TC_MAX ? ntc : w.n_tw;
@@ -837,6 +847,27 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         // ---- owner epilogue (half-warp per owned action, lane = substep): G-way minimum of
         //      the partial blocks, exact in/out, values (Alg 8), V*(a)
         const float* rcv = s_recv + p * (int)G * NOWN * BLK;
+        // G-way minimum of the partial blocks spread over the whole CTA, one (action, substep,
+        // tau) per thread, into s_stage (free: this CTA's scatter completed before BAR1)
+        float* s_M = s_stage;
+        {
+          const int sstride = NOWN * BLK;
+          for (int i = tid; i < n_own * W * NTAU; i += NT) {
+            const int oa = i / (W * NTAU), r2 = i - oa * (W * NTAU);
+            const float* src = rcv + oa * BLK + r2;
+            float M0 = src[0], M1 = FLT_MAX, M2 = FLT_MAX, M3 = FLT_MAX;
+            int b = 1;
+            for (; b + 3 < (int)G; b += 4) {  // four independent load streams
+              M0 = fminf(M0, src[b * sstride]);
+              M1 = fminf(M1, src[(b + 1) * sstride]);
+              M2 = fminf(M2, src[(b + 2) * sstride]);
+              M3 = fminf(M3, src[(b + 3) * sstride]);
+            }
+            for (; b < (int)G; ++b) M0 = fminf(M0, src[b * sstride]);
+            s_M[i] = fminf(fminf(M0, M1), fminf(M2, M3));
+          }
+          __syncthreads();
+        }
         const int hw = tid >> 4, hl = tid & 15;
         const int n_hw = NT >> 4;
         for (int oa0 = 0; oa0 < NOWN; oa0 += n_hw) {  // uniform trip count across the CTA
@@ -847,26 +878,9 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           float mi = FLT_MAX;
           int amb = 0;
           if (act) {
-            const float* src = rcv + oa * BLK + hl * NTAU;
-            const int sstride = NOWN * BLK;
-            float M[NTAU], M1[NTAU], M2[NTAU], M3[NTAU];
+            float M[NTAU];
 #pragma unroll
-            for (int t = 0; t < NTAU; ++t) M[t] = M1[t] = M2[t] = M3[t] = src[t];
-            int b = 1;
-            for (; b + 3 < (int)G; b += 4) {  // four independent load streams
-#pragma unroll
-              for (int t = 0; t < NTAU; ++t) {
-                M[t] = fminf(M[t], src[b * sstride + t]);
-                M1[t] = fminf(M1[t], src[(b + 1) * sstride + t]);
-                M2[t] = fminf(M2[t], src[(b + 2) * sstride + t]);
-                M3[t] = fminf(M3[t], src[(b + 3) * sstride + t]);
-              }
-            }
-            for (; b < (int)G; ++b)
-#pragma unroll
-              for (int t = 0; t < NTAU; ++t) M[t] = fminf(M[t], src[b * sstride + t]);
-#pragma unroll
-            for (int t = 0; t < NTAU; ++t) M[t] = fminf(fminf(M[t], M1[t]), fminf(M2[t], M3[t]));
+            for (int t = 0; t < NTAU; ++t) M[t] = s_M[(oa * W + hl) * NTAU + t];
             if (xmode == 1) {  // this GPU's minima -> export buffer; the decision waits for import
 #pragma unroll
               for (int t = 0; t < NTAU; ++t) args.xbuf[st * NTAU + t] = __float_as_uint(M[t]);
@@ -993,8 +1007,9 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
 
       // ---- a7/a8: every warp decides redundantly (identical inputs -> identical decisions),
       //      so no barrier is needed before the next step
-      double v1 = -INFINITY, v2 = -INFINITY;
-      int a1 = INT_MAX, a2 = INT_MAX;
+      double v1 = -INFINITY;
+      int a1 = INT_MAX;
+      bool near = false;
       if (!fin) {
         // a7: top-2 over V* (Alg 9; ties -> lowest index, R13).  Lane l holds its best
         // and second-best among a = l, l+32, ...; REDUX max over order-preserving keys.
@@ -1011,15 +1026,13 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         const int w1 = argmax_key(0xffffffffu, li1 != INT_MAX, dkey(lb1), (unsigned)li1);
         a1 = __shfl_sync(0xffffffffu, li1, w1);
         v1 = __shfl_sync(0xffffffffu, lb1, w1);
-        // runner-up: every lane's best excluding a1
+        // near-tie (R-north-star: top-2 gap < 1e-4 S): v1 - v2 < thr with v2 the runner-up
+        // <=> some lane's best action other than a1 is within thr -- one vote, no second argmax
         const bool own = lane == w1;
         const double cv = own ? lb2 : lb1;
         const int ci = own ? li2 : li1;
-        const int w2 = argmax_key(0xffffffffu, ci != INT_MAX, dkey(cv), (unsigned)ci);
-        if (w2 >= 0) {
-          a2 = __shfl_sync(0xffffffffu, ci, w2);
-          v2 = __shfl_sync(0xffffffffu, cv, w2);
-        }
+        const double thr = w.near_tie_rel * s_vsc[a1];
+        near = __any_sync(0xffffffffu, ci != INT_MAX && v1 - cv < thr);
       }
       FMDP_MARK(PH_ARGMAX)
       const uint32_t c0 = s_stay[p];
@@ -1047,7 +1060,6 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           fail_step = st == 0 ? -1 : k;
           done = true;
         } else {
-          const bool near = (A > 1) && (v1 - v2 < w.near_tie_rel * s_vsc[a1]);
           const int4 p1 = s_pos[a1 * W + 0];  // s_{t+1} <- Delta_1[a*] (Alg 1)
           if (rank == 0 && tid == 0) {
             args.astar[sbase + k] = a1;
@@ -1063,7 +1075,9 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           psi = p1.w;
           fl = s_flags[a1];
           fin = fl != 0 || k >= w.max_steps;
-          if (k - rq.start_k >= args.budget) {  // step budget spent: pause at state k
+          // slice budget spent: pause at state k (the head never pauses; with a stop flag the
+          // others keep going until the head has finished -- free work in a single-wave slice)
+          if (!rq.head && k - rq.start_k >= args.budget && (!args.stop || ctl->stop[p])) {
             status = -1;
             done = true;
           }
@@ -1099,6 +1113,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
 
     // ------------------------------------------------------------ request epilogue
     cluster.sync();  // n_exact contributions of every CTA have landed in rank 0
+    if (rank == 0 && tid == 0 && rq.head && args.stop && status >= 0) atomicExch(args.stop, 1);
     if (rank == 0 && tid == 0 && !args.eval) {
       Out o;
       o.status = status;
