@@ -133,15 +133,15 @@ struct Layout {
     o_sfix = o; o = al(o + sizeof(double) * AW);
     o_vT = o;   o = al(o + sizeof(float) * AW);
     o_mI = o;   o = al(o + sizeof(float) * AW);
-    o_vstar = o; o = al(o + sizeof(double) * A);
-    o_vsc = o;  o = al(o + sizeof(double) * A);
+    o_vstar = o; o = al(o + sizeof(double) * 2 * A);  // {V*(a), S(a)} pairs (one 16 B DSMEM push)
+    o_vsc = o;
     o_conf = o; o = al(o + sizeof(uint32_t) * (A + 1));
     o_confg = o; o = al(o + sizeof(uint32_t) * (A + 1));
     o_flags = o; o = al(o + sizeof(int32_t) * A);
-    o_stay = o; o = al(o + sizeof(uint32_t) * 2);
+    o_stay = o; o = al(o + sizeof(uint32_t) * 2 * 16);  // [parity][source rank] slice minima
     o_amb = o;  o = al(o + sizeof(int32_t) * AMB_MAX);
     o_tc = o;   o = al(o + sizeof(int32_t) * 2 * TC_MAX);  // candidate lists, by step parity
-    o_bar = o;  o = al(o + sizeof(uint64_t) * 4);
+    o_bar = o;  o = al(o + sizeof(uint64_t) * 8);   // 3 TMA ring + 2 reduce-scatter + 2 V* mbarriers
     o_ctl = o;  o = al(o + 512);
     total = o;
   }

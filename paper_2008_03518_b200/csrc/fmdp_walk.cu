@@ -60,6 +60,27 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// DSMEM push (sm_90+): st.async into a cluster CTA's shared memory, completing bytes on that
+// CTA's mbarrier -- replaces a cluster barrier (and its MEMBAR.GPU + L1 flush) per exchange.
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, unsigned rank) {
+  uint32_t d;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(rank));
+  return d;
+}
+__device__ __forceinline__ void st_async_f4(uint32_t ra, float4 v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(ra),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_u32(uint32_t ra, uint32_t v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];" ::"r"(ra), "r"(v), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_d2(uint32_t ra, double a, double b, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(ra), "d"(a),
+               "d"(b), "r"(rbar)
+               : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
@@ -357,8 +378,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   double* s_sfix = reinterpret_cast<double*>(smem + L.o_sfix);
   float* s_vT = reinterpret_cast<float*>(smem + L.o_vT);
   float* s_mI = reinterpret_cast<float*>(smem + L.o_mI);
-  double* s_vstar = reinterpret_cast<double*>(smem + L.o_vstar);
-  double* s_vsc = reinterpret_cast<double*>(smem + L.o_vsc);
+  double2* s_vv = reinterpret_cast<double2*>(smem + L.o_vstar);  // {V*(a), S(a)}
   uint32_t* s_conf = reinterpret_cast<uint32_t*>(smem + L.o_conf);
   int32_t* s_flags = reinterpret_cast<int32_t*>(smem + L.o_flags);
   uint32_t* s_stay = reinterpret_cast<uint32_t*>(smem + L.o_stay);
@@ -391,11 +411,12 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   if (w.n_tw <= TW_SMEM)
     for (int i = tid; i < w.n_tw; i += NT) s_tw[i] = w.tw[i];
   if (tid == 0) {
-    for (int b = 0; b < 3; ++b) mbar_init(&s_bar[b], 1);
+    for (int b = 0; b < 7; ++b) mbar_init(&s_bar[b], 1);  // 0-2 TMA ring, 3-4 reduce-scatter, 5-6 V*
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   uint32_t par = 0;      // next wait parity per ring buffer (bit b)
+  uint32_t parX = 0;     // next wait parity of the exchange mbarriers: bits 0-1 reduce-scatter, 2-3 V*
   uint32_t pending = 0;  // ring buffers issued and not yet waited
   int cnt2 = 0;          // (tid 0) active count of row K+2, loaded one step ahead
 
@@ -458,8 +479,6 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       cnt2 = row_count(w, K0 + 2);
       issue_row(w, K0, n0, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, args.shard_rank, args.shard_world);
       issue_row(w, K0 + 1, n1, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, args.shard_rank, args.shard_world);
-      s_stay[0] = w.sat_d2;
-      s_stay[1] = w.sat_d2;
     }
     {
       const int64_t K0 = rq.t0 + k;
@@ -495,9 +514,16 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           cnt2 = row_count(w, K + 3);  // consumed next step: latency hidden by this step
         }
         ctl->nsurv[((k + 1) & 1) * 2] = 0;  // step k+1, chunk 0 (last used in step k-1)
-        if (args.stop && rank == 0) {  // one reading for the whole cluster, visible after BAR1
-          const int f = *(volatile int32_t*)args.stop;
-          for (unsigned b = 0; b < G; ++b) cluster.map_shared_rank(&ctl->stop[p], b)[0] = f;
+        // this step's exchange phases: slice minima (4 B from every CTA), reduce-scatter
+        // blocks of the owned actions (from every CTA), the stop flag (from rank 0), V*(a)
+        const uint32_t bytesA = (xmode != 2 ? 4u * G : 0u) +
+                                ((!fin && xmode != 2) ? (uint32_t)(4 * G * n_own * BLK) : 0u) + (args.stop ? 4u : 0u);
+        mbar_arrive_tx(&s_bar[3 + p], bytesA);
+        if (!fin) mbar_arrive_tx(&s_bar[5 + p], (uint32_t)(16 * A));
+        if (args.stop && rank == 0) {  // one reading for the whole cluster
+          const uint32_t f = (uint32_t)*(volatile int32_t*)args.stop;
+          const uint32_t la = smem_u32(&ctl->stop[p]), lb = smem_u32(&s_bar[3 + p]);
+          for (unsigned b = 0; b < G; ++b) st_async_u32(mapa_u32(la, b), f, mapa_u32(lb, b));
         }
       }
       if (!args.eval && !fin) pending |= 1u << bK2;
@@ -819,37 +845,43 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       if (tid == 0) {  // step k+1's counters: every warp has left step k-1 (this barrier)
         ctl->namb[p ^ 1] = 0;
         ctl->stay_local[p ^ 1] = w.sat_d2;
-        s_stay[p ^ 1] = w.sat_d2;  // written remotely in step k+1, after the cluster barriers of k
       }
-      // slice separation minimum -> every CTA; reduce-scatter of the per-action blocks
-      if (xmode == 2) {
-        if (tid == 0) s_stay[p] = args.xbuf[NTAU * AW];  // all-reduced over the GPUs
-      } else if (tid < (int)G && ctl->stay_local[p] < w.sat_d2) {
-        atomicMin(cluster.map_shared_rank(&s_stay[p], tid), ctl->stay_local[p]);
-      }
+      // slice separation minimum -> every CTA; reduce-scatter of the per-action blocks into the
+      // owner CTA (a mod G): DSMEM pushes completing on the receiver's mbarrier of this parity
+      const uint32_t barA = smem_u32(&s_bar[3 + p]);
+      if (xmode != 2 && tid < (int)G)
+        st_async_u32(mapa_u32(smem_u32(&s_stay[p * 16 + rank]), tid), ctl->stay_local[p], mapa_u32(barA, tid));
       if (!fin && xmode != 2) {
         const int par_off = p * (int)G * NOWN * BLK;
         const int nv = BLK / 4;
         for (int i = tid; i < A * nv; i += NT) {
           const int a = i / nv, e = i % nv;
-          float4* dst = reinterpret_cast<float4*>(cluster.map_shared_rank(s_recv, a % (int)G) + par_off +
-                                                  ((int)rank * NOWN + a / (int)G) * BLK);
-          dst[e] = reinterpret_cast<const float4*>(s_stage + a * BLK)[e];
+          const unsigned own = (unsigned)(a % (int)G);
+          const uint32_t la = smem_u32(s_recv + par_off + ((int)rank * NOWN + a / (int)G) * BLK + 4 * e);
+          st_async_f4(mapa_u32(la, own), reinterpret_cast<const float4*>(s_stage + a * BLK)[e], mapa_u32(barA, own));
         }
         FMDP_MARK(PH_SCATTER)
       }
-      cluster.sync();
+      mbar_wait(&s_bar[3 + p], (parX >> p) & 1u);
+      parX ^= 1u << p;
       FMDP_MARK(PH_BAR1)
-      // co-simulation barrier failure, as every CTA of the cluster saw it at this step
-      if (xmode == 1 && rank == 0 && tid == 0) args.xbuf[NTAU * AW] = s_stay[p];
+      // exact nearest-plan d^2 of state k over the whole row (Sec IV.I): min of the slice minima
+      uint32_t stay_all = w.sat_d2;
+      if (xmode == 2) {
+        stay_all = args.xbuf[NTAU * AW];  // all-reduced over the GPUs
+      } else {
+        for (int b = 0; b < (int)G; ++b) stay_all = min(stay_all, s_stay[p * 16 + b]);
+      }
+      if (xmode == 1 && rank == 0 && tid == 0) args.xbuf[NTAU * AW] = stay_all;
 
       if (!fin) {
         // ---- owner epilogue (half-warp per owned action, lane = substep): G-way minimum of
         //      the partial blocks, exact in/out, values (Alg 8), V*(a)
         const float* rcv = s_recv + p * (int)G * NOWN * BLK;
         // G-way minimum of the partial blocks spread over the whole CTA, one (action, substep,
-        // tau) per thread, into s_stage (free: this CTA's scatter completed before BAR1)
+        // tau) per thread, into s_stage (free once every thread has pushed its blocks)
         float* s_M = s_stage;
+        __syncthreads();  // every thread of this CTA has pushed its s_stage blocks
         {
           const int sstride = NOWN * BLK;
           for (int i = tid; i < n_own * W * NTAU; i += NT) {
@@ -989,10 +1021,9 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
               bt = ot;
             }
           }
-          if (oa < n_own && hl < (int)G) {  // broadcast V*(a) and S(a) to CTA hl
+          if (oa < n_own && hl < (int)G) {  // push {V*(a), S(a)} to CTA hl
             const double vstar = w.vmax_init_zero ? fmax(0.0, bv) : bv;
-            cluster.map_shared_rank(s_vstar, hl)[a] = vstar;
-            cluster.map_shared_rank(s_vsc, hl)[a] = bs;
+            st_async_d2(mapa_u32(smem_u32(&s_vv[a]), hl), vstar, bs, mapa_u32(smem_u32(&s_bar[5 + p]), hl));
             if (args.eval && hl == 0) args.dbg_vstar[a] = vstar;
           }
         }
@@ -1001,7 +1032,8 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           ctl->n_exact = 0;
         }
         FMDP_MARK(PH_OWNER)
-        cluster.sync();
+        mbar_wait(&s_bar[5 + p], (parX >> (2 + p)) & 1u);
+        parX ^= 1u << (2 + p);
         FMDP_MARK(PH_BAR2)
       }
 
@@ -1016,7 +1048,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         double lb1 = -INFINITY, lb2 = -INFINITY;
         int li1 = INT_MAX, li2 = INT_MAX;
         for (int a = lane; a < A; a += 32) {
-          const double v = s_vstar[a];
+          const double v = s_vv[a].x;
           if (better(v, a, lb1, li1)) {
             lb2 = lb1; li2 = li1; lb1 = v; li1 = a;
           } else if (better(v, a, lb2, li2)) {
@@ -1031,11 +1063,11 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         const bool own = lane == w1;
         const double cv = own ? lb2 : lb1;
         const int ci = own ? li2 : li1;
-        const double thr = w.near_tie_rel * s_vsc[a1];
+        const double thr = w.near_tie_rel * s_vv[a1].y;
         near = __any_sync(0xffffffffu, ci != INT_MAX && v1 - cv < thr);
       }
       FMDP_MARK(PH_ARGMAX)
-      const uint32_t c0 = s_stay[p];
+      const uint32_t c0 = stay_all;
       bool done = false;
       if (xmode == 1) {  // export step: no decision in this launch
         status = -1;
