@@ -529,7 +529,7 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
     // and rolls back any pending request whose computed steps could see a newly committed
     // plan to its first influenced step.  Result: identical to the sequential loop.
     // slice budget: measured optimum on configs[1] (tools/sweep_budget.py)
-    const int budget = ctx->launch.step_budget > 0 ? ctx->launch.step_budget : (ctx->launch.cull ? 512 : 128);
+    const int budget = ctx->launch.step_budget > 0 ? ctx->launch.step_budget : 128;
     std::vector<char> fin(n, 0);
     std::vector<int> kdone(n, 0);
     int rollbacks = 0;
