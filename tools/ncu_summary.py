@@ -61,14 +61,14 @@ traffic = None
 for rep, title in (('walk_batch', 'configs[1] batch slice, 100 walkers x G=1 (full path)'),
                    ('walk_cull2', 'configs[1] request, f1 culling, G=2')):
     m = raw(f'gpurun_out/{rep}.ncu-rep')
-    lines += [f"## walk_kernel<3> — {title}\n", "| metric | value |", "|---|---|"]
+    lines += [f"## walk_kernel<3, false> — {title}\n", "| metric | value |", "|---|---|"]
     for k in WANT:
         if k in m:
             lines.append(f"| `{k}` | {m[k][0]} {m[k][1]} |")
     if rep == 'walk_batch':
         rd = float(m['dram__bytes_read.sum'][0].replace(',', '')) * (1e6 if m['dram__bytes_read.sum'][1] == 'Mbyte' else 1e3 if m['dram__bytes_read.sum'][1] == 'Kbyte' else 1e9 if m['dram__bytes_read.sum'][1] == 'Gbyte' else 1)
         wr = float(m['dram__bytes_write.sum'][0].replace(',', '')) * (1e6 if m['dram__bytes_write.sum'][1] == 'Mbyte' else 1e3 if m['dram__bytes_write.sum'][1] == 'Kbyte' else 1e9 if m['dram__bytes_write.sum'][1] == 'Gbyte' else 1)
-        traffic = dict(kernel="walk_kernel<3>", capture=f"{rnd} walk_batch (tools/ncu_batch.py, first launch)",
+        traffic = dict(kernel="walk_kernel<3, false>", capture=f"{rnd} walk_batch (tools/ncu_batch.py, first launch)",
                        dram_bytes_read=int(rd), dram_bytes_write=int(wr), per_launch_bytes=int(rd + wr),
                        note="DRAM traffic per launch; the kernel is FP32-pipe bound, plan rows are L2-resident")
     h, d = source(f'gpurun_out/{rep}.ncu-rep')
