@@ -388,6 +388,17 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   Ctl* ctl = reinterpret_cast<Ctl*>(smem + L.o_ctl);
   const int RAWW = L.RAWW, BLK = L.BLK, NOWN = L.NOWN;
   const int4* tw = (w.n_tw <= TW_SMEM) ? s_tw : w.tw;
+  // reduce-scatter element of this thread (i = tid): action, float4 index, owner, offsets --
+  // fixed for the launch, so no integer divisions on the step's critical path
+  const int SC_NV = BLK / 4;
+  int sc_src = 0, sc_dst = 0;
+  unsigned sc_own = 0;
+  if (tid < A * SC_NV) {
+    const int a = tid / SC_NV, e = tid % SC_NV;
+    sc_own = (unsigned)(a % (int)G);
+    sc_src = a * BLK + 4 * e;
+    sc_dst = ((int)rank * NOWN + a / (int)G) * BLK + 4 * e;
+  }
   // plan-sharded multi-GPU step: xmode 1 exports this GPU's per-(state, tau)
   // minima and nearest-plan distance, xmode 2 imports their all-reduced minimum and decides
   const int xmode = args.xmode;
@@ -418,7 +429,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   uint32_t par = 0;      // next wait parity per ring buffer (bit b)
   uint32_t parX = 0;     // next wait parity of the exchange mbarriers: bits 0-1 reduce-scatter, 2-3 V*
   uint32_t pending = 0;  // ring buffers issued and not yet waited
-  int cnt2 = 0;          // (tid 0) active count of row K+2, loaded one step ahead
+  int cnt2 = 0;          // (I/O thread NT-1) active count of row K+2, loaded one step ahead
 
   for (;;) {
     // ------------------------------------------------------------ next request
@@ -476,13 +487,13 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       }
       const int64_t K0 = rq.t0 + k;
       const int n0 = row_count(w, K0), n1 = row_count(w, K0 + 1);
-      cnt2 = row_count(w, K0 + 2);
       issue_row(w, K0, n0, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, args.shard_rank, args.shard_world);
       issue_row(w, K0 + 1, n1, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, args.shard_rank, args.shard_world);
     }
     {
       const int64_t K0 = rq.t0 + k;
       pending |= (1u << (K0 % 3)) | (1u << ((K0 + 1) % 3));
+      if (tid == NT - 1) cnt2 = row_count(w, K0 + 2);  // the I/O thread's row count, one step ahead
     }
     __syncthreads();
     // terrain candidates for the first step (exact cull: wells that can reach a projected state)
@@ -508,25 +519,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       int4* s_pos = s_pos2 + p * AW;
       // fan origin of this step's projected states (hot-loop formulation)
       const int ox = (W >> 1) * s_dxy[psi].x, oy = (W >> 1) * s_dxy[psi].y;
-      if (tid == 0) {
-        if (!args.eval && !fin) {
-          issue_row(w, K + 2, cnt2, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, args.shard_rank, args.shard_world);
-          cnt2 = row_count(w, K + 3);  // consumed next step: latency hidden by this step
-        }
-        ctl->nsurv[((k + 1) & 1) * 2] = 0;  // step k+1, chunk 0 (last used in step k-1)
-        // this step's exchange phases: slice minima (4 B from every CTA), reduce-scatter
-        // blocks of the owned actions (from every CTA), the stop flag (from rank 0), V*(a)
-        const uint32_t bytesA = (xmode != 2 ? 4u * G : 0u) +
-                                ((!fin && xmode != 2) ? (uint32_t)(4 * G * n_own * BLK) : 0u) + (args.stop ? 4u : 0u);
-        mbar_arrive_tx(&s_bar[3 + p], bytesA);
-        if (!fin) mbar_arrive_tx(&s_bar[5 + p], (uint32_t)(16 * A));
-        if (args.stop && rank == 0) {  // one reading for the whole cluster
-          const uint32_t f = (uint32_t)*(volatile int32_t*)args.stop;
-          const uint32_t la = smem_u32(&ctl->stop[p]), lb = smem_u32(&s_bar[3 + p]);
-          for (unsigned b = 0; b < G; ++b) st_async_u32(mapa_u32(la, b), f, mapa_u32(lb, b));
-        }
-      }
-      if (!args.eval && !fin) pending |= 1u << bK2;
+      if (!args.eval && !fin) pending |= 1u << bK2;  // row K+2: issued below by the I/O thread
       FMDP_MARK(PH_TOP)
 
       float sx = 0.f, sy = 0.f, sz[C];
@@ -618,6 +611,28 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           s_sfix[st] = vpos + valt;
         }
         FMDP_MARK(PH_FIX)
+      }
+
+      // ---- per-step I/O, on the CTA's last thread after the projection barrier (thread 0 owns
+      //      projection columns; this one has no build work in the latency-bound configurations):
+      //      prefetch of row K+2 (its ring buffer last held row K-1, consumed in step k-1),
+      //      this step's exchange phases -- slice minima (4 B from every CTA), reduce-scatter
+      //      blocks of the owned actions (from every CTA), the stop flag (from rank 0), V*(a)
+      if (tid == NT - 1) {
+        if (!args.eval && !fin) {
+          issue_row(w, K + 2, cnt2, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, args.shard_rank, args.shard_world);
+          cnt2 = row_count(w, K + 3);  // consumed next step: latency hidden by this step
+        }
+        ctl->nsurv[((k + 1) & 1) * 2] = 0;  // step k+1, chunk 0 (last used in step k-1)
+        const uint32_t bytesA = (xmode != 2 ? 4u * G : 0u) +
+                                ((!fin && xmode != 2) ? (uint32_t)(4 * G * n_own * BLK) : 0u) + (args.stop ? 4u : 0u);
+        mbar_arrive_tx(&s_bar[3 + p], bytesA);
+        if (!fin) mbar_arrive_tx(&s_bar[5 + p], (uint32_t)(16 * A));
+        if (args.stop && rank == 0) {  // one reading for the whole cluster
+          const uint32_t f = (uint32_t)*(volatile int32_t*)args.stop;
+          const uint32_t la = smem_u32(&ctl->stop[p]), lb = smem_u32(&s_bar[3 + p]);
+          for (unsigned b = 0; b < G; ++b) st_async_u32(mapa_u32(la, b), f, mapa_u32(lb, b));
+        }
       }
 
       // ---- a1 + a4: stage row K, wells, hot loop; exact nearest-plan distance of q ("stay")
@@ -866,13 +881,18 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       if (xmode != 2 && tid < (int)G)
         st_async_u32(mapa_u32(smem_u32(&s_stay[p * 16 + rank]), tid), ctl->stay_local[p], mapa_u32(barA, tid));
       if (!fin && xmode != 2) {
-        const int par_off = p * (int)G * NOWN * BLK;
-        const int nv = BLK / 4;
-        for (int i = tid; i < A * nv; i += NT) {
-          const int a = i / nv, e = i % nv;
-          const unsigned own = (unsigned)(a % (int)G);
-          const uint32_t la = smem_u32(s_recv + par_off + ((int)rank * NOWN + a / (int)G) * BLK + 4 * e);
-          st_async_f4(mapa_u32(la, own), reinterpret_cast<const float4*>(s_stage + a * BLK)[e], mapa_u32(barA, own));
+        const uint32_t recv_p = smem_u32(s_recv) + 4u * (uint32_t)(p * (int)G * NOWN * BLK);
+        for (int i = tid, j = 0; i < A * SC_NV; i += NT, ++j) {
+          int src = sc_src, dst = sc_dst;
+          unsigned own = sc_own;
+          if (j) {  // only when A * BLK / 4 > threads (A = 85)
+            const int a = i / SC_NV, e = i % SC_NV;
+            own = (unsigned)(a % (int)G);
+            src = a * BLK + 4 * e;
+            dst = ((int)rank * NOWN + a / (int)G) * BLK + 4 * e;
+          }
+          st_async_f4(mapa_u32(recv_p + 4u * dst, own), *reinterpret_cast<const float4*>(s_stage + src),
+                      mapa_u32(barA, own));
         }
         FMDP_MARK(PH_SCATTER)
       }
