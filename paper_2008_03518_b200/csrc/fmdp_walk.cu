@@ -377,7 +377,6 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   double* s_fix = reinterpret_cast<double*>(smem + L.o_fix);
   double* s_sfix = reinterpret_cast<double*>(smem + L.o_sfix);
   float* s_vT = reinterpret_cast<float*>(smem + L.o_vT);
-  float* s_mI = reinterpret_cast<float*>(smem + L.o_mI);
   double2* s_vv = reinterpret_cast<double2*>(smem + L.o_vstar);  // {V*(a), S(a)}
   uint32_t* s_conf = reinterpret_cast<uint32_t*>(smem + L.o_conf);
   int32_t* s_flags = reinterpret_cast<int32_t*>(smem + L.o_flags);
@@ -912,28 +911,91 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         // ---- owner epilogue (half-warp per owned action, lane = substep): G-way minimum of
         //      the partial blocks, exact in/out, values (Alg 8), V*(a)
         const float* rcv = s_recv + p * (int)G * NOWN * BLK;
-        // G-way minimum of the partial blocks spread over the whole CTA, one (action, substep,
-        // tau) per thread, into s_stage (free once every thread has pushed its blocks)
+        // Pass 1 (whole CTA, one owned (action, substep, tau) per thread): G-way minimum of the
+        // partial blocks (multi-GPU: export / import), |s - o|^2 added back, radius test ->
+        // s_M = the in-radius d^2, FLT_MAX (outside), or -1 (inside the FP32 band: exact below).
+        // s_M lives in s_stage, free once every thread of this CTA has pushed its blocks.
         float* s_M = s_stage;
-        __syncthreads();  // every thread of this CTA has pushed its s_stage blocks
-        {
-          const int sstride = NOWN * BLK;
-          for (int i = tid; i < n_own * W * NTAU; i += NT) {
-            const int oa = i / (W * NTAU), r2 = i - oa * (W * NTAU);
+        __syncthreads();
+        const int nitem = n_own * W * NTAU;
+        for (int i = tid; i < nitem; i += NT) {
+          const int oa = i / (W * NTAU), r2 = i - oa * (W * NTAU);
+          const int l = r2 / NTAU, t = r2 - l * NTAU;
+          const int st = ((int)rank + oa * (int)G) * W + l;
+          float M;
+          if (xmode == 2) {
+            M = __uint_as_float(args.xbuf[st * NTAU + t]);
+          } else {
+            const int sstride = NOWN * BLK;
             const float* src = rcv + oa * BLK + r2;
             float M0 = src[0], M1 = FLT_MAX, M2 = FLT_MAX, M3 = FLT_MAX;
-            int b = 1;
-            for (; b + 3 < (int)G; b += 4) {  // four independent load streams
-              M0 = fminf(M0, src[b * sstride]);
-              M1 = fminf(M1, src[(b + 1) * sstride]);
-              M2 = fminf(M2, src[(b + 2) * sstride]);
-              M3 = fminf(M3, src[(b + 3) * sstride]);
+            int bb = 1;
+            for (; bb + 3 < (int)G; bb += 4) {  // four independent load streams
+              M0 = fminf(M0, src[bb * sstride]);
+              M1 = fminf(M1, src[(bb + 1) * sstride]);
+              M2 = fminf(M2, src[(bb + 2) * sstride]);
+              M3 = fminf(M3, src[(bb + 3) * sstride]);
             }
-            for (; b < (int)G; ++b) M0 = fminf(M0, src[b * sstride]);
-            s_M[i] = fminf(fminf(M0, M1), fminf(M2, M3));
+            for (; bb < (int)G; ++bb) M0 = fminf(M0, src[bb * sstride]);
+            M = fminf(fminf(M0, M1), fminf(M2, M3));
+            if (xmode == 1) args.xbuf[st * NTAU + t] = __float_as_uint(M);  // this GPU's minima
           }
-          __syncthreads();
+          const int4 q4 = s_pos[st];
+          const int dx = q4.x - qx - ox, dy = q4.y - qy - oy, dz = q4.z - qz;
+          M += (float)(dx * dx + dy * dy + dz * dz);  // exact integer < 2^24; one rounding
+          float out = FLT_MAX;
+          if (M < w.R2lo[t]) {
+            out = M;
+          } else if (M <= w.R2hi[t]) {
+            out = -1.f;
+            const int idx = atomicAdd(&ctl->namb[p], 1);
+            if (idx < AMB_MAX) s_amb[idx] = i;
+          }
+          s_M[i] = out;
         }
+        __syncthreads();
+        FMDP_MARK(PH_OWN1)
+        const int namb = ctl->namb[p];  // uniform after the barrier
+        if (namb) {
+          // Exact fallback: min over the WHOLE row K of the int64 d^2 for each flagged (state,
+          // tau); each CTA resolves its own states (rare)
+          const int nK = row_count(w, K);
+          const int32_t* rowg = w.rows + (size_t)K * 4 * w.row_cap;
+          const int nit = namb <= AMB_MAX ? namb : nitem;  // overflow: walk every owned item
+          for (int it2 = 0; it2 < nit; ++it2) {
+            const int i = namb <= AMB_MAX ? s_amb[it2] : it2;
+            if (s_M[i] != -1.f) continue;
+            const int oa = i / (W * NTAU), r2 = i - oa * (W * NTAU);
+            const int l = r2 / NTAU, t = r2 - l * NTAU;
+            const int sti = ((int)rank + oa * (int)G) * W + l;
+            if (tid == 0) ctl->xmin = ULLONG_MAX;
+            __syncthreads();
+            const int4 q4 = s_pos[sti];
+            unsigned long long best = ULLONG_MAX;
+            for (int j = tid; j < nK; j += NT) {
+              const uint32_t pv = (uint32_t)rowg[3 * w.row_cap + j];
+              const int64_t cx = rowg[j] + (int64_t)w.k_tau[t] * sext(pv, 11);
+              const int64_t cy = rowg[w.row_cap + j] + (int64_t)w.k_tau[t] * sext(pv >> 11, 11);
+              const int64_t cz = rowg[2 * w.row_cap + j] + (int64_t)w.k_tau[t] * sext(pv >> 22, 10);
+              const int64_t ddx = q4.x - cx, ddy = q4.y - cy, ddz = q4.z - cz;
+              best = min(best, (unsigned long long)(ddx * ddx + ddy * ddy + ddz * ddz));
+            }
+            if (cosim)  // batch peers of clock K
+              best = min(best, cs_exact_peers(args.cs_pub + (size_t)(K & 1) * args.cs_n * 2, args.cs_n, r, q4,
+                                              w.k_tau[t]));
+            for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+            if (lane == 0 && best != ULLONG_MAX) atomicMin(&ctl->xmin, best);
+            __syncthreads();
+            if (tid == 0) {
+              const unsigned long long x = ctl->xmin;
+              s_M[i] = ((int64_t)x < w.R2_tau[t]) ? (float)x : FLT_MAX;
+              atomicAdd(&ctl->n_exact, 1);
+            }
+            __syncthreads();
+          }
+          if (tid == 0) ctl->namb[p] = 0;
+        }
+        // Pass 2 (half-warp per owned action, lane = substep): values (Alg 8), V*(a)
         const int hw = tid >> 4, hl = tid & 15;
         const int n_hw = NT >> 4;
         for (int oa0 = 0; oa0 < NOWN; oa0 += n_hw) {  // uniform trip count across the CTA
@@ -942,92 +1004,9 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           const int a = (int)rank + oa * (int)G;
           const int st = a * W + hl;
           float mi = FLT_MAX;
-          int amb = 0;
           if (act) {
-            float M[NTAU];
 #pragma unroll
-            for (int t = 0; t < NTAU; ++t) M[t] = s_M[(oa * W + hl) * NTAU + t];
-            if (xmode == 1) {  // this GPU's minima -> export buffer; the decision waits for import
-#pragma unroll
-              for (int t = 0; t < NTAU; ++t) args.xbuf[st * NTAU + t] = __float_as_uint(M[t]);
-            } else if (xmode == 2) {
-#pragma unroll
-              for (int t = 0; t < NTAU; ++t) M[t] = __uint_as_float(args.xbuf[st * NTAU + t]);
-            }
-            {  // |s - o|^2 back in (exact integer < 2^24; one rounding)
-              const int4 q4 = s_pos[st];
-              const int dx = q4.x - qx - ox, dy = q4.y - qy - oy, dz = q4.z - qz;
-              const float s2 = (float)(dx * dx + dy * dy + dz * dz);
-#pragma unroll
-              for (int t = 0; t < NTAU; ++t) M[t] += s2;
-            }
-#pragma unroll
-            for (int t = 0; t < NTAU; ++t) {
-              if (M[t] < w.R2lo[t]) {
-                mi = fminf(mi, M[t]);
-              } else if (M[t] <= w.R2hi[t]) {  // inside the 2^-20 band: decided exactly below
-                amb = 1;
-                const int idx = atomicAdd(&ctl->namb[p], 1);
-                if (idx < AMB_MAX) s_amb[idx] = st * NTAU + t;
-              }
-            }
-            s_mI[st] = mi;
-          }
-          FMDP_MARK(PH_OWN1)
-          if (__syncthreads_or(amb)) {
-            // Exact fallback: min over the WHOLE row K of the int64 d^2 for each flagged
-            // (state, tau); each CTA resolves its own states (rare).
-            const int namb = ctl->namb[p];
-            const int nK = row_count(w, K);
-            const int32_t* rowg = w.rows + (size_t)K * 4 * w.row_cap;
-            const int nitems = namb <= AMB_MAX ? namb : n_hw * W * NTAU;
-            for (int it2 = 0; it2 < nitems; ++it2) {
-              int item;
-              if (namb <= AMB_MAX) {
-                item = s_amb[it2];
-              } else {  // overflow: walk every owned (state, tau) of this pass, re-test the band
-                const int oa2 = oa0 + it2 / (W * NTAU), rem = it2 % (W * NTAU), l2 = rem / NTAU, t = rem % NTAU;
-                if (oa2 >= n_own) continue;
-                float M = FLT_MAX;
-                for (int b = 0; b < (int)G; ++b) M = fminf(M, rcv[(b * NOWN + oa2) * BLK + l2 * NTAU + t]);
-                if (xmode == 2) M = __uint_as_float(args.xbuf[((((int)rank + oa2 * (int)G) * W + l2) * NTAU + t)]);
-                {
-                  const int4 q4 = s_pos[((int)rank + oa2 * (int)G) * W + l2];
-                  const int dx = q4.x - qx - ox, dy = q4.y - qy - oy, dz = q4.z - qz;
-                  M += (float)(dx * dx + dy * dy + dz * dz);
-                }
-                if (!(M >= w.R2lo[t] && M <= w.R2hi[t])) continue;
-                item = (((int)rank + oa2 * (int)G) * W + l2) * NTAU + t;
-              }
-              const int sti = item / NTAU, t = item % NTAU;
-              if (tid == 0) ctl->xmin = ULLONG_MAX;
-              __syncthreads();
-              const int4 q4 = s_pos[sti];
-              unsigned long long best = ULLONG_MAX;
-              for (int j = tid; j < nK; j += NT) {
-                const uint32_t pv = (uint32_t)rowg[3 * w.row_cap + j];
-                const int64_t cx = rowg[j] + (int64_t)w.k_tau[t] * sext(pv, 11);
-                const int64_t cy = rowg[w.row_cap + j] + (int64_t)w.k_tau[t] * sext(pv >> 11, 11);
-                const int64_t cz = rowg[2 * w.row_cap + j] + (int64_t)w.k_tau[t] * sext(pv >> 22, 10);
-                const int64_t dx = q4.x - cx, dy = q4.y - cy, dz = q4.z - cz;
-                best = min(best, (unsigned long long)(dx * dx + dy * dy + dz * dz));
-              }
-              if (cosim)  // batch peers of clock K
-                best = min(best, cs_exact_peers(args.cs_pub + (size_t)(K & 1) * args.cs_n * 2, args.cs_n, r, q4,
-                                                w.k_tau[t]));
-              for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
-              if (lane == 0 && best != ULLONG_MAX) atomicMin(&ctl->xmin, best);
-              __syncthreads();
-              if (tid == 0) {
-                const unsigned long long x = ctl->xmin;
-                if ((int64_t)x < w.R2_tau[t]) s_mI[sti] = fminf(s_mI[sti], (float)x);
-                atomicAdd(&ctl->n_exact, 1);
-              }
-              __syncthreads();
-            }
-            if (tid == 0) ctl->namb[p] = 0;
-            if (act) mi = s_mI[st];
-            __syncthreads();
+            for (int t = 0; t < NTAU; ++t) mi = fminf(mi, s_M[(oa * W + hl) * NTAU + t]);
           }
           // a6 values
           double v = -INFINITY, sc = 0.0;
