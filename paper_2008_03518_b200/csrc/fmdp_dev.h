@@ -54,6 +54,7 @@ struct World {
   uint64_t cell_magic;          // ceil(2^40 / cell): exact floor division for offsets < 2^25
   const int32_t* height;        // [ny][nx] units
   const int2* dxy;              // heading lattice table [HL]
+  const int2* proj;             // cumulative displacement [HL][n_turn][W]: sum_{s<=t} (DX,DY)[psi + s*turn]
 };
 
 struct Req {

@@ -56,6 +56,7 @@ struct fmdp_ctx {
   int4* d_tw = nullptr;
   int32_t* d_height = nullptr;
   int2* d_dxy = nullptr;
+  int2* d_proj = nullptr;  // cumulative projection offsets [HL][n_turn][W]
 
   // per-request scratch (grown on demand)
   int slots_cap = 0;
@@ -890,6 +891,8 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   ctx->d_rows = (int32_t*)dalloc(ctx, sizeof(int32_t) * row_words * (size_t)w.horizon);
   ctx->d_counts = (int32_t*)dalloc(ctx, sizeof(int32_t) * (size_t)w.horizon);
   ctx->d_dxy = (int2*)dalloc(ctx, sizeof(int2) * w.HL);
+  const size_t nproj = (size_t)w.HL * a.n_turn * a.window;
+  ctx->d_proj = (int2*)dalloc(ctx, sizeof(int2) * nproj);
   ctx->d_queue = (int32_t*)dalloc(ctx, sizeof(int32_t) * 4);
   ctx->d_stop = ctx->d_queue ? ctx->d_queue + 2 : nullptr;
   ctx->d_pairctr = (unsigned long long*)dalloc(ctx, sizeof(unsigned long long));
@@ -900,7 +903,7 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   ctx->d_dbg_conf = (uint32_t*)dalloc(ctx, sizeof(uint32_t) * (A + 1));
   ctx->d_dbg_astar = (int32_t*)dalloc(ctx, sizeof(int32_t) * 4);
   ctx->d_xbuf = (uint32_t*)dalloc(ctx, sizeof(uint32_t) * ((size_t)A * a.window * fmdp::NTAU + 1));
-  if (!ctx->d_rows || !ctx->d_counts || !ctx->d_dxy || !ctx->d_queue || !ctx->d_pairctr || !ctx->d_prof || !ctx->d_dbg_vstar ||
+  if (!ctx->d_rows || !ctx->d_counts || !ctx->d_dxy || !ctx->d_proj || !ctx->d_queue || !ctx->d_pairctr || !ctx->d_prof || !ctx->d_dbg_vstar ||
       !ctx->d_dbg_v || !ctx->d_dbg_s || !ctx->d_dbg_conf || !ctx->d_dbg_astar || !ctx->d_xbuf) {
     fmdp_destroy(ctx);
     return FMDP_E_NOMEM;
@@ -908,6 +911,21 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   cudaMemset(ctx->d_rows, 0, sizeof(int32_t) * row_words * (size_t)w.horizon);
   cudaMemset(ctx->d_counts, 0, sizeof(int32_t) * (size_t)w.horizon);
   cudaMemcpy(ctx->d_dxy, lat.data(), sizeof(int2) * w.HL, cudaMemcpyHostToDevice);
+  {  // Alg 3 projection offsets of every (heading, turn, substep): integer sums of lattice steps
+    std::vector<int2> proj(nproj);
+    for (int psi = 0; psi < w.HL; ++psi)
+      for (int it = 0; it < a.n_turn; ++it) {
+        int x = 0, y = 0, ps = psi;
+        for (int t = 1; t <= a.window; ++t) {
+          ps = ((ps + a.turn_steps[it]) % w.HL + w.HL) % w.HL;
+          x += lat[ps].x;
+          y += lat[ps].y;
+          proj[((size_t)psi * a.n_turn + it) * a.window + (t - 1)] = make_int2(x, y);
+        }
+      }
+    cudaMemcpy(ctx->d_proj, proj.data(), sizeof(int2) * nproj, cudaMemcpyHostToDevice);
+  }
+  w.proj = ctx->d_proj;
   ctx->counts.assign((size_t)w.horizon, 0);
   w.rows = ctx->d_rows;
   w.counts = ctx->d_counts;

@@ -544,25 +544,12 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         FMDP_MARK(PH_SCAN)
         // ---- a2 forward projection (Alg 3): column (turn it, substep t) on the integer lattice
         const int it = col_it, t = col_t, h = col_h;
-        int x = qx, y = qy, ps = psi;
-        {
-          // psi_s = psi + s*h (closed form): the W table loads are independent
-          int ax[MAX_W], ay[MAX_W];
-#pragma unroll
-          for (int s = 1; s <= MAX_W; ++s) {
-            int pss = psi + s * h;
-            pss = pss >= w.HL ? pss - w.HL : (pss < 0 ? pss + w.HL : pss);
-            const int2 d = s <= t ? s_dxy[pss] : make_int2(0, 0);
-            ax[s - 1] = d.x;
-            ay[s - 1] = d.y;
-            if (s == t) ps = pss;
-          }
-#pragma unroll
-          for (int s = 0; s < MAX_W; ++s) {
-            x += ax[s];
-            y += ay[s];
-          }
-        }
+        // cumulative lattice displacement of (psi, turn, t) from the host-built table (one L2 load
+        // instead of t dependent lattice steps); final heading psi + t*h mod HL
+        const int2 cum = __ldg(&w.proj[((size_t)psi * w.n_turn + it) * W + (t - 1)]);
+        const int x = qx + cum.x, y = qy + cum.y;
+        int ps = (psi + t * h) % w.HL;
+        ps += ps < 0 ? w.HL : 0;
         // offsets from the fan origin o = q + (W/2) (DX, DY)[psi], doubled: the hot loop
         // evaluates |s - c|^2 - |s - o|^2 = Q + 2 (s - o).X with X = o - c, Q = |X|^2
         sx = (float)(2 * (x - qx - ox));
@@ -903,7 +890,9 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       if (xmode == 2) {
         stay_all = args.xbuf[NTAU * AW];  // all-reduced over the GPUs
       } else {
-        for (int b = 0; b < (int)G; ++b) stay_all = min(stay_all, s_stay[p * 16 + b]);
+#pragma unroll
+        for (int b = 0; b < 16; ++b)  // independent loads (G <= 16)
+          if (b < (int)G) stay_all = min(stay_all, s_stay[p * 16 + b]);
       }
       if (xmode == 1 && rank == 0 && tid == 0) args.xbuf[NTAU * AW] = stay_all;
 
@@ -1021,19 +1010,13 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
             }
           }
           // V*(a) = max(init, max_t V), term scale at the first maximising t: half-warp shuffles
-          double bv = v, bs = sc;
-          int bt = act ? hl : 99;
+          // (max of V over the half-warp, then the first substep attaining it by vote, then
+          //  its scale: one double per shuffle round instead of two doubles and an index)
+          double bv = v;
 #pragma unroll
-          for (int o = 8; o > 0; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, bv, o, 16);
-            const double os = __shfl_xor_sync(0xffffffffu, bs, o, 16);
-            const int ot = __shfl_xor_sync(0xffffffffu, bt, o, 16);
-            if (ov > bv || (ov == bv && ot < bt)) {
-              bv = ov;
-              bs = os;
-              bt = ot;
-            }
-          }
+          for (int o = 8; o > 0; o >>= 1) bv = fmax(bv, __shfl_xor_sync(0xffffffffu, bv, o, 16));
+          const unsigned hit = (__ballot_sync(0xffffffffu, act && v == bv) >> (lane & 16)) & 0xffffu;
+          const double bs = __shfl_sync(0xffffffffu, sc, (lane & 16) + (hit ? __ffs(hit) - 1 : 0));
           if (oa < n_own && hl < (int)G) {  // push {V*(a), S(a)} to CTA hl
             const double vstar = w.vmax_init_zero ? fmax(0.0, bv) : bv;
             st_async_d2(mapa_u32(smem_u32(&s_vv[a]), hl), vstar, bs, mapa_u32(smem_u32(&s_bar[5 + p]), hl));
