@@ -348,6 +348,9 @@ def run_native(args):
                      "kernel": "walk_kernel<3, false>", "ops_per_pair": OPS_PER_PAIR,
                      "ops_per_pair_basis": "algorithmic, SURVEY §8(d) d.3 (3 differences, 3 squares/fmas, 1 min)",
                      "pipe_frac": exec_tops / peak_tops, "exec_ops_per_pair": EXEC_OPS_PER_PAIR,
+                     "loop_ceiling": "isolated hot loop saturates the FMA pipe at 34-36 pairs/clk/SM (register-"
+                                     "operand FFMA2 at half the nominal lane rate; tools/hotbench, "
+                                     "profiles/r01_hotbench.txt)",
                      "peak_basis": f"FP32 pipe: 148 SM x 128 lanes x {peak_clock:.0f} MHz (MEASURED_PEAKS sm_max_mhz)"},
         "e2e": {"value": e2e_value, "unit": "requests/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,

@@ -708,12 +708,16 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           // (state, well) pair: |s - c|^2 - |s - o|^2 = Q + 2(s-o).X, the horizontal part
           // shared by the C climbs (2 FFMA2), one FFMA2 per climb; FMNMX3 folds both plans of a
           // pair into the running minimum (|s - o|^2 is added back by the owner)
-#define FMDP_WELL2(T, XY, ZQ)                                  \
-  {                                                            \
-    const f2 h = fma2(sy2, (XY).y, fma2(sx2, (XY).x, (ZQ).y)); \
-    _Pragma("unroll") for (int cc_ = 0; cc_ < C; ++cc_) {      \
-      m[cc_][T] = min3(m[cc_][T], fma2(sz2[cc_], (ZQ).x, h));  \
-    }                                                          \
+// One plan pair, all five wells, ordered by the shared operand (sx2, then sy2, then each
+// climb's sz2) so that consecutive FFMA2s are independent and reuse one register operand.
+#define FMDP_PAIR(E)                                                                   \
+  {                                                                                    \
+    f2 h_[NTAU];                                                                       \
+    _Pragma("unroll") for (int t_ = 0; t_ < NTAU; ++t_) h_[t_] = fma2(sx2, (E)[2 * t_].x, (E)[2 * t_ + 1].y); \
+    _Pragma("unroll") for (int t_ = 0; t_ < NTAU; ++t_) h_[t_] = fma2(sy2, (E)[2 * t_].y, h_[t_]);           \
+    _Pragma("unroll") for (int cc_ = 0; cc_ < C; ++cc_)                                \
+      _Pragma("unroll") for (int t_ = 0; t_ < NTAU; ++t_)                              \
+        m[cc_][t_] = min3(m[cc_][t_], fma2(sz2[cc_], (E)[2 * t_ + 1].x, h_[t_]));     \
   }
           const int npf = ns >> 1;  // full pairs; an odd tail is peeled below
           // the first tau's two records of the next pair load while this pair computes, so the
@@ -727,18 +731,16 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
             n1 = c8[1];
           }
           for (int pp = grp; pp < npf; pp += NGW, c8 += cstep) {
-            const ulonglong2 e0 = n0, e1 = n1;
-            const ulonglong2 e2 = c8[2], e3 = c8[3], e4 = c8[4], e5 = c8[5], e6 = c8[6], e7 = c8[7], e8 = c8[8],
-                             e9 = c8[9];
+            ulonglong2 e[10];
+            e[0] = n0;
+            e[1] = n1;
+#pragma unroll
+            for (int i = 2; i < 10; ++i) e[i] = c8[i];
             if (pp + NGW < npf) {
               n0 = c8[cstep];
               n1 = c8[cstep + 1];
             }
-            FMDP_WELL2(0, e0, e1)
-            FMDP_WELL2(1, e2, e3)
-            FMDP_WELL2(2, e4, e5)
-            FMDP_WELL2(3, e6, e7)
-            FMDP_WELL2(4, e8, e9)
+            FMDP_PAIR(e)
           }
           if ((ns & 1) && npf % NGW == grp) {  // odd tail: the partner slot is a well at infinity
             const ulonglong2* t8 = cen2 + (PAIR_STRIDE / 4) * npf;
@@ -754,13 +756,9 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
                 e[i].y = hi_set(e[i].y, 0.f);
               }
             }
-            FMDP_WELL2(0, e[0], e[1])
-            FMDP_WELL2(1, e[2], e[3])
-            FMDP_WELL2(2, e[4], e[5])
-            FMDP_WELL2(3, e[6], e[7])
-            FMDP_WELL2(4, e[8], e[9])
+            FMDP_PAIR(e)
           }
-#undef FMDP_WELL2
+#undef FMDP_PAIR
           if (tid == 0 && args.pairs) atomicAdd(args.pairs, (unsigned long long)ns * NTAU * AW);
         };
 
