@@ -31,7 +31,7 @@ METRIC = "FCFS requests scheduled/sec and ms/request vs #accepted plans, 1/2/4/8
 WORKLOAD = ("configs[1]: batch of 100 FCFS requests against 3000 accepted plans with a 256-well terrain "
             "grid, 16x16 km dense urban airspace, 9 headings x 3 climbs, W=10")
 OPS_PER_PAIR = 7.0  # algorithmic FP32 ops per (state, well) pair
-EXEC_OPS_PER_PAIR = 5.0 / 3.0  # FP32 lane-ops the kernel executes per pair at 3 climbs ((2 + C)/C)
+EXEC_OPS_PER_PAIR = 4.0 / 3.0  # FP32 lane-ops the kernel executes per pair at 3 climbs ((2 + C - 1)/C, level climb skipped)
 
 
 def parse():

@@ -22,6 +22,7 @@ struct World {
   int32_t A, W, n_turn, n_climb, HL;
   int32_t turn[MAX_TURN];
   int32_t climb[MAX_CLIMB];
+  int32_t zero_climb;           // index of the level-flight climb (0 units), -1 if none
   int32_t k_tau[NTAU];          // tau / dt substeps (padding taus: k = 0, R2 = 0)
   int64_t R2_tau[NTAU];         // exact R_tau^2, units^2
   float cull2f_tau[NTAU];       // (R_tau + reach + 1)^2 (1 + 2^-16): conservative FP32 f1 cull threshold

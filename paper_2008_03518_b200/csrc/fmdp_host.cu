@@ -789,6 +789,9 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   w.HL = a.heading_lattice;
   for (int i = 0; i < a.n_turn; ++i) w.turn[i] = a.turn_steps[i];
   for (int i = 0; i < a.n_climb; ++i) w.climb[i] = a.climb_units[i];
+  w.zero_climb = -1;
+  for (int i = 0; i < a.n_climb; ++i)
+    if (a.climb_units[i] == 0) w.zero_climb = i;
   int64_t Rmax = 0;
   for (int i = 0; i < fmdp::NTAU; ++i) {
     if (i < a.n_tau) {

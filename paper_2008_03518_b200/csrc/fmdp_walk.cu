@@ -18,6 +18,7 @@
 //   a6-a8  every CTA redundantly: combine (Alg 8), max over t, argmax (Alg 9),
 //       advance (Alg 1), terminal tests (Sec IV.I)
 #include <cooperative_groups.h>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include <cfloat>
@@ -704,7 +705,10 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           }
         };
         // Hot loop over ns well records (two plans per packed instruction).
-        auto hot = [&](int ns) {
+        auto hot_loop = [&](int ns, auto zero_mid) {
+          // zero_mid: the middle climb is level flight, so its FFMA2 (0 * Z + h) is exactly h
+          // and is skipped -- bit-identical, one FFMA2 per tau and plan pair fewer
+          constexpr bool ZM = decltype(zero_mid)::value;
           // (state, well) pair: |s - c|^2 - |s - o|^2 = Q + 2(s-o).X, the horizontal part
           // shared by the C climbs (2 FFMA2), one FFMA2 per climb; FMNMX3 folds both plans of a
           // pair into the running minimum (|s - o|^2 is added back by the owner)
@@ -717,7 +721,8 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
     _Pragma("unroll") for (int t_ = 0; t_ < NTAU; ++t_) h_[t_] = fma2(sy2, (E)[2 * t_].y, h_[t_]);           \
     _Pragma("unroll") for (int cc_ = 0; cc_ < C; ++cc_)                                \
       _Pragma("unroll") for (int t_ = 0; t_ < NTAU; ++t_)                              \
-        m[cc_][t_] = min3(m[cc_][t_], fma2(sz2[cc_], (E)[2 * t_ + 1].x, h_[t_]));     \
+        m[cc_][t_] = min3(m[cc_][t_], (ZM && cc_ == C / 2) ? h_[t_]                    \
+                                                           : fma2(sz2[cc_], (E)[2 * t_ + 1].x, h_[t_])); \
   }
           const int npf = ns >> 1;  // full pairs; an odd tail is peeled below
           // the first tau's two records of the next pair load while this pair computes, so the
@@ -760,6 +765,10 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           }
 #undef FMDP_PAIR
           if (tid == 0 && args.pairs) atomicAdd(args.pairs, (unsigned long long)ns * NTAU * AW);
+        };
+        auto hot = [&](int ns) {
+          if (w.zero_climb == C / 2) hot_loop(ns, std::true_type{});
+          else hot_loop(ns, std::false_type{});
         };
 
         // batch peers at clock K (Alg 5, P^- of Table DS), five wells each, staged
