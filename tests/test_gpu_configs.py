@@ -133,3 +133,28 @@ def test_a85_random_small(F, seed):
     st = orc.replay(sc.src[0], sc.dst[0], int(sc.t0[0]), r.traj, hd, ast, r.status)
     assert st.n_fail == 0
     ctx.close()
+
+
+@pytest.mark.parametrize("climbs,turns", [
+    ((0,), (-8, -4, 0, 4, 8)),                 # C = 1: 512-thread instantiation, level flight only
+    ((-16, 8, 16), (-8, -4, 0, 4, 8)),         # C = 3 without a level climb: general hot loop
+    ((-24, -16, 0, 16, 24), (-6, 0, 6)),       # C = 5, level climb in the middle
+])
+def test_action_sets(F, climbs, turns):
+    """Hot-loop variants by climb set: every (state, action, t) value, a*, separation minima
+    and a whole trajectory against the oracle; culled and G = 4 runs bit-identical."""
+    sc = fs.random_small(61, n_plans=250, half_m=1500.0, n_buildings=20, climb_units=climbs, turn_steps=turns)
+    orc = O.for_scenario(sc)
+    ctx = ctx_for(F, sc)
+    for q, psi, g, K in fs.random_states(62, sc, 8):
+        check_step(ctx.eval_step(q, psi, g, K), orc.eval_step(q, psi, g, K), f"climbs {climbs}")
+    r = ctx.schedule(sc.src[0], sc.dst[0], int(sc.t0[0]))
+    ast, hd, _ = ctx.steplog(0)
+    st = orc.replay(sc.src[0], sc.dst[0], int(sc.t0[0]), r.traj, hd, ast, r.status)
+    assert st.n_fail == 0 and r.n_states > 20
+    n0 = ctx.num_plans()
+    ctx.truncate(n0 - 1 if r.accepted else n0)
+    ctx.set_launch(cull=1, cluster_size=4)
+    r2 = ctx.schedule(sc.src[0], sc.dst[0], int(sc.t0[0]))
+    assert (r2.status, r2.n_states) == (r.status, r.n_states) and (r2.traj == r.traj).all()
+    ctx.close()
