@@ -73,7 +73,8 @@ for rep, title in (('walk_batch', 'configs[1] batch slice, 100 walkers x G=1 (fu
                        note="DRAM traffic per launch; the kernel is FP32-pipe bound, plan rows are L2-resident")
     h, d = source(f'gpurun_out/{rep}.ncu-rep')
     iss = h.index("Warp Stall Sampling (All Samples)"); ie = h.index("Instructions Executed"); isrc = h.index("Source")
-    ex = [float(r[ie] or 0) for r in d]
+    # hottest compute region: skip mbarrier spin-waits (SYNCS / YIELD loops)
+    ex = [0.0 if any(k in r[isrc] for k in ('SYNCS', 'YIELD', 'NANOSLEEP')) else float(r[ie] or 0) for r in d]
     mx = max(ex)
     hot = [i for i, e in enumerate(ex) if e >= 0.9 * mx]
     a, b = min(hot), max(hot) + 1
