@@ -87,6 +87,11 @@ for rep, title in (('walk_batch', 'configs[1] batch slice, 100 walkers x G=1 (fu
         tok = r[isrc].split()
         op = tok[1] if tok and tok[0].startswith('@') else (tok[0] if tok else '')
         ops[op.split('.')[0]] += 1
+    if b - a < 10:
+        lines += ["", "No dominant loop (latency-bound step): per-source-line stall attribution in "
+                  f"profiles/{rnd}_lines_{'cull2' if 'cull' in rep else 'batch_full'}.txt (tools/ncu_lines.py).",
+                  "Whole kernel: " + ", ".join(f"{k} {v:.1f}%" for k, v in sorted(allst.items(), key=lambda x: -x[1])) + ".", ""]
+        continue
     lines += ["", f"Most-executed loop: {b - a} SASS instructions, {hs / ts * 100:.1f} % of warp-stall samples; "
               + "reasons: " + ", ".join(f"{k} {v:.1f}%" for k, v in sorted(st.items(), key=lambda x: -x[1])) + ".",
               "Instruction mix: " + ", ".join(f"{k} {v}" for k, v in ops.most_common()) + ".",
