@@ -58,6 +58,7 @@ class Airspace:
     sep_m: float = 150.0
     max_steps: int = 4000
     vmax_init_zero: int = 0
+    valuation: int = 0                   # 0 Alg 8 (max over the window), 1 Alg 1 endpoint
     near_tie_rel: float = 1e-4
     # store geometry (library side only; the oracle ignores these)
     lo_m: Tuple[float, float, float] = (-8000.0, -8000.0, 0.0)

@@ -101,6 +101,9 @@ typedef struct fmdp_airspace {
   double near_tie_rel;             /* 1e-4: near-tie threshold for logging               */
   int64_t horizon_steps;           /* number of time rows in the plan store              */
   int32_t row_capacity;            /* plan slots per time row (multiple of 4)            */
+  int32_t valuation;               /* 0: Alg 8 V*(a) = max over the window;  */
+                                   /* 1: Alg 1 endpoint only, V*(a) = V(Delta_10(a))     */
+                                   /*    (R31)           */
 } fmdp_airspace;
 
 /* Terrain: manually placed wells (Table PK) and a ground-height raster used only

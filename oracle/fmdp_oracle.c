@@ -381,6 +381,10 @@ int orc_eval_step_peers(const orc_params* p, const orc_terrain* T, const orc_sto
     }
     vstar[a] = vmax;  /* P:754 */
     vsc[a] = best_sc;
+    if (p->valuation == 1) {  /* Alg 1 P:174-213: the value of the endpoint of Delta_10 (R31) */
+      vstar[a] = v[a * W + W - 1];
+      vsc[a] = scale[a * W + W - 1];
+    }
   }
 
   /* Select best action (Alg 9 P:771), lowest index on ties (R13). */

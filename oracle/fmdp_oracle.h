@@ -47,6 +47,7 @@ typedef struct orc_params {
   int32_t max_steps;
   int32_t vmax_init_zero;                    /* 1: literal Alg 8 V_max <- 0   */
   double near_tie_rel;                       /* 1e-4 (north star)                     */
+  int32_t valuation;                         /* 0 Alg 8 max over t; 1 Alg 1 endpoint   */
 } orc_params;
 
 /* Terrain: manually placed wells (Table PK) + a height raster for collision. */

@@ -47,6 +47,7 @@ class Params(C.Structure):
         ("deck_alt_m", C.c_double), ("deck_scale", C.c_double),
         ("capture_m", C.c_double), ("sep_m", C.c_double),
         ("max_steps", C.c_int32), ("vmax_init_zero", C.c_int32), ("near_tie_rel", C.c_double),
+        ("valuation", C.c_int32),
     ]
 
 
@@ -137,6 +138,7 @@ def params_of(air) -> Params:
     p.deck_alt_m, p.deck_scale = air.deck_alt_m, air.deck_scale
     p.capture_m, p.sep_m = air.capture_m, air.sep_m
     p.max_steps, p.vmax_init_zero, p.near_tie_rel = air.max_steps, air.vmax_init_zero, air.near_tie_rel
+    p.valuation = getattr(air, "valuation", 0)
     return p
 
 

@@ -42,6 +42,7 @@ struct World {
   int32_t zdeck_u;
   double deck_scale, u_m;
   int32_t max_steps, vmax_init_zero;
+  int32_t endpoint;             // 1: Alg 1 valuation, V*(a) = V at the last substep
   double near_tie_rel;
   // accepted-plan store: rows[K] = { x[cap], y[cap], z[cap], vpack[cap] } (int32 SoA)
   int64_t horizon;

@@ -685,6 +685,7 @@ void fmdp_airspace_default(fmdp_airspace* a) {
   a->sep_min_m = 150.0;
   a->max_steps = 4000;
   a->vmax_init_zero = 0;
+  a->valuation = 0;
   a->near_tie_rel = 1e-4;
   a->horizon_steps = 8192;
   a->row_capacity = 4096;
@@ -733,6 +734,7 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
     return bad(FMDP_E_ARG, "deck/capture/sep must be multiples of u");
   if (a.horizon_steps < 4 || a.row_capacity < 4 || a.row_capacity % 4) return bad(FMDP_E_ARG, "store geometry");
   if (a.max_steps < 1) return bad(FMDP_E_ARG, "max_steps");
+  if (a.valuation != 0 && a.valuation != 1) return bad(FMDP_E_ARG, "valuation must be 0 (Alg 8) or 1 (Alg 1)");
 
   ctx->air = a;
   ctx->turn.assign(a.turn_steps, a.turn_steps + a.n_turn);
@@ -825,6 +827,7 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   w.u_m = a.u_m;
   w.max_steps = a.max_steps;
   w.vmax_init_zero = a.vmax_init_zero;
+  w.endpoint = a.valuation == 1 ? 1 : 0;
   w.near_tie_rel = a.near_tie_rel;
   w.horizon = a.horizon_steps;
   w.row_cap = a.row_capacity;

@@ -1019,13 +1019,19 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           // V*(a) = max(init, max_t V), term scale at the first maximising t: half-warp shuffles
           // (max of V over the half-warp, then the first substep attaining it by vote, then
           //  its scale: one double per shuffle round instead of two doubles and an index)
-          double bv = v;
+          double bv, bs;
+          if (w.endpoint) {  // Alg 1: the value of the window's endpoint (R31)
+            bv = __shfl_sync(0xffffffffu, v, (lane & 16) + W - 1);
+            bs = __shfl_sync(0xffffffffu, sc, (lane & 16) + W - 1);
+          } else {
+            bv = v;
 #pragma unroll
-          for (int o = 8; o > 0; o >>= 1) bv = fmax(bv, __shfl_xor_sync(0xffffffffu, bv, o, 16));
-          const unsigned hit = (__ballot_sync(0xffffffffu, act && v == bv) >> (lane & 16)) & 0xffffu;
-          const double bs = __shfl_sync(0xffffffffu, sc, (lane & 16) + (hit ? __ffs(hit) - 1 : 0));
+            for (int o = 8; o > 0; o >>= 1) bv = fmax(bv, __shfl_xor_sync(0xffffffffu, bv, o, 16));
+            const unsigned hit = (__ballot_sync(0xffffffffu, act && v == bv) >> (lane & 16)) & 0xffffu;
+            bs = __shfl_sync(0xffffffffu, sc, (lane & 16) + (hit ? __ffs(hit) - 1 : 0));
+          }
           if (oa < n_own && hl < (int)G) {  // push {V*(a), S(a)} to CTA hl
-            const double vstar = w.vmax_init_zero ? fmax(0.0, bv) : bv;
+            const double vstar = (w.vmax_init_zero && !w.endpoint) ? fmax(0.0, bv) : bv;
             st_async_d2(mapa_u32(smem_u32(&s_vv[a]), hl), vstar, bs, mapa_u32(smem_u32(&s_bar[5 + p]), hl));
             if (args.eval && hl == 0) args.dbg_vstar[a] = vstar;
           }

@@ -45,7 +45,7 @@ class Airspace(C.Structure):
         ("terr_r", C.c_double), ("terr_gamma", C.c_double), ("deck_alt_m", C.c_double), ("deck_scale", C.c_double),
         ("capture_radius_m", C.c_double), ("sep_min_m", C.c_double),
         ("max_steps", C.c_int32), ("vmax_init_zero", C.c_int32), ("near_tie_rel", C.c_double),
-        ("horizon_steps", C.c_int64), ("row_capacity", C.c_int32),
+        ("horizon_steps", C.c_int64), ("row_capacity", C.c_int32), ("valuation", C.c_int32),
     ]
 
 
@@ -194,6 +194,7 @@ class FMDP:
         a.capture_radius_m, a.sep_min_m = airspace.capture_m, airspace.sep_m
         a.max_steps, a.vmax_init_zero, a.near_tie_rel = airspace.max_steps, airspace.vmax_init_zero, airspace.near_tie_rel
         a.horizon_steps, a.row_capacity = airspace.horizon_steps, airspace.row_capacity
+        a.valuation = getattr(airspace, "valuation", 0)
         self.max_steps = int(airspace.max_steps)
         self.W = int(airspace.W)
         t = Terrain()

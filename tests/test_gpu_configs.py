@@ -158,3 +158,23 @@ def test_action_sets(F, climbs, turns):
     r2 = ctx.schedule(sc.src[0], sc.dst[0], int(sc.t0[0]))
     assert (r2.status, r2.n_states) == (r.status, r.n_states) and (r2.traj == r.traj).all()
     ctx.close()
+
+
+def test_endpoint_valuation(F):
+    """SURVEY f4, Alg 1 endpoint-only valuation (R31): values, V*(a) = V(a, W), a*, separation
+    minima and a whole trajectory against the oracle; culled and G = 4 runs bit-identical."""
+    sc = fs.random_small(71, n_plans=300, half_m=1500.0, n_buildings=20, valuation=1)
+    orc = O.for_scenario(sc)
+    ctx = ctx_for(F, sc)
+    for q, psi, g, K in fs.random_states(72, sc, 10):
+        check_step(ctx.eval_step(q, psi, g, K), orc.eval_step(q, psi, g, K), "endpoint")
+    r = ctx.schedule(sc.src[0], sc.dst[0], int(sc.t0[0]))
+    ast, hd, _ = ctx.steplog(0)
+    st = orc.replay(sc.src[0], sc.dst[0], int(sc.t0[0]), r.traj, hd, ast, r.status)
+    assert st.n_fail == 0 and r.n_states > 20
+    n0 = ctx.num_plans()
+    ctx.truncate(n0 - 1 if r.accepted else n0)
+    ctx.set_launch(cull=1, cluster_size=4)
+    r2 = ctx.schedule(sc.src[0], sc.dst[0], int(sc.t0[0]))
+    assert (r2.status, r2.n_states) == (r.status, r.n_states) and (r2.traj == r.traj).all()
+    ctx.close()
