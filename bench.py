@@ -301,10 +301,50 @@ def run_native(args):
                 "paper_note": "paper's GPU, A=1350 actions (context, not the target)",
                 "sizes": out}
 
+    def measure_latency(plan_counts=(0, 1000, 3000, 10000, 30000), reps=2, min_steps=200):
+        # metric "ms/request vs #accepted plans" (Fig perf1): one request against
+        # stores of P reflecting-line plans at the configs[1] traffic density (box side ~ sqrt P),
+        # the first of the scenario's requests that flies >= min_steps; cluster size from the
+        # cost model for a lone walker; device time of the walk launches
+        out = []
+        for P in plan_counts:
+            sc_p = fs.config_scaled(args.seed + 7 + 1000 * rank, P)
+            lctx = FMDP(sc_p.airspace, sc_p.terrain, device=local, stream=stream)
+            if P:
+                lctx.add_plans(sc_p.plans)
+            row = {"plans": P, "box_km": round(2 * sc_p.airspace.hi_m[0] / 1000.0, 1)}
+            pick = 0
+            lctx.set_launch(cull=1)
+            for i in range(len(sc_p.t0)):
+                r = lctx.schedule(sc_p.src[i], sc_p.dst[i], int(sc_p.t0[i]), want_traj=False)
+                lctx.truncate(P)
+                if r.n_states - 1 >= min_steps:
+                    pick = i
+                    break
+            row["request"] = pick
+            for cull in (0, 1):
+                lctx.set_launch(cull=cull)
+                best = None
+                for _ in range(reps):
+                    r = lctx.schedule(sc_p.src[pick], sc_p.dst[pick], int(sc_p.t0[pick]), want_traj=False)
+                    st = lctx.stats()
+                    lctx.truncate(P)
+                    if best is None or st["device_ms"] < best[0]:
+                        best = (st["device_ms"], st["steps"], r.status, st["cluster_size"])
+                row["culled" if cull else "full"] = {
+                    "ms_per_request": best[0], "us_per_step": best[0] * 1e3 / max(1, best[1]), "steps": best[1],
+                    "status": best[2], "cluster_size": best[3]}
+            lctx.close()
+            out.append(row)
+        return {"what": "single-request latency vs accepted plans (metric: ms/request vs #accepted plans; Fig "
+                        "perf1): fmdp_synth.config_scaled, constant configs[1] density; device time of the walk",
+                "points": out}
+
     M = measure(0)       # every (state, well) pair evaluated
     Mc = measure(1)      # exact culling, bit-identical outputs
     Md = measure_departures()
     Mco = measure_cosim()
+    Mlat = measure_latency()
     h2d = n * C_REQUEST_BYTES
     tot_ms, value, e2e_value, d2h = M["tot_ms"], M["value"], M["e2e_value"], M["d2h"]
     stats = M["st_all"][-1]
@@ -366,6 +406,7 @@ def run_native(args):
             "same_results_as_full": same, "clocks": Mc["clocks"]},
         "f3_departures": Md,
         "f2_cosim": Mco,
+        "latency_vs_plans": Mlat,
     }
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(sc, args.cpu_sample_s)

@@ -364,3 +364,21 @@ def cosim_ring(seed: int, n_batch: int, n_plans: int = 100, radius_m: float = 12
     t0 = rng.integers(0, max(1, t0_max), n_batch).astype(np.int64)
     return Scenario(a, Terrain(), plans, m2u(src).astype(np.int32), m2u(dst).astype(np.int32), t0,
                     name=f"cosim{seed}x{n_batch}")
+
+
+def config_scaled(seed: int, n_plans: int, rows: int = 3000, n_requests: int = 20) -> Scenario:
+    """Fig perf1 (performance vs accepted plans) at constant traffic density: n_plans
+    reflecting lines in a square box sized for the configs[1] density (3000 plans per
+    16 x 16 km, never smaller than that box), z in [60, 1500] m, the configs[1] city (256
+    buildings in the central 10 km) and 3-7 km requests between its vertiports."""
+    rng = np.random.default_rng(seed)
+    half = max(8000.0, 8000.0 * float(np.sqrt(max(n_plans, 1) / 3000.0)))
+    a = Airspace(max_steps=min(4000, rows - 320), lo_m=(-half, -half, 0.0), hi_m=(half, half, 1500.0),
+                 horizon_steps=rows + 8, row_capacity=((n_plans + n_requests + 64) + 3) // 4 * 4)
+    terrain = manhattan_terrain(rng, 256, core_half_m=5000.0, raster_half_m=8000.0)
+    lo, hi = m2u(a.lo_m), m2u(a.hi_m)
+    plans = (reflecting_lines_fast(rng, n_plans, lo, hi, (0, rows), z_lo_u=int(m2u(60)), z_hi_u=int(m2u(1500)))
+             if n_plans else [])
+    pads = vertiports(rng, 200, 5000.0, terrain)
+    src, dst, t0 = request_pairs(rng, pads, n_requests, 3000.0, 7000.0, (0, 300))
+    return Scenario(a, terrain, plans, src, dst, t0, name=f"scaled{n_plans}")
