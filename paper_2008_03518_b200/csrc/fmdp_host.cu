@@ -98,7 +98,8 @@ struct fmdp_ctx {
   int mc_cache_cs[17] = {0};
   double fan_radius_u = 0;             // bound on |s - o| (hot-loop origin), units
   double band_rel[fmdp::NTAU] = {0};   // FP32 filter band per tau, relative to R^2
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
+  cudaStream_t stream2 = nullptr;  // second stream of a split FCFS slice (the non-head walkers)
 };
 
 namespace {
@@ -270,14 +271,15 @@ double mean_plans(const fmdp_ctx* ctx) {
 
 // Cluster size for a round of n_run trajectories: the G minimising waves(G) * t(G) among the
 // sizes that can run.
-void choose_launch(fmdp_ctx* ctx, int n_run, int* G_out, int* nc_out) {
+void choose_launch(fmdp_ctx* ctx, int n_run, int* G_out, int* nc_out, int sm_cap = 0) {
   int best_G = 1;
   double best = 1e300;
   const double plans = mean_plans(ctx);
   const int sizes[] = {16, 8, 4, 2, 1};
   for (int G : sizes) {
     if (ctx->launch.cluster_size && G != ctx->launch.cluster_size) continue;
-    const int mc = max_clusters(ctx, G);
+    int mc = max_clusters(ctx, G);
+    if (sm_cap > 0) mc = std::min(mc, sm_cap / G);  // SMs left to this launch
     if (mc <= 0) continue;
     int conc = std::min(mc, n_run);
     if (ctx->launch.max_walkers > 0) conc = std::min(conc, ctx->launch.max_walkers);
@@ -289,6 +291,7 @@ void choose_launch(fmdp_ctx* ctx, int n_run, int* G_out, int* nc_out) {
     }
   }
   int mc = std::max(1, max_clusters(ctx, best_G));
+  if (sm_cap > 0) mc = std::max(1, std::min(mc, sm_cap / best_G));
   int conc = std::min(mc, n_run);
   if (ctx->launch.max_walkers > 0) conc = std::min(conc, ctx->launch.max_walkers);
   *G_out = best_G;
@@ -364,6 +367,51 @@ fmdp_status run_walk(fmdp_ctx* ctx, const std::vector<Req>& run, bool eval, int 
   ctx->stats.device_ms += ms;
   ctx->stats.kernels += 1;
   if (std::getenv("FMDP_DEBUG")) std::fprintf(stderr, "fmdp: walk n=%zu G=%d clusters=%d %.3f ms\n", run.size(), G, nc, ms);
+  return FMDP_OK;
+}
+
+// A split FCFS slice: the head (run[0], the earliest pending request -- everything before it is
+// committed, so it can never be rolled back) alone at the cluster size a lone walker would use,
+// on the library stream; the other pending requests concurrently on a second stream with the
+// SMs left, cluster size from the cost model.  They go on past `budget` until the head has
+// finished (the device stop flag the head sets), so the slice is as long as the head's
+// remaining trajectory -- the FCFS critical path -- and never waits on anything else.
+fmdp_status run_split(fmdp_ctx* ctx, std::vector<Req>& run, int budget) {
+  const int n = (int)run.size();
+  for (Req& r : run) r.head = 0;
+  run[0].head = 1;
+  const int Gh = solo_cluster_size(ctx);
+  int Go = 0, nco = 0;
+  choose_launch(ctx, n - 1, &Go, &nco, ctx->num_sms - Gh);
+  CK(cudaMemcpyAsync(ctx->d_reqs, run.data(), sizeof(Req) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemsetAsync(ctx->d_queue, 0, 2 * sizeof(int32_t), ctx->stream));  // [0] head, [1] others
+  CK(cudaMemsetAsync(ctx->d_stop, 0, sizeof(int32_t), ctx->stream));
+  CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  CK(cudaStreamWaitEvent(ctx->stream2, ctx->ev0, 0));
+  fmdp::WalkArgs ah = make_args(ctx, run, false, budget);
+  ah.reqs = ctx->d_reqs;
+  ah.n_reqs = 1;
+  ah.queue = ctx->d_queue;
+  ah.stop = ctx->d_stop;
+  fmdp::WalkArgs ao = ah;
+  ao.reqs = ctx->d_reqs + 1;
+  ao.n_reqs = n - 1;
+  ao.queue = ctx->d_queue + 1;
+  CK(fmdp::launch_walk(ctx->w, ah, ctx->C, Gh, 1, threads_for(ctx), chunk_for(ctx), rawcap_for(ctx), ctx->stream));
+  CK(fmdp::launch_walk(ctx->w, ao, ctx->C, Go, nco, threads_for(ctx), chunk_for(ctx), rawcap_for(ctx), ctx->stream2));
+  CK(cudaEventRecord(ctx->ev2, ctx->stream2));
+  CK(cudaStreamWaitEvent(ctx->stream, ctx->ev2, 0));
+  CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  CK(cudaEventSynchronize(ctx->ev1));
+  CK(cudaGetLastError());
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  ctx->stats.device_ms += ms;
+  ctx->stats.kernels += 2;
+  ctx->stats.cluster_size = Gh;
+  ctx->stats.walkers = std::max(ctx->stats.walkers, 1 + nco);
+  if (std::getenv("FMDP_DEBUG"))
+    std::fprintf(stderr, "fmdp: split walk n=%d head G=%d others G=%d clusters=%d %.3f ms\n", n, Gh, Go, nco, ms);
   return FMDP_OK;
 }
 
@@ -548,16 +596,15 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
         // runs the head (request c: everything before it is committed, so it can never be
         // rolled back) to completion; the others go on past `budget` until it is done -- their
         // extra steps cost no wall time and stay valid unless a rollback discards them.
-        int G = 0, nc = 0;
-        choose_launch(ctx, (int)run.size(), &G, &nc);
-        const bool single = nc >= (int)run.size() && G >= solo_cluster_size(ctx);
-        fmdp::WalkArgs a = make_args(ctx, run, false, budget);
-        if (single) {
-          run[0].head = 1;  // run[0] is request c
+        if (run.size() >= 2) {
+          if ((st = run_split(ctx, run, budget))) return st;  // run[0] is request c
+        } else {
+          run[0].head = 1;
+          fmdp::WalkArgs a = make_args(ctx, run, false, budget);
           CK(cudaMemsetAsync(ctx->d_stop, 0, sizeof(int32_t), ctx->stream));
           a.stop = ctx->d_stop;
+          if ((st = run_walk(ctx, run, false, budget, &a, solo_cluster_size(ctx), 1))) return st;
         }
-        if ((st = run_walk(ctx, run, false, budget, &a, G, nc))) return st;
         runs += (int)run.size();
         ctx->stats.rounds += 1;
       }
@@ -781,6 +828,8 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   }
   cudaEventCreate(&ctx->ev0);
   cudaEventCreate(&ctx->ev1);
+  cudaEventCreate(&ctx->ev2);
+  if (cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking) != cudaSuccess) return bad(FMDP_E_CUDA, "stream");
 
   World& w = ctx->w;
   std::memset(&w, 0, sizeof(w));
@@ -996,6 +1045,8 @@ void fmdp_destroy(fmdp_ctx* ctx) {
   for (void* p : a) dfree(ctx, p);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->ev2) cudaEventDestroy(ctx->ev2);
+  if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
