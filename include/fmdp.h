@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define FMDP_ABI_VERSION 1
+#define FMDP_ABI_VERSION 2  /* 2: fmdp_airspace.valuation */
 
 typedef struct fmdp_ctx fmdp_ctx; /* opaque; owns device memory, plan store, scratch */
 typedef int32_t fmdp_status;
@@ -282,6 +282,8 @@ fmdp_status fmdp_eval_step(fmdp_ctx* ctx, fmdp_qpos pos, int32_t heading, fmdp_q
 fmdp_status fmdp_get_stats(const fmdp_ctx* ctx, fmdp_stats* out);
 int32_t fmdp_num_actions(const fmdp_ctx* ctx);
 const char* fmdp_strerror(fmdp_status s);
+/* Text of the context's last error; with ctx == NULL, the reason this thread's last
+ * fmdp_create failed. */
 const char* fmdp_last_error(const fmdp_ctx* ctx);
 
 #ifdef __cplusplus

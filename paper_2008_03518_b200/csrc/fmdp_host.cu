@@ -104,6 +104,8 @@ struct fmdp_ctx {
 
 namespace {
 
+thread_local std::string g_create_error = "";  // reason of this thread's last failed fmdp_create
+
 const char* kStatusText[] = {"ok", "invalid argument", "out of memory", "CUDA error", "row capacity exceeded",
                              "duplicate", "buffer too small", "out of range", "no sm_100 device"};
 
@@ -745,7 +747,7 @@ const char* fmdp_strerror(fmdp_status s) {
   return "unknown status";
 }
 
-const char* fmdp_last_error(const fmdp_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+const char* fmdp_last_error(const fmdp_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_error.c_str(); }
 
 int32_t fmdp_num_actions(const fmdp_ctx* ctx) { return ctx ? ctx->A : 0; }
 
@@ -753,12 +755,15 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
                         fmdp_ctx** out) {
   if (!air || !out) return FMDP_E_ARG;
   *out = nullptr;
-  if (air->abi_version != FMDP_ABI_VERSION) return FMDP_E_ARG;
+  if (air->abi_version != FMDP_ABI_VERSION) {
+    g_create_error = "fmdp_airspace.abi_version does not match FMDP_ABI_VERSION (header / library mismatch)";
+    return FMDP_E_ARG;
+  }
   fmdp_ctx* ctx = new (std::nothrow) fmdp_ctx();
   if (!ctx) return FMDP_E_NOMEM;
-  auto bad = [&](fmdp_status s, const char* m) {
-    std::fprintf(stderr, "fmdp_create: %s\n", m);
-    delete ctx;
+  auto bad = [&](fmdp_status s, const char* m) {  // release what was created so far
+    g_create_error = m;
+    fmdp_destroy(ctx);
     return s;
   };
   const fmdp_airspace& a = *air;
@@ -960,8 +965,7 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   ctx->d_xbuf = (uint32_t*)dalloc(ctx, sizeof(uint32_t) * ((size_t)A * a.window * fmdp::NTAU + 1));
   if (!ctx->d_rows || !ctx->d_counts || !ctx->d_dxy || !ctx->d_proj || !ctx->d_queue || !ctx->d_pairctr || !ctx->d_prof || !ctx->d_dbg_vstar ||
       !ctx->d_dbg_v || !ctx->d_dbg_s || !ctx->d_dbg_conf || !ctx->d_dbg_astar || !ctx->d_xbuf) {
-    fmdp_destroy(ctx);
-    return FMDP_E_NOMEM;
+    return bad(FMDP_E_NOMEM, "device allocation failed");
   }
   cudaMemset(ctx->d_rows, 0, sizeof(int32_t) * row_words * (size_t)w.horizon);
   cudaMemset(ctx->d_counts, 0, sizeof(int32_t) * (size_t)w.horizon);
@@ -988,16 +992,14 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
 
   if (ter && ter->n_wells > 0) {
     if (!ter->center || !ter->radius_u) {
-      fmdp_destroy(ctx);
-      return FMDP_E_ARG;
+      return bad(FMDP_E_ARG, "terrain arrays missing");
     }
     std::vector<int4> tw(ter->n_wells);
     for (int i = 0; i < ter->n_wells; ++i)
       tw[i] = make_int4(ter->center[i].x, ter->center[i].y, ter->center[i].z, ter->radius_u[i]);
     ctx->d_tw = (int4*)dalloc(ctx, sizeof(int4) * tw.size());
     if (!ctx->d_tw) {
-      fmdp_destroy(ctx);
-      return FMDP_E_NOMEM;
+      return bad(FMDP_E_NOMEM, "device allocation failed");
     }
     cudaMemcpy(ctx->d_tw, tw.data(), sizeof(int4) * tw.size(), cudaMemcpyHostToDevice);
     w.n_tw = ter->n_wells;
@@ -1005,14 +1007,12 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   }
   if (ter && ter->nx > 0 && ter->ny > 0) {
     if (!ter->height_u || ter->cell_u <= 0) {
-      fmdp_destroy(ctx);
-      return FMDP_E_ARG;
+      return bad(FMDP_E_ARG, "terrain arrays missing");
     }
     const size_t nh = (size_t)ter->nx * ter->ny;
     ctx->d_height = (int32_t*)dalloc(ctx, sizeof(int32_t) * nh);
     if (!ctx->d_height) {
-      fmdp_destroy(ctx);
-      return FMDP_E_NOMEM;
+      return bad(FMDP_E_NOMEM, "device allocation failed");
     }
     cudaMemcpy(ctx->d_height, ter->height_u, sizeof(int32_t) * nh, cudaMemcpyHostToDevice);
     w.nx = ter->nx;
@@ -1024,15 +1024,10 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
     w.height = ctx->d_height;
   }
   ctx->cap_states = a.max_steps + 2;
-  if (threads_for(ctx) > (ctx->C == 1 ? 512 : 384) || fmdp::walk_smem_bytes(w, ctx->C, threads_for(ctx), kChunk, kChunk, 16) > 227 * 1024) {
-    fmdp_destroy(ctx);
-    return FMDP_E_ARG;
-  }
+  if (threads_for(ctx) > (ctx->C == 1 ? 512 : 384) || fmdp::walk_smem_bytes(w, ctx->C, threads_for(ctx), kChunk, kChunk, 16) > 227 * 1024)
+    return bad(FMDP_E_ARG, "action lattice too large for one CTA (threads / shared memory)");
   cudaError_t e = cudaDeviceSynchronize();
-  if (e != cudaSuccess) {
-    fmdp_destroy(ctx);
-    return FMDP_E_CUDA;
-  }
+  if (e != cudaSuccess) return bad(FMDP_E_CUDA, cudaGetErrorString(e));
   *out = ctx;
   return FMDP_OK;
 }

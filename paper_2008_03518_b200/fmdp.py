@@ -16,7 +16,7 @@ import numpy as np
 
 from .build import LIB
 
-ABI_VERSION = 1
+ABI_VERSION = 2  # include/fmdp.h FMDP_ABI_VERSION
 ACCEPTED, REJ_CONFLICT, REJ_TERRAIN, REJ_TIMEOUT = 0, 1, 2, 3
 STATUS_NAMES = {0: "ACCEPTED", 1: "REJ_CONFLICT", 2: "REJ_TERRAIN", 3: "REJ_TIMEOUT"}
 BATCH_SEQUENTIAL = 1
@@ -230,7 +230,9 @@ class FMDP:
         self.ctx = C.c_void_p()
         rc = self.L.fmdp_create(C.byref(a), C.byref(t), C.byref(d), C.byref(self.ctx))
         if rc != 0:
-            raise FmdpError(f"fmdp_create failed: {self.L.fmdp_strerror(rc).decode()} ({rc})")
+            why = self.L.fmdp_last_error(None).decode()
+            self.ctx = None
+            raise FmdpError(f"fmdp_create failed: {self.L.fmdp_strerror(rc).decode()} ({rc}) {why}")
         self.A = int(self.L.fmdp_num_actions(self.ctx))
 
     # ------------------------------------------------------------------ plumbing

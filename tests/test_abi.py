@@ -61,3 +61,16 @@ def test_product_package_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".h", ".cpp")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", txt).lower().replace("no cpu fallback", ""), f
+
+
+def test_abi_version_matches_the_header():
+    """The binding's ABI version and its fmdp_airspace mirror follow include/fmdp.h."""
+    import re
+    from paper_2008_03518_b200 import fmdp
+    hdr = open(os.path.join(ROOT, "include", "fmdp.h")).read()
+    assert int(re.search(r"#define FMDP_ABI_VERSION (\d+)", hdr).group(1)) == fmdp.ABI_VERSION
+    body = hdr[hdr.index("typedef struct fmdp_airspace"):hdr.index("} fmdp_airspace;")]
+    names = re.findall(r"^\s+(?:const\s+)?[\w\s\*]+?\b(\w+)(?:\[\d+\])?\s*[;,]", body, re.M)
+    fields = [f for f, _ in fmdp.Airspace._fields_]
+    assert names[-1] == fields[-1] == "valuation"
+    assert len(fields) >= 30

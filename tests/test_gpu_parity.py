@@ -318,3 +318,17 @@ def test_departure_candidates(F):
         assert rp.n_fail == 0
     ctx.close()
     ref.close()
+
+
+def test_create_errors_are_reported(F):
+    """A rejected scenario frees everything it created and reports why (fmdp_last_error(NULL))."""
+    with pytest.raises(F.FmdpError, match="u/dt/window"):
+        F.FMDP(fs.Airspace(W=0), fs.Terrain(), device=0)
+    with pytest.raises(F.FmdpError, match="valuation"):
+        F.FMDP(fs.Airspace(valuation=3), fs.Terrain(), device=0)
+    for _ in range(3):  # repeated failures leak no streams / events / memory
+        with pytest.raises(F.FmdpError):
+            F.FMDP(fs.Airspace(sep_m=500.0), fs.Terrain(), device=0)
+    ctx = F.FMDP(fs.Airspace(), fs.Terrain(), device=0)
+    assert ctx.A == 27
+    ctx.close()
