@@ -2,7 +2,7 @@
  * fmdp.h -- C ABI of the B200-native FastMDP-GPU hot path (arXiv 2008.03518).
  *
  * Paper passages are cited as P:n = line n of the paper source; the readings
- * of ambiguous passages (R1..R23) are listed in DESIGN.md "Readings".
+ * of ambiguous passages (R1..R31) are listed in DESIGN.md "Readings".
  *
  * Model (one request = one aircraft, N = 1):
  *   At every 0.1 s step k of the requesting aircraft's trajectory (Fig 3a loop P:272-289)
@@ -15,7 +15,8 @@
  *             around p_j + v_j tau                   (Alg 7, Table PK)
  *       V^T = max over terrain wells of [d < R] 1000 * .99^d   (Alg 6, Table PK)
  *       V_alt = 1000 - z if z < deck else 0          (Alg 1, R6/R7)
- *   V*(a) = max_t V(a,t) (Alg 8), a* = argmax (Alg 9, lowest index on ties),
+ *   V*(a) = max_t V(a,t) (Alg 8; airspace.valuation = 1: V(a,W), Alg 1),
+ *   a* = argmax (Alg 9, lowest index on ties),
  *   the aircraft advances one substep along a* (Alg 1), and the terminal state is
  *   determined (Sec IV.I): separation conflict with any accepted plan (exact),
  *   terrain, goal capture, timeout.  An accepted trajectory is appended to the plan store
