@@ -230,6 +230,38 @@ fmdp_status fmdp_schedule_sharded(fmdp_ctx* ctx, const fmdp_shard* shard, uint64
                                   fmdp_vec3 dst, int64_t t0_step, fmdp_result* res, fmdp_qpos* traj,
                                   int32_t traj_cap);
 
+/* Plan-sharded multi-GPU scheduling, production form (SURVEY §8(e) "Mechanism"): the same
+ * partitioning and decisions as fmdp_schedule_sharded, but the per-step exchange runs INSIDE
+ * one persistent walker launch per request -- no host round-trip per step.  Each step every
+ * CTA of rank r stores its owned per-(projected state, tau) minima (FP32 bits) and the
+ * nearest-plan d^2 into slot [step parity][r] of every peer's exchange area (P2P stores over
+ * NVLink / NVSwitch), releases a step tag (st.relaxed.sys after fence.sys), acquires the peers'
+ * tags for the step (ld.acquire.sys) and takes the elementwise minimum; every rank then decides
+ * identically, so results are bit-identical to one GPU.
+ *
+ * Setup (collective, once, before any fmdp_schedule_p2p):
+ *   1. fmdp_p2p_export(ctx, world, &handle, &ptr): allocates this rank's exchange area
+ *      (cudaMalloc, zeroed: 2*world*16 tags + 2*world*(A*W*5+16) words) and returns its CUDA
+ *      IPC handle (64 bytes; zeroed if IPC is unavailable) and its device pointer.
+ *   2. exchange (handle, ptr) among the ranks (e.g. torch.distributed.all_gather_object).
+ *   3. fmdp_p2p_connect(ctx, rank, world, handles[world], ptrs[world]): peer q's area is
+ *      ptrs[q] when ptrs != NULL and ptrs[q] != NULL (the same process: contexts on one or
+ *      several devices; peer access is enabled), else cudaIpcOpenMemHandle(handles[q]).
+ *      Resets this rank's tags; every rank must connect before any rank schedules.
+ * fmdp_schedule_p2p: collective -- every rank calls it with the same request, on identical
+ * stores and launch settings (the cluster size must agree), concurrently (the walkers wait for
+ * each other every step).  A peer that does not arrive within ~2 s makes the call return
+ * FMDP_E_CUDA ("peer exchange timed out"); export and connect again before the next call.
+ * world <= 8. */
+typedef struct fmdp_p2p_handle {
+  unsigned char bytes[64];
+} fmdp_p2p_handle;
+fmdp_status fmdp_p2p_export(fmdp_ctx* ctx, int32_t world, fmdp_p2p_handle* handle, void** dev_ptr);
+fmdp_status fmdp_p2p_connect(fmdp_ctx* ctx, int32_t rank, int32_t world, const fmdp_p2p_handle* handles,
+                             void* const* dev_ptrs);
+fmdp_status fmdp_schedule_p2p(fmdp_ctx* ctx, uint64_t aircraft_id, fmdp_vec3 src, fmdp_vec3 dst, int64_t t0_step,
+                              fmdp_result* res, fmdp_qpos* traj, int32_t traj_cap);
+
 /* Departure-time candidates ("recommended take-off time"):
  * schedule one request for n_delays candidate departures t0_step + delays[i] in parallel, all
  * against the current store (the candidates are alternatives, they do not see each other);

@@ -84,6 +84,12 @@ struct fmdp_ctx {
   int cs_cap = 0;
   uint32_t* d_xbuf = nullptr;  // multi-GPU exchange buffer [A*W*NTAU + 1]
   int xmode = 0, shard_rank = 0, shard_world = 1;
+  // in-kernel multi-GPU exchange (fmdp_p2p_*): own area, peer table, step-tag sequence
+  void* x_area = nullptr;
+  int x_world = 0, x_me = -1, x_slot = 0;
+  std::vector<void*> x_ipc;                // IPC-opened peer areas
+  fmdp::XPeer* d_xpeers = nullptr;         // [XMAX]
+  unsigned long long* d_xseq = nullptr;    // [1] sequence, then [1] int32 error flag
   double *d_dbg_vstar = nullptr, *d_dbg_v = nullptr, *d_dbg_s = nullptr;
   uint32_t* d_dbg_conf = nullptr;
   int32_t* d_dbg_astar = nullptr;
@@ -130,6 +136,16 @@ void* dalloc(fmdp_ctx* ctx, size_t bytes) {
   }
   if (p) ctx->allocs.push_back(p);
   return p;
+}
+
+// Close the IPC-opened peer areas and free this rank's exchange area (fmdp_p2p_*).
+void x_release(fmdp_ctx* ctx) {
+  for (void* p : ctx->x_ipc) cudaIpcCloseMemHandle(p);
+  ctx->x_ipc.clear();
+  if (ctx->x_area) cudaFree(ctx->x_area);
+  ctx->x_area = nullptr;
+  ctx->x_world = 0;
+  ctx->x_me = -1;
 }
 
 void dfree(fmdp_ctx* ctx, void* p) {
@@ -268,7 +284,7 @@ double mean_plans(const fmdp_ctx* ctx) {
   int64_t tot = 0, nz = 0;
   for (int32_t c : ctx->counts)
     if (c) { tot += c; ++nz; }
-  return nz ? (double)tot / nz : 0.0;
+  return nz ? (double)tot / nz / ctx->shard_world : 0.0;  // plans per row this GPU evaluates
 }
 
 // Cluster size for a round of n_run trajectories: the G minimising waves(G) * t(G) among the
@@ -339,6 +355,12 @@ fmdp::WalkArgs make_args(fmdp_ctx* ctx, const std::vector<Req>& run, bool eval, 
   a.shard_rank = ctx->shard_rank;
   a.shard_world = ctx->shard_world;
   a.xbuf = ctx->d_xbuf;
+  a.x_me = ctx->x_me;
+  a.x_world = ctx->x_world;
+  a.x_slot = ctx->x_slot;
+  a.x_peers = ctx->d_xpeers;
+  a.x_seq = ctx->d_xseq;
+  a.x_err = ctx->d_xseq ? reinterpret_cast<int32_t*>(ctx->d_xseq + 1) : nullptr;
   a.dbg_vstar = ctx->d_dbg_vstar;
   a.dbg_v = ctx->d_dbg_v;
   a.dbg_s = ctx->d_dbg_s;
@@ -1036,6 +1058,7 @@ void fmdp_destroy(fmdp_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  x_release(ctx);
   std::vector<void*> a = ctx->allocs;
   for (void* p : a) dfree(ctx, p);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -1150,6 +1173,31 @@ fmdp_status fmdp_schedule(fmdp_ctx* ctx, uint64_t aircraft_id, fmdp_vec3 src, fm
   return schedule_many(ctx, &r, 1, res, traj, traj_cap, FMDP_BATCH_SEQUENTIAL);
 }
 
+// Result of a single-request walk (sharded paths): commit if accepted, fill res, copy traj.
+fmdp_status finish_single(fmdp_ctx* ctx, const std::vector<Req>& base, uint64_t aircraft_id, fmdp_result* res,
+                          fmdp_qpos* traj) {
+  fmdp_status st = FMDP_OK;
+  const Out& o = ctx->h_out[0];
+  std::vector<uint32_t> plan_id(1, 0xffffffffu);
+  std::vector<uint64_t> aircraft(1, aircraft_id);
+  if (o.status == FMDP_ACCEPTED && (st = commit_slots(ctx, {0}, base, aircraft, plan_id))) return st;
+  res->status = o.status;
+  res->plan_id = plan_id[0];
+  res->n_states = o.n_states;
+  res->fail_step = o.fail_step;
+  res->min_sep_m = std::sqrt((double)o.min_sep_d2) * ctx->air.u_m;
+  res->n_near_ties = o.n_near_ties;
+  res->n_exact = o.n_exact;
+  if (traj) {
+    CK(cudaMemcpy(traj, ctx->d_traj, sizeof(fmdp_qpos) * o.n_states, cudaMemcpyDeviceToHost));
+  }
+  unsigned long long pc = 0;
+  CK(cudaMemcpy(&pc, ctx->d_pairctr, sizeof(pc), cudaMemcpyDeviceToHost));
+  ctx->stats.pair_evals = (int64_t)pc;
+  ctx->last_n = 1;
+  return FMDP_OK;
+}
+
 fmdp_status fmdp_schedule_sharded(fmdp_ctx* ctx, const fmdp_shard* shard, uint64_t aircraft_id, fmdp_vec3 src,
                                   fmdp_vec3 dst, int64_t t0_step, fmdp_result* res, fmdp_qpos* traj,
                                   int32_t traj_cap) {
@@ -1202,25 +1250,125 @@ fmdp_status fmdp_schedule_sharded(fmdp_ctx* ctx, const fmdp_shard* shard, uint64
   }
   ctx->shard_rank = 0;
   ctx->shard_world = 1;
-  const Out& o = ctx->h_out[0];
-  std::vector<uint32_t> plan_id(1, 0xffffffffu);
-  std::vector<uint64_t> aircraft(1, aircraft_id);
-  if (o.status == FMDP_ACCEPTED && (st = commit_slots(ctx, {0}, base, aircraft, plan_id))) return st;
-  res->status = o.status;
-  res->plan_id = plan_id[0];
-  res->n_states = o.n_states;
-  res->fail_step = o.fail_step;
-  res->min_sep_m = std::sqrt((double)o.min_sep_d2) * ctx->air.u_m;
-  res->n_near_ties = o.n_near_ties;
-  res->n_exact = o.n_exact;
-  if (traj) {
-    CK(cudaMemcpy(traj, ctx->d_traj, sizeof(fmdp_qpos) * o.n_states, cudaMemcpyDeviceToHost));
+  return finish_single(ctx, base, aircraft_id, res, traj);
+}
+
+// ----------------------------------------------------------------------------- in-kernel exchange
+fmdp_status fmdp_p2p_export(fmdp_ctx* ctx, int32_t world, fmdp_p2p_handle* handle, void** dev_ptr) {
+  if (!ctx || !handle || world < 1 || world > fmdp::XMAX) return fail(ctx, FMDP_E_ARG, "world must be 1..8");
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  x_release(ctx);
+  if (!ctx->d_xpeers) {
+    ctx->d_xpeers = (fmdp::XPeer*)dalloc(ctx, sizeof(fmdp::XPeer) * fmdp::XMAX);
+    ctx->d_xseq = (unsigned long long*)dalloc(ctx, 2 * sizeof(unsigned long long));
+    if (!ctx->d_xpeers || !ctx->d_xseq) return fail(ctx, FMDP_E_NOMEM, "exchange tables");
   }
-  unsigned long long pc = 0;
-  CK(cudaMemcpy(&pc, ctx->d_pairctr, sizeof(pc), cudaMemcpyDeviceToHost));
-  ctx->stats.pair_evals = (int64_t)pc;
-  ctx->last_n = 1;
+  const int slot = ((ctx->A * ctx->W * fmdp::NTAU + 16) + 3) & ~3;
+  const size_t bytes = fmdp::x_area_bytes(world, slot);
+  if (cudaMalloc(&ctx->x_area, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    ctx->x_area = nullptr;
+    return fail(ctx, FMDP_E_NOMEM, "exchange area");
+  }
+  CK(cudaMemset(ctx->x_area, 0, bytes));
+  ctx->x_world = world;
+  ctx->x_slot = slot;
+  static_assert(sizeof(cudaIpcMemHandle_t) == sizeof(handle->bytes), "IPC handle size");
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, ctx->x_area) == cudaSuccess) {
+    std::memcpy(handle->bytes, &h, sizeof(h));
+  } else {  // no IPC here: in-process peers (dev_ptrs) still work
+    cudaGetLastError();
+    std::memset(handle->bytes, 0, sizeof(handle->bytes));
+  }
+  if (dev_ptr) *dev_ptr = ctx->x_area;
   return FMDP_OK;
+}
+
+fmdp_status fmdp_p2p_connect(fmdp_ctx* ctx, int32_t rank, int32_t world, const fmdp_p2p_handle* handles,
+                             void* const* dev_ptrs) {
+  if (!ctx) return FMDP_E_ARG;
+  if (!ctx->x_area || world != ctx->x_world) return fail(ctx, FMDP_E_ARG, "fmdp_p2p_export(world) first");
+  if (rank < 0 || rank >= world) return fail(ctx, FMDP_E_ARG, "rank out of range");
+  CK(cudaSetDevice(ctx->device));
+  for (void* p : ctx->x_ipc) cudaIpcCloseMemHandle(p);
+  ctx->x_ipc.clear();
+  ctx->x_me = -1;
+  const size_t flag_bytes = (size_t)2 * world * 16 * sizeof(unsigned long long);
+  std::vector<fmdp::XPeer> tab(fmdp::XMAX, fmdp::XPeer{nullptr, nullptr});
+  for (int q = 0; q < world; ++q) {
+    void* base = nullptr;
+    if (q == rank) {
+      base = ctx->x_area;
+    } else if (dev_ptrs && dev_ptrs[q]) {
+      base = dev_ptrs[q];
+      cudaPointerAttributes at{};
+      CK(cudaPointerGetAttributes(&at, base));
+      if (at.device != ctx->device) {
+        int ok = 0;
+        CK(cudaDeviceCanAccessPeer(&ok, ctx->device, at.device));
+        if (!ok) return fail(ctx, FMDP_E_CUDA, "no peer access between the devices");
+        const cudaError_t e = cudaDeviceEnablePeerAccess(at.device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+          return fail(ctx, FMDP_E_CUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+        cudaGetLastError();
+      }
+    } else {
+      if (!handles) return fail(ctx, FMDP_E_ARG, "peer handle missing");
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, handles[q].bytes, sizeof(h));
+      CK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+      ctx->x_ipc.push_back(base);
+    }
+    tab[q].flag = reinterpret_cast<unsigned long long*>(base);
+    tab[q].recv = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(base) + flag_bytes);
+  }
+  CK(cudaMemcpy(ctx->d_xpeers, tab.data(), sizeof(fmdp::XPeer) * fmdp::XMAX, cudaMemcpyHostToDevice));
+  CK(cudaMemset(ctx->d_xseq, 0, 2 * sizeof(unsigned long long)));
+  CK(cudaMemset(ctx->x_area, 0, flag_bytes));  // this rank's tags restart with the sequence
+  CK(cudaDeviceSynchronize());
+  ctx->x_me = rank;
+  return FMDP_OK;
+}
+
+fmdp_status fmdp_schedule_p2p(fmdp_ctx* ctx, uint64_t aircraft_id, fmdp_vec3 src, fmdp_vec3 dst, int64_t t0_step,
+                              fmdp_result* res, fmdp_qpos* traj, int32_t traj_cap) {
+  if (!ctx || !res) return fail(ctx, FMDP_E_ARG, "null argument");
+  if (ctx->x_me < 0) return fail(ctx, FMDP_E_ARG, "fmdp_p2p_connect first");
+  if (traj && traj_cap < ctx->w.max_steps + 1) return fail(ctx, FMDP_E_BUFFER, "traj_cap must be >= max_steps + 1");
+  CK(cudaSetDevice(ctx->device));
+  std::memset(&ctx->stats, 0, sizeof(ctx->stats));
+  fmdp_request rq;
+  rq.aircraft_id = aircraft_id;
+  rq.src = src;
+  rq.dst = dst;
+  rq.t0_step = t0_step;
+  std::vector<Req> base;
+  fmdp_status st = prepare_requests(ctx, &rq, 1, base);
+  if (st) return st;
+  if ((st = ensure_slots(ctx, 1))) return st;
+  CK(cudaMemsetAsync(ctx->d_pairctr, 0, sizeof(unsigned long long), ctx->stream));
+  ctx->shard_rank = ctx->x_me;
+  ctx->shard_world = ctx->x_world;
+  ctx->xmode = 3;
+  const int G = solo_cluster_size(ctx);  // identical on every rank (identical stores, settings)
+  const fmdp::WalkArgs a = make_args(ctx, base, false, INT_MAX);
+  st = run_walk(ctx, base, false, INT_MAX, &a, G, 1);
+  ctx->xmode = 0;
+  ctx->shard_rank = 0;
+  ctx->shard_world = 1;
+  if (st) return st;
+  int32_t xerr = 0;
+  CK(cudaMemcpy(&xerr, ctx->d_xseq + 1, sizeof(xerr), cudaMemcpyDeviceToHost));
+  if (xerr) {
+    ctx->x_me = -1;
+    return fail(ctx, FMDP_E_CUDA, "peer exchange timed out (a rank did not call fmdp_schedule_p2p)");
+  }
+  if ((st = fetch_out(ctx, 1))) return st;
+  ctx->stats.steps += ctx->h_out[0].steps_run;
+  ctx->stats.rounds += 1;
+  return finish_single(ctx, base, aircraft_id, res, traj);
 }
 
 // Co-simulated batch: one cluster per request, all resident at once (they wait for

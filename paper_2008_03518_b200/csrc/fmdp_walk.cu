@@ -1,6 +1,6 @@
 // fmdp_walk.cu -- sm_100a kernels of the FastMDP-GPU hot path.
 //
-// walk_kernel<C, CS>: one thread-block CLUSTER of G CTAs walks one request's whole trajectory
+// walk_kernel<C, MODE>: one thread-block CLUSTER of G CTAs walks one request's whole trajectory
 // (Fig 3a loop) with no host round trip per step; clusters take requests from
 // a device queue.  Per decision step k (clock row K = t0 + k):
 //   a1  stage the CTA's slice of row K (and prefetch row K+2) with cp.async.bulk (TMA)
@@ -292,6 +292,74 @@ __device__ __noinline__ bool cs_idle(int4* pub_all, unsigned* arrive, int32_t* e
   return true;
 }
 
+// ----------------------------------------------------------------------------- multi-GPU exchange
+// In-kernel plan-sharded step exchange (xmode 3, SURVEY §8(e) production form).  Every rank runs
+// the same persistent walker over its shard of every time row; per step each CTA has stored its
+// owned per-(state, tau) minima into every peer's receive slot (P2P stores, NVLink) before
+// calling this.  Here it adds its nearest-plan d^2, releases the step tag to every peer
+// (bar.sync + fence.sys + relaxed.sys store: the CTA's stores are ordered before the tag) and
+// acquires the peers' tags for this step.  Two parities suffice: a rank writes tag s+2 into a
+// peer's parity-s slot only after it saw the peer's tag s+1, which the peer releases after it
+// finished reading its slot of tag s.  A wait longer than ~2 s (a peer is not running) sets
+// *err and every later wait returns at once: the walk then ends with wrong values and the host
+// reports FMDP_E_CUDA.  All threads of one CTA; returns the minimum d^2 over the ranks.
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __noinline__ uint32_t x_exchange(const XPeer* peers, int me, int world, int slot, unsigned cta,
+                                            unsigned long long seq, uint32_t stay, int32_t* err) {
+  const int par = (int)(seq & 1ull);
+  const size_t mine = (size_t)(par * world + me);
+  if (threadIdx.x == 0)
+    for (int q = 0; q < world; ++q)
+      if (q != me) __stcg(peers[q].recv + mine * slot + (slot - 16) + cta, stay);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int q = 0; q < world; ++q)
+      if (q != me) st_relaxed_sys_u64(peers[q].flag + mine * 16 + cta, seq);
+    const unsigned long long* own = peers[me].flag;
+    for (int q = 0; q < world; ++q) {
+      if (q == me) continue;
+      const unsigned long long* f = own + (size_t)(par * world + q) * 16 + cta;
+      if (ld_acquire_sys_u64(f) >= seq) continue;
+      const long long t0 = clock64();
+      while (ld_acquire_sys_u64(f) < seq) {
+        if (*(volatile int32_t*)err) break;
+        if (clock64() - t0 > (4ll << 30)) {
+          atomicExch(err, 1);
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  uint32_t m = stay;
+  const uint32_t* rv = peers[me].recv;
+  for (int q = 0; q < world; ++q)
+    if (q != me) m = min(m, __ldcg(rv + (size_t)(par * world + q) * slot + (slot - 16) + cta));
+  return m;
+}
+
+// G-way minimum of one (state, tau) item over the partial blocks of the cluster's CTAs
+__device__ __forceinline__ float gway_min(const float* src, int G, int sstride) {
+  float M0 = src[0], M1 = FLT_MAX, M2 = FLT_MAX, M3 = FLT_MAX;
+  int bb = 1;
+  for (; bb + 3 < G; bb += 4) {  // four independent load streams
+    M0 = fminf(M0, src[bb * sstride]);
+    M1 = fminf(M1, src[(bb + 1) * sstride]);
+    M2 = fminf(M2, src[(bb + 2) * sstride]);
+    M3 = fminf(M3, src[(bb + 3) * sstride]);
+  }
+  for (; bb < G; ++bb) M0 = fminf(M0, src[bb * sstride]);
+  return fminf(fminf(M0, M1), fminf(M2, M3));
+}
+
 struct TauSteps {
   int k[NTAU];
 };
@@ -346,7 +414,7 @@ __device__ __noinline__ unsigned long long cs_exact_peers(const int4* pub, int n
 enum Phase { PH_PROJ, PH_FIX, PH_WAIT, PH_HOT, PH_STAGE, PH_SCATTER, PH_BAR1, PH_OWNER, PH_BAR2, PH_DECIDE,
              PH_TOP, PH_SCAN, PH_PLOOP, PH_BUILD, PH_OWN1, PH_ARGMAX, PH_FLAGS, PH_N };
 
-template <int C, bool CS>
+template <int C, int MODE>
 __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
     walk_kernel(const World w, const WalkArgs args, const int CH, const int RAWCAP, const int NGW) {
   cg::cluster_group cluster = cg::this_cluster();
@@ -401,10 +469,14 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   }
   // plan-sharded multi-GPU step: xmode 1 exports this GPU's per-(state, tau)
   // minima and nearest-plan distance, xmode 2 imports their all-reduced minimum and decides
-  const int xmode = args.xmode;
+  // MODE 2: in-kernel exchange with the peer GPUs (xmode 3), no host round-trip per step
+  constexpr bool XP = MODE == 2;
+  const int xmode = XP ? 3 : args.xmode;
   // SURVEY f2 co-simulated batch: a separate instantiation, so the FCFS walker carries no
   // co-simulation code at all (measured: any of it on the step path costs ~1.5 %)
-  const int cosim = CS ? 1 : 0;
+  const int cosim = MODE == 1 ? 1 : 0;
+  const unsigned long long xseq0 = XP ? *args.x_seq : 0ull;  // step tags continue across launches
+  unsigned long long xit = 0;
 
   const bool prof = args.prof != nullptr && rank == 0 && tid == 0;
   unsigned long long pacc[PH_N];
@@ -902,6 +974,27 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           if (b < (int)G) stay_all = min(stay_all, s_stay[p * 16 + b]);
       }
       if (xmode == 1 && rank == 0 && tid == 0) args.xbuf[NTAU * AW] = stay_all;
+      if (XP) {
+        // this GPU's minima of the owned items -> every peer's receive slot, then
+        // the step tag; the minima over all ranks are taken in pass 1 below
+        __syncthreads();  // s_stage (s_M) is free once every thread of this CTA has pushed its blocks
+        ++xit;
+        const unsigned long long seq = xseq0 + xit;
+        if (!fin) {
+          const float* rcv = s_recv + p * (int)G * NOWN * BLK;
+          const size_t xo = (size_t)((int)(seq & 1ull) * args.x_world + args.x_me) * args.x_slot;
+          const int nitem = n_own * W * NTAU;
+          for (int i = tid; i < nitem; i += NT) {
+            const int oa = i / (W * NTAU), r2 = i - oa * (W * NTAU);
+            const int st = ((int)rank + oa * (int)G) * W + r2 / NTAU;
+            const float M = gway_min(rcv + oa * BLK + r2, (int)G, NOWN * BLK);
+            s_stage[i] = M;
+            for (int q = 0; q < args.x_world; ++q)
+              if (q != args.x_me) __stcg(args.x_peers[q].recv + xo + st * NTAU + r2 % NTAU, __float_as_uint(M));
+          }
+        }
+        stay_all = x_exchange(args.x_peers, args.x_me, args.x_world, args.x_slot, rank, seq, stay_all, args.x_err);
+      }
 
       if (!fin) {
         // ---- owner epilogue (half-warp per owned action, lane = substep): G-way minimum of
@@ -921,19 +1014,14 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           float M;
           if (xmode == 2) {
             M = __uint_as_float(args.xbuf[st * NTAU + t]);
+          } else if (XP) {  // minimum over the ranks (this GPU's from pass 1a)
+            M = s_M[i];
+            const uint32_t* rv = args.x_peers[args.x_me].recv + st * NTAU + t;
+            for (int q = 0; q < args.x_world; ++q)
+              if (q != args.x_me)
+                M = fminf(M, __uint_as_float(__ldcg(rv + (size_t)((int)((xseq0 + xit) & 1ull) * args.x_world + q) * args.x_slot)));
           } else {
-            const int sstride = NOWN * BLK;
-            const float* src = rcv + oa * BLK + r2;
-            float M0 = src[0], M1 = FLT_MAX, M2 = FLT_MAX, M3 = FLT_MAX;
-            int bb = 1;
-            for (; bb + 3 < (int)G; bb += 4) {  // four independent load streams
-              M0 = fminf(M0, src[bb * sstride]);
-              M1 = fminf(M1, src[(bb + 1) * sstride]);
-              M2 = fminf(M2, src[(bb + 2) * sstride]);
-              M3 = fminf(M3, src[(bb + 3) * sstride]);
-            }
-            for (; bb < (int)G; ++bb) M0 = fminf(M0, src[bb * sstride]);
-            M = fminf(fminf(M0, M1), fminf(M2, M3));
+            M = gway_min(rcv + oa * BLK + r2, (int)G, NOWN * BLK);
             if (xmode == 1) args.xbuf[st * NTAU + t] = __float_as_uint(M);  // this GPU's minima
           }
           const int4 q4 = s_pos[st];
@@ -1154,6 +1242,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
 
     // ------------------------------------------------------------ request epilogue
     cluster.sync();  // n_exact contributions of every CTA have landed in rank 0
+    if (XP && rank == 0 && tid == 0) *args.x_seq = xseq0 + xit;  // read by the next launch
     if (rank == 0 && tid == 0 && rq.head && args.stop && status >= 0) atomicExch(args.stop, 1);
     if (rank == 0 && tid == 0 && !args.eval) {
       Out o;
@@ -1262,15 +1351,15 @@ int walk_threads(int ncol, int max_threads) {
   return 32 * ((ncol + cpw - 1) / cpw);
 }
 
-template <int C, bool CS>
+template <int C, int MODE>
 static cudaError_t launch_walk_t(const World& w, const WalkArgs& a, int cluster, int n_clusters, int threads,
                                  int chunk, int rawcap, cudaStream_t s) {
   Layout L;
   L.build(w.HL, chunk, rawcap, threads, C, w.n_turn * w.W, w.A, w.A * w.W, cluster);
-  cudaError_t e = cudaFuncSetAttribute(walk_kernel<C, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+  cudaError_t e = cudaFuncSetAttribute(walk_kernel<C, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
   if (cluster > 8) {
-    e = cudaFuncSetAttribute(walk_kernel<C, CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaFuncSetAttribute(walk_kernel<C, MODE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg = {};
@@ -1286,17 +1375,17 @@ static cudaError_t launch_walk_t(const World& w, const WalkArgs& a, int cluster,
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const int ngw = walk_groups_per_warp(w.n_turn * w.W, threads);
-  return cudaLaunchKernelEx(&cfg, walk_kernel<C, CS>, w, a, chunk, rawcap, ngw);
+  return cudaLaunchKernelEx(&cfg, walk_kernel<C, MODE>, w, a, chunk, rawcap, ngw);
 }
 
-template <int C, bool CS>
+template <int C, int MODE>
 static cudaError_t max_clusters_t(const World& w, int cluster, int threads, int chunk, int rawcap, int* out) {
   Layout L;
   L.build(w.HL, chunk, rawcap, threads, C, w.n_turn * w.W, w.A, w.A * w.W, cluster);
-  cudaError_t e = cudaFuncSetAttribute(walk_kernel<C, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+  cudaError_t e = cudaFuncSetAttribute(walk_kernel<C, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
   if (cluster > 8) {
-    e = cudaFuncSetAttribute(walk_kernel<C, CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaFuncSetAttribute(walk_kernel<C, MODE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg = {};
@@ -1310,32 +1399,37 @@ static cudaError_t max_clusters_t(const World& w, int cluster, int threads, int 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaOccupancyMaxActiveClusters(out, walk_kernel<C, CS>, &cfg);
+  return cudaOccupancyMaxActiveClusters(out, walk_kernel<C, MODE>, &cfg);
 }
 
 cudaError_t launch_walk(const World& w, const WalkArgs& a, int n_climb, int cluster, int n_clusters, int threads,
                         int chunk, int rawcap, cudaStream_t s) {
-  const bool cs = a.cosim != 0;
-  switch (n_climb) {
-    case 1: return cs ? launch_walk_t<1, true>(w, a, cluster, n_clusters, threads, chunk, rawcap, s)
-                      : launch_walk_t<1, false>(w, a, cluster, n_clusters, threads, chunk, rawcap, s);
-    case 3: return cs ? launch_walk_t<3, true>(w, a, cluster, n_clusters, threads, chunk, rawcap, s)
-                      : launch_walk_t<3, false>(w, a, cluster, n_clusters, threads, chunk, rawcap, s);
-    case 5: return cs ? launch_walk_t<5, true>(w, a, cluster, n_clusters, threads, chunk, rawcap, s)
-                      : launch_walk_t<5, false>(w, a, cluster, n_clusters, threads, chunk, rawcap, s);
+  const int mode = a.cosim ? 1 : (a.xmode == 3 ? 2 : 0);
+#define FMDP_LW(c, m) launch_walk_t<c, m>(w, a, cluster, n_clusters, threads, chunk, rawcap, s)
+  switch (n_climb * 4 + mode) {
+    case 4: return FMDP_LW(1, 0);
+    case 5: return FMDP_LW(1, 1);
+    case 6: return FMDP_LW(1, 2);
+    case 12: return FMDP_LW(3, 0);
+    case 13: return FMDP_LW(3, 1);
+    case 14: return FMDP_LW(3, 2);
+    case 20: return FMDP_LW(5, 0);
+    case 21: return FMDP_LW(5, 1);
+    case 22: return FMDP_LW(5, 2);
     default: return cudaErrorInvalidValue;
   }
+#undef FMDP_LW
 }
 
 cudaError_t walk_max_clusters(const World& w, int n_climb, int cluster, int threads, int chunk, int rawcap, int* out,
                               bool cosim) {
   switch (n_climb) {
-    case 1: return cosim ? max_clusters_t<1, true>(w, cluster, threads, chunk, rawcap, out)
-                         : max_clusters_t<1, false>(w, cluster, threads, chunk, rawcap, out);
-    case 3: return cosim ? max_clusters_t<3, true>(w, cluster, threads, chunk, rawcap, out)
-                         : max_clusters_t<3, false>(w, cluster, threads, chunk, rawcap, out);
-    case 5: return cosim ? max_clusters_t<5, true>(w, cluster, threads, chunk, rawcap, out)
-                         : max_clusters_t<5, false>(w, cluster, threads, chunk, rawcap, out);
+    case 1: return cosim ? max_clusters_t<1, 1>(w, cluster, threads, chunk, rawcap, out)
+                         : max_clusters_t<1, 0>(w, cluster, threads, chunk, rawcap, out);
+    case 3: return cosim ? max_clusters_t<3, 1>(w, cluster, threads, chunk, rawcap, out)
+                         : max_clusters_t<3, 0>(w, cluster, threads, chunk, rawcap, out);
+    case 5: return cosim ? max_clusters_t<5, 1>(w, cluster, threads, chunk, rawcap, out)
+                         : max_clusters_t<5, 0>(w, cluster, threads, chunk, rawcap, out);
     default: return cudaErrorInvalidValue;
   }
 }

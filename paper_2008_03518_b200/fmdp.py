@@ -85,6 +85,10 @@ class Shard(C.Structure):
     _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("allreduce_min_u32", ALLREDUCE_FN), ("user", C.c_void_p)]
 
 
+class P2PHandle(C.Structure):
+    _fields_ = [("bytes", C.c_ubyte * 64)]
+
+
 class Stats(C.Structure):
     _fields_ = [("steps", C.c_int64), ("pair_evals", C.c_int64), ("rounds", C.c_int32), ("reruns", C.c_int32),
                 ("cluster_size", C.c_int32), ("walkers", C.c_int32), ("kernels", C.c_int32),
@@ -96,6 +100,7 @@ PHASES = ("projection", "goal_terrain", "row_wait", "hot_loop", "stage", "reduce
 
 EXPORTS = ["fmdp_airspace_default", "fmdp_create", "fmdp_destroy", "fmdp_set_launch", "fmdp_add_plan",
            "fmdp_add_plans", "fmdp_schedule", "fmdp_schedule_batch", "fmdp_schedule_sharded",
+           "fmdp_p2p_export", "fmdp_p2p_connect", "fmdp_schedule_p2p",
            "fmdp_schedule_departures", "fmdp_schedule_cosim", "fmdp_cosim_max", "fmdp_get_steplog", "fmdp_get_plan",
            "fmdp_num_plans", "fmdp_truncate", "fmdp_eval_step", "fmdp_get_stats", "fmdp_num_actions",
            "fmdp_strerror", "fmdp_last_error"]
@@ -127,6 +132,9 @@ def lib():
         L.fmdp_cosim_max.restype = i32
         L.fmdp_schedule_sharded.argtypes = [vp, C.POINTER(Shard), C.c_uint64, Vec3, Vec3, i64, C.POINTER(Result), vp,
                                             i32]
+        L.fmdp_p2p_export.argtypes = [vp, i32, C.POINTER(P2PHandle), C.POINTER(vp)]
+        L.fmdp_p2p_connect.argtypes = [vp, i32, i32, vp, vp]
+        L.fmdp_schedule_p2p.argtypes = [vp, C.c_uint64, Vec3, Vec3, i64, C.POINTER(Result), vp, i32]
         L.fmdp_get_steplog.argtypes = [vp, i32, vp, vp, vp, i32, C.POINTER(i32)]
         L.fmdp_get_plan.argtypes = [vp, C.c_uint32, C.POINTER(i64), vp, i32, C.POINTER(i32)]
         L.fmdp_num_plans.argtypes = [vp, C.POINTER(C.c_uint32)]
@@ -376,6 +384,34 @@ class FMDP:
                                                  int(t0), C.byref(r), _p(traj), cap), "fmdp_schedule_sharded")
         return self._res(r, traj)
 
+    def p2p_export(self, world: int):
+        """Allocate this rank's in-kernel exchange area; returns (64-byte IPC handle, device pointer)."""
+        h = P2PHandle()
+        ptr = C.c_void_p()
+        self._check(self.L.fmdp_p2p_export(self.ctx, int(world), C.byref(h), C.byref(ptr)), "fmdp_p2p_export")
+        return bytes(h.bytes), int(ptr.value or 0)
+
+    def p2p_connect(self, rank: int, world: int, handles, ptrs=None):
+        """Attach the peers' exchange areas: ``ptrs[q]`` (same process) where given and non-zero,
+        else the IPC handle ``handles[q]``."""
+        hs = (P2PHandle * world)()
+        for q, hb in enumerate(handles):
+            C.memmove(hs[q].bytes, bytes(hb), 64)
+        pp = (C.c_void_p * world)(*[(ptrs[q] or None) if ptrs is not None else None for q in range(world)])
+        self._check(self.L.fmdp_p2p_connect(self.ctx, int(rank), int(world), C.cast(hs, C.c_void_p),
+                                            C.cast(pp, C.c_void_p) if ptrs is not None else None),
+                    "fmdp_p2p_connect")
+
+    def schedule_p2p(self, src, dst, t0: int, aircraft_id: int = 0, want_traj: bool = True) -> ScheduleResult:
+        """Plan-sharded request with the per-step exchange inside the walker kernel (SURVEY §8(e)
+        production form).  Collective: every connected rank calls it with the same request."""
+        cap = self.max_steps + 1
+        traj = np.zeros((cap, 3), np.int32) if want_traj else None
+        r = Result()
+        self._check(self.L.fmdp_schedule_p2p(self.ctx, aircraft_id, self._vec(src), self._vec(dst), int(t0),
+                                             C.byref(r), _p(traj), cap), "fmdp_schedule_p2p")
+        return self._res(r, traj)
+
     def schedule_departures(self, src, dst, t0: int, delays, aircraft_id: int = 0, want_traj: bool = True):
         """SURVEY f3: candidate departures t0 + delays[i] in parallel against the current store;
         returns (results, chosen index or -1); the chosen candidate is appended."""
@@ -435,3 +471,28 @@ def allreduce_min_torch(group=None, device=None):
         dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
         arr[:] = t.cpu().numpy().astype(np.uint32)
     return f
+
+
+def p2p_connect_local(ctxs: Sequence["FMDP"]):
+    """Connect contexts of THIS process (one per rank; on one or several devices) for
+    ``schedule_p2p``: the peers' exchange areas are passed as device pointers."""
+    world = len(ctxs)
+    ex = [c.p2p_export(world) for c in ctxs]
+    for r, c in enumerate(ctxs):
+        c.p2p_connect(r, world, [h for h, _ in ex], [p for _, p in ex])
+
+
+def p2p_connect_group(ctx: "FMDP", group=None):
+    """Connect this process's context with the other ranks of a torch.distributed group (one
+    process per GPU): exchange areas are shared by CUDA IPC handles (pointers when two ranks
+    live in one process).  Collective; ends with a barrier so no rank schedules early."""
+    import os as _os
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    h, p = ctx.p2p_export(world)
+    info = [None] * world
+    dist.all_gather_object(info, (h, p, _os.getpid()), group=group)
+    pid = _os.getpid()
+    ptrs = [pp if (q == rank or ppid == pid) else 0 for q, (_, pp, ppid) in enumerate(info)]
+    ctx.p2p_connect(rank, world, [hh for hh, _, _ in info], ptrs)
+    dist.barrier(group=group)

@@ -48,3 +48,45 @@ def test_gloo_allreduce_min_and_timing(tmp_path):
         assert (got == want).all() and got.dtype == np.uint32
         t, tot = np.load(tmp_path / f"t{r}.npy")
         assert t == world and tot == 100.0 * world
+
+
+class _FakeCtx:
+    """Stands in for FMDP: records what p2p_connect_group hands to the library."""
+
+    def __init__(self, rank):
+        self.rank = rank
+        self.got = None
+
+    def p2p_export(self, world):
+        return bytes([self.rank + 1]) * 64, 0x1000 * (self.rank + 1)
+
+    def p2p_connect(self, rank, world, handles, ptrs):
+        self.got = (rank, world, [h[0] for h in handles], list(ptrs))
+
+
+def _connect_worker(rank, world, port, out_dir):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2008_03518_b200.fmdp import p2p_connect_group
+    c = _FakeCtx(rank)
+    p2p_connect_group(c)
+    r, w, hs, ps = c.got
+    np.save(os.path.join(out_dir, f"c{rank}.npy"), np.array([r, w] + hs + ps, dtype=np.int64))
+    dist.destroy_process_group()
+
+
+def test_gloo_p2p_connect_group_exchanges_handles(tmp_path):
+    """In-kernel exchange setup: every rank receives every rank's IPC handle in
+    rank order; a peer in another process is reached through its handle (pointer 0), its own
+    area through its own pointer."""
+    world = 2
+    mp.spawn(_connect_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        got = np.load(tmp_path / f"c{r}.npy").tolist()
+        assert got[:2] == [r, world]
+        assert got[2:4] == [1, 2]
+        want_ptrs = [0x1000 * (q + 1) if q == r else 0 for q in range(world)]
+        assert got[4:6] == want_ptrs

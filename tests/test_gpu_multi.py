@@ -78,3 +78,79 @@ def test_sharded_two_ranks_bit_identical(tmp_path):
         for i, w in enumerate(want):
             assert st[i][0] == w.status and st[i][1] == w.n_states
             assert (np.load(tmp_path / f"t{r}_{i}.npy") == w.traj).all()
+
+
+# --------------------------------------------------------------------------- in-kernel exchange
+# fmdp_schedule_p2p (SURVEY §8(e) production form): the per-step exchange runs inside the walker
+# kernels through the peers' exchange areas.  On one GPU the "ranks" are contexts of this
+# process, each walker on its own stream; the protocol (P2P stores, step tags, parity buffers)
+# is the one the NVLink peers use, only the pointers are local.
+
+def _p2p_ranks(sc, world, cull=0):
+    from paper_2008_03518_b200.fmdp import FMDP, p2p_connect_local
+    ctxs = []
+    for _ in range(world):
+        c = FMDP(sc.airspace, sc.terrain)
+        c.add_plans(sc.plans)
+        c.set_launch(cull=cull)
+        ctxs.append(c)
+    p2p_connect_local(ctxs)
+    return ctxs
+
+
+def _p2p_call(ctxs, src, dst, t0):
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(len(ctxs)) as ex:
+        futs = [ex.submit(c.schedule_p2p, src, dst, t0) for c in ctxs]
+        return [f.result(timeout=120) for f in futs]
+
+
+@pytest.mark.parametrize("world,cull", [(1, 0), (2, 0), (3, 1), (4, 0)])
+def test_p2p_bit_identical_to_one_gpu(world, cull):
+    from paper_2008_03518_b200.fmdp import FMDP
+    sc = _scenario()
+    ref = FMDP(sc.airspace, sc.terrain)
+    ref.add_plans(sc.plans)
+    ctxs = _p2p_ranks(sc, world, cull)
+    for i in range(sc.n_requests):
+        want = ref.schedule(sc.src[i], sc.dst[i], int(sc.t0[i]))
+        got = _p2p_call(ctxs, sc.src[i], sc.dst[i], int(sc.t0[i]))
+        for g in got:  # every rank took every decision identically, appended the same plan
+            assert g.status == want.status and g.n_states == want.n_states
+            assert (g.traj == want.traj).all()
+            assert g.min_sep_m == want.min_sep_m and g.plan_id == want.plan_id
+            assert g.n_near_ties == want.n_near_ties
+    assert all(c.num_plans() == ref.num_plans() for c in ctxs)
+    for c in ctxs + [ref]:
+        c.close()
+
+
+def test_p2p_shards_the_pairs():
+    """Each rank evaluates only its shard: pair evaluations sum to the single-GPU count."""
+    from paper_2008_03518_b200.fmdp import FMDP
+    sc = _scenario()
+    ref = FMDP(sc.airspace, sc.terrain)
+    ref.add_plans(sc.plans)
+    ref.schedule(sc.src[0], sc.dst[0], int(sc.t0[0]))
+    want = ref.stats()["pair_evals"]
+    ctxs = _p2p_ranks(sc, 2)
+    _p2p_call(ctxs, sc.src[0], sc.dst[0], int(sc.t0[0]))
+    got = [c.stats()["pair_evals"] for c in ctxs]
+    assert sum(got) == want and min(got) > 0.3 * want
+    for c in ctxs + [ref]:
+        c.close()
+
+
+def test_p2p_missing_peer_times_out_and_reconnects():
+    from paper_2008_03518_b200.fmdp import FmdpError, p2p_connect_local
+    sc = _scenario()
+    ctxs = _p2p_ranks(sc, 2)
+    with pytest.raises(FmdpError, match="timed out"):
+        ctxs[0].schedule_p2p(sc.src[0], sc.dst[0], int(sc.t0[0]))  # rank 1 never calls
+    with pytest.raises(FmdpError, match="connect"):
+        ctxs[0].schedule_p2p(sc.src[0], sc.dst[0], int(sc.t0[0]))
+    p2p_connect_local(ctxs)
+    ok = _p2p_call(ctxs, sc.src[1], sc.dst[1], int(sc.t0[1]))
+    assert ok[0].status == ok[1].status and (ok[0].traj == ok[1].traj).all()
+    for c in ctxs:
+        c.close()
