@@ -43,7 +43,17 @@ def parse():
     p.add_argument("--seed", type=int, default=2)
     p.add_argument("--cpu-sample-s", type=float, default=15.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-c4", action="store_true", help="skip the configs[3] 100k-plan latency block")
+    p.add_argument("--only-c4", action="store_true", help="run only the configs[3] block and print it")
     return p.parse_args()
+
+
+_T0 = time.perf_counter()
+
+
+def _log(msg: str):
+    """Progress on stderr (the JSON line alone goes to stdout)."""
+    print(f"[bench {time.perf_counter() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
 
 
 def dist_env():
@@ -340,11 +350,110 @@ def run_native(args):
                         "perf1): fmdp_synth.config_scaled, constant configs[1] density; device time of the walk",
                 "points": out}
 
+    def measure_c4(rank_counts=(2, 4), n_req=2):
+        # configs[3] (100k accepted plans): single-request latency of one context (full, culled) and
+        # of the plan-sharded in-kernel exchange (fmdp_schedule_p2p).  N = 1: the
+        # ranks are contexts on this GPU, each walker on its own stream -- the protocol of the
+        # NVLink peers (P2P stores, step tags), sharing this GPU's 148 SMs.  N > 1: one rank per
+        # GPU, exchange areas shared by CUDA IPC; device time, max over ranks.
+        from concurrent.futures import ThreadPoolExecutor
+        from paper_2008_03518_b200.fmdp import pack_plans, p2p_connect_group, p2p_connect_local
+        _log("c4: generating configs[3]")
+        sc4 = fs.config_c4(rows=1200)  # the same store on every rank
+        P = len(sc4.plans)
+        reqs = list(range(min(n_req, sc4.n_requests)))
+
+        packed = pack_plans(sc4.plans)
+
+        def mk():
+            c = FMDP(sc4.airspace, sc4.terrain, device=local)
+            c.add_plans_packed(*packed)
+            return c
+
+        def row(ms, steps, status, G):
+            return {"ms_per_request": ms / len(reqs), "us_per_step": ms * 1e3 / max(1, steps), "steps": steps,
+                    "status": status, "cluster_size": G}
+
+        def run_single(c, cull):
+            c.set_launch(cull=cull)
+            ms = steps = 0
+            st = []
+            for i in reqs:
+                r = c.schedule(sc4.src[i], sc4.dst[i], int(sc4.t0[i]), want_traj=False)
+                s_ = c.stats()
+                ms += s_["device_ms"]; steps += s_["steps"]; st.append(r.status)
+                c.truncate(P)
+            return row(ms, steps, st, s_["cluster_size"]), st
+
+        def run_p2p(cs, cull, n_world):
+            for c in cs:
+                c.set_launch(cull=cull)
+            ms = steps = 0
+            st = []
+            for i in reqs:
+                with ThreadPoolExecutor(len(cs)) as ex:
+                    rs = list(ex.map(lambda c: c.schedule_p2p(sc4.src[i], sc4.dst[i], int(sc4.t0[i]),
+                                                              want_traj=False), cs))
+                stats = [c.stats() for c in cs]
+                ms += max_over_ranks(max(s_["device_ms"] for s_ in stats), n_world)
+                steps += stats[0]["steps"]; st.append(rs[0].status)
+                for c in cs:
+                    c.truncate(P)
+            return row(ms, steps, st, stats[0]["cluster_size"]), st
+
+        out = {"what": "configs[3] single-request latency at 100k accepted plans; p2p = plan-sharded with the "
+                       "per-step exchange inside the walker kernel (fmdp_schedule_p2p)",
+               "plans": P, "rows": 1200, "requests": len(reqs)}
+        _log("c4: store ready")
+        base = mk()
+        _log("c4: context 0 loaded")
+        if world == 1:
+            out["single"] = {}
+            want = None
+            for cull in (0, 1):
+                out["single"]["culled" if cull else "full"], want = run_single(base, cull)
+                _log(f"c4: single cull={cull} {out['single']['culled' if cull else 'full']}")
+            out["ranks_are"] = "contexts on this one B200 (own stream each; they share its 148 SMs)"
+            ctxs = [base] + [mk() for _ in range(max(rank_counts) - 1)]
+            _log(f"c4: {len(ctxs)} contexts loaded")
+            out["p2p"] = []
+            for R in rank_counts:
+                p2p_connect_local(ctxs[:R])
+                e = {"ranks": R}
+                for cull in (0, 1):
+                    e["culled" if cull else "full"], st = run_p2p(ctxs[:R], cull, 1)
+                    _log(f"c4: p2p ranks={R} cull={cull} {e['culled' if cull else 'full']}")
+                    e["same_status_as_single"] = st == want
+                out["p2p"].append(e)
+            for c in ctxs:
+                c.close()
+        else:
+            out["ranks_are"] = f"{world} GPUs, one process each (CUDA IPC exchange areas, NVLink P2P stores)"
+            p2p_connect_group(base)
+            e = {"ranks": world}
+            for cull in (0, 1):
+                e["culled" if cull else "full"], _ = run_p2p([base], cull, world)
+            out["p2p"] = [e]
+            base.close()
+        return out
+
+    if args.only_c4:
+        out = measure_c4()
+        if rank == 0:
+            print(json.dumps({"c4_sharded": out}), flush=True)
+        return 0
+    _log("configs[1] batch, full path")
     M = measure(0)       # every (state, well) pair evaluated
+    _log("configs[1] batch, f1 culling")
     Mc = measure(1)      # exact culling, bit-identical outputs
+    _log("f3 departures")
     Md = measure_departures()
+    _log("f2 co-simulation")
     Mco = measure_cosim()
+    _log("latency vs plans")
     Mlat = measure_latency()
+    _log("configs[3] sharded latency")
+    Mc4 = None if args.no_c4 else measure_c4()
     h2d = n * C_REQUEST_BYTES
     tot_ms, value, e2e_value, d2h = M["tot_ms"], M["value"], M["e2e_value"], M["d2h"]
     stats = M["st_all"][-1]
@@ -385,7 +494,7 @@ def run_native(args):
         "roofline": {"bound": "alu", "achieved": achieved_tops, "peak": peak_tops, "unit": "Top/s",
                      "frac": achieved_tops / peak_tops, "traffic": traffic,
                      "traffic_source": "profiles/r01_traffic.json (ncu --set full, bytes per walk launch)",
-                     "kernel": "walk_kernel<3, false>", "ops_per_pair": OPS_PER_PAIR,
+                     "kernel": "walk_kernel<3, 0>", "ops_per_pair": OPS_PER_PAIR,
                      "ops_per_pair_basis": "algorithmic, SURVEY §8(d) d.3 (3 differences, 3 squares/fmas, 1 min)",
                      "pipe_frac": exec_tops / peak_tops, "exec_ops_per_pair": EXEC_OPS_PER_PAIR,
                      "loop_ceiling": "isolated hot loop saturates the FMA pipe at 34-36 pairs/clk/SM (register-"
@@ -408,6 +517,8 @@ def run_native(args):
         "f2_cosim": Mco,
         "latency_vs_plans": Mlat,
     }
+    if Mc4 is not None:
+        line["c4_sharded"] = Mc4
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(sc, args.cpu_sample_s)
     print(json.dumps(line), flush=True)

@@ -232,27 +232,29 @@ fmdp_status fmdp_schedule_sharded(fmdp_ctx* ctx, const fmdp_shard* shard, uint64
 
 /* Plan-sharded multi-GPU scheduling, production form (SURVEY §8(e) "Mechanism"): the same
  * partitioning and decisions as fmdp_schedule_sharded, but the per-step exchange runs INSIDE
- * one persistent walker launch per request -- no host round-trip per step.  Each step every
- * CTA of rank r stores its owned per-(projected state, tau) minima (FP32 bits) and the
- * nearest-plan d^2 into slot [step parity][r] of every peer's exchange area (P2P stores over
- * NVLink / NVSwitch), releases a step tag (st.relaxed.sys after fence.sys), acquires the peers'
- * tags for the step (ld.acquire.sys) and takes the elementwise minimum; every rank then decides
- * identically, so results are bit-identical to one GPU.
+ * one persistent walker launch per request -- no host round-trip per step.  Each step the owner
+ * CTA of every (projected state, tau) item on rank r stores {its minimum (FP32 bits), step tag}
+ * as ONE 8-byte word into slot [step parity][r] of every peer's exchange area (P2P stores over
+ * NVLink / NVSwitch) and polls its own area until the peers' words carry this step's tag (value
+ * and readiness arrive together: no fence, no flag); CTA 0 does the same for the nearest-plan
+ * distance and broadcasts the minimum over its cluster.  Every rank then decides identically,
+ * so results are bit-identical to one GPU.
  *
  * Setup (collective, once, before any fmdp_schedule_p2p):
  *   1. fmdp_p2p_export(ctx, world, &handle, &ptr): allocates this rank's exchange area
- *      (cudaMalloc, zeroed: 2*world*16 tags + 2*world*(A*W*5+16) words) and returns its CUDA
- *      IPC handle (64 bytes; zeroed if IPC is unavailable) and its device pointer.
+ *      (cudaMalloc, zeroed: 2 * world * (A*W*5 + 16) 8-byte words) and returns its CUDA IPC
+ *      handle (64 bytes; zeroed if IPC is unavailable) and its device pointer.
  *   2. exchange (handle, ptr) among the ranks (e.g. torch.distributed.all_gather_object).
  *   3. fmdp_p2p_connect(ctx, rank, world, handles[world], ptrs[world]): peer q's area is
  *      ptrs[q] when ptrs != NULL and ptrs[q] != NULL (the same process: contexts on one or
  *      several devices; peer access is enabled), else cudaIpcOpenMemHandle(handles[q]).
- *      Resets this rank's tags; every rank must connect before any rank schedules.
+ *      Resets this rank's area and tag sequence; every rank must connect before any rank
+ *      schedules.
  * fmdp_schedule_p2p: collective -- every rank calls it with the same request, on identical
  * stores and launch settings (the cluster size must agree), concurrently (the walkers wait for
- * each other every step).  A peer that does not arrive within ~2 s makes the call return
- * FMDP_E_CUDA ("peer exchange timed out"); export and connect again before the next call.
- * world <= 8. */
+ * each other every step).  A peer whose words do not arrive within ~2 s (~8 s for a launch's
+ * first step) makes the call return FMDP_E_CUDA ("peer exchange timed out"); the store is not
+ * changed; export and connect again before the next call.  world <= 8. */
 typedef struct fmdp_p2p_handle {
   unsigned char bytes[64];
 } fmdp_p2p_handle;

@@ -113,25 +113,24 @@ struct WalkArgs {
   int32_t* cs_err;              // set on a barrier timeout (walkers not co-resident)
   // in-kernel plan-sharded exchange (xmode 3, SURVEY §8(e) production form): one persistent
   // launch per request on every rank; per step each CTA stores its owned per-(state, tau) minima
-  // and the nearest-plan d^2 into every peer's receive slot (P2P stores over NVLink) and
-  // releases a step-tagged flag; see XPeer
+  // and the nearest-plan d^2 as {value, step tag} words into every peer's receive slot (P2P
+  // stores over NVLink) and polls its own slots for the peers' words; see XPeer
   int32_t x_me, x_world, x_slot;      // this rank, ranks, words per (parity, source) slot
   const XPeer* x_peers;             // [x_world] device table (entry x_me = this GPU's own area)
   unsigned long long* x_seq;          // this rank's exchange sequence number (step tags)
-  int32_t* x_err;                     // set on a flag-wait timeout (a peer is not running)
+  int32_t* x_err;                     // set on a poll timeout (a peer is not running)
 };
 
-// One rank's exchange area as seen from this GPU (peer pointers: IPC-opened or same process).
-//   flag[(par * world + src) * 16 + cta]: tag of the last step `src`'s CTA `cta` published
-//   recv[(par * world + src) * slot + i]: i < A*W*NTAU: FP32 bits of src's minimum for item i
-//                                         i = slot - 16 + cta: src's nearest-plan d^2
+// One rank's exchange area as seen from this GPU (peer pointer: IPC-opened or same process):
+//   recv[(par * world + src) * slot + i] = {value, step tag} (one 8-byte word, written by rank
+//   src with a single 64-bit store): i < A*W*NTAU: FP32 bits of src's minimum for (state, tau)
+//   item i; i = slot - 16 + cta: src's nearest-plan d^2 (CTA cta).
 struct XPeer {
-  uint32_t* recv;
-  unsigned long long* flag;
+  unsigned long long* recv;
 };
 constexpr int XMAX = 8;               // ranks of one exchange (one node)
 inline size_t x_area_bytes(int world, int slot) {
-  return (size_t)2 * world * 16 * sizeof(unsigned long long) + (size_t)2 * world * slot * sizeof(uint32_t);
+  return (size_t)2 * world * slot * sizeof(unsigned long long);
 }
 
 // Shared-memory carve-up, identical on host (size) and device (offsets).

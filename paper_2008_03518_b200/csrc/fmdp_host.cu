@@ -1295,8 +1295,7 @@ fmdp_status fmdp_p2p_connect(fmdp_ctx* ctx, int32_t rank, int32_t world, const f
   for (void* p : ctx->x_ipc) cudaIpcCloseMemHandle(p);
   ctx->x_ipc.clear();
   ctx->x_me = -1;
-  const size_t flag_bytes = (size_t)2 * world * 16 * sizeof(unsigned long long);
-  std::vector<fmdp::XPeer> tab(fmdp::XMAX, fmdp::XPeer{nullptr, nullptr});
+  std::vector<fmdp::XPeer> tab(fmdp::XMAX, fmdp::XPeer{nullptr});
   for (int q = 0; q < world; ++q) {
     void* base = nullptr;
     if (q == rank) {
@@ -1321,12 +1320,11 @@ fmdp_status fmdp_p2p_connect(fmdp_ctx* ctx, int32_t rank, int32_t world, const f
       CK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
       ctx->x_ipc.push_back(base);
     }
-    tab[q].flag = reinterpret_cast<unsigned long long*>(base);
-    tab[q].recv = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(base) + flag_bytes);
+    tab[q].recv = reinterpret_cast<unsigned long long*>(base);
   }
   CK(cudaMemcpy(ctx->d_xpeers, tab.data(), sizeof(fmdp::XPeer) * fmdp::XMAX, cudaMemcpyHostToDevice));
   CK(cudaMemset(ctx->d_xseq, 0, 2 * sizeof(unsigned long long)));
-  CK(cudaMemset(ctx->x_area, 0, flag_bytes));  // this rank's tags restart with the sequence
+  CK(cudaMemset(ctx->x_area, 0, fmdp::x_area_bytes(world, ctx->x_slot)));  // tags restart with the sequence
   CK(cudaDeviceSynchronize());
   ctx->x_me = rank;
   return FMDP_OK;
@@ -1349,6 +1347,7 @@ fmdp_status fmdp_schedule_p2p(fmdp_ctx* ctx, uint64_t aircraft_id, fmdp_vec3 src
   if (st) return st;
   if ((st = ensure_slots(ctx, 1))) return st;
   CK(cudaMemsetAsync(ctx->d_pairctr, 0, sizeof(unsigned long long), ctx->stream));
+  CK(cudaMemsetAsync(ctx->d_prof, 0, sizeof(unsigned long long) * fmdp::N_PHASES, ctx->stream));
   ctx->shard_rank = ctx->x_me;
   ctx->shard_world = ctx->x_world;
   ctx->xmode = 3;
@@ -1368,6 +1367,11 @@ fmdp_status fmdp_schedule_p2p(fmdp_ctx* ctx, uint64_t aircraft_id, fmdp_vec3 src
   if ((st = fetch_out(ctx, 1))) return st;
   ctx->stats.steps += ctx->h_out[0].steps_run;
   ctx->stats.rounds += 1;
+  if (ctx->launch.profile) {
+    unsigned long long ph[fmdp::N_PHASES];
+    CK(cudaMemcpy(ph, ctx->d_prof, sizeof(ph), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < fmdp::N_PHASES; ++i) ctx->stats.phase_cycles[i] = (int64_t)ph[i];
+  }
   return finish_single(ctx, base, aircraft_id, res, traj);
 }
 

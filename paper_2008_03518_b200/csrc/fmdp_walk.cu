@@ -18,6 +18,7 @@
 //   a6-a8  every CTA redundantly: combine (Alg 8), max over t, argmax (Alg 9),
 //       advance (Alg 1), terminal tests (Sec IV.I)
 #include <cooperative_groups.h>
+#include <mutex>
 #include <type_traits>
 #include <cuda_runtime.h>
 
@@ -169,7 +170,10 @@ struct Ctl {
   int32_t hgt[MAX_TURN];      // ground height under Delta_1 of every turn (cp.async target)
   int32_t cs_ok;              // scratch of cs_idle
   int32_t stop[2];            // head-finished flag seen by rank 0 at the top of the step, by parity
+  uint32_t xstay[2];          // multi-GPU: nearest-plan d^2 over the ranks (from CTA 0), by parity
+  unsigned long long* xp[XMAX];  // multi-GPU: every rank's receive area (loaded once per launch)
 };
+static_assert(sizeof(Ctl) <= 512, "Ctl exceeds its shared-memory slot (Layout::o_ctl)");
 
 // Stage row K's slice for this CTA (slots [lo, lo+n) of n_row active slots): the first CH
 // plans go to ring buffer K % 3 with cp.async.bulk (TMA bulk copy), completion on its
@@ -294,56 +298,77 @@ __device__ __noinline__ bool cs_idle(int4* pub_all, unsigned* arrive, int32_t* e
 
 // ----------------------------------------------------------------------------- multi-GPU exchange
 // In-kernel plan-sharded step exchange (xmode 3, SURVEY §8(e) production form).  Every rank runs
-// the same persistent walker over its shard of every time row; per step each CTA has stored its
-// owned per-(state, tau) minima into every peer's receive slot (P2P stores, NVLink) before
-// calling this.  Here it adds its nearest-plan d^2, releases the step tag to every peer
-// (bar.sync + fence.sys + relaxed.sys store: the CTA's stores are ordered before the tag) and
-// acquires the peers' tags for this step.  Two parities suffice: a rank writes tag s+2 into a
-// peer's parity-s slot only after it saw the peer's tag s+1, which the peer releases after it
-// finished reading its slot of tag s.  A wait longer than ~2 s (a peer is not running) sets
-// *err and every later wait returns at once: the walk then ends with wrong values and the host
-// reports FMDP_E_CUDA.  All threads of one CTA; returns the minimum d^2 over the ranks.
-__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
+// the same persistent walker over its shard of every time row.  Each exchanged value travels as
+// one 8-byte word {value, step tag} written with a single 64-bit store straight into the peer's
+// receive slot (P2P over NVLink; the store is single-copy atomic), and the reader polls the word
+// until it carries this step's tag -- value and "ready" arrive together, so no fence and no
+// separate flag are needed.  Two parities suffice: CTA c of a rank writes its words of step s+2
+// only after it has read every word of step s+1 from the peer's CTA c, which that CTA wrote after
+// it had finished reading step s (CTA barriers in between).  A poll longer than ~2 s (a peer is
+// not running) sets *err and returns the stale value; every later poll returns at once, the walk
+// ends with wrong values and the host reports FMDP_E_CUDA.
+__device__ __forceinline__ void st_ll(unsigned long long* p, uint32_t v, uint32_t tag) {
+  asm volatile("st.volatile.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(v), "r"(tag) : "memory");
 }
-__device__ __forceinline__ void st_relaxed_sys_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __noinline__ uint32_t x_exchange(const XPeer* peers, int me, int world, int slot, unsigned cta,
-                                            unsigned long long seq, uint32_t stay, int32_t* err) {
-  const int par = (int)(seq & 1ull);
-  const size_t mine = (size_t)(par * world + me);
-  if (threadIdx.x == 0)
-    for (int q = 0; q < world; ++q)
-      if (q != me) __stcg(peers[q].recv + mine * slot + (slot - 16) + cta, stay);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    for (int q = 0; q < world; ++q)
-      if (q != me) st_relaxed_sys_u64(peers[q].flag + mine * 16 + cta, seq);
-    const unsigned long long* own = peers[me].flag;
-    for (int q = 0; q < world; ++q) {
-      if (q == me) continue;
-      const unsigned long long* f = own + (size_t)(par * world + q) * 16 + cta;
-      if (ld_acquire_sys_u64(f) >= seq) continue;
-      const long long t0 = clock64();
-      while (ld_acquire_sys_u64(f) < seq) {
-        if (*(volatile int32_t*)err) break;
-        if (clock64() - t0 > (4ll << 30)) {
-          atomicExch(err, 1);
-          break;
-        }
-      }
+__device__ __noinline__ uint32_t ld_ll_wait(const unsigned long long* p, uint32_t tag, int32_t* err, long long budget) {
+  const long long t0 = clock64();
+  uint32_t v, t;
+  for (;;) {
+    asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(v), "=r"(t) : "l"(p) : "memory");
+    if (t == tag) return v;
+    if (*(volatile int32_t*)err) return v;
+    if (clock64() - t0 > budget) {
+      atomicExch(err, 1);
+      return v;
     }
   }
-  __syncthreads();
-  uint32_t m = stay;
-  const uint32_t* rv = peers[me].recv;
+}
+// Poll budget in SM cycles: ~2 s, ~8 s for a launch's first exchange (the ranks' launches may
+// be skewed by their hosts).  Liveness: every poll is bounded, and every polled value is read by
+// exactly one CTA of the cluster (items: their owner; the nearest-plan d^2: CTA 0, which then
+// broadcasts it over DSMEM), so a timeout can make ranks disagree but never splits a cluster.
+__device__ __forceinline__ long long x_budget(unsigned long long xit) { return xit == 1 ? (16ll << 30) : (4ll << 30); }
+__device__ __forceinline__ uint32_t ld_ll(const unsigned long long* p, uint32_t tag, int32_t* err, long long budget) {
+  uint32_t v, t;
+  asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(v), "=r"(t) : "l"(p) : "memory");
+  return t == tag ? v : ld_ll_wait(p, tag, err, budget);
+}
+// Minimum of v and the peers' words at item index io of this step: all loads issued first
+// (independent round trips), tags checked after; a word not yet there is polled.
+__device__ __forceinline__ float x_min_peers(const unsigned long long* own, int me, int world, int slot, int par,
+                                             int io, uint32_t tag, int32_t* err, long long budget, float v) {
+  uint32_t wv[XMAX - 1], wt[XMAX - 1];
+#pragma unroll
+  for (int j = 0; j < XMAX - 1; ++j) {
+    if (j < world - 1) {
+      const int q = j < me ? j : j + 1;
+      asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];"
+                   : "=r"(wv[j]), "=r"(wt[j])
+                   : "l"(own + (size_t)(par * world + q) * slot + io)
+                   : "memory");
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < XMAX - 1; ++j) {
+    if (j < world - 1) {
+      const int q = j < me ? j : j + 1;
+      const uint32_t x = wt[j] == tag ? wv[j] : ld_ll_wait(own + (size_t)(par * world + q) * slot + io, tag, err, budget);
+      v = fminf(v, __uint_as_float(x));
+    }
+  }
+  return v;
+}
+// Words of (parity, source rank) in a rank's receive area: [0, A*W*NTAU) the per-(state, tau)
+// minima, slot - 16 + cta the nearest-plan d^2 of CTA cta.
+__device__ __forceinline__ size_t x_word(int par, int world, int src, int slot, int i) {
+  return (size_t)(par * world + src) * slot + i;
+}
+// Nearest-plan d^2: min over the ranks (CTA 0, thread 0; the own value was published earlier).
+__device__ __noinline__ uint32_t x_stay_min(const unsigned long long* own, int me, int world, int slot, int par,
+                                            uint32_t tag, uint32_t stay, int32_t* err, long long budget) {
   for (int q = 0; q < world; ++q)
-    if (q != me) m = min(m, __ldcg(rv + (size_t)(par * world + q) * slot + (slot - 16) + cta));
-  return m;
+    if (q != me) stay = min(stay, ld_ll(own + x_word(par, world, q, slot, slot - 16), tag, err, budget));
+  return stay;
 }
 
 // G-way minimum of one (state, tau) item over the partial blocks of the cluster's CTAs
@@ -497,6 +522,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
     for (int b = 0; b < 7; ++b) mbar_init(&s_bar[b], 1);  // 0-2 TMA ring, 3-4 reduce-scatter, 5-6 V*
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (XP && tid < args.x_world) ctl->xp[tid] = args.x_peers[tid].recv;
   __syncthreads();
   uint32_t par = 0;      // next wait parity per ring buffer (bit b)
   uint32_t parX = 0;     // next wait parity of the exchange mbarriers: bits 0-1 reduce-scatter, 2-3 V*
@@ -686,7 +712,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         const uint32_t bytesA = (xmode != 2 ? 4u * G : 0u) +
                                 ((!fin && xmode != 2) ? (uint32_t)(4 * G * n_own * BLK) : 0u) + (args.stop ? 4u : 0u);
         mbar_arrive_tx(&s_bar[3 + p], bytesA);
-        if (!fin) mbar_arrive_tx(&s_bar[5 + p], (uint32_t)(16 * A));
+        if (!fin) mbar_arrive_tx(&s_bar[5 + p], (uint32_t)(16 * A) + (XP ? 4u : 0u));
         if (args.stop && rank == 0) {  // one reading for the whole cluster
           const uint32_t f = (uint32_t)*(volatile int32_t*)args.stop;
           const uint32_t la = smem_u32(&ctl->stop[p]), lb = smem_u32(&s_bar[3 + p]);
@@ -974,28 +1000,26 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           if (b < (int)G) stay_all = min(stay_all, s_stay[p * 16 + b]);
       }
       if (xmode == 1 && rank == 0 && tid == 0) args.xbuf[NTAU * AW] = stay_all;
-      if (XP) {
-        // this GPU's minima of the owned items -> every peer's receive slot, then
-        // the step tag; the minima over all ranks are taken in pass 1 below
-        __syncthreads();  // s_stage (s_M) is free once every thread of this CTA has pushed its blocks
+      uint32_t xtag = 0;
+      int xpar = 0;
+      if (XP) {  // publish this GPU's nearest-plan d^2 to every peer (CTA 0)
         ++xit;
-        const unsigned long long seq = xseq0 + xit;
-        if (!fin) {
-          const float* rcv = s_recv + p * (int)G * NOWN * BLK;
-          const size_t xo = (size_t)((int)(seq & 1ull) * args.x_world + args.x_me) * args.x_slot;
-          const int nitem = n_own * W * NTAU;
-          for (int i = tid; i < nitem; i += NT) {
-            const int oa = i / (W * NTAU), r2 = i - oa * (W * NTAU);
-            const int st = ((int)rank + oa * (int)G) * W + r2 / NTAU;
-            const float M = gway_min(rcv + oa * BLK + r2, (int)G, NOWN * BLK);
-            s_stage[i] = M;
-            for (int q = 0; q < args.x_world; ++q)
-              if (q != args.x_me) __stcg(args.x_peers[q].recv + xo + st * NTAU + r2 % NTAU, __float_as_uint(M));
+        xtag = (uint32_t)(xseq0 + xit);
+        xpar = (int)((xseq0 + xit) & 1ull);
+        if (rank == 0 && tid == 0)
+          for (int q = 0; q < args.x_world; ++q)
+            if (q != args.x_me)
+              st_ll(ctl->xp[q] + x_word(xpar, args.x_world, args.x_me, args.x_slot, args.x_slot - 16), stay_all, xtag);
+        if (fin) {  // no owner epilogue in this step: CTA 0 collects the peers' values, broadcasts
+          if (rank == 0 && tid == 0) {
+            const uint32_t m = x_stay_min(ctl->xp[args.x_me], args.x_me, args.x_world, args.x_slot, xpar, xtag,
+                                          stay_all, args.x_err, x_budget(xit));
+            for (unsigned b = 0; b < G; ++b) cluster.map_shared_rank(ctl, b)->xstay[p] = m;
           }
+          cluster.sync();
+          stay_all = ctl->xstay[p];
         }
-        stay_all = x_exchange(args.x_peers, args.x_me, args.x_world, args.x_slot, rank, seq, stay_all, args.x_err);
       }
-
       if (!fin) {
         // ---- owner epilogue (half-warp per owned action, lane = substep): G-way minimum of
         //      the partial blocks, exact in/out, values (Alg 8), V*(a)
@@ -1007,6 +1031,19 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         float* s_M = s_stage;
         __syncthreads();
         const int nitem = n_own * W * NTAU;
+        if (XP) {  // this GPU's minima of the owned items -> every peer (all sends
+                   // before any poll); each thread keeps its own items' minima in s_M
+          for (int i = tid; i < nitem; i += NT) {
+            const int oa = i / (W * NTAU), r2 = i - oa * (W * NTAU);
+            const int io = (((int)rank + oa * (int)G) * W + r2 / NTAU) * NTAU + r2 % NTAU;
+            const float M = gway_min(rcv + oa * BLK + r2, (int)G, NOWN * BLK);
+            s_M[i] = M;
+            for (int q = 0; q < args.x_world; ++q)
+              if (q != args.x_me)
+                st_ll(ctl->xp[q] + x_word(xpar, args.x_world, args.x_me, args.x_slot, io), __float_as_uint(M),
+                      xtag);
+          }
+        }
         for (int i = tid; i < nitem; i += NT) {
           const int oa = i / (W * NTAU), r2 = i - oa * (W * NTAU);
           const int l = r2 / NTAU, t = r2 - l * NTAU;
@@ -1014,12 +1051,9 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           float M;
           if (xmode == 2) {
             M = __uint_as_float(args.xbuf[st * NTAU + t]);
-          } else if (XP) {  // minimum over the ranks (this GPU's from pass 1a)
-            M = s_M[i];
-            const uint32_t* rv = args.x_peers[args.x_me].recv + st * NTAU + t;
-            for (int q = 0; q < args.x_world; ++q)
-              if (q != args.x_me)
-                M = fminf(M, __uint_as_float(__ldcg(rv + (size_t)((int)((xseq0 + xit) & 1ull) * args.x_world + q) * args.x_slot)));
+          } else if (XP) {  // this GPU's minimum (sent below) and the peers' minima
+            M = x_min_peers(ctl->xp[args.x_me], args.x_me, args.x_world, args.x_slot, xpar, st * NTAU + t,
+                            xtag, args.x_err, x_budget(xit), s_M[i]);
           } else {
             M = gway_min(rcv + oa * BLK + r2, (int)G, NOWN * BLK);
             if (xmode == 1) args.xbuf[st * NTAU + t] = __float_as_uint(M);  // this GPU's minima
@@ -1036,6 +1070,12 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
             if (idx < AMB_MAX) s_amb[idx] = i;
           }
           s_M[i] = out;
+        }
+        if (XP && rank == 0 && tid == 0) {  // -> every CTA with its V* pushes (one reader per value)
+          const uint32_t m = x_stay_min(ctl->xp[args.x_me], args.x_me, args.x_world, args.x_slot, xpar, xtag, stay_all,
+                                        args.x_err, x_budget(xit));
+          const uint32_t la = smem_u32(&ctl->xstay[p]), lb = smem_u32(&s_bar[5 + p]);
+          for (unsigned b = 0; b < G; ++b) st_async_u32(mapa_u32(la, b), m, mapa_u32(lb, b));
         }
         __syncthreads();
         FMDP_MARK(PH_OWN1)
@@ -1131,6 +1171,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         FMDP_MARK(PH_OWNER)
         mbar_wait(&s_bar[5 + p], (parX >> (2 + p)) & 1u);
         parX ^= 1u << (2 + p);
+        if (XP) stay_all = ctl->xstay[p];  // over the ranks, from CTA 0
         FMDP_MARK(PH_BAR2)
       }
 
@@ -1351,17 +1392,38 @@ int walk_threads(int ncol, int max_threads) {
   return 32 * ((ncol + cpw - 1) / cpw);
 }
 
+// Function attributes, set once per device and raised only when a launch needs more (not on
+// every launch: concurrent walkers of the multi-GPU exchange launch from several host threads).
+template <int C, int MODE>
+static cudaError_t set_walk_attrs(int smem, int cluster) {
+  static std::mutex mu;
+  static int done_smem[64] = {0};
+  static bool done_np[64] = {false};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  dev &= 63;
+  std::lock_guard<std::mutex> lk(mu);
+  if (smem > done_smem[dev]) {
+    e = cudaFuncSetAttribute(walk_kernel<C, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    done_smem[dev] = smem;
+  }
+  if (cluster > 8 && !done_np[dev]) {
+    e = cudaFuncSetAttribute(walk_kernel<C, MODE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    done_np[dev] = true;
+  }
+  return cudaSuccess;
+}
+
 template <int C, int MODE>
 static cudaError_t launch_walk_t(const World& w, const WalkArgs& a, int cluster, int n_clusters, int threads,
                                  int chunk, int rawcap, cudaStream_t s) {
   Layout L;
   L.build(w.HL, chunk, rawcap, threads, C, w.n_turn * w.W, w.A, w.A * w.W, cluster);
-  cudaError_t e = cudaFuncSetAttribute(walk_kernel<C, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+  cudaError_t e = set_walk_attrs<C, MODE>((int)L.total, cluster);
   if (e != cudaSuccess) return e;
-  if (cluster > 8) {
-    e = cudaFuncSetAttribute(walk_kernel<C, MODE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cluster * n_clusters, 1, 1);
   cfg.blockDim = dim3(threads, 1, 1);
@@ -1382,12 +1444,8 @@ template <int C, int MODE>
 static cudaError_t max_clusters_t(const World& w, int cluster, int threads, int chunk, int rawcap, int* out) {
   Layout L;
   L.build(w.HL, chunk, rawcap, threads, C, w.n_turn * w.W, w.A, w.A * w.W, cluster);
-  cudaError_t e = cudaFuncSetAttribute(walk_kernel<C, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+  cudaError_t e = set_walk_attrs<C, MODE>((int)L.total, cluster);
   if (e != cudaSuccess) return e;
-  if (cluster > 8) {
-    e = cudaFuncSetAttribute(walk_kernel<C, MODE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cluster, 1, 1);
   cfg.blockDim = dim3(threads, 1, 1);

@@ -274,12 +274,16 @@ class FMDP:
     def add_plans(self, plans: Sequence[Tuple[int, np.ndarray]], aircraft_ids=None) -> int:
         if not plans:
             return self.num_plans()
-        t0 = np.ascontiguousarray([p[0] for p in plans], np.int64)
-        n = np.ascontiguousarray([len(p[1]) for p in plans], np.int32)
-        st = np.ascontiguousarray(np.concatenate([np.asarray(p[1], np.int32).reshape(-1, 3) for p in plans]), np.int32)
+        return self.add_plans_packed(*pack_plans(plans), aircraft_ids=aircraft_ids)
+
+    def add_plans_packed(self, t0: np.ndarray, n: np.ndarray, st: np.ndarray, aircraft_ids=None) -> int:
+        """add_plans from ``pack_plans`` arrays (t0[P] int64, n[P] int32, states[sum n][3] int32)."""
+        t0 = np.ascontiguousarray(t0, np.int64)
+        n = np.ascontiguousarray(n, np.int32)
+        st = np.ascontiguousarray(st, np.int32)
         ids = None if aircraft_ids is None else np.ascontiguousarray(aircraft_ids, np.uint64)
         first = C.c_uint32()
-        self._check(self.L.fmdp_add_plans(self.ctx, len(plans), _p(ids), _p(t0), _p(n), _p(st), C.byref(first)),
+        self._check(self.L.fmdp_add_plans(self.ctx, len(t0), _p(ids), _p(t0), _p(n), _p(st), C.byref(first)),
                     "fmdp_add_plans")
         return int(first.value)
 
@@ -471,6 +475,14 @@ def allreduce_min_torch(group=None, device=None):
         dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
         arr[:] = t.cpu().numpy().astype(np.uint32)
     return f
+
+
+def pack_plans(plans: Sequence[Tuple[int, np.ndarray]]):
+    """(t0, n, states) arrays of a plan list, the layout fmdp_add_plans takes."""
+    t0 = np.ascontiguousarray([p[0] for p in plans], np.int64)
+    n = np.ascontiguousarray([len(p[1]) for p in plans], np.int32)
+    st = np.ascontiguousarray(np.concatenate([np.asarray(p[1], np.int32).reshape(-1, 3) for p in plans]), np.int32)
+    return t0, n, st
 
 
 def p2p_connect_local(ctxs: Sequence["FMDP"]):
