@@ -386,20 +386,29 @@ def run_native(args):
             return row(ms, steps, st, s_["cluster_size"]), st
 
         def run_p2p(cs, cull, n_world):
+            # every rank takes part in every collective, also after a failed call (reported)
             for c in cs:
                 c.set_launch(cull=cull)
             ms = steps = 0
-            st = []
+            st, errs = [], []
             for i in reqs:
-                with ThreadPoolExecutor(len(cs)) as ex:
-                    rs = list(ex.map(lambda c: c.schedule_p2p(sc4.src[i], sc4.dst[i], int(sc4.t0[i]),
-                                                              want_traj=False), cs))
-                stats = [c.stats() for c in cs]
-                ms += max_over_ranks(max(s_["device_ms"] for s_ in stats), n_world)
-                steps += stats[0]["steps"]; st.append(rs[0].status)
+                try:
+                    with ThreadPoolExecutor(len(cs)) as ex:
+                        rs = list(ex.map(lambda c: c.schedule_p2p(sc4.src[i], sc4.dst[i], int(sc4.t0[i]),
+                                                                  want_traj=False), cs))
+                    stats = [c.stats() for c in cs]
+                    t = max(s_["device_ms"] for s_ in stats)
+                    steps += stats[0]["steps"]; st.append(rs[0].status)
+                except Exception as e:  # noqa: BLE001 -- reported in the JSON line
+                    errs.append(str(e))
+                    t = float("nan")
+                ms += max_over_ranks(t, n_world)
                 for c in cs:
                     c.truncate(P)
-            return row(ms, steps, st, stats[0]["cluster_size"]), st
+            out_row = row(ms, steps, st, cs[0].stats()["cluster_size"])
+            if errs:
+                out_row["errors"] = errs[:2]
+            return out_row, st
 
         out = {"what": "configs[3] single-request latency at 100k accepted plans; p2p = plan-sharded with the "
                        "per-step exchange inside the walker kernel (fmdp_schedule_p2p)",
@@ -429,10 +438,13 @@ def run_native(args):
                 c.close()
         else:
             out["ranks_are"] = f"{world} GPUs, one process each (CUDA IPC exchange areas, NVLink P2P stores)"
-            p2p_connect_group(base)
             e = {"ranks": world}
-            for cull in (0, 1):
-                e["culled" if cull else "full"], _ = run_p2p([base], cull, world)
+            try:
+                p2p_connect_group(base)  # raises on every rank if any rank failed
+                for cull in (0, 1):
+                    e["culled" if cull else "full"], _ = run_p2p([base], cull, world)
+            except Exception as ex:  # noqa: BLE001 -- reported in the JSON line
+                e["error"] = str(ex)
             out["p2p"] = [e]
             base.close()
         return out

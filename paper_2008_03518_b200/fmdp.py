@@ -497,7 +497,8 @@ def p2p_connect_local(ctxs: Sequence["FMDP"]):
 def p2p_connect_group(ctx: "FMDP", group=None):
     """Connect this process's context with the other ranks of a torch.distributed group (one
     process per GPU): exchange areas are shared by CUDA IPC handles (pointers when two ranks
-    live in one process).  Collective; ends with a barrier so no rank schedules early."""
+    live in one process).  Collective; ends with an all-gather of every rank's outcome, so no
+    rank schedules before all are connected, and a failure on any rank raises on all."""
     import os as _os
     import torch.distributed as dist
     rank, world = dist.get_rank(group), dist.get_world_size(group)
@@ -506,5 +507,13 @@ def p2p_connect_group(ctx: "FMDP", group=None):
     dist.all_gather_object(info, (h, p, _os.getpid()), group=group)
     pid = _os.getpid()
     ptrs = [pp if (q == rank or ppid == pid) else 0 for q, (_, pp, ppid) in enumerate(info)]
-    ctx.p2p_connect(rank, world, [hh for hh, _, _ in info], ptrs)
-    dist.barrier(group=group)
+    err = ""
+    try:
+        ctx.p2p_connect(rank, world, [hh for hh, _, _ in info], ptrs)
+    except Exception as e:  # every rank learns of it below: no rank is left waiting in a collective
+        err = f"rank {rank}: {e}"
+    errs = [None] * world
+    dist.all_gather_object(errs, err, group=group)
+    bad = [e for e in errs if e]
+    if bad:
+        raise FmdpError("p2p_connect_group failed: " + "; ".join(bad))

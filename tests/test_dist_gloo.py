@@ -62,6 +62,8 @@ class _FakeCtx:
 
     def p2p_connect(self, rank, world, handles, ptrs):
         self.got = (rank, world, [h[0] for h in handles], list(ptrs))
+        if self.rank == 1 and getattr(self, "fail", False):
+            raise RuntimeError("no peer access")
 
 
 def _connect_worker(rank, world, port, out_dir):
@@ -74,7 +76,15 @@ def _connect_worker(rank, world, port, out_dir):
     c = _FakeCtx(rank)
     p2p_connect_group(c)
     r, w, hs, ps = c.got
-    np.save(os.path.join(out_dir, f"c{rank}.npy"), np.array([r, w] + hs + ps, dtype=np.int64))
+    # a failure on one rank raises on every rank (nobody is left in a collective)
+    c2 = _FakeCtx(rank)
+    c2.fail = True
+    raised = 0
+    try:
+        p2p_connect_group(c2)
+    except Exception as e:
+        raised = int("rank 1: no peer access" in str(e))
+    np.save(os.path.join(out_dir, f"c{rank}.npy"), np.array([r, w] + hs + ps + [raised], dtype=np.int64))
     dist.destroy_process_group()
 
 
@@ -90,3 +100,4 @@ def test_gloo_p2p_connect_group_exchanges_handles(tmp_path):
         assert got[2:4] == [1, 2]
         want_ptrs = [0x1000 * (q + 1) if q == r else 0 for q in range(world)]
         assert got[4:6] == want_ptrs
+        assert got[6] == 1
