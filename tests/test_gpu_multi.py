@@ -154,3 +154,42 @@ def test_p2p_missing_peer_times_out_and_reconnects():
     assert ok[0].status == ok[1].status and (ok[0].traj == ok[1].traj).all()
     for c in ctxs:
         c.close()
+
+
+def _ipc_worker(rank, world, port, out_dir):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2008_03518_b200.fmdp import FMDP, p2p_connect_group
+    sc = _scenario()
+    ctx = FMDP(sc.airspace, sc.terrain, device=0)
+    ctx.add_plans(sc.plans)
+    p2p_connect_group(ctx)
+    for i in range(sc.n_requests):
+        r = ctx.schedule_p2p(sc.src[i], sc.dst[i], int(sc.t0[i]))
+        np.save(os.path.join(out_dir, f"ipc{rank}_{i}.npy"), np.concatenate([[r.status, r.n_states], r.traj.ravel()]))
+    ctx.close()
+    dist.destroy_process_group()
+
+
+def test_p2p_two_processes_cuda_ipc(tmp_path):
+    """The cross-process form: exchange areas mapped by CUDA IPC handles all-gathered over a
+    torch.distributed group (p2p_connect_group).  Both processes share this one GPU (without
+    MPS only by time-slicing, so this checks the mapping and the protocol, not speed)."""
+    from paper_2008_03518_b200.fmdp import FMDP
+    sc = _scenario()
+    ref = FMDP(sc.airspace, sc.terrain)
+    ref.add_plans(sc.plans)
+    want = [ref.schedule(sc.src[i], sc.dst[i], int(sc.t0[i])) for i in range(sc.n_requests)]
+    ref.close()
+    assert max(w.n_states for w in want) > 50
+    mp.spawn(_ipc_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    for r in range(2):
+        for i, w in enumerate(want):
+            got = np.load(tmp_path / f"ipc{r}_{i}.npy")
+            assert got[0] == w.status and got[1] == w.n_states
+            assert (got[2:].reshape(-1, 3) == w.traj).all()

@@ -19,10 +19,15 @@ def worker(rank, world, port):
     torch.cuda.set_device(0)
     import fmdp_synth as fs
     from paper_2008_03518_b200.fmdp import FMDP, p2p_connect_group
-    sc = fs.random_small(71, n_plans=300, n_requests=2, half_m=1500.0, n_buildings=30, max_steps=400, t0_max=40)
+    sc = fs.random_small(71, n_plans=300, n_requests=8, half_m=1500.0, n_buildings=30, max_steps=400, t0_max=40)
     ref = FMDP(sc.airspace, sc.terrain)
     ref.add_plans(sc.plans)
-    want = ref.schedule(sc.src[0], sc.dst[0], int(sc.t0[0]))
+    j = 0
+    for j in range(sc.n_requests):
+        want = ref.schedule(sc.src[j], sc.dst[j], int(sc.t0[j]))
+        ref.truncate(len(sc.plans))
+        if want.n_states > 50:
+            break
     ref.close()
     ctx = FMDP(sc.airspace, sc.terrain)
     ctx.add_plans(sc.plans)
@@ -30,7 +35,7 @@ def worker(rank, world, port):
     dist.barrier()
     t = time.perf_counter()
     try:
-        got = ctx.schedule_p2p(sc.src[0], sc.dst[0], int(sc.t0[0]))
+        got = ctx.schedule_p2p(sc.src[j], sc.dst[j], int(sc.t0[j]))
         ok = got.status == want.status and got.n_states == want.n_states and (got.traj == want.traj).all()
         print(f"rank {rank}: status {got.status} n {got.n_states} identical={ok} "
               f"{time.perf_counter() - t:.2f} s", flush=True)
