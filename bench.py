@@ -43,8 +43,8 @@ def parse():
     p.add_argument("--seed", type=int, default=2)
     p.add_argument("--cpu-sample-s", type=float, default=15.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--no-c4", action="store_true", help="skip the configs[3] 100k-plan latency block")
-    p.add_argument("--only-c4", action="store_true", help="run only the configs[3] block and print it")
+    p.add_argument("--no-c4", action="store_true", help="skip the configs[2] / configs[3] blocks")
+    p.add_argument("--only-c4", action="store_true", help="run only the configs[2] / configs[3] blocks")
     return p.parse_args()
 
 
@@ -449,10 +449,56 @@ def run_native(args):
             base.close()
         return out
 
+    def measure_c3():
+        # configs[2]: 1000 FCFS requests growing the store from 0 plans.  (i) sequential
+        # fmdp_schedule calls: host wall time per call from entry to return incl. the trajectory
+        # copy (SURVEY §8(d) d.1 "ms/request", median / p95), binned by #accepted plans before the
+        # call -- the metric's "ms/request vs #accepted plans"; (ii) the same 1000 requests as one
+        # fmdp_schedule_batch call (identical results by construction, checked).  §8(a) path.
+        import numpy as np
+        sc3 = fs.config_c3()
+        c = FMDP(sc3.airspace, sc3.terrain, device=local)
+        c.set_launch(cull=0)
+        rows = []
+        for i in range(sc3.n_requests):
+            n_acc = c.num_plans()
+            t = time.perf_counter()
+            r = c.schedule(sc3.src[i], sc3.dst[i], int(sc3.t0[i]))
+            dt = (time.perf_counter() - t) * 1e3
+            st = c.stats()
+            rows.append((n_acc, dt, st["device_ms"], st["steps"], r.status, r.n_states))
+        seq = [(x[4], x[5]) for x in rows]
+        total_s = sum(x[1] for x in rows) / 1e3
+        bins = []
+        edges = list(range(0, max(x[0] for x in rows) + 200, 200))
+        for lo, hi in zip(edges[:-1], edges[1:]):
+            sel = [x for x in rows if lo <= x[0] < hi]
+            if not sel:
+                continue
+            hw = np.array([x[1] for x in sel])
+            steps = sum(x[3] for x in sel)
+            bins.append({"accepted_plans": [lo, hi], "requests": len(sel),
+                         "host_ms_median": float(np.median(hw)), "host_ms_p95": float(np.percentile(hw, 95)),
+                         "steps_per_request": steps / len(sel),
+                         "device_us_per_step": sum(x[2] for x in sel) * 1e3 / max(1, steps)})
+        c.truncate(0)
+        t = time.perf_counter()
+        res = c.schedule_batch(sc3.src, sc3.dst, sc3.t0)
+        batch_s = time.perf_counter() - t
+        same = [(r.status, r.n_states) for r in res] == seq
+        c.close()
+        return {"what": "configs[2]: 1000 FCFS requests from an empty store (dense urban, terrain), §8(a) path; "
+                        "host wall per fmdp_schedule call incl. trajectory copy, by #accepted plans before it",
+                "requests": sc3.n_requests, "accepted": int(sum(1 for x in rows if x[4] == 0)),
+                "sequential_requests_per_s": sc3.n_requests / total_s,
+                "batch_requests_per_s": sc3.n_requests / batch_s, "batch_same_results": same,
+                "host_ms_median": float(np.median([x[1] for x in rows])),
+                "host_ms_p95": float(np.percentile([x[1] for x in rows], 95)), "by_accepted_plans": bins}
+
     if args.only_c4:
-        out = measure_c4()
+        out = {"c3_growth": measure_c3(), "c4_sharded": measure_c4()}
         if rank == 0:
-            print(json.dumps({"c4_sharded": out}), flush=True)
+            print(json.dumps(out), flush=True)
         return 0
     _log("configs[1] batch, full path")
     M = measure(0)       # every (state, well) pair evaluated
@@ -464,6 +510,8 @@ def run_native(args):
     Mco = measure_cosim()
     _log("latency vs plans")
     Mlat = measure_latency()
+    _log("configs[2] sequential growth")
+    Mc3 = None if args.no_c4 else measure_c3()
     _log("configs[3] sharded latency")
     Mc4 = None if args.no_c4 else measure_c4()
     h2d = n * C_REQUEST_BYTES
@@ -529,6 +577,8 @@ def run_native(args):
         "f2_cosim": Mco,
         "latency_vs_plans": Mlat,
     }
+    if Mc3 is not None:
+        line["c3_growth"] = Mc3
     if Mc4 is not None:
         line["c4_sharded"] = Mc4
     if not args.no_cpu_baseline:

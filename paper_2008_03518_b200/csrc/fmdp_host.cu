@@ -639,25 +639,32 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
         if (o.status < 0) kdone[r.slot] = o.n_states - 1;
         else fin[r.slot] = 1;
       }
-      // influence of every finished, accepted request j on every later pending request i
+      // influence of every finished, accepted request j that can be committed in this slice --
+      // the finished run [c, c_end) -- on every later request i (only newly committed plans
+      // can roll anything back, and only requests of that run can be committed now)
+      int c_end = c;
+      while (c_end < n && fin[c_end]) ++c_end;
       std::vector<InflPair> pairs;
       std::vector<int32_t> ns(n);
       for (int i = 0; i < n; ++i) ns[i] = ctx->h_out[i].n_states;
-      for (int i = c + 1; i < n; ++i)
-        for (int j = c; j < i; ++j)
-          if (fin[j] && ctx->h_out[j].status == FMDP_ACCEPTED) pairs.push_back({i, j});
+      for (int j = c; j < c_end; ++j)
+        if (ctx->h_out[j].status == FMDP_ACCEPTED)
+          for (int i = j + 1; i < n; ++i) pairs.push_back({i, j});
       std::vector<int32_t> kf;
       if (!pairs.empty()) {
         CK(cudaMemcpyAsync(ctx->d_nstates, ns.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
         if ((st = influence(ctx, pairs, kf))) return st;
       }
+      // pairs by request i (first influenced step kf), and the plans committed so far
+      std::vector<std::vector<std::pair<int, int>>> by_i(n);
+      for (size_t q = 0; q < pairs.size(); ++q)
+        if (kf[q] != INT_MAX) by_i[pairs[q].i].push_back({pairs[q].j, kf[q]});
       std::vector<int> newly;
+      std::vector<char> is_new(n, 0);
       auto first_influence = [&](int i) {
         int best = INT_MAX;
-        for (size_t p = 0; p < pairs.size(); ++p)
-          if (pairs[p].i == i && kf[p] != INT_MAX &&
-              std::find(newly.begin(), newly.end(), pairs[p].j) != newly.end())
-            best = std::min(best, kf[p]);
+        for (const auto& e : by_i[i])
+          if (is_new[e.first]) best = std::min(best, e.second);
         return best;
       };
       while (c < n && fin[c]) {
@@ -668,7 +675,10 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
           ++rollbacks;
           break;
         }
-        if (ctx->h_out[c].status == FMDP_ACCEPTED) newly.push_back(c);
+        if (ctx->h_out[c].status == FMDP_ACCEPTED) {
+          newly.push_back(c);
+          is_new[c] = 1;
+        }
         ++c;
       }
       if ((st = commit_slots(ctx, newly, base, aircraft, plan_id))) return st;
