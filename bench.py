@@ -364,6 +364,7 @@ def run_native(args):
         reqs = list(range(min(n_req, sc4.n_requests)))
 
         packed = pack_plans(sc4.plans)
+        sc4.plans = []  # host memory: the packed arrays are all the contexts need
 
         def mk():
             c = FMDP(sc4.airspace, sc4.terrain, device=local)
@@ -496,7 +497,7 @@ def run_native(args):
                 "host_ms_p95": float(np.percentile([x[1] for x in rows], 95)), "by_accepted_plans": bins}
 
     if args.only_c4:
-        out = {"c3_growth": measure_c3(), "c4_sharded": measure_c4()}
+        out = {"c3_growth": measure_c3() if rank == 0 else None, "c4_sharded": measure_c4()}
         if rank == 0:
             print(json.dumps(out), flush=True)
         return 0
@@ -511,7 +512,7 @@ def run_native(args):
     _log("latency vs plans")
     Mlat = measure_latency()
     _log("configs[2] sequential growth")
-    Mc3 = None if args.no_c4 else measure_c3()
+    Mc3 = None if (args.no_c4 or rank != 0) else measure_c3()  # no collectives: rank 0 only
     _log("configs[3] sharded latency")
     Mc4 = None if args.no_c4 else measure_c4()
     h2d = n * C_REQUEST_BYTES
