@@ -340,10 +340,10 @@ def run_native(args):
                     st = lctx.stats()
                     lctx.truncate(P)
                     if best is None or st["device_ms"] < best[0]:
-                        best = (st["device_ms"], st["steps"], r.status, st["cluster_size"])
+                        best = (st["device_ms"], st["steps"], r.status, st["cluster_size"], max(1, st["split"]))
                 row["culled" if cull else "full"] = {
                     "ms_per_request": best[0], "us_per_step": best[0] * 1e3 / max(1, best[1]), "steps": best[1],
-                    "status": best[2], "cluster_size": best[3]}
+                    "status": best[2], "cluster_size": best[3], "clusters": best[4]}
             lctx.close()
             out.append(row)
         return {"what": "single-request latency vs accepted plans (metric: ms/request vs #accepted plans; Fig "
@@ -371,12 +371,12 @@ def run_native(args):
             c.add_plans_packed(*packed)
             return c
 
-        def row(ms, steps, status, G):
+        def row(ms, steps, status, G, k=1):
             return {"ms_per_request": ms / len(reqs), "us_per_step": ms * 1e3 / max(1, steps), "steps": steps,
-                    "status": status, "cluster_size": G}
+                    "status": status, "cluster_size": G, "clusters": k}
 
-        def run_single(c, cull):
-            c.set_launch(cull=cull)
+        def run_single(c, cull, split):
+            c.set_launch(cull=cull, split=split)
             ms = steps = 0
             st = []
             for i in reqs:
@@ -384,7 +384,8 @@ def run_native(args):
                 s_ = c.stats()
                 ms += s_["device_ms"]; steps += s_["steps"]; st.append(r.status)
                 c.truncate(P)
-            return row(ms, steps, st, s_["cluster_size"]), st
+            c.set_launch(cull=cull)
+            return row(ms, steps, st, s_["cluster_size"], max(1, s_["split"])), st
 
         def run_p2p(cs, cull, n_world):
             # every rank takes part in every collective, also after a failed call (reported)
@@ -411,18 +412,22 @@ def run_native(args):
                 out_row["errors"] = errs[:2]
             return out_row, st
 
-        out = {"what": "configs[3] single-request latency at 100k accepted plans; p2p = plan-sharded with the "
-                       "per-step exchange inside the walker kernel (fmdp_schedule_p2p)",
+        out = {"what": "configs[3] single-request latency at 100k accepted plans; one_cluster = one 16-CTA "
+                       "cluster; split = fmdp_schedule with the request split over k clusters of this GPU "
+                       "(cost model; in-kernel exchange); p2p = plan-sharded ranks (fmdp_schedule_p2p)",
                "plans": P, "rows": 1200, "requests": len(reqs)}
         _log("c4: store ready")
         base = mk()
         _log("c4: context 0 loaded")
         if world == 1:
-            out["single"] = {}
+            out["one_cluster"], out["split"] = {}, {}
             want = None
             for cull in (0, 1):
-                out["single"]["culled" if cull else "full"], want = run_single(base, cull)
-                _log(f"c4: single cull={cull} {out['single']['culled' if cull else 'full']}")
+                key = "culled" if cull else "full"
+                out["one_cluster"][key], want = run_single(base, cull, 1)
+                out["split"][key], st = run_single(base, cull, 0)
+                out["split"]["same_status"] = st == want
+                _log(f"c4: one cluster cull={cull} {out['one_cluster'][key]}; split {out['split'][key]}")
             out["ranks_are"] = "contexts on this one B200 (own stream each; they share its 148 SMs)"
             ctxs = [base] + [mk() for _ in range(max(rank_counts) - 1)]
             _log(f"c4: {len(ctxs)} contexts loaded")

@@ -135,6 +135,11 @@ typedef struct fmdp_launch {
   int32_t step_budget;    /* batch: decision steps per trajectory per slice, 0 = auto (128) */
   int32_t cull;           /* 1: SURVEY f1 exact culling -- skip plans none of whose wells can */
                           /* reach a projected state (outputs bit-identical)               */
+  int32_t split;          /* single-request walks (fmdp_schedule, FMDP_BATCH_SEQUENTIAL):  */
+                          /* clusters sharing one request, each over a shard of every time */
+                          /* row, combined per step by the in-kernel exchange of           */
+                          /* fmdp_schedule_p2p (outputs bit-identical).  0 = auto (cost    */
+                          /* model: large stores), 1 = off, 2..8 = that many clusters      */
 } fmdp_launch;
 
 typedef struct fmdp_request {
@@ -168,6 +173,8 @@ typedef struct fmdp_stats {
   int64_t phase_cycles[17]; /* profile=1: CTA-0 cycles per phase: projection, goal/terrain, */
                            /* row wait, hot loop, stage, reduce-scatter, barrier 1,         */
                            /* owner epilogue, barrier 2, decide                             */
+  int32_t split;           /* clusters that shared the last single-request walk (launch.split) */
+  int32_t pad;
 } fmdp_stats;
 
 /* Fill *a with the defaults of DESIGN.md Appendix A (the arrays point to static storage). */

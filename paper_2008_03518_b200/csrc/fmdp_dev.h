@@ -119,6 +119,8 @@ struct WalkArgs {
   const XPeer* x_peers;             // [x_world] device table (entry x_me = this GPU's own area)
   unsigned long long* x_seq;          // this rank's exchange sequence number (step tags)
   int32_t* x_err;                     // set on a poll timeout (a peer is not running)
+  int32_t x_intra;                    // 1: the launch's clusters are the ranks (x_me = cluster
+                                      // index, x_world = clusters; x_seq / queue per cluster)
 };
 
 // One rank's exchange area as seen from this GPU (peer pointer: IPC-opened or same process):

@@ -89,6 +89,12 @@ struct fmdp_ctx {
   int x_world = 0, x_me = -1, x_slot = 0;
   std::vector<void*> x_ipc;                // IPC-opened peer areas
   fmdp::XPeer* d_xpeers = nullptr;         // [XMAX]
+  // one request split over clusters of this GPU (fmdp_launch.split): the same exchange, the
+  // launch's clusters as ranks; areas / tags / queues kept across launches (tags monotonic)
+  unsigned long long* d_xin_area = nullptr;  // XMAX areas of XMAX ranks
+  fmdp::XPeer* d_xin_peers = nullptr;        // [XMAX]
+  unsigned long long* d_xin_seq = nullptr;   // [XMAX] per-cluster sequence, then int32 error, queues
+  int xin_world = 0;                         // cluster count of the last split launch (layout)
   unsigned long long* d_xseq = nullptr;    // [1] sequence, then [1] int32 error flag
   double *d_dbg_vstar = nullptr, *d_dbg_v = nullptr, *d_dbg_s = nullptr;
   uint32_t* d_dbg_conf = nullptr;
@@ -564,6 +570,80 @@ fmdp_status prepare_requests(fmdp_ctx* ctx, const fmdp_request* reqs, int n, std
   return FMDP_OK;
 }
 
+// Clusters for one request walked alone (fmdp_launch.split): 1, or k clusters of 16 CTAs each
+// over a shard of every row, combined per step by the in-kernel exchange.  Auto: the cost model
+// t(k) = step_cycles(plans / k, 16) + exchange, exchange = 4000 + 2000 (k - 1) cycles
+// (measured: tools/p2p_probe.py, profiles/r01_p2p_probe.txt), k resident at once.
+int split_for(fmdp_ctx* ctx) {
+  if (ctx->launch.split == 1 || (ctx->launch.cluster_size && ctx->launch.cluster_size != 16)) return 1;
+  const int kmax = std::min(fmdp::XMAX, std::min(ctx->num_sms / 16, max_clusters(ctx, 16)));
+  if (kmax < 2) return 1;
+  if (ctx->launch.split >= 2) return std::min(ctx->launch.split, kmax);
+  const double plans = mean_plans(ctx);
+  int best = 1;
+  double tb = step_cycles(ctx, plans, solo_cluster_size(ctx));
+  for (int k = 2; k <= kmax; ++k) {
+    const double t = step_cycles(ctx, plans / k, 16) + 4000.0 + 2000.0 * (k - 1);
+    if (t < tb - 1e-9) {
+      tb = t;
+      best = k;
+    }
+  }
+  return best;
+}
+
+// One request, alone on the device: a plain walk, or split over k clusters (bit-identical).
+fmdp_status run_single(fmdp_ctx* ctx, const Req& r) {
+  const int k = split_for(ctx);
+  if (k <= 1) return run_walk(ctx, {r}, false);
+  const int slot = ((ctx->A * ctx->W * fmdp::NTAU + 16) + 3) & ~3;
+  const size_t area_words = fmdp::x_area_bytes(fmdp::XMAX, slot) / sizeof(unsigned long long);
+  if (!ctx->d_xin_area) {
+    ctx->d_xin_area = (unsigned long long*)dalloc(ctx, sizeof(unsigned long long) * area_words * fmdp::XMAX);
+    ctx->d_xin_peers = (fmdp::XPeer*)dalloc(ctx, sizeof(fmdp::XPeer) * fmdp::XMAX);
+    ctx->d_xin_seq = (unsigned long long*)dalloc(ctx, sizeof(unsigned long long) * (fmdp::XMAX + 1 + fmdp::XMAX));
+    if (!ctx->d_xin_area || !ctx->d_xin_peers || !ctx->d_xin_seq) return fail(ctx, FMDP_E_NOMEM, "split exchange");
+    ctx->xin_world = 0;
+  }
+  unsigned long long* seq = ctx->d_xin_seq;
+  int32_t* err = reinterpret_cast<int32_t*>(seq + fmdp::XMAX);
+  int32_t* queue = reinterpret_cast<int32_t*>(seq + fmdp::XMAX + 1);
+  if (k != ctx->xin_world) {  // new layout: clean areas, tags restart
+    std::vector<fmdp::XPeer> tab(fmdp::XMAX, fmdp::XPeer{nullptr});
+    for (int q = 0; q < k; ++q) tab[q].recv = ctx->d_xin_area + (size_t)q * area_words;
+    CK(cudaMemcpyAsync(ctx->d_xin_peers, tab.data(), sizeof(fmdp::XPeer) * fmdp::XMAX, cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CK(cudaMemsetAsync(ctx->d_xin_area, 0, sizeof(unsigned long long) * area_words * fmdp::XMAX, ctx->stream));
+    CK(cudaMemsetAsync(seq, 0, sizeof(unsigned long long) * (fmdp::XMAX + 1), ctx->stream));
+    ctx->xin_world = k;
+  }
+  CK(cudaMemsetAsync(queue, 0, sizeof(int32_t) * fmdp::XMAX, ctx->stream));
+  ctx->xmode = 3;
+  ctx->shard_rank = 0;
+  ctx->shard_world = k;
+  fmdp::WalkArgs a = make_args(ctx, {r}, false, INT_MAX);
+  a.x_intra = 1;
+  a.x_me = 0;
+  a.x_world = k;
+  a.x_slot = slot;
+  a.x_peers = ctx->d_xin_peers;
+  a.x_seq = seq;
+  a.x_err = err;
+  a.queue = queue;
+  fmdp_status st = run_walk(ctx, {r}, false, INT_MAX, &a, 16, k);
+  ctx->xmode = 0;
+  ctx->shard_world = 1;
+  if (st) return st;
+  ctx->stats.split = k;
+  int32_t e = 0;
+  CK(cudaMemcpy(&e, err, sizeof(e), cudaMemcpyDeviceToHost));
+  if (e) {
+    ctx->xin_world = 0;
+    return fail(ctx, FMDP_E_CUDA, "split request: cluster exchange timed out (clusters not co-resident)");
+  }
+  return FMDP_OK;
+}
+
 fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_result* res, fmdp_qpos* traj,
                           int32_t traj_cap_each, int32_t flags) {
   if (!ctx || (n > 0 && (!reqs || !res)) || n < 0) return fail(ctx, FMDP_E_ARG, "null argument");
@@ -587,7 +667,7 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
   int runs = 0;
   if (flags & FMDP_BATCH_SEQUENTIAL) {
     for (int i = 0; i < n; ++i) {
-      if ((st = run_walk(ctx, {base[i]}, false))) return st;
+      if ((st = run_single(ctx, base[i]))) return st;
       ++runs;
       ctx->stats.rounds += 1;
       if ((st = fetch_out(ctx, n))) return st;

@@ -500,10 +500,16 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   // SURVEY f2 co-simulated batch: a separate instantiation, so the FCFS walker carries no
   // co-simulation code at all (measured: any of it on the step path costs ~1.5 %)
   const int cosim = MODE == 1 ? 1 : 0;
-  const unsigned long long xseq0 = XP ? *args.x_seq : 0ull;  // step tags continue across launches
+  // x_intra: the launch's clusters are the ranks (one GPU, one request split over several
+  // clusters); otherwise this launch is rank x_me of a multi-GPU exchange
+  const int xcl = (XP && args.x_intra) ? (int)(blockIdx.x / G) : 0;
+  const int xme = (XP && args.x_intra) ? xcl : args.x_me;
+  const bool lead = xcl == 0;  // writes the request's outputs (every cluster decides the same)
+  const int srank = (XP && args.x_intra) ? xcl : args.shard_rank;
+  const unsigned long long xseq0 = XP ? args.x_seq[xcl] : 0ull;  // step tags continue across launches
   unsigned long long xit = 0;
 
-  const bool prof = args.prof != nullptr && rank == 0 && tid == 0;
+  const bool prof = args.prof != nullptr && rank == 0 && tid == 0 && (blockIdx.x / G) == 0;
   unsigned long long pacc[PH_N];
 #pragma unroll
   for (int i = 0; i < PH_N; ++i) pacc[i] = 0;
@@ -532,7 +538,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   for (;;) {
     // ------------------------------------------------------------ next request
     if (rank == 0 && tid == 0) {
-      int r = atomicAdd(args.queue, 1);
+      int r = atomicAdd(args.queue + xcl, 1);
       for (unsigned b = 0; b < G; ++b) cluster.map_shared_rank(&ctl->req, b)[0] = r;
     }
     cluster.sync();
@@ -576,7 +582,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           min_sep = min(min_sep, args.stepd2[sbase + kk]);
         }
       }
-      if (rank == 0 && k == 0 && !args.eval) {
+      if (lead && rank == 0 && k == 0 && !args.eval) {
         int32_t* tq = args.traj + 3 * sbase;
         tq[0] = rq.src[0]; tq[1] = rq.src[1]; tq[2] = rq.src[2];
         args.heading[sbase] = rq.psi0;
@@ -585,8 +591,8 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       }
       const int64_t K0 = rq.t0 + k;
       const int n0 = row_count(w, K0), n1 = row_count(w, K0 + 1);
-      issue_row(w, K0, n0, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, args.shard_rank, args.shard_world);
-      issue_row(w, K0 + 1, n1, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, args.shard_rank, args.shard_world);
+      issue_row(w, K0, n0, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, srank, args.shard_world);
+      issue_row(w, K0 + 1, n1, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, srank, args.shard_world);
     }
     {
       const int64_t K0 = rq.t0 + k;
@@ -705,7 +711,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       //      blocks of the owned actions (from every CTA), the stop flag (from rank 0), V*(a)
       if (tid == NT - 1) {
         if (!args.eval && !fin) {
-          issue_row(w, K + 2, cnt2, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, args.shard_rank, args.shard_world);
+          issue_row(w, K + 2, cnt2, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, srank, args.shard_world);
           cnt2 = row_count(w, K + 3);  // consumed next step: latency hidden by this step
         }
         ctl->nsurv[((k + 1) & 1) * 2] = 0;  // step k+1, chunk 0 (last used in step k-1)
@@ -1008,11 +1014,11 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         xpar = (int)((xseq0 + xit) & 1ull);
         if (rank == 0 && tid == 0)
           for (int q = 0; q < args.x_world; ++q)
-            if (q != args.x_me)
-              st_ll(ctl->xp[q] + x_word(xpar, args.x_world, args.x_me, args.x_slot, args.x_slot - 16), stay_all, xtag);
+            if (q != xme)
+              st_ll(ctl->xp[q] + x_word(xpar, args.x_world, xme, args.x_slot, args.x_slot - 16), stay_all, xtag);
         if (fin) {  // no owner epilogue in this step: CTA 0 collects the peers' values, broadcasts
           if (rank == 0 && tid == 0) {
-            const uint32_t m = x_stay_min(ctl->xp[args.x_me], args.x_me, args.x_world, args.x_slot, xpar, xtag,
+            const uint32_t m = x_stay_min(ctl->xp[xme], xme, args.x_world, args.x_slot, xpar, xtag,
                                           stay_all, args.x_err, x_budget(xit));
             for (unsigned b = 0; b < G; ++b) cluster.map_shared_rank(ctl, b)->xstay[p] = m;
           }
@@ -1039,8 +1045,8 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
             const float M = gway_min(rcv + oa * BLK + r2, (int)G, NOWN * BLK);
             s_M[i] = M;
             for (int q = 0; q < args.x_world; ++q)
-              if (q != args.x_me)
-                st_ll(ctl->xp[q] + x_word(xpar, args.x_world, args.x_me, args.x_slot, io), __float_as_uint(M),
+              if (q != xme)
+                st_ll(ctl->xp[q] + x_word(xpar, args.x_world, xme, args.x_slot, io), __float_as_uint(M),
                       xtag);
           }
         }
@@ -1052,7 +1058,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           if (xmode == 2) {
             M = __uint_as_float(args.xbuf[st * NTAU + t]);
           } else if (XP) {  // this GPU's minimum (sent below) and the peers' minima
-            M = x_min_peers(ctl->xp[args.x_me], args.x_me, args.x_world, args.x_slot, xpar, st * NTAU + t,
+            M = x_min_peers(ctl->xp[xme], xme, args.x_world, args.x_slot, xpar, st * NTAU + t,
                             xtag, args.x_err, x_budget(xit), s_M[i]);
           } else {
             M = gway_min(rcv + oa * BLK + r2, (int)G, NOWN * BLK);
@@ -1072,7 +1078,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           s_M[i] = out;
         }
         if (XP && rank == 0 && tid == 0) {  // -> every CTA with its V* pushes (one reader per value)
-          const uint32_t m = x_stay_min(ctl->xp[args.x_me], args.x_me, args.x_world, args.x_slot, xpar, xtag, stay_all,
+          const uint32_t m = x_stay_min(ctl->xp[xme], xme, args.x_world, args.x_slot, xpar, xtag, stay_all,
                                         args.x_err, x_budget(xit));
           const uint32_t la = smem_u32(&ctl->xstay[p]), lb = smem_u32(&s_bar[5 + p]);
           for (unsigned b = 0; b < G; ++b) st_async_u32(mapa_u32(la, b), m, mapa_u32(lb, b));
@@ -1217,7 +1223,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         }
         done = true;
       } else {
-        if (rank == 0 && tid == 0) args.stepd2[sbase + k] = c0;
+        if (lead && rank == 0 && tid == 0) args.stepd2[sbase + k] = c0;
         min_sep = min(min_sep, c0);
         // Determine terminal state of state k (Sec IV.I): conflict, terrain, goal, timeout
         int st = -1;
@@ -1231,7 +1237,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           done = true;
         } else {
           const int4 p1 = s_pos[a1 * W + 0];  // s_{t+1} <- Delta_1[a*] (Alg 1)
-          if (rank == 0 && tid == 0) {
+          if (lead && rank == 0 && tid == 0) {
             args.astar[sbase + k] = a1;
             args.ntie[sbase + k] = near ? 1 : 0;
             int32_t* tq = args.traj + 3 * (sbase + k + 1);
@@ -1283,9 +1289,9 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
 
     // ------------------------------------------------------------ request epilogue
     cluster.sync();  // n_exact contributions of every CTA have landed in rank 0
-    if (XP && rank == 0 && tid == 0) *args.x_seq = xseq0 + xit;  // read by the next launch
-    if (rank == 0 && tid == 0 && rq.head && args.stop && status >= 0) atomicExch(args.stop, 1);
-    if (rank == 0 && tid == 0 && !args.eval) {
+    if (XP && rank == 0 && tid == 0) args.x_seq[xcl] = xseq0 + xit;  // read by the next launch
+    if (lead && rank == 0 && tid == 0 && rq.head && args.stop && status >= 0) atomicExch(args.stop, 1);
+    if (lead && rank == 0 && tid == 0 && !args.eval) {
       Out o;
       o.status = status;
       o.n_states = k + 1;

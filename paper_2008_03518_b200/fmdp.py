@@ -66,7 +66,7 @@ class Devices(C.Structure):
 
 class Launch(C.Structure):
     _fields_ = [("cluster_size", C.c_int32), ("max_walkers", C.c_int32), ("threads", C.c_int32),
-                ("profile", C.c_int32), ("step_budget", C.c_int32), ("cull", C.c_int32)]
+                ("profile", C.c_int32), ("step_budget", C.c_int32), ("cull", C.c_int32), ("split", C.c_int32)]
 
 
 class Request(C.Structure):
@@ -92,7 +92,8 @@ class P2PHandle(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("steps", C.c_int64), ("pair_evals", C.c_int64), ("rounds", C.c_int32), ("reruns", C.c_int32),
                 ("cluster_size", C.c_int32), ("walkers", C.c_int32), ("kernels", C.c_int32),
-                ("device_ms", C.c_double), ("phase_cycles", C.c_int64 * 17)]
+                ("device_ms", C.c_double), ("phase_cycles", C.c_int64 * 17), ("split", C.c_int32),
+                ("pad", C.c_int32)]
 
 PHASES = ("projection", "goal_terrain", "row_wait", "hot_loop", "stage", "reduce_scatter", "barrier1",
           "owner_epilogue", "barrier2", "decide", "top", "tscan", "proj_loop", "build", "own_classify", "argmax", "flags")
@@ -266,8 +267,8 @@ class FMDP:
     def __exit__(self, *exc):
         self.close()
 
-    def set_launch(self, cluster_size=0, max_walkers=0, threads=0, profile=0, step_budget=0, cull=0):
-        l = Launch(cluster_size, max_walkers, threads, profile, step_budget, cull)
+    def set_launch(self, cluster_size=0, max_walkers=0, threads=0, profile=0, step_budget=0, cull=0, split=0):
+        l = Launch(cluster_size, max_walkers, threads, profile, step_budget, cull, split)
         self._check(self.L.fmdp_set_launch(self.ctx, C.byref(l)), "fmdp_set_launch")
 
     # ------------------------------------------------------------------ store

@@ -193,3 +193,28 @@ def test_p2p_two_processes_cuda_ipc(tmp_path):
             got = np.load(tmp_path / f"ipc{r}_{i}.npy")
             assert got[0] == w.status and got[1] == w.n_states
             assert (got[2:].reshape(-1, 3) == w.traj).all()
+
+
+@pytest.mark.parametrize("split,cull", [(2, 0), (3, 1), (4, 0), (8, 1)])
+def test_split_request_bit_identical(split, cull):
+    """fmdp_launch.split: one request walked by several clusters of this GPU, each over a shard
+    of every row, combined per step by the in-kernel exchange -- identical to one cluster."""
+    from paper_2008_03518_b200.fmdp import FMDP
+    sc = _scenario()
+    ref = FMDP(sc.airspace, sc.terrain)
+    ref.add_plans(sc.plans)
+    ref.set_launch(cull=cull, split=1)
+    ctx = FMDP(sc.airspace, sc.terrain)
+    ctx.add_plans(sc.plans)
+    ctx.set_launch(cull=cull, split=split)
+    for i in range(sc.n_requests):
+        a = ref.schedule(sc.src[i], sc.dst[i], int(sc.t0[i]))
+        b = ctx.schedule(sc.src[i], sc.dst[i], int(sc.t0[i]))
+        assert 2 <= ctx.stats()["split"] <= split  # capped by the co-resident 16-CTA clusters
+        assert a.status == b.status and a.n_states == b.n_states and (a.traj == b.traj).all()
+        assert a.min_sep_m == b.min_sep_m and a.plan_id == b.plan_id and a.n_near_ties == b.n_near_ties
+        ha, hb = ref.steplog(0), ctx.steplog(0)
+        assert all((x == y).all() for x, y in zip(ha, hb))
+    assert ref.stats()["split"] == 0 or ref.stats()["split"] == 1
+    ref.close()
+    ctx.close()
