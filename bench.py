@@ -184,7 +184,7 @@ def run_native(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import fmdp_synth as fs
-    from paper_2008_03518_b200.fmdp import FMDP, Request, Result
+    from paper_2008_03518_b200.fmdp import FMDP, Request, Result, pack_plans
 
     sc = fs.config_c2(seed=args.seed + 1000 * rank)  # replica r: its own seeded batch and store
     stream = torch.cuda.Stream(device=local)
@@ -501,8 +501,45 @@ def run_native(args):
                 "host_ms_median": float(np.median([x[1] for x in rows])),
                 "host_ms_p95": float(np.percentile([x[1] for x in rows], 95)), "by_accepted_plans": bins}
 
+    def measure_c5():
+        # configs[4] roofline stress: 1M accepted plans (64 time rows), 17 x 5 = 85 actions; one
+        # request walked on the §8(a) full path, one 16-CTA cluster vs split over clusters
+        # (cost model), and culled; device time, pair evaluations against the FP32 pipe peak
+        sc5 = fs.config_c5(rows=64)
+        packed = pack_plans(sc5.plans)
+        sc5.plans = []
+        c = FMDP(sc5.airspace, sc5.terrain, device=local)
+        c.add_plans_packed(*packed)
+        del packed
+        P = c.num_plans()
+        out = {"what": "configs[4]: 1M accepted plans (64 rows), A = 85 (17 headings x 5 climbs), one request, "
+                       "device time of the walk (1965 MHz peak clock)",
+               "plans": P, "actions": sc5.airspace.n_actions}
+        for name, cull, split in (("full_one_cluster", 0, 1), ("full_split", 0, 0), ("culled", 1, 0)):
+            c.set_launch(cull=cull, split=split)
+            r = c.schedule(sc5.src[0], sc5.dst[0], int(sc5.t0[0]), want_traj=False)
+            st = c.stats()
+            c.truncate(P)
+            secs = st["device_ms"] / 1e3
+            pps = st["pair_evals"] / secs if secs > 0 else 0.0
+            sms = max(1, st["split"]) * st["cluster_size"]
+            C5 = len(sc5.airspace.climb_units)
+            out[name] = {"us_per_step": st["device_ms"] * 1e3 / max(1, st["steps"]), "steps": st["steps"],
+                         "status": r.status, "clusters": max(1, st["split"]), "cluster_size": st["cluster_size"],
+                         "pair_evals_per_s": pps,
+                         # 7 algorithmic ops per pair against the lane peak (can exceed 1: the Q + 2(s-o).X
+                         # formulation executes (2 + C - 1) / C lane-ops per pair)
+                         "algorithmic_ops_frac": pps * OPS_PER_PAIR / (148 * 128 * 1965e6),
+                         "pipe_frac": pps * (2 + C5 - 1) / C5 / (148 * 128 * 1965e6),
+                         "pairs_per_clk_per_sm_used": pps / (sms * 1965e6),
+                         "loop_ceiling_pairs_per_clk_per_sm": "34-36 (C = 3, profiles/r01_hotbench.txt)"}
+            _log(f"c5: {name} {out[name]}")
+        c.close()
+        return out
+
     if args.only_c4:
-        out = {"c3_growth": measure_c3() if rank == 0 else None, "c4_sharded": measure_c4()}
+        out = {"c3_growth": measure_c3() if rank == 0 else None, "c4_sharded": measure_c4(),
+               "c5_stress": measure_c5() if rank == 0 else None}
         if rank == 0:
             print(json.dumps(out), flush=True)
         return 0
@@ -520,6 +557,8 @@ def run_native(args):
     Mc3 = None if (args.no_c4 or rank != 0) else measure_c3()  # no collectives: rank 0 only
     _log("configs[3] sharded latency")
     Mc4 = None if args.no_c4 else measure_c4()
+    _log("configs[4] roofline stress")
+    Mc5 = None if (args.no_c4 or rank != 0) else measure_c5()
     h2d = n * C_REQUEST_BYTES
     tot_ms, value, e2e_value, d2h = M["tot_ms"], M["value"], M["e2e_value"], M["d2h"]
     stats = M["st_all"][-1]
@@ -587,6 +626,8 @@ def run_native(args):
         line["c3_growth"] = Mc3
     if Mc4 is not None:
         line["c4_sharded"] = Mc4
+    if Mc5 is not None:
+        line["c5_stress"] = Mc5
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(sc, args.cpu_sample_s)
     print(json.dumps(line), flush=True)

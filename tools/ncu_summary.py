@@ -37,11 +37,14 @@ def stalls(hdr, data, a, b):
 
 lines = [f"# {rnd} — ncu evidence (B200, sm_100a)\n",
          "Captures (`ncu --set full --clock-control none --import-source on -k regex:walk_kernel -c 1`):",
-         "- `walk_batch`: first walk launch of the configs[1] FCFS batch (`tools/ncu_batch.py`: 100 requests x",
-         "  128-step slice, one single-CTA walker per request) — the bench's dominant kernel, §8(a) path;",
-         "- `walk_cull2`: one configs[1] request with SURVEY f1 culling on a 2-CTA cluster (`tools/ncu_cull.py 2`).",
+         "- `walk_batch`: first walk launch of the configs[1] FCFS batch (`tools/ncu_batch.py`): the first",
+         "  slice's head request alone at G = 16 to completion -- the batch's critical path -- §8(a) path;",
+         "- `walk_cull2`: one configs[1] request with SURVEY f1 culling on a 2-CTA cluster (`tools/ncu_cull.py 2`);",
+         "- `walk_c5split`: configs[4] (1M plans, A = 85) one request on the full path split over the",
+         "  co-resident 16-CTA clusters with the in-kernel exchange (`tools/ncu_c5.py`), the roofline stress.",
          "Launch list: `ncu --metrics gpu__time_duration.sum --clock-control none` of `python bench.py --steps 1",
-         "--warmup 3 --no-cpu-baseline` (cold-cache, serialised: compare shares, not absolutes).\n"]
+         "--warmup 3 --no-cpu-baseline --no-c4` (the headline blocks; cold-cache, serialised: compare shares,",
+         "not absolutes; the configs[2..4] blocks are left out: ncu serialises the p2p ranks' kernels).\n"]
 rows = list(csv.reader(open('gpurun_out/launches.csv')))
 hi = [i for i, r in enumerate(rows) if r and r[0] == 'ID'][0]
 hdr = rows[hi]; data = rows[hi + 1:]
@@ -58,17 +61,21 @@ for k in sorted(t, key=lambda k: -t[k]):
     lines.append(f"| `{k}` | {n[k]} | {t[k] / 1e6:.2f} | {t[k] / tot * 100:.1f}% |")
 lines.append("")
 traffic = None
-for rep, title in (('walk_batch', 'configs[1] batch slice, 100 walkers x G=1 (full path)'),
-                   ('walk_cull2', 'configs[1] request, f1 culling, G=2')):
+import os
+for rep, kern, title in (('walk_batch', 'walk_kernel<3, 0>', 'configs[1] batch, first slice head (full path)'),
+                         ('walk_cull2', 'walk_kernel<3, 0>', 'configs[1] request, f1 culling, G=2'),
+                         ('walk_c5split', 'walk_kernel<5, 2>', 'configs[4] 1M plans, A = 85, split request (full path)')):
+    if not os.path.exists(f'gpurun_out/{rep}.ncu-rep'):
+        continue
     m = raw(f'gpurun_out/{rep}.ncu-rep')
-    lines += [f"## walk_kernel<3, false> — {title}\n", "| metric | value |", "|---|---|"]
+    lines += [f"## {kern} — {title}\n", "| metric | value |", "|---|---|"]
     for k in WANT:
         if k in m:
             lines.append(f"| `{k}` | {m[k][0]} {m[k][1]} |")
     if rep == 'walk_batch':
         rd = float(m['dram__bytes_read.sum'][0].replace(',', '')) * (1e6 if m['dram__bytes_read.sum'][1] == 'Mbyte' else 1e3 if m['dram__bytes_read.sum'][1] == 'Kbyte' else 1e9 if m['dram__bytes_read.sum'][1] == 'Gbyte' else 1)
         wr = float(m['dram__bytes_write.sum'][0].replace(',', '')) * (1e6 if m['dram__bytes_write.sum'][1] == 'Mbyte' else 1e3 if m['dram__bytes_write.sum'][1] == 'Kbyte' else 1e9 if m['dram__bytes_write.sum'][1] == 'Gbyte' else 1)
-        traffic = dict(kernel="walk_kernel<3, false>", capture=f"{rnd} walk_batch (tools/ncu_batch.py, first launch)",
+        traffic = dict(kernel="walk_kernel<3, 0>", capture=f"{rnd} walk_batch (tools/ncu_batch.py, first launch)",
                        dram_bytes_read=int(rd), dram_bytes_write=int(wr), per_launch_bytes=int(rd + wr),
                        note="DRAM traffic per launch; the kernel is FP32-pipe bound, plan rows are L2-resident")
     h, d = source(f'gpurun_out/{rep}.ncu-rep')
@@ -89,7 +96,7 @@ for rep, title in (('walk_batch', 'configs[1] batch slice, 100 walkers x G=1 (fu
         ops[op.split('.')[0]] += 1
     if b - a < 10:
         lines += ["", "No dominant loop (latency-bound step): per-source-line stall attribution in "
-                  f"profiles/{rnd}_lines_{'cull2' if 'cull' in rep else 'batch_full'}.txt (tools/ncu_lines.py).",
+                  f"profiles/{rnd}_lines_{rep}.txt (tools/ncu_lines.py).",
                   "Whole kernel: " + ", ".join(f"{k} {v:.1f}%" for k, v in sorted(allst.items(), key=lambda x: -x[1])) + ".", ""]
         continue
     lines += ["", f"Most-executed loop: {b - a} SASS instructions, {hs / ts * 100:.1f} % of warp-stall samples; "
