@@ -598,10 +598,12 @@ fmdp_status run_single(fmdp_ctx* ctx, const Req& r) {
   if (k <= 1) return run_walk(ctx, {r}, false);
   const int slot = ((ctx->A * ctx->W * fmdp::NTAU + 16) + 3) & ~3;
   const size_t area_words = fmdp::x_area_bytes(fmdp::XMAX, slot) / sizeof(unsigned long long);
-  if (!ctx->d_xin_area) {
-    ctx->d_xin_area = (unsigned long long*)dalloc(ctx, sizeof(unsigned long long) * area_words * fmdp::XMAX);
-    ctx->d_xin_peers = (fmdp::XPeer*)dalloc(ctx, sizeof(fmdp::XPeer) * fmdp::XMAX);
-    ctx->d_xin_seq = (unsigned long long*)dalloc(ctx, sizeof(unsigned long long) * (fmdp::XMAX + 1 + fmdp::XMAX));
+  if (!ctx->d_xin_area || !ctx->d_xin_peers || !ctx->d_xin_seq) {
+    if (!ctx->d_xin_area)
+      ctx->d_xin_area = (unsigned long long*)dalloc(ctx, sizeof(unsigned long long) * area_words * fmdp::XMAX);
+    if (!ctx->d_xin_peers) ctx->d_xin_peers = (fmdp::XPeer*)dalloc(ctx, sizeof(fmdp::XPeer) * fmdp::XMAX);
+    if (!ctx->d_xin_seq)
+      ctx->d_xin_seq = (unsigned long long*)dalloc(ctx, sizeof(unsigned long long) * (fmdp::XMAX + 1 + fmdp::XMAX));
     if (!ctx->d_xin_area || !ctx->d_xin_peers || !ctx->d_xin_seq) return fail(ctx, FMDP_E_NOMEM, "split exchange");
     ctx->xin_world = 0;
   }
@@ -1349,11 +1351,9 @@ fmdp_status fmdp_p2p_export(fmdp_ctx* ctx, int32_t world, fmdp_p2p_handle* handl
   CK(cudaSetDevice(ctx->device));
   CK(cudaStreamSynchronize(ctx->stream));
   x_release(ctx);
-  if (!ctx->d_xpeers) {
-    ctx->d_xpeers = (fmdp::XPeer*)dalloc(ctx, sizeof(fmdp::XPeer) * fmdp::XMAX);
-    ctx->d_xseq = (unsigned long long*)dalloc(ctx, 2 * sizeof(unsigned long long));
-    if (!ctx->d_xpeers || !ctx->d_xseq) return fail(ctx, FMDP_E_NOMEM, "exchange tables");
-  }
+  if (!ctx->d_xpeers) ctx->d_xpeers = (fmdp::XPeer*)dalloc(ctx, sizeof(fmdp::XPeer) * fmdp::XMAX);
+  if (!ctx->d_xseq) ctx->d_xseq = (unsigned long long*)dalloc(ctx, 2 * sizeof(unsigned long long));  // seq, error
+  if (!ctx->d_xpeers || !ctx->d_xseq) return fail(ctx, FMDP_E_NOMEM, "exchange tables");
   const int slot = ((ctx->A * ctx->W * fmdp::NTAU + 16) + 3) & ~3;
   const size_t bytes = fmdp::x_area_bytes(world, slot);
   if (cudaMalloc(&ctx->x_area, bytes) != cudaSuccess) {
