@@ -410,6 +410,8 @@ fmdp_status run_split(fmdp_ctx* ctx, std::vector<Req>& run, int budget) {
   const int n = (int)run.size();
   for (Req& r : run) r.head = 0;
   run[0].head = 1;
+  // the head runs as one cluster: splitting it over clusters (fmdp_launch.split) takes SMs from
+  // the others and measured slower (configs[1]: 155.5 -> 171 ms per batch, tools/ab_headsplit.py)
   const int Gh = solo_cluster_size(ctx);
   int Go = 0, nco = 0;
   choose_launch(ctx, n - 1, &Go, &nco, ctx->num_sms - Gh);
@@ -572,8 +574,8 @@ fmdp_status prepare_requests(fmdp_ctx* ctx, const fmdp_request* reqs, int n, std
 
 // Clusters for one request walked alone (fmdp_launch.split): 1, or k clusters of 16 CTAs each
 // over a shard of every row, combined per step by the in-kernel exchange.  Auto: the cost model
-// t(k) = step_cycles(plans / k, 16) + exchange, exchange = 4000 + 2000 (k - 1) cycles
-// (measured: tools/p2p_probe.py, profiles/r01_p2p_probe.txt), k resident at once.
+// t(k) = step_cycles(plans / k, 16) + exchange, exchange = 2400 + 1150 (k - 1) cycles
+// (fit to tools/p2p_probe.py at 3000 / 30000 plans, profiles/r01_p2p_probe.txt), k resident at once.
 int split_for(fmdp_ctx* ctx) {
   if (ctx->launch.split == 1 || (ctx->launch.cluster_size && ctx->launch.cluster_size != 16)) return 1;
   const int kmax = std::min(fmdp::XMAX, std::min(ctx->num_sms / 16, max_clusters(ctx, 16)));
@@ -583,7 +585,7 @@ int split_for(fmdp_ctx* ctx) {
   int best = 1;
   double tb = step_cycles(ctx, plans, solo_cluster_size(ctx));
   for (int k = 2; k <= kmax; ++k) {
-    const double t = step_cycles(ctx, plans / k, 16) + 4000.0 + 2000.0 * (k - 1);
+    const double t = step_cycles(ctx, plans / k, 16) + 2400.0 + 1150.0 * (k - 1);
     if (t < tb - 1e-9) {
       tb = t;
       best = k;
@@ -592,10 +594,9 @@ int split_for(fmdp_ctx* ctx) {
   return best;
 }
 
-// One request, alone on the device: a plain walk, or split over k clusters (bit-identical).
-fmdp_status run_single(fmdp_ctx* ctx, const Req& r) {
-  const int k = split_for(ctx);
-  if (k <= 1) return run_walk(ctx, {r}, false);
+// Exchange state of a request split over k clusters of this GPU (allocated once; a new k
+// resets the areas and tag sequences) and the walk arguments that select it.
+fmdp_status prepare_intra(fmdp_ctx* ctx, int k, fmdp::WalkArgs& a) {
   const int slot = ((ctx->A * ctx->W * fmdp::NTAU + 16) + 3) & ~3;
   const size_t area_words = fmdp::x_area_bytes(fmdp::XMAX, slot) / sizeof(unsigned long long);
   if (!ctx->d_xin_area || !ctx->d_xin_peers || !ctx->d_xin_seq) {
@@ -620,10 +621,9 @@ fmdp_status run_single(fmdp_ctx* ctx, const Req& r) {
     ctx->xin_world = k;
   }
   CK(cudaMemsetAsync(queue, 0, sizeof(int32_t) * fmdp::XMAX, ctx->stream));
-  ctx->xmode = 3;
-  ctx->shard_rank = 0;
-  ctx->shard_world = k;
-  fmdp::WalkArgs a = make_args(ctx, {r}, false, INT_MAX);
+  a.xmode = 3;
+  a.shard_rank = 0;
+  a.shard_world = k;
   a.x_intra = 1;
   a.x_me = 0;
   a.x_world = k;
@@ -632,18 +632,29 @@ fmdp_status run_single(fmdp_ctx* ctx, const Req& r) {
   a.x_seq = seq;
   a.x_err = err;
   a.queue = queue;
-  fmdp_status st = run_walk(ctx, {r}, false, INT_MAX, &a, 16, k);
-  ctx->xmode = 0;
-  ctx->shard_world = 1;
-  if (st) return st;
-  ctx->stats.split = k;
+  return FMDP_OK;
+}
+
+fmdp_status check_intra(fmdp_ctx* ctx) {
   int32_t e = 0;
-  CK(cudaMemcpy(&e, err, sizeof(e), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&e, ctx->d_xin_seq + fmdp::XMAX, sizeof(e), cudaMemcpyDeviceToHost));
   if (e) {
     ctx->xin_world = 0;
     return fail(ctx, FMDP_E_CUDA, "split request: cluster exchange timed out (clusters not co-resident)");
   }
   return FMDP_OK;
+}
+
+// One request, alone on the device: a plain walk, or split over k clusters (bit-identical).
+fmdp_status run_single(fmdp_ctx* ctx, const Req& r) {
+  const int k = split_for(ctx);
+  if (k <= 1) return run_walk(ctx, {r}, false);
+  fmdp::WalkArgs a = make_args(ctx, {r}, false, INT_MAX);
+  fmdp_status st = prepare_intra(ctx, k, a);
+  if (st) return st;
+  if ((st = run_walk(ctx, {r}, false, INT_MAX, &a, 16, k))) return st;
+  ctx->stats.split = k;
+  return check_intra(ctx);
 }
 
 fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_result* res, fmdp_qpos* traj,

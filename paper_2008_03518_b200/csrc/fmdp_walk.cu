@@ -363,12 +363,14 @@ __device__ __forceinline__ float x_min_peers(const unsigned long long* own, int 
 __device__ __forceinline__ size_t x_word(int par, int world, int src, int slot, int i) {
   return (size_t)(par * world + src) * slot + i;
 }
-// Nearest-plan d^2: min over the ranks (CTA 0, thread 0; the own value was published earlier).
-__device__ __noinline__ uint32_t x_stay_min(const unsigned long long* own, int me, int world, int slot, int par,
-                                            uint32_t tag, uint32_t stay, int32_t* err, long long budget) {
-  for (int q = 0; q < world; ++q)
-    if (q != me) stay = min(stay, ld_ll(own + x_word(par, world, q, slot, slot - 16), tag, err, budget));
-  return stay;
+// Nearest-plan d^2: min over the ranks (warp 0 of CTA 0, lane q polls rank q's word in parallel;
+// the own value was published earlier).  All 32 lanes; the result is in every lane.
+__device__ __forceinline__ uint32_t x_stay_min(const unsigned long long* own, int me, int world, int slot, int par,
+                                               uint32_t tag, uint32_t stay, int32_t* err, long long budget) {
+  const int lane = threadIdx.x & 31;
+  uint32_t v = stay;
+  if (lane < world && lane != me) v = min(v, ld_ll(own + x_word(par, world, lane, slot, slot - 16), tag, err, budget));
+  return __reduce_min_sync(0xffffffffu, v);
 }
 
 // G-way minimum of one (state, tau) item over the partial blocks of the cluster's CTAs
@@ -1012,15 +1014,13 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         ++xit;
         xtag = (uint32_t)(xseq0 + xit);
         xpar = (int)((xseq0 + xit) & 1ull);
-        if (rank == 0 && tid == 0)
-          for (int q = 0; q < args.x_world; ++q)
-            if (q != xme)
-              st_ll(ctl->xp[q] + x_word(xpar, args.x_world, xme, args.x_slot, args.x_slot - 16), stay_all, xtag);
+        if (rank == 0 && tid < args.x_world && tid != xme)  // lane q -> rank q
+          st_ll(ctl->xp[tid] + x_word(xpar, args.x_world, xme, args.x_slot, args.x_slot - 16), stay_all, xtag);
         if (fin) {  // no owner epilogue in this step: CTA 0 collects the peers' values, broadcasts
-          if (rank == 0 && tid == 0) {
+          if (rank == 0 && warp == 0) {
             const uint32_t m = x_stay_min(ctl->xp[xme], xme, args.x_world, args.x_slot, xpar, xtag,
                                           stay_all, args.x_err, x_budget(xit));
-            for (unsigned b = 0; b < G; ++b) cluster.map_shared_rank(ctl, b)->xstay[p] = m;
+            if (lane < (int)G) cluster.map_shared_rank(ctl, lane)->xstay[p] = m;
           }
           cluster.sync();
           stay_all = ctl->xstay[p];
@@ -1077,11 +1077,11 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           }
           s_M[i] = out;
         }
-        if (XP && rank == 0 && tid == 0) {  // -> every CTA with its V* pushes (one reader per value)
+        if (XP && rank == 0 && warp == 0) {  // -> every CTA with its V* pushes (one reader per value)
           const uint32_t m = x_stay_min(ctl->xp[xme], xme, args.x_world, args.x_slot, xpar, xtag, stay_all,
                                         args.x_err, x_budget(xit));
-          const uint32_t la = smem_u32(&ctl->xstay[p]), lb = smem_u32(&s_bar[5 + p]);
-          for (unsigned b = 0; b < G; ++b) st_async_u32(mapa_u32(la, b), m, mapa_u32(lb, b));
+          if (lane < (int)G)
+            st_async_u32(mapa_u32(smem_u32(&ctl->xstay[p]), lane), m, mapa_u32(smem_u32(&s_bar[5 + p]), lane));
         }
         __syncthreads();
         FMDP_MARK(PH_OWN1)
