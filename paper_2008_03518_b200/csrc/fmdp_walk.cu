@@ -337,23 +337,26 @@ __device__ __forceinline__ uint32_t ld_ll(const unsigned long long* p, uint32_t 
 // (independent round trips), tags checked after; a word not yet there is polled.
 __device__ __forceinline__ float x_min_peers(const unsigned long long* own, int me, int world, int slot, int par,
                                              int io, uint32_t tag, int32_t* err, long long budget, float v) {
-  uint32_t wv[XMAX - 1], wt[XMAX - 1];
+#pragma unroll 1
+  for (int j0 = 0; j0 < world - 1; j0 += 4) {  // four peers' words in flight at a time
+    uint32_t wv[4], wt[4];
 #pragma unroll
-  for (int j = 0; j < XMAX - 1; ++j) {
-    if (j < world - 1) {
-      const int q = j < me ? j : j + 1;
-      asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];"
-                   : "=r"(wv[j]), "=r"(wt[j])
-                   : "l"(own + (size_t)(par * world + q) * slot + io)
-                   : "memory");
+    for (int j = 0; j < 4; ++j) {
+      const int q = (j0 + j) < me ? (j0 + j) : (j0 + j) + 1;
+      if (j0 + j < world - 1)
+        asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];"
+                     : "=r"(wv[j]), "=r"(wt[j])
+                     : "l"(own + (size_t)(par * world + q) * slot + io)
+                     : "memory");
     }
-  }
 #pragma unroll
-  for (int j = 0; j < XMAX - 1; ++j) {
-    if (j < world - 1) {
-      const int q = j < me ? j : j + 1;
-      const uint32_t x = wt[j] == tag ? wv[j] : ld_ll_wait(own + (size_t)(par * world + q) * slot + io, tag, err, budget);
-      v = fminf(v, __uint_as_float(x));
+    for (int j = 0; j < 4; ++j) {
+      const int q = (j0 + j) < me ? (j0 + j) : (j0 + j) + 1;
+      if (j0 + j < world - 1) {
+        const uint32_t x =
+            wt[j] == tag ? wv[j] : ld_ll_wait(own + (size_t)(par * world + q) * slot + io, tag, err, budget);
+        v = fminf(v, __uint_as_float(x));
+      }
     }
   }
   return v;
