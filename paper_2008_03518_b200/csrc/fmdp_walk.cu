@@ -499,9 +499,13 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   }
   // plan-sharded multi-GPU step: xmode 1 exports this GPU's per-(state, tau)
   // minima and nearest-plan distance, xmode 2 imports their all-reduced minimum and decides
-  // MODE 2: in-kernel exchange with the peer GPUs (xmode 3), no host round-trip per step
+  // MODE 2: in-kernel exchange with the peer GPUs (xmode 3), no host round-trip per step;
+  // MODE 3: the reference / debug instantiation -- the host-stepped exchange (xmode 1 export /
+  // 2 import) and fmdp_eval_step's one-step evaluation.  MODE 0 / 1 / 2 carry neither (measured:
+  // their code on the step path costs 1.7 % full / 3.4 % culled on the configs[1] batch).
   constexpr bool XP = MODE == 2;
-  const int xmode = XP ? 3 : args.xmode;
+  const int xmode = XP ? 3 : (MODE == 3 ? args.xmode : 0);
+  const bool evalm = MODE == 3 && args.eval;
   // SURVEY f2 co-simulated batch: a separate instantiation, so the FCFS walker carries no
   // co-simulation code at all (measured: any of it on the step path costs ~1.5 %)
   const int cosim = MODE == 1 ? 1 : 0;
@@ -581,13 +585,13 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       ctl->stay_local[0] = ctl->stay_local[1] = w.sat_d2;
       ctl->nsurv[0] = ctl->nsurv[1] = ctl->nsurv[2] = ctl->nsurv[3] = 0;
       ctl->n_exact = 0;
-      if (rank == 0 && k > 0 && !args.eval) {  // resume: aggregates of the kept prefix
+      if (rank == 0 && k > 0 && !evalm) {  // resume: aggregates of the kept prefix
         for (int kk = 0; kk < k; ++kk) {
           n_near += args.ntie[sbase + kk];
           min_sep = min(min_sep, args.stepd2[sbase + kk]);
         }
       }
-      if (lead && rank == 0 && k == 0 && !args.eval) {
+      if (lead && rank == 0 && k == 0 && !evalm) {
         int32_t* tq = args.traj + 3 * sbase;
         tq[0] = rq.src[0]; tq[1] = rq.src[1]; tq[2] = rq.src[2];
         args.heading[sbase] = rq.psi0;
@@ -616,7 +620,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       }
     }
     int fl = ctl->fl0;
-    bool fin = !args.eval && fl != 0;  // only the separation test of state k remains
+    bool fin = !evalm && fl != 0;  // only the separation test of state k remains
     cluster.sync();
 
     // ------------------------------------------------------------ step loop
@@ -628,7 +632,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       int4* s_pos = s_pos2 + p * AW;
       // fan origin of this step's projected states (hot-loop formulation)
       const int ox = (W >> 1) * s_dxy[psi].x, oy = (W >> 1) * s_dxy[psi].y;
-      if (!args.eval && !fin) pending |= 1u << bK2;  // row K+2: issued below by the I/O thread
+      if (!evalm && !fin) pending |= 1u << bK2;  // row K+2: issued below by the I/O thread
       FMDP_MARK(PH_TOP)
 
       float sx = 0.f, sy = 0.f, sz[C];
@@ -715,7 +719,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       //      this step's exchange phases -- slice minima (4 B from every CTA), reduce-scatter
       //      blocks of the owned actions (from every CTA), the stop flag (from rank 0), V*(a)
       if (tid == NT - 1) {
-        if (!args.eval && !fin) {
+        if (!evalm && !fin) {
           issue_row(w, K + 2, cnt2, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, srank, args.shard_world);
           cnt2 = row_count(w, K + 3);  // consumed next step: latency hidden by this step
         }
@@ -1148,7 +1152,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
             const double neg = (double)fmaxf(vI, s_vT[st]);
             v = s_fix[st] - neg;
             sc = s_sfix[st] + neg;
-            if (args.eval) {
+            if (evalm) {
               args.dbg_v[st] = v;
               args.dbg_s[st] = sc;
             }
@@ -1170,7 +1174,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           if (oa < n_own && hl < (int)G) {  // push {V*(a), S(a)} to CTA hl
             const double vstar = (w.vmax_init_zero && !w.endpoint) ? fmax(0.0, bv) : bv;
             st_async_d2(mapa_u32(smem_u32(&s_vv[a]), hl), vstar, bs, mapa_u32(smem_u32(&s_bar[5 + p]), hl));
-            if (args.eval && hl == 0) args.dbg_vstar[a] = vstar;
+            if (evalm && hl == 0) args.dbg_vstar[a] = vstar;
           }
         }
         if (tid == 0 && ctl->n_exact && rank != 0) {
@@ -1219,7 +1223,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       if (xmode == 1) {  // export step: no decision in this launch
         status = -1;
         done = true;
-      } else if (args.eval) {
+      } else if (evalm) {
         if (rank == 0 && tid == 0) {
           args.dbg_conf[A] = c0;
           args.dbg_astar[0] = a1;
@@ -1271,7 +1275,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
     }
 
     // eval only: separation minimum of every action's Delta_1 vs the whole row K+1 (debug hook)
-    if (args.eval && rank == 0) {
+    if (evalm && rank == 0) {
       __syncthreads();
       for (int a = tid; a < A; a += NT) s_conf[a] = w.sat_d2;
       __syncthreads();
@@ -1294,7 +1298,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
     cluster.sync();  // n_exact contributions of every CTA have landed in rank 0
     if (XP && rank == 0 && tid == 0) args.x_seq[xcl] = xseq0 + xit;  // read by the next launch
     if (lead && rank == 0 && tid == 0 && rq.head && args.stop && status >= 0) atomicExch(args.stop, 1);
-    if (lead && rank == 0 && tid == 0 && !args.eval) {
+    if (lead && rank == 0 && tid == 0 && !evalm) {
       Out o;
       o.status = status;
       o.n_states = k + 1;
@@ -1471,18 +1475,21 @@ static cudaError_t max_clusters_t(const World& w, int cluster, int threads, int 
 
 cudaError_t launch_walk(const World& w, const WalkArgs& a, int n_climb, int cluster, int n_clusters, int threads,
                         int chunk, int rawcap, cudaStream_t s) {
-  const int mode = a.cosim ? 1 : (a.xmode == 3 ? 2 : 0);
+  const int mode = a.cosim ? 1 : (a.xmode == 3 ? 2 : ((a.xmode || a.eval) ? 3 : 0));
 #define FMDP_LW(c, m) launch_walk_t<c, m>(w, a, cluster, n_clusters, threads, chunk, rawcap, s)
   switch (n_climb * 4 + mode) {
     case 4: return FMDP_LW(1, 0);
     case 5: return FMDP_LW(1, 1);
     case 6: return FMDP_LW(1, 2);
+    case 7: return FMDP_LW(1, 3);
     case 12: return FMDP_LW(3, 0);
     case 13: return FMDP_LW(3, 1);
     case 14: return FMDP_LW(3, 2);
+    case 15: return FMDP_LW(3, 3);
     case 20: return FMDP_LW(5, 0);
     case 21: return FMDP_LW(5, 1);
     case 22: return FMDP_LW(5, 2);
+    case 23: return FMDP_LW(5, 3);
     default: return cudaErrorInvalidValue;
   }
 #undef FMDP_LW
