@@ -506,6 +506,9 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   constexpr bool XP = MODE == 2;
   const int xmode = XP ? 3 : (MODE == 3 ? args.xmode : 0);
   const bool evalm = MODE == 3 && args.eval;
+  // SURVEY f1 culling: MODE 4 is the culled FCFS walker, MODE 0 the full one (each carries only
+  // its own build pass); the other instantiations decide at run time
+  const bool cullm = MODE == 4 ? true : (MODE == 0 ? false : args.cull != 0);
   // SURVEY f2 co-simulated batch: a separate instantiation, so the FCFS walker carries no
   // co-simulation code at all (measured: any of it on the step path costs ~1.5 %)
   const int cosim = MODE == 1 ? 1 : 0;
@@ -518,7 +521,9 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   const unsigned long long xseq0 = XP ? args.x_seq[xcl] : 0ull;  // step tags continue across launches
   unsigned long long xit = 0;
 
-  const bool prof = args.prof != nullptr && rank == 0 && tid == 0 && (blockIdx.x / G) == 0;
+  // per-phase cycle accounting: not in the FCFS walkers (MODE 0 / 4); a profiled FCFS walk runs
+  // in the reference instantiation (MODE 3)
+  const bool prof = MODE != 0 && MODE != 4 && args.prof != nullptr && rank == 0 && tid == 0 && (blockIdx.x / G) == 0;
   unsigned long long pacc[PH_N];
 #pragma unroll
   for (int i = 0; i < PH_N; ++i) pacc[i] = 0;
@@ -753,7 +758,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         // plan j of the CTA slice: the first RAWCAP were staged by TMA, the rest are read from L2
         const int32_t* rb = s_raw + (size_t)bK * 4 * RAWW + ctl->sl_off[bK];
         const int32_t* rg = w.rows + (size_t)K * 4 * w.row_cap + lo;
-        const int SC = args.cull ? RAWCAP : CH;  // plans per build pass
+        const int SC = cullm ? RAWCAP : CH;  // plans per build pass
         const ulonglong2* cen2 = reinterpret_cast<const ulonglong2*>(s_cen);
 
         // Build pass over plans [c0, c0+nc) of the slice: exact nearest-plan distance (stay);
@@ -908,14 +913,14 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           int nc;
           if (!peers) {
             nc = min(SC, n - c0);
-            build(c0, nc, args.cull != 0, counter);
+            build(c0, nc, cullm, counter);
           } else {
             nc = build_peers();
           }
           if (fin) continue;
           FMDP_MARK(PH_BUILD)
           __syncthreads();
-          const int ns = (args.cull && !peers) ? *counter : nc;
+          const int ns = (cullm && !peers) ? *counter : nc;
           if (tid == 0) ctl->nsurv[(k & 1) * 2 + ((cidx + 1) & 1)] = 0;  // next pass's counter
           if (ns <= CH) {
             hot(ns);
@@ -1475,21 +1480,24 @@ static cudaError_t max_clusters_t(const World& w, int cluster, int threads, int 
 
 cudaError_t launch_walk(const World& w, const WalkArgs& a, int n_climb, int cluster, int n_clusters, int threads,
                         int chunk, int rawcap, cudaStream_t s) {
-  const int mode = a.cosim ? 1 : (a.xmode == 3 ? 2 : ((a.xmode || a.eval) ? 3 : 0));
+  const int mode = a.cosim ? 1 : (a.xmode == 3 ? 2 : ((a.xmode || a.eval || a.prof) ? 3 : (a.cull ? 4 : 0)));
 #define FMDP_LW(c, m) launch_walk_t<c, m>(w, a, cluster, n_clusters, threads, chunk, rawcap, s)
-  switch (n_climb * 4 + mode) {
-    case 4: return FMDP_LW(1, 0);
-    case 5: return FMDP_LW(1, 1);
-    case 6: return FMDP_LW(1, 2);
-    case 7: return FMDP_LW(1, 3);
-    case 12: return FMDP_LW(3, 0);
-    case 13: return FMDP_LW(3, 1);
-    case 14: return FMDP_LW(3, 2);
-    case 15: return FMDP_LW(3, 3);
-    case 20: return FMDP_LW(5, 0);
-    case 21: return FMDP_LW(5, 1);
-    case 22: return FMDP_LW(5, 2);
-    case 23: return FMDP_LW(5, 3);
+  switch (n_climb * 8 + mode) {
+    case 8: return FMDP_LW(1, 0);
+    case 9: return FMDP_LW(1, 1);
+    case 10: return FMDP_LW(1, 2);
+    case 11: return FMDP_LW(1, 3);
+    case 12: return FMDP_LW(1, 4);
+    case 24: return FMDP_LW(3, 0);
+    case 25: return FMDP_LW(3, 1);
+    case 26: return FMDP_LW(3, 2);
+    case 27: return FMDP_LW(3, 3);
+    case 28: return FMDP_LW(3, 4);
+    case 40: return FMDP_LW(5, 0);
+    case 41: return FMDP_LW(5, 1);
+    case 42: return FMDP_LW(5, 2);
+    case 43: return FMDP_LW(5, 3);
+    case 44: return FMDP_LW(5, 4);
     default: return cudaErrorInvalidValue;
   }
 #undef FMDP_LW
