@@ -518,6 +518,9 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   const int xme = (XP && args.x_intra) ? xcl : args.x_me;
   const bool lead = xcl == 0;  // writes the request's outputs (every cluster decides the same)
   const int srank = (XP && args.x_intra) ? xcl : args.shard_rank;
+  // plan shards exist only in the exchange instantiations (MODE 2 / 3): the FCFS walkers stage
+  // whole rows, without the shard's 64-bit divisions in their code
+  const int sworld = (MODE == 2 || MODE == 3) ? args.shard_world : 1;
   const unsigned long long xseq0 = XP ? args.x_seq[xcl] : 0ull;  // step tags continue across launches
   unsigned long long xit = 0;
 
@@ -605,8 +608,8 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       }
       const int64_t K0 = rq.t0 + k;
       const int n0 = row_count(w, K0), n1 = row_count(w, K0 + 1);
-      issue_row(w, K0, n0, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, srank, args.shard_world);
-      issue_row(w, K0 + 1, n1, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, srank, args.shard_world);
+      issue_row(w, K0, n0, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, srank, sworld);
+      issue_row(w, K0 + 1, n1, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, srank, sworld);
     }
     {
       const int64_t K0 = rq.t0 + k;
@@ -725,7 +728,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       //      blocks of the owned actions (from every CTA), the stop flag (from rank 0), V*(a)
       if (tid == NT - 1) {
         if (!evalm && !fin) {
-          issue_row(w, K + 2, cnt2, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, srank, args.shard_world);
+          issue_row(w, K + 2, cnt2, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, srank, sworld);
           cnt2 = row_count(w, K + 3);  // consumed next step: latency hidden by this step
         }
         ctl->nsurv[((k + 1) & 1) * 2] = 0;  // step k+1, chunk 0 (last used in step k-1)
