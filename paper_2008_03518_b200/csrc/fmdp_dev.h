@@ -130,7 +130,8 @@ struct WalkArgs {
 struct XPeer {
   unsigned long long* recv;
 };
-constexpr int XMAX = 8;               // ranks of one exchange (one node)
+constexpr int XMAX = 16;              // ranks of one exchange (clusters of one GPU)
+constexpr int XNODE = 8;              // ranks of a multi-GPU exchange (GPUs of one node)
 inline size_t x_area_bytes(int world, int slot) {
   return (size_t)2 * world * slot * sizeof(unsigned long long);
 }

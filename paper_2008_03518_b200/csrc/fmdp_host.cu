@@ -572,25 +572,37 @@ fmdp_status prepare_requests(fmdp_ctx* ctx, const fmdp_request* reqs, int n, std
   return FMDP_OK;
 }
 
-// Clusters for one request walked alone (fmdp_launch.split): 1, or k clusters of 16 CTAs each
-// over a shard of every row, combined per step by the in-kernel exchange.  Auto: the cost model
-// t(k) = step_cycles(plans / k, 16) + exchange, exchange = 2400 + 1150 (k - 1) cycles
-// (fit to tools/p2p_probe.py at 3000 / 30000 plans, profiles/r01_p2p_probe.txt), k resident at once.
-int split_for(fmdp_ctx* ctx) {
-  if (ctx->launch.split == 1 || (ctx->launch.cluster_size && ctx->launch.cluster_size != 16)) return 1;
-  const int kmax = std::min(fmdp::XMAX, std::min(ctx->num_sms / 16, max_clusters(ctx, 16)));
-  if (kmax < 2) return 1;
-  if (ctx->launch.split >= 2) return std::min(ctx->launch.split, kmax);
+// Clusters for one request walked alone (fmdp_launch.split): 1, or k clusters of G = 16 or 8
+// CTAs each over a shard of every row, combined per step by the in-kernel exchange.  Auto: the
+// cost model t(G, k) = step_cycles(plans / k, G) + exchange, exchange = 2400 + 1150 (k - 1)
+// cycles (fit to tools/p2p_probe.py at 3000 / 30000 plans, profiles/r01_p2p_probe.txt), the
+// k clusters resident at once.  Returns k (1: no split) and the cluster size in *G_out.
+int split_for(fmdp_ctx* ctx, int* G_out) {
+  *G_out = 16;
+  if (ctx->launch.split == 1) return 1;
   const double plans = mean_plans(ctx);
-  int best = 1;
+  int best = 1, bestG = 16;
   double tb = step_cycles(ctx, plans, solo_cluster_size(ctx));
-  for (int k = 2; k <= kmax; ++k) {
-    const double t = step_cycles(ctx, plans / k, 16) + 2400.0 + 1150.0 * (k - 1);
-    if (t < tb - 1e-9) {
-      tb = t;
-      best = k;
+  for (int G : {16, 8}) {
+    if (ctx->launch.cluster_size && ctx->launch.cluster_size != G) continue;
+    const int kmax = std::min(fmdp::XMAX, std::min(ctx->num_sms / G, max_clusters(ctx, G)));
+    if (ctx->launch.split >= 2) {  // forced k: the largest cluster size that fits it
+      if (kmax >= std::min(ctx->launch.split, fmdp::XMAX) || G == 8) {
+        *G_out = G;
+        return std::max(1, std::min(ctx->launch.split, kmax));
+      }
+      continue;
+    }
+    for (int k = 2; k <= kmax; ++k) {
+      const double t = step_cycles(ctx, plans / k, G) + 2400.0 + 1150.0 * (k - 1);
+      if (t < tb - 1e-9) {
+        tb = t;
+        best = k;
+        bestG = G;
+      }
     }
   }
+  *G_out = bestG;
   return best;
 }
 
@@ -647,12 +659,13 @@ fmdp_status check_intra(fmdp_ctx* ctx) {
 
 // One request, alone on the device: a plain walk, or split over k clusters (bit-identical).
 fmdp_status run_single(fmdp_ctx* ctx, const Req& r) {
-  const int k = split_for(ctx);
+  int G = 16;
+  const int k = split_for(ctx, &G);
   if (k <= 1) return run_walk(ctx, {r}, false);
   fmdp::WalkArgs a = make_args(ctx, {r}, false, INT_MAX);
   fmdp_status st = prepare_intra(ctx, k, a);
   if (st) return st;
-  if ((st = run_walk(ctx, {r}, false, INT_MAX, &a, 16, k))) return st;
+  if ((st = run_walk(ctx, {r}, false, INT_MAX, &a, G, k))) return st;
   ctx->stats.split = k;
   return check_intra(ctx);
 }
@@ -1358,7 +1371,7 @@ fmdp_status fmdp_schedule_sharded(fmdp_ctx* ctx, const fmdp_shard* shard, uint64
 
 // ----------------------------------------------------------------------------- in-kernel exchange
 fmdp_status fmdp_p2p_export(fmdp_ctx* ctx, int32_t world, fmdp_p2p_handle* handle, void** dev_ptr) {
-  if (!ctx || !handle || world < 1 || world > fmdp::XMAX) return fail(ctx, FMDP_E_ARG, "world must be 1..8");
+  if (!ctx || !handle || world < 1 || world > fmdp::XNODE) return fail(ctx, FMDP_E_ARG, "world must be 1..8");
   CK(cudaSetDevice(ctx->device));
   CK(cudaStreamSynchronize(ctx->stream));
   x_release(ctx);
