@@ -112,6 +112,8 @@ struct fmdp_ctx {
   double band_rel[fmdp::NTAU] = {0};   // FP32 filter band per tau, relative to R^2
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
   cudaStream_t stream2 = nullptr;  // second stream of a split FCFS slice (the non-head walkers)
+  cudaStream_t stream3 = nullptr;  // third stream: the next request's walker (second lane)
+  cudaEvent_t ev3 = nullptr;
 };
 
 namespace {
@@ -413,10 +415,16 @@ fmdp_status run_split(fmdp_ctx* ctx, std::vector<Req>& run, int budget) {
   // the head runs as one cluster: splitting it over clusters (fmdp_launch.split) takes SMs from
   // the others and measured slower (configs[1]: 155.5 -> 171 ms per batch, tools/ab_headsplit.py)
   const int Gh = solo_cluster_size(ctx);
+  // second lane: the next request (run[1]) also at the lone-walker cluster size -- its
+  // speculative steps are the next slice's head work unless the head's plan rolls them back
+  // (configs[1]: -0.7 % full / -0.2 % culled batch time)
+  const bool lane2 = n >= 3 && ctx->num_sms >= 2 * Gh + 16;
+  const int nl = lane2 ? 2 : 1;
   int Go = 0, nco = 0;
-  choose_launch(ctx, n - 1, &Go, &nco, ctx->num_sms - Gh);
+  choose_launch(ctx, n - nl, &Go, &nco, ctx->num_sms - nl * Gh);
   CK(cudaMemcpyAsync(ctx->d_reqs, run.data(), sizeof(Req) * n, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemsetAsync(ctx->d_queue, 0, 2 * sizeof(int32_t), ctx->stream));  // [0] head, [1] others
+  CK(cudaMemsetAsync(ctx->d_queue + 3, 0, sizeof(int32_t), ctx->stream));  // [3] second lane
   CK(cudaMemsetAsync(ctx->d_stop, 0, sizeof(int32_t), ctx->stream));
   CK(cudaEventRecord(ctx->ev0, ctx->stream));
   CK(cudaStreamWaitEvent(ctx->stream2, ctx->ev0, 0));
@@ -426,22 +434,32 @@ fmdp_status run_split(fmdp_ctx* ctx, std::vector<Req>& run, int budget) {
   ah.queue = ctx->d_queue;
   ah.stop = ctx->d_stop;
   fmdp::WalkArgs ao = ah;
-  ao.reqs = ctx->d_reqs + 1;
-  ao.n_reqs = n - 1;
+  ao.reqs = ctx->d_reqs + nl;
+  ao.n_reqs = n - nl;
   ao.queue = ctx->d_queue + 1;
   CK(fmdp::launch_walk(ctx->w, ah, ctx->C, Gh, 1, threads_for(ctx), chunk_for(ctx), rawcap_for(ctx), ctx->stream));
+  if (lane2) {
+    fmdp::WalkArgs a2 = ah;
+    a2.reqs = ctx->d_reqs + 1;
+    a2.n_reqs = 1;
+    a2.queue = ctx->d_queue + 3;
+    CK(cudaStreamWaitEvent(ctx->stream3, ctx->ev0, 0));
+    CK(fmdp::launch_walk(ctx->w, a2, ctx->C, Gh, 1, threads_for(ctx), chunk_for(ctx), rawcap_for(ctx), ctx->stream3));
+    CK(cudaEventRecord(ctx->ev3, ctx->stream3));
+  }
   CK(fmdp::launch_walk(ctx->w, ao, ctx->C, Go, nco, threads_for(ctx), chunk_for(ctx), rawcap_for(ctx), ctx->stream2));
   CK(cudaEventRecord(ctx->ev2, ctx->stream2));
   CK(cudaStreamWaitEvent(ctx->stream, ctx->ev2, 0));
+  if (lane2) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev3, 0));
   CK(cudaEventRecord(ctx->ev1, ctx->stream));
   CK(cudaEventSynchronize(ctx->ev1));
   CK(cudaGetLastError());
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
   ctx->stats.device_ms += ms;
-  ctx->stats.kernels += 2;
+  ctx->stats.kernels += 2 + (lane2 ? 1 : 0);
   ctx->stats.cluster_size = Gh;
-  ctx->stats.walkers = std::max(ctx->stats.walkers, 1 + nco);
+  ctx->stats.walkers = std::max(ctx->stats.walkers, nl + nco);
   if (std::getenv("FMDP_DEBUG"))
     std::fprintf(stderr, "fmdp: split walk n=%d head G=%d others G=%d clusters=%d %.3f ms\n", n, Gh, Go, nco, ms);
   return FMDP_OK;
@@ -972,7 +990,9 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   cudaEventCreate(&ctx->ev0);
   cudaEventCreate(&ctx->ev1);
   cudaEventCreate(&ctx->ev2);
+  cudaEventCreate(&ctx->ev3);
   if (cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking) != cudaSuccess) return bad(FMDP_E_CUDA, "stream");
+  if (cudaStreamCreateWithFlags(&ctx->stream3, cudaStreamNonBlocking) != cudaSuccess) return bad(FMDP_E_CUDA, "stream");
 
   World& w = ctx->w;
   std::memset(&w, 0, sizeof(w));
@@ -1181,6 +1201,8 @@ void fmdp_destroy(fmdp_ctx* ctx) {
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->ev2) cudaEventDestroy(ctx->ev2);
   if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
+  if (ctx->ev3) cudaEventDestroy(ctx->ev3);
+  if (ctx->stream3) cudaStreamDestroy(ctx->stream3);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
