@@ -63,7 +63,7 @@ lines.append("")
 traffic = None
 import os
 for rep, kern, title in (('walk_batch', 'walk_kernel<3, 0>', 'configs[1] batch, first slice head (full path)'),
-                         ('walk_cull2', 'walk_kernel<3, 0>', 'configs[1] request, f1 culling, G=2'),
+                         ('walk_cull2', 'walk_kernel<3, 4>', 'configs[1] request, f1 culling, G=2'),
                          ('walk_c5split', 'walk_kernel<5, 2>', 'configs[4] 1M plans, A = 85, split request (full path)')):
     if not os.path.exists(f'gpurun_out/{rep}.ncu-rep'):
         continue
