@@ -179,10 +179,18 @@ def run_native(args):
     rank, world, local = dist_env()
     import numpy as np
     import torch
+    # FMDP_BENCH_SAME_DEVICE=1 (testing the N > 1 code path on a one-GPU box): every rank on
+    # device 0, gloo for the host-side collectives; the ranks' kernels then only time-slice
+    same = os.environ.get("FMDP_BENCH_SAME_DEVICE") == "1"
+    if same:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if same:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import fmdp_synth as fs
     from paper_2008_03518_b200.fmdp import FMDP, Request, Result, pack_plans
 
