@@ -218,3 +218,27 @@ def test_split_request_bit_identical(split, cull):
     assert ref.stats()["split"] == 0 or ref.stats()["split"] == 1
     ref.close()
     ctx.close()
+
+
+@pytest.mark.parametrize("air,split", [(dict(valuation=1), 3),
+                                       (dict(turn_steps=tuple(range(-8, 9)), climb_units=(-32, -16, 0, 16, 32)), 4)])
+def test_split_request_variants(air, split):
+    """The split request with Alg 1 endpoint valuation and with 17 x 5 = 85 actions
+    (configs[4] action set, C = 5): identical to one cluster."""
+    from paper_2008_03518_b200.fmdp import FMDP
+    sc = fs.random_small(73, n_plans=300, n_requests=3, half_m=1500.0, n_buildings=20, max_steps=400, t0_max=40,
+                         **air)
+    ref = FMDP(sc.airspace, sc.terrain)
+    ref.add_plans(sc.plans)
+    ref.set_launch(split=1)
+    ctx = FMDP(sc.airspace, sc.terrain)
+    ctx.add_plans(sc.plans)
+    ctx.set_launch(split=split)
+    for i in range(sc.n_requests):
+        a = ref.schedule(sc.src[i], sc.dst[i], int(sc.t0[i]))
+        b = ctx.schedule(sc.src[i], sc.dst[i], int(sc.t0[i]))
+        assert ctx.stats()["split"] >= 2
+        assert a.status == b.status and a.n_states == b.n_states and (a.traj == b.traj).all()
+        assert a.min_sep_m == b.min_sep_m and a.n_near_ties == b.n_near_ties
+    ref.close()
+    ctx.close()
