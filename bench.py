@@ -395,10 +395,11 @@ def run_native(args):
             c.set_launch(cull=cull)
             return row(ms, steps, st, s_["cluster_size"], max(1, s_["split"])), st
 
-        def run_p2p(cs, cull, n_world):
-            # every rank takes part in every collective, also after a failed call (reported)
+        def run_p2p(cs, cull, n_world, split=0):
+            # every rank takes part in every collective, also after a failed call (reported);
+            # split: clusters per rank (0 = cost model, 1 = one: the ranks sharing one GPU)
             for c in cs:
-                c.set_launch(cull=cull)
+                c.set_launch(cull=cull, split=split)
             ms = steps = 0
             st, errs = [], []
             for i in reqs:
@@ -415,7 +416,8 @@ def run_native(args):
                 ms += max_over_ranks(t, n_world)
                 for c in cs:
                     c.truncate(P)
-            out_row = row(ms, steps, st, cs[0].stats()["cluster_size"])
+            st0 = cs[0].stats()
+            out_row = row(ms, steps, st, st0["cluster_size"], max(1, st0["split"]))
             if errs:
                 out_row["errors"] = errs[:2]
             return out_row, st
@@ -440,12 +442,14 @@ def run_native(args):
             ctxs = [base] + [mk() for _ in range(max(rank_counts) - 1)]
             _log(f"c4: {len(ctxs)} contexts loaded")
             out["p2p"] = []
-            for R in rank_counts:
+            # ranks sharing this GPU: one cluster each (R x 16 CTAs resident), and the two-level
+            # exchange with 2 ranks x 3 clusters
+            for R, k in [(r_, 1) for r_ in rank_counts] + [(2, 3)]:
                 p2p_connect_local(ctxs[:R])
-                e = {"ranks": R}
+                e = {"ranks": R, "clusters_per_rank": k}
                 for cull in (0, 1):
-                    e["culled" if cull else "full"], st = run_p2p(ctxs[:R], cull, 1)
-                    _log(f"c4: p2p ranks={R} cull={cull} {e['culled' if cull else 'full']}")
+                    e["culled" if cull else "full"], st = run_p2p(ctxs[:R], cull, 1, split=k)
+                    _log(f"c4: p2p ranks={R} x{k} cull={cull} {e['culled' if cull else 'full']}")
                     e["same_status_as_single"] = st == want
                 out["p2p"].append(e)
             for c in ctxs:

@@ -120,7 +120,11 @@ struct WalkArgs {
   unsigned long long* x_seq;          // this rank's exchange sequence number (step tags)
   int32_t* x_err;                     // set on a poll timeout (a peer is not running)
   int32_t x_intra;                    // 1: the launch's clusters are the ranks (x_me = cluster
-                                      // index, x_world = clusters; x_seq / queue per cluster)
+                                      // index, x_world = clusters; x_seq / queue per cluster;
+                                      // plan shard = shard_rank + cluster index of shard_world)
+  int32_t x_inter;                    // 1: two-level exchange -- after the clusters of this GPU,
+  int32_t x_iworld, x_ime;            //    cluster c of each of the x_iworld GPUs (this: x_ime)
+  const XPeer* x_ipeers;              //    [XMAX clusters][XNODE GPUs] receive areas
 };
 
 // One rank's exchange area as seen from this GPU (peer pointer: IPC-opened or same process):

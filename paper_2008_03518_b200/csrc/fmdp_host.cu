@@ -95,6 +95,13 @@ struct fmdp_ctx {
   fmdp::XPeer* d_xin_peers = nullptr;        // [XMAX]
   unsigned long long* d_xin_seq = nullptr;   // [XMAX] per-cluster sequence, then int32 error, queues
   int xin_world = 0;                         // cluster count of the last split launch (layout)
+  // multi-GPU two-level exchange: inter-GPU areas of every cluster index, this GPU's intra
+  // level (areas, peers, monotonic per-cluster tag sequence + error flag + queues)
+  fmdp::XPeer* d_ipeers = nullptr;           // [XMAX][XNODE]
+  unsigned long long* d_xh_area = nullptr;
+  fmdp::XPeer* d_xh_peers = nullptr;         // [XMAX]
+  unsigned long long* d_xh_seq = nullptr;    // [XMAX] sequence, then int32 error, then int32 queues
+  unsigned long long xh_seq = 0;             // common tag sequence of every cluster (host copy)
   unsigned long long* d_xseq = nullptr;    // [1] sequence, then [1] int32 error flag
   double *d_dbg_vstar = nullptr, *d_dbg_v = nullptr, *d_dbg_s = nullptr;
   uint32_t* d_dbg_conf = nullptr;
@@ -1401,7 +1408,7 @@ fmdp_status fmdp_p2p_export(fmdp_ctx* ctx, int32_t world, fmdp_p2p_handle* handl
   if (!ctx->d_xseq) ctx->d_xseq = (unsigned long long*)dalloc(ctx, 2 * sizeof(unsigned long long));  // seq, error
   if (!ctx->d_xpeers || !ctx->d_xseq) return fail(ctx, FMDP_E_NOMEM, "exchange tables");
   const int slot = ((ctx->A * ctx->W * fmdp::NTAU + 16) + 3) & ~3;
-  const size_t bytes = fmdp::x_area_bytes(world, slot);
+  const size_t bytes = fmdp::x_area_bytes(world, slot) * fmdp::XMAX;  // one area per cluster index
   if (cudaMalloc(&ctx->x_area, bytes) != cudaSuccess) {
     cudaGetLastError();
     ctx->x_area = nullptr;
@@ -1432,6 +1439,15 @@ fmdp_status fmdp_p2p_connect(fmdp_ctx* ctx, int32_t rank, int32_t world, const f
   ctx->x_ipc.clear();
   ctx->x_me = -1;
   std::vector<fmdp::XPeer> tab(fmdp::XMAX, fmdp::XPeer{nullptr});
+  std::vector<fmdp::XPeer> itab((size_t)fmdp::XMAX * fmdp::XNODE, fmdp::XPeer{nullptr});
+  const size_t hwords = fmdp::x_area_bytes(fmdp::XMAX, ctx->x_slot) / sizeof(unsigned long long);
+  if (!ctx->d_ipeers) ctx->d_ipeers = (fmdp::XPeer*)dalloc(ctx, sizeof(fmdp::XPeer) * itab.size());
+  if (!ctx->d_xh_area) ctx->d_xh_area = (unsigned long long*)dalloc(ctx, sizeof(unsigned long long) * hwords * fmdp::XMAX);
+  if (!ctx->d_xh_peers) ctx->d_xh_peers = (fmdp::XPeer*)dalloc(ctx, sizeof(fmdp::XPeer) * fmdp::XMAX);
+  if (!ctx->d_xh_seq)
+    ctx->d_xh_seq = (unsigned long long*)dalloc(ctx, sizeof(unsigned long long) * (2 * fmdp::XMAX + 1));
+  if (!ctx->d_ipeers || !ctx->d_xh_area || !ctx->d_xh_peers || !ctx->d_xh_seq)
+    return fail(ctx, FMDP_E_NOMEM, "exchange tables");
   for (int q = 0; q < world; ++q) {
     void* base = nullptr;
     if (q == rank) {
@@ -1457,10 +1473,22 @@ fmdp_status fmdp_p2p_connect(fmdp_ctx* ctx, int32_t rank, int32_t world, const f
       ctx->x_ipc.push_back(base);
     }
     tab[q].recv = reinterpret_cast<unsigned long long*>(base);
+    for (int c = 0; c < fmdp::XMAX; ++c)  // cluster c's area on GPU q
+      itab[(size_t)c * fmdp::XNODE + q].recv =
+          reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(base) + c * fmdp::x_area_bytes(world, ctx->x_slot));
   }
   CK(cudaMemcpy(ctx->d_xpeers, tab.data(), sizeof(fmdp::XPeer) * fmdp::XMAX, cudaMemcpyHostToDevice));
   CK(cudaMemset(ctx->d_xseq, 0, 2 * sizeof(unsigned long long)));
-  CK(cudaMemset(ctx->x_area, 0, fmdp::x_area_bytes(world, ctx->x_slot)));  // tags restart with the sequence
+  CK(cudaMemset(ctx->x_area, 0, fmdp::x_area_bytes(world, ctx->x_slot) * fmdp::XMAX));  // tags restart
+  CK(cudaMemcpy(ctx->d_ipeers, itab.data(), sizeof(fmdp::XPeer) * itab.size(), cudaMemcpyHostToDevice));
+  {  // this GPU's level: cluster q's area
+    std::vector<fmdp::XPeer> htab(fmdp::XMAX, fmdp::XPeer{nullptr});
+    for (int q = 0; q < fmdp::XMAX; ++q) htab[q].recv = ctx->d_xh_area + (size_t)q * hwords;
+    CK(cudaMemcpy(ctx->d_xh_peers, htab.data(), sizeof(fmdp::XPeer) * fmdp::XMAX, cudaMemcpyHostToDevice));
+  }
+  CK(cudaMemset(ctx->d_xh_area, 0, sizeof(unsigned long long) * hwords * fmdp::XMAX));
+  CK(cudaMemset(ctx->d_xh_seq, 0, sizeof(unsigned long long) * (2 * fmdp::XMAX + 1)));
+  ctx->xh_seq = 0;
   CK(cudaDeviceSynchronize());
   ctx->x_me = rank;
   return FMDP_OK;
@@ -1484,22 +1512,55 @@ fmdp_status fmdp_schedule_p2p(fmdp_ctx* ctx, uint64_t aircraft_id, fmdp_vec3 src
   if ((st = ensure_slots(ctx, 1))) return st;
   CK(cudaMemsetAsync(ctx->d_pairctr, 0, sizeof(unsigned long long), ctx->stream));
   CK(cudaMemsetAsync(ctx->d_prof, 0, sizeof(unsigned long long) * fmdp::N_PHASES, ctx->stream));
-  ctx->shard_rank = ctx->x_me;
-  ctx->shard_world = ctx->x_world;
-  ctx->xmode = 3;
-  const int G = solo_cluster_size(ctx);  // identical on every rank (identical stores, settings)
-  const fmdp::WalkArgs a = make_args(ctx, base, false, INT_MAX);
-  st = run_walk(ctx, base, false, INT_MAX, &a, G, 1);
-  ctx->xmode = 0;
-  ctx->shard_rank = 0;
+  // two-level exchange: k clusters on every GPU (the split cost model on this GPU's shard; the
+  // same k on every rank: identical stores, settings and devices), cluster c of each GPU
+  // exchanging with cluster c of every other GPU
+  const int N = ctx->x_world, me = ctx->x_me;
+  ctx->shard_world = N;
+  int G = 16;
+  int k = split_for(ctx, &G);
+  if (k <= 1) {
+    k = 1;
+    G = solo_cluster_size(ctx);
+  }
   ctx->shard_world = 1;
+  unsigned long long* seq = ctx->d_xh_seq;
+  int32_t* err = reinterpret_cast<int32_t*>(seq + fmdp::XMAX);
+  int32_t* queue = reinterpret_cast<int32_t*>(seq + fmdp::XMAX + 1);
+  {  // every cluster starts from the common sequence (monotonic: no stale tag can match)
+    std::vector<unsigned long long> s0(fmdp::XMAX, ctx->xh_seq);
+    CK(cudaMemcpyAsync(seq, s0.data(), sizeof(unsigned long long) * fmdp::XMAX, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemsetAsync(queue, 0, sizeof(int32_t) * fmdp::XMAX, ctx->stream));
+  }
+  ctx->xmode = 3;
+  fmdp::WalkArgs a = make_args(ctx, base, false, INT_MAX);
+  ctx->xmode = 0;
+  a.xmode = 3;
+  a.x_intra = 1;
+  a.x_me = 0;
+  a.x_world = k;
+  a.x_slot = ctx->x_slot;
+  a.x_peers = ctx->d_xh_peers;
+  a.x_seq = seq;
+  a.x_err = err;
+  a.queue = queue;
+  a.shard_rank = me * k;
+  a.shard_world = N * k;
+  a.x_inter = 1;
+  a.x_iworld = N;
+  a.x_ime = me;
+  a.x_ipeers = ctx->d_ipeers;
+  st = run_walk(ctx, base, false, INT_MAX, &a, G, k);
   if (st) return st;
-  int32_t xerr = 0;
-  CK(cudaMemcpy(&xerr, ctx->d_xseq + 1, sizeof(xerr), cudaMemcpyDeviceToHost));
-  if (xerr) {
+  ctx->stats.split = k;
+  unsigned long long tail[2] = {0, 0};  // cluster 0's sequence, error flag
+  CK(cudaMemcpy(tail, seq, sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&tail[1], seq + fmdp::XMAX, sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  if ((int32_t)tail[1]) {
     ctx->x_me = -1;
     return fail(ctx, FMDP_E_CUDA, "peer exchange timed out (a rank did not call fmdp_schedule_p2p)");
   }
+  ctx->xh_seq = tail[0];
   if ((st = fetch_out(ctx, 1))) return st;
   ctx->stats.steps += ctx->h_out[0].steps_run;
   ctx->stats.rounds += 1;

@@ -172,6 +172,7 @@ struct Ctl {
   int32_t stop[2];            // head-finished flag seen by rank 0 at the top of the step, by parity
   uint32_t xstay[2];          // multi-GPU: nearest-plan d^2 over the ranks (from CTA 0), by parity
   unsigned long long* xp[XMAX];  // multi-GPU: every rank's receive area (loaded once per launch)
+  unsigned long long* xip[XNODE];  // two-level exchange: cluster xcl's area on every GPU
 };
 static_assert(sizeof(Ctl) <= 512, "Ctl exceeds its shared-memory slot (Layout::o_ctl)");
 
@@ -376,6 +377,15 @@ __device__ __forceinline__ uint32_t x_stay_min(const unsigned long long* own, in
   return __reduce_min_sync(0xffffffffu, v);
 }
 
+// Second level of the nearest-plan exchange: this GPU's value -> cluster xcl of every other GPU
+// (lane q -> GPU q), then the minimum over the GPUs.  Warp 0 of CTA 0; every lane gets it.
+__device__ __forceinline__ uint32_t x_stay_inter(unsigned long long* const* xip, int me, int world, int slot, int par,
+                                                 uint32_t tag, uint32_t m, int32_t* err, long long budget) {
+  const int lane = threadIdx.x & 31;
+  if (lane < world && lane != me) st_ll(xip[lane] + x_word(par, world, me, slot, slot - 16), m, tag);
+  return x_stay_min(xip[me], me, world, slot, par, tag, m, err, budget);
+}
+
 // G-way minimum of one (state, tau) item over the partial blocks of the cluster's CTAs
 __device__ __forceinline__ float gway_min(const float* src, int G, int sstride) {
   float M0 = src[0], M1 = FLT_MAX, M2 = FLT_MAX, M3 = FLT_MAX;
@@ -566,8 +576,11 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   // clusters); otherwise this launch is rank x_me of a multi-GPU exchange
   const int xcl = (XP && args.x_intra) ? (int)(blockIdx.x / G) : 0;
   const int xme = (XP && args.x_intra) ? xcl : args.x_me;
+  // two-level exchange (x_inter): the clusters of this GPU first (xme / x_world, above), then
+  // cluster xcl of every GPU (rank x_ime of x_iworld) over NVLink
+  const bool xinter = XP && args.x_inter;
   const bool lead = xcl == 0;  // writes the request's outputs (every cluster decides the same)
-  const int srank = (XP && args.x_intra) ? xcl : args.shard_rank;
+  const int srank = (XP && args.x_intra) ? args.shard_rank + xcl : args.shard_rank;
   // plan shards exist only in the exchange instantiations (MODE 2 / 3): the FCFS walkers stage
   // whole rows, without the shard's 64-bit divisions in their code
   const int sworld = (MODE == 2 || MODE == 3) ? args.shard_world : 1;
@@ -596,6 +609,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (XP && tid < args.x_world) ctl->xp[tid] = args.x_peers[tid].recv;
+  if (xinter && tid < args.x_iworld) ctl->xip[tid] = args.x_ipeers[xcl * XNODE + tid].recv;
   __syncthreads();
   uint32_t par = 0;      // next wait parity per ring buffer (bit b)
   uint32_t parX = 0;     // next wait parity of the exchange mbarriers: bits 0-1 reduce-scatter, 2-3 V*
@@ -1083,8 +1097,10 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           st_ll(ctl->xp[tid] + x_word(xpar, args.x_world, xme, args.x_slot, args.x_slot - 16), stay_all, xtag);
         if (fin) {  // no owner epilogue in this step: CTA 0 collects the peers' values, broadcasts
           if (rank == 0 && warp == 0) {
-            const uint32_t m = x_stay_min(ctl->xp[xme], xme, args.x_world, args.x_slot, xpar, xtag,
-                                          stay_all, args.x_err, x_budget(xit));
+            uint32_t m = x_stay_min(ctl->xp[xme], xme, args.x_world, args.x_slot, xpar, xtag,
+                                    stay_all, args.x_err, x_budget(xit));
+            if (xinter) m = x_stay_inter(ctl->xip, args.x_ime, args.x_iworld, args.x_slot, xpar, xtag, m, args.x_err,
+                                         x_budget(xit));
             if (lane < (int)G) cluster.map_shared_rank(ctl, lane)->xstay[p] = m;
           }
           cluster.sync();
@@ -1125,6 +1141,14 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           } else if (XP) {  // this GPU's minimum (sent below) and the peers' minima
             M = x_min_peers(ctl->xp[xme], xme, args.x_world, args.x_slot, xpar, st * NTAU + t,
                             xtag, args.x_err, x_budget(xit), s_M[i]);
+            if (xinter) {  // this GPU's minimum -> cluster xcl of every other GPU, then theirs
+              const int io = st * NTAU + t;
+              for (int q = 0; q < args.x_iworld; ++q)
+                if (q != args.x_ime)
+                  st_ll(ctl->xip[q] + x_word(xpar, args.x_iworld, args.x_ime, args.x_slot, io), __float_as_uint(M), xtag);
+              M = x_min_peers(ctl->xip[args.x_ime], args.x_ime, args.x_iworld, args.x_slot, xpar, io, xtag, args.x_err,
+                              x_budget(xit), M);
+            }
           } else {
             M = gway_min(rcv + oa * BLK + r2, (int)G, NOWN * BLK);
             if (xmode == 1) args.xbuf[st * NTAU + t] = __float_as_uint(M);  // this GPU's minima
@@ -1143,8 +1167,10 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           s_M[i] = out;
         }
         if (XP && rank == 0 && warp == 0) {  // -> every CTA with its V* pushes (one reader per value)
-          const uint32_t m = x_stay_min(ctl->xp[xme], xme, args.x_world, args.x_slot, xpar, xtag, stay_all,
-                                        args.x_err, x_budget(xit));
+          uint32_t m = x_stay_min(ctl->xp[xme], xme, args.x_world, args.x_slot, xpar, xtag, stay_all,
+                                  args.x_err, x_budget(xit));
+          if (xinter) m = x_stay_inter(ctl->xip, args.x_ime, args.x_iworld, args.x_slot, xpar, xtag, m, args.x_err,
+                                       x_budget(xit));
           if (lane < (int)G)
             st_async_u32(mapa_u32(smem_u32(&ctl->xstay[p]), lane), m, mapa_u32(smem_u32(&s_bar[5 + p]), lane));
         }

@@ -86,13 +86,13 @@ def test_sharded_two_ranks_bit_identical(tmp_path):
 # process, each walker on its own stream; the protocol (P2P stores, step tags, parity buffers)
 # is the one the NVLink peers use, only the pointers are local.
 
-def _p2p_ranks(sc, world, cull=0):
+def _p2p_ranks(sc, world, cull=0, split=0):
     from paper_2008_03518_b200.fmdp import FMDP, p2p_connect_local
     ctxs = []
     for _ in range(world):
         c = FMDP(sc.airspace, sc.terrain)
         c.add_plans(sc.plans)
-        c.set_launch(cull=cull)
+        c.set_launch(cull=cull, split=split)
         ctxs.append(c)
     p2p_connect_local(ctxs)
     return ctxs
@@ -105,16 +105,22 @@ def _p2p_call(ctxs, src, dst, t0):
         return [f.result(timeout=120) for f in futs]
 
 
-@pytest.mark.parametrize("world,cull", [(1, 0), (2, 0), (3, 1), (4, 0)])
-def test_p2p_bit_identical_to_one_gpu(world, cull):
+@pytest.mark.parametrize("world,cull,split", [(1, 0, 0), (2, 0, 0), (3, 1, 0), (4, 0, 0),
+                                              (2, 0, 2), (2, 1, 3), (3, 0, 2)])
+def test_p2p_bit_identical_to_one_gpu(world, cull, split):
+    """split >= 2: the two-level exchange -- `split` clusters per rank exchange among themselves,
+    then cluster c of every rank with cluster c of the others."""
     from paper_2008_03518_b200.fmdp import FMDP
     sc = _scenario()
     ref = FMDP(sc.airspace, sc.terrain)
     ref.add_plans(sc.plans)
-    ctxs = _p2p_ranks(sc, world, cull)
+    ref.set_launch(split=1)
+    ctxs = _p2p_ranks(sc, world, cull, split)
     for i in range(sc.n_requests):
         want = ref.schedule(sc.src[i], sc.dst[i], int(sc.t0[i]))
         got = _p2p_call(ctxs, sc.src[i], sc.dst[i], int(sc.t0[i]))
+        if split:
+            assert all(c.stats()["split"] == split for c in ctxs)
         for g in got:  # every rank took every decision identically, appended the same plan
             assert g.status == want.status and g.n_states == want.n_states
             assert (g.traj == want.traj).all()

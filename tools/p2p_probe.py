@@ -41,6 +41,8 @@ def main(plan_counts=(0, 3000, 30000), ranks=(1, 2, 4), reps=3):
                 best = v if best is None else min(best, v)
             row = {"plans": P, "cull": cull, "single_us_per_step": round(best, 2), "G": s["cluster_size"]}
             for R in ranks:
+                for c in ctxs[:R]:  # ranks sharing this GPU: one cluster each
+                    c.set_launch(cull=cull, split=1)
                 p2p_connect_local(ctxs[:R])
                 best = None
                 for _ in range(reps):
@@ -83,6 +85,8 @@ def phases(P=3000):
                       "phases": per_step(ctxs[0].stats())}), flush=True)
     ctxs[0].truncate(P)
     for R in (1, 2):
+        for c in ctxs[:R]:
+            c.set_launch(profile=1, split=1)
         p2p_connect_local(ctxs[:R])
         with ThreadPoolExecutor(R) as ex:
             list(ex.map(lambda c: c.schedule_p2p(sc.src[i], sc.dst[i], int(sc.t0[i]), want_traj=False), ctxs[:R]))
