@@ -245,11 +245,15 @@ fmdp_status fmdp_schedule_sharded(fmdp_ctx* ctx, const fmdp_shard* shard, uint64
  * NVLink / NVSwitch) and polls its own area until the peers' words carry this step's tag (value
  * and readiness arrive together: no fence, no flag); CTA 0 does the same for the nearest-plan
  * distance and broadcasts the minimum over its cluster.  Every rank then decides identically,
- * so results are bit-identical to one GPU.
+ * so results are bit-identical to one GPU.  Each rank may run k clusters (fmdp_launch.split,
+ * auto from the cost model on its shard; every rank must use the same settings): the clusters
+ * of a GPU first exchange among themselves, then cluster c of every GPU with cluster c of the
+ * others (two-level exchange; plan shard g*k + c of N*k).
  *
  * Setup (collective, once, before any fmdp_schedule_p2p):
  *   1. fmdp_p2p_export(ctx, world, &handle, &ptr): allocates this rank's exchange area
- *      (cudaMalloc, zeroed: 2 * world * (A*W*5 + 16) 8-byte words) and returns its CUDA IPC
+ *      (cudaMalloc, zeroed: 16 cluster blocks of 2 * world * (A*W*5 + 16) 8-byte words) and
+ *      returns its CUDA IPC
  *      handle (64 bytes; zeroed if IPC is unavailable) and its device pointer.
  *   2. exchange (handle, ptr) among the ranks (e.g. torch.distributed.all_gather_object).
  *   3. fmdp_p2p_connect(ctx, rank, world, handles[world], ptrs[world]): peer q's area is
