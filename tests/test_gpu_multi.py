@@ -248,3 +248,24 @@ def test_split_request_variants(air, split):
         assert a.min_sep_m == b.min_sep_m and a.n_near_ties == b.n_near_ties
     ref.close()
     ctx.close()
+
+
+def test_p2p_cluster_count_changes_between_requests():
+    """The two-level exchange's tag sequence is monotonic across launches: changing the number
+    of clusters per rank between requests on one connection (2 -> 1 -> 3 -> 2) never lets a
+    stale word match, and every request stays identical to one GPU."""
+    from paper_2008_03518_b200.fmdp import FMDP
+    sc = fs.random_small(71, n_plans=300, n_requests=4, half_m=1500.0, n_buildings=30, max_steps=400, t0_max=40)
+    ref = FMDP(sc.airspace, sc.terrain)
+    ref.add_plans(sc.plans)
+    ref.set_launch(split=1)
+    ctxs = _p2p_ranks(sc, 2)
+    for i, k in enumerate((2, 1, 3, 2)):
+        for c in ctxs:
+            c.set_launch(split=k)
+        want = ref.schedule(sc.src[i], sc.dst[i], int(sc.t0[i]))
+        got = _p2p_call(ctxs, sc.src[i], sc.dst[i], int(sc.t0[i]))
+        for g in got:
+            assert g.status == want.status and g.n_states == want.n_states and (g.traj == want.traj).all()
+    for c in ctxs + [ref]:
+        c.close()
