@@ -380,9 +380,9 @@ __device__ __forceinline__ uint32_t x_stay_min(const unsigned long long* own, in
 // Second level of the nearest-plan exchange: this GPU's value -> cluster xcl of every other GPU
 // (lane q -> GPU q), then the minimum over the GPUs.  Warp 0 of CTA 0; every lane gets it.
 __device__ __forceinline__ uint32_t x_stay_inter(unsigned long long* const* xip, int me, int world, int slot, int par,
-                                                 uint32_t tag, uint32_t m, int32_t* err, long long budget) {
+                                                 uint32_t tag, uint32_t m, int32_t* err, long long budget, bool send) {
   const int lane = threadIdx.x & 31;
-  if (lane < world && lane != me) st_ll(xip[lane] + x_word(par, world, me, slot, slot - 16), m, tag);
+  if (send && lane < world && lane != me) st_ll(xip[lane] + x_word(par, world, me, slot, slot - 16), m, tag);
   return x_stay_min(xip[me], me, world, slot, par, tag, m, err, budget);
 }
 
@@ -1095,12 +1095,15 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         xpar = (int)((xseq0 + xit) & 1ull);
         if (rank == 0 && tid < args.x_world && tid != xme)  // lane q -> rank q
           st_ll(ctl->xp[tid] + x_word(xpar, args.x_world, xme, args.x_slot, args.x_slot - 16), stay_all, xtag);
+        // one cluster per GPU: this value is already the GPU's -> the other GPUs right away
+        if (xinter && args.x_world == 1 && rank == 0 && tid < args.x_iworld && tid != args.x_ime)
+          st_ll(ctl->xip[tid] + x_word(xpar, args.x_iworld, args.x_ime, args.x_slot, args.x_slot - 16), stay_all, xtag);
         if (fin) {  // no owner epilogue in this step: CTA 0 collects the peers' values, broadcasts
           if (rank == 0 && warp == 0) {
             uint32_t m = x_stay_min(ctl->xp[xme], xme, args.x_world, args.x_slot, xpar, xtag,
                                     stay_all, args.x_err, x_budget(xit));
             if (xinter) m = x_stay_inter(ctl->xip, args.x_ime, args.x_iworld, args.x_slot, xpar, xtag, m, args.x_err,
-                                         x_budget(xit));
+                                         x_budget(xit), args.x_world > 1);
             if (lane < (int)G) cluster.map_shared_rank(ctl, lane)->xstay[p] = m;
           }
           cluster.sync();
@@ -1129,6 +1132,11 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
               if (q != xme)
                 st_ll(ctl->xp[q] + x_word(xpar, args.x_world, xme, args.x_slot, io), __float_as_uint(M),
                       xtag);
+            if (xinter && args.x_world == 1)  // one cluster per GPU: straight to the other GPUs
+              for (int q = 0; q < args.x_iworld; ++q)
+                if (q != args.x_ime)
+                  st_ll(ctl->xip[q] + x_word(xpar, args.x_iworld, args.x_ime, args.x_slot, io), __float_as_uint(M),
+                        xtag);
           }
         }
         for (int i = tid; i < nitem; i += NT) {
@@ -1143,9 +1151,11 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
                             xtag, args.x_err, x_budget(xit), s_M[i]);
             if (xinter) {  // this GPU's minimum -> cluster xcl of every other GPU, then theirs
               const int io = st * NTAU + t;
-              for (int q = 0; q < args.x_iworld; ++q)
-                if (q != args.x_ime)
-                  st_ll(ctl->xip[q] + x_word(xpar, args.x_iworld, args.x_ime, args.x_slot, io), __float_as_uint(M), xtag);
+              if (args.x_world > 1)  // (one cluster per GPU: sent with the first level above)
+                for (int q = 0; q < args.x_iworld; ++q)
+                  if (q != args.x_ime)
+                    st_ll(ctl->xip[q] + x_word(xpar, args.x_iworld, args.x_ime, args.x_slot, io), __float_as_uint(M),
+                          xtag);
               M = x_min_peers(ctl->xip[args.x_ime], args.x_ime, args.x_iworld, args.x_slot, xpar, io, xtag, args.x_err,
                               x_budget(xit), M);
             }
@@ -1170,7 +1180,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           uint32_t m = x_stay_min(ctl->xp[xme], xme, args.x_world, args.x_slot, xpar, xtag, stay_all,
                                   args.x_err, x_budget(xit));
           if (xinter) m = x_stay_inter(ctl->xip, args.x_ime, args.x_iworld, args.x_slot, xpar, xtag, m, args.x_err,
-                                       x_budget(xit));
+                                       x_budget(xit), args.x_world > 1);
           if (lane < (int)G)
             st_async_u32(mapa_u32(smem_u32(&ctl->xstay[p]), lane), m, mapa_u32(smem_u32(&s_bar[5 + p]), lane));
         }
