@@ -131,7 +131,8 @@ typedef struct fmdp_launch {
   int32_t cluster_size;   /* CTAs cooperating on one trajectory (1..16), 0 = auto        */
   int32_t max_walkers;    /* concurrent trajectories in a batch round, 0 = auto          */
   int32_t threads;        /* threads per CTA, 0 = auto                                   */
-  int32_t profile;        /* 1: accumulate per-phase cycles of CTA 0 (fmdp_stats)        */
+  int32_t profile;        /* 1: per-phase cycles of CTA 0 (fmdp_stats), FCFS walks only;  */
+                          /*    they then run in the reference kernel instantiation      */
   int32_t step_budget;    /* batch: decision steps per trajectory per slice, 0 = auto (128) */
   int32_t cull;           /* 1: SURVEY f1 exact culling -- skip plans none of whose wells can */
                           /* reach a projected state (outputs bit-identical)               */

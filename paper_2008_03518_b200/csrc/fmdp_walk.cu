@@ -587,9 +587,9 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   const unsigned long long xseq0 = XP ? args.x_seq[xcl] : 0ull;  // step tags continue across launches
   unsigned long long xit = 0;
 
-  // per-phase cycle accounting: not in the FCFS walkers (MODE 0 / 4); a profiled FCFS walk runs
-  // in the reference instantiation (MODE 3)
-  const bool prof = MODE != 0 && MODE != 4 && args.prof != nullptr && rank == 0 && tid == 0 && (blockIdx.x / G) == 0;
+  // per-phase cycle accounting: only in the reference instantiation (MODE 3; a profiled FCFS
+  // walk runs there) -- its marks cost up to 6 % of a latency-bound step elsewhere
+  const bool prof = MODE == 3 && args.prof != nullptr && rank == 0 && tid == 0;
   unsigned long long pacc[PH_N];
 #pragma unroll
   for (int i = 0; i < PH_N; ++i) pacc[i] = 0;
