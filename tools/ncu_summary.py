@@ -83,8 +83,13 @@ for rep, kern, title in (('walk_batch', 'walk_kernel<3, 0>', 'configs[1] batch, 
     # hottest compute region: skip mbarrier spin-waits (SYNCS / YIELD loops)
     ex = [0.0 if any(k in r[isrc] for k in ('SYNCS', 'YIELD', 'NANOSLEEP')) else float(r[ie] or 0) for r in d]
     mx = max(ex)
-    hot = [i for i, e in enumerate(ex) if e >= 0.9 * mx]
-    a, b = min(hot), max(hot) + 1
+    im = ex.index(mx)  # the contiguous block around the most-executed instruction
+    a = im
+    while a > 0 and ex[a - 1] >= 0.9 * mx:
+        a -= 1
+    b = im + 1
+    while b < len(ex) and ex[b] >= 0.9 * mx:
+        b += 1
     ts = sum(float(r[iss] or 0) for r in d)
     hs = sum(float(r[iss] or 0) for r in d[a:b])
     st = stalls(h, d, a, b)
