@@ -632,7 +632,10 @@ def run_native(args):
                    "actions": sc.airspace.n_actions, "W": sc.airspace.W, "l2": "flushed between steps (256 MB write)",
                    "parallelism": f"replicas{world}" if world > 1 else "single-gpu"},
         "ms_per_request": tot_ms / args.steps / n,
-        "requests_accepted": acc, "states_per_request": states / n, "device_steps_per_batch": steps_dev / args.steps,
+        "requests_accepted": acc, "acceptance_rate": acc / n,
+        "near_ties_per_batch": sum(r.n_near_ties for r in res_last),
+        "exact_band_rescans_per_batch": sum(r.n_exact for r in res_last),
+        "states_per_request": states / n, "device_steps_per_batch": steps_dev / args.steps,
         "action_plan_evals_per_s": pairs / 5.0 / sc.airspace.W / (tot_ms / 1e3) * world,
         "pair_evals_per_s": pairs / (tot_ms / 1e3) * world,
         "rounds": stats["rounds"], "reruns": stats["reruns"],

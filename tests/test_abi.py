@@ -74,3 +74,16 @@ def test_abi_version_matches_the_header():
     fields = [f for f, _ in fmdp.Airspace._fields_]
     assert names[-1] == fields[-1] == "valuation"
     assert len(fields) >= 30
+
+
+def test_pack_plans_layout():
+    """pack_plans (binding-side marshalling for fmdp_add_plans): t0[P] int64, n[P] int32 and the
+    states of all plans concatenated in order, [sum n][3] int32."""
+    import numpy as np
+    from paper_2008_03518_b200.fmdp import pack_plans
+    plans = [(5, np.arange(6).reshape(2, 3)), (0, np.array([[7, 8, 9]])), (12, np.arange(9).reshape(3, 3) + 100)]
+    t0, n, st = pack_plans(plans)
+    assert t0.dtype == np.int64 and n.dtype == np.int32 and st.dtype == np.int32
+    assert t0.tolist() == [5, 0, 12] and n.tolist() == [2, 1, 3]
+    assert st.shape == (6, 3) and st.flags["C_CONTIGUOUS"]
+    assert (st[:2] == plans[0][1]).all() and (st[2] == [7, 8, 9]).all() and (st[3:] == plans[2][1]).all()
