@@ -5,7 +5,7 @@ sys.path.insert(0, '.')
 import fmdp_synth as fs
 from paper_2008_03518_b200.fmdp import FMDP
 
-for name, sc, i in (("c2", fs.config_c2(), 2), ("c4", fs.config_c4(), 0)):
+for name, sc, i in (("c2", fs.config_c2(), 2), ("c4", fs.config_c4(rows=1200), 0)):
     ctx = FMDP(sc.airspace, sc.terrain)
     ctx.add_plans(sc.plans)
     n0 = ctx.num_plans()
