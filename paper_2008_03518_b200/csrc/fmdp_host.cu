@@ -141,6 +141,18 @@ fmdp_status fail(fmdp_ctx* c, fmdp_status s, const std::string& msg) {
     if (e_ != cudaSuccess) return fail(ctx, FMDP_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
+// Makes the context's device current for one API call and restores the caller's on return.
+struct DevGuard {
+  int prev = -1;
+  bool swapped = false;
+  explicit DevGuard(int dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) swapped = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DevGuard() {
+    if (swapped) cudaSetDevice(prev);
+  }
+};
+
 void* dalloc(fmdp_ctx* ctx, size_t bytes) {
   if (bytes == 0) bytes = 16;
   void* p = nullptr;
@@ -698,6 +710,7 @@ fmdp_status run_single(fmdp_ctx* ctx, const Req& r) {
 fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_result* res, fmdp_qpos* traj,
                           int32_t traj_cap_each, int32_t flags) {
   if (!ctx || (n > 0 && (!reqs || !res)) || n < 0) return fail(ctx, FMDP_E_ARG, "null argument");
+  DevGuard dev_guard(ctx->device);  // the context's device for this call, the caller's restored after
   if (traj && traj_cap_each < ctx->w.max_steps + 1)
     return fail(ctx, FMDP_E_BUFFER, "traj_cap must be >= max_steps + 1");
   std::memset(&ctx->stats, 0, sizeof(ctx->stats));
@@ -980,7 +993,11 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
     return bad(FMDP_E_NODEV, "no CUDA device");
   }
   if (prop.major != 10) return bad(FMDP_E_NODEV, "libfmdp is built for sm_100a only");
-  if (cudaSetDevice(dev) != cudaSuccess) return bad(FMDP_E_NODEV, "cudaSetDevice failed");
+  DevGuard dev_guard(dev);  // the caller's current device is restored on return
+  {
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess || cur != dev) return bad(FMDP_E_NODEV, "cudaSetDevice failed");
+  }
   ctx->device = dev;
   ctx->num_sms = prop.multiProcessorCount;
   if (devs) {
@@ -1199,7 +1216,7 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
 
 void fmdp_destroy(fmdp_ctx* ctx) {
   if (!ctx) return;
-  cudaSetDevice(ctx->device);
+  DevGuard dev_guard(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   x_release(ctx);
   std::vector<void*> a = ctx->allocs;
@@ -1234,6 +1251,7 @@ fmdp_status fmdp_add_plans(fmdp_ctx* ctx, int32_t n_plans, const uint64_t* aircr
                            const int32_t* n_states, const fmdp_qpos* states, uint32_t* first_id) {
   if (!ctx || n_plans < 0 || (n_plans > 0 && (!t0_steps || !n_states || !states)))
     return fail(ctx, FMDP_E_ARG, "null argument");
+  DevGuard dev_guard(ctx->device);  // the context's device for this call, the caller's restored after
   if (first_id) *first_id = (uint32_t)ctx->plans.size();
   if (n_plans == 0) return FMDP_OK;
   std::vector<int64_t> t0(n_plans);
@@ -1349,6 +1367,7 @@ fmdp_status fmdp_schedule_sharded(fmdp_ctx* ctx, const fmdp_shard* shard, uint64
   if (!ctx || !shard || !res || !shard->allreduce_min_u32 || shard->world < 1 || shard->rank < 0 ||
       shard->rank >= shard->world)
     return fail(ctx, FMDP_E_ARG, "invalid shard description");
+  DevGuard dev_guard(ctx->device);  // the context's device for this call, the caller's restored after
   if (traj && traj_cap < ctx->w.max_steps + 1) return fail(ctx, FMDP_E_BUFFER, "traj_cap must be >= max_steps + 1");
   std::memset(&ctx->stats, 0, sizeof(ctx->stats));
   fmdp_request rq;
@@ -1401,7 +1420,7 @@ fmdp_status fmdp_schedule_sharded(fmdp_ctx* ctx, const fmdp_shard* shard, uint64
 // ----------------------------------------------------------------------------- in-kernel exchange
 fmdp_status fmdp_p2p_export(fmdp_ctx* ctx, int32_t world, fmdp_p2p_handle* handle, void** dev_ptr) {
   if (!ctx || !handle || world < 1 || world > fmdp::XNODE) return fail(ctx, FMDP_E_ARG, "world must be 1..8");
-  CK(cudaSetDevice(ctx->device));
+  DevGuard dev_guard(ctx->device);  // the context's device for this call, the caller's restored after
   CK(cudaStreamSynchronize(ctx->stream));
   x_release(ctx);
   if (!ctx->d_xpeers) ctx->d_xpeers = (fmdp::XPeer*)dalloc(ctx, sizeof(fmdp::XPeer) * fmdp::XMAX);
@@ -1434,7 +1453,7 @@ fmdp_status fmdp_p2p_connect(fmdp_ctx* ctx, int32_t rank, int32_t world, const f
   if (!ctx) return FMDP_E_ARG;
   if (!ctx->x_area || world != ctx->x_world) return fail(ctx, FMDP_E_ARG, "fmdp_p2p_export(world) first");
   if (rank < 0 || rank >= world) return fail(ctx, FMDP_E_ARG, "rank out of range");
-  CK(cudaSetDevice(ctx->device));
+  DevGuard dev_guard(ctx->device);  // the context's device for this call, the caller's restored after
   for (void* p : ctx->x_ipc) cudaIpcCloseMemHandle(p);
   ctx->x_ipc.clear();
   ctx->x_me = -1;
@@ -1499,7 +1518,7 @@ fmdp_status fmdp_schedule_p2p(fmdp_ctx* ctx, uint64_t aircraft_id, fmdp_vec3 src
   if (!ctx || !res) return fail(ctx, FMDP_E_ARG, "null argument");
   if (ctx->x_me < 0) return fail(ctx, FMDP_E_ARG, "fmdp_p2p_connect first");
   if (traj && traj_cap < ctx->w.max_steps + 1) return fail(ctx, FMDP_E_BUFFER, "traj_cap must be >= max_steps + 1");
-  CK(cudaSetDevice(ctx->device));
+  DevGuard dev_guard(ctx->device);  // the context's device for this call, the caller's restored after
   std::memset(&ctx->stats, 0, sizeof(ctx->stats));
   fmdp_request rq;
   rq.aircraft_id = aircraft_id;
@@ -1602,6 +1621,7 @@ fmdp_status fmdp_schedule_departures(fmdp_ctx* ctx, uint64_t aircraft_id, fmdp_v
                                      int64_t t0_step, int32_t n_delays, const int64_t* delays, fmdp_result* res,
                                      fmdp_qpos* traj, int32_t traj_cap, int32_t* chosen) {
   if (!ctx || n_delays < 1 || !delays || !res || !chosen) return fail(ctx, FMDP_E_ARG, "null argument");
+  DevGuard dev_guard(ctx->device);  // the context's device for this call, the caller's restored after
   if (traj && traj_cap < ctx->w.max_steps + 1) return fail(ctx, FMDP_E_BUFFER, "traj_cap must be >= max_steps + 1");
   std::memset(&ctx->stats, 0, sizeof(ctx->stats));
   *chosen = -1;
@@ -1653,6 +1673,7 @@ fmdp_status fmdp_schedule_departures(fmdp_ctx* ctx, uint64_t aircraft_id, fmdp_v
 
 int32_t fmdp_cosim_max(fmdp_ctx* ctx) {
   if (!ctx) return 0;
+  DevGuard dev_guard(ctx->device);  // occupancy queries use the current device
   int m = 0;
   for (int G : {1, 2, 4, 8, 16})
     if (!ctx->launch.cluster_size || G == ctx->launch.cluster_size) m = std::max(m, max_clusters(ctx, G, true));
@@ -1662,6 +1683,7 @@ int32_t fmdp_cosim_max(fmdp_ctx* ctx) {
 fmdp_status fmdp_schedule_cosim(fmdp_ctx* ctx, const fmdp_request* reqs, int32_t n, fmdp_result* res, fmdp_qpos* traj,
                                 int32_t traj_cap_each) {
   if (!ctx || n < 1 || !reqs || !res) return fail(ctx, FMDP_E_ARG, "null argument");
+  DevGuard dev_guard(ctx->device);  // the context's device for this call, the caller's restored after
   if (traj && traj_cap_each < ctx->w.max_steps + 1) return fail(ctx, FMDP_E_BUFFER, "traj_cap must be >= max_steps + 1");
   std::memset(&ctx->stats, 0, sizeof(ctx->stats));
   std::vector<Req> base;
@@ -1732,6 +1754,7 @@ fmdp_status fmdp_schedule_batch(fmdp_ctx* ctx, const fmdp_request* reqs, int32_t
 fmdp_status fmdp_get_steplog(fmdp_ctx* ctx, int32_t index, int32_t* astar, int32_t* heading, int32_t* near_tie,
                              int32_t cap, int32_t* n) {
   if (!ctx || index < 0 || index >= ctx->last_n) return fail(ctx, FMDP_E_ARG, "no such request in the last call");
+  DevGuard dev_guard(ctx->device);
   const int ns = ctx->h_out[index].n_states;
   if (n) *n = ns;
   if (cap < ns) return FMDP_E_BUFFER;
@@ -1766,6 +1789,7 @@ fmdp_status fmdp_num_plans(const fmdp_ctx* ctx, uint32_t* n) {
 
 fmdp_status fmdp_truncate(fmdp_ctx* ctx, uint32_t n_plans) {
   if (!ctx) return FMDP_E_ARG;
+  DevGuard dev_guard(ctx->device);  // the context's device for this call, the caller's restored after
   if (n_plans >= ctx->plans.size()) return FMDP_OK;
   // later plans occupy the top slots of each of their rows (appends are in id order)
   for (size_t i = n_plans; i < ctx->plans.size(); ++i) {
@@ -1784,6 +1808,7 @@ fmdp_status fmdp_eval_step(fmdp_ctx* ctx, fmdp_qpos pos, int32_t heading, fmdp_q
                            double* vstar, double* v_at, double* scale_at, int32_t* conflict, int64_t* min_d2,
                            int32_t* a_star) {
   if (!ctx || !vstar) return fail(ctx, FMDP_E_ARG, "null argument");
+  DevGuard dev_guard(ctx->device);  // the context's device for this call, the caller's restored after
   if (clock_step < 0 || clock_step + 1 >= ctx->w.horizon) return fail(ctx, FMDP_E_RANGE, "clock outside horizon");
   if (heading < 0 || heading >= ctx->w.HL) return fail(ctx, FMDP_E_ARG, "heading outside the lattice");
   fmdp_status st = ensure_slots(ctx, 1);

@@ -269,3 +269,17 @@ def test_p2p_cluster_count_changes_between_requests():
             assert g.status == want.status and g.n_states == want.n_states and (g.traj == want.traj).all()
     for c in ctxs + [ref]:
         c.close()
+
+
+def test_api_keeps_the_callers_current_device():
+    """Every call runs on the context's device and leaves the caller's current device as it was
+    (one process may hold contexts on several GPUs)."""
+    import torch
+    from paper_2008_03518_b200.fmdp import FMDP
+    sc = _scenario()
+    before = torch.cuda.current_device()
+    ctx = FMDP(sc.airspace, sc.terrain, device=0)
+    ctx.add_plans(sc.plans)
+    ctx.schedule(sc.src[0], sc.dst[0], int(sc.t0[0]))
+    assert torch.cuda.current_device() == before
+    ctx.close()
