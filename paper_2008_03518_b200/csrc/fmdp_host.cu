@@ -746,7 +746,11 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
     // and rolls back any pending request whose computed steps could see a newly committed
     // plan to its first influenced step.  Result: identical to the sequential loop.
     // slice budget: measured optimum on configs[1] (tools/sweep_budget.py)
-    const int budget = ctx->launch.step_budget > 0 ? ctx->launch.step_budget : 128;
+    // The others of a split slice run until the head has finished and then `budget` more steps
+    // at most, so the budget only lengthens a slice past the FCFS critical path: measured best
+    // (tools/sweep_budget.py, profiles/r01_sweep_budget.txt) 1-2 full (676 -> 750 req/s vs 128),
+    // 64 culled
+    const int budget = ctx->launch.step_budget > 0 ? ctx->launch.step_budget : (ctx->launch.cull ? 64 : 2);
     std::vector<char> fin(n, 0);
     std::vector<int> kdone(n, 0);
     int rollbacks = 0;
