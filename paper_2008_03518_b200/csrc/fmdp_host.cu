@@ -434,11 +434,14 @@ fmdp_status run_split(fmdp_ctx* ctx, std::vector<Req>& run, int budget) {
   // the head runs as one cluster: splitting it over clusters (fmdp_launch.split) takes SMs from
   // the others and measured slower (configs[1]: 155.5 -> 171 ms per batch, tools/ab_headsplit.py)
   const int Gh = solo_cluster_size(ctx);
-  // second lane: the next request (run[1]) also at the lone-walker cluster size -- its
-  // speculative steps are the next slice's head work unless the head's plan rolls them back
-  // (configs[1]: -0.7 % full / -0.2 % culled batch time)
-  const bool lane2 = n >= 3 && ctx->num_sms >= 2 * Gh + 16;
-  const int nl = lane2 ? 2 : 1;
+  // lanes: the next m = 3 requests also walk at the lone-walker cluster size -- their
+  // speculative steps are the next slices' head work unless a commit rolls them back
+  // (configs[1] full batch 135.4 -> 131.2 -> 125.9 -> 120.2 -> 122.9 ms for m = 0..4, culled
+  // 59.4 -> 58.9 ms; tools/ab_full.py with the slice budget of 2 / 64)
+  int m = std::min(3, n - 2);
+  while (m > 0 && ctx->num_sms < (1 + m) * Gh + 16) --m;
+  const bool lane2 = m > 0;
+  const int nl = 1 + m;
   int Go = 0, nco = 0;
   choose_launch(ctx, n - nl, &Go, &nco, ctx->num_sms - nl * Gh);
   CK(cudaMemcpyAsync(ctx->d_reqs, run.data(), sizeof(Req) * n, cudaMemcpyHostToDevice, ctx->stream));
@@ -460,10 +463,10 @@ fmdp_status run_split(fmdp_ctx* ctx, std::vector<Req>& run, int budget) {
   if (lane2) {
     fmdp::WalkArgs a2 = ah;
     a2.reqs = ctx->d_reqs + 1;
-    a2.n_reqs = 1;
+    a2.n_reqs = m;
     a2.queue = ctx->d_queue + 3;
     CK(cudaStreamWaitEvent(ctx->stream3, ctx->ev0, 0));
-    CK(fmdp::launch_walk(ctx->w, a2, ctx->C, Gh, 1, threads_for(ctx), chunk_for(ctx), rawcap_for(ctx), ctx->stream3));
+    CK(fmdp::launch_walk(ctx->w, a2, ctx->C, Gh, m, threads_for(ctx), chunk_for(ctx), rawcap_for(ctx), ctx->stream3));
     CK(cudaEventRecord(ctx->ev3, ctx->stream3));
   }
   CK(fmdp::launch_walk(ctx->w, ao, ctx->C, Go, nco, threads_for(ctx), chunk_for(ctx), rawcap_for(ctx), ctx->stream2));
