@@ -423,7 +423,7 @@ fmdp_status run_walk(fmdp_ctx* ctx, const std::vector<Req>& run, bool eval, int 
 
 // A split FCFS slice: the head (run[0], the earliest pending request -- everything before it is
 // committed, so it can never be rolled back) alone at the cluster size a lone walker would use,
-// on the library stream; the next three requests as lanes at the same size, and the other
+// on the library stream; the next two requests as lanes at the same size, and the other
 // pending requests on the SMs left at half that size, concurrently.  They go on past `budget` until the head has
 // finished (the device stop flag the head sets), so the slice is as long as the head's
 // remaining trajectory -- the FCFS critical path -- and never waits on anything else.
@@ -434,11 +434,11 @@ fmdp_status run_split(fmdp_ctx* ctx, std::vector<Req>& run, int budget) {
   // the head runs as one cluster: splitting it over clusters (fmdp_launch.split) takes SMs from
   // the others and measured slower (configs[1]: 155.5 -> 171 ms per batch, tools/ab_headsplit.py)
   const int Gh = solo_cluster_size(ctx);
-  // lanes: the next m = 3 requests also walk at the lone-walker cluster size -- their
+  // lanes: the next m = 2 requests also walk at the lone-walker cluster size -- their
   // speculative steps are the next slices' head work unless a commit rolls them back
-  // (configs[1] full batch 135.4 -> 131.2 -> 125.9 -> 120.2 -> 122.9 ms for m = 0..4, culled
-  // 59.4 -> 58.9 ms; tools/ab_full.py with the slice budget of 2 / 64)
-  int m = std::min(3, n - 2);
+  // (configs[1] full batch 115.3 / 109.2 / 108.6 / 111.8 / 115.0 / 121.5 ms for m = 0..5 with
+  // the others at half the head's cluster size and the slice budget of 2; culled 58.6-59.0)
+  int m = std::min(2, n - 2);
   while (m > 0 && ctx->num_sms < (1 + m) * Gh + 16) --m;
   const bool lane2 = m > 0;
   const int nl = 1 + m;
