@@ -133,7 +133,7 @@ typedef struct fmdp_launch {
   int32_t threads;        /* threads per CTA, 0 = auto                                   */
   int32_t profile;        /* 1: per-phase cycles of CTA 0 (fmdp_stats), FCFS walks only;  */
                           /*    they then run in the reference kernel instantiation      */
-  int32_t step_budget;    /* batch: steps the non-head walkers of a slice may run past the head's end, 0 = auto (2 full / 64 culled) */
+  int32_t step_budget;    /* batch: steps the non-head walkers of a slice may run past the head's end, 0 = auto (2) */
   int32_t cull;           /* 1: SURVEY f1 exact culling -- skip plans none of whose wells can */
                           /* reach a projected state (outputs bit-identical)               */
   int32_t split;          /* single-request walks (fmdp_schedule, FMDP_BATCH_SEQUENTIAL):  */

@@ -755,9 +755,9 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
     // slice budget: measured optimum on configs[1] (tools/sweep_budget.py)
     // The others of a split slice run until the head has finished and then `budget` more steps
     // at most, so the budget only lengthens a slice past the FCFS critical path: measured best
-    // (tools/sweep_budget.py, profiles/r01_sweep_budget.txt) 1-2 full (676 -> 750 req/s vs 128),
-    // 64 culled
-    const int budget = ctx->launch.step_budget > 0 ? ctx->launch.step_budget : (ctx->launch.cull ? 64 : 2);
+    // (tools/sweep_budget.py, profiles/r01_sweep_budget.txt) 1-2 on both paths (full 676 -> 750
+    // req/s against 128 before the lanes; culled 1647 -> 1694 against 64 with them)
+    const int budget = ctx->launch.step_budget > 0 ? ctx->launch.step_budget : 2;
     std::vector<char> fin(n, 0);
     std::vector<int> kdone(n, 0);
     int rollbacks = 0;

@@ -7,7 +7,7 @@ sc = fs.config_c2()
 ctx = FMDP(sc.airspace, sc.terrain)
 ctx.add_plans(sc.plans)
 n0 = ctx.num_plans()
-BUDGETS = {1: (8, 16, 32, 64, 128), 0: (1, 2, 4, 8, 16)}
+BUDGETS = {1: (2, 4, 8, 16), 0: ()}
 for cull in (1, 0):
     for budget in BUDGETS[cull]:
         ctx.set_launch(cull=cull, step_budget=budget)
