@@ -32,6 +32,7 @@ WORKLOAD = ("configs[1]: batch of 100 FCFS requests against 3000 accepted plans 
             "grid, 16x16 km dense urban airspace, 9 headings x 3 climbs, W=10")
 OPS_PER_PAIR = 7.0  # algorithmic FP32 ops per (state, well) pair
 EXEC_OPS_PER_PAIR = 4.0 / 3.0  # FP32 lane-ops the kernel executes per pair at 3 climbs ((2 + C - 1)/C, level climb skipped)
+LOOP_CEILING_PAIRS_PER_CLK_SM = 35.0  # isolated hot loop, C = 3 (tools/hotbench, profiles/r01_hotbench.txt: 34-36)
 
 
 def parse():
@@ -126,21 +127,67 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_baseline(sc, budget_s: float):
+def cpu_baseline(sc, budget_s: float, gpu=None):
     """The oracle as it stands (fp64 C, one core): FCFS requests of the same batch, in order,
-    until the time budget is spent."""
+    until the time budget is spent.  With ``gpu`` (per request: status, trajectory, headings,
+    actions of the timed GPU batch) the same requests are also checked against the GPU path: a
+    request whose oracle trajectory equals the GPU's has no divergent step; otherwise the oracle
+    lockstep-replays the GPU trajectory (store = the GPU's earlier accepted plans) and counts the
+    steps where the GPU took the other action of a logged near-tie (north-star rule) and any
+    failure."""
     from oracle import oracle as O
     orc = O.for_scenario(sc)
     t0 = time.perf_counter()
     done = states = 0
+    mine = []
     while done < sc.n_requests and time.perf_counter() - t0 < budget_s:
         r = orc.schedule(sc.src[done], sc.dst[done], int(sc.t0[done]))
+        mine.append(r)
         states += r.n_states
         done += 1
     dt = time.perf_counter() - t0
-    return {"value": done / dt, "unit": "requests/s", "cores": 1, "kind": "oracle",
-            "sample": f"first {done} of {sc.n_requests} requests of the same FCFS batch ({states} states) "
-                      f"in {dt:.1f} s, single thread"}
+    out = {"value": done / dt, "unit": "requests/s", "cores": 1, "kind": "oracle",
+           "sample": f"first {done} of {sc.n_requests} requests of the same FCFS batch ({states} states) "
+                     f"in {dt:.1f} s, single thread"}
+    if gpu is not None:
+        rep = O.for_scenario(sc)
+        div = fail = ident = 0
+        for i in range(min(done, len(gpu))):
+            st_g, tr, hd, ast = gpu[i]
+            if st_g == mine[i].status and len(tr) == mine[i].n_states and (tr == mine[i].traj).all():
+                ident += 1
+            else:
+                rs = rep.replay(sc.src[i], sc.dst[i], int(sc.t0[i]), tr, hd, ast, st_g)
+                div += rs.n_divergent
+                fail += rs.n_fail
+            if st_g == 0:
+                rep.add_plan(int(sc.t0[i]), tr)
+        out["parity"] = {"requests_checked": min(done, len(gpu)), "identical_to_oracle": ident,
+                         "divergent_steps": div, "failed_steps": fail,
+                         "rule": "divergent = GPU took the other action of a logged near-tie (top-2 gap < 1e-4 S); "
+                                 "failed = any other difference (must be 0)"}
+    return out
+
+
+def committed_pairs(sc, res, A, W, n_tau=5):
+    """(state, intruder well) pairs the method evaluates for the committed decision steps of one
+    FCFS batch: request i decides at steps k = 0..n_i-2, each over A*W states x
+    n_tau wells of every plan active at row t0_i + k -- the initial store plus the plans the
+    batch accepted before i.  Speculative work that was rolled back is not method work."""
+    import numpy as np
+    H = int(sc.airspace.horizon_steps)
+    cnt = np.zeros(H + 1, np.int64)
+    for t0, st in sc.plans:
+        cnt[t0] += 1
+        cnt[min(H, t0 + len(st))] -= 1
+    cnt = np.cumsum(cnt)[:H]
+    tot = 0
+    for i, r in enumerate(res):
+        t0 = int(sc.t0[i])
+        tot += int(cnt[t0:t0 + max(0, r.n_states - 1)].sum())
+        if r.status == 0:
+            cnt[t0:t0 + r.n_states] += 1
+    return tot * A * W * n_tau
 
 
 def run_reference(args):
@@ -239,18 +286,24 @@ def run_native(args):
             torch.distributed.barrier()
         # e2e: through the public API with host requests, trajectories and results copied back
         e2e_times, d2h = [], 0
+        gpu_log = None
         for _ in range(max(1, args.steps)):
             torch.cuda.synchronize()
             res, ms = one(True)
             e2e_times.append(ms)
             d2h = sum(r.n_states for r in res) * 12 + n * C_RESULT_BYTES
+            if gpu_log is None:  # the oracle checks these requests beside the cpu_baseline (rank 0)
+                gpu_log = []
+                for i in range(min(n, 12)):
+                    ast, hd, _ = ctx.steplog(i)
+                    gpu_log.append((res[i].status, res[i].traj, hd, ast))
             reset()
         tot_ms = max_over_ranks(sum(times), world)
         e2e_ms = max_over_ranks(sum(e2e_times), world)
         return dict(tot_ms=tot_ms, e2e_ms=e2e_ms,
                     value=sum_over_ranks(n * args.steps, world) / (tot_ms / 1e3),
                     e2e_value=sum_over_ranks(n * len(e2e_times), world) / (e2e_ms / 1e3), d2h=d2h,
-                    st_all=st_all, res_last=res_last, clocks=clk.summary(),
+                    st_all=st_all, res_last=res_last, clocks=clk.summary(), gpu_log=gpu_log,
                     walk_ms=sum(s["device_ms"] for s in st_all), pairs=sum(s["pair_evals"] for s in st_all),
                     launches=sum(s["kernels"] for s in st_all), steps_dev=sum(s["steps"] for s in st_all))
 
@@ -616,12 +669,23 @@ def run_native(args):
         pass
     peak_tops = 148 * 128 * peak_clock * 1e6 / 1e12
     traffic = None
-    try:  # dram read+write bytes per walk launch from the committed ncu --set full capture
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))["per_launch_bytes"]
-    except Exception:
-        pass
-    achieved_tops = pairs * OPS_PER_PAIR / (walk_ms / 1e3) / 1e12 if walk_ms > 0 else 0.0
+    traffic_src = None
+    for tname in ("r02_traffic.json", "r01_traffic.json"):  # dram read+write bytes per walk launch
+        try:                                                 # from the committed ncu --set full capture
+            traffic = json.load(open(os.path.join(ROOT, "profiles", tname)))["per_launch_bytes"]
+            traffic_src = f"profiles/{tname} (ncu --set full, dram bytes per walk launch)"
+            break
+        except Exception:
+            pass
+    # roofline of the dominant kernel on the METHOD's work: pairs of the committed decision steps
+    # (not the device counter, which includes speculative steps that were rolled back and the
+    # paused walkers' extra steps); the executed-op and loop-ceiling fractions beside it
+    A_, W_ = sc.airspace.n_actions, sc.airspace.W
+    cpairs = committed_pairs(sc, res_last, A_, W_) * args.steps
+    achieved_tops = cpairs * OPS_PER_PAIR / (walk_ms / 1e3) / 1e12 if walk_ms > 0 else 0.0
     exec_tops = pairs * EXEC_OPS_PER_PAIR / (walk_ms / 1e3) / 1e12 if walk_ms > 0 else 0.0
+    loop_ceiling = LOOP_CEILING_PAIRS_PER_CLK_SM * 148 * peak_clock * 1e6  # pairs/s
+    cpairs_c = committed_pairs(sc, Mc["res_last"], A_, W_) * args.steps
     if rank != 0:
         return 0
     line = {
@@ -641,10 +705,15 @@ def run_native(args):
         "rounds": stats["rounds"], "reruns": stats["reruns"],
         "roofline": {"bound": "alu", "achieved": achieved_tops, "peak": peak_tops, "unit": "Top/s",
                      "frac": achieved_tops / peak_tops, "traffic": traffic,
-                     "traffic_source": "profiles/r01_traffic.json (ncu --set full, bytes per walk launch)",
+                     "traffic_source": traffic_src,
                      "kernel": "walk_kernel<3, 0>", "ops_per_pair": OPS_PER_PAIR,
                      "ops_per_pair_basis": "algorithmic, SURVEY §8(d) d.3 (3 differences, 3 squares/fmas, 1 min)",
-                     "pipe_frac": exec_tops / peak_tops, "exec_ops_per_pair": EXEC_OPS_PER_PAIR,
+                     "committed_pairs_per_step": cpairs / args.steps,
+                     "device_pairs_per_step": pairs / args.steps,
+                     "speculation_overhead": pairs / max(1, cpairs),
+                     "exec_pipe_frac": exec_tops / peak_tops, "exec_ops_per_pair": EXEC_OPS_PER_PAIR,
+                     "loop_ceiling_frac": (cpairs / (walk_ms / 1e3)) / loop_ceiling if walk_ms > 0 else 0.0,
+                     "loop_ceiling_pairs_per_clk_sm": LOOP_CEILING_PAIRS_PER_CLK_SM,
                      "loop_ceiling": "isolated hot loop saturates the FMA pipe at 34-36 pairs/clk/SM (register-"
                                      "operand FFMA2 at half the nominal lane rate; tools/hotbench, "
                                      "profiles/r01_hotbench.txt)",
@@ -660,6 +729,8 @@ def run_native(args):
                     "d2h_bytes_per_step": Mc["d2h"]},
             "walk_device_ms_per_step": Mc["walk_ms"] / args.steps,
             "pair_evals_per_step": Mc["pairs"] / args.steps, "gpu_launches": Mc["launches"],
+            "committed_pairs_per_step": cpairs_c / args.steps,
+            "roofline_frac": cpairs_c * OPS_PER_PAIR / (Mc["walk_ms"] / 1e3) / 1e12 / peak_tops,
             "same_results_as_full": same, "clocks": Mc["clocks"]},
         "f3_departures": Md,
         "f2_cosim": Mco,
@@ -672,7 +743,8 @@ def run_native(args):
     if Mc5 is not None:
         line["c5_stress"] = Mc5
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(sc, args.cpu_sample_s)
+        line["cpu_baseline"] = cpu_baseline(sc, args.cpu_sample_s, M["gpu_log"])
+        line["divergent_steps"] = line["cpu_baseline"]["parity"]["divergent_steps"]
     print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:

@@ -308,6 +308,20 @@ int32_t fmdp_cosim_max(fmdp_ctx* ctx);
 fmdp_status fmdp_get_steplog(fmdp_ctx* ctx, int32_t index, int32_t* astar, int32_t* heading,
                              int32_t* near_tie, int32_t cap, int32_t* n);
 
+/* Parity trace of the walk kernels themselves (north-star tolerance check on the path the batch
+ * actually runs): after fmdp_set_trace(ctx, m) every later schedule / schedule_batch call records,
+ * for its requests 0..m-1, V*(a) (Alg 8) and its term scale S(a) = V+ + max(V^T,V^I) +
+ * V_alt at the maximising substep (R25) of every decision step, in whichever kernel
+ * instantiation (full, culled, split slices) computes that step -- a step re-run after a
+ * speculative rollback overwrites its entry.  m = 0 turns it off.  Device memory: m * (max_steps
+ * + 2) * A * 16 bytes.  Errors: E_ARG (m < 0), E_NOMEM. */
+fmdp_status fmdp_set_trace(fmdp_ctx* ctx, int32_t n_requests);
+/* The trace of request `index` (< m) of the last call: vstar / scale [k * A + a] for the decision
+ * steps k = 0..n-2 (n = n_states); *n receives n - 1.  cap_steps < n - 1 -> E_BUFFER.  Either
+ * pointer may be NULL.  E_ARG if the request was not traced. */
+fmdp_status fmdp_get_trace(fmdp_ctx* ctx, int32_t index, double* vstar, double* scale, int32_t cap_steps,
+                           int32_t* n);
+
 fmdp_status fmdp_get_plan(fmdp_ctx* ctx, uint32_t plan_id, int64_t* t0_step, fmdp_qpos* buf,
                           int32_t cap, int32_t* n);
 fmdp_status fmdp_num_plans(const fmdp_ctx* ctx, uint32_t* n);

@@ -103,6 +103,9 @@ struct WalkArgs {
   uint32_t* dbg_conf;           // [A+1]
   int32_t* dbg_astar;           // [1]
   unsigned long long* pairs;    // hot-loop pair counter (stats)
+  int32_t* stepx;               // [slot][cap] exact-fallback count of step k (zeroed by the host)
+  double2* vtrace;              // [vtrace_n][cap][A] {V*(a), S(a)} per step (fmdp_set_trace), or null
+  int32_t vtrace_n;
   unsigned long long* prof;     // [PH_N] per-phase cycles of rank 0 (nullptr = off)
   // co-simulated batch: one cluster per request, all on one clock
   int32_t cosim;                // 1: batch peers are wells (Alg 5) and separation partners

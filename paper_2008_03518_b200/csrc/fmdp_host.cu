@@ -66,6 +66,9 @@ struct fmdp_ctx {
   int32_t *d_traj = nullptr, *d_heading = nullptr, *d_astar = nullptr;
   uint32_t* d_stepd2 = nullptr;
   int8_t* d_ntie = nullptr;
+  int32_t* d_stepx = nullptr;  // [slot][cap] exact-fallback count per step (zeroed per call / rollback)
+  double2* d_vtrace = nullptr; // fmdp_set_trace: [vtrace_n][cap][A] {V*(a), S(a)} per step
+  int vtrace_n = 0;
   int32_t* d_queue = nullptr;
   int32_t* d_stop = nullptr;   // head-finished flag of a single-wave slice
   int32_t* d_nstates = nullptr;
@@ -242,18 +245,45 @@ int32_t initial_heading(const fmdp_ctx* ctx, const int32_t s[3], const int32_t g
   return (int32_t)h;
 }
 
+// Per-request scratch for n requests (grown on demand), and the per-step exact counts of the
+// call zeroed.  Growth is all-or-nothing: every new buffer is allocated before any old one is
+// released, so a failed allocation leaves the previous (smaller) set intact and consistent.
 fmdp_status ensure_slots(fmdp_ctx* ctx, int n) {
-  if (n <= ctx->slots_cap) return FMDP_OK;
-  const int m = std::max(n, 2 * ctx->slots_cap);
   const size_t cap = (size_t)ctx->cap_states;
-  fmdp_status s;
-  if ((s = grow(ctx, ctx->d_reqs, m)) || (s = grow(ctx, ctx->d_out, m)) || (s = grow(ctx, ctx->d_traj, 3 * cap * m)) ||
-      (s = grow(ctx, ctx->d_heading, cap * m)) || (s = grow(ctx, ctx->d_astar, cap * m)) ||
-      (s = grow(ctx, ctx->d_stepd2, cap * m)) || (s = grow(ctx, ctx->d_ntie, cap * m)) ||
-      (s = grow(ctx, ctx->d_nstates, m)) || (s = grow(ctx, ctx->d_t0s, m)))
-    return s;
-  ctx->slots_cap = m;
-  ctx->h_out.resize(m);
+  if (n > ctx->slots_cap) {
+    const size_t m = (size_t)std::max(n, 2 * ctx->slots_cap);
+    struct B {
+      void** dst;
+      size_t bytes;
+      void* p;
+    } b[] = {{(void**)&ctx->d_reqs, sizeof(Req) * m, nullptr},        {(void**)&ctx->d_out, sizeof(Out) * m, nullptr},
+             {(void**)&ctx->d_traj, 12 * cap * m, nullptr},           {(void**)&ctx->d_heading, 4 * cap * m, nullptr},
+             {(void**)&ctx->d_astar, 4 * cap * m, nullptr},           {(void**)&ctx->d_stepd2, 4 * cap * m, nullptr},
+             {(void**)&ctx->d_ntie, cap * m, nullptr},                {(void**)&ctx->d_stepx, 4 * cap * m, nullptr},
+             {(void**)&ctx->d_nstates, sizeof(int32_t) * m, nullptr}, {(void**)&ctx->d_t0s, sizeof(int64_t) * m, nullptr}};
+    for (B& e : b) {
+      e.p = dalloc(ctx, e.bytes);
+      if (!e.p) {
+        for (B& f : b) dfree(ctx, f.p);
+        return fail(ctx, FMDP_E_NOMEM, "device allocation failed (request scratch)");
+      }
+    }
+    for (B& e : b) {
+      dfree(ctx, *e.dst);
+      *e.dst = e.p;
+    }
+    ctx->slots_cap = (int)m;
+    ctx->h_out.resize(m);
+  }
+  if (n > 0) CK(cudaMemsetAsync(ctx->d_stepx, 0, sizeof(int32_t) * cap * (size_t)n, ctx->stream));
+  return FMDP_OK;
+}
+
+// Rollback of request slot i to step k1: its per-step exact counts from k1 on are recomputed.
+fmdp_status clear_stepx(fmdp_ctx* ctx, int i, int k1) {
+  const size_t cap = (size_t)ctx->cap_states;
+  if (k1 < 0 || (size_t)k1 >= cap) return FMDP_OK;
+  CK(cudaMemsetAsync(ctx->d_stepx + (size_t)i * cap + k1, 0, sizeof(int32_t) * (cap - k1), ctx->stream));
   return FMDP_OK;
 }
 
@@ -395,6 +425,9 @@ fmdp::WalkArgs make_args(fmdp_ctx* ctx, const std::vector<Req>& run, bool eval, 
   a.dbg_astar = ctx->d_dbg_astar;
   a.pairs = ctx->d_pairctr;
   a.prof = ctx->launch.profile ? ctx->d_prof : nullptr;
+  a.stepx = ctx->d_stepx;
+  a.vtrace = ctx->vtrace_n > 0 ? ctx->d_vtrace : nullptr;
+  a.vtrace_n = ctx->vtrace_n;
   return a;
 }
 
@@ -509,10 +542,12 @@ fmdp_status append_device(fmdp_ctx* ctx, const std::vector<int64_t>& t0, const s
     tot += n[i];
     maxn = std::max(maxn, n[i]);
   }
+  // slots from a copy of the host mirror: ctx->counts changes only once the append succeeded
+  std::vector<int32_t> cnt = ctx->counts;
   std::vector<int32_t> slots(tot);
   size_t o = 0;
   for (int i = 0; i < np; ++i)
-    for (int s = 0; s < n[i]; ++s) slots[o++] = ctx->counts[t0[i] + s]++;
+    for (int s = 0; s < n[i]; ++s) slots[o++] = cnt[t0[i] + s]++;
   fmdp_status st = ensure_up(ctx, tot);
   if (st) return st;
   if (np > ctx->app_cap) {
@@ -532,9 +567,9 @@ fmdp_status append_device(fmdp_ctx* ctx, const std::vector<int64_t>& t0, const s
   CK(cudaMemcpyAsync(ctx->d_up, slots.data(), sizeof(int32_t) * tot, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->d_app, ap.data(), sizeof(AppendPlan) * np, cudaMemcpyHostToDevice, ctx->stream));
   CK(fmdp::launch_append(ctx->d_rows, ctx->w.row_cap, ctx->w.horizon, ctx->d_app, np, maxn, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->d_counts, ctx->counts.data(), sizeof(int32_t) * ctx->counts.size(), cudaMemcpyHostToDevice,
-                     ctx->stream));
+  CK(cudaMemcpyAsync(ctx->d_counts, cnt.data(), sizeof(int32_t) * cnt.size(), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  ctx->counts.swap(cnt);
   ctx->stats.kernels += 1;
   return FMDP_OK;
 }
@@ -567,16 +602,21 @@ fmdp_status commit_slots(fmdp_ctx* ctx, const std::vector<int>& slots, const std
     ds.push_back(ctx->d_traj + (size_t)s * ctx->cap_states * 3);
   }
   if (!rows_fit(ctx, t0, n)) return fail(ctx, FMDP_E_CAPACITY, "time row capacity exceeded on commit");
+  std::vector<PlanRec> recs(slots.size());
   for (size_t i = 0; i < slots.size(); ++i) {
-    PlanRec p;
-    p.aircraft = aircraft[slots[i]];
-    p.t0 = t0[i];
-    p.states.resize((size_t)3 * n[i]);
-    CK(cudaMemcpyAsync(p.states.data(), ds[i], sizeof(int32_t) * 3 * n[i], cudaMemcpyDeviceToHost, ctx->stream));
-    plan_id[slots[i]] = (uint32_t)ctx->plans.size();
-    ctx->plans.push_back(std::move(p));
+    recs[i].aircraft = aircraft[slots[i]];
+    recs[i].t0 = t0[i];
+    recs[i].states.resize((size_t)3 * n[i]);
+    CK(cudaMemcpyAsync(recs[i].states.data(), ds[i], sizeof(int32_t) * 3 * n[i], cudaMemcpyDeviceToHost, ctx->stream));
   }
-  return append_device(ctx, t0, n, ds);
+  // host records and plan ids only once the device append succeeded (append_device syncs)
+  fmdp_status st = append_device(ctx, t0, n, ds);
+  if (st) return st;
+  for (size_t i = 0; i < slots.size(); ++i) {
+    plan_id[slots[i]] = (uint32_t)ctx->plans.size();
+    ctx->plans.push_back(std::move(recs[i]));
+  }
+  return FMDP_OK;
 }
 
 fmdp_status influence(fmdp_ctx* ctx, const std::vector<InflPair>& pairs, std::vector<int32_t>& kf) {
@@ -828,6 +868,7 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
           fin[c] = 0;
           kdone[c] = k1;
           ++rollbacks;
+          if ((st = clear_stepx(ctx, c, k1))) return st;
           break;
         }
         if (ctx->h_out[c].status == FMDP_ACCEPTED) {
@@ -844,9 +885,11 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
           fin[i] = 0;
           kdone[i] = k1;
           ++rollbacks;
+          if ((st = clear_stepx(ctx, i, k1))) return st;
         } else if (k1 < kdone[i]) {
           kdone[i] = k1;
           ++rollbacks;
+          if ((st = clear_stepx(ctx, i, k1))) return st;
         }
       }
     }
@@ -1776,6 +1819,38 @@ fmdp_status fmdp_get_steplog(fmdp_ctx* ctx, int32_t index, int32_t* astar, int32
     std::vector<int8_t> t(ns);
     CK(cudaMemcpy(t.data(), ctx->d_ntie + b, ns, cudaMemcpyDeviceToHost));
     for (int i = 0; i < ns; ++i) near_tie[i] = t[i];
+  }
+  return FMDP_OK;
+}
+
+fmdp_status fmdp_set_trace(fmdp_ctx* ctx, int32_t n_requests) {
+  if (!ctx || n_requests < 0) return fail(ctx, FMDP_E_ARG, "n_requests must be >= 0");
+  DevGuard dev_guard(ctx->device);
+  if (n_requests > ctx->vtrace_n || (n_requests > 0 && !ctx->d_vtrace)) {
+    dfree(ctx, ctx->d_vtrace);
+    ctx->d_vtrace = (double2*)dalloc(ctx, sizeof(double2) * (size_t)n_requests * ctx->cap_states * ctx->A);
+    if (!ctx->d_vtrace) {
+      ctx->vtrace_n = 0;
+      return fail(ctx, FMDP_E_NOMEM, "trace buffer");
+    }
+  }
+  ctx->vtrace_n = n_requests;
+  return FMDP_OK;
+}
+
+fmdp_status fmdp_get_trace(fmdp_ctx* ctx, int32_t index, double* vstar, double* scale, int32_t cap_steps, int32_t* n) {
+  if (!ctx || index < 0 || index >= ctx->last_n || index >= ctx->vtrace_n || !ctx->d_vtrace)
+    return fail(ctx, FMDP_E_ARG, "request not traced in the last call (fmdp_set_trace)");
+  DevGuard dev_guard(ctx->device);
+  const int ns = std::max(0, ctx->h_out[index].n_states - 1);  // decision steps 0..n-2
+  if (n) *n = ns;
+  if (cap_steps < ns) return FMDP_E_BUFFER;
+  std::vector<double2> t((size_t)ns * ctx->A);
+  if (ns) CK(cudaMemcpy(t.data(), ctx->d_vtrace + (size_t)index * ctx->cap_states * ctx->A, sizeof(double2) * t.size(),
+                        cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < t.size(); ++i) {
+    if (vstar) vstar[i] = t[i].x;
+    if (scale) scale[i] = t[i].y;
   }
   return FMDP_OK;
 }

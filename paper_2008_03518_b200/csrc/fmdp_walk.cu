@@ -83,6 +83,44 @@ __device__ __forceinline__ void st_async_d2(uint32_t ra, double a, double b, uin
                "d"(b), "r"(rbar)
                : "memory");
 }
+// The same pushes for a one-CTA cluster (G = 1): DSMEM accesses (mapa / st.async) need a cluster
+// of at least two CTAs (compute-sanitizer memcheck, profiles/r02_sanitizer.md), so the value is a
+// plain shared store, released to the waiting threads by a CTA fence, and its bytes are completed
+// on the CTA's own mbarrier (complete_tx; the tx-count may go transiently negative, exactly as when
+// an st.async lands before the expect_tx).
+__device__ __forceinline__ void complete_tx_local(uint32_t bar, uint32_t bytes) {
+  asm volatile("fence.acq_rel.cta;" ::: "memory");
+  asm volatile("mbarrier.complete_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void push_u32(bool solo, uint32_t a, unsigned dst, uint32_t v, uint32_t bar) {
+  if (solo) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+    complete_tx_local(bar, 4);
+  } else {
+    st_async_u32(mapa_u32(a, dst), v, mapa_u32(bar, dst));
+  }
+}
+__device__ __forceinline__ void push_f4(bool solo, uint32_t a, unsigned dst, float4 v, uint32_t bar) {
+  if (solo) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+    complete_tx_local(bar, 16);
+  } else {
+    st_async_f4(mapa_u32(a, dst), v, mapa_u32(bar, dst));
+  }
+}
+__device__ __forceinline__ void push_d2(bool solo, uint32_t a, unsigned dst, double x, double y, uint32_t bar) {
+  if (solo) {
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(x), "d"(y) : "memory");
+    complete_tx_local(bar, 16);
+  } else {
+    st_async_d2(mapa_u32(a, dst), x, y, mapa_u32(bar, dst));
+  }
+}
+// Generic pointer to `p` in cluster CTA `r` (the own pointer in a one-CTA cluster, see above).
+template <class T>
+__device__ __forceinline__ T* peer_ptr(cg::cluster_group& cl, T* p, unsigned r, bool solo) {
+  return solo ? p : cl.map_shared_rank(p, r);
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
@@ -285,6 +323,7 @@ __device__ __noinline__ bool cs_idle(int4* pub_all, unsigned* arrive, int32_t* e
       asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(arrive) : "memory");
       ctl->cs_ok = cs_wait_until(arrive, err, (unsigned)n * (unsigned)(K - k0 + 1)) ? 1 : 0;
     }
+    __syncwarp();  // warp 0 reconverges after thread 0's spin before the aligned CTA barrier
     __syncthreads();
     const bool ok = ctl->cs_ok != 0;
     bool all = until_all;
@@ -308,14 +347,24 @@ __device__ __noinline__ bool cs_idle(int4* pub_all, unsigned* arrive, int32_t* e
 // it had finished reading step s (CTA barriers in between).  A poll longer than ~2 s (a peer is
 // not running) sets *err and returns the stale value; every later poll returns at once, the walk
 // ends with wrong values and the host reports FMDP_E_CUDA.
+// The word is ONE aligned 64-bit scalar access on both sides (st/ld.relaxed.sys.b64: single-copy
+// atomic; a vector access would be two element accesses in unspecified order, so a reader could
+// see the new tag with the old value): value in the low half, tag in the high half.
 __device__ __forceinline__ void st_ll(unsigned long long* p, uint32_t v, uint32_t tag) {
-  asm volatile("st.volatile.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(v), "r"(tag) : "memory");
+  const unsigned long long w = (unsigned long long)v | ((unsigned long long)tag << 32);
+  asm volatile("st.relaxed.sys.global.b64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
+__device__ __forceinline__ void ld_word(const unsigned long long* p, uint32_t& v, uint32_t& t) {
+  unsigned long long w;
+  asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+  v = (uint32_t)w;
+  t = (uint32_t)(w >> 32);
 }
 __device__ __noinline__ uint32_t ld_ll_wait(const unsigned long long* p, uint32_t tag, int32_t* err, long long budget) {
   const long long t0 = clock64();
   uint32_t v, t;
   for (;;) {
-    asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(v), "=r"(t) : "l"(p) : "memory");
+    ld_word(p, v, t);
     if (t == tag) return v;
     if (*(volatile int32_t*)err) return v;
     if (clock64() - t0 > budget) {
@@ -331,7 +380,7 @@ __device__ __noinline__ uint32_t ld_ll_wait(const unsigned long long* p, uint32_
 __device__ __forceinline__ long long x_budget(unsigned long long xit) { return xit == 1 ? (16ll << 30) : (4ll << 30); }
 __device__ __forceinline__ uint32_t ld_ll(const unsigned long long* p, uint32_t tag, int32_t* err, long long budget) {
   uint32_t v, t;
-  asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(v), "=r"(t) : "l"(p) : "memory");
+  ld_word(p, v, t);
   return t == tag ? v : ld_ll_wait(p, tag, err, budget);
 }
 // Minimum of v and the peers' words at item index io of this step: all loads issued first
@@ -344,11 +393,7 @@ __device__ __forceinline__ float x_min_peers(const unsigned long long* own, int 
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int q = (j0 + j) < me ? (j0 + j) : (j0 + j) + 1;
-      if (j0 + j < world - 1)
-        asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];"
-                     : "=r"(wv[j]), "=r"(wt[j])
-                     : "l"(own + (size_t)(par * world + q) * slot + io)
-                     : "memory");
+      if (j0 + j < world - 1) ld_word(own + (size_t)(par * world + q) * slot + io, wv[j], wt[j]);
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -459,7 +504,8 @@ struct TauK {
 };
 __device__ __forceinline__ void exact_fallback(float* s_M, const int32_t* s_amb, const int4* s_pos, int namb, int nitem,
                                                const int32_t* rowg, int nK, int row_cap, int rank, int G, int W,
-                                               const TauK& tk, Ctl* ctl, const int4* cs_pub_K, int cs_n, int self) {
+                                               const TauK& tk, Ctl* ctl, const int4* cs_pub_K, int cs_n, int self,
+                                               int32_t* stepx_k) {
   const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31;
   const int nit = namb <= AMB_MAX ? namb : nitem;  // overflow: walk every owned item
   for (int it2 = 0; it2 < nit; ++it2) {
@@ -490,14 +536,16 @@ __device__ __forceinline__ void exact_fallback(float* s_M, const int32_t* s_amb,
       const unsigned long long x = ctl->xmin;
       s_M[i] = ((int64_t)x < tk.r2[t]) ? (float)x : FLT_MAX;
       atomicAdd(&ctl->n_exact, 1);
+      if (stepx_k) atomicAdd(stepx_k, 1);  // per-step count: a resumed walk sums its kept prefix
     }
     __syncthreads();
   }
 }
 __device__ __noinline__ void exact_fallback_call(float* s_M, const int32_t* s_amb, const int4* s_pos, int namb,
                                                  int nitem, const int32_t* rowg, int nK, int row_cap, int rank, int G,
-                                                 int W, TauK tk, Ctl* ctl, const int4* cs_pub_K, int cs_n, int self) {
-  exact_fallback(s_M, s_amb, s_pos, namb, nitem, rowg, nK, row_cap, rank, G, W, tk, ctl, cs_pub_K, cs_n, self);
+                                                 int W, TauK tk, Ctl* ctl, const int4* cs_pub_K, int cs_n, int self,
+                                                 int32_t* stepx_k) {
+  exact_fallback(s_M, s_amb, s_pos, namb, nitem, rowg, nK, row_cap, rank, G, W, tk, ctl, cs_pub_K, cs_n, self, stepx_k);
 }
 
 // Per-phase cycle accounting (rank 0, thread 0), enabled when args.prof != nullptr.
@@ -511,6 +559,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   const unsigned rank = cluster.block_rank();
   const unsigned G = cluster.num_blocks();
   const unsigned lgG = 31 - __clz(G);  // G is a power of two
+  const bool solo = G == 1;            // one-CTA cluster: no DSMEM (push_* / peer_ptr)
   const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int W = w.W, A = w.A, AW = A * W;
   const int NCOL = w.n_turn * W;
@@ -610,7 +659,10 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   }
   if (XP && tid < args.x_world) ctl->xp[tid] = args.x_peers[tid].recv;
   if (xinter && tid < args.x_iworld) ctl->xip[tid] = args.x_ipeers[xcl * XNODE + tid].recv;
-  __syncthreads();
+  // every CTA of the cluster has started and initialised its mbarriers before any DSMEM access
+  // (the first request's broadcast below wrote into CTAs that might not have entered yet:
+  // compute-sanitizer racecheck, profiles/r02_sanitizer.md)
+  cluster.sync();
   uint32_t par = 0;      // next wait parity per ring buffer (bit b)
   uint32_t parX = 0;     // next wait parity of the exchange mbarriers: bits 0-1 reduce-scatter, 2-3 V*
   uint32_t pending = 0;  // ring buffers issued and not yet waited
@@ -620,7 +672,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
     // ------------------------------------------------------------ next request
     if (rank == 0 && tid == 0) {
       int r = atomicAdd(args.queue + xcl, 1);
-      for (unsigned b = 0; b < G; ++b) cluster.map_shared_rank(&ctl->req, b)[0] = r;
+      for (unsigned b = 0; b < G; ++b) peer_ptr(cluster, &ctl->req, b, solo)[0] = r;
     }
     cluster.sync();
     const int r = *(volatile int32_t*)&ctl->req;
@@ -645,7 +697,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       psi = args.heading[sbase + k];
     }
     // per-request aggregates, kept by thread 0 of rank 0
-    int n_near = 0, steps_run = 0, status = 0, fail_step = -1;
+    int n_near = 0, steps_run = 0, status = 0, fail_step = -1, nex0 = 0;
     uint32_t min_sep = w.sat_d2;
     if (tid == 0) {
       // terminal flags of the starting state (terrain, goal; timeout cannot apply: k < max_steps)
@@ -661,6 +713,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         for (int kk = 0; kk < k; ++kk) {
           n_near += args.ntie[sbase + kk];
           min_sep = min(min_sep, args.stepd2[sbase + kk]);
+          if (args.stepx) nex0 += args.stepx[sbase + kk];
         }
       }
       if (lead && rank == 0 && k == 0 && !evalm) {
@@ -760,15 +813,19 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         FMDP_MARK(PH_PLOOP)
         __syncthreads();
         FMDP_MARK(PH_PROJ)
-        // ---- a3 goal (FP32 ex2), deck, a5 terrain (exact predicate, FP32 ex2 value): owned states
+        // ---- a3 goal (fp64), deck, a5 terrain (exact predicate, FP32 ex2 value): owned states.
+        //      Taken by the CTA's last threads (the first ones carry the build pass of the row
+        //      slice), so the fp64 latency overlaps the row wait and the build.
         const int ntc = ctl->ntc[p];
         const int32_t* s_tc = s_tc2 + p * TC_MAX;
-        for (int i = tid; i < n_own * W; i += NT) {
+        for (int i = (tid == NT - 1) ? NT - 1 : NT - 2 - tid; i < n_own * W; i += NT) {
           const int st = ((int)rank + (i / W) * (int)G) * W + i % W;
           const int4 q4 = s_pos[st];
-          // FP32: exact integer offsets (< 2^24), |rel err| ~ 2^-21 << the 1e-5 S tolerance (R25)
-          const float gx = (float)(q4.x - rq.dst[0]), gy = (float)(q4.y - rq.dst[1]), gz = (float)(q4.z - rq.dst[2]);
-          const double vpos = (double)(w.goal_rf * ex2_approx(w.goal_l2gf * sqrtf(fmaf(gz, gz, fmaf(gy, gy, gx * gx)))));
+          // fp64: exact integer d^2 < 2^52, correctly rounded sqrt, exp2 within an ulp
+          // -- agrees with the oracle's pow to ~1e-15, so the level / climb near-ties of the goal
+          // term (gaps ~1e-7 relative at 10 km) are decided as the oracle does
+          const double gx = (double)(q4.x - rq.dst[0]), gy = (double)(q4.y - rq.dst[1]), gz = (double)(q4.z - rq.dst[2]);
+          const double vpos = w.goal_r * exp2(w.goal_l2g * sqrt(fma(gz, gz, fma(gy, gy, gx * gx))));
           const double valt = (q4.z < w.zdeck_u) ? (w.deck_scale - w.u_m * (double)q4.z) : 0.0;
           int64_t mT = INT64_MAX;
           const int nt = ntc <= TC_MAX ? ntc : w.n_tw;
@@ -803,7 +860,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         if (args.stop && rank == 0) {  // one reading for the whole cluster
           const uint32_t f = (uint32_t)*(volatile int32_t*)args.stop;
           const uint32_t la = smem_u32(&ctl->stop[p]), lb = smem_u32(&s_bar[3 + p]);
-          for (unsigned b = 0; b < G; ++b) st_async_u32(mapa_u32(la, b), f, mapa_u32(lb, b));
+          for (unsigned b = 0; b < G; ++b) push_u32(solo, la, b, f, lb);
         }
       }
 
@@ -962,6 +1019,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         auto build_peers = [&]() -> int {
           // (a failed wait sets cs_err: the host discards the batch; later waits return at once)
           if (tid == 0) cs_wait(args, K);
+          __syncwarp();
           __syncthreads();
           const int npr = args.cs_n > (int)rank ? (args.cs_n - (int)rank + (int)G - 1) / (int)G : 0;
           TauSteps kt;
@@ -1057,7 +1115,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       // owner CTA (a mod G): DSMEM pushes completing on the receiver's mbarrier of this parity
       const uint32_t barA = smem_u32(&s_bar[3 + p]);
       if (xmode != 2 && tid < (int)G)
-        st_async_u32(mapa_u32(smem_u32(&s_stay[p * 16 + rank]), tid), ctl->stay_local[p], mapa_u32(barA, tid));
+        push_u32(solo, smem_u32(&s_stay[p * 16 + rank]), tid, ctl->stay_local[p], barA);
       if (!fin && xmode != 2) {
         const uint32_t recv_p = smem_u32(s_recv) + 4u * (uint32_t)(p * (int)G * NOWN * BLK);
         for (int i = tid, j = 0; i < A * SC_NV; i += NT, ++j) {
@@ -1069,8 +1127,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
             src = a * BLK + 4 * e;
             dst = ((int)rank * NOWN + a / (int)G) * BLK + 4 * e;
           }
-          st_async_f4(mapa_u32(recv_p + 4u * dst, own), *reinterpret_cast<const float4*>(s_stage + src),
-                      mapa_u32(barA, own));
+          push_f4(solo, recv_p + 4u * dst, own, *reinterpret_cast<const float4*>(s_stage + src), barA);
         }
         FMDP_MARK(PH_SCATTER)
       }
@@ -1104,7 +1161,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
                                     stay_all, args.x_err, x_budget(xit));
             if (xinter) m = x_stay_inter(ctl->xip, args.x_ime, args.x_iworld, args.x_slot, xpar, xtag, m, args.x_err,
                                          x_budget(xit), args.x_world > 1);
-            if (lane < (int)G) cluster.map_shared_rank(ctl, lane)->xstay[p] = m;
+            if (lane < (int)G) peer_ptr(cluster, ctl, lane, solo)->xstay[p] = m;
           }
           cluster.sync();
           stay_all = ctl->xstay[p];
@@ -1182,7 +1239,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           if (xinter) m = x_stay_inter(ctl->xip, args.x_ime, args.x_iworld, args.x_slot, xpar, xtag, m, args.x_err,
                                        x_budget(xit), args.x_world > 1);
           if (lane < (int)G)
-            st_async_u32(mapa_u32(smem_u32(&ctl->xstay[p]), lane), m, mapa_u32(smem_u32(&s_bar[5 + p]), lane));
+            push_u32(solo, smem_u32(&ctl->xstay[p]), lane, m, smem_u32(&s_bar[5 + p]));
         }
         __syncthreads();
         FMDP_MARK(PH_OWN1)
@@ -1200,12 +1257,13 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           }
           const int32_t* rowg = w.rows + (size_t)K * 4 * w.row_cap;
           const int4* csK = cosim ? args.cs_pub + (size_t)(K & 1) * args.cs_n * 2 : nullptr;
+          int32_t* sxk = (args.stepx && lead && !evalm) ? args.stepx + sbase + k : nullptr;
           if (MODE == 0)
             exact_fallback_call(s_M, s_amb, s_pos, namb, nitem, rowg, row_count(w, K), w.row_cap, (int)rank, (int)G,
-                                W, tk, ctl, csK, args.cs_n, r);
+                                W, tk, ctl, csK, args.cs_n, r, sxk);
           else
             exact_fallback(s_M, s_amb, s_pos, namb, nitem, rowg, row_count(w, K), w.row_cap, (int)rank, (int)G, W, tk,
-                           ctl, csK, args.cs_n, r);
+                           ctl, csK, args.cs_n, r, sxk);
           if (tid == 0) ctl->namb[p] = 0;
         }
         // Pass 2 (half-warp per owned action, lane = substep): values (Alg 8), V*(a)
@@ -1249,8 +1307,12 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           }
           if (oa < n_own && hl < (int)G) {  // push {V*(a), S(a)} to CTA hl
             const double vstar = (w.vmax_init_zero && !w.endpoint) ? fmax(0.0, bv) : bv;
-            st_async_d2(mapa_u32(smem_u32(&s_vv[a]), hl), vstar, bs, mapa_u32(smem_u32(&s_bar[5 + p]), hl));
+            push_d2(solo, smem_u32(&s_vv[a]), hl, vstar, bs, smem_u32(&s_bar[5 + p]));
             if (evalm && hl == 0) args.dbg_vstar[a] = vstar;
+            // parity trace of the walk itself (fmdp_set_trace): {V*(a), S(a)} of every step of
+            // the first vtrace_n requests, in whichever instantiation runs them
+            if (args.vtrace && hl == 0 && lead && !evalm && rq.slot < args.vtrace_n)
+              args.vtrace[((size_t)rq.slot * args.cap + k) * A + a] = make_double2(vstar, bs);
           }
         }
         if (tid == 0 && ctl->n_exact && rank != 0) {
@@ -1380,7 +1442,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       o.n_states = k + 1;
       o.fail_step = fail_step;
       o.n_near_ties = n_near;
-      o.n_exact = ctl->n_exact;
+      o.n_exact = nex0 + ctl->n_exact;
       o.steps_run = steps_run;
       o.min_sep_d2 = min_sep;
       o.pad = 0;

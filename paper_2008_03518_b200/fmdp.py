@@ -104,7 +104,7 @@ EXPORTS = ["fmdp_airspace_default", "fmdp_create", "fmdp_destroy", "fmdp_set_lau
            "fmdp_p2p_export", "fmdp_p2p_connect", "fmdp_schedule_p2p",
            "fmdp_schedule_departures", "fmdp_schedule_cosim", "fmdp_cosim_max", "fmdp_get_steplog", "fmdp_get_plan",
            "fmdp_num_plans", "fmdp_truncate", "fmdp_eval_step", "fmdp_get_stats", "fmdp_num_actions",
-           "fmdp_strerror", "fmdp_last_error"]
+           "fmdp_strerror", "fmdp_last_error", "fmdp_set_trace", "fmdp_get_trace"]
 
 _lib = None
 
@@ -137,6 +137,8 @@ def lib():
         L.fmdp_p2p_connect.argtypes = [vp, i32, i32, vp, vp]
         L.fmdp_schedule_p2p.argtypes = [vp, C.c_uint64, Vec3, Vec3, i64, C.POINTER(Result), vp, i32]
         L.fmdp_get_steplog.argtypes = [vp, i32, vp, vp, vp, i32, C.POINTER(i32)]
+        L.fmdp_set_trace.argtypes = [vp, i32]
+        L.fmdp_get_trace.argtypes = [vp, i32, vp, vp, i32, C.POINTER(i32)]
         L.fmdp_get_plan.argtypes = [vp, C.c_uint32, C.POINTER(i64), vp, i32, C.POINTER(i32)]
         L.fmdp_num_plans.argtypes = [vp, C.POINTER(C.c_uint32)]
         L.fmdp_truncate.argtypes = [vp, C.c_uint32]
@@ -218,12 +220,20 @@ class FMDP:
         d = Devices()
         d.device = device
         d.stream = None
+        if torch_alloc and stream is None:
+            # blocks from torch's caching allocator are stream-ordered: the library must run on the
+            # stream they are allocated for, so the context gets its own torch stream (never
+            # torch's current stream, whose pending kernels a non-blocking library stream would
+            # not be ordered against)
+            import torch
+            stream = torch.cuda.Stream(device=device)
+        self._stream = stream
         if stream is not None:
             d.stream = C.c_void_p(int(getattr(stream, "cuda_stream", stream)))
         if torch_alloc:
             import torch  # plumbing only: device memory from torch's caching allocator
             dev = torch.device("cuda", device)
-            tstream = stream if stream is not None else torch.cuda.current_stream(dev)
+            tstream = stream
 
             def _alloc(nbytes, user):
                 return int(torch.cuda.caching_allocator_alloc(int(nbytes), device=dev, stream=tstream))
@@ -441,6 +451,20 @@ class FMDP:
                     "fmdp_get_steplog")
         k = n.value
         return ast[:max(k - 1, 0)].copy(), hd[:k].copy(), nt[:max(k - 1, 0)].copy()
+
+    def set_trace(self, n_requests: int):
+        """Record V*(a), S(a) of every decision step of the first n_requests of later calls."""
+        self._check(self.L.fmdp_set_trace(self.ctx, int(n_requests)), "fmdp_set_trace")
+
+    def trace(self, index: int):
+        """(vstar[n_steps, A], scale[n_steps, A]) of request `index` of the last call."""
+        n = C.c_int32()
+        cap = self.max_steps + 2
+        vs = np.zeros(cap * self.A, np.float64)
+        sc = np.zeros(cap * self.A, np.float64)
+        self._check(self.L.fmdp_get_trace(self.ctx, int(index), _p(vs), _p(sc), cap, C.byref(n)), "fmdp_get_trace")
+        k = n.value
+        return vs[:k * self.A].reshape(k, self.A), sc[:k * self.A].reshape(k, self.A)
 
     def eval_step(self, q, psi: int, goal, K: int):
         A, W = self.A, self.W

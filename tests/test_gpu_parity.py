@@ -129,6 +129,7 @@ def test_c1_trajectory_lockstep_replay(F):
     ast, hd, _ = ctx.steplog(0)
     st = orc.replay(sc.src[0], sc.dst[0], int(sc.t0[0]), r.traj, hd, ast, r.status)
     assert st.n_fail == 0, f"first failing step {st.first_fail_step}"
+    print(f"\nc1 replay: {st.n_steps_checked} steps, {st.n_near_ties} near-ties, {st.n_divergent} divergent")
     ref = orc.schedule(sc.src[0], sc.dst[0], int(sc.t0[0]), commit=False)
     if st.n_divergent == 0:
         assert r.status == ref.status and r.n_states == ref.n_states and (r.traj == ref.traj).all()
@@ -152,13 +153,16 @@ def _replay_fcfs(sc, results, gpu_ctx):
     """Oracle lockstep replay of every request against the store the GPU had at that
     request (initial plans + earlier GPU-accepted plans, in FCFS order)."""
     orc = O.for_scenario(sc)
-    fails = 0
+    fails = div = steps = 0
     for i, r in enumerate(results):
         ast, hd, _ = gpu_ctx.steplog(i)
         st = orc.replay(sc.src[i], sc.dst[i], int(sc.t0[i]), r.traj, hd, ast, r.status)
         fails += st.n_fail
+        div += st.n_divergent
+        steps += st.n_steps_checked
         if r.status == 0:
             orc.add_plan(int(sc.t0[i]), r.traj)
+    print(f"\nFCFS replay: {steps} steps, {div} divergent, {fails} failing")
     return fails
 
 
@@ -173,6 +177,7 @@ def test_batch_speculative_equals_sequential_and_oracle(F):
         for x, y in zip(spec, seq):
             assert x.status == y.status and x.n_states == y.n_states and (x.traj == y.traj).all()
             assert x.plan_id == y.plan_id and x.min_sep_m == y.min_sep_m and x.n_near_ties == y.n_near_ties
+            assert x.n_exact == y.n_exact  # per-step exact counts survive pauses and rollbacks
     assert a.num_plans() == b.num_plans()
     for pid in range(len(sc.plans), a.num_plans()):
         ta, sa = a.get_plan(pid)
