@@ -7,13 +7,28 @@
  * min-distance identity, no culling: every (projected state, peak) pair is
  * evaluated as Algs 4, 6, 7 state it.
  *
- * Build: gcc -O2 -ffp-contract=off -fno-fast-math -fPIC -shared -o liboracle.so fmdp_oracle.c -lm
+ * Build: gcc -O2 -ffp-contract=off -fno-fast-math -fopenmp -fPIC -shared -o liboracle.so fmdp_oracle.c -lm
+ *
+ * Threads (SURVEY §8(c) c.7, (d) d.5 ii): orc_set_threads(n > 1) spreads the per-state loops of
+ * one decision step over n OpenMP threads (host timing of the baseline only).  Every per-state
+ * value is a max over the same wells in the same order whichever thread computes it, so the
+ * results are identical to the single-thread run (tested).
  */
 #include "fmdp_oracle.h"
 
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+static int g_threads = 1;
+
+int orc_set_threads(int n) {
+  g_threads = n < 1 ? 1 : n;
+  return g_threads;
+}
 
 /* ------------------------------------------------------------------------- */
 /* Parameter conversion to integer units (R23: u-quantised world).  */
@@ -316,6 +331,7 @@ int orc_eval_step_peers(const orc_params* p, const orc_terrain* T, const orc_sto
   if ((rc = orc_project(p, q, psi, proj, ppsi))) goto done;
 
   /* Process positive rewards (Alg 4): P+ = { goal } (Alg 2, Table PK, R8). */
+#pragma omp parallel for num_threads(g_threads) if (g_threads > 1) schedule(static)
   for (int i = 0; i < AW; ++i) {
     vpos[i] = 0.0;
     double V = orc_goal_value(p, d2_of(&proj[3 * i], g));
@@ -323,6 +339,7 @@ int orc_eval_step_peers(const orc_params* p, const orc_terrain* T, const orc_sto
   }
 
   /* Process negative terrain rewards (Alg 6). */
+#pragma omp parallel for num_threads(g_threads) if (g_threads > 1) schedule(static)
   for (int i = 0; i < AW; ++i) {
     vter[i] = 0.0;
     for (int w = 0; T && w < T->n_wells; ++w) {
@@ -334,17 +351,42 @@ int orc_eval_step_peers(const orc_params* p, const orc_terrain* T, const orc_sto
 
   /* Process negative intruder rewards (Alg 7): five wells per plan active at row K. */
   for (int i = 0; i < AW; ++i) vint[i] = 0.0;
-  for (int32_t j = 0; j < orc_store_count(S); ++j) {
-    int32_t pos[3], vel[3], cen[3 * ORC_MAX_TAU];
-    int64_t rad[ORC_MAX_TAU];
-    if (!orc_store_sample(S, j, K, pos, vel)) continue;
-    orc_build_wells(p, pos, vel, cen, rad);  /* Alg 2 */
-    for (int tau = 0; tau < p->n_tau; ++tau) {
-      for (int i = 0; i < AW; ++i) {
-        double V = orc_well_value(p->intr_r, p->intr_gamma, p->u_m, d2_of(&proj[3 * i], &cen[3 * tau]), rad[tau]);
-        if (V > vint[i]) vint[i] = V;  /* P:715-716 */
+  if (g_threads <= 1) {
+    for (int32_t j = 0; j < orc_store_count(S); ++j) {
+      int32_t pos[3], vel[3], cen[3 * ORC_MAX_TAU];
+      int64_t rad[ORC_MAX_TAU];
+      if (!orc_store_sample(S, j, K, pos, vel)) continue;
+      orc_build_wells(p, pos, vel, cen, rad);  /* Alg 2 */
+      for (int tau = 0; tau < p->n_tau; ++tau) {
+        for (int i = 0; i < AW; ++i) {
+          double V = orc_well_value(p->intr_r, p->intr_gamma, p->u_m, d2_of(&proj[3 * i], &cen[3 * tau]), rad[tau]);
+          if (V > vint[i]) vint[i] = V;
+        }
       }
     }
+  } else {
+    /* the same wells (plan order, then tau), built once; each state's max over them in that
+     * order on one thread -- the single-thread result exactly */
+    const int32_t np = orc_store_count(S), nt = p->n_tau;
+    int32_t* cen = (int32_t*)malloc(sizeof(int32_t) * 3 * ORC_MAX_TAU * (size_t)(np > 0 ? np : 1));
+    int64_t* rad = (int64_t*)malloc(sizeof(int64_t) * ORC_MAX_TAU * (size_t)(np > 0 ? np : 1));
+    if (!cen || !rad) { free(cen); free(rad); rc = ORC_E_NOMEM; goto done; }
+    int32_t nw = 0;
+    for (int32_t j = 0; j < np; ++j) {
+      int32_t pos[3], vel[3];
+      if (!orc_store_sample(S, j, K, pos, vel)) continue;
+      orc_build_wells(p, pos, vel, &cen[3 * nt * nw], &rad[nt * nw]);
+      nw++;
+    }
+#pragma omp parallel for num_threads(g_threads) schedule(static)
+    for (int i = 0; i < AW; ++i) {
+      for (int32_t w = 0; w < nw * nt; ++w) {
+        double V = orc_well_value(p->intr_r, p->intr_gamma, p->u_m, d2_of(&proj[3 * i], &cen[3 * w]), rad[w]);
+        if (V > vint[i]) vint[i] = V;
+      }
+    }
+    free(cen);
+    free(rad);
   }
 
   /* Process negative rewards (Alg 5): five wells per batch peer (P^-, Alg 2

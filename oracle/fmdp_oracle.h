@@ -103,6 +103,8 @@ enum { ORC_OK = 0, ORC_E_ARG = -1, ORC_E_NOMEM = -2, ORC_E_RANGE = -7 };
 enum { ORC_ACCEPTED = 0, ORC_REJ_CONFLICT = 1, ORC_REJ_TERRAIN = 2, ORC_REJ_TIMEOUT = 3 };
 
 int orc_check_params(const orc_params* p);
+/* OpenMP threads for the per-state loops of a decision step (timing only; results identical). */
+int orc_set_threads(int n);
 int orc_tables(const orc_params* p, int32_t* DX, int32_t* DY);
 int32_t orc_initial_heading(const orc_params* p, const int32_t src[3], const int32_t dst[3]);
 int orc_build_wells(const orc_params* p, const int32_t pos[3], const int32_t vel[3],

@@ -18,7 +18,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "fmdp_oracle.c")
 LIB = os.path.join(HERE, "liboracle.so")
-CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-std=gnu11", "-fPIC", "-shared", "-Wall"]
+CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-std=gnu11", "-fPIC", "-shared", "-Wall"]
 
 ACCEPTED, REJ_CONFLICT, REJ_TERRAIN, REJ_TIMEOUT = 0, 1, 2, 3
 _lock = threading.Lock()
@@ -83,6 +83,8 @@ def lib():
             vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
             P = C.POINTER(Params)
             L.orc_check_params.argtypes = [P]
+            L.orc_set_threads.argtypes = [C.c_int]
+            L.orc_set_threads.restype = C.c_int
             L.orc_tables.argtypes = [P, vp, vp]
             L.orc_initial_heading.argtypes = [P, vp, vp]
             L.orc_initial_heading.restype = i32
@@ -377,6 +379,11 @@ class Oracle:
         if rc:
             raise RuntimeError(f"orc_cosim_replay failed ({rc})")
         return [st[i] for i in range(n)]
+
+
+def set_threads(n: int) -> int:
+    """OpenMP threads of the oracle's per-state loops (host timing only; identical results)."""
+    return int(lib().orc_set_threads(int(n)))
 
 
 def for_scenario(sc, plans=True) -> Oracle:

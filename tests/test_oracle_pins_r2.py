@@ -198,3 +198,27 @@ def test_terrain_collision_constructed_building(i):
         t2 = fs.Terrain(nx=NY, ny=NX, x0=X0, y0=Y0, cell=CELL, height=np.ascontiguousarray(T.height.T))
         r2 = O.Oracle(fs.Airspace(), t2).schedule(fs.m2u(src_m), fs.m2u(dst_m), 0, commit=False)
         assert not (r2.status == O.REJ_TERRAIN and r2.fail_step == k)
+
+
+# --------------------------------------------------------------------------- OpenMP timing variant
+def test_openmp_variant_identical_to_single_thread():
+    """the multi-threaded oracle (host timing of the baseline) computes every
+    per-state max over the same wells in the same order -> bit-identical outputs."""
+    sc = fs.random_small(17, n_plans=80, n_requests=2, half_m=1200.0, n_buildings=20)
+    states = fs.random_states(18, sc, 5)
+    outs = []
+    try:
+        for th in (1, 4):
+            O.set_threads(th)
+            o = O.for_scenario(sc)
+            steps = [o.eval_step(q, psi, g, K) for q, psi, g, K in states]
+            r = o.schedule(sc.src[0], sc.dst[0], sc.t0[0], commit=False)
+            outs.append((steps, r))
+    finally:
+        O.set_threads(1)
+    for a, b in zip(outs[0][0], outs[1][0]):
+        for f in ("v_pos", "v_int", "v_ter", "v_alt", "v", "vstar", "conf_d2"):
+            assert (getattr(a, f) == getattr(b, f)).all(), f
+        assert a.a_star == b.a_star and a.gap == b.gap
+    ra, rb = outs[0][1], outs[1][1]
+    assert ra.status == rb.status and (ra.traj == rb.traj).all() and (ra.astar == rb.astar).all()
