@@ -311,6 +311,24 @@ __device__ __noinline__ bool cs_wait_until(const unsigned* arrive, int32_t* err,
 __device__ __forceinline__ bool cs_wait(const WalkArgs& a, int64_t K) {
   return cs_wait_until(a.cs_arrive, a.cs_err, (unsigned)a.cs_n * (unsigned)(K - a.cs_k0 + 1));
 }
+// Non-aligned CTA barriers (barrier.sync / barrier.red without .aligned): the lanes of a warp may
+// arrive separately -- used where thread 0 spins on the co-simulation clock while its warp-mates
+// wait (compute-sanitizer synccheck flags the aligned __syncthreads there).
+__device__ __forceinline__ void bar_sync_na() { asm volatile("barrier.sync 0;" ::: "memory"); }
+__device__ __forceinline__ bool bar_and_na(bool v) {
+  uint32_t r;
+  asm volatile(
+      "{\n"
+      ".reg .pred a, b;\n"
+      "setp.ne.u32 a, %1, 0;\n"
+      "barrier.red.and.pred b, 0, a;\n"
+      "selp.u32 %0, 1, 0, b;\n"
+      "}\n"
+      : "=r"(r)
+      : "r"((uint32_t)v)
+      : "memory");
+  return r != 0;
+}
 // Clocks [K0, K1) (or until every walker has finished) on which walker i is not flying:
 // publish flags, keep the clock.  All threads of one CTA; false on a barrier failure.
 __device__ __noinline__ bool cs_idle(int4* pub_all, unsigned* arrive, int32_t* err, int n, int64_t k0, Ctl* ctl, int i,
@@ -323,13 +341,12 @@ __device__ __noinline__ bool cs_idle(int4* pub_all, unsigned* arrive, int32_t* e
       asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(arrive) : "memory");
       ctl->cs_ok = cs_wait_until(arrive, err, (unsigned)n * (unsigned)(K - k0 + 1)) ? 1 : 0;
     }
-    __syncwarp();  // warp 0 reconverges after thread 0's spin before the aligned CTA barrier
-    __syncthreads();
+    bar_sync_na();
     const bool ok = ctl->cs_ok != 0;
     bool all = until_all;
     if (ok && until_all)
       for (int j = threadIdx.x; j < n; j += blockDim.x) all &= __ldcg(&pub[2 * j]).w == CS_FINISHED;
-    all = __syncthreads_and(all);  // also orders cs_ok's read before the next write
+    all = bar_and_na(all);  // also orders cs_ok's read before the next write
     if (!ok) return false;
     if (all) return true;
   }
@@ -1019,8 +1036,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         auto build_peers = [&]() -> int {
           // (a failed wait sets cs_err: the host discards the batch; later waits return at once)
           if (tid == 0) cs_wait(args, K);
-          __syncwarp();
-          __syncthreads();
+          bar_sync_na();
           const int npr = args.cs_n > (int)rank ? (args.cs_n - (int)rank + (int)G - 1) / (int)G : 0;
           TauSteps kt;
 #pragma unroll

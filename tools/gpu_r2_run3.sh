@@ -1,0 +1,3 @@
+python -c "import __graft_entry__ as g; g.build()"
+timeout 600 python tools/step_probe.py --plans 0,3000 --reqs 2 --sizes 16,2 --phases --batch 2>&1 | tail -20
+timeout 600 compute-sanitizer --tool synccheck --print-limit 5 python tools/sanitize.py cosim > gpurun_out/san3_synccheck_cosim.txt 2>&1; echo "synccheck cosim rc=$?"; tail -2 gpurun_out/san3_synccheck_cosim.txt
