@@ -60,6 +60,11 @@ class Airspace:
     vmax_init_zero: int = 0
     valuation: int = 0                   # 0 Alg 8 (max over the window), 1 Alg 1 endpoint
     near_tie_rel: float = 1e-4
+    # acceleration actions (R32): speed increments in units per substep per
+    # substep, speed clamped to [speed_min_mps, speed_max_mps] (both 0: constant speed_mps)
+    acc_units: Tuple[int, ...] = (0,)
+    speed_min_mps: float = 0.0
+    speed_max_mps: float = 0.0
     # store geometry (library side only; the oracle ignores these)
     lo_m: Tuple[float, float, float] = (-8000.0, -8000.0, 0.0)
     hi_m: Tuple[float, float, float] = (8000.0, 8000.0, 1500.0)
@@ -68,7 +73,7 @@ class Airspace:
 
     @property
     def n_actions(self) -> int:
-        return len(self.turn_steps) * len(self.climb_units)
+        return len(self.turn_steps) * len(self.acc_units) * len(self.climb_units)
 
     def replace(self, **kw) -> "Airspace":
         return dataclasses.replace(self, **kw)

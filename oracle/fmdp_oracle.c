@@ -45,6 +45,7 @@ static int to_units(double x, double u, int64_t* out) {
 
 typedef struct conv {
   int64_t step_u;                 /* v0*dt/u                          */
+  int64_t vmin_u, vmax_u;         /* speed bounds, units per substep (R32) */
   int64_t k_tau[ORC_MAX_TAU];     /* tau/dt substeps (Table PK)   */
   int64_t R_tau[ORC_MAX_TAU];     /* 300+10 tau metres -> units         */
   int64_t R_max;
@@ -56,6 +57,16 @@ static int convert(const orc_params* p, conv* c) {
   if (p->n_turn < 1 || p->n_turn > ORC_MAX_TURN || p->n_climb < 1 || p->n_climb > ORC_MAX_CLIMB) return ORC_E_ARG;
   if (p->n_tau < 0 || p->n_tau > ORC_MAX_TAU) return ORC_E_ARG;
   if (to_units(p->speed_mps * p->dt_s, p->u_m, &c->step_u)) return ORC_E_ARG;
+  /* acceleration actions (R32): speed in units per substep, clamped to
+   * [speed_min, speed_max]; with no bounds given (0) the speed is held at v0 */
+  if (p->n_acc < 1 || p->n_acc > ORC_MAX_ACC) return ORC_E_ARG;
+  if (p->speed_min_mps > 0 || p->speed_max_mps > 0) {
+    if (to_units(p->speed_min_mps * p->dt_s, p->u_m, &c->vmin_u)) return ORC_E_ARG;
+    if (to_units(p->speed_max_mps * p->dt_s, p->u_m, &c->vmax_u)) return ORC_E_ARG;
+    if (c->vmin_u < 1 || c->vmin_u > c->step_u || c->step_u > c->vmax_u) return ORC_E_ARG;
+  } else {
+    c->vmin_u = c->vmax_u = c->step_u;
+  }
   c->R_max = 0;
   for (int i = 0; i < p->n_tau; ++i) {
     double k = p->tau_s[i] / p->dt_s;
@@ -80,6 +91,29 @@ int orc_check_params(const orc_params* p) {
 /* D[psi] = L*(cos, sin)(2*pi*psi/HL) rounded, defined on the first octant and */
 /* reflected / rotated so the lattice is exactly symmetric.                    */
 /* ------------------------------------------------------------------------- */
+/* Displacement of one substep at heading psi and speed v (units per substep): the lattice above
+ * with L = v (R32; at v = v0 it is exactly the constant-speed table). */
+void orc_direction(int32_t HL, int64_t v, int32_t psi, int32_t* dx, int32_t* dy) {
+  const int Q = HL / 4, O = HL / 8;
+  const double L = (double)v;
+  int quad = psi / Q, r = psi % Q;
+  double a, b;
+  if (r <= O) {
+    a = rint(L * cos(2.0 * M_PI * r / HL));
+    b = rint(L * sin(2.0 * M_PI * r / HL));
+  } else {
+    int m = Q - r;
+    a = rint(L * sin(2.0 * M_PI * m / HL));
+    b = rint(L * cos(2.0 * M_PI * m / HL));
+  }
+  switch (quad) {
+    case 0: *dx = (int32_t)a;  *dy = (int32_t)b;  break;
+    case 1: *dx = (int32_t)-b; *dy = (int32_t)a;  break;
+    case 2: *dx = (int32_t)-a; *dy = (int32_t)-b; break;
+    default: *dx = (int32_t)b; *dy = (int32_t)-a; break;
+  }
+}
+
 int orc_tables(const orc_params* p, int32_t* DX, int32_t* DY) {
   conv c;
   if (convert(p, &c)) return ORC_E_ARG;
@@ -138,38 +172,59 @@ int orc_build_wells(const orc_params* p, const int32_t pos[3], const int32_t vel
 }
 
 /* ------------------------------------------------------------------------- */
-/* Forward projection (Alg 3): the action (turn h, climb c) is held  */
-/* for W substeps; psi_t = psi_{t-1} + h, q_t = q_{t-1} + (DX,DY)[psi_t] + c.  */
-/* Action index a = i_turn * n_climb + i_climb.                                */
+/* Forward projection (Alg 3): the action (turn h, acceleration acc, climb c) is held */
+/* for W substeps; psi_t = psi_{t-1} + h, v_t = clamp(v_{t-1} + acc, vmin, vmax),              */
+/* q_t = q_{t-1} + (D(psi_t, v_t), c)  (SPEC step_dynamics: heading, then speed, then move).   */
+/* Action index a = (i_turn * n_acc + i_acc) * n_climb + i_climb (n_acc = 1: i_turn*n_climb+c). */
 /* ------------------------------------------------------------------------- */
-int orc_project(const orc_params* p, const int32_t q[3], int32_t psi, int32_t* states, int32_t* psi_out) {
-  int32_t* DX = (int32_t*)malloc(sizeof(int32_t) * p->HL);
-  int32_t* DY = (int32_t*)malloc(sizeof(int32_t) * p->HL);
-  if (!DX || !DY) { free(DX); free(DY); return ORC_E_NOMEM; }
-  if (orc_tables(p, DX, DY)) { free(DX); free(DY); return ORC_E_ARG; }
+int orc_project_v(const orc_params* p, const int32_t q[3], int32_t psi, int32_t v, int32_t* states,
+                  int32_t* psi_out, int32_t* v_out) {
+  conv c;
+  if (convert(p, &c)) return ORC_E_ARG;
   const int W = p->W;
   for (int it = 0; it < p->n_turn; ++it) {
-    for (int ic = 0; ic < p->n_climb; ++ic) {
-      int a = it * p->n_climb + ic;
-      int64_t x = q[0], y = q[1], z = q[2];
-      int32_t h = psi;
-      for (int t = 1; t <= W; ++t) {
-        h = pmod((int64_t)h + p->turn_steps[it], p->HL);
-        x += DX[h];
-        y += DY[h];
-        z += p->climb_units[ic];
-        int idx = a * W + (t - 1);
-        states[3 * idx + 0] = (int32_t)x;
-        states[3 * idx + 1] = (int32_t)y;
-        states[3 * idx + 2] = (int32_t)z;
-        if (psi_out) psi_out[idx] = h;
+    for (int ia = 0; ia < p->n_acc; ++ia) {
+      for (int ic = 0; ic < p->n_climb; ++ic) {
+        int a = (it * p->n_acc + ia) * p->n_climb + ic;
+        int64_t x = q[0], y = q[1], z = q[2];
+        int32_t h = psi;
+        int64_t sp = v;
+        for (int t = 1; t <= W; ++t) {
+          h = pmod((int64_t)h + p->turn_steps[it], p->HL);
+          sp += p->acc_units[ia];
+          if (sp < c.vmin_u) sp = c.vmin_u;
+          if (sp > c.vmax_u) sp = c.vmax_u;
+          int32_t dx, dy;
+          orc_direction(p->HL, sp, h, &dx, &dy);
+          x += dx;
+          y += dy;
+          z += p->climb_units[ic];
+          int idx = a * W + (t - 1);
+          states[3 * idx + 0] = (int32_t)x;
+          states[3 * idx + 1] = (int32_t)y;
+          states[3 * idx + 2] = (int32_t)z;
+          if (psi_out) psi_out[idx] = h;
+          if (v_out) v_out[idx] = (int32_t)sp;
+        }
       }
     }
   }
-  free(DX);
-  free(DY);
   return ORC_OK;
 }
+
+int orc_project(const orc_params* p, const int32_t q[3], int32_t psi, int32_t* states, int32_t* psi_out) {
+  conv c;
+  if (convert(p, &c)) return ORC_E_ARG;
+  return orc_project_v(p, q, psi, (int32_t)c.step_u, states, psi_out, NULL);
+}
+
+int32_t orc_initial_speed(const orc_params* p) {
+  conv c;
+  if (convert(p, &c)) return -1;
+  return (int32_t)c.step_u;
+}
+
+static int n_actions(const orc_params* p) { return p->n_turn * p->n_acc * p->n_climb; }
 
 /* ------------------------------------------------------------------------- */
 /* Peak values.                                                                */
@@ -299,19 +354,36 @@ static int terrain_collision(const orc_terrain* T, const int32_t q[3]) {
 /* ------------------------------------------------------------------------- */
 /* One decision step: Algs 2-9 in the order of Fig 3a.             */
 /* ------------------------------------------------------------------------- */
+static int eval_step_core(const orc_params* p, const orc_terrain* T, const orc_store* S, const int32_t q[3],
+                          int32_t psi, int32_t v, const int32_t g[3], int64_t K, int32_t n_peer,
+                          const int32_t* peer_pos, const int32_t* peer_vel, orc_step_out* out);
+
 int orc_eval_step(const orc_params* p, const orc_terrain* T, const orc_store* S,
                   const int32_t q[3], int32_t psi, const int32_t g[3], int64_t K, orc_step_out* out) {
   return orc_eval_step_peers(p, T, S, q, psi, g, K, 0, NULL, NULL, out);
 }
 
+/* One decision step from (q, psi, speed v) -- the acceleration actions of SURVEY f4 (R32). */
+int orc_eval_step_v(const orc_params* p, const orc_terrain* T, const orc_store* S, const int32_t q[3], int32_t psi,
+                    int32_t v, const int32_t g[3], int64_t K, orc_step_out* out) {
+  return eval_step_core(p, T, S, q, psi, v, g, K, 0, NULL, NULL, out);
+}
+
 int orc_eval_step_peers(const orc_params* p, const orc_terrain* T, const orc_store* S,
                         const int32_t q[3], int32_t psi, const int32_t g[3], int64_t K, int32_t n_peer,
                         const int32_t* peer_pos, const int32_t* peer_vel, orc_step_out* out) {
+  return eval_step_core(p, T, S, q, psi, orc_initial_speed(p), g, K, n_peer, peer_pos, peer_vel, out);
+}
+
+static int eval_step_core(const orc_params* p, const orc_terrain* T, const orc_store* S, const int32_t q[3],
+                          int32_t psi, int32_t v0, const int32_t g[3], int64_t K, int32_t n_peer,
+                          const int32_t* peer_pos, const int32_t* peer_vel, orc_step_out* out) {
   conv c;
-  if (convert(p, &c) || !out) return ORC_E_ARG;
-  const int A = p->n_turn * p->n_climb, W = p->W, AW = A * W;
+  if (convert(p, &c) || !out || v0 < c.vmin_u || v0 > c.vmax_u) return ORC_E_ARG;
+  const int A = n_actions(p), W = p->W, AW = A * W;
   int32_t* proj = (int32_t*)malloc(sizeof(int32_t) * 3 * AW);
   int32_t* ppsi = (int32_t*)malloc(sizeof(int32_t) * AW);
+  int32_t* pv = (int32_t*)malloc(sizeof(int32_t) * AW);
   double* vpos = (double*)malloc(sizeof(double) * AW);
   double* vint = (double*)malloc(sizeof(double) * AW);
   double* vter = (double*)malloc(sizeof(double) * AW);
@@ -322,13 +394,13 @@ int orc_eval_step_peers(const orc_params* p, const orc_terrain* T, const orc_sto
   double* vsc = (double*)malloc(sizeof(double) * A);
   double* vneg = (double*)malloc(sizeof(double) * AW);
   int rc = ORC_OK;
-  if (!proj || !ppsi || !vpos || !vint || !vter || !valt || !v || !scale || !vstar || !vsc || !vneg) {
+  if (!proj || !ppsi || !pv || !vpos || !vint || !vter || !valt || !v || !scale || !vstar || !vsc || !vneg) {
     rc = ORC_E_NOMEM;
     goto done;
   }
 
   /* Forward project (Alg 3). */
-  if ((rc = orc_project(p, q, psi, proj, ppsi))) goto done;
+  if ((rc = orc_project_v(p, q, psi, v0, proj, ppsi, pv))) goto done;
 
   /* Process positive rewards (Alg 4): P+ = { goal } (Alg 2, Table PK, R8). */
 #pragma omp parallel for num_threads(g_threads) if (g_threads > 1) schedule(static)
@@ -460,9 +532,10 @@ int orc_eval_step_peers(const orc_params* p, const orc_terrain* T, const orc_sto
   if (out->vstar_scale) memcpy(out->vstar_scale, vsc, sizeof(double) * A);
   if (out->proj) memcpy(out->proj, proj, sizeof(int32_t) * 3 * AW);
   if (out->proj_psi) memcpy(out->proj_psi, ppsi, sizeof(int32_t) * AW);
+  if (out->proj_v) memcpy(out->proj_v, pv, sizeof(int32_t) * AW);
 
 done:
-  free(proj); free(ppsi); free(vpos); free(vint); free(vter); free(valt);
+  free(proj); free(ppsi); free(pv); free(vpos); free(vint); free(vter); free(valt);
   free(v); free(scale); free(vstar); free(vsc); free(vneg);
   return rc;
 }
@@ -473,12 +546,20 @@ done:
 int orc_schedule(const orc_params* p, const orc_terrain* T, const orc_store* S,
                  const int32_t src[3], const int32_t dst[3], int64_t t0, int32_t cap,
                  int32_t* traj, int32_t* heading, int32_t* astar, orc_result* res) {
+  return orc_schedule_v(p, T, S, src, dst, t0, cap, traj, heading, NULL, astar, res);
+}
+
+/* The same with the speed of every state (R32: v0 at departure, then the chosen action's). */
+int orc_schedule_v(const orc_params* p, const orc_terrain* T, const orc_store* S,
+                   const int32_t src[3], const int32_t dst[3], int64_t t0, int32_t cap,
+                   int32_t* traj, int32_t* heading, int32_t* speed, int32_t* astar, orc_result* res) {
   conv c;
   if (convert(p, &c) || !traj || !heading || !res || cap < 1 || t0 < 0) return ORC_E_ARG;
-  const int A = p->n_turn * p->n_climb, W = p->W;
+  const int A = n_actions(p), W = p->W;
   const int64_t sat = c.R_max * c.R_max, sep2 = c.sep_u * c.sep_u, cap2 = c.cap_u * c.cap_u;
   int32_t q[3] = {src[0], src[1], src[2]};
   int32_t psi = orc_initial_heading(p, src, dst);
+  int32_t v = (int32_t)c.step_u;
   int64_t K = t0;
   int32_t k = 0;
   memset(res, 0, sizeof(*res));
@@ -486,6 +567,7 @@ int orc_schedule(const orc_params* p, const orc_terrain* T, const orc_store* S,
   res->min_sep_d2 = sat;
   memcpy(&traj[0], q, sizeof(q));
   heading[0] = psi;
+  if (speed) speed[0] = v;
 
   /* Initial terminal tests at the departure row. */
   int64_t n0 = nearest_d2(S, q, K, sat);
@@ -496,7 +578,8 @@ int orc_schedule(const orc_params* p, const orc_terrain* T, const orc_store* S,
 
   int32_t* proj = (int32_t*)malloc(sizeof(int32_t) * 3 * A * W);
   int32_t* ppsi = (int32_t*)malloc(sizeof(int32_t) * A * W);
-  if (!proj || !ppsi) { free(proj); free(ppsi); return ORC_E_NOMEM; }
+  int32_t* pv = (int32_t*)malloc(sizeof(int32_t) * A * W);
+  if (!proj || !ppsi || !pv) { free(proj); free(ppsi); free(pv); return ORC_E_NOMEM; }
   int rc = ORC_OK;
   for (;;) {
     if (k + 1 >= cap) { rc = ORC_E_RANGE; break; }
@@ -504,17 +587,20 @@ int orc_schedule(const orc_params* p, const orc_terrain* T, const orc_store* S,
     memset(&o, 0, sizeof(o));
     o.proj = proj;
     o.proj_psi = ppsi;
-    if ((rc = orc_eval_step(p, T, S, q, psi, dst, K, &o))) break;
+    o.proj_v = pv;
+    if ((rc = orc_eval_step_v(p, T, S, q, psi, v, dst, K, &o))) break;
     if (o.near_tie) res->n_near_ties += 1;
     if (astar) astar[k] = o.a_star;
     /* s_{t+1} <- Delta_1[a*] (Alg 1; R5). */
     int i1 = o.a_star * W + 0;
     q[0] = proj[3 * i1 + 0]; q[1] = proj[3 * i1 + 1]; q[2] = proj[3 * i1 + 2];
     psi = ppsi[i1];
+    v = pv[i1];
     k += 1;
     K += 1;
     memcpy(&traj[3 * k], q, sizeof(q));
     heading[k] = psi;
+    if (speed) speed[k] = v;
     /* Determine terminal state (Sec IV.I), priority order R15/R16/R20. */
     int64_t nd = nearest_d2(S, q, K, sat);
     if (nd < res->min_sep_d2) res->min_sep_d2 = nd;
@@ -526,6 +612,7 @@ int orc_schedule(const orc_params* p, const orc_terrain* T, const orc_store* S,
   res->n_states = k + 1;
   free(proj);
   free(ppsi);
+  free(pv);
   return rc;
 }
 
@@ -558,20 +645,33 @@ int orc_replay(const orc_params* p, const orc_terrain* T, const orc_store* S,
                const int32_t src[3], const int32_t dst[3], int64_t t0,
                int32_t n, const int32_t* traj, const int32_t* heading, const int32_t* astar,
                int32_t status, orc_replay_stats* st) {
+  return orc_replay_v(p, T, S, src, dst, t0, n, traj, heading, NULL, astar, status, st);
+}
+
+/* speed: the speed of every state (R32), or NULL for constant speed v0. */
+int orc_replay_v(const orc_params* p, const orc_terrain* T, const orc_store* S,
+                 const int32_t src[3], const int32_t dst[3], int64_t t0,
+                 int32_t n, const int32_t* traj, const int32_t* heading, const int32_t* speed, const int32_t* astar,
+                 int32_t status, orc_replay_stats* st) {
   conv c;
   if (convert(p, &c) || !st || n < 1) return ORC_E_ARG;
   memset(st, 0, sizeof(*st));
   st->first_fail_step = -1;
-  const int A = p->n_turn * p->n_climb, W = p->W;
+  const int A = n_actions(p), W = p->W;
   const int64_t sat = c.R_max * c.R_max, sep2 = c.sep_u * c.sep_u, cap2 = c.cap_u * c.cap_u;
 #define FAIL(k_) do { st->n_fail++; if (st->first_fail_step < 0) st->first_fail_step = (k_); } while (0)
   if (traj[0] != src[0] || traj[1] != src[1] || traj[2] != src[2]) FAIL(0);
   if (heading[0] != orc_initial_heading(p, src, dst)) FAIL(0);
+  if (speed && speed[0] != c.step_u) FAIL(0);
   double* vstar = (double*)malloc(sizeof(double) * A);
   double* vsc = (double*)malloc(sizeof(double) * A);
   int32_t* proj = (int32_t*)malloc(sizeof(int32_t) * 3 * A * W);
   int32_t* ppsi = (int32_t*)malloc(sizeof(int32_t) * A * W);
-  if (!vstar || !vsc || !proj || !ppsi) { free(vstar); free(vsc); free(proj); free(ppsi); return ORC_E_NOMEM; }
+  int32_t* pv = (int32_t*)malloc(sizeof(int32_t) * A * W);
+  if (!vstar || !vsc || !proj || !ppsi || !pv) {
+    free(vstar); free(vsc); free(proj); free(ppsi); free(pv);
+    return ORC_E_NOMEM;
+  }
   for (int32_t k = 0; k < n; ++k) {
     const int32_t* q = &traj[3 * k];
     int64_t K = t0 + k;
@@ -593,7 +693,8 @@ int orc_replay(const orc_params* p, const orc_terrain* T, const orc_store* S,
     o.vstar_scale = vsc;
     o.proj = proj;
     o.proj_psi = ppsi;
-    if (orc_eval_step(p, T, S, q, heading[k], dst, K, &o)) { FAIL(k); break; }
+    o.proj_v = pv;
+    if (orc_eval_step_v(p, T, S, q, heading[k], speed ? speed[k] : (int32_t)c.step_u, dst, K, &o)) { FAIL(k); break; }
     st->n_steps_checked++;
     if (o.near_tie) st->n_near_ties++;
     int ag = astar ? astar[k] : o.a_star;
@@ -605,11 +706,11 @@ int orc_replay(const orc_params* p, const orc_terrain* T, const orc_store* S,
     int i1 = ag * W;
     const int32_t* q1 = &traj[3 * (k + 1)];
     if (q1[0] != proj[3 * i1] || q1[1] != proj[3 * i1 + 1] || q1[2] != proj[3 * i1 + 2] ||
-        heading[k + 1] != ppsi[i1])
+        heading[k + 1] != ppsi[i1] || (speed && speed[k + 1] != pv[i1]))
       FAIL(k);
   }
 #undef FAIL
-  free(vstar); free(vsc); free(proj); free(ppsi);
+  free(vstar); free(vsc); free(proj); free(ppsi); free(pv);
   return ORC_OK;
 }
 
@@ -654,7 +755,8 @@ int orc_cosim(const orc_params* p, const orc_terrain* T, const orc_store* S, int
               int32_t* traj, int32_t* heading, int32_t* astar, orc_result* res) {
   conv c;
   if (convert(p, &c) || n < 1 || !src || !dst || !t0 || !traj || !heading || !res || cap < 2) return ORC_E_ARG;
-  const int A = p->n_turn * p->n_climb, W = p->W;
+  if (c.vmin_u != c.vmax_u) return ORC_E_ARG;  /* co-simulation: constant-speed actions only */
+  const int A = n_actions(p), W = p->W;
   const int64_t sat = c.R_max * c.R_max, sep2 = c.sep_u * c.sep_u, cap2 = c.cap_u * c.cap_u;
   int32_t* DX = (int32_t*)malloc(sizeof(int32_t) * p->HL);
   int32_t* DY = (int32_t*)malloc(sizeof(int32_t) * p->HL);
@@ -758,7 +860,7 @@ int orc_cosim_replay(const orc_params* p, const orc_terrain* T, const orc_store*
                      const int32_t* status, orc_replay_stats* st) {
   conv c;
   if (convert(p, &c) || n < 1 || !st || !n_states || !traj || !heading || !status) return ORC_E_ARG;
-  const int A = p->n_turn * p->n_climb, W = p->W;
+  const int A = n_actions(p), W = p->W;
   const int64_t sat = c.R_max * c.R_max, sep2 = c.sep_u * c.sep_u, cap2 = c.cap_u * c.cap_u;
   int32_t* DX = (int32_t*)malloc(sizeof(int32_t) * p->HL);
   int32_t* DY = (int32_t*)malloc(sizeof(int32_t) * p->HL);

@@ -27,6 +27,7 @@ extern "C" {
 #define ORC_MAX_TURN 32
 #define ORC_MAX_CLIMB 32
 #define ORC_MAX_TAU 8
+#define ORC_MAX_ACC 16
 
 /* Scenario parameters in physical units; converted to integer units internally. */
 typedef struct orc_params {
@@ -48,6 +49,11 @@ typedef struct orc_params {
   int32_t vmax_init_zero;                    /* 1: literal Alg 8 V_max <- 0   */
   double near_tie_rel;                       /* 1e-4 (north star)                     */
   int32_t valuation;                         /* 0 Alg 8 max over t; 1 Alg 1 endpoint   */
+  /* acceleration actions (R32): n_acc speed increments (units per
+   * substep per substep), speed clamped to [speed_min, speed_max] m/s (both 0: speed held at
+   * speed_mps).  A = n_turn * n_acc * n_climb, a = (i_turn * n_acc + i_acc) * n_climb + i_climb. */
+  int32_t n_acc;  int32_t acc_units[ORC_MAX_ACC];
+  double speed_min_mps, speed_max_mps;
 } orc_params;
 
 /* Terrain: manually placed wells (Table PK) + a height raster for collision. */
@@ -80,6 +86,7 @@ typedef struct orc_step_out {
   double gap;        /* V*(a*) - V*(a_second)                */
   int32_t near_tie;  /* gap < near_tie_rel * vstar_scale[a*] */
   double* v_neg;     /* [A*W] V^- (Alg 5; batch peers) */
+  int32_t* proj_v;   /* [A*W] projected speeds (units per substep, R32) */
 } orc_step_out;
 
 typedef struct orc_result {
@@ -110,6 +117,11 @@ int32_t orc_initial_heading(const orc_params* p, const int32_t src[3], const int
 int orc_build_wells(const orc_params* p, const int32_t pos[3], const int32_t vel[3],
                     int32_t* centers, int64_t* radius_u);
 int orc_project(const orc_params* p, const int32_t q[3], int32_t psi, int32_t* states, int32_t* psi_out);
+/* Acceleration actions: projection from speed v (units per substep). */
+int orc_project_v(const orc_params* p, const int32_t q[3], int32_t psi, int32_t v, int32_t* states,
+                  int32_t* psi_out, int32_t* v_out);
+void orc_direction(int32_t HL, int64_t v, int32_t psi, int32_t* dx, int32_t* dy);
+int32_t orc_initial_speed(const orc_params* p);
 double orc_goal_value(const orc_params* p, int64_t d2);
 double orc_well_value(double r, double gamma, double u_m, int64_t d2, int64_t R_u);
 double orc_deck_penalty(const orc_params* p, int32_t z);
@@ -131,6 +143,15 @@ int orc_eval_step_peers(const orc_params* p, const orc_terrain* T, const orc_sto
 int orc_schedule(const orc_params* p, const orc_terrain* T, const orc_store* S,
                  const int32_t src[3], const int32_t dst[3], int64_t t0, int32_t cap,
                  int32_t* traj, int32_t* heading, int32_t* astar, orc_result* res);
+int orc_eval_step_v(const orc_params* p, const orc_terrain* T, const orc_store* S, const int32_t q[3], int32_t psi,
+                    int32_t v, const int32_t g[3], int64_t K, orc_step_out* out);
+int orc_schedule_v(const orc_params* p, const orc_terrain* T, const orc_store* S,
+                   const int32_t src[3], const int32_t dst[3], int64_t t0, int32_t cap,
+                   int32_t* traj, int32_t* heading, int32_t* speed, int32_t* astar, orc_result* res);
+int orc_replay_v(const orc_params* p, const orc_terrain* T, const orc_store* S,
+                 const int32_t src[3], const int32_t dst[3], int64_t t0,
+                 int32_t n, const int32_t* traj, const int32_t* heading, const int32_t* speed, const int32_t* astar,
+                 int32_t status, orc_replay_stats* st);
 int orc_schedule_batch(const orc_params* p, const orc_terrain* T, orc_store* S, int32_t n,
                        const int32_t* src, const int32_t* dst, const int64_t* t0, int32_t cap,
                        int32_t* traj, int32_t* heading, int32_t* astar, orc_result* res);

@@ -48,6 +48,8 @@ class Params(C.Structure):
         ("capture_m", C.c_double), ("sep_m", C.c_double),
         ("max_steps", C.c_int32), ("vmax_init_zero", C.c_int32), ("near_tie_rel", C.c_double),
         ("valuation", C.c_int32),
+        ("n_acc", C.c_int32), ("acc_units", C.c_int32 * 16), ("speed_min_mps", C.c_double),
+        ("speed_max_mps", C.c_double),
     ]
 
 
@@ -62,7 +64,7 @@ class StepOut(C.Structure):
                 ("v", C.c_void_p), ("scale", C.c_void_p), ("vstar", C.c_void_p), ("vstar_scale", C.c_void_p),
                 ("conf_d2", C.c_void_p), ("proj", C.c_void_p), ("proj_psi", C.c_void_p),
                 ("a_star", C.c_int32), ("a_second", C.c_int32), ("gap", C.c_double), ("near_tie", C.c_int32),
-                ("v_neg", C.c_void_p)]
+                ("v_neg", C.c_void_p), ("proj_v", C.c_void_p)]
 
 
 class Result(C.Structure):
@@ -110,6 +112,14 @@ def lib():
                                            C.POINTER(ReplayStats)]
             L.orc_schedule.argtypes = [P, C.POINTER(Terrain), vp, vp, vp, i64, i32, vp, vp, vp,
                                        C.POINTER(Result)]
+            L.orc_schedule_v.argtypes = [P, C.POINTER(Terrain), vp, vp, vp, i64, i32, vp, vp, vp, vp,
+                                         C.POINTER(Result)]
+            L.orc_replay_v.argtypes = [P, C.POINTER(Terrain), vp, vp, vp, i64, i32, vp, vp, vp, vp, i32,
+                                       C.POINTER(ReplayStats)]
+            L.orc_eval_step_v.argtypes = [P, C.POINTER(Terrain), vp, vp, i32, i32, vp, i64, C.POINTER(StepOut)]
+            L.orc_project_v.argtypes = [P, vp, i32, i32, vp, vp, vp]
+            L.orc_initial_speed.argtypes = [P]
+            L.orc_initial_speed.restype = i32
             L.orc_schedule_batch.argtypes = [P, C.POINTER(Terrain), vp, i32, vp, vp, vp, i32, vp, vp, vp,
                                              C.POINTER(Result)]
             L.orc_replay.argtypes = [P, C.POINTER(Terrain), vp, vp, vp, i64, i32, vp, vp, vp, i32,
@@ -141,6 +151,12 @@ def params_of(air) -> Params:
     p.capture_m, p.sep_m = air.capture_m, air.sep_m
     p.max_steps, p.vmax_init_zero, p.near_tie_rel = air.max_steps, air.vmax_init_zero, air.near_tie_rel
     p.valuation = getattr(air, "valuation", 0)
+    acc = tuple(getattr(air, "acc_units", (0,)))
+    p.n_acc = len(acc)
+    for i, v in enumerate(acc):
+        p.acc_units[i] = v
+    p.speed_min_mps = float(getattr(air, "speed_min_mps", 0.0))
+    p.speed_max_mps = float(getattr(air, "speed_max_mps", 0.0))
     return p
 
 
@@ -158,6 +174,7 @@ class StepResult:
     conf_d2: np.ndarray
     proj: np.ndarray
     proj_psi: np.ndarray
+    proj_v: np.ndarray
     a_star: int
     a_second: int
     gap: float
@@ -174,6 +191,7 @@ class SchedResult:
     traj: np.ndarray
     heading: np.ndarray
     astar: np.ndarray
+    speed: np.ndarray = None
 
 
 class Oracle:
@@ -241,13 +259,18 @@ class Oracle:
         assert self.L.orc_build_wells(C.byref(self.p), _ptr(p), _ptr(v), _ptr(c), _ptr(r)) == 0
         return c, r
 
-    def project(self, q, psi):
+    def project(self, q, psi, v=None, with_speed=False):
         A, W = self.A, self.air.W
         st = np.zeros((A, W, 3), np.int32)
         ps = np.zeros((A, W), np.int32)
+        sp = np.zeros((A, W), np.int32)
         qq = np.ascontiguousarray(q, np.int32)
-        assert self.L.orc_project(C.byref(self.p), _ptr(qq), int(psi), _ptr(st), _ptr(ps)) == 0
-        return st, ps
+        v = self.initial_speed() if v is None else int(v)
+        assert self.L.orc_project_v(C.byref(self.p), _ptr(qq), int(psi), v, _ptr(st), _ptr(ps), _ptr(sp)) == 0
+        return (st, ps, sp) if with_speed else (st, ps)
+
+    def initial_speed(self) -> int:
+        return int(self.L.orc_initial_speed(C.byref(self.p)))
 
     def goal_value(self, d2: int) -> float:
         return float(self.L.orc_goal_value(C.byref(self.p), int(d2)))
@@ -265,8 +288,9 @@ class Oracle:
         return (pos, vel) if ok else None
 
     # ---- one decision step --------------------------------------------------
-    def eval_step(self, q, psi, goal, K, peer_pos=None, peer_vel=None) -> StepResult:
-        """Algs 2-9 at clock K; optional batch peers (Alg 5) as [n, 3] pos / vel."""
+    def eval_step(self, q, psi, goal, K, peer_pos=None, peer_vel=None, v=None) -> StepResult:
+        """Algs 2-9 at clock K; optional batch peers (SURVEY f2, Alg 5) as [n, 3] pos / vel;
+        optional speed v (units per substep; acceleration actions, R32)."""
         A, W = self.A, self.air.W
         arr = {k: np.zeros(A * W, np.float64) for k in ("v_pos", "v_int", "v_ter", "v_alt", "v_neg", "v", "scale")}
         vstar = np.zeros(A, np.float64)
@@ -274,21 +298,28 @@ class Oracle:
         conf = np.zeros(A, np.int64)
         proj = np.zeros(A * W * 3, np.int32)
         pps = np.zeros(A * W, np.int32)
+        pv_ = np.zeros(A * W, np.int32)
         o = StepOut()
-        for k, v in arr.items():
-            setattr(o, k, _ptr(v))
+        for k_, a_ in arr.items():
+            setattr(o, k_, _ptr(a_))
         o.vstar, o.vstar_scale, o.conf_d2, o.proj, o.proj_psi = _ptr(vstar), _ptr(vsc), _ptr(conf), _ptr(proj), _ptr(pps)
+        o.proj_v = _ptr(pv_)
         qq = np.ascontiguousarray(q, np.int32)
         gg = np.ascontiguousarray(goal, np.int32)
         npeer = 0 if peer_pos is None else len(peer_pos)
         pp = np.ascontiguousarray(np.reshape(peer_pos, (-1, 3)) if npeer else np.zeros((0, 3)), np.int32)
         pv = np.ascontiguousarray(np.reshape(peer_vel, (-1, 3)) if npeer else np.zeros((0, 3)), np.int32)
-        rc = self.L.orc_eval_step_peers(C.byref(self.p), C.byref(self.T), self.S, _ptr(qq), int(psi), _ptr(gg), int(K),
-                                        npeer, _ptr(pp), _ptr(pv), C.byref(o))
+        if v is not None:
+            assert npeer == 0, "speed-carrying steps are not co-simulated"
+            rc = self.L.orc_eval_step_v(C.byref(self.p), C.byref(self.T), self.S, _ptr(qq), int(psi), int(v), _ptr(gg),
+                                        int(K), C.byref(o))
+        else:
+            rc = self.L.orc_eval_step_peers(C.byref(self.p), C.byref(self.T), self.S, _ptr(qq), int(psi), _ptr(gg),
+                                            int(K), npeer, _ptr(pp), _ptr(pv), C.byref(o))
         if rc:
             raise RuntimeError(f"orc_eval_step failed ({rc})")
         return StepResult(**{k: v.reshape(A, W) for k, v in arr.items()}, vstar=vstar, vstar_scale=vsc,
-                          conf_d2=conf, proj=proj.reshape(A, W, 3), proj_psi=pps.reshape(A, W),
+                          conf_d2=conf, proj=proj.reshape(A, W, 3), proj_psi=pps.reshape(A, W), proj_v=pv_.reshape(A, W),
                           a_star=o.a_star, a_second=o.a_second, gap=o.gap, near_tie=bool(o.near_tie))
 
     # ---- requests -----------------------------------------------------------
@@ -296,17 +327,18 @@ class Oracle:
         cap = self.air.max_steps + 2
         traj = np.zeros((cap, 3), np.int32)
         hd = np.zeros(cap, np.int32)
+        sp = np.zeros(cap, np.int32)
         ast = np.full(cap, -1, np.int32)
         r = Result()
         s = np.ascontiguousarray(src, np.int32)
         d = np.ascontiguousarray(dst, np.int32)
-        rc = self.L.orc_schedule(C.byref(self.p), C.byref(self.T), self.S, _ptr(s), _ptr(d), int(t0), cap,
-                                 _ptr(traj), _ptr(hd), _ptr(ast), C.byref(r))
+        rc = self.L.orc_schedule_v(C.byref(self.p), C.byref(self.T), self.S, _ptr(s), _ptr(d), int(t0), cap,
+                                   _ptr(traj), _ptr(hd), _ptr(sp), _ptr(ast), C.byref(r))
         if rc:
             raise RuntimeError(f"orc_schedule failed ({rc})")
         n = r.n_states
         out = SchedResult(r.status, n, r.fail_step, r.n_near_ties, r.min_sep_d2, traj[:n].copy(), hd[:n].copy(),
-                          ast[:max(n - 1, 0)].copy())
+                          ast[:max(n - 1, 0)].copy(), sp[:n].copy())
         if commit and r.status == ACCEPTED:
             self.add_plan(int(t0), out.traj)
         return out
@@ -314,15 +346,16 @@ class Oracle:
     def schedule_batch(self, src, dst, t0):
         return [self.schedule(src[i], dst[i], int(t0[i]), commit=True) for i in range(len(t0))]
 
-    def replay(self, src, dst, t0, traj, heading, astar, status) -> ReplayStats:
+    def replay(self, src, dst, t0, traj, heading, astar, status, speed=None) -> ReplayStats:
         st = ReplayStats()
         tr = np.ascontiguousarray(traj, np.int32)
         hd = np.ascontiguousarray(heading, np.int32)
+        sp = None if speed is None else np.ascontiguousarray(speed, np.int32)
         ast = None if astar is None else np.ascontiguousarray(astar, np.int32)
         s = np.ascontiguousarray(src, np.int32)
         d = np.ascontiguousarray(dst, np.int32)
-        rc = self.L.orc_replay(C.byref(self.p), C.byref(self.T), self.S, _ptr(s), _ptr(d), int(t0), int(tr.shape[0]),
-                               _ptr(tr), _ptr(hd), _ptr(ast), int(status), C.byref(st))
+        rc = self.L.orc_replay_v(C.byref(self.p), C.byref(self.T), self.S, _ptr(s), _ptr(d), int(t0),
+                                 int(tr.shape[0]), _ptr(tr), _ptr(hd), _ptr(sp), _ptr(ast), int(status), C.byref(st))
         if rc:
             raise RuntimeError(f"orc_replay failed ({rc})")
         return st

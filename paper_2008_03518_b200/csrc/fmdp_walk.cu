@@ -304,41 +304,29 @@ __device__ __forceinline__ void cs_publish(const WalkArgs& a, int i, int64_t K, 
                                            int vy, int vz) {
   cs_publish_at(a.cs_pub + ((size_t)(K & 1) * a.cs_n + i) * 2, x, y, z, flags, vx, vy, vz, a.cs_arrive);
 }
-// true once every walker has published clock K; false on a timeout (~2 s: the walkers are not
-// all resident) or when another walker timed out.  (Plain pointers: a reference to the kernel
+// Whole-warp wait (all 32 lanes, warp-uniform result): true once the arrival counter reached
+// target, false on a timeout (~2 s: the walkers are not all resident) or when another walker timed
+// out.  Lane 0 polls and the warp stays converged, so no lane spins alone while its warp-mates
+// wait at a CTA barrier (compute-sanitizer synccheck).  (Plain pointers: a reference to the kernel
 // parameters would force a local copy of them.)
-__device__ __noinline__ bool cs_wait_until(const unsigned* arrive, int32_t* err, unsigned target) {
-  if (ld_acquire_gpu(arrive) >= target) return true;
+__device__ __noinline__ bool cs_wait_warp(const unsigned* arrive, int32_t* err, unsigned target) {
   const long long t0 = clock64();
   for (;;) {
-    if (ld_acquire_gpu(arrive) >= target) return true;
-    if (*(volatile int32_t*)err) return false;
-    if (clock64() - t0 > (4ll << 30)) {
-      atomicExch(err, 1);
-      return false;
+    int st = 0;  // 1 ready, 2 failed
+    if ((threadIdx.x & 31) == 0) {
+      if (ld_acquire_gpu(arrive) >= target) st = 1;
+      else if (*(volatile int32_t*)err) st = 2;
+      else if (clock64() - t0 > (4ll << 30)) {
+        atomicExch(err, 1);
+        st = 2;
+      }
     }
+    st = __shfl_sync(0xffffffffu, st, 0);
+    if (st) return st == 1;
   }
 }
 __device__ __forceinline__ bool cs_wait(const WalkArgs& a, int64_t K) {
-  return cs_wait_until(a.cs_arrive, a.cs_err, (unsigned)a.cs_n * (unsigned)(K - a.cs_k0 + 1));
-}
-// Non-aligned CTA barriers (barrier.sync / barrier.red without .aligned): the lanes of a warp may
-// arrive separately -- used where thread 0 spins on the co-simulation clock while its warp-mates
-// wait (compute-sanitizer synccheck flags the aligned __syncthreads there).
-__device__ __forceinline__ void bar_sync_na() { asm volatile("barrier.sync 0;" ::: "memory"); }
-__device__ __forceinline__ bool bar_and_na(bool v) {
-  uint32_t r;
-  asm volatile(
-      "{\n"
-      ".reg .pred a, b;\n"
-      "setp.ne.u32 a, %1, 0;\n"
-      "barrier.red.and.pred b, 0, a;\n"
-      "selp.u32 %0, 1, 0, b;\n"
-      "}\n"
-      : "=r"(r)
-      : "r"((uint32_t)v)
-      : "memory");
-  return r != 0;
+  return cs_wait_warp(a.cs_arrive, a.cs_err, (unsigned)a.cs_n * (unsigned)(K - a.cs_k0 + 1));
 }
 // Clocks [K0, K1) (or until every walker has finished) on which walker i is not flying:
 // publish flags, keep the clock.  All threads of one CTA; false on a barrier failure.
@@ -346,18 +334,22 @@ __device__ __noinline__ bool cs_idle(int4* pub_all, unsigned* arrive, int32_t* e
                                      int64_t K0, int64_t K1, int flags, bool until_all) {
   for (int64_t K = K0; until_all || K < K1; ++K) {
     int4* pub = pub_all + (size_t)(K & 1) * n * 2;
-    if (threadIdx.x == 0) {
-      __stcg(pub + 2 * i, make_int4(0, 0, 0, flags));
-      __stcg(pub + 2 * i + 1, make_int4(0, 0, 0, 0));
-      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(arrive) : "memory");
-      ctl->cs_ok = cs_wait_until(arrive, err, (unsigned)n * (unsigned)(K - k0 + 1)) ? 1 : 0;
+    if (threadIdx.x < 32) {
+      if (threadIdx.x == 0) {
+        __stcg(pub + 2 * i, make_int4(0, 0, 0, flags));
+        __stcg(pub + 2 * i + 1, make_int4(0, 0, 0, 0));
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(arrive) : "memory");
+      }
+      __syncwarp();
+      const bool okw = cs_wait_warp(arrive, err, (unsigned)n * (unsigned)(K - k0 + 1));
+      if (threadIdx.x == 0) ctl->cs_ok = okw ? 1 : 0;
     }
-    bar_sync_na();
+    __syncthreads();
     const bool ok = ctl->cs_ok != 0;
     bool all = until_all;
     if (ok && until_all)
       for (int j = threadIdx.x; j < n; j += blockDim.x) all &= __ldcg(&pub[2 * j]).w == CS_FINISHED;
-    all = bar_and_na(all);  // also orders cs_ok's read before the next write
+    all = __syncthreads_and(all);  // also orders cs_ok's read before the next write
     if (!ok) return false;
     if (all) return true;
   }
@@ -1067,8 +1059,8 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         // j = rank + i*G.  The clock wait sits after the row's hot loop, overlapping it.
         auto build_peers = [&]() -> int {
           // (a failed wait sets cs_err: the host discards the batch; later waits return at once)
-          if (tid == 0) cs_wait(args, K);
-          bar_sync_na();
+          if (warp == 0) cs_wait(args, K);
+          __syncthreads();
           const int npr = args.cs_n > (int)rank ? (args.cs_n - (int)rank + (int)G - 1) / (int)G : 0;
           TauSteps kt;
 #pragma unroll
@@ -1198,7 +1190,10 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         }
         FMDP_MARK(PH_SCATTER)
       }
-      mbar_wait(&s_bar[3 + p], (parX >> p) & 1u);
+      // (one-CTA cluster: the pushes were plain stores of this CTA, all issued before this barrier,
+      // so a CTA barrier orders them -- the form compute-sanitizer racecheck can follow)
+      if (solo) __syncthreads();
+      else mbar_wait(&s_bar[3 + p], (parX >> p) & 1u);
       parX ^= 1u << p;
       FMDP_MARK(PH_BAR1)
       // exact nearest-plan d^2 of state k over the whole row (Sec IV.I): min of the slice minima
@@ -1382,7 +1377,8 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           ctl->n_exact = 0;
         }
         FMDP_MARK(PH_OWNER)
-        mbar_wait(&s_bar[5 + p], (parX >> (2 + p)) & 1u);
+        if (solo) __syncthreads();
+        else mbar_wait(&s_bar[5 + p], (parX >> (2 + p)) & 1u);
         parX ^= 1u << (2 + p);
         if (XP) stay_all = ctl->xstay[p];  // over the ranks, from CTA 0
         FMDP_MARK(PH_BAR2)
