@@ -387,3 +387,15 @@ def config_scaled(seed: int, n_plans: int, rows: int = 3000, n_requests: int = 2
     pads = vertiports(rng, 200, 5000.0, terrain)
     src, dst, t0 = request_pairs(rng, pads, n_requests, 3000.0, 7000.0, (0, 300))
     return Scenario(a, terrain, plans, src, dst, t0, name=f"scaled{n_plans}")
+
+
+def airspace_f4(**kw) -> Airspace:
+    """the paper-scale action space A = 1350 (Table DS / KI captions P:387),
+    factorised 15 turns x 9 accelerations x 10 climbs (SPEC's 15 x 10 x 9, R32):
+    turns -7..7 lattice steps per substep (+-1.75 deg / 0.1 s), speed increments -4..4 units per
+    substep per substep (+-6.25 m/s^2), speed in [30, 60] m/s, climbs -40..32 units per substep
+    in steps of 8 (-6.25 .. +5 m/s; 0 is the middle entry)."""
+    base = dict(turn_steps=tuple(range(-7, 8)), acc_units=tuple(range(-4, 5)),
+                climb_units=tuple(range(-40, 33, 8)), speed_min_mps=30.0, speed_max_mps=60.0)
+    base.update(kw)
+    return Airspace(**base)

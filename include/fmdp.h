@@ -223,12 +223,10 @@ fmdp_status fmdp_schedule_batch(fmdp_ctx* ctx, const fmdp_request* reqs, int32_t
 /* Plan-sharded multi-GPU scheduling, host-stepped reference path.
  * Every rank holds the same store (plans added identically on all ranks) and evaluates only
  * its shard of every time row (slots [n*rank/world, n*(rank+1)/world)).  Per decision step
- * each projected state's value -- the minimum over tau of the in-radius squared distance to the
- * rank's wells (FP32 bits; FLT_MAX: none in radius; bit pattern 1: some tau inside the FP32
- * filter band, exact rescan) -- and the nearest-plan distance (uint32), A*W + 1 values, are
- * combined with allreduce_min_u32 (in place, elementwise unsigned MIN over ranks, e.g.
- * ncclAllReduce(ncclMin) / gloo); every rank then takes the identical decision.  The per-rank
- * classification commutes with the minimum, so results are bit-identical to one GPU.
+ * the per-(projected state, tau) minimum squared distances (FP32 bits) and the nearest-plan
+ * distance (uint32) -- A*W*5 + 1 values -- are combined with allreduce_min_u32 (in place,
+ * elementwise MIN over ranks, e.g. ncclAllReduce(ncclMin) / gloo); every rank then takes the
+ * identical decision.  Minima are exact, so results are bit-identical to one GPU.
  * Collective call: every rank must call it with the same request.  The callback returns 0
  * on success. */
 typedef struct fmdp_shard {
@@ -243,7 +241,7 @@ fmdp_status fmdp_schedule_sharded(fmdp_ctx* ctx, const fmdp_shard* shard, uint64
 /* Plan-sharded multi-GPU scheduling, production form (SURVEY §8(e) "Mechanism"): the same
  * partitioning and decisions as fmdp_schedule_sharded, but the per-step exchange runs INSIDE
  * one persistent walker launch per request -- no host round-trip per step.  Each step the owner
- * CTA of every projected state on rank r stores {its value (FP32 bits, as above), step tag}
+ * CTA of every (projected state, tau) item on rank r stores {its minimum (FP32 bits), step tag}
  * as ONE 8-byte word into slot [step parity][r] of every peer's exchange area (P2P stores over
  * NVLink / NVSwitch) and polls its own area until the peers' words carry this step's tag (value
  * and readiness arrive together: no fence, no flag); CTA 0 does the same for the nearest-plan
@@ -255,7 +253,7 @@ fmdp_status fmdp_schedule_sharded(fmdp_ctx* ctx, const fmdp_shard* shard, uint64
  *
  * Setup (collective, once, before any fmdp_schedule_p2p):
  *   1. fmdp_p2p_export(ctx, world, &handle, &ptr): allocates this rank's exchange area
- *      (cudaMalloc, zeroed: 16 cluster blocks of 2 * world * (A*W + 16) 8-byte words) and
+ *      (cudaMalloc, zeroed: 16 cluster blocks of 2 * world * (A*W*5 + 16) 8-byte words) and
  *      returns its CUDA IPC
  *      handle (64 bytes; zeroed if IPC is unavailable) and its device pointer.
  *   2. exchange (handle, ptr) among the ranks (e.g. torch.distributed.all_gather_object).

@@ -57,6 +57,7 @@ struct World {
   uint64_t cell_magic;          // ceil(2^40 / cell): exact floor division for offsets < 2^25
   const int32_t* height;        // [ny][nx] units
   const int2* dxy;              // heading lattice table [HL]
+  const int2* proj;             // cumulative displacement [HL][n_turn][W]: sum_{s<=t} (DX,DY)[psi + s*turn]
 };
 
 struct Req {
@@ -96,7 +97,7 @@ struct WalkArgs {
   int32_t cull;                 // 1: f1 exact culling of plans whose wells cannot reach the states
   int32_t shard_rank, shard_world;  // plan shard of this GPU; 0, 1 = whole rows
   int32_t xmode;                // 0 normal; 1 export per-(state,tau) minima + stay; 2 import and decide
-  uint32_t* xbuf;               // [A*W + 1] exchange buffer (state values as float bits / stay d^2)
+  uint32_t* xbuf;               // [A*W*NTAU + 1] exchange buffer (float bits / stay d^2)
   double* dbg_vstar;            // [A]
   double* dbg_v;                // [A*W]
   double* dbg_s;                // [A*W]
@@ -132,8 +133,8 @@ struct WalkArgs {
 
 // One rank's exchange area as seen from this GPU (peer pointer: IPC-opened or same process):
 //   recv[(par * world + src) * slot + i] = {value, step tag} (one 8-byte word, written by rank
-//   src with a single 64-bit store): i < A*W: FP32 bits of src's value of projected state i
-//   (fmdp_walk.cu AMB_BITS); i = slot - 16 + cta: src's nearest-plan d^2 (CTA cta).
+//   src with a single 64-bit store): i < A*W*NTAU: FP32 bits of src's minimum for (state, tau)
+//   item i; i = slot - 16 + cta: src's nearest-plan d^2 (CTA cta).
 struct XPeer {
   unsigned long long* recv;
 };
@@ -144,7 +145,7 @@ inline size_t x_area_bytes(int world, int slot) {
 }
 
 // Shared-memory carve-up, identical on host (size) and device (offsets).
-//   BLK: per-action block of the reduce-scatter = W state values, padded to float4.
+//   BLK: per-action block of the reduce-scatter = W*NTAU (state, tau) minima, padded to float4.
 struct Layout {
   int HL, CH, RAWCAP, NT, C, NCOL, A, AW, G, BLK, NOWN, RAWW;
   size_t o_dxy, o_tw, o_raw, o_cen, o_stage, o_recv, o_pos, o_fix, o_sfix, o_vT, o_mI, o_vstar, o_vsc, o_conf,
@@ -152,7 +153,7 @@ struct Layout {
   __host__ __device__ static size_t al(size_t x) { return (x + 15) & ~size_t(15); }
   __host__ __device__ void build(int hl, int ch, int rawcap, int nt, int c, int ncol, int a, int aw, int g) {
     HL = hl; CH = ch; RAWCAP = rawcap; NT = nt; C = c; NCOL = ncol; A = a; AW = aw; G = g;
-    BLK = ((AW / A) + 3) & ~3;  // one value per (action, substep): fmdp_walk.cu AMB_BITS
+    BLK = ((AW / A) * NTAU + 3) & ~3;
     NOWN = (A + G - 1) / G;             // max actions owned by one CTA
     RAWW = RAWCAP + 8;                  // words per SoA array in one raw row buffer
     size_t o = 0;

@@ -56,6 +56,7 @@ struct fmdp_ctx {
   int4* d_tw = nullptr;
   int32_t* d_height = nullptr;
   int2* d_dxy = nullptr;
+  int2* d_proj = nullptr;  // cumulative projection offsets [HL][n_turn][W]
 
   // per-request scratch (grown on demand)
   int slots_cap = 0;
@@ -84,7 +85,7 @@ struct fmdp_ctx {
   int4* d_cspub = nullptr;     // co-simulation publish buffer [2][n][2]
   int32_t* d_csctr = nullptr;  // [0] arrivals, [1] barrier error
   int cs_cap = 0;
-  uint32_t* d_xbuf = nullptr;  // multi-GPU exchange buffer [A*W + 1]
+  uint32_t* d_xbuf = nullptr;  // multi-GPU exchange buffer [A*W*NTAU + 1]
   int xmode = 0, shard_rank = 0, shard_world = 1;
   // in-kernel multi-GPU exchange (fmdp_p2p_*): own area, peer table, step-tag sequence
   void* x_area = nullptr;
@@ -692,7 +693,7 @@ int split_for(fmdp_ctx* ctx, int* G_out) {
 // Exchange state of a request split over k clusters of this GPU (allocated once; a new k
 // resets the areas and tag sequences) and the walk arguments that select it.
 fmdp_status prepare_intra(fmdp_ctx* ctx, int k, fmdp::WalkArgs& a) {
-  const int slot = ((ctx->A * ctx->W + 16) + 3) & ~3;
+  const int slot = ((ctx->A * ctx->W * fmdp::NTAU + 16) + 3) & ~3;
   const size_t area_words = fmdp::x_area_bytes(fmdp::XMAX, slot) / sizeof(unsigned long long);
   if (!ctx->d_xin_area || !ctx->d_xin_peers || !ctx->d_xin_seq) {
     if (!ctx->d_xin_area)
@@ -1186,6 +1187,8 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   ctx->d_rows = (int32_t*)dalloc(ctx, sizeof(int32_t) * row_words * (size_t)w.horizon);
   ctx->d_counts = (int32_t*)dalloc(ctx, sizeof(int32_t) * (size_t)w.horizon);
   ctx->d_dxy = (int2*)dalloc(ctx, sizeof(int2) * w.HL);
+  const size_t nproj = (size_t)w.HL * a.n_turn * a.window;
+  ctx->d_proj = (int2*)dalloc(ctx, sizeof(int2) * nproj);
   ctx->d_queue = (int32_t*)dalloc(ctx, sizeof(int32_t) * 4);
   ctx->d_stop = ctx->d_queue ? ctx->d_queue + 2 : nullptr;
   ctx->d_pairctr = (unsigned long long*)dalloc(ctx, sizeof(unsigned long long));
@@ -1195,14 +1198,29 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   ctx->d_dbg_s = (double*)dalloc(ctx, sizeof(double) * A * a.window);
   ctx->d_dbg_conf = (uint32_t*)dalloc(ctx, sizeof(uint32_t) * (A + 1));
   ctx->d_dbg_astar = (int32_t*)dalloc(ctx, sizeof(int32_t) * 4);
-  ctx->d_xbuf = (uint32_t*)dalloc(ctx, sizeof(uint32_t) * ((size_t)A * a.window + 1));
-  if (!ctx->d_rows || !ctx->d_counts || !ctx->d_dxy || !ctx->d_queue || !ctx->d_pairctr || !ctx->d_prof || !ctx->d_dbg_vstar ||
+  ctx->d_xbuf = (uint32_t*)dalloc(ctx, sizeof(uint32_t) * ((size_t)A * a.window * fmdp::NTAU + 1));
+  if (!ctx->d_rows || !ctx->d_counts || !ctx->d_dxy || !ctx->d_proj || !ctx->d_queue || !ctx->d_pairctr || !ctx->d_prof || !ctx->d_dbg_vstar ||
       !ctx->d_dbg_v || !ctx->d_dbg_s || !ctx->d_dbg_conf || !ctx->d_dbg_astar || !ctx->d_xbuf) {
     return bad(FMDP_E_NOMEM, "device allocation failed");
   }
   cudaMemset(ctx->d_rows, 0, sizeof(int32_t) * row_words * (size_t)w.horizon);
   cudaMemset(ctx->d_counts, 0, sizeof(int32_t) * (size_t)w.horizon);
   cudaMemcpy(ctx->d_dxy, lat.data(), sizeof(int2) * w.HL, cudaMemcpyHostToDevice);
+  {  // Alg 3 projection offsets of every (heading, turn, substep): integer sums of lattice steps
+    std::vector<int2> proj(nproj);
+    for (int psi = 0; psi < w.HL; ++psi)
+      for (int it = 0; it < a.n_turn; ++it) {
+        int x = 0, y = 0, ps = psi;
+        for (int t = 1; t <= a.window; ++t) {
+          ps = ((ps + a.turn_steps[it]) % w.HL + w.HL) % w.HL;
+          x += lat[ps].x;
+          y += lat[ps].y;
+          proj[((size_t)psi * a.n_turn + it) * a.window + (t - 1)] = make_int2(x, y);
+        }
+      }
+    cudaMemcpy(ctx->d_proj, proj.data(), sizeof(int2) * nproj, cudaMemcpyHostToDevice);
+  }
+  w.proj = ctx->d_proj;
   ctx->counts.assign((size_t)w.horizon, 0);
   w.rows = ctx->d_rows;
   w.counts = ctx->d_counts;
@@ -1416,7 +1434,7 @@ fmdp_status fmdp_schedule_sharded(fmdp_ctx* ctx, const fmdp_shard* shard, uint64
   if (st) return st;
   if ((st = ensure_slots(ctx, 1))) return st;
   CK(cudaMemsetAsync(ctx->d_pairctr, 0, sizeof(unsigned long long), ctx->stream));
-  const int nx = ctx->A * ctx->W + 1;
+  const int nx = ctx->A * ctx->W * fmdp::NTAU + 1;
   std::vector<uint32_t> hbuf(nx);
   ctx->shard_rank = shard->rank;
   ctx->shard_world = shard->world;
@@ -1462,7 +1480,7 @@ fmdp_status fmdp_p2p_export(fmdp_ctx* ctx, int32_t world, fmdp_p2p_handle* handl
   if (!ctx->d_xpeers) ctx->d_xpeers = (fmdp::XPeer*)dalloc(ctx, sizeof(fmdp::XPeer) * fmdp::XMAX);
   if (!ctx->d_xseq) ctx->d_xseq = (unsigned long long*)dalloc(ctx, 2 * sizeof(unsigned long long));  // seq, error
   if (!ctx->d_xpeers || !ctx->d_xseq) return fail(ctx, FMDP_E_NOMEM, "exchange tables");
-  const int slot = ((ctx->A * ctx->W + 16) + 3) & ~3;
+  const int slot = ((ctx->A * ctx->W * fmdp::NTAU + 16) + 3) & ~3;
   const size_t bytes = fmdp::x_area_bytes(world, slot) * fmdp::XMAX;  // one area per cluster index
   if (cudaMalloc(&ctx->x_area, bytes) != cudaSuccess) {
     cudaGetLastError();

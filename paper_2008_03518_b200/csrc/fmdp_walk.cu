@@ -164,17 +164,6 @@ __device__ __forceinline__ float min3(float a, f2 p) {
 
 __device__ __forceinline__ int sext(uint32_t v, int bits) { return (int)(v << (32 - bits)) >> (32 - bits); }
 
-// Per projected state the kernels carry ONE value through every reduction (plan groups, CTAs,
-// clusters, GPUs): the minimum over tau of the in-radius FP32 d^2, FLT_MAX if no tau's well is in
-// radius, or AMB_BITS -- the smallest positive float, below every real d^2 (an FP32 d^2 is 0 or
-// >= 1: small distances are computed exactly) -- if some tau's minimum lies in the FP32 band
-// (exact int64 rescan by the owner).  Classifying each partial minimum before the reduction is
-// exact: a globally in-radius (state, tau) minimum is in radius in the partial that holds it, and
-// every in-radius partial is >= the global minimum; an ambiguous partial forces the rescan unless
-// some partial is exactly 0 (then 0 is the answer).  The order is the same as unsigned order of
-// the bits (host-stepped all-reduce of uint32 minima).
-constexpr uint32_t AMB_BITS = 1u;
-
 // exact squared distance, saturated at sat (= R_max^2 < 2^30): valid because any component
 // >= R_max already implies d^2 >= R_max^2.
 __device__ __forceinline__ uint32_t clamp_d2(int dx, int dy, int dz, int rmax, uint32_t sat) {
@@ -334,18 +323,14 @@ __device__ __noinline__ bool cs_idle(int4* pub_all, unsigned* arrive, int32_t* e
                                      int64_t K0, int64_t K1, int flags, bool until_all) {
   for (int64_t K = K0; until_all || K < K1; ++K) {
     int4* pub = pub_all + (size_t)(K & 1) * n * 2;
-    if (threadIdx.x < 32) {
-      if (threadIdx.x == 0) {
-        __stcg(pub + 2 * i, make_int4(0, 0, 0, flags));
-        __stcg(pub + 2 * i + 1, make_int4(0, 0, 0, 0));
-        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(arrive) : "memory");
-      }
-      __syncwarp();
-      const bool okw = cs_wait_warp(arrive, err, (unsigned)n * (unsigned)(K - k0 + 1));
-      if (threadIdx.x == 0) ctl->cs_ok = okw ? 1 : 0;
+    if (threadIdx.x == 0) {
+      __stcg(pub + 2 * i, make_int4(0, 0, 0, flags));
+      __stcg(pub + 2 * i + 1, make_int4(0, 0, 0, 0));
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(arrive) : "memory");
     }
-    __syncthreads();
-    const bool ok = ctl->cs_ok != 0;
+    // every warp waits on its own (uniform code path for the whole CTA; the CTA barrier then
+    // orders the pub reads below after the acquiring load)
+    const bool ok = __syncthreads_and(cs_wait_warp(arrive, err, (unsigned)n * (unsigned)(K - k0 + 1)));
     bool all = until_all;
     if (ok && until_all)
       for (int j = threadIdx.x; j < n; j += blockDim.x) all &= __ldcg(&pub[2 * j]).w == CS_FINISHED;
@@ -427,8 +412,8 @@ __device__ __forceinline__ float x_min_peers(const unsigned long long* own, int 
   }
   return v;
 }
-// Words of (parity, source rank) in a rank's receive area: [0, A*W) the per-state values
-// (AMB_BITS), slot - 16 + cta the nearest-plan d^2 of CTA cta.
+// Words of (parity, source rank) in a rank's receive area: [0, A*W*NTAU) the per-(state, tau)
+// minima, slot - 16 + cta the nearest-plan d^2 of CTA cta.
 __device__ __forceinline__ size_t x_word(int par, int world, int src, int slot, int i) {
   return (size_t)(par * world + src) * slot + i;
 }
@@ -515,10 +500,9 @@ __device__ __noinline__ unsigned long long cs_exact_peers(const int4* pub, int n
   return best;
 }
 
-// Exact fallback of the owner pass (rare): for every owned state flagged ambiguous (some tau's
-// FP32 minimum inside the band, s_M[i] == AMB), per tau the exact int64 minimum d^2 over the WHOLE
-// row K (and, co-simulating, the batch peers of clock K); the state's value is the minimum over
-// the taus whose exact minimum is inside the radius.  All threads of the CTA, item by item.
+// Exact fallback of the owner pass (rare): for every (state, tau) item flagged inside the FP32
+// band (s_M[i] == -1), the exact int64 minimum d^2 over the WHOLE row K (and, co-simulating, the
+// batch peers of clock K); all threads of the CTA, item by item.
 struct TauK {
   int k[NTAU];
   int64_t r2[NTAU];
@@ -531,41 +515,36 @@ __device__ __forceinline__ void exact_fallback(float* s_M, const int32_t* s_amb,
   const int nit = namb <= AMB_MAX ? namb : nitem;  // overflow: walk every owned item
   for (int it2 = 0; it2 < nit; ++it2) {
     const int i = namb <= AMB_MAX ? s_amb[it2] : it2;
-    if (__float_as_uint(s_M[i]) != AMB_BITS) continue;
-    const int oa = i / W, l = i - oa * W;
+    if (s_M[i] != -1.f) continue;
+    const int oa = i / (W * NTAU), r2 = i - oa * (W * NTAU);
+    const int l = r2 / NTAU, t = r2 - l * NTAU;
     const int sti = (rank + oa * G) * W + l;
+    if (tid == 0) ctl->xmin = ULLONG_MAX;
+    __syncthreads();
     const int4 q4 = s_pos[sti];
-    float out = FLT_MAX;
-    for (int t = 0; t < NTAU; ++t) {
-      if (tk.r2[t] <= 0) continue;  // padding tau
-      if (tid == 0) ctl->xmin = ULLONG_MAX;
-      __syncthreads();
-      const int kt = tk.k[t];
-      unsigned long long best = ULLONG_MAX;
-      for (int j = tid; j < nK; j += NT) {
-        const uint32_t pv = (uint32_t)rowg[3 * row_cap + j];
-        const int64_t cx = rowg[j] + (int64_t)kt * sext(pv, 11);
-        const int64_t cy = rowg[row_cap + j] + (int64_t)kt * sext(pv >> 11, 11);
-        const int64_t cz = rowg[2 * row_cap + j] + (int64_t)kt * sext(pv >> 22, 10);
-        const int64_t ddx = q4.x - cx, ddy = q4.y - cy, ddz = q4.z - cz;
-        best = min(best, (unsigned long long)(ddx * ddx + ddy * ddy + ddz * ddz));
-      }
-      if (cs_pub_K)  // batch peers of clock K
-        best = min(best, cs_exact_peers(cs_pub_K, cs_n, self, q4, kt));
-      for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
-      if (lane == 0 && best != ULLONG_MAX) atomicMin(&ctl->xmin, best);
-      __syncthreads();
-      const unsigned long long x = ctl->xmin;
-      if ((int64_t)x < tk.r2[t]) out = fminf(out, (float)x);
-      __syncthreads();
+    const int kt = tk.k[t];
+    unsigned long long best = ULLONG_MAX;
+    for (int j = tid; j < nK; j += NT) {
+      const uint32_t pv = (uint32_t)rowg[3 * row_cap + j];
+      const int64_t cx = rowg[j] + (int64_t)kt * sext(pv, 11);
+      const int64_t cy = rowg[row_cap + j] + (int64_t)kt * sext(pv >> 11, 11);
+      const int64_t cz = rowg[2 * row_cap + j] + (int64_t)kt * sext(pv >> 22, 10);
+      const int64_t ddx = q4.x - cx, ddy = q4.y - cy, ddz = q4.z - cz;
+      best = min(best, (unsigned long long)(ddx * ddx + ddy * ddy + ddz * ddz));
     }
+    if (cs_pub_K)  // batch peers of clock K
+      best = min(best, cs_exact_peers(cs_pub_K, cs_n, self, q4, kt));
+    for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if (lane == 0 && best != ULLONG_MAX) atomicMin(&ctl->xmin, best);
+    __syncthreads();
     if (tid == 0) {
-      s_M[i] = out;
+      const unsigned long long x = ctl->xmin;
+      s_M[i] = ((int64_t)x < tk.r2[t]) ? (float)x : FLT_MAX;
       atomicAdd(&ctl->n_exact, 1);
       if (stepx_k) atomicAdd(stepx_k, 1);  // per-step count: a resumed walk sums its kept prefix
     }
+    __syncthreads();
   }
-  __syncthreads();
 }
 __device__ __noinline__ void exact_fallback_call(float* s_M, const int32_t* s_amb, const int4* s_pos, int namb,
                                                  int nitem, const int32_t* rowg, int nK, int row_cap, int rank, int G,
@@ -815,21 +794,14 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           }
         }
         FMDP_MARK(PH_SCAN)
-        // ---- a2 forward projection (Alg 3): column (turn it, substep t) on the integer lattice:
-        //      psi_s = psi + s*h (mod HL), q_t = q + sum_{s <= t} (DX, DY)[psi_s], the lattice in
-        //      shared memory (independent loads, no L2 round trip on the step's critical path)
+        // ---- a2 forward projection (Alg 3): column (turn it, substep t) on the integer lattice
         const int it = col_it, t = col_t, h = col_h;
-        int x = qx, y = qy, ps = psi;
-        for (int s2 = 1; s2 <= W; ++s2) {
-          const int pn = ps + h;
-          const int pw = pn >= w.HL ? pn - w.HL : (pn < 0 ? pn + w.HL : pn);
-          if (s2 <= t) {
-            const int2 d = s_dxy[pw];
-            x += d.x;
-            y += d.y;
-            ps = pw;
-          }
-        }
+        // cumulative lattice displacement of (psi, turn, t) from the host-built table (one L2 load
+        // instead of t dependent lattice steps); final heading psi + t*h mod HL
+        const int2 cum = __ldg(&w.proj[((size_t)psi * w.n_turn + it) * W + (t - 1)]);
+        const int x = qx + cum.x, y = qy + cum.y;
+        int ps = (psi + t * h) % w.HL;
+        ps += ps < 0 ? w.HL : 0;
         // offsets from the fan origin o = q + (W/2) (DX, DY)[psi], doubled: the hot loop
         // evaluates |s - c|^2 - |s - o|^2 = Q + 2 (s - o).X with X = o - c, Q = |X|^2
         sx = (float)(2 * (x - qx - ox));
@@ -1059,7 +1031,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         // j = rank + i*G.  The clock wait sits after the row's hot loop, overlapping it.
         auto build_peers = [&]() -> int {
           // (a failed wait sets cs_err: the host discards the batch; later waits return at once)
-          if (warp == 0) cs_wait(args, K);
+          cs_wait(args, K);  // every warp (a failed wait sets cs_err; the host discards the batch)
           __syncthreads();
           const int npr = args.cs_n > (int)rank ? (args.cs_n - (int)rank + (int)G - 1) / (int)G : 0;
           TauSteps kt;
@@ -1127,41 +1099,26 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           }
         }
         FMDP_MARK(PH_FLAGS)
-        // radius classification in the column thread, per plan group (AMB_BITS): M = e + |s - o|^2
-        // (|s - o|^2 an exact integer < 2^24, one rounding), in radius below R^2 (1 - band), in
-        // the band -> ambiguous; then the group minimum inside the warp and per-action blocks [t]
-        // in s_stage -- one value per projected state instead of one per (state, tau)
-        float vm[C];
-        {
-          const int hx = __float2int_rn(sx) >> 1, hy = __float2int_rn(sy) >> 1;
-          const int h2 = hx * hx + hy * hy;
-#pragma unroll
-          for (int c = 0; c < C; ++c) {
-            const int dz = w.climb[c] * col_t;
-            const float so2 = (float)(h2 + dz * dz);
-            float best = FLT_MAX;
-            bool amb = false;
-#pragma unroll
-            for (int t = 0; t < NTAU; ++t) {
-              const float M = m[c][t] + so2;
-              if (M < w.R2lo[t]) best = fminf(best, M);
-              else amb |= M <= w.R2hi[t];
-            }
-            vm[c] = amb ? __uint_as_float(AMB_BITS) : best;
-          }
-        }
+        // group minimum inside the warp, then per-action blocks [t][tau] in s_stage
+        // (rounds over all C*NTAU values are unrolled so the shuffles overlap)
         if (CPW <= 8) {
 #pragma unroll
-          for (int c = 0; c < C; ++c) vm[c] = fminf(vm[c], __shfl_xor_sync(0xffffffffu, vm[c], 8));
+          for (int c = 0; c < C; ++c)
+#pragma unroll
+            for (int t = 0; t < NTAU; ++t) m[c][t] = fminf(m[c][t], __shfl_xor_sync(0xffffffffu, m[c][t], 8));
         }
         if (CPW <= 16) {
 #pragma unroll
-          for (int c = 0; c < C; ++c) vm[c] = fminf(vm[c], __shfl_xor_sync(0xffffffffu, vm[c], 16));
+          for (int c = 0; c < C; ++c)
+#pragma unroll
+            for (int t = 0; t < NTAU; ++t) m[c][t] = fminf(m[c][t], __shfl_xor_sync(0xffffffffu, m[c][t], 16));
         }
         if (grp == 0 && col < NCOL) {
           const int it = col / W, t1 = col % W;
 #pragma unroll
-          for (int c = 0; c < C; ++c) s_stage[(it * C + c) * BLK + t1] = vm[c];
+          for (int c = 0; c < C; ++c)
+#pragma unroll
+            for (int t = 0; t < NTAU; ++t) s_stage[(it * C + c) * BLK + t1 * NTAU + t] = m[c][t];
         }
         FMDP_MARK(PH_STAGE)
       }
@@ -1199,13 +1156,13 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       // exact nearest-plan d^2 of state k over the whole row (Sec IV.I): min of the slice minima
       uint32_t stay_all = w.sat_d2;
       if (xmode == 2) {
-        stay_all = args.xbuf[AW];  // all-reduced over the GPUs
+        stay_all = args.xbuf[NTAU * AW];  // all-reduced over the GPUs
       } else {
 #pragma unroll
         for (int b = 0; b < 16; ++b)  // independent loads (G <= 16)
           if (b < (int)G) stay_all = min(stay_all, s_stay[p * 16 + b]);
       }
-      if (xmode == 1 && rank == 0 && tid == 0) args.xbuf[AW] = stay_all;
+      if (xmode == 1 && rank == 0 && tid == 0) args.xbuf[NTAU * AW] = stay_all;
       uint32_t xtag = 0;
       int xpar = 0;
       if (XP) {  // publish this GPU's nearest-plan d^2 to every peer (CTA 0)
@@ -1233,18 +1190,18 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         // ---- owner epilogue (half-warp per owned action, lane = substep): G-way minimum of
         //      the partial blocks, exact in/out, values (Alg 8), V*(a)
         const float* rcv = s_recv + p * (int)G * NOWN * BLK;
-        // Pass 1 (whole CTA, one owned (action, substep) state per thread): G-way minimum of the
-        // partial blocks (multi-GPU: export / import) -> s_M = the state's in-radius d^2, FLT_MAX,
-        // or AMB_BITS (exact rescan below).  s_M lives in s_stage, free once every thread of this
-        // CTA has pushed its blocks.
+        // Pass 1 (whole CTA, one owned (action, substep, tau) per thread): G-way minimum of the
+        // partial blocks (multi-GPU: export / import), |s - o|^2 added back, radius test ->
+        // s_M = the in-radius d^2, FLT_MAX (outside), or -1 (inside the FP32 band: exact below).
+        // s_M lives in s_stage, free once every thread of this CTA has pushed its blocks.
         float* s_M = s_stage;
         __syncthreads();
-        const int nitem = n_own * W;
+        const int nitem = n_own * W * NTAU;
         if (XP) {  // this GPU's minima of the owned items -> every peer (all sends
                    // before any poll); each thread keeps its own items' minima in s_M
           for (int i = tid; i < nitem; i += NT) {
-            const int oa = i / W, r2 = i - oa * W;
-            const int io = ((int)rank + oa * (int)G) * W + r2;
+            const int oa = i / (W * NTAU), r2 = i - oa * (W * NTAU);
+            const int io = (((int)rank + oa * (int)G) * W + r2 / NTAU) * NTAU + r2 % NTAU;
             const float M = gway_min(rcv + oa * BLK + r2, (int)G, NOWN * BLK);
             s_M[i] = M;
             for (int q = 0; q < args.x_world; ++q)
@@ -1259,16 +1216,17 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           }
         }
         for (int i = tid; i < nitem; i += NT) {
-          const int oa = i / W, r2 = i - oa * W;
-          const int st = ((int)rank + oa * (int)G) * W + r2;
+          const int oa = i / (W * NTAU), r2 = i - oa * (W * NTAU);
+          const int l = r2 / NTAU, t = r2 - l * NTAU;
+          const int st = ((int)rank + oa * (int)G) * W + l;
           float M;
           if (xmode == 2) {
-            M = __uint_as_float(args.xbuf[st]);
+            M = __uint_as_float(args.xbuf[st * NTAU + t]);
           } else if (XP) {  // this GPU's minimum (sent below) and the peers' minima
-            M = x_min_peers(ctl->xp[xme], xme, args.x_world, args.x_slot, xpar, st,
+            M = x_min_peers(ctl->xp[xme], xme, args.x_world, args.x_slot, xpar, st * NTAU + t,
                             xtag, args.x_err, x_budget(xit), s_M[i]);
             if (xinter) {  // this GPU's minimum -> cluster xcl of every other GPU, then theirs
-              const int io = st;
+              const int io = st * NTAU + t;
               if (args.x_world > 1)  // (one cluster per GPU: sent with the first level above)
                 for (int q = 0; q < args.x_iworld; ++q)
                   if (q != args.x_ime)
@@ -1279,13 +1237,20 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
             }
           } else {
             M = gway_min(rcv + oa * BLK + r2, (int)G, NOWN * BLK);
-            if (xmode == 1) args.xbuf[st] = __float_as_uint(M);  // this GPU's minima
+            if (xmode == 1) args.xbuf[st * NTAU + t] = __float_as_uint(M);  // this GPU's minima
           }
-          if (__float_as_uint(M) == AMB_BITS) {
+          const int4 q4 = s_pos[st];
+          const int dx = q4.x - qx - ox, dy = q4.y - qy - oy, dz = q4.z - qz;
+          M += (float)(dx * dx + dy * dy + dz * dz);  // exact integer < 2^24; one rounding
+          float out = FLT_MAX;
+          if (M < w.R2lo[t]) {
+            out = M;
+          } else if (M <= w.R2hi[t]) {
+            out = -1.f;
             const int idx = atomicAdd(&ctl->namb[p], 1);
             if (idx < AMB_MAX) s_amb[idx] = i;
           }
-          s_M[i] = M;
+          s_M[i] = out;
         }
         if (XP && rank == 0 && warp == 0) {  // -> every CTA with its V* pushes (one reader per value)
           uint32_t m = x_stay_min(ctl->xp[xme], xme, args.x_world, args.x_slot, xpar, xtag, stay_all,
@@ -1299,8 +1264,8 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         FMDP_MARK(PH_OWN1)
         const int namb = ctl->namb[p];  // uniform after the barrier
         if (namb) {
-          // Exact fallback: min over the WHOLE row K of the int64 d^2 of every tau of each flagged
-          // state; each CTA resolves its own states (rare).  Out of line in the
+          // Exact fallback: min over the WHOLE row K of the int64 d^2 for each flagged (state,
+          // tau); each CTA resolves its own states (rare).  Out of line in the
           // full FCFS walker (smaller step code: -0.6 % batch time), inline elsewhere (measured:
           // the culled walker does not gain from the call)
           TauK tk;
@@ -1328,7 +1293,11 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           const bool act = oa < n_own && hl < W;
           const int a = (int)rank + oa * (int)G;
           const int st = a * W + hl;
-          const float mi = act ? s_M[oa * W + hl] : FLT_MAX;
+          float mi = FLT_MAX;
+          if (act) {
+#pragma unroll
+            for (int t = 0; t < NTAU; ++t) mi = fminf(mi, s_M[(oa * W + hl) * NTAU + t]);
+          }
           // a6 values
           double v = -INFINITY, sc = 0.0;
           if (act) {
@@ -1349,18 +1318,11 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
             bv = __shfl_sync(0xffffffffu, v, (lane & 16) + W - 1);
             bs = __shfl_sync(0xffffffffu, sc, (lane & 16) + W - 1);
           } else {
-            // max over the half-warp by order-preserving 64-bit keys (two 32-bit REDUX instead of
-            // four rounds of double shuffles; v + 0 folds -0 into +0 so equal values have equal
-            // keys), then the first substep holding it (ballot) and its value and scale
-            const unsigned hmask = 0xffffu << (lane & 16);
-            const unsigned long long key = act ? dkey(v + 0.0) : 0ull;
-            const unsigned khi = (unsigned)(key >> 32), klo = (unsigned)key;
-            const unsigned mhi = __reduce_max_sync(hmask, khi);
-            const unsigned mlo = __reduce_max_sync(hmask, khi == mhi ? klo : 0u);
-            const unsigned hit = (__ballot_sync(0xffffffffu, act && khi == mhi && klo == mlo) >> (lane & 16)) & 0xffffu;
-            const int src = (lane & 16) + (hit ? __ffs(hit) - 1 : 0);
-            bv = __shfl_sync(0xffffffffu, v, src);
-            bs = __shfl_sync(0xffffffffu, sc, src);
+            bv = v;
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) bv = fmax(bv, __shfl_xor_sync(0xffffffffu, bv, o, 16));
+            const unsigned hit = (__ballot_sync(0xffffffffu, act && v == bv) >> (lane & 16)) & 0xffffu;
+            bs = __shfl_sync(0xffffffffu, sc, (lane & 16) + (hit ? __ffs(hit) - 1 : 0));
           }
           if (oa < n_own && hl < (int)G) {  // push {V*(a), S(a)} to CTA hl
             const double vstar = (w.vmax_init_zero && !w.endpoint) ? fmax(0.0, bv) : bv;
