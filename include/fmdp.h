@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define FMDP_ABI_VERSION 2  /* 2: fmdp_airspace.valuation */
+#define FMDP_ABI_VERSION 3  /* 2: fmdp_airspace.valuation; 3: acceleration actions (n_acc ...) */
 
 typedef struct fmdp_ctx fmdp_ctx; /* opaque; owns device memory, plan store, scratch */
 typedef int32_t fmdp_status;
@@ -105,6 +105,19 @@ typedef struct fmdp_airspace {
   int32_t valuation;               /* 0: Alg 8 V*(a) = max over the window;  */
                                    /* 1: Alg 1 endpoint only, V*(a) = V(Delta_10(a))     */
                                    /*    (R31)           */
+  /* Acceleration actions (the paper's A = 1350, Table DS / KI captions P:387,
+   * P:417; SPEC 15 x 10 x 9; R32).  The action becomes (turn, speed increment, climb),
+   * index a = (i_turn * n_acc + i_acc) * n_climb + i_climb; per substep psi += turn, v = clamp(v
+   * + acc, [speed_min, speed_max]), position += (D(psi, v), climb) with D the heading lattice of
+   * step length v (units per substep).  n_acc = 1 with acc_units = {0} and speed_min = speed_max
+   * = 0 is the constant-speed model.  With acceleration actions n_climb must be 3 or 10; every
+   * request then runs alone on the whole GPU (action space tiled over the clusters, the tiles'
+   * top-2 exchanged per step); batches are sequential; co-simulation, departures and the
+   * multi-GPU entry points return FMDP_E_ARG. */
+  int32_t n_acc;                   /* <= 16                                              */
+  const int32_t* acc_units;        /* speed increments, units per substep per substep     */
+  double speed_min;                /* m/s; speed_min <= speed <= speed_max, multiples of  */
+  double speed_max;                /* u per dt                                            */
 } fmdp_airspace;
 
 /* Terrain: manually placed wells (Table PK) and a ground-height raster used only
@@ -302,6 +315,11 @@ fmdp_status fmdp_schedule_cosim(fmdp_ctx* ctx, const fmdp_request* reqs, int32_t
 /* Largest co-simulated batch the device can run (co-resident walkers). */
 int32_t fmdp_cosim_max(fmdp_ctx* ctx);
 
+/* Speed of every state of the last trajectory of request `index` (units per substep; the
+ * constant speed*dt/u without acceleration actions).  E_BUFFER (required size in *n) if cap is
+ * smaller than the trajectory. */
+fmdp_status fmdp_get_speeds(fmdp_ctx* ctx, int32_t index, int32_t* speed, int32_t cap, int32_t* n);
+
 /* Per-step log of the last trajectory of request `index` of the last schedule /
  * schedule_batch call: action a*_k, heading psi_k, and near-tie flag per step (k < n).
  * Any pointer may be NULL. */
@@ -339,6 +357,12 @@ fmdp_status fmdp_truncate(fmdp_ctx* ctx, uint32_t n_plans);
 fmdp_status fmdp_eval_step(fmdp_ctx* ctx, fmdp_qpos pos, int32_t heading, fmdp_qpos goal,
                            int64_t clock_step, double* vstar, double* v_at, double* scale_at,
                            int32_t* conflict, int64_t* min_d2, int32_t* a_star);
+
+/* The same from speed speed_u (units per substep; <= 0: the airspace's speed), for acceleration
+ * actions (airspace.n_acc; R32).  E_ARG if speed_u lies outside [speed_min, speed_max]. */
+fmdp_status fmdp_eval_step_v(fmdp_ctx* ctx, fmdp_qpos pos, int32_t heading, int32_t speed_u, fmdp_qpos goal,
+                             int64_t clock_step, double* vstar, double* v_at, double* scale_at, int32_t* conflict,
+                             int64_t* min_d2, int32_t* a_star);
 
 fmdp_status fmdp_get_stats(const fmdp_ctx* ctx, fmdp_stats* out);
 int32_t fmdp_num_actions(const fmdp_ctx* ctx);

@@ -8,7 +8,11 @@ namespace fmdp {
 
 constexpr int NTAU = 5;         // intruder wells per plan (Table PK: "5 rewards")
 constexpr int MAX_TURN = 32;
-constexpr int MAX_CLIMB = 5;
+constexpr int MAX_CLIMB = 10;
+constexpr int MAX_ACC = 16;     // speed increments of the acceleration actions
+constexpr int WIDE_G = 8;       // cluster size of the wide (action-tiled) walker
+constexpr int WIDE_HPT = 8;     // horizontal paths (turn, acceleration) per cluster tile
+constexpr int WB_WORDS = 12;    // words of one cluster's decision record (wide walker)
 constexpr int MAX_W = 16;
 constexpr int MAX_AW = 1024;    // projected states per step (A*W)
 constexpr int AMB_MAX = 64;     // ambiguous (state, tau) minima handled per step
@@ -58,6 +62,16 @@ struct World {
   const int32_t* height;        // [ny][nx] units
   const int2* dxy;              // heading lattice table [HL]
   const int2* proj;             // cumulative displacement [HL][n_turn][W]: sum_{s<=t} (DX,DY)[psi + s*turn]
+  // acceleration actions -> the wide walker (MODE 5).  The action
+  // space (turn, acceleration, climb) is tiled over the launch's clusters by horizontal path hp =
+  // i_turn * n_acc + i_acc: cluster c owns paths [c*hpt, c*hpt + hpt) and, like any walker, splits
+  // every time row over its CTAs; per step the clusters exchange their tile's top-2 (decision
+  // board).  In a wide World A = hpt * C and n_turn = hpt (one tile); A_all is the whole space.
+  int32_t wide;                 // 1: acceleration actions (MODE 5 launches only)
+  int32_t A_all, n_hp, hpt, n_turn_all, n_acc;
+  int32_t acc[MAX_ACC];         // speed increments, units per substep per substep
+  int32_t vmin, vmax, v0;       // speed bounds / departure speed, units per substep
+  const int2* spd;              // [vmax - vmin + 1][HL] displacement of one substep at (speed, heading)
 };
 
 struct Req {
@@ -68,6 +82,8 @@ struct Req {
   int64_t t0;
   int32_t slot;                 // output slot
   int32_t head;                 // 1: the earliest pending FCFS request (never paused; sets *stop when done)
+  int32_t speed0;               // departure speed, units per substep (0: the airspace's speed)
+  int32_t pad;
 };
 
 struct Out {
@@ -98,6 +114,10 @@ struct WalkArgs {
   int32_t shard_rank, shard_world;  // plan shard of this GPU; 0, 1 = whole rows
   int32_t xmode;                // 0 normal; 1 export per-(state,tau) minima + stay; 2 import and decide
   uint32_t* xbuf;               // [A*W*NTAU + 1] exchange buffer (float bits / stay d^2)
+  int32_t* speed;               // [slot][cap] speed of state k (wide walker)
+  unsigned long long* wb;       // wide walker decision board [2][clusters][WB_WORDS] LL words
+  unsigned long long wseq0;     // board tag base of this launch (host-tracked, monotonic)
+  int32_t* werr;                // board poll timeout flag
   double* dbg_vstar;            // [A]
   double* dbg_v;                // [A*W]
   double* dbg_s;                // [A*W]

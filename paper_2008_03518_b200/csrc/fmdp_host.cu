@@ -42,7 +42,13 @@ struct fmdp_ctx {
   std::vector<void*> allocs;
 
   fmdp_airspace air{};
-  std::vector<int32_t> turn, climb;
+  std::vector<int32_t> turn, climb, acc;
+  bool wide = false;                 // acceleration actions: the wide walker
+  int wide_k = 0;                    // clusters (action tiles) of one wide launch
+  int2* d_spd = nullptr;             // (speed, heading) displacement table
+  int32_t* d_speed = nullptr;        // [slot][cap] speed of state k
+  unsigned long long* d_wb = nullptr;  // decision board [2][k][WB_WORDS]
+  int32_t* d_wq = nullptr;           // [k] request queues of the clusters, then the board error flag
   std::vector<double> tau_s, tau_r;
   World w{};
   int A = 0, W = 0, C = 0;
@@ -260,6 +266,7 @@ fmdp_status ensure_slots(fmdp_ctx* ctx, int n) {
              {(void**)&ctx->d_traj, 12 * cap * m, nullptr},           {(void**)&ctx->d_heading, 4 * cap * m, nullptr},
              {(void**)&ctx->d_astar, 4 * cap * m, nullptr},           {(void**)&ctx->d_stepd2, 4 * cap * m, nullptr},
              {(void**)&ctx->d_ntie, cap * m, nullptr},                {(void**)&ctx->d_stepx, 4 * cap * m, nullptr},
+             {(void**)&ctx->d_speed, 4 * cap * m, nullptr},
              {(void**)&ctx->d_nstates, sizeof(int32_t) * m, nullptr}, {(void**)&ctx->d_t0s, sizeof(int64_t) * m, nullptr}};
     for (B& e : b) {
       e.p = dalloc(ctx, e.bytes);
@@ -297,7 +304,7 @@ fmdp_status ensure_up(fmdp_ctx* ctx, size_t words) {
 }
 
 int threads_for(const fmdp_ctx* ctx) {
-  const int tmax = ctx->C == 1 ? 512 : 384;  // kernel __launch_bounds__
+  const int tmax = ctx->C == 1 ? 512 : (ctx->C >= 10 ? 320 : 384);  // kernel __launch_bounds__
   return fmdp::walk_threads(ctx->w.n_turn * ctx->w.W, tmax);
 }
 
@@ -426,6 +433,9 @@ fmdp::WalkArgs make_args(fmdp_ctx* ctx, const std::vector<Req>& run, bool eval, 
   a.pairs = ctx->d_pairctr;
   a.prof = ctx->launch.profile ? ctx->d_prof : nullptr;
   a.stepx = ctx->d_stepx;
+  a.speed = ctx->d_speed;
+  a.wb = ctx->d_wb;
+  a.werr = ctx->d_wq ? ctx->d_wq + fmdp::XMAX * 4 : nullptr;
   a.vtrace = ctx->vtrace_n > 0 ? ctx->d_vtrace : nullptr;
   a.vtrace_n = ctx->vtrace_n;
   return a;
@@ -437,7 +447,18 @@ fmdp_status run_walk(fmdp_ctx* ctx, const std::vector<Req>& run, bool eval, int 
   if (run.empty()) return FMDP_OK;
   CK(cudaMemcpyAsync(ctx->d_reqs, run.data(), sizeof(Req) * run.size(), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemsetAsync(ctx->d_queue, 0, sizeof(int32_t), ctx->stream));
-  const fmdp::WalkArgs a = over ? *over : make_args(ctx, run, eval, budget);
+  fmdp::WalkArgs a = over ? *over : make_args(ctx, run, eval, budget);
+  if (ctx->wide) {
+    // wide walker: every cluster of the launch walks the same requests over its action
+    // tile (its own request queue), all co-resident; fresh decision board (tags restart at 1)
+    if (max_clusters(ctx, fmdp::WIDE_G) < ctx->wide_k)
+      return fail(ctx, FMDP_E_CAPACITY, "wide walker: the action tiles' clusters are not co-resident");
+    CK(cudaMemsetAsync(ctx->d_wq, 0, sizeof(int32_t) * (fmdp::XMAX * 4 + 4), ctx->stream));
+    CK(cudaMemsetAsync(ctx->d_wb, 0, sizeof(unsigned long long) * 2 * fmdp::WB_WORDS * ctx->wide_k, ctx->stream));
+    a.queue = ctx->d_wq;
+    G = fmdp::WIDE_G;
+    nc = ctx->wide_k;
+  }
   if (G == 0) choose_launch(ctx, (int)run.size(), &G, &nc);
   ctx->stats.cluster_size = G;
   ctx->stats.walkers = std::max(ctx->stats.walkers, nc);
@@ -451,6 +472,11 @@ fmdp_status run_walk(fmdp_ctx* ctx, const std::vector<Req>& run, bool eval, int 
   ctx->stats.device_ms += ms;
   ctx->stats.kernels += 1;
   if (std::getenv("FMDP_DEBUG")) std::fprintf(stderr, "fmdp: walk n=%zu G=%d clusters=%d %.3f ms\n", run.size(), G, nc, ms);
+  if (ctx->wide) {
+    int32_t e = 0;
+    CK(cudaMemcpy(&e, ctx->d_wq + fmdp::XMAX * 4, sizeof(e), cudaMemcpyDeviceToHost));
+    if (e) return fail(ctx, FMDP_E_CUDA, "wide walker: decision board timed out");
+  }
   return FMDP_OK;
 }
 
@@ -743,6 +769,7 @@ fmdp_status check_intra(fmdp_ctx* ctx) {
 
 // One request, alone on the device: a plain walk, or split over k clusters (bit-identical).
 fmdp_status run_single(fmdp_ctx* ctx, const Req& r) {
+  if (ctx->wide) return run_walk(ctx, {r}, false);
   int G = 16;
   const int k = split_for(ctx, &G);
   if (k <= 1) return run_walk(ctx, {r}, false);
@@ -776,7 +803,7 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
   CK(cudaMemcpyAsync(ctx->d_t0s, t0s.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, ctx->stream));
 
   int runs = 0;
-  if (flags & FMDP_BATCH_SEQUENTIAL) {
+  if ((flags & FMDP_BATCH_SEQUENTIAL) || ctx->wide) {  // wide walks take the whole GPU: in order
     for (int i = 0; i < n; ++i) {
       if ((st = run_single(ctx, base[i]))) return st;
       ++runs;
@@ -965,6 +992,11 @@ void fmdp_airspace_default(fmdp_airspace* a) {
   a->max_steps = 4000;
   a->vmax_init_zero = 0;
   a->valuation = 0;
+  static const int32_t accs[1] = {0};
+  a->n_acc = 1;
+  a->acc_units = accs;
+  a->speed_min = 0.0;
+  a->speed_max = 0.0;
   a->near_tie_rel = 1e-4;
   a->horizon_steps = 8192;
   a->row_capacity = 4096;
@@ -1002,10 +1034,16 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   if (a.n_turn < 1 || a.n_turn > fmdp::MAX_TURN || !a.turn_steps) return bad(FMDP_E_ARG, "turns");
   for (int i = 0; i < a.n_turn; ++i)
     if (std::abs(a.turn_steps[i]) >= a.heading_lattice) return bad(FMDP_E_ARG, "turn step beyond the lattice");
-  if (!(a.n_climb == 1 || a.n_climb == 3 || a.n_climb == 5) || !a.climb_units) return bad(FMDP_E_ARG, "climbs");
+  if (a.n_acc < 1 || a.n_acc > fmdp::MAX_ACC || !a.acc_units) return bad(FMDP_E_ARG, "n_acc / acc_units");
+  const bool wide = a.n_acc > 1 || a.acc_units[0] != 0 || a.speed_min > 0 || a.speed_max > 0;
+  if (!a.climb_units || (wide ? !(a.n_climb == 3 || a.n_climb == 10)
+                              : !(a.n_climb == 1 || a.n_climb == 3 || a.n_climb == 5)))
+    return bad(FMDP_E_ARG, wide ? "climbs: 3 or 10 with acceleration actions" : "climbs");
   if (a.n_tau < 1 || a.n_tau > fmdp::NTAU || !a.tau_s || !a.tau_radius_m) return bad(FMDP_E_ARG, "tau");
-  const int A = a.n_turn * a.n_climb;
-  if (A * a.window > fmdp::MAX_AW) return bad(FMDP_E_ARG, "A*W too large");
+  const int A = a.n_turn * a.n_acc * a.n_climb;
+  const int n_hp = a.n_turn * a.n_acc;                       // horizontal paths (turn, acceleration)
+  const int hpt = wide ? std::min(fmdp::WIDE_HPT, n_hp) : a.n_turn;  // paths per cluster tile
+  if ((wide ? hpt * a.n_climb : A) * a.window > fmdp::MAX_AW) return bad(FMDP_E_ARG, "A*W too large");
   int64_t step_u;
   if (!integral(a.speed * a.dt / a.u_m, &step_u) || step_u <= 0 || step_u > 1000) return bad(FMDP_E_ARG, "speed");
   for (int i = 0; i < a.n_climb; ++i)
@@ -1030,6 +1068,10 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   ctx->A = A;
   ctx->W = a.window;
   ctx->C = a.n_climb;
+  ctx->wide = wide;
+  ctx->acc.assign(a.acc_units, a.acc_units + a.n_acc);
+  ctx->air.acc_units = ctx->acc.data();
+  ctx->wide_k = wide ? (n_hp + hpt - 1) / hpt : 0;
   const double lo[3] = {a.lo.x, a.lo.y, a.lo.z}, hi[3] = {a.hi.x, a.hi.y, a.hi.z};
   for (int d = 0; d < 3; ++d) {
     ctx->lo_u[d] = std::llrint(lo[d] / a.u_m);
@@ -1074,9 +1116,16 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
 
   World& w = ctx->w;
   std::memset(&w, 0, sizeof(w));
-  w.A = A;
+  w.A = wide ? hpt * a.n_climb : A;  // wide: one cluster tile
   w.W = a.window;
-  w.n_turn = a.n_turn;
+  w.n_turn = hpt;  // = n_turn without acceleration actions (one tile = every path)
+  w.n_turn_all = a.n_turn;
+  w.wide = wide ? 1 : 0;
+  w.A_all = A;
+  w.n_hp = n_hp;
+  w.hpt = hpt;
+  w.n_acc = a.n_acc;
+  for (int i = 0; i < a.n_acc; ++i) w.acc[i] = a.acc_units[i];
   w.n_climb = a.n_climb;
   w.HL = a.heading_lattice;
   for (int i = 0; i < a.n_turn; ++i) w.turn[i] = a.turn_steps[i];
@@ -1126,6 +1175,28 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   build_lattice(w.HL, step_u, lat);
   double maxd = 0;
   for (const int2& d : lat) maxd = std::max(maxd, std::sqrt((double)d.x * d.x + (double)d.y * d.y));
+  // acceleration actions (R32): speeds [vmin, vmax] units per substep; D(psi, v) = the lattice of
+  // step length v -- one table row per speed (at v = v0 the constant-speed lattice)
+  std::vector<int2> spd;
+  w.v0 = (int32_t)step_u;
+  w.vmin = w.vmax = (int32_t)step_u;
+  if (wide) {
+    int64_t vmin = step_u, vmax = step_u;
+    if (a.speed_min > 0 || a.speed_max > 0) {
+      if (!integral(a.speed_min * a.dt / a.u_m, &vmin) || !integral(a.speed_max * a.dt / a.u_m, &vmax) || vmin < 1 ||
+          vmin > step_u || step_u > vmax || vmax > 1000)
+        return bad(FMDP_E_ARG, "speed_min <= speed <= speed_max, multiples of u per dt, <= 1000 units per substep");
+    }
+    w.vmin = (int32_t)vmin;
+    w.vmax = (int32_t)vmax;
+    spd.resize((size_t)(vmax - vmin + 1) * w.HL);
+    std::vector<int2> row;
+    for (int64_t sp = vmin; sp <= vmax; ++sp) {
+      build_lattice(w.HL, sp, row);
+      std::copy(row.begin(), row.end(), spd.begin() + (size_t)(sp - vmin) * w.HL);
+      for (const int2& d : row) maxd = std::max(maxd, std::sqrt((double)d.x * d.x + (double)d.y * d.y));
+    }
+  }
   int maxc = 0;
   for (int c : ctx->climb) maxc = std::max(maxc, std::abs(c));
   w.reach_u = (int32_t)(a.window * ((int64_t)std::ceil(maxd) + maxc) + 1);
@@ -1153,7 +1224,9 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
         }
       }
     }
-    const double S = std::sqrt((double)s2max) + (double)a.window * maxc + 1.0;
+    double S = std::sqrt((double)s2max) + (double)a.window * maxc + 1.0;
+    if (wide)  // any speed profile: |s - o| <= |s - q| + |o - q| <= W max|D| + (W/2) |D(., v0)|
+      S = (double)a.window * (std::ceil(maxd) + maxc) + (double)(a.window / 2) * (double)(step_u + 1) + 1.0;
     ctx->fan_radius_u = S;
     for (int i = 0; i < a.n_tau; ++i) {
       const double R = std::sqrt((double)w.R2_tau[i]);
@@ -1187,7 +1260,7 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   ctx->d_rows = (int32_t*)dalloc(ctx, sizeof(int32_t) * row_words * (size_t)w.horizon);
   ctx->d_counts = (int32_t*)dalloc(ctx, sizeof(int32_t) * (size_t)w.horizon);
   ctx->d_dxy = (int2*)dalloc(ctx, sizeof(int2) * w.HL);
-  const size_t nproj = (size_t)w.HL * a.n_turn * a.window;
+  const size_t nproj = (size_t)w.HL * w.n_turn * a.window;  // (wide walkers use d_spd instead)
   ctx->d_proj = (int2*)dalloc(ctx, sizeof(int2) * nproj);
   ctx->d_queue = (int32_t*)dalloc(ctx, sizeof(int32_t) * 4);
   ctx->d_stop = ctx->d_queue ? ctx->d_queue + 2 : nullptr;
@@ -1209,7 +1282,7 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   {  // Alg 3 projection offsets of every (heading, turn, substep): integer sums of lattice steps
     std::vector<int2> proj(nproj);
     for (int psi = 0; psi < w.HL; ++psi)
-      for (int it = 0; it < a.n_turn; ++it) {
+      for (int it = 0; it < (wide ? 0 : a.n_turn); ++it) {
         int x = 0, y = 0, ps = psi;
         for (int t = 1; t <= a.window; ++t) {
           ps = ((ps + a.turn_steps[it]) % w.HL + w.HL) % w.HL;
@@ -1221,6 +1294,15 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
     cudaMemcpy(ctx->d_proj, proj.data(), sizeof(int2) * nproj, cudaMemcpyHostToDevice);
   }
   w.proj = ctx->d_proj;
+  if (wide) {  // (speed, heading) table; decision board and per-cluster queues of the wide walker
+    ctx->d_spd = (int2*)dalloc(ctx, sizeof(int2) * spd.size());
+    ctx->d_wb = (unsigned long long*)dalloc(ctx, sizeof(unsigned long long) * 2 * fmdp::WB_WORDS * ctx->wide_k);
+    ctx->d_wq = (int32_t*)dalloc(ctx, sizeof(int32_t) * (fmdp::XMAX * 4 + 4));
+    if (!ctx->d_spd || !ctx->d_wb || !ctx->d_wq || ctx->wide_k > fmdp::XMAX * 4)
+      return bad(FMDP_E_NOMEM, "device allocation failed (wide walker)");
+    cudaMemcpy(ctx->d_spd, spd.data(), sizeof(int2) * spd.size(), cudaMemcpyHostToDevice);
+    w.spd = ctx->d_spd;
+  }
   ctx->counts.assign((size_t)w.horizon, 0);
   w.rows = ctx->d_rows;
   w.counts = ctx->d_counts;
@@ -1260,7 +1342,8 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
     w.height = ctx->d_height;
   }
   ctx->cap_states = a.max_steps + 2;
-  if (threads_for(ctx) > (ctx->C == 1 ? 512 : 384) || fmdp::walk_smem_bytes(w, ctx->C, threads_for(ctx), kChunk, kChunk, 16) > 227 * 1024)
+  if (threads_for(ctx) > (ctx->C == 1 ? 512 : (ctx->C >= 10 ? 320 : 384)) ||
+      fmdp::walk_smem_bytes(w, ctx->C, threads_for(ctx), kChunk, kChunk, wide ? fmdp::WIDE_G : 16) > 227 * 1024)
     return bad(FMDP_E_ARG, "action lattice too large for one CTA (threads / shared memory)");
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return bad(FMDP_E_CUDA, cudaGetErrorString(e));
@@ -1418,6 +1501,7 @@ fmdp_status finish_single(fmdp_ctx* ctx, const std::vector<Req>& base, uint64_t 
 fmdp_status fmdp_schedule_sharded(fmdp_ctx* ctx, const fmdp_shard* shard, uint64_t aircraft_id, fmdp_vec3 src,
                                   fmdp_vec3 dst, int64_t t0_step, fmdp_result* res, fmdp_qpos* traj,
                                   int32_t traj_cap) {
+  if (ctx && ctx->wide) return fail(ctx, FMDP_E_ARG, "not available with acceleration actions (wide walker)");
   if (!ctx || !shard || !res || !shard->allreduce_min_u32 || shard->world < 1 || shard->rank < 0 ||
       shard->rank >= shard->world)
     return fail(ctx, FMDP_E_ARG, "invalid shard description");
@@ -1473,6 +1557,7 @@ fmdp_status fmdp_schedule_sharded(fmdp_ctx* ctx, const fmdp_shard* shard, uint64
 
 // ----------------------------------------------------------------------------- in-kernel exchange
 fmdp_status fmdp_p2p_export(fmdp_ctx* ctx, int32_t world, fmdp_p2p_handle* handle, void** dev_ptr) {
+  if (ctx && ctx->wide) return fail(ctx, FMDP_E_ARG, "not available with acceleration actions (wide walker)");
   if (!ctx || !handle || world < 1 || world > fmdp::XNODE) return fail(ctx, FMDP_E_ARG, "world must be 1..8");
   DevGuard dev_guard(ctx->device);  // the context's device for this call, the caller's restored after
   CK(cudaStreamSynchronize(ctx->stream));
@@ -1569,6 +1654,7 @@ fmdp_status fmdp_p2p_connect(fmdp_ctx* ctx, int32_t rank, int32_t world, const f
 
 fmdp_status fmdp_schedule_p2p(fmdp_ctx* ctx, uint64_t aircraft_id, fmdp_vec3 src, fmdp_vec3 dst, int64_t t0_step,
                               fmdp_result* res, fmdp_qpos* traj, int32_t traj_cap) {
+  if (ctx && ctx->wide) return fail(ctx, FMDP_E_ARG, "not available with acceleration actions (wide walker)");
   if (!ctx || !res) return fail(ctx, FMDP_E_ARG, "null argument");
   if (ctx->x_me < 0) return fail(ctx, FMDP_E_ARG, "fmdp_p2p_connect first");
   if (traj && traj_cap < ctx->w.max_steps + 1) return fail(ctx, FMDP_E_BUFFER, "traj_cap must be >= max_steps + 1");
@@ -1674,6 +1760,7 @@ int cosim_cluster_size(fmdp_ctx* ctx, int n) {
 fmdp_status fmdp_schedule_departures(fmdp_ctx* ctx, uint64_t aircraft_id, fmdp_vec3 src, fmdp_vec3 dst,
                                      int64_t t0_step, int32_t n_delays, const int64_t* delays, fmdp_result* res,
                                      fmdp_qpos* traj, int32_t traj_cap, int32_t* chosen) {
+  if (ctx && ctx->wide) return fail(ctx, FMDP_E_ARG, "not available with acceleration actions (wide walker)");
   if (!ctx || n_delays < 1 || !delays || !res || !chosen) return fail(ctx, FMDP_E_ARG, "null argument");
   DevGuard dev_guard(ctx->device);  // the context's device for this call, the caller's restored after
   if (traj && traj_cap < ctx->w.max_steps + 1) return fail(ctx, FMDP_E_BUFFER, "traj_cap must be >= max_steps + 1");
@@ -1726,6 +1813,7 @@ fmdp_status fmdp_schedule_departures(fmdp_ctx* ctx, uint64_t aircraft_id, fmdp_v
 }
 
 int32_t fmdp_cosim_max(fmdp_ctx* ctx) {
+  if (ctx && ctx->wide) return 0;
   if (!ctx) return 0;
   DevGuard dev_guard(ctx->device);  // occupancy queries use the current device
   int m = 0;
@@ -1736,6 +1824,7 @@ int32_t fmdp_cosim_max(fmdp_ctx* ctx) {
 
 fmdp_status fmdp_schedule_cosim(fmdp_ctx* ctx, const fmdp_request* reqs, int32_t n, fmdp_result* res, fmdp_qpos* traj,
                                 int32_t traj_cap_each) {
+  if (ctx && ctx->wide) return fail(ctx, FMDP_E_ARG, "not available with acceleration actions (wide walker)");
   if (!ctx || n < 1 || !reqs || !res) return fail(ctx, FMDP_E_ARG, "null argument");
   DevGuard dev_guard(ctx->device);  // the context's device for this call, the caller's restored after
   if (traj && traj_cap_each < ctx->w.max_steps + 1) return fail(ctx, FMDP_E_BUFFER, "traj_cap must be >= max_steps + 1");
@@ -1855,6 +1944,21 @@ fmdp_status fmdp_get_trace(fmdp_ctx* ctx, int32_t index, double* vstar, double* 
   return FMDP_OK;
 }
 
+fmdp_status fmdp_get_speeds(fmdp_ctx* ctx, int32_t index, int32_t* speed, int32_t cap, int32_t* n) {
+  if (!ctx || index < 0 || index >= ctx->last_n) return fail(ctx, FMDP_E_ARG, "no such request in the last call");
+  DevGuard dev_guard(ctx->device);
+  const int ns = ctx->h_out[index].n_states;
+  if (n) *n = ns;
+  if (cap < ns) return FMDP_E_BUFFER;
+  if (!speed) return FMDP_OK;
+  if (!ctx->wide) {  // constant speed
+    for (int i = 0; i < ns; ++i) speed[i] = ctx->w.v0;
+    return FMDP_OK;
+  }
+  CK(cudaMemcpy(speed, ctx->d_speed + (size_t)index * ctx->cap_states, sizeof(int32_t) * ns, cudaMemcpyDeviceToHost));
+  return FMDP_OK;
+}
+
 fmdp_status fmdp_get_plan(fmdp_ctx* ctx, uint32_t plan_id, int64_t* t0_step, fmdp_qpos* buf, int32_t cap, int32_t* n) {
   if (!ctx || plan_id >= ctx->plans.size()) return fail(ctx, FMDP_E_ARG, "no such plan");
   const PlanRec& p = ctx->plans[plan_id];
@@ -1893,10 +1997,18 @@ fmdp_status fmdp_truncate(fmdp_ctx* ctx, uint32_t n_plans) {
 fmdp_status fmdp_eval_step(fmdp_ctx* ctx, fmdp_qpos pos, int32_t heading, fmdp_qpos goal, int64_t clock_step,
                            double* vstar, double* v_at, double* scale_at, int32_t* conflict, int64_t* min_d2,
                            int32_t* a_star) {
+  return fmdp_eval_step_v(ctx, pos, heading, 0, goal, clock_step, vstar, v_at, scale_at, conflict, min_d2, a_star);
+}
+
+fmdp_status fmdp_eval_step_v(fmdp_ctx* ctx, fmdp_qpos pos, int32_t heading, int32_t speed_u, fmdp_qpos goal,
+                             int64_t clock_step, double* vstar, double* v_at, double* scale_at, int32_t* conflict,
+                             int64_t* min_d2, int32_t* a_star) {
   if (!ctx || !vstar) return fail(ctx, FMDP_E_ARG, "null argument");
   DevGuard dev_guard(ctx->device);  // the context's device for this call, the caller's restored after
   if (clock_step < 0 || clock_step + 1 >= ctx->w.horizon) return fail(ctx, FMDP_E_RANGE, "clock outside horizon");
   if (heading < 0 || heading >= ctx->w.HL) return fail(ctx, FMDP_E_ARG, "heading outside the lattice");
+  if (speed_u > 0 && (speed_u < ctx->w.vmin || speed_u > ctx->w.vmax))
+    return fail(ctx, FMDP_E_ARG, "speed outside [speed_min, speed_max]");
   fmdp_status st = ensure_slots(ctx, 1);
   if (st) return st;
   Req r;
@@ -1904,6 +2016,7 @@ fmdp_status fmdp_eval_step(fmdp_ctx* ctx, fmdp_qpos pos, int32_t heading, fmdp_q
   r.src[0] = pos.x; r.src[1] = pos.y; r.src[2] = pos.z;
   r.dst[0] = goal.x; r.dst[1] = goal.y; r.dst[2] = goal.z;
   r.psi0 = heading;
+  r.speed0 = speed_u;
   r.t0 = clock_step;
   r.slot = 0;
   if ((st = run_walk(ctx, {r}, true))) return st;

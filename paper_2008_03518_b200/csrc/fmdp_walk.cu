@@ -557,8 +557,13 @@ __device__ __noinline__ void exact_fallback_call(float* s_M, const int32_t* s_am
 enum Phase { PH_PROJ, PH_FIX, PH_WAIT, PH_HOT, PH_STAGE, PH_SCATTER, PH_BAR1, PH_OWNER, PH_BAR2, PH_DECIDE,
              PH_TOP, PH_SCAN, PH_PLOOP, PH_BUILD, PH_OWN1, PH_ARGMAX, PH_FLAGS, PH_N };
 
+// Inverse of dkey.
+__device__ __forceinline__ double undkey(unsigned long long k) {
+  return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+
 template <int C, int MODE>
-__global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
+__global__ void __launch_bounds__(C == 1 ? 512 : (C >= 10 ? 320 : 384), 1)
     walk_kernel(const World w, const WalkArgs args, const int CH, const int RAWCAP, const int NGW) {
   cg::cluster_group cluster = cg::this_cluster();
   const unsigned rank = cluster.block_rank();
@@ -574,6 +579,20 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   const int col = warp * CPW + (lane % CPW), grp = lane / CPW;
   const int col_it = min(col / W, w.n_turn - 1), col_t = col % W + 1;  // this thread's column
   const int col_h = w.turn[col_it];
+  // wide walker (MODE 5, SURVEY f4 acceleration actions): this cluster's tile of horizontal paths
+  // hp = i_turn * n_acc + i_acc; the thread's path's turn and speed increment; local action a of
+  // the tile is global action hp0 * C + a (climb innermost)
+  constexpr bool WIDE = MODE == 5;
+  const int wcl = WIDE ? (int)(blockIdx.x / G) : 0;
+  const int hp0 = WIDE ? wcl * w.hpt : 0;
+  const int A_tile = WIDE ? min(w.hpt, w.n_hp - hp0) * C : w.A;
+  const int aoff = WIDE ? hp0 * C : 0;
+  int col_hw = col_h, col_acc = 0;
+  if (WIDE) {
+    const int hp = min(hp0 + col_it, w.n_hp - 1);
+    col_hw = w.turn[hp / w.n_acc];
+    col_acc = w.acc[hp % w.n_acc];
+  }
   // actions owned by this CTA (reduce-scatter target and epilogue): a = rank + oa*G
   const int n_own = (A > (int)rank) ? (A - (int)rank + (int)G - 1) / (int)G : 0;
 
@@ -619,7 +638,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   // their code on the step path costs 1.7 % full / 3.4 % culled on the configs[1] batch).
   constexpr bool XP = MODE == 2;
   const int xmode = XP ? 3 : (MODE == 3 ? args.xmode : 0);
-  const bool evalm = MODE == 3 && args.eval;
+  const bool evalm = (MODE == 3 || MODE == 5) && args.eval;
   // SURVEY f1 culling: MODE 4 is the culled FCFS walker, MODE 0 the full one (each carries only
   // its own build pass); the other instantiations decide at run time
   const bool cullm = MODE == 4 ? true : (MODE == 0 ? false : args.cull != 0);
@@ -628,7 +647,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   const int cosim = MODE == 1 ? 1 : 0;
   // x_intra: the launch's clusters are the ranks (one GPU, one request split over several
   // clusters); otherwise this launch is rank x_me of a multi-GPU exchange
-  const int xcl = (XP && args.x_intra) ? (int)(blockIdx.x / G) : 0;
+  const int xcl = (XP && args.x_intra) ? (int)(blockIdx.x / G) : wcl;
   const int xme = (XP && args.x_intra) ? xcl : args.x_me;
   // two-level exchange (x_inter): the clusters of this GPU first (xme / x_world, above), then
   // cluster xcl of every GPU (rank x_ime of x_iworld) over NVLink
@@ -692,7 +711,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
     }
     // walker state, identical in every thread of every CTA of the cluster
     int k = rq.start_k;
-    int qx, qy, qz, psi;
+    int qx, qy, qz, psi, v = rq.speed0 > 0 ? rq.speed0 : w.v0;  // v: speed, the wide walker's extra state
     if (k == 0) {
       qx = rq.src[0]; qy = rq.src[1]; qz = rq.src[2];
       psi = rq.psi0;
@@ -700,7 +719,9 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       const int32_t* tq = args.traj + 3 * (sbase + k);
       qx = tq[0]; qy = tq[1]; qz = tq[2];
       psi = args.heading[sbase + k];
+      if (WIDE) v = args.speed[sbase + k];
     }
+    unsigned wit = 0;  // wide walker: decision-board steps of this request (tags 1, 2, ...)
     // per-request aggregates, kept by thread 0 of rank 0
     int n_near = 0, steps_run = 0, status = 0, fail_step = -1, nex0 = 0;
     uint32_t min_sep = w.sat_d2;
@@ -725,6 +746,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         int32_t* tq = args.traj + 3 * sbase;
         tq[0] = rq.src[0]; tq[1] = rq.src[1]; tq[2] = rq.src[2];
         args.heading[sbase] = rq.psi0;
+        if (WIDE) args.speed[sbase] = w.v0;
         if (cosim)  // departure: level flight along the initial heading (R28)
           cs_publish(args, r, rq.t0, qx, qy, qz, CS_PRESENT, s_dxy[psi].x, s_dxy[psi].y, 0);
       }
@@ -798,10 +820,31 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         const int it = col_it, t = col_t, h = col_h;
         // cumulative lattice displacement of (psi, turn, t) from the host-built table (one L2 load
         // instead of t dependent lattice steps); final heading psi + t*h mod HL
-        const int2 cum = __ldg(&w.proj[((size_t)psi * w.n_turn + it) * W + (t - 1)]);
-        const int x = qx + cum.x, y = qy + cum.y;
-        int ps = (psi + t * h) % w.HL;
-        ps += ps < 0 ? w.HL : 0;
+        int x, y, ps;
+        if (WIDE) {  // R32: psi_s = psi + s h, v_s = clamp(v + s acc), q_t = q + sum_{s<=t} D(psi_s, v_s)
+          int xx = qx, yy = qy, pp = psi, sp = v;
+          for (int s2 = 1; s2 <= W; ++s2) {
+            const int pn = pp + col_hw;
+            const int pw2 = pn >= w.HL ? pn - w.HL : (pn < 0 ? pn + w.HL : pn);
+            const int sn = min(max(sp + col_acc, w.vmin), w.vmax);
+            if (s2 <= t) {
+              const int2 d = __ldg(&w.spd[(size_t)(sn - w.vmin) * w.HL + pw2]);
+              xx += d.x;
+              yy += d.y;
+              pp = pw2;
+              sp = sn;
+            }
+          }
+          x = xx;
+          y = yy;
+          ps = pp | (sp << 16);  // heading and speed of the state (s_pos .w)
+        } else {
+          const int2 cum = __ldg(&w.proj[((size_t)psi * w.n_turn + it) * W + (t - 1)]);
+          x = qx + cum.x;
+          y = qy + cum.y;
+          ps = (psi + t * h) % w.HL;
+          ps += ps < 0 ? w.HL : 0;
+        }
         // offsets from the fan origin o = q + (W/2) (DX, DY)[psi], doubled: the hot loop
         // evaluates |s - c|^2 - |s - o|^2 = Q + 2 (s - o).X with X = o - c, Q = |X|^2
         sx = (float)(2 * (x - qx - ox));
@@ -1290,8 +1333,8 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         const int n_hw = NT >> 4;
         for (int oa0 = 0; oa0 < NOWN; oa0 += n_hw) {  // uniform trip count across the CTA
           const int oa = oa0 + hw;
-          const bool act = oa < n_own && hl < W;
           const int a = (int)rank + oa * (int)G;
+          const bool act = oa < n_own && hl < W && a < A_tile;
           const int st = a * W + hl;
           float mi = FLT_MAX;
           if (act) {
@@ -1306,8 +1349,8 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
             v = s_fix[st] - neg;
             sc = s_sfix[st] + neg;
             if (evalm) {
-              args.dbg_v[st] = v;
-              args.dbg_s[st] = sc;
+              args.dbg_v[st + aoff * W] = v;
+              args.dbg_s[st + aoff * W] = sc;
             }
           }
           // V*(a) = max(init, max_t V), term scale at the first maximising t: half-warp shuffles
@@ -1327,11 +1370,11 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           if (oa < n_own && hl < (int)G) {  // push {V*(a), S(a)} to CTA hl
             const double vstar = (w.vmax_init_zero && !w.endpoint) ? fmax(0.0, bv) : bv;
             push_d2(solo, smem_u32(&s_vv[a]), hl, vstar, bs, smem_u32(&s_bar[5 + p]));
-            if (evalm && hl == 0) args.dbg_vstar[a] = vstar;
+            if (evalm && hl == 0 && a < A_tile) args.dbg_vstar[a + aoff] = vstar;
             // parity trace of the walk itself (fmdp_set_trace): {V*(a), S(a)} of every step of
             // the first vtrace_n requests, in whichever instantiation runs them
-            if (args.vtrace && hl == 0 && lead && !evalm && rq.slot < args.vtrace_n)
-              args.vtrace[((size_t)rq.slot * args.cap + k) * A + a] = make_double2(vstar, bs);
+            if (args.vtrace && hl == 0 && !evalm && rq.slot < args.vtrace_n && (WIDE ? a < A_tile : lead))
+              args.vtrace[((size_t)rq.slot * args.cap + k) * (WIDE ? w.A_all : A) + a + aoff] = make_double2(vstar, bs);
           }
         }
         if (tid == 0 && ctl->n_exact && rank != 0) {
@@ -1351,7 +1394,85 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       double v1 = -INFINITY;
       int a1 = INT_MAX;
       bool near = false;
-      if (!fin && A <= 32) {
+      int4 nxt = make_int4(0, 0, 0, 0);  // wide walker: Delta_1(a*) (x, y, z, psi | v << 16)
+      int nfl = 0;                       //              and its terrain / goal flags
+      if (WIDE && !fin) {
+        // a7 over the whole action space, tiled over the clusters: every CTA takes its tile's
+        // top-2 (lanes hold a = lane, lane+32, ...); CTA 0 of each cluster publishes {key1, global
+        // a1, S(a1), key2, Delta_1(a1), flags} on the decision board (tagged 8-byte words); every
+        // warp reads every cluster's record and takes the global argmax (lowest global index on
+        // ties: tiles are contiguous index ranges) and the global runner-up for the near-tie
+        double lb1 = -INFINITY, lb2 = -INFINITY;
+        int li1 = INT_MAX, li2 = INT_MAX;
+        for (int a = lane; a < A_tile; a += 32) {
+          const double vv = s_vv[a].x;
+          if (better(vv, a, lb1, li1)) {
+            lb2 = lb1; li2 = li1; lb1 = vv; li1 = a;
+          } else if (better(vv, a, lb2, li2)) {
+            lb2 = vv; li2 = a;
+          }
+        }
+        const int w1 = argmax_key(0xffffffffu, li1 != INT_MAX, dkey(lb1 + 0.0), (unsigned)li1);
+        const int ta1 = __shfl_sync(0xffffffffu, li1, w1);
+        const bool own = lane == w1;
+        const double cv = own ? lb2 : lb1;
+        const int ci = own ? li2 : li1;
+        const int w2 = argmax_key(0xffffffffu, ci != INT_MAX, dkey(cv + 0.0), (unsigned)ci);
+        const double tv2 = w2 >= 0 ? __shfl_sync(0xffffffffu, cv, w2) : -INFINITY;
+        const int nclu = (int)(gridDim.x / G);
+        ++wit;
+        const int wpar = (int)(wit & 1u);
+        if (rank == 0 && warp == 0 && lane < WB_WORDS) {
+          const unsigned long long k1 = dkey(s_vv[ta1].x + 0.0), k2 = dkey(tv2 + 0.0);
+          const unsigned long long sb = (unsigned long long)__double_as_longlong(s_vv[ta1].y);
+          const int4 d1 = s_pos[ta1 * W];
+          uint32_t val = 0;
+          switch (lane) {
+            case 0: val = (uint32_t)(k1 >> 32); break;
+            case 1: val = (uint32_t)k1; break;
+            case 2: val = (uint32_t)(ta1 + aoff); break;
+            case 3: val = (uint32_t)(sb >> 32); break;
+            case 4: val = (uint32_t)sb; break;
+            case 5: val = (uint32_t)(k2 >> 32); break;
+            case 6: val = (uint32_t)k2; break;
+            case 7: val = (uint32_t)d1.x; break;
+            case 8: val = (uint32_t)d1.y; break;
+            case 9: val = (uint32_t)d1.z; break;
+            case 10: val = (uint32_t)d1.w; break;
+            default: val = (uint32_t)s_flags[ta1]; break;
+          }
+          st_ll(args.wb + ((size_t)wpar * nclu + wcl) * WB_WORDS + lane, val, wit);
+        }
+        // every warp: lane c reads cluster c's record (all loads first, polls after)
+        uint32_t rec[WB_WORDS];
+        const unsigned long long* rb = args.wb + ((size_t)wpar * nclu + lane) * WB_WORDS;
+        const long long bud = (4ll << 30);
+#pragma unroll
+        for (int j = 0; j < WB_WORDS; ++j) {
+          rec[j] = 0;
+          if (lane < nclu) rec[j] = ld_ll(rb + j, wit, args.werr, bud);
+        }
+        const bool okc = lane < nclu;
+        const unsigned long long gk1 = ((unsigned long long)rec[0] << 32) | rec[1];
+        const int wl = argmax_key(0xffffffffu, okc, gk1, rec[2]);
+        a1 = (int)__shfl_sync(0xffffffffu, rec[2], wl);
+        const unsigned long long wk1 = __shfl_sync(0xffffffffu, gk1, wl);
+        v1 = undkey(wk1);
+        const unsigned long long sbits = ((unsigned long long)__shfl_sync(0xffffffffu, rec[3], wl) << 32) |
+                                         __shfl_sync(0xffffffffu, rec[4], wl);
+        const double thr = w.near_tie_rel * __longlong_as_double((long long)sbits);
+        // runner-up: every other cluster's best, and the winner cluster's second
+        const unsigned long long gk2 = ((unsigned long long)rec[5] << 32) | rec[6];
+        const unsigned long long ck = lane == wl ? gk2 : gk1;
+        const unsigned chi = okc ? (unsigned)(ck >> 32) : 0u;
+        const unsigned mhi = __reduce_max_sync(0xffffffffu, chi);
+        const unsigned mlo = __reduce_max_sync(0xffffffffu, (okc && chi == mhi) ? (unsigned)ck : 0u);
+        const unsigned long long k2max = ((unsigned long long)mhi << 32) | mlo;
+        near = nclu * (int)A_tile > 1 && k2max != 0ull && v1 - undkey(k2max) < thr;
+        nxt = make_int4((int)__shfl_sync(0xffffffffu, rec[7], wl), (int)__shfl_sync(0xffffffffu, rec[8], wl),
+                        (int)__shfl_sync(0xffffffffu, rec[9], wl), (int)__shfl_sync(0xffffffffu, rec[10], wl));
+        nfl = (int)__shfl_sync(0xffffffffu, rec[11], wl);
+      } else if (!fin && A <= 32) {
         // a7 (Alg 9; ties -> lowest index, R13): lane a holds V*(a); REDUX max over
         // order-preserving keys, lowest index among equal keys; near-tie (north star: top-2 gap
         // < near_tie_rel * S) <=> some other action is within the threshold of the winner
@@ -1393,8 +1514,8 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         status = -1;
         done = true;
       } else if (evalm) {
-        if (rank == 0 && tid == 0) {
-          args.dbg_conf[A] = c0;
+        if (lead && rank == 0 && tid == 0) {
+          args.dbg_conf[WIDE ? w.A_all : A] = c0;
           args.dbg_astar[0] = a1;
         }
         done = true;
@@ -1412,20 +1533,23 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           fail_step = st == 0 ? -1 : k;
           done = true;
         } else {
-          const int4 p1 = s_pos[a1 * W + 0];  // s_{t+1} <- Delta_1[a*] (Alg 1)
+          const int4 p1 = WIDE ? nxt : s_pos[a1 * W + 0];  // s_{t+1} <- Delta_1[a*] (Alg 1)
+          const int npsi = WIDE ? (p1.w & 0xffff) : p1.w;
           if (lead && rank == 0 && tid == 0) {
             args.astar[sbase + k] = a1;
             args.ntie[sbase + k] = near ? 1 : 0;
             int32_t* tq = args.traj + 3 * (sbase + k + 1);
             tq[0] = p1.x; tq[1] = p1.y; tq[2] = p1.z;
-            args.heading[sbase + k + 1] = p1.w;
+            args.heading[sbase + k + 1] = npsi;
+            if (WIDE) args.speed[sbase + k + 1] = p1.w >> 16;
           }
           n_near += near ? 1 : 0;
           steps_run += 1;
           k += 1;
           qx = p1.x; qy = p1.y; qz = p1.z;
-          psi = p1.w;
-          fl = s_flags[a1];
+          psi = npsi;
+          if (WIDE) v = p1.w >> 16;
+          fl = WIDE ? nfl : s_flags[a1];
           fin = fl != 0 || k >= w.max_steps;
           // slice budget spent: pause at state k (the head never pauses; with a stop flag the
           // others keep going until the head has finished -- free work in a single-wave slice)
@@ -1447,6 +1571,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
     if (evalm && rank == 0) {
       __syncthreads();
       for (int a = tid; a < A; a += NT) s_conf[a] = w.sat_d2;
+      const int A = A_tile;  // (the tile's real actions; global index a + aoff)
       __syncthreads();
       const int4* s_pos = s_pos2 + (k & 1) * AW;
       const int64_t K1 = rq.t0 + 1;
@@ -1460,7 +1585,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         if (d < w.sat_d2) atomicMin(&s_conf[a], d);
       }
       __syncthreads();
-      for (int a = tid; a < A; a += NT) args.dbg_conf[a] = s_conf[a];
+      for (int a = tid; a < A; a += NT) args.dbg_conf[a + aoff] = s_conf[a];
     }
 
     // ------------------------------------------------------------ request epilogue
@@ -1644,7 +1769,7 @@ static cudaError_t max_clusters_t(const World& w, int cluster, int threads, int 
 
 cudaError_t launch_walk(const World& w, const WalkArgs& a, int n_climb, int cluster, int n_clusters, int threads,
                         int chunk, int rawcap, cudaStream_t s) {
-  const int mode = a.cosim ? 1 : (a.xmode == 3 ? 2 : ((a.xmode || a.eval || a.prof) ? 3 : (a.cull ? 4 : 0)));
+  const int mode = w.wide ? 5 : (a.cosim ? 1 : (a.xmode == 3 ? 2 : ((a.xmode || a.eval || a.prof) ? 3 : (a.cull ? 4 : 0))));
 #define FMDP_LW(c, m) launch_walk_t<c, m>(w, a, cluster, n_clusters, threads, chunk, rawcap, s)
   switch (n_climb * 8 + mode) {
     case 8: return FMDP_LW(1, 0);
@@ -1662,6 +1787,8 @@ cudaError_t launch_walk(const World& w, const WalkArgs& a, int n_climb, int clus
     case 42: return FMDP_LW(5, 2);
     case 43: return FMDP_LW(5, 3);
     case 44: return FMDP_LW(5, 4);
+    case 29: return FMDP_LW(3, 5);    // wide walker (acceleration actions)
+    case 85: return FMDP_LW(10, 5);   // A = 15 x 9 x 10 = 1350
     default: return cudaErrorInvalidValue;
   }
 #undef FMDP_LW
@@ -1669,6 +1796,13 @@ cudaError_t launch_walk(const World& w, const WalkArgs& a, int n_climb, int clus
 
 cudaError_t walk_max_clusters(const World& w, int n_climb, int cluster, int threads, int chunk, int rawcap, int* out,
                               bool cosim) {
+  if (w.wide) {
+    switch (n_climb) {
+      case 3: return max_clusters_t<3, 5>(w, cluster, threads, chunk, rawcap, out);
+      case 10: return max_clusters_t<10, 5>(w, cluster, threads, chunk, rawcap, out);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (n_climb) {
     case 1: return cosim ? max_clusters_t<1, 1>(w, cluster, threads, chunk, rawcap, out)
                          : max_clusters_t<1, 0>(w, cluster, threads, chunk, rawcap, out);

@@ -16,7 +16,7 @@ import numpy as np
 
 from .build import LIB
 
-ABI_VERSION = 2  # include/fmdp.h FMDP_ABI_VERSION
+ABI_VERSION = 3  # include/fmdp.h FMDP_ABI_VERSION
 ACCEPTED, REJ_CONFLICT, REJ_TERRAIN, REJ_TIMEOUT = 0, 1, 2, 3
 STATUS_NAMES = {0: "ACCEPTED", 1: "REJ_CONFLICT", 2: "REJ_TERRAIN", 3: "REJ_TIMEOUT"}
 BATCH_SEQUENTIAL = 1
@@ -46,6 +46,8 @@ class Airspace(C.Structure):
         ("capture_radius_m", C.c_double), ("sep_min_m", C.c_double),
         ("max_steps", C.c_int32), ("vmax_init_zero", C.c_int32), ("near_tie_rel", C.c_double),
         ("horizon_steps", C.c_int64), ("row_capacity", C.c_int32), ("valuation", C.c_int32),
+        ("n_acc", C.c_int32), ("acc_units", C.POINTER(C.c_int32)), ("speed_min", C.c_double),
+        ("speed_max", C.c_double),
     ]
 
 
@@ -104,7 +106,8 @@ EXPORTS = ["fmdp_airspace_default", "fmdp_create", "fmdp_destroy", "fmdp_set_lau
            "fmdp_p2p_export", "fmdp_p2p_connect", "fmdp_schedule_p2p",
            "fmdp_schedule_departures", "fmdp_schedule_cosim", "fmdp_cosim_max", "fmdp_get_steplog", "fmdp_get_plan",
            "fmdp_num_plans", "fmdp_truncate", "fmdp_eval_step", "fmdp_get_stats", "fmdp_num_actions",
-           "fmdp_strerror", "fmdp_last_error", "fmdp_set_trace", "fmdp_get_trace"]
+           "fmdp_strerror", "fmdp_last_error", "fmdp_set_trace", "fmdp_get_trace", "fmdp_get_speeds",
+           "fmdp_eval_step_v"]
 
 _lib = None
 
@@ -138,11 +141,13 @@ def lib():
         L.fmdp_schedule_p2p.argtypes = [vp, C.c_uint64, Vec3, Vec3, i64, C.POINTER(Result), vp, i32]
         L.fmdp_get_steplog.argtypes = [vp, i32, vp, vp, vp, i32, C.POINTER(i32)]
         L.fmdp_set_trace.argtypes = [vp, i32]
+        L.fmdp_get_speeds.argtypes = [vp, i32, vp, i32, C.POINTER(i32)]
         L.fmdp_get_trace.argtypes = [vp, i32, vp, vp, i32, C.POINTER(i32)]
         L.fmdp_get_plan.argtypes = [vp, C.c_uint32, C.POINTER(i64), vp, i32, C.POINTER(i32)]
         L.fmdp_num_plans.argtypes = [vp, C.POINTER(C.c_uint32)]
         L.fmdp_truncate.argtypes = [vp, C.c_uint32]
         L.fmdp_eval_step.argtypes = [vp, QPos, i32, QPos, i64, vp, vp, vp, vp, vp, vp]
+        L.fmdp_eval_step_v.argtypes = [vp, QPos, i32, i32, QPos, i64, vp, vp, vp, vp, vp, vp]
         L.fmdp_get_stats.argtypes = [vp, C.POINTER(Stats)]
         L.fmdp_num_actions.argtypes = [vp]
         L.fmdp_num_actions.restype = i32
@@ -186,8 +191,9 @@ class FMDP:
         arr_i = lambda v: np.ascontiguousarray(v, np.int32)
         arr_d = lambda v: np.ascontiguousarray(v, np.float64)
         turn, climb = arr_i(airspace.turn_steps), arr_i(airspace.climb_units)
+        acc = arr_i(getattr(airspace, "acc_units", (0,)))
         tau, rad = arr_d(airspace.tau_s), arr_d(airspace.tau_radius_m)
-        self._keep += [turn, climb, tau, rad]
+        self._keep += [turn, climb, tau, rad, acc]
         a.abi_version = ABI_VERSION
         a.lo = Vec3(*airspace.lo_m)
         a.hi = Vec3(*airspace.hi_m)
@@ -206,6 +212,9 @@ class FMDP:
         a.max_steps, a.vmax_init_zero, a.near_tie_rel = airspace.max_steps, airspace.vmax_init_zero, airspace.near_tie_rel
         a.horizon_steps, a.row_capacity = airspace.horizon_steps, airspace.row_capacity
         a.valuation = getattr(airspace, "valuation", 0)
+        a.n_acc, a.acc_units = len(acc), acc.ctypes.data_as(C.POINTER(C.c_int32))
+        a.speed_min = float(getattr(airspace, "speed_min_mps", 0.0))
+        a.speed_max = float(getattr(airspace, "speed_max_mps", 0.0))
         self.max_steps = int(airspace.max_steps)
         self.W = int(airspace.W)
         t = Terrain()
@@ -452,6 +461,14 @@ class FMDP:
         k = n.value
         return ast[:max(k - 1, 0)].copy(), hd[:k].copy(), nt[:max(k - 1, 0)].copy()
 
+    def speeds(self, index: int):
+        """Speed of every state (units per substep) of request `index` of the last call."""
+        n = C.c_int32()
+        cap = self.max_steps + 2
+        sp = np.zeros(cap, np.int32)
+        self._check(self.L.fmdp_get_speeds(self.ctx, int(index), _p(sp), cap, C.byref(n)), "fmdp_get_speeds")
+        return sp[:n.value].copy()
+
     def set_trace(self, n_requests: int):
         """Record V*(a), S(a) of every decision step of the first n_requests of later calls."""
         self._check(self.L.fmdp_set_trace(self.ctx, int(n_requests)), "fmdp_set_trace")
@@ -466,7 +483,8 @@ class FMDP:
         k = n.value
         return vs[:k * self.A].reshape(k, self.A), sc[:k * self.A].reshape(k, self.A)
 
-    def eval_step(self, q, psi: int, goal, K: int):
+    def eval_step(self, q, psi: int, goal, K: int, speed: int = 0):
+        """One decision step (debug / parity hook); speed in units per substep (0: the airspace's)."""
         A, W = self.A, self.W
         vstar = np.zeros(A, np.float64)
         v = np.zeros(A * W, np.float64)
@@ -474,8 +492,9 @@ class FMDP:
         conf = np.zeros(A, np.int32)
         md2 = np.zeros(A + 1, np.int64)
         a = C.c_int32()
-        self._check(self.L.fmdp_eval_step(self.ctx, QPos(*[int(x) for x in q]), int(psi), QPos(*[int(x) for x in goal]),
-                                          int(K), _p(vstar), _p(v), _p(s), _p(conf), _p(md2), C.byref(a)),
+        self._check(self.L.fmdp_eval_step_v(self.ctx, QPos(*[int(x) for x in q]), int(psi), int(speed),
+                                            QPos(*[int(x) for x in goal]), int(K), _p(vstar), _p(v), _p(s), _p(conf),
+                                            _p(md2), C.byref(a)),
                     "fmdp_eval_step")
         return dict(vstar=vstar, v=v.reshape(A, W), scale=s.reshape(A, W), conflict=conf, min_d2=md2, a_star=a.value)
 

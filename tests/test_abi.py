@@ -72,8 +72,9 @@ def test_abi_version_matches_the_header():
     body = hdr[hdr.index("typedef struct fmdp_airspace"):hdr.index("} fmdp_airspace;")]
     names = re.findall(r"^\s+(?:const\s+)?[\w\s\*]+?\b(\w+)(?:\[\d+\])?\s*[;,]", body, re.M)
     fields = [f for f, _ in fmdp.Airspace._fields_]
-    assert names[-1] == fields[-1] == "valuation"
-    assert len(fields) >= 30
+    assert names[-1] == fields[-1] == "speed_max"
+    assert "n_acc" in fields and "acc_units" in fields and fields[-4] == "n_acc"
+    assert len(fields) >= 34
 
 
 def test_pack_plans_layout():
