@@ -399,3 +399,78 @@ def airspace_f4(**kw) -> Airspace:
                 climb_units=tuple(range(-40, 33, 8)), speed_min_mps=30.0, speed_max_mps=60.0)
     base.update(kw)
     return Airspace(**base)
+
+
+class ReflectingLinesPacked:
+    """n reflecting-line plans (the reflecting_lines_fast recipe, every plan active over ``rows``)
+    drawn once, materialised on demand in packed chunks -- for stores too large to hold on the host
+    (configs[3] at 4000 rows: 4.8 GB of states; configs[4] at 3000 rows: 36 GB).
+    ``chunks(c)`` yields (t0[m], n[m], states[m * rows, 3]) in plan order (the fmdp_add_plans
+    layout); ``window(K0, K1)`` returns every plan restricted to rows [K0, K1) as (t0, states)
+    pairs -- the rows an oracle needs to evaluate steps at rows K0 .. K1 - 2 (R11 forward
+    differences)."""
+
+    def __init__(self, rng: np.random.Generator, n: int, lo_u, hi_u, rows: Tuple[int, int],
+                 speed_mps=(30.0, 60.0), vz_units=(-16, 16), z_lo_u=None, z_hi_u=None):
+        lo_u = np.asarray(lo_u, np.int64)
+        hi_u = np.asarray(hi_u, np.int64)
+        zlo = int(lo_u[2] if z_lo_u is None else z_lo_u)
+        zhi = int(hi_u[2] if z_hi_u is None else z_hi_u)
+        self.lo3 = np.array([lo_u[0], lo_u[1], zlo], np.int64)
+        self.hi3 = np.array([hi_u[0], hi_u[1], zhi], np.int64)
+        self.p0 = np.stack([rng.integers(self.lo3[d], self.hi3[d] + 1, size=n) for d in range(3)], axis=1)
+        sp = rng.uniform(*speed_mps, size=n) * 0.1 * U_PER_M
+        th = rng.uniform(0.0, 2.0 * np.pi, size=n)
+        self.v = np.stack([np.rint(sp * np.cos(th)), np.rint(sp * np.sin(th)),
+                           rng.integers(vz_units[0], vz_units[1] + 1, size=n)], axis=1).astype(np.int64)
+        self.n, self.rows = n, rows
+
+    def _states(self, a: int, b: int, k0: int, k1: int) -> np.ndarray:
+        K = np.arange(k0 - self.rows[0], k1 - self.rows[0], dtype=np.int64)[None, :, None]
+        L = (self.hi3 - self.lo3)[None, None, :]
+        raw = self.p0[a:b, None, :] + self.v[a:b, None, :] * K - self.lo3[None, None, :]
+        y = np.mod(raw, 2 * L)
+        y = np.where(y > L, 2 * L - y, y)
+        return (self.lo3[None, None, :] + y).astype(np.int32)
+
+    def chunks(self, chunk: int = 4096):
+        nk = self.rows[1] - self.rows[0]
+        for a in range(0, self.n, chunk):
+            b = min(self.n, a + chunk)
+            st = self._states(a, b, self.rows[0], self.rows[1]).reshape(-1, 3)
+            yield (np.full(b - a, self.rows[0], np.int64), np.full(b - a, nk, np.int32), st)
+
+    def window(self, K0: int, K1: int):
+        st = self._states(0, self.n, K0, K1)
+        return [(int(K0), st[j]) for j in range(self.n)]
+
+
+def config_c4_full(seed: int = 4, n_plans: int = 100_000, rows: int = 4000, n_requests: int = 10,
+                   n_buildings: int = 256):
+    """configs[3] at its defined size: 100k plans over 4000 rows (6.4 GB store), packed on demand
+    (returns the scenario without host plans, and the ReflectingLinesPacked generator).  Same
+    recipe and RNG stream as config_c4."""
+    rng = np.random.default_rng(seed)
+    a = Airspace(max_steps=min(4000, rows - 8), lo_m=(-50000.0, -50000.0, 0.0), hi_m=(50000.0, 50000.0, 1500.0),
+                 horizon_steps=rows + 8, row_capacity=((n_plans + n_requests + 64) + 3) // 4 * 4)
+    terrain = manhattan_terrain(rng, n_buildings, core_half_m=5000.0, raster_half_m=8000.0)
+    lo, hi = m2u(a.lo_m), m2u(a.hi_m)
+    gen = ReflectingLinesPacked(rng, n_plans, lo, hi, (0, rows), z_lo_u=int(m2u(60)), z_hi_u=int(m2u(1500)))
+    pads = vertiports(rng, 40, 5000.0, terrain)
+    src, dst, t0 = request_pairs(rng, pads, n_requests, 4500.0, 5500.0, (0, 1))
+    return Scenario(a, terrain, [], src, dst, t0, name="c4full"), gen
+
+
+def config_c5_full(seed: int = 5, n_plans: int = 1_000_000, rows: int = 3000, n_requests: int = 10):
+    """configs[4] at its defined size: 1M plans over 3000 rows (48 GB store), A = 85, packed on
+    demand.  Same recipe and RNG stream as config_c5."""
+    rng = np.random.default_rng(seed)
+    a = Airspace(max_steps=min(4000, rows - 8), lo_m=(-125000.0, -125000.0, 0.0), hi_m=(125000.0, 125000.0, 2350.0),
+                 horizon_steps=rows + 8, row_capacity=((n_plans + n_requests + 64) + 3) // 4 * 4,
+                 turn_steps=tuple(range(-8, 9)), climb_units=(-32, -16, 0, 16, 32))
+    terrain = manhattan_terrain(rng, 256, core_half_m=5000.0, raster_half_m=8000.0)
+    lo, hi = m2u(a.lo_m), m2u(a.hi_m)
+    gen = ReflectingLinesPacked(rng, n_plans, lo, hi, (0, rows), z_lo_u=int(m2u(60)), z_hi_u=int(m2u(2350)))
+    pads = vertiports(rng, 40, 5000.0, terrain)
+    src, dst, t0 = request_pairs(rng, pads, n_requests, 4500.0, 5500.0, (0, 1))
+    return Scenario(a, terrain, [], src, dst, t0, name="c5full"), gen

@@ -11,7 +11,8 @@ constexpr int MAX_TURN = 32;
 constexpr int MAX_CLIMB = 10;
 constexpr int MAX_ACC = 16;     // speed increments of the acceleration actions
 constexpr int WIDE_G = 8;       // cluster size of the wide (action-tiled) walker
-constexpr int WIDE_HPT = 8;     // horizontal paths (turn, acceleration) per cluster tile
+constexpr int WIDE_HPT = 9;     // horizontal paths (turn, acceleration) per cluster tile (135 / 9 = 15
+                                // clusters of 8 CTAs: co-resident on 148 SMs)
 constexpr int WB_WORDS = 12;    // words of one cluster's decision record (wide walker)
 constexpr int MAX_W = 16;
 constexpr int MAX_AW = 1024;    // projected states per step (A*W)

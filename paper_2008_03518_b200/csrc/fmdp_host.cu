@@ -304,7 +304,7 @@ fmdp_status ensure_up(fmdp_ctx* ctx, size_t words) {
 }
 
 int threads_for(const fmdp_ctx* ctx) {
-  const int tmax = ctx->C == 1 ? 512 : (ctx->C >= 10 ? 320 : 384);  // kernel __launch_bounds__
+  const int tmax = ctx->C == 1 ? 512 : 384;  // kernel __launch_bounds__
   return fmdp::walk_threads(ctx->w.n_turn * ctx->w.W, tmax);
 }
 
@@ -1342,7 +1342,7 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
     w.height = ctx->d_height;
   }
   ctx->cap_states = a.max_steps + 2;
-  if (threads_for(ctx) > (ctx->C == 1 ? 512 : (ctx->C >= 10 ? 320 : 384)) ||
+  if (threads_for(ctx) > (ctx->C == 1 ? 512 : 384) ||
       fmdp::walk_smem_bytes(w, ctx->C, threads_for(ctx), kChunk, kChunk, wide ? fmdp::WIDE_G : 16) > 227 * 1024)
     return bad(FMDP_E_ARG, "action lattice too large for one CTA (threads / shared memory)");
   cudaError_t e = cudaDeviceSynchronize();

@@ -563,7 +563,7 @@ __device__ __forceinline__ double undkey(unsigned long long k) {
 }
 
 template <int C, int MODE>
-__global__ void __launch_bounds__(C == 1 ? 512 : (C >= 10 ? 320 : 384), 1)
+__global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
     walk_kernel(const World w, const WalkArgs args, const int CH, const int RAWCAP, const int NGW) {
   cg::cluster_group cluster = cg::this_cluster();
   const unsigned rank = cluster.block_rank();

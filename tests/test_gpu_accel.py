@@ -23,7 +23,7 @@ def F():
     return fmdp
 
 
-SMALL = dict(turn_steps=(-6, 0, 6), acc_units=(-4, 0, 4), climb_units=(-16, 0, 16))  # 9 paths: 2 tiles
+SMALL = dict(turn_steps=(-6, -3, 0, 3, 6), acc_units=(-4, 0, 4), climb_units=(-16, 0, 16))  # 15 paths: tiles 9 + 6
 
 
 def _scenario(seed, n_plans, f4_kw, **kw):
@@ -34,7 +34,7 @@ def _scenario(seed, n_plans, f4_kw, **kw):
     return fs.Scenario(air, sc.terrain, sc.plans, sc.src, sc.dst, sc.t0, name=sc.name + "f4")
 
 
-@pytest.mark.parametrize("f4_kw", [SMALL, {}], ids=["27actions_2tiles", "1350actions"])
+@pytest.mark.parametrize("f4_kw", [SMALL, {}], ids=["45actions_2tiles", "1350actions"])
 def test_eval_step_parity(F, f4_kw):
     sc = _scenario(91, 150, f4_kw, half_m=1500.0, n_buildings=20)
     orc = O.for_scenario(sc)
@@ -52,7 +52,7 @@ def test_eval_step_parity(F, f4_kw):
     ctx.close()
 
 
-@pytest.mark.parametrize("f4_kw", [SMALL, {}], ids=["27actions_2tiles", "1350actions"])
+@pytest.mark.parametrize("f4_kw", [SMALL, {}], ids=["45actions_2tiles", "1350actions"])
 def test_trajectories_replayed_with_speeds(F, f4_kw):
     sc = _scenario(93, 120, f4_kw, n_requests=3, half_m=1200.0, n_buildings=15, max_steps=400, t0_max=40)
     orc = O.for_scenario(sc)
