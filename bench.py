@@ -415,8 +415,9 @@ def run_native(args):
     def measure_latency(plan_counts=(0, 1000, 3000, 10000, 30000), reps=2, min_steps=200):
         # metric "ms/request vs #accepted plans" (Fig perf1): one request against
         # stores of P reflecting-line plans at the configs[1] traffic density (box side ~ sqrt P),
-        # the first of the scenario's requests that flies >= min_steps; cluster size from the
-        # cost model for a lone walker; device time of the walk launches
+        # the first of the scenario's requests that is ACCEPTED after >= min_steps (a full trip,
+        # not a truncated rejection; else the longest one); cluster size from the cost model for a
+        # lone walker; device time of the walk launches
         out = []
         for P in plan_counts:
             sc_p = fs.config_scaled(args.seed + 7 + 1000 * rank, P)
@@ -424,14 +425,17 @@ def run_native(args):
             if P:
                 lctx.add_plans(sc_p.plans)
             row = {"plans": P, "box_km": round(2 * sc_p.airspace.hi_m[0] / 1000.0, 1)}
-            pick = 0
+            pick, longest = None, (-1, 0)
             lctx.set_launch(cull=1)
             for i in range(len(sc_p.t0)):
                 r = lctx.schedule(sc_p.src[i], sc_p.dst[i], int(sc_p.t0[i]), want_traj=False)
                 lctx.truncate(P)
-                if r.n_states - 1 >= min_steps:
+                longest = max(longest, (r.n_states, i))
+                if r.status == 0 and r.n_states - 1 >= min_steps:
                     pick = i
                     break
+            if pick is None:
+                pick = longest[1]
             row["request"] = pick
             for cull in (0, 1):
                 lctx.set_launch(cull=cull)
@@ -560,6 +564,89 @@ def run_native(args):
             base.close()
         return out
 
+    def measure_f4(n_req=3):
+        # the paper-scale action space A = 1350 (15 turns x 9 speed increments x 10
+        # climbs; Table DS / KI captions P:387) against the configs[1] store, requests
+        # walked one at a time by the wide walker (the action space tiled over 15 clusters);
+        # compared with Fig perf1's per-step time at 3000 plans (context, the paper's GPUs)
+        air = fs.airspace_f4().replace(lo_m=sc.airspace.lo_m, hi_m=sc.airspace.hi_m,
+                                       horizon_steps=sc.airspace.horizon_steps, row_capacity=sc.airspace.row_capacity,
+                                       max_steps=sc.airspace.max_steps)
+        fctx = FMDP(air, sc.terrain, device=local, stream=stream)
+        fctx.add_plans(sc.plans)
+        f0 = fctx.num_plans()
+        out = {"what": "SURVEY f4: A = 1350 actions (15 turns x 9 accelerations x 10 climbs, DESIGN.md R32) against "
+                       "the configs[1] store (3000 plans, 256 terrain wells), one request at a time on the whole GPU "
+                       "(wide walker: 15 clusters x 8 CTAs); parity: tests/test_gpu_accel.py",
+               "actions": fctx.A,
+               "paper_fig_perf1_ms_per_step_at_3000_plans": {"rtx2080": 4.929 + 0.0566 * 3000,
+                                                              "titan_xp": 1.706 + 0.0369 * 3000},
+               "paper_note": "linear fits of Fig perf1 (SURVEY App. B), A = 1350, fp64, other GPUs: context only"}
+        for cull in (0, 1):
+            fctx.set_launch(cull=cull)
+            rows = []
+            for i in range(n_req):
+                r = fctx.schedule(sc.src[i], sc.dst[i], int(sc.t0[i]), want_traj=False)
+                st = fctx.stats()
+                fctx.truncate(f0)
+                rows.append((st["device_ms"], st["steps"], r.status, st["pair_evals"]))
+            ms = sum(x[0] for x in rows)
+            steps = sum(x[1] for x in rows)
+            out["culled" if cull else "full"] = {
+                "us_per_step": ms * 1e3 / max(1, steps), "ms_per_request": ms / n_req, "steps": steps,
+                "statuses": [x[2] for x in rows], "pair_evals_per_s": sum(x[3] for x in rows) / (ms / 1e3)}
+        fctx.close()
+        return out
+
+    def measure_c4_full(n_seq=12, n_batch=100):
+        # configs[3] at its defined size: 100k plans over 4000 rows (6.4 GB store),
+        # n_seq sequential 5 km requests (full / culled; ms/request reported over the accepted
+        # full-length trips and over all) and one FCFS batch of n_batch requests (culled)
+        sc4, gen = fs.config_c4_full(n_requests=max(n_seq, n_batch))
+        c = FMDP(sc4.airspace, sc4.terrain, device=local, stream=stream)
+        t = time.perf_counter()
+        for t0c, nc, stc in gen.chunks(8192):
+            c.add_plans_packed(t0c, nc, stc)
+        load_s = time.perf_counter() - t
+        P = c.num_plans()
+        out = {"what": "configs[3] at its defined size: 100k accepted plans x 4000 rows (100 x 100 km, ~6.9 "
+                       "plans/km^3), 5 km requests; sequential fmdp_schedule calls (device time) and one batch",
+               "plans": P, "rows": 4000, "load_s": load_s}
+        for cull in (0, 1):
+            c.set_launch(cull=cull)
+            rows = []
+            for i in range(n_seq):
+                r = c.schedule(sc4.src[i], sc4.dst[i], int(sc4.t0[i]), want_traj=False)
+                st = c.stats()
+                c.truncate(P)
+                rows.append((st["device_ms"], st["steps"], r.status, max(1, st["split"]), st["cluster_size"]))
+            acc = [x for x in rows if x[2] == 0]
+            out["sequential_culled" if cull else "sequential_full"] = {
+                "requests": n_seq, "accepted": len(acc),
+                "ms_per_accepted_request": sum(x[0] for x in acc) / len(acc) if acc else None,
+                "steps_per_accepted_request": sum(x[1] for x in acc) / len(acc) if acc else None,
+                "ms_per_request": sum(x[0] for x in rows) / n_seq,
+                "us_per_step": sum(x[0] for x in rows) * 1e3 / max(1, sum(x[1] for x in rows)),
+                "statuses": [x[2] for x in rows], "clusters": rows[0][3], "cluster_size": rows[0][4]}
+            _log(f"c4 full: cull={cull} {out['sequential_culled' if cull else 'sequential_full']}")
+        c.set_launch(cull=1)
+        reqs4 = c.make_requests(sc4.src[:n_batch], sc4.dst[:n_batch], sc4.t0[:n_batch])
+        times = []
+        for _ in range(2):
+            with torch.cuda.stream(stream):
+                ev0.record(stream)
+                res = c.schedule_batch(None, None, None, want_traj=False, reqs=reqs4)
+                ev1.record(stream)
+            ev1.synchronize()
+            times.append(ev0.elapsed_time(ev1))
+            c.truncate(P)
+        out["batch_culled"] = {"requests": n_batch, "ms": min(times), "requests_per_s": n_batch / (min(times) / 1e3),
+                               "accepted": sum(r.accepted for r in res),
+                               "states_per_request": sum(r.n_states for r in res) / n_batch}
+        _log(f"c4 full: batch {out['batch_culled']}")
+        c.close()
+        return out
+
     def measure_c3():
         # configs[2]: 1000 FCFS requests growing the store from 0 plans.  (i) sequential
         # fmdp_schedule calls: host wall time per call from entry to return incl. the trajectory
@@ -672,7 +759,8 @@ def run_native(args):
 
     if args.only_c4:
         out = {"c3_growth": measure_c3() if rank == 0 else None, "c4_sharded": measure_c4(),
-               "c5_stress": measure_c5()}
+               "c4_full_size": measure_c4_full() if rank == 0 else None,
+               "f4_a1350": measure_f4() if rank == 0 else None, "c5_stress": measure_c5()}
         if rank == 0:
             print(json.dumps(out), flush=True)
         return 0
@@ -686,10 +774,14 @@ def run_native(args):
     Mco = measure_cosim()
     _log("latency vs plans")
     Mlat = measure_latency()
+    _log("f4 A = 1350")
+    Mf4 = measure_f4() if rank == 0 else None
     _log("configs[2] sequential growth")
     Mc3 = None if (args.no_c4 or rank != 0) else measure_c3()  # no collectives: rank 0 only
     _log("configs[3] sharded latency")
     Mc4 = None if args.no_c4 else measure_c4()
+    _log("configs[3] full size")
+    Mc4f = None if (args.no_c4 or rank != 0) else measure_c4_full()
     _log("configs[4] roofline stress")
     Mc5 = None if args.no_c4 else measure_c5()
     h2d = n * C_REQUEST_BYTES
@@ -780,6 +872,10 @@ def run_native(args):
         line["c3_growth"] = Mc3
     if Mc4 is not None:
         line["c4_sharded"] = Mc4
+    if Mc4f is not None:
+        line["c4_full_size"] = Mc4f
+    if Mf4 is not None:
+        line["f4_a1350"] = Mf4
     if Mc5 is not None:
         line["c5_stress"] = Mc5
     if not args.no_cpu_baseline:
