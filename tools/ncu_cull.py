@@ -7,7 +7,7 @@ sc = fs.config_c2()
 ctx = FMDP(sc.airspace, sc.terrain)
 ctx.add_plans(sc.plans)
 G = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-ctx.set_launch(cluster_size=G, cull=1)
+ctx.set_launch(cluster_size=G, cull=1, split=1)
 r = ctx.schedule(sc.src[2], sc.dst[2], int(sc.t0[2]))
 print("status", r.status, "n", r.n_states, ctx.stats()["device_ms"])
 ctx.close()
