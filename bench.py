@@ -8,9 +8,10 @@ restored (fmdp_truncate) and L2 is flushed between steps, outside the timed regi
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
-N > 1 (torchrun, one process per GPU): every rank schedules an independent replica batch
-("independent parallel instances") -> weak scaling, value = all ranks' requests / max
-time over ranks.  --impl reference times the oracle (oracle/, fp64 C) on host cores on a
+N > 1 (torchrun, one process per GPU): the same configs[1] batch request-sharded over the ranks
+(fmdp_schedule_batch_dist: rank i % N walks request i, finished requests all-gathered once per
+speculative round, in-order commits on every rank) -> strong scaling, value = the
+batch's requests / max time over ranks.  --impl reference times the oracle (oracle/, fp64 C) on host cores on a
 bounded sample of the same workload.
 """
 from __future__ import annotations
@@ -279,9 +280,15 @@ def run_native(args):
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import fmdp_synth as fs
-    from paper_2008_03518_b200.fmdp import FMDP, Request, Result, pack_plans
+    from paper_2008_03518_b200.fmdp import FMDP, Request, Result, allgather_torch, pack_plans
+    gather = None
+    if world > 1:
+        gather = allgather_torch(device=None if same else torch.device("cuda", local))
 
-    sc = fs.config_c2(seed=args.seed + 1000 * rank)  # replica r: its own seeded batch and store
+    # N > 1: ONE configs[1] FCFS batch, request-sharded over the ranks (fmdp_schedule_batch_dist:
+    # rank i % N walks request i, finished requests all-gathered once per speculative round, commits
+    # in array order on every rank -- SURVEY §8(e) second partitioning): the same seed everywhere
+    sc = fs.config_c2(seed=args.seed)
     stream = torch.cuda.Stream(device=local)
     ctx = FMDP(sc.airspace, sc.terrain, device=local, stream=stream)
     ctx.add_plans(sc.plans)
@@ -294,7 +301,10 @@ def run_native(args):
     def one(want_traj):
         with torch.cuda.stream(stream):
             ev0.record(stream)
-            res = ctx.schedule_batch(None, None, None, want_traj=want_traj, reqs=reqs)
+            if gather is None:
+                res = ctx.schedule_batch(None, None, None, want_traj=want_traj, reqs=reqs)
+            else:
+                res = ctx.schedule_batch_dist(None, None, None, gather, rank, world, want_traj=want_traj, reqs=reqs)
             ev1.record(stream)
         ev1.synchronize()
         return res, ev0.elapsed_time(ev1)
@@ -340,9 +350,9 @@ def run_native(args):
             reset()
         tot_ms = max_over_ranks(sum(times), world)
         e2e_ms = max_over_ranks(sum(e2e_times), world)
-        return dict(tot_ms=tot_ms, e2e_ms=e2e_ms,
-                    value=sum_over_ranks(n * args.steps, world) / (tot_ms / 1e3),
-                    e2e_value=sum_over_ranks(n * len(e2e_times), world) / (e2e_ms / 1e3), d2h=d2h,
+        return dict(tot_ms=tot_ms, e2e_ms=e2e_ms,  # one batch of n requests per step, all ranks together
+                    value=n * args.steps / (tot_ms / 1e3),
+                    e2e_value=n * len(e2e_times) / (e2e_ms / 1e3), d2h=d2h,
                     st_all=st_all, res_last=res_last, clocks=clk.summary(), gpu_log=gpu_log,
                     walk_ms=sum(s["device_ms"] for s in st_all), pairs=sum(s["pair_evals"] for s in st_all),
                     launches=sum(s["kernels"] for s in st_all), steps_dev=sum(s["steps"] for s in st_all))
@@ -822,11 +832,13 @@ def run_native(args):
         return 0
     line = {
         "metric": METRIC, "value": value, "unit": "requests/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOAD, "plans": len(sc.plans), "requests": n, "terrain_wells": int(len(sc.terrain.radius)),
                    "actions": sc.airspace.n_actions, "W": sc.airspace.W, "l2": "flushed between steps (256 MB write)",
-                   "parallelism": f"replicas{world}" if world > 1 else "single-gpu"},
+                   "parallelism": f"request-sharded{world} (one FCFS batch, fmdp_schedule_batch_dist)" if world > 1
+                   else "single-gpu"},
         "ms_per_request": tot_ms / args.steps / n,
         "requests_accepted": acc, "acceptance_rate": acc / n,
         "near_ties_per_batch": sum(r.n_near_ties for r in res_last),

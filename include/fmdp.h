@@ -233,6 +233,24 @@ fmdp_status fmdp_schedule_batch(fmdp_ctx* ctx, const fmdp_request* reqs, int32_t
                                 fmdp_result* res, fmdp_qpos* traj, int32_t traj_cap_each,
                                 int32_t flags);
 
+/* Request-sharded FCFS batch over several GPUs (SURVEY §8(e) "second partitioning"
+ * "independent parallel instances" made exact): every rank holds the same store (the same plans
+ * added in the same order) and calls this collectively with the same requests.  Request i is walked
+ * by rank i % world; after every speculative round the ranks all-gather the requests that finished
+ * in it (status, trajectory, headings, actions, near-tie flags: n * 37 bytes + 40 per request), so
+ * every rank takes the same in-order commit and rollback decisions and appends the
+ * same plans.  Results -- on every rank -- are identical to fmdp_schedule_batch on one GPU.
+ * allgather: every rank contributes `bytes` bytes at `send`; on return `recv` holds world blocks of
+ * `bytes` bytes in rank order (e.g. ncclAllGather / gloo); 0 on success, else the call fails with
+ * FMDP_E_INTERNAL.  Not with acceleration actions. */
+typedef struct fmdp_gather {
+  int32_t rank, world;
+  int32_t (*allgather)(const void* send, void* recv, int64_t bytes, void* user);
+  void* user;
+} fmdp_gather;
+fmdp_status fmdp_schedule_batch_dist(fmdp_ctx* ctx, const fmdp_gather* gather, const fmdp_request* reqs, int32_t n,
+                                     fmdp_result* res, fmdp_qpos* traj, int32_t traj_cap_each);
+
 /* Plan-sharded multi-GPU scheduling, host-stepped reference path.
  * Every rank holds the same store (plans added identically on all ranks) and evaluates only
  * its shard of every time row (slots [n*rank/world, n*(rank+1)/world)).  Per decision step

@@ -781,8 +781,86 @@ fmdp_status run_single(fmdp_ctx* ctx, const Req& r) {
   return check_intra(ctx);
 }
 
+// Request-sharded FCFS (fmdp_schedule_batch_dist): after a round, every rank's requests that finished
+// in it -- Out record, trajectory, headings, actions, near-tie flags -- are all-gathered, written
+// into every rank's scratch (device and h_out) at their slots, and marked finished, so every rank
+// sees the same finished set and takes the same commit / rollback decisions.
+struct FinRec {
+  int32_t slot, n;
+  Out out;
+};
+fmdp_status gather_finished(fmdp_ctx* ctx, const fmdp_gather* g, const std::vector<int>& mine, std::vector<char>& fin,
+                            std::vector<int>& kdone) {
+  const size_t cap = (size_t)ctx->cap_states;
+  std::vector<unsigned char> buf;
+  auto put = [&](const void* p, size_t b) {
+    const size_t o = buf.size();
+    buf.resize(o + ((b + 7) & ~size_t(7)));
+    std::memcpy(buf.data() + o, p, b);
+  };
+  for (int s : mine) {
+    const Out& o = ctx->h_out[s];
+    FinRec r{s, o.n_states, o};
+    put(&r, sizeof(r));
+    const size_t n = (size_t)o.n_states;
+    std::vector<int32_t> tmp(3 * n);
+    CK(cudaMemcpy(tmp.data(), ctx->d_traj + s * cap * 3, sizeof(int32_t) * 3 * n, cudaMemcpyDeviceToHost));
+    put(tmp.data(), sizeof(int32_t) * 3 * n);
+    CK(cudaMemcpy(tmp.data(), ctx->d_heading + s * cap, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+    put(tmp.data(), sizeof(int32_t) * n);
+    CK(cudaMemcpy(tmp.data(), ctx->d_astar + s * cap, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+    put(tmp.data(), sizeof(int32_t) * n);
+    std::vector<int8_t> nt(n);
+    CK(cudaMemcpy(nt.data(), ctx->d_ntie + s * cap, n, cudaMemcpyDeviceToHost));
+    put(nt.data(), n);
+  }
+  const int W = g->world;
+  int64_t mine_b = (int64_t)buf.size();
+  std::vector<int64_t> sizes(W);
+  if (g->allgather(&mine_b, sizes.data(), sizeof(int64_t), g->user))
+    return fail(ctx, FMDP_E_INTERNAL, "allgather callback failed (sizes)");
+  int64_t mx = 0;
+  for (int64_t b : sizes) mx = std::max(mx, b);
+  if (mx == 0) return FMDP_OK;
+  buf.resize((size_t)mx, 0);
+  std::vector<unsigned char> all((size_t)mx * W);
+  if (g->allgather(buf.data(), all.data(), mx, g->user))
+    return fail(ctx, FMDP_E_INTERNAL, "allgather callback failed (records)");
+  for (int q = 0; q < W; ++q) {
+    const unsigned char* p = all.data() + (size_t)q * mx;
+    const unsigned char* e = p + sizes[q];
+    while (p < e) {
+      FinRec r;
+      std::memcpy(&r, p, sizeof(r));
+      p += (sizeof(r) + 7) & ~size_t(7);
+      const size_t n = (size_t)r.n;
+      const size_t s = (size_t)r.slot;
+      const size_t bt = sizeof(int32_t) * 3 * n, bh = sizeof(int32_t) * n;
+      if (q != g->rank) {
+        ctx->h_out[s] = r.out;
+        CK(cudaMemcpy(ctx->d_out + s, &r.out, sizeof(Out), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->d_traj + s * cap * 3, p, bt, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->d_heading + s * cap, p + ((bt + 7) & ~size_t(7)), bh, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->d_astar + s * cap, p + ((bt + 7) & ~size_t(7)) + ((bh + 7) & ~size_t(7)), bh,
+                      cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->d_ntie + s * cap, p + ((bt + 7) & ~size_t(7)) + 2 * ((bh + 7) & ~size_t(7)), n,
+                      cudaMemcpyHostToDevice));
+      }
+      p += ((bt + 7) & ~size_t(7)) + 2 * ((bh + 7) & ~size_t(7)) + ((n + 7) & ~size_t(7));
+      fin[s] = 1;
+      kdone[s] = r.n - 1;
+    }
+  }
+  return FMDP_OK;
+}
+
 fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_result* res, fmdp_qpos* traj,
-                          int32_t traj_cap_each, int32_t flags) {
+                          int32_t traj_cap_each, int32_t flags, const fmdp_gather* g = nullptr) {
+  const bool dist = g && g->world > 1;
+  if (dist && (g->rank < 0 || g->rank >= g->world || !g->allgather))
+    return fail(ctx, FMDP_E_ARG, "invalid fmdp_gather");
+  if (dist && (ctx->wide || (flags & FMDP_BATCH_SEQUENTIAL)))
+    return fail(ctx, FMDP_E_ARG, "request sharding needs the speculative constant-speed batch");
   if (!ctx || (n > 0 && (!reqs || !res)) || n < 0) return fail(ctx, FMDP_E_ARG, "null argument");
   DevGuard dev_guard(ctx->device);  // the context's device for this call, the caller's restored after
   if (traj && traj_cap_each < ctx->w.max_steps + 1)
@@ -832,7 +910,7 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
     while (c < n) {
       std::vector<Req> run;
       for (int i = c; i < n; ++i)
-        if (!fin[i]) {
+        if (!fin[i] && (!dist || i % g->world == g->rank)) {  // request sharding: rank i % world
           Req r = base[i];
           r.start_k = kdone[i];
           run.push_back(r);
@@ -855,12 +933,17 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
         ctx->stats.rounds += 1;
       }
       if ((st = fetch_out(ctx, n))) return st;
+      std::vector<int> mine;  // own requests that finished in this round
       for (const Req& r : run) {
         const Out& o = ctx->h_out[r.slot];
         ctx->stats.steps += o.steps_run;
         if (o.status < 0) kdone[r.slot] = o.n_states - 1;
-        else fin[r.slot] = 1;
+        else {
+          fin[r.slot] = 1;
+          mine.push_back(r.slot);
+        }
       }
+      if (dist && (st = gather_finished(ctx, g, mine, fin, kdone))) return st;
       // influence of every finished, accepted request j that can be committed in this slice --
       // the finished run [c, c_end) -- on every later request i (only newly committed plans
       // can roll anything back, and only requests of that run can be committed now)
@@ -871,7 +954,8 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
       for (int i = 0; i < n; ++i) ns[i] = ctx->h_out[i].n_states;
       for (int j = c; j < c_end; ++j)
         if (ctx->h_out[j].status == FMDP_ACCEPTED)
-          for (int i = j + 1; i < n; ++i) pairs.push_back({i, j});
+          for (int i = j + 1; i < n; ++i)  // sharded: the trajectories this rank holds
+            if (!dist || fin[i] || i % g->world == g->rank) pairs.push_back({i, j});
       std::vector<int32_t> kf;
       if (!pairs.empty()) {
         CK(cudaMemcpyAsync(ctx->d_nstates, ns.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
@@ -1887,6 +1971,12 @@ fmdp_status fmdp_schedule_cosim(fmdp_ctx* ctx, const fmdp_request* reqs, int32_t
   ctx->stats.pair_evals = (int64_t)pc;
   ctx->last_n = n;
   return FMDP_OK;
+}
+
+fmdp_status fmdp_schedule_batch_dist(fmdp_ctx* ctx, const fmdp_gather* g, const fmdp_request* reqs, int32_t n,
+                                     fmdp_result* res, fmdp_qpos* traj, int32_t traj_cap_each) {
+  if (!ctx || !g) return fail(ctx, FMDP_E_ARG, "null argument");
+  return schedule_many(ctx, reqs, n, res, traj, traj_cap_each, 0, g);
 }
 
 fmdp_status fmdp_schedule_batch(fmdp_ctx* ctx, const fmdp_request* reqs, int32_t n, fmdp_result* res,

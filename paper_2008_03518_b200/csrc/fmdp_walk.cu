@@ -1201,9 +1201,8 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       if (xmode == 2) {
         stay_all = args.xbuf[NTAU * AW];  // all-reduced over the GPUs
       } else {
-#pragma unroll
-        for (int b = 0; b < 16; ++b)  // independent loads (G <= 16)
-          if (b < (int)G) stay_all = min(stay_all, s_stay[p * 16 + b]);
+        // lane b reads source b's slice minimum (G <= 16), one REDUX per warp
+        stay_all = __reduce_min_sync(0xffffffffu, lane < (int)G ? s_stay[p * 16 + lane] : w.sat_d2);
       }
       if (xmode == 1 && rank == 0 && tid == 0) args.xbuf[NTAU * AW] = stay_all;
       uint32_t xtag = 0;

@@ -83,6 +83,13 @@ class Result(C.Structure):
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int32, C.POINTER(C.c_uint32), C.c_int32, C.c_void_p)
 
 
+GATHER_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
+
+
+class Gather(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("allgather", GATHER_FN), ("user", C.c_void_p)]
+
+
 class Shard(C.Structure):
     _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("allreduce_min_u32", ALLREDUCE_FN), ("user", C.c_void_p)]
 
@@ -107,7 +114,7 @@ EXPORTS = ["fmdp_airspace_default", "fmdp_create", "fmdp_destroy", "fmdp_set_lau
            "fmdp_schedule_departures", "fmdp_schedule_cosim", "fmdp_cosim_max", "fmdp_get_steplog", "fmdp_get_plan",
            "fmdp_num_plans", "fmdp_truncate", "fmdp_eval_step", "fmdp_get_stats", "fmdp_num_actions",
            "fmdp_strerror", "fmdp_last_error", "fmdp_set_trace", "fmdp_get_trace", "fmdp_get_speeds",
-           "fmdp_eval_step_v"]
+           "fmdp_eval_step_v", "fmdp_schedule_batch_dist"]
 
 _lib = None
 
@@ -141,6 +148,7 @@ def lib():
         L.fmdp_schedule_p2p.argtypes = [vp, C.c_uint64, Vec3, Vec3, i64, C.POINTER(Result), vp, i32]
         L.fmdp_get_steplog.argtypes = [vp, i32, vp, vp, vp, i32, C.POINTER(i32)]
         L.fmdp_set_trace.argtypes = [vp, i32]
+        L.fmdp_schedule_batch_dist.argtypes = [vp, C.POINTER(Gather), vp, i32, vp, vp, i32]
         L.fmdp_get_speeds.argtypes = [vp, i32, vp, i32, C.POINTER(i32)]
         L.fmdp_get_trace.argtypes = [vp, i32, vp, vp, i32, C.POINTER(i32)]
         L.fmdp_get_plan.argtypes = [vp, C.c_uint32, C.POINTER(i64), vp, i32, C.POINTER(i32)]
@@ -371,6 +379,35 @@ class FMDP:
                     "fmdp_schedule_batch")
         return [self._res(res[i], None if traj is None else traj[i]) for i in range(n)]
 
+    def schedule_batch_dist(self, src, dst, t0, allgather, rank: int, world: int, want_traj: bool = True,
+                            reqs=None) -> List[ScheduleResult]:
+        """Request-sharded FCFS batch (SURVEY §8(e) second partitioning; collective over the ranks):
+        ``allgather(block: bytes) -> list of world equal-size bytes blocks in rank order`` (see
+        ``allgather_torch``).  Every rank returns the full results, identical to schedule_batch."""
+        def _cb(send, recv, nbytes, user):
+            try:
+                blk = C.string_at(send, nbytes) if nbytes else b""
+                out = allgather(blk)
+                if len(out) != world or any(len(b) != nbytes for b in out):
+                    return 1
+                C.memmove(recv, b"".join(out), nbytes * world)
+                return 0
+            except Exception:  # reported as FMDP_E_INTERNAL
+                return 1
+
+        cb = GATHER_FN(_cb)
+        g = Gather(int(rank), int(world), cb, None)
+        if reqs is None:
+            reqs = self.make_requests(src, dst, t0)
+        n = len(reqs)
+        res = (Result * n)()
+        cap = self.max_steps + 1
+        traj = np.zeros((n, cap, 3), np.int32) if want_traj else None
+        self._check(self.L.fmdp_schedule_batch_dist(self.ctx, C.byref(g), C.cast(reqs, C.c_void_p), n,
+                                                    C.cast(res, C.c_void_p), _p(traj), cap),
+                    "fmdp_schedule_batch_dist")
+        return [self._res(res[i], None if traj is None else traj[i]) for i in range(n)]
+
     def schedule_cosim(self, src, dst, t0, want_traj: bool = True, reqs=None) -> List[ScheduleResult]:
         """co-simulated batch (mutually aware, one clock); accepted plans appended in order."""
         if reqs is None:
@@ -518,6 +555,23 @@ def allreduce_min_torch(group=None, device=None):
             t = t.to(device)
         dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
         arr[:] = t.cpu().numpy().astype(np.uint32)
+    return f
+
+
+def allgather_torch(group=None, device=None):
+    """All-gather of equal-size byte blocks over a torch.distributed group (plumbing for
+    ``schedule_batch_dist``): NCCL when ``device`` is a CUDA device, else gloo."""
+    import torch
+    import torch.distributed as dist
+
+    def f(block: bytes):
+        world = dist.get_world_size(group)
+        t = torch.frombuffer(bytearray(block), dtype=torch.uint8) if block else torch.zeros(0, dtype=torch.uint8)
+        if device is not None:
+            t = t.to(device)
+        out = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(out, t, group=group)
+        return [bytes(o.cpu().numpy().tobytes()) for o in out]
     return f
 
 

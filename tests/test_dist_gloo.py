@@ -101,3 +101,33 @@ def test_gloo_p2p_connect_group_exchanges_handles(tmp_path):
         want_ptrs = [0x1000 * (q + 1) if q == r else 0 for q in range(world)]
         assert got[4:6] == want_ptrs
         assert got[6] == 1
+
+
+def _gather_worker(rank, world, port, out_dir):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2008_03518_b200.fmdp import allgather_torch
+    f = allgather_torch()
+    # the two exchanges of one fmdp_schedule_batch_dist round: block sizes (8 bytes), then the
+    # records padded to the largest block; and an all-empty round (no request finished anywhere)
+    sizes = f(np.array([17 * (rank + 1)], np.int64).tobytes())
+    blocks = f(bytes([rank + 1]) * 40)
+    empty = f(b"")
+    import json
+    json.dump([np.frombuffer(b"".join(sizes), np.int64).tolist(), [b[0] for b in blocks], [len(b) for b in blocks],
+               [len(e) for e in empty]], open(os.path.join(out_dir, f"g{rank}.json"), "w"))
+    dist.destroy_process_group()
+
+
+def test_gloo_allgather_blocks(tmp_path):
+    """allgather_torch (plumbing of the request-sharded batch, fmdp_schedule_batch_dist): equal-size
+    byte blocks gathered in rank order, also empty ones."""
+    world = 2
+    mp.spawn(_gather_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        import json
+        sizes, first, lens, empty = json.load(open(tmp_path / f"g{r}.json"))
+        assert sizes == [17, 34] and first == [1, 2] and lens == [40, 40] and empty == [0, 0]
