@@ -662,7 +662,10 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
 
   // per-phase cycle accounting: only in the reference instantiation (MODE 3; a profiled FCFS
   // walk runs there) -- its marks cost up to 6 % of a latency-bound step elsewhere
-  const bool prof = MODE == 3 && args.prof != nullptr && rank == 0 && tid == 0;
+#ifndef FMDP_PROF_TID  // A/B builds (tools/ab_variants.py) may profile another thread's view of the step
+#define FMDP_PROF_TID 0
+#endif
+  const bool prof = MODE == 3 && args.prof != nullptr && rank == 0 && tid == (FMDP_PROF_TID < 0 ? NT + FMDP_PROF_TID : FMDP_PROF_TID);
   unsigned long long pacc[PH_N];
 #pragma unroll
   for (int i = 0; i < PH_N; ++i) pacc[i] = 0;
@@ -881,7 +884,11 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           // -- agrees with the oracle's pow to ~1e-15, so the level / climb near-ties of the goal
           // term (gaps ~1e-7 relative at 10 km) are decided as the oracle does
           const double gx = (double)(q4.x - rq.dst[0]), gy = (double)(q4.y - rq.dst[1]), gz = (double)(q4.z - rq.dst[2]);
+#ifdef FMDP_AB_GOAL32  // A/B only: the round-1 FP32 goal term, to measure what fp64 costs
+          const double vpos = (double)(w.goal_rf * ex2_approx(w.goal_l2gf * sqrtf((float)fma(gz, gz, fma(gy, gy, gx * gx)))));
+#else
           const double vpos = w.goal_r * exp2(w.goal_l2g * sqrt(fma(gz, gz, fma(gy, gy, gx * gx))));
+#endif
           const double valt = (q4.z < w.zdeck_u) ? (w.deck_scale - w.u_m * (double)q4.z) : 0.0;
           int64_t mT = INT64_MAX;
           const int nt = ntc <= TC_MAX ? ntc : w.n_tw;

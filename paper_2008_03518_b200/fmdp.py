@@ -123,9 +123,10 @@ def lib():
     """Load the in-tree libfmdp.so (raises if it was not built)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB):
-            raise FmdpError(f"{LIB} not built: run paper_2008_03518_b200.build.build() (nvcc, sm_100a)")
-        L = C.CDLL(LIB)
+        path = os.environ.get("FMDP_LIB_VARIANT") or LIB  # A/B builds of the same sources (tools/ab_variants.py)
+        if not os.path.exists(path):
+            raise FmdpError(f"{path} not built: run paper_2008_03518_b200.build.build() (nvcc, sm_100a)")
+        L = C.CDLL(path)
         vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
         L.fmdp_airspace_default.argtypes = [C.POINTER(Airspace)]
         L.fmdp_airspace_default.restype = None
