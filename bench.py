@@ -47,6 +47,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-c4", action="store_true", help="skip the configs[2] / configs[3] blocks")
     p.add_argument("--only-c4", action="store_true", help="run only the configs[2] / configs[3] blocks")
+    p.add_argument("--c5-full", action="store_true",
+                   help="add configs[4] at its defined size (1M plans x 3000 rows, 48 GB; minutes to load)")
     return p.parse_args()
 
 
@@ -657,6 +659,38 @@ def run_native(args):
         c.close()
         return out
 
+    def measure_c5_full(n_req=10):
+        # configs[4] at its defined size: 1M plans over 3000 rows (48 GB store on one
+        # B200), A = 85; 10 single requests on the full path (split over the co-resident clusters)
+        # and culled; device time
+        sc5, gen = fs.config_c5_full(n_requests=n_req)
+        c = FMDP(sc5.airspace, sc5.terrain, device=local, stream=stream)
+        t = time.perf_counter()
+        for t0c, nc, stc in gen.chunks(16384, device=torch.device("cuda", local)):
+            c.add_plans_packed(t0c, nc, stc)
+        load_s = time.perf_counter() - t
+        P = c.num_plans()
+        out = {"what": "configs[4] at its defined size: 1M accepted plans x 3000 rows (250 x 250 km, 48 GB store), "
+                       "A = 85, single requests (device time); parity: tests/test_gpu_big.py (FMDP_BIG=1)",
+               "plans": P, "rows": 3000, "load_s": load_s, "store_gb": 16.0 * P * (3000 + 8) / 1e9}
+        for name, cull in (("full_split", 0), ("culled", 1)):
+            c.set_launch(cull=cull)
+            rows = []
+            for i in range(n_req if cull else min(3, n_req)):
+                r = c.schedule(sc5.src[i], sc5.dst[i], int(sc5.t0[i]), want_traj=False)
+                st = c.stats()
+                c.truncate(P)
+                rows.append((st["device_ms"], st["steps"], r.status, st["pair_evals"], max(1, st["split"]),
+                             st["cluster_size"]))
+            ms, steps = sum(x[0] for x in rows), sum(x[1] for x in rows)
+            out[name] = {"requests": len(rows), "us_per_step": ms * 1e3 / max(1, steps), "steps": steps,
+                         "ms_per_request": ms / len(rows), "statuses": [x[2] for x in rows],
+                         "pair_evals_per_s": sum(x[3] for x in rows) / (ms / 1e3), "clusters": rows[0][4],
+                         "cluster_size": rows[0][5]}
+            _log(f"c5 full: {name} {out[name]}")
+        c.close()
+        return out
+
     def measure_c3():
         # configs[2]: 1000 FCFS requests growing the store from 0 plans.  (i) sequential
         # fmdp_schedule calls: host wall time per call from entry to return incl. the trajectory
@@ -886,6 +920,9 @@ def run_native(args):
         line["c4_sharded"] = Mc4
     if Mc4f is not None:
         line["c4_full_size"] = Mc4f
+    if args.c5_full and rank == 0:
+        _log("configs[4] full size")
+        line["c5_full_size"] = measure_c5_full()
     if Mf4 is not None:
         line["f4_a1350"] = Mf4
     if Mc5 is not None:

@@ -433,11 +433,27 @@ class ReflectingLinesPacked:
         y = np.where(y > L, 2 * L - y, y)
         return (self.lo3[None, None, :] + y).astype(np.int32)
 
-    def chunks(self, chunk: int = 4096):
+    def _states_torch(self, a: int, b: int, k0: int, k1: int, device) -> np.ndarray:
+        import torch  # the same integer arithmetic on a GPU (input generation only), bit-identical
+        p0 = torch.as_tensor(self.p0[a:b], device=device)
+        v = torch.as_tensor(self.v[a:b], device=device)
+        lo3 = torch.as_tensor(self.lo3, device=device)
+        L = torch.as_tensor(self.hi3 - self.lo3, device=device)
+        K = torch.arange(k0 - self.rows[0], k1 - self.rows[0], dtype=torch.int64, device=device)[None, :, None]
+        raw = p0[:, None, :] + v[:, None, :] * K - lo3
+        y = torch.remainder(raw, 2 * L)
+        y = torch.where(y > L, 2 * L - y, y)
+        return (lo3 + y).to(torch.int32).cpu().numpy()
+
+    def chunks(self, chunk: int = 4096, device=None):
+        """Packed chunks; with `device` (a CUDA device) the fold runs there (same integers)."""
         nk = self.rows[1] - self.rows[0]
         for a in range(0, self.n, chunk):
             b = min(self.n, a + chunk)
-            st = self._states(a, b, self.rows[0], self.rows[1]).reshape(-1, 3)
+            if device is None:
+                st = self._states(a, b, self.rows[0], self.rows[1]).reshape(-1, 3)
+            else:
+                st = self._states_torch(a, b, self.rows[0], self.rows[1], device).reshape(-1, 3)
             yield (np.full(b - a, self.rows[0], np.int64), np.full(b - a, nk, np.int32), st)
 
     def window(self, K0: int, K1: int):

@@ -873,11 +873,14 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         __syncthreads();
         FMDP_MARK(PH_PROJ)
         // ---- a3 goal (fp64), deck, a5 terrain (exact predicate, FP32 ex2 value): owned states.
-        //      Taken by the CTA's last threads (the first ones carry the build pass of the row
-        //      slice), so the fp64 latency overlaps the row wait and the build.
+        //      Taken from the second-last warp downwards: the first threads carry the build pass
+        //      of the row slice, and the last warp holds the I/O thread (its row-count load and
+        //      TMA issue would serialise with divergent FIX lanes of the same warp), so the fp64
+        //      latency overlaps the row wait and the build (measured: the FIX lanes sharing the
+        //      I/O thread's warp were the step's last arrivals)
         const int ntc = ctl->ntc[tcb];
         const int32_t* s_tc = s_tc2 + tcb * TC_MAX;
-        for (int i = (tid == NT - 1) ? NT - 1 : NT - 2 - tid; i < n_own * W; i += NT) {
+        for (int i = (2 * NT - 33 - tid) % NT; i < n_own * W; i += NT) {
           const int st = ((int)rank + (i / W) * (int)G) * W + i % W;
           const int4 q4 = s_pos[st];
           // fp64: exact integer d^2 < 2^52, correctly rounded sqrt, exp2 within an ulp

@@ -12,8 +12,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
     "base": [],
-    "goal32": ["FMDP_AB_GOAL32"],
-    "prof_fix": ["FMDP_PROF_TID=-2"],
+    "prof_fix": ["FMDP_PROF_TID=-33"],
+    "old": None,  # a previously built .so kept in ab/ (not rebuilt)
 }
 
 
@@ -21,6 +21,8 @@ def build():
     from paper_2008_03518_b200.build import build as b
     os.makedirs(os.path.join(ROOT, "ab"), exist_ok=True)
     for name, d in VARIANTS.items():
+        if d is None:
+            continue
         print(b(force=True, out=os.path.join(ROOT, "ab", f"libfmdp_{name}.so"), defines=d))
 
 
