@@ -170,7 +170,7 @@ inline size_t x_area_bytes(int world, int slot) {
 struct Layout {
   int HL, CH, RAWCAP, NT, C, NCOL, A, AW, G, BLK, NOWN, RAWW;
   size_t o_dxy, o_tw, o_raw, o_cen, o_stage, o_recv, o_pos, o_fix, o_sfix, o_vT, o_mI, o_vstar, o_vsc, o_conf,
-      o_confg, o_flags, o_stay, o_amb, o_tc, o_bar, o_ctl, total;
+      o_confg, o_flags, o_stay, o_amb, o_tc, o_bar, o_ctl, o_M, total;
   __host__ __device__ static size_t al(size_t x) { return (x + 15) & ~size_t(15); }
   __host__ __device__ void build(int hl, int ch, int rawcap, int nt, int c, int ncol, int a, int aw, int g) {
     HL = hl; CH = ch; RAWCAP = rawcap; NT = nt; C = c; NCOL = ncol; A = a; AW = aw; G = g;
@@ -200,6 +200,7 @@ struct Layout {
     o_tc = o;   o = al(o + sizeof(int32_t) * 2 * TC_MAX);  // candidate lists, by step parity
     o_bar = o;  o = al(o + sizeof(uint64_t) * 8);   // 3 TMA ring + 2 reduce-scatter + 2 V* mbarriers
     o_ctl = o;  o = al(o + 512);
+    o_M = o;    o = al(o + sizeof(float) * (size_t)NOWN * BLK);  // owner pass: in-radius minima of the owned items
     total = o;
   }
 };

@@ -802,134 +802,6 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
 #pragma unroll
       for (int c = 0; c < C; ++c) sz2[c] = 0;
       int x1 = 0, y1 = 0;  // Delta_1 of this turn (t = 1 columns, group 0)
-      if (!fin) {
-        // ---- a5 candidates of steps k+1 .. k+1+TC_WIN when this list's window ends with step k
-        //      (rescan from q_k: every later state within the window is at most TC_WIN substep
-        //      reaches away) into the other list buffer, switched to after the hot loop
-        if (k + 1 > tc_end) {
-          const int64_t grow = (int64_t)w.reach_u + (int64_t)(TC_WIN + 1) * w.step_reach_u;
-          for (int i = tid; i < w.n_tw; i += NT) {
-            const int4 t = tw[i];
-            const int64_t dx = t.x - qx, dy = t.y - qy, dz = t.z - qz;
-            const int64_t rr = (int64_t)t.w + grow;
-            if (dx * dx + dy * dy + dz * dz < rr * rr) {
-              const int slot = atomicAdd(&ctl->ntc[tcb ^ 1], 1);
-              if (slot < TC_MAX) s_tc2[(tcb ^ 1) * TC_MAX + slot] = i;
-            }
-          }
-        }
-        FMDP_MARK(PH_SCAN)
-        // ---- a2 forward projection (Alg 3): column (turn it, substep t) on the integer lattice
-        const int it = col_it, t = col_t, h = col_h;
-        // cumulative lattice displacement of (psi, turn, t) from the host-built table (one L2 load
-        // instead of t dependent lattice steps); final heading psi + t*h mod HL
-        int x, y, ps;
-        if (WIDE) {  // R32: psi_s = psi + s h, v_s = clamp(v + s acc), q_t = q + sum_{s<=t} D(psi_s, v_s)
-          int xx = qx, yy = qy, pp = psi, sp = v;
-          for (int s2 = 1; s2 <= W; ++s2) {
-            const int pn = pp + col_hw;
-            const int pw2 = pn >= w.HL ? pn - w.HL : (pn < 0 ? pn + w.HL : pn);
-            const int sn = min(max(sp + col_acc, w.vmin), w.vmax);
-            if (s2 <= t) {
-              const int2 d = __ldg(&w.spd[(size_t)(sn - w.vmin) * w.HL + pw2]);
-              xx += d.x;
-              yy += d.y;
-              pp = pw2;
-              sp = sn;
-            }
-          }
-          x = xx;
-          y = yy;
-          ps = pp | (sp << 16);  // heading and speed of the state (s_pos .w)
-        } else {
-          const int2 cum = __ldg(&w.proj[((size_t)psi * w.n_turn + it) * W + (t - 1)]);
-          x = qx + cum.x;
-          y = qy + cum.y;
-          ps = (psi + t * h) % w.HL;
-          ps += ps < 0 ? w.HL : 0;
-        }
-        // offsets from the fan origin o = q + (W/2) (DX, DY)[psi], doubled: the hot loop
-        // evaluates |s - c|^2 - |s - o|^2 = Q + 2 (s - o).X with X = o - c, Q = |X|^2
-        sx = (float)(2 * (x - qx - ox));
-        sy = (float)(2 * (y - qy - oy));
-#pragma unroll
-        for (int c = 0; c < C; ++c) sz[c] = (float)(2 * w.climb[c] * t);
-        sx2 = pk2(sx, sx);
-        sy2 = pk2(sy, sy);
-#pragma unroll
-        for (int c = 0; c < C; ++c) sz2[c] = pk2(sz[c], sz[c]);
-        if (grp == 0 && col < NCOL) {
-#pragma unroll
-          for (int c = 0; c < C; ++c) s_pos[(it * C + c) * W + (t - 1)] = make_int4(x, y, qz + w.climb[c] * t, ps);
-          if (t == 1) {  // raster load in flight during the hot loop (LDGSTS), consumed after it
-            const int32_t* cell = ground_cell(w, x, y);
-            if (cell) cp_async4(&ctl->hgt[it], cell);
-            else ctl->hgt[it] = INT_MIN;
-            x1 = x;
-            y1 = y;
-          }
-        }
-        FMDP_MARK(PH_PLOOP)
-        __syncthreads();
-        FMDP_MARK(PH_PROJ)
-        // ---- a3 goal (fp64), deck, a5 terrain (exact predicate, FP32 ex2 value): owned states.
-        //      Taken from the second-last warp downwards: the first threads carry the build pass
-        //      of the row slice, and the last warp holds the I/O thread (its row-count load and
-        //      TMA issue would serialise with divergent FIX lanes of the same warp), so the fp64
-        //      latency overlaps the row wait and the build (measured: the FIX lanes sharing the
-        //      I/O thread's warp were the step's last arrivals)
-        const int ntc = ctl->ntc[tcb];
-        const int32_t* s_tc = s_tc2 + tcb * TC_MAX;
-        for (int i = (2 * NT - 33 - tid) % NT; i < n_own * W; i += NT) {
-          const int st = ((int)rank + (i / W) * (int)G) * W + i % W;
-          const int4 q4 = s_pos[st];
-          // fp64: exact integer d^2 < 2^52, correctly rounded sqrt, exp2 within an ulp
-          // -- agrees with the oracle's pow to ~1e-15, so the level / climb near-ties of the goal
-          // term (gaps ~1e-7 relative at 10 km) are decided as the oracle does
-          const double gx = (double)(q4.x - rq.dst[0]), gy = (double)(q4.y - rq.dst[1]), gz = (double)(q4.z - rq.dst[2]);
-#ifdef FMDP_AB_GOAL32  // A/B only: the round-1 FP32 goal term, to measure what fp64 costs
-          const double vpos = (double)(w.goal_rf * ex2_approx(w.goal_l2gf * sqrtf((float)fma(gz, gz, fma(gy, gy, gx * gx)))));
-#else
-          const double vpos = w.goal_r * exp2(w.goal_l2g * sqrt(fma(gz, gz, fma(gy, gy, gx * gx))));
-#endif
-          const double valt = (q4.z < w.zdeck_u) ? (w.deck_scale - w.u_m * (double)q4.z) : 0.0;
-          int64_t mT = INT64_MAX;
-          const int nt = ntc <= TC_MAX ? ntc : w.n_tw;
-          for (int c = 0; c < nt; ++c) {
-            const int4 t4 = tw[ntc <= TC_MAX ? s_tc[c] : c];
-            const int64_t dx = q4.x - t4.x, dy = q4.y - t4.y, dz = q4.z - t4.z;
-            const int64_t d2 = dx * dx + dy * dy + dz * dz;
-            if (d2 < (int64_t)t4.w * t4.w && d2 < mT) mT = d2;
-          }
-          s_vT[st] = (mT != INT64_MAX) ? w.terr_r * ex2_approx(w.terr_l2g * sqrtf((float)mT)) : 0.f;
-          s_fix[st] = vpos - valt;
-          s_sfix[st] = vpos + valt;
-        }
-        FMDP_MARK(PH_FIX)
-      }
-
-      // ---- per-step I/O, on the CTA's last thread after the projection barrier (thread 0 owns
-      //      projection columns; this one has no build work in the latency-bound configurations):
-      //      prefetch of row K+2 (its ring buffer last held row K-1, consumed in step k-1),
-      //      this step's exchange phases -- slice minima (4 B from every CTA), reduce-scatter
-      //      blocks of the owned actions (from every CTA), the stop flag (from rank 0), V*(a)
-      if (tid == NT - 1) {
-        if (!evalm && !fin) {
-          issue_row(w, K + 2, cnt2, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, srank, sworld);
-          cnt2 = row_count(w, K + 3);  // consumed next step: latency hidden by this step
-        }
-        ctl->nsurv[((k + 1) & 1) * 2] = 0;  // step k+1, chunk 0 (last used in step k-1)
-        const uint32_t bytesA = (xmode != 2 ? 4u * G : 0u) +
-                                ((!fin && xmode != 2) ? (uint32_t)(4 * G * n_own * BLK) : 0u) + (args.stop ? 4u : 0u);
-        mbar_arrive_tx(&s_bar[3 + p], bytesA);
-        if (!fin) mbar_arrive_tx(&s_bar[5 + p], (uint32_t)(16 * A) + (XP ? 4u : 0u));
-        if (args.stop && rank == 0) {  // one reading for the whole cluster
-          const uint32_t f = (uint32_t)*(volatile int32_t*)args.stop;
-          const uint32_t la = smem_u32(&ctl->stop[p]), lb = smem_u32(&s_bar[3 + p]);
-          for (unsigned b = 0; b < G; ++b) push_u32(solo, la, b, f, lb);
-        }
-      }
-
       // ---- a1 + a4: stage row K, wells, hot loop; exact nearest-plan distance of q ("stay")
       float m[C][NTAU];
 #pragma unroll
@@ -1096,6 +968,139 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         };
 
         const int n_chunks = xmode != 2 ? (n + SC - 1) / SC : 0;
+        // the first chunk's well records are built BEFORE the projection: the build needs only q,
+        // the fan origin and row K (staged two steps ahead), so it overlaps the projection's
+        // table load, and the projection barrier also publishes the records (one CTA barrier less)
+        if (n_chunks > 0) build(0, min(SC, n), cullm, &ctl->nsurv[(k & 1) * 2]);
+        FMDP_MARK(PH_BUILD)
+        if (!fin) {
+          // ---- a5 candidates of steps k+1 .. k+1+TC_WIN when this list's window ends with step k
+          //      (rescan from q_k: every later state within the window is at most TC_WIN substep
+          //      reaches away) into the other list buffer, switched to after the hot loop
+          if (k + 1 > tc_end) {
+            const int64_t grow = (int64_t)w.reach_u + (int64_t)(TC_WIN + 1) * w.step_reach_u;
+            for (int i = tid; i < w.n_tw; i += NT) {
+              const int4 t = tw[i];
+              const int64_t dx = t.x - qx, dy = t.y - qy, dz = t.z - qz;
+              const int64_t rr = (int64_t)t.w + grow;
+              if (dx * dx + dy * dy + dz * dz < rr * rr) {
+                const int slot = atomicAdd(&ctl->ntc[tcb ^ 1], 1);
+                if (slot < TC_MAX) s_tc2[(tcb ^ 1) * TC_MAX + slot] = i;
+              }
+            }
+          }
+          FMDP_MARK(PH_SCAN)
+          // ---- a2 forward projection (Alg 3): column (turn it, substep t) on the integer lattice
+          const int it = col_it, t = col_t, h = col_h;
+          // cumulative lattice displacement of (psi, turn, t) from the host-built table (one L2 load
+          // instead of t dependent lattice steps); final heading psi + t*h mod HL
+          int x, y, ps;
+          if (WIDE) {  // R32: psi_s = psi + s h, v_s = clamp(v + s acc), q_t = q + sum_{s<=t} D(psi_s, v_s)
+            int xx = qx, yy = qy, pp = psi, sp = v;
+            for (int s2 = 1; s2 <= W; ++s2) {
+              const int pn = pp + col_hw;
+              const int pw2 = pn >= w.HL ? pn - w.HL : (pn < 0 ? pn + w.HL : pn);
+              const int sn = min(max(sp + col_acc, w.vmin), w.vmax);
+              if (s2 <= t) {
+                const int2 d = __ldg(&w.spd[(size_t)(sn - w.vmin) * w.HL + pw2]);
+                xx += d.x;
+                yy += d.y;
+                pp = pw2;
+                sp = sn;
+              }
+            }
+            x = xx;
+            y = yy;
+            ps = pp | (sp << 16);  // heading and speed of the state (s_pos .w)
+          } else {
+            const int2 cum = __ldg(&w.proj[((size_t)psi * w.n_turn + it) * W + (t - 1)]);
+            x = qx + cum.x;
+            y = qy + cum.y;
+            ps = (psi + t * h) % w.HL;
+            ps += ps < 0 ? w.HL : 0;
+          }
+          // offsets from the fan origin o = q + (W/2) (DX, DY)[psi], doubled: the hot loop
+          // evaluates |s - c|^2 - |s - o|^2 = Q + 2 (s - o).X with X = o - c, Q = |X|^2
+          sx = (float)(2 * (x - qx - ox));
+          sy = (float)(2 * (y - qy - oy));
+  #pragma unroll
+          for (int c = 0; c < C; ++c) sz[c] = (float)(2 * w.climb[c] * t);
+          sx2 = pk2(sx, sx);
+          sy2 = pk2(sy, sy);
+  #pragma unroll
+          for (int c = 0; c < C; ++c) sz2[c] = pk2(sz[c], sz[c]);
+          if (grp == 0 && col < NCOL) {
+  #pragma unroll
+            for (int c = 0; c < C; ++c) s_pos[(it * C + c) * W + (t - 1)] = make_int4(x, y, qz + w.climb[c] * t, ps);
+            if (t == 1) {  // raster load in flight during the hot loop (LDGSTS), consumed after it
+              const int32_t* cell = ground_cell(w, x, y);
+              if (cell) cp_async4(&ctl->hgt[it], cell);
+              else ctl->hgt[it] = INT_MIN;
+              x1 = x;
+              y1 = y;
+            }
+          }
+          FMDP_MARK(PH_PLOOP)
+          __syncthreads();
+          FMDP_MARK(PH_PROJ)
+          // ---- a3 goal (fp64), deck, a5 terrain (exact predicate, FP32 ex2 value): owned states.
+          //      Taken from the second-last warp downwards: the first threads carry the build pass
+          //      of the row slice, and the last warp holds the I/O thread (its row-count load and
+          //      TMA issue would serialise with divergent FIX lanes of the same warp), so the fp64
+          //      latency overlaps the row wait and the build (measured: the FIX lanes sharing the
+          //      I/O thread's warp were the step's last arrivals)
+          const int ntc = ctl->ntc[tcb];
+          const int32_t* s_tc = s_tc2 + tcb * TC_MAX;
+          for (int i = (2 * NT - 33 - tid) % NT; i < n_own * W; i += NT) {
+            const int st = ((int)rank + (i / W) * (int)G) * W + i % W;
+            const int4 q4 = s_pos[st];
+            // fp64: exact integer d^2 < 2^52, correctly rounded sqrt, exp2 within an ulp
+            // -- agrees with the oracle's pow to ~1e-15, so the level / climb near-ties of the goal
+            // term (gaps ~1e-7 relative at 10 km) are decided as the oracle does
+            const double gx = (double)(q4.x - rq.dst[0]), gy = (double)(q4.y - rq.dst[1]), gz = (double)(q4.z - rq.dst[2]);
+  #ifdef FMDP_AB_GOAL32  // A/B only: the round-1 FP32 goal term, to measure what fp64 costs
+            const double vpos = (double)(w.goal_rf * ex2_approx(w.goal_l2gf * sqrtf((float)fma(gz, gz, fma(gy, gy, gx * gx)))));
+  #else
+            const double vpos = w.goal_r * exp2(w.goal_l2g * sqrt(fma(gz, gz, fma(gy, gy, gx * gx))));
+  #endif
+            const double valt = (q4.z < w.zdeck_u) ? (w.deck_scale - w.u_m * (double)q4.z) : 0.0;
+            int64_t mT = INT64_MAX;
+            const int nt = ntc <= TC_MAX ? ntc : w.n_tw;
+            for (int c = 0; c < nt; ++c) {
+              const int4 t4 = tw[ntc <= TC_MAX ? s_tc[c] : c];
+              const int64_t dx = q4.x - t4.x, dy = q4.y - t4.y, dz = q4.z - t4.z;
+              const int64_t d2 = dx * dx + dy * dy + dz * dz;
+              if (d2 < (int64_t)t4.w * t4.w && d2 < mT) mT = d2;
+            }
+            s_vT[st] = (mT != INT64_MAX) ? w.terr_r * ex2_approx(w.terr_l2g * sqrtf((float)mT)) : 0.f;
+            s_fix[st] = vpos - valt;
+            s_sfix[st] = vpos + valt;
+          }
+          FMDP_MARK(PH_FIX)
+        }
+
+        // ---- per-step I/O, on the CTA's last thread after the projection barrier (thread 0 owns
+        //      projection columns; this one has no build work in the latency-bound configurations):
+        //      prefetch of row K+2 (its ring buffer last held row K-1, consumed in step k-1),
+        //      this step's exchange phases -- slice minima (4 B from every CTA), reduce-scatter
+        //      blocks of the owned actions (from every CTA), the stop flag (from rank 0), V*(a)
+        if (tid == NT - 1) {
+          if (!evalm && !fin) {
+            issue_row(w, K + 2, cnt2, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, srank, sworld);
+            cnt2 = row_count(w, K + 3);  // consumed next step: latency hidden by this step
+          }
+          ctl->nsurv[((k + 1) & 1) * 2] = 0;  // step k+1, chunk 0 (last used in step k-1)
+          const uint32_t bytesA = (xmode != 2 ? 4u * G : 0u) +
+                                  ((!fin && xmode != 2) ? (uint32_t)(4 * G * n_own * BLK) : 0u) + (args.stop ? 4u : 0u);
+          mbar_arrive_tx(&s_bar[3 + p], bytesA);
+          if (!fin) mbar_arrive_tx(&s_bar[5 + p], (uint32_t)(16 * A) + (XP ? 4u : 0u));
+          if (args.stop && rank == 0) {  // one reading for the whole cluster
+            const uint32_t f = (uint32_t)*(volatile int32_t*)args.stop;
+            const uint32_t la = smem_u32(&ctl->stop[p]), lb = smem_u32(&s_bar[3 + p]);
+            for (unsigned b = 0; b < G; ++b) push_u32(solo, la, b, f, lb);
+          }
+        }
+
         for (int cidx = 0; cidx < n_chunks + cosim; ++cidx) {
           const int c0 = cidx * SC;
           const bool peers = cidx == n_chunks;
@@ -1103,13 +1108,12 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           int nc;
           if (!peers) {
             nc = min(SC, n - c0);
-            build(c0, nc, cullm, counter);
+            if (cidx > 0) build(c0, nc, cullm, counter);  // chunk 0: built before the projection
           } else {
             nc = build_peers();
           }
           if (fin) continue;
-          FMDP_MARK(PH_BUILD)
-          __syncthreads();
+          if (cidx > 0 || peers) __syncthreads();
           const int ns = (cullm && !peers) ? *counter : nc;
           if (tid == 0) ctl->nsurv[(k & 1) * 2 + ((cidx + 1) & 1)] = 0;  // next pass's counter
           if (ns <= CH) {
@@ -1245,9 +1249,9 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         // Pass 1 (whole CTA, one owned (action, substep, tau) per thread): G-way minimum of the
         // partial blocks (multi-GPU: export / import), |s - o|^2 added back, radius test ->
         // s_M = the in-radius d^2, FLT_MAX (outside), or -1 (inside the FP32 band: exact below).
-        // s_M lives in s_stage, free once every thread of this CTA has pushed its blocks.
-        float* s_M = s_stage;
-        __syncthreads();
+        // s_M has its own buffer (not s_stage, which other threads of this CTA may still be reading
+        // for their pushes to other owners: no CTA barrier needed before this pass).
+        float* s_M = reinterpret_cast<float*>(smem + L.o_M);
         const int nitem = n_own * W * NTAU;
         if (XP) {  // this GPU's minima of the owned items -> every peer (all sends
                    // before any poll); each thread keeps its own items' minima in s_M
