@@ -1065,7 +1065,11 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   #endif
             const double valt = (q4.z < w.zdeck_u) ? (w.deck_scale - w.u_m * (double)q4.z) : 0.0;
             int64_t mT = INT64_MAX;
+#ifdef FMDP_AB_NOTERR  // A/B timing only: no terrain candidates (wrong values)
+            const int nt = 0;
+#else
             const int nt = ntc <= TC_MAX ? ntc : w.n_tw;
+#endif
             for (int c = 0; c < nt; ++c) {
               const int4 t4 = tw[ntc <= TC_MAX ? s_tc[c] : c];
               const int64_t dx = q4.x - t4.x, dy = q4.y - t4.y, dz = q4.z - t4.z;
@@ -1292,7 +1296,11 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
                               x_budget(xit), M);
             }
           } else {
+#ifdef FMDP_AB_P1FIRST  // A/B timing only (wrong values): no G-way minimum
+            M = rcv[oa * BLK + r2];
+#else
             M = gway_min(rcv + oa * BLK + r2, (int)G, NOWN * BLK);
+#endif
             if (xmode == 1) args.xbuf[st * NTAU + t] = __float_as_uint(M);  // this GPU's minima
           }
           const int4 q4 = s_pos[st];
@@ -1316,6 +1324,9 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           if (lane < (int)G)
             push_u32(solo, smem_u32(&ctl->xstay[p]), lane, m, smem_u32(&s_bar[5 + p]));
         }
+#ifdef FMDP_AB_FINE  // A/B profiling only: the pass-1 loop itself, before its barrier ('projection' slot)
+        FMDP_MARK(PH_PROJ)
+#endif
         __syncthreads();
         FMDP_MARK(PH_OWN1)
         const int namb = ctl->namb[p];  // uniform after the barrier

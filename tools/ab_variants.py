@@ -12,8 +12,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
     "base": [],
-    "prof_fix": ["FMDP_PROF_TID=-33"],
-    "old": None,  # a previously built .so kept in ab/ (not rebuilt)
+    "fine0": ["FMDP_AB_FINE"],
+    "old": None,
 }
 
 
@@ -48,7 +48,7 @@ for cull in (0, 1):
     st = ctx.stats(); ctx.truncate(n0)
     ph = {k: round(v / st["steps"]) for k, v in st["phase_cycles"].items() if v}
     out.append(f"G16 cull={cull} us/step={best:.2f} phases={ph}")
-for cull in (0, 1):
+for cull in (0, 1) if "--batch" in sys.argv else ():
     ctx.set_launch(cull=cull)
     ms = []
     for _ in range(3):
