@@ -805,6 +805,8 @@ def run_native(args):
         out = {"c3_growth": measure_c3() if rank == 0 else None, "c4_sharded": measure_c4(),
                "c4_full_size": measure_c4_full() if rank == 0 else None,
                "f4_a1350": measure_f4() if rank == 0 else None, "c5_stress": measure_c5()}
+        if args.c5_full and rank == 0:
+            out["c5_full_size"] = measure_c5_full()
         if rank == 0:
             print(json.dumps(out), flush=True)
         return 0
