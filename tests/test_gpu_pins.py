@@ -53,3 +53,39 @@ def test_terrain_collision_on_the_gpu(F, i):
     ref = O.Oracle(fs.Airspace(), building_raster()).schedule(fs.m2u(src_m), fs.m2u(dst_m), 0, commit=False)
     assert (r.traj == ref.traj).all()
     ctx.close()
+
+
+def test_exact_fallback_overflow_and_terrain_candidate_overflow(F):
+    """The two capacity fallbacks of a step (round-1 review: untested): more than AMB_MAX = 64
+    (state, tau) minima inside the FP32 band (-> the owner rescans every owned item exactly), and
+    more than TC_MAX = 128 terrain wells within reach (-> the whole well list is scanned).  Values,
+    V*, a* and separation minima against the oracle element by element."""
+    air = fs.Airspace(lo_m=(-3000.0, -3000.0, 0.0), hi_m=(3000.0, 3000.0, 1000.0), horizon_steps=64, row_capacity=256,
+                      max_steps=20)
+    q = np.array([0, 0, 300 * U], np.int32)
+    orc_st, _ = O.Oracle(air).project(q, 0)          # the 270 projected states (oracle geometry, exact)
+    R = 450 * U
+    # a stationary plan exactly R from 90 distinct projected states (d^2 = R^2: inside the band,
+    # only the exact int64 test decides -- out, strict <) -> >= 90 ambiguous items in one step
+    plans = []
+    for a in range(0, 27, 3):
+        for t in range(10):
+            s = orc_st[a, t].astype(np.int64)
+            p = s + np.array([0, 0, R])              # straight above: |p - s| = R exactly
+            plans.append((0, np.repeat(p[None], 30, axis=0).astype(np.int32)))
+    # 200 terrain wells hugging the fan (all within reach of every step's states)
+    rng = np.random.default_rng(3)
+    cen = np.stack([rng.integers(-60 * U, 60 * U, 200), rng.integers(-60 * U, 60 * U, 200),
+                    rng.integers(250 * U, 350 * U, 200)], 1).astype(np.int32)
+    terr = fs.Terrain(center=cen, radius=np.full(200, 80 * U, np.int32))
+    orc = O.Oracle(air, terr, plans)
+    ctx = F.FMDP(air, terr, device=0)
+    ctx.add_plans(plans)
+    g = q + np.array([40000, 0, 0], np.int32)
+    for G in (1, 4):  # one CTA owns all 270 states (>= 90 band items > AMB_MAX), then 4 owners
+        ctx.set_launch(cluster_size=G)
+        for K in (0, 5):
+            ref = orc.eval_step(q, 0, g, K)
+            gpu = ctx.eval_step(q, 0, g, K)
+            check_step(gpu, ref, f"overflow G={G} K={K}")
+    ctx.close()

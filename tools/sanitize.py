@@ -95,7 +95,57 @@ def case_p2p():
         c.close()
 
 
+def case_f4():
+    # the wide walker (A = 45 over two action tiles, decision board) and the request-sharded batch
+    kw = dict(turn_steps=(-6, -3, 0, 3, 6), acc_units=(-4, 0, 4), climb_units=(-16, 0, 16))
+    sc = fs.random_small(93, n_plans=60, n_requests=2, half_m=1200.0, max_steps=120, t0_max=20)
+    air = fs.airspace_f4(**kw).replace(lo_m=sc.airspace.lo_m, hi_m=sc.airspace.hi_m,
+                                       horizon_steps=sc.airspace.horizon_steps,
+                                       row_capacity=sc.airspace.row_capacity, max_steps=120)
+    ctx = FMDP(air, sc.terrain, device=0, torch_alloc=False)
+    ctx.add_plans(sc.plans)
+    res = ctx.schedule_batch(sc.src, sc.dst, sc.t0)
+    print("f4:", [r.status for r in res], [r.n_states for r in res])
+    ctx.close()
+
+
+def case_dist():
+    import threading
+    sc = fs.random_small(71, n_plans=60, n_requests=6, half_m=1200.0, max_steps=150, t0_max=40)
+    ref = FMDP(sc.airspace, sc.terrain, device=0, torch_alloc=False)
+    ref.add_plans(sc.plans)
+    want = ref.schedule_batch(sc.src, sc.dst, sc.t0)
+    ref.close()
+    ctxs = []
+    for _ in range(2):
+        c = FMDP(sc.airspace, sc.terrain, device=0, torch_alloc=False)
+        c.add_plans(sc.plans)
+        ctxs.append(c)
+    bar = threading.Barrier(2)
+    slots = [None, None]
+
+    def gather(r):
+        def f(block):
+            slots[r] = block
+            bar.wait()
+            out = list(slots)
+            bar.wait()
+            return out
+        return f
+    out = [None, None]
+    th = [threading.Thread(target=lambda r=r: out.__setitem__(r, ctxs[r].schedule_batch_dist(
+        sc.src, sc.dst, sc.t0, gather(r), r, 2))) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert all(_same(a, b) for r in range(2) for a, b in zip(out[r], want)), "dist batch differs"
+    print("dist:", [r.status for r in want])
+    for c in ctxs:
+        c.close()
+
+
 if __name__ == "__main__":
-    for name in sys.argv[1:] or ["c1", "c2s", "cosim", "p2p"]:
+    for name in sys.argv[1:] or ["c1", "c2s", "cosim", "p2p", "f4", "dist"]:
         globals()["case_" + name]()
     print("sanitize cases ok")
