@@ -497,7 +497,10 @@ fmdp_status run_split(fmdp_ctx* ctx, std::vector<Req>& run, int budget) {
   // speculative steps are the next slices' head work unless a commit rolls them back
   // (configs[1] full batch 115.3 / 109.2 / 108.6 / 111.8 / 115.0 / 121.5 ms for m = 0..5 with
   // the others at half the head's cluster size and the slice budget of 2; culled 58.6-59.0)
-  int m = std::min(2, n - 2);
+  // (FMDP_TUNE_LANES / FMDP_TUNE_GO: tuning overrides for tools/sweep_split.py only)
+  static const int lanes_env = std::getenv("FMDP_TUNE_LANES") ? std::atoi(std::getenv("FMDP_TUNE_LANES")) : 2;
+  static const int go_env = std::getenv("FMDP_TUNE_GO") ? std::atoi(std::getenv("FMDP_TUNE_GO")) : 0;
+  int m = std::min(lanes_env, n - 2);
   while (m > 0 && ctx->num_sms < (1 + m) * Gh + 16) --m;
   const bool lane2 = m > 0;
   const int nl = 1 + m;
@@ -505,7 +508,7 @@ fmdp_status run_split(fmdp_ctx* ctx, std::vector<Req>& run, int budget) {
   // earliest pending requests, which become the next heads (the all-requests cost model of
   // choose_launch optimises the wrong objective here: configs[1] full batch 119.9 -> 111.7 ms,
   // culled 58.7 -> 58.5 ms, configs[2] unchanged)
-  const int Go = std::max(1, Gh / 2);
+  const int Go = go_env > 0 ? go_env : std::max(1, Gh / 2);
   const int nco = std::max(1, std::min(n - nl, std::min(max_clusters(ctx, Go), (ctx->num_sms - nl * Gh) / Go)));
   CK(cudaMemcpyAsync(ctx->d_reqs, run.data(), sizeof(Req) * n, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemsetAsync(ctx->d_queue, 0, 2 * sizeof(int32_t), ctx->stream));  // [0] head, [1] others
