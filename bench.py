@@ -437,17 +437,19 @@ def run_native(args):
             if P:
                 lctx.add_plans(sc_p.plans)
             row = {"plans": P, "box_km": round(2 * sc_p.airspace.hi_m[0] / 1000.0, 1)}
-            pick, longest = None, (-1, 0)
+            pick, longest_acc, longest = None, (-1, 0), (-1, 0)
             lctx.set_launch(cull=1)
             for i in range(len(sc_p.t0)):
                 r = lctx.schedule(sc_p.src[i], sc_p.dst[i], int(sc_p.t0[i]), want_traj=False)
                 lctx.truncate(P)
                 longest = max(longest, (r.n_states, i))
-                if r.status == 0 and r.n_states - 1 >= min_steps:
-                    pick = i
-                    break
-            if pick is None:
-                pick = longest[1]
+                if r.status == 0:
+                    longest_acc = max(longest_acc, (r.n_states, i))
+                    if r.n_states - 1 >= min_steps:
+                        pick = i
+                        break
+            if pick is None:  # the longest accepted trip, else the longest trip
+                pick = longest_acc[1] if longest_acc[0] > 0 else longest[1]
             row["request"] = pick
             for cull in (0, 1):
                 lctx.set_launch(cull=cull)

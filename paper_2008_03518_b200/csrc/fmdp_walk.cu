@@ -1209,9 +1209,10 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         FMDP_MARK(PH_SCATTER)
       }
       // (one-CTA cluster: the pushes were plain stores of this CTA, all issued before this barrier,
-      // so a CTA barrier orders them -- the form compute-sanitizer racecheck can follow)
+      // so a CTA barrier orders them -- the form compute-sanitizer racecheck can follow; the phase
+      // is still waited, as synccheck requires of every mbarrier phase)
       if (solo) __syncthreads();
-      else mbar_wait(&s_bar[3 + p], (parX >> p) & 1u);
+      mbar_wait(&s_bar[3 + p], (parX >> p) & 1u);
       parX ^= 1u << p;
       FMDP_MARK(PH_BAR1)
       // exact nearest-plan d^2 of state k over the whole row (Sec IV.I): min of the slice minima
@@ -1407,7 +1408,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         }
         FMDP_MARK(PH_OWNER)
         if (solo) __syncthreads();
-        else mbar_wait(&s_bar[5 + p], (parX >> (2 + p)) & 1u);
+        mbar_wait(&s_bar[5 + p], (parX >> (2 + p)) & 1u);
         parX ^= 1u << (2 + p);
         if (XP) stay_all = ctl->xstay[p];  // over the ranks, from CTA 0
         FMDP_MARK(PH_BAR2)
