@@ -100,3 +100,23 @@ def test_wide_rejects_what_it_does_not_support(F):
         ctx.schedule_departures(fs.m2u([0, 0, 100]), fs.m2u([500, 0, 100]), 0, [0, 10])
     assert ctx.cosim_max() == 0
     ctx.close()
+
+
+def test_wide_culled_bit_identical(F):
+    """SURVEY f1 culling inside the wide walker: every step and trajectory bit-identical."""
+    sc = _scenario(95, 200, {}, n_requests=2, half_m=1500.0, n_buildings=10, max_steps=300, t0_max=30)
+    outs = []
+    for cull in (0, 1):
+        ctx = F.FMDP(sc.airspace, sc.terrain, device=0)
+        ctx.add_plans(sc.plans)
+        ctx.set_launch(cull=cull)
+        steps = [ctx.eval_step(q, psi, g, K, speed=300) for q, psi, g, K in fs.random_states(96, sc, 3)]
+        res = ctx.schedule_batch(sc.src, sc.dst, sc.t0)
+        outs.append((steps, res, [ctx.speeds(i) for i in range(len(res))]))
+        ctx.close()
+    for a, b in zip(outs[0][0], outs[1][0]):
+        assert (a["v"] == b["v"]).all() and (a["vstar"] == b["vstar"]).all() and a["a_star"] == b["a_star"]
+    for x, y in zip(outs[0][1], outs[1][1]):
+        assert x.status == y.status and x.n_states == y.n_states and (x.traj == y.traj).all()
+    for p, q in zip(outs[0][2], outs[1][2]):
+        assert (p == q).all()
