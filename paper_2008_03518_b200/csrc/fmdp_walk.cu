@@ -915,17 +915,46 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
             n0 = c8[0];
             n1 = c8[1];
           }
-          for (int pp = grp; pp < npf; pp += NGW, c8 += cstep) {
-            ulonglong2 e[10];
-            e[0] = n0;
-            e[1] = n1;
+          if constexpr (C >= 10) {
+            // ten climbs per thread (wide walker): 50 running minima leave no room for all ten
+            // records of a pair, so the loop streams them tau by tau -- the next tau's two records
+            // load while this tau's 21 instructions (2 + 9 FFMA2, 10 FMNMX3) run
+            for (int pp = grp; pp < npf; pp += NGW, c8 += cstep) {
+              ulonglong2 r0 = n0, r1 = n1;
 #pragma unroll
-            for (int i = 2; i < 10; ++i) e[i] = c8[i];
-            if (pp + NGW < npf) {
-              n0 = c8[cstep];
-              n1 = c8[cstep + 1];
+              for (int t_ = 0; t_ < NTAU; ++t_) {
+                ulonglong2 q0 = r0, q1 = r1;
+                if (t_ + 1 < NTAU) {
+                  q0 = c8[2 * t_ + 2];
+                  q1 = c8[2 * t_ + 3];
+                } else if (pp + NGW < npf) {
+                  q0 = c8[cstep];
+                  q1 = c8[cstep + 1];
+                }
+                f2 hh = fma2(sx2, r0.x, r1.y);
+                hh = fma2(sy2, r0.y, hh);
+#pragma unroll
+                for (int cc_ = 0; cc_ < C; ++cc_)
+                  m[cc_][t_] = min3(m[cc_][t_], (ZM && cc_ == C / 2) ? hh : fma2(sz2[cc_], r1.x, hh));
+                r0 = q0;
+                r1 = q1;
+              }
+              n0 = r0;
+              n1 = r1;
             }
-            FMDP_PAIR(e)
+          } else {
+            for (int pp = grp; pp < npf; pp += NGW, c8 += cstep) {
+              ulonglong2 e[10];
+              e[0] = n0;
+              e[1] = n1;
+#pragma unroll
+              for (int i = 2; i < 10; ++i) e[i] = c8[i];
+              if (pp + NGW < npf) {
+                n0 = c8[cstep];
+                n1 = c8[cstep + 1];
+              }
+              FMDP_PAIR(e)
+            }
           }
           if ((ns & 1) && npf % NGW == grp) {  // odd tail: the partner slot is a well at infinity
             const ulonglong2* t8 = cen2 + (PAIR_STRIDE / 4) * npf;
