@@ -1164,8 +1164,9 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           }
         }
       }
-      if (!fin && k + 1 > tc_end) {  // the rescanned list takes over at step k+1; the old one is
-        if (tid == 0) ctl->ntc[tcb] = 0;  // consumed (FIX precedes the barriers above)
+      int tc_free = -1;  // the list consumed by this step's FIX: its counter is reset after the
+      if (!fin && k + 1 > tc_end) {  // next CTA barrier (a step with an empty row slice has no
+        tc_free = tcb;               // barrier between the FIX and this point: racecheck)
         tcb ^= 1;
         tc_end = k + 1 + TC_WIN;
       }
@@ -1216,6 +1217,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       if (tid == 0) {  // step k+1's counters: every warp has left step k-1 (this barrier)
         ctl->namb[p ^ 1] = 0;
         ctl->stay_local[p ^ 1] = w.sat_d2;
+        if (tc_free >= 0) ctl->ntc[tc_free] = 0;  // every thread has finished this step's FIX
       }
       // slice separation minimum -> every CTA; reduce-scatter of the per-action blocks into the
       // owner CTA (a mod G): DSMEM pushes completing on the receiver's mbarrier of this parity
