@@ -66,6 +66,8 @@ enum {
   FMDP_E_RANGE = -7,     /* position outside the airspace / 2^24-unit span, or a plan   */
                          /* running past horizon_steps, or |velocity| beyond packing    */
   FMDP_E_NODEV = -8,     /* no sm_100 device                                            */
+  FMDP_E_IO = -9,        /* plan-store file could not be opened / read / written, or is */
+                         /* not a plan-store file (fmdp_save_plans / fmdp_load_plans)   */
   FMDP_E_INTERNAL = -99
 };
 
@@ -364,6 +366,19 @@ fmdp_status fmdp_num_plans(const fmdp_ctx* ctx, uint32_t* n);
 
 /* Remove every plan with id >= n_plans (restores the store of an earlier moment). */
 fmdp_status fmdp_truncate(fmdp_ctx* ctx, uint32_t n_plans);
+
+/* Plan-store persistence (the accepted flight plans are "loaded from a file" at start-up and
+ * every newly accepted plan is added to it).  fmdp_save_plans writes plans
+ * [first_id, num_plans) in id order to `path` (created / truncated); fmdp_load_plans appends every
+ * plan of the file to the store through fmdp_add_plans (same validation: E_RANGE / E_CAPACITY leave
+ * the plans before the offending chunk committed) and returns the first new id in *first_id (may be
+ * NULL).  File layout, little-endian: "FMDPPLN1" (8 bytes), uint32 version = 1, uint32 reserved = 0,
+ * uint64 n_plans; then per plan: uint64 aircraft_id, int64 t0_step, int32 n, int32 reserved = 0,
+ * n x {int32 x, y, z} (the quantised states, u = 2^-6 m).  Positions are stored in units, so a file
+ * loads into any context whose airspace and horizon contain them.  Errors: E_ARG (null ctx/path,
+ * first_id > num_plans), E_IO (open / short read / write failure / bad magic or version). */
+fmdp_status fmdp_save_plans(const fmdp_ctx* ctx, const char* path, uint32_t first_id);
+fmdp_status fmdp_load_plans(fmdp_ctx* ctx, const char* path, uint32_t* first_id);
 
 /* One decision step at (pos, heading) for goal `goal` at clock row `clock_step`, run by
  * the same device code as fmdp_schedule (parity / debug hook; V mirrors Table DS "V",

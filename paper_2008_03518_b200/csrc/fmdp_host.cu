@@ -137,7 +137,7 @@ namespace {
 thread_local std::string g_create_error = "";  // reason of this thread's last failed fmdp_create
 
 const char* kStatusText[] = {"ok", "invalid argument", "out of memory", "CUDA error", "row capacity exceeded",
-                             "duplicate", "buffer too small", "out of range", "no sm_100 device"};
+                             "duplicate", "buffer too small", "out of range", "no sm_100 device", "plan-store file I/O error"};
 
 fmdp_status fail(fmdp_ctx* c, fmdp_status s, const std::string& msg) {
   if (c) c->err = msg;
@@ -2085,6 +2085,68 @@ fmdp_status fmdp_truncate(fmdp_ctx* ctx, uint32_t n_plans) {
                      ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return FMDP_OK;
+}
+
+namespace {
+const char kStoreMagic[8] = {'F', 'M', 'D', 'P', 'P', 'L', 'N', '1'};
+struct FileCloser {
+  FILE* f;
+  ~FileCloser() {
+    if (f) std::fclose(f);
+  }
+};
+}  // namespace
+
+fmdp_status fmdp_save_plans(const fmdp_ctx* ctx, const char* path, uint32_t first_id) {
+  if (!ctx || !path || first_id > ctx->plans.size()) return FMDP_E_ARG;
+  fmdp_ctx* c = const_cast<fmdp_ctx*>(ctx);  // only for the error text
+  FileCloser fc{std::fopen(path, "wb")};
+  if (!fc.f) return fail(c, FMDP_E_IO, std::string("cannot create ") + path);
+  const uint32_t ver[2] = {1u, 0u};
+  const uint64_t np = ctx->plans.size() - first_id;
+  bool ok = std::fwrite(kStoreMagic, 1, 8, fc.f) == 8 && std::fwrite(ver, 4, 2, fc.f) == 2 &&
+            std::fwrite(&np, 8, 1, fc.f) == 1;
+  for (size_t i = first_id; ok && i < ctx->plans.size(); ++i) {
+    const PlanRec& p = ctx->plans[i];
+    const int32_t n[2] = {(int32_t)(p.states.size() / 3), 0};
+    ok = std::fwrite(&p.aircraft, 8, 1, fc.f) == 1 && std::fwrite(&p.t0, 8, 1, fc.f) == 1 &&
+         std::fwrite(n, 4, 2, fc.f) == 2 &&
+         std::fwrite(p.states.data(), 4, p.states.size(), fc.f) == p.states.size();
+  }
+  ok = ok && std::fflush(fc.f) == 0;
+  return ok ? FMDP_OK : fail(c, FMDP_E_IO, std::string("write failed: ") + path);
+}
+
+fmdp_status fmdp_load_plans(fmdp_ctx* ctx, const char* path, uint32_t* first_id) {
+  if (!ctx || !path) return fail(ctx, FMDP_E_ARG, "null argument");
+  FileCloser fc{std::fopen(path, "rb")};
+  if (!fc.f) return fail(ctx, FMDP_E_IO, std::string("cannot open ") + path);
+  char magic[8];
+  uint32_t ver[2];
+  uint64_t np = 0;
+  if (std::fread(magic, 1, 8, fc.f) != 8 || std::memcmp(magic, kStoreMagic, 8) != 0 ||
+      std::fread(ver, 4, 2, fc.f) != 2 || ver[0] != 1u || std::fread(&np, 8, 1, fc.f) != 1)
+    return fail(ctx, FMDP_E_IO, std::string("not a version-1 plan-store file: ") + path);
+  std::vector<uint64_t> ids;
+  std::vector<int64_t> t0;
+  std::vector<int32_t> n, st;
+  for (uint64_t i = 0; i < np; ++i) {
+    uint64_t id;
+    int64_t t;
+    int32_t nn[2];
+    if (std::fread(&id, 8, 1, fc.f) != 1 || std::fread(&t, 8, 1, fc.f) != 1 || std::fread(nn, 4, 2, fc.f) != 2 ||
+        nn[0] < 1 || nn[0] > (1 << 24))
+      return fail(ctx, FMDP_E_IO, std::string("truncated or corrupt plan record in ") + path);
+    const size_t off = st.size();
+    st.resize(off + 3 * (size_t)nn[0]);
+    if (std::fread(st.data() + off, 4, 3 * (size_t)nn[0], fc.f) != 3 * (size_t)nn[0])
+      return fail(ctx, FMDP_E_IO, std::string("truncated plan states in ") + path);
+    ids.push_back(id);
+    t0.push_back(t);
+    n.push_back(nn[0]);
+  }
+  return fmdp_add_plans(ctx, (int32_t)np, ids.data(), t0.data(), n.data(),
+                        reinterpret_cast<const fmdp_qpos*>(st.data()), first_id);
 }
 
 fmdp_status fmdp_eval_step(fmdp_ctx* ctx, fmdp_qpos pos, int32_t heading, fmdp_qpos goal, int64_t clock_step,

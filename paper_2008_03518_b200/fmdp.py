@@ -114,7 +114,7 @@ EXPORTS = ["fmdp_airspace_default", "fmdp_create", "fmdp_destroy", "fmdp_set_lau
            "fmdp_schedule_departures", "fmdp_schedule_cosim", "fmdp_cosim_max", "fmdp_get_steplog", "fmdp_get_plan",
            "fmdp_num_plans", "fmdp_truncate", "fmdp_eval_step", "fmdp_get_stats", "fmdp_num_actions",
            "fmdp_strerror", "fmdp_last_error", "fmdp_set_trace", "fmdp_get_trace", "fmdp_get_speeds",
-           "fmdp_eval_step_v", "fmdp_schedule_batch_dist"]
+           "fmdp_eval_step_v", "fmdp_schedule_batch_dist", "fmdp_save_plans", "fmdp_load_plans"]
 
 _lib = None
 
@@ -155,6 +155,8 @@ def lib():
         L.fmdp_get_plan.argtypes = [vp, C.c_uint32, C.POINTER(i64), vp, i32, C.POINTER(i32)]
         L.fmdp_num_plans.argtypes = [vp, C.POINTER(C.c_uint32)]
         L.fmdp_truncate.argtypes = [vp, C.c_uint32]
+        L.fmdp_save_plans.argtypes = [vp, C.c_char_p, C.c_uint32]
+        L.fmdp_load_plans.argtypes = [vp, C.c_char_p, C.POINTER(C.c_uint32)]
         L.fmdp_eval_step.argtypes = [vp, QPos, i32, QPos, i64, vp, vp, vp, vp, vp, vp]
         L.fmdp_eval_step_v.argtypes = [vp, QPos, i32, i32, QPos, i64, vp, vp, vp, vp, vp, vp]
         L.fmdp_get_stats.argtypes = [vp, C.POINTER(Stats)]
@@ -338,6 +340,16 @@ class FMDP:
 
     def truncate(self, n_plans: int):
         self._check(self.L.fmdp_truncate(self.ctx, int(n_plans)), "fmdp_truncate")
+
+    def save_plans(self, path, first_id: int = 0):
+        """Write plans [first_id, num_plans) to `path` (include/fmdp.h fmdp_save_plans)."""
+        self._check(self.L.fmdp_save_plans(self.ctx, os.fsencode(path), int(first_id)), "fmdp_save_plans")
+
+    def load_plans(self, path) -> int:
+        """Append every plan of a plan-store file; returns the first new plan id."""
+        fid = C.c_uint32()
+        self._check(self.L.fmdp_load_plans(self.ctx, os.fsencode(path), C.byref(fid)), "fmdp_load_plans")
+        return int(fid.value)
 
     # ------------------------------------------------------------------ requests
     def _vec(self, q_units):

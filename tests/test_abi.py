@@ -88,3 +88,13 @@ def test_pack_plans_layout():
     assert t0.tolist() == [5, 0, 12] and n.tolist() == [2, 1, 3]
     assert st.shape == (6, 3) and st.flags["C_CONTIGUOUS"]
     assert (st[:2] == plans[0][1]).all() and (st[2] == [7, 8, 9]).all() and (st[3:] == plans[2][1]).all()
+
+
+def test_store_file_errors_without_gpu(tmp_path):
+    """fmdp_save_plans / fmdp_load_plans argument errors need no device (include/fmdp.h)."""
+    import ctypes as C
+    from paper_2008_03518_b200 import fmdp as F
+    L = F.lib()
+    assert L.fmdp_strerror(-9).decode() == "plan-store file I/O error"
+    assert L.fmdp_save_plans(None, str(tmp_path / "x").encode(), 0) == -1
+    assert L.fmdp_load_plans(None, str(tmp_path / "x").encode(), None) == -1
