@@ -87,7 +87,8 @@ typedef struct fmdp_airspace {
   double speed;                    /* constant ground speed v0, m/s; v0*dt/u integral    */
   int32_t heading_lattice;         /* H_L headings, divisible by 8 (R14)                 */
   int32_t n_turn;                  /* <= 32                                              */
-  const int32_t* turn_steps;       /* lattice steps per substep, ascending               */
+  const int32_t* turn_steps;       /* lattice steps per substep, ascending; |step| * window
+                                      < heading_lattice (FMDP_E_ARG otherwise)            */
   int32_t n_climb;                 /* 1, 3 or 5                                          */
   const int32_t* climb_units;      /* z units per substep, ascending                     */
   double goal_r, goal_gamma;       /* 200, 0.999 (Table PK, R8)                    */

@@ -166,15 +166,15 @@ inline size_t x_area_bytes(int world, int slot) {
 }
 
 // Shared-memory carve-up, identical on host (size) and device (offsets).
-//   BLK: per-action block of the reduce-scatter = W*NTAU (state, tau) minima, padded to float4.
 struct Layout {
-  int HL, CH, RAWCAP, NT, C, NCOL, A, AW, G, BLK, NOWN, RAWW;
+  int HL, CH, RAWCAP, NT, C, NCOL, A, AW, G, WT, BLK, NOWN, RAWW;
   size_t o_dxy, o_tw, o_raw, o_cen, o_stage, o_recv, o_pos, o_fix, o_sfix, o_vT, o_mI, o_vstar, o_vsc, o_conf,
       o_confg, o_flags, o_stay, o_amb, o_tc, o_bar, o_ctl, o_M, total;
   __host__ __device__ static size_t al(size_t x) { return (x + 15) & ~size_t(15); }
   __host__ __device__ void build(int hl, int ch, int rawcap, int nt, int c, int ncol, int a, int aw, int g) {
     HL = hl; CH = ch; RAWCAP = rawcap; NT = nt; C = c; NCOL = ncol; A = a; AW = aw; G = g;
-    BLK = ((AW / A) * NTAU + 3) & ~3;
+    WT = (AW / A) * NTAU;               // (state, tau) items of one action
+    BLK = (WT + 3) & ~3;                // per-action block of the reduce-scatter, padded to 16 B
     NOWN = (A + G - 1) / G;             // max actions owned by one CTA
     RAWW = RAWCAP + 8;                  // words per SoA array in one raw row buffer
     size_t o = 0;
@@ -183,7 +183,9 @@ struct Layout {
     o_raw = o;  o = al(o + sizeof(int32_t) * 4 * RAWW * 3);
     size_t cen = sizeof(float) * PAIR_STRIDE * ((CH + 1) / 2);  // plan-pair well records
     o_cen = o;  o = al(o + cen);
-    o_stage = o; o = al(o + sizeof(float) * (size_t)A * BLK);
+    // reduce-scatter: the CTA's per-action minima staged by owner CTA ([owner][slot][BLK], one
+    // contiguous run per owner = one bulk DSMEM copy), received per source CTA and step parity
+    o_stage = o; o = al(o + sizeof(float) * (size_t)G * NOWN * BLK);
     o_recv = o; o = al(o + sizeof(float) * 2 * (size_t)G * NOWN * BLK);
     o_pos = o;  o = al(o + sizeof(int4) * 2 * AW);   // double-buffered by step parity
     o_fix = o;  o = al(o + sizeof(double) * AW);
@@ -200,7 +202,7 @@ struct Layout {
     o_tc = o;   o = al(o + sizeof(int32_t) * 2 * TC_MAX);  // candidate lists, by step parity
     o_bar = o;  o = al(o + sizeof(uint64_t) * 8);   // 3 TMA ring + 2 reduce-scatter + 2 V* mbarriers
     o_ctl = o;  o = al(o + 512);
-    o_M = o;    o = al(o + sizeof(float) * (size_t)NOWN * BLK);  // owner pass: in-radius minima of the owned items
+    o_M = o;    o = al(o + sizeof(float) * (size_t)NOWN * WT);  // owner pass: in-radius minima of the owned items
     total = o;
   }
 };

@@ -1120,7 +1120,8 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   if (a.heading_lattice < 8 || a.heading_lattice % 8) return bad(FMDP_E_ARG, "heading_lattice % 8");
   if (a.n_turn < 1 || a.n_turn > fmdp::MAX_TURN || !a.turn_steps) return bad(FMDP_E_ARG, "turns");
   for (int i = 0; i < a.n_turn; ++i)
-    if (std::abs(a.turn_steps[i]) >= a.heading_lattice) return bad(FMDP_E_ARG, "turn step beyond the lattice");
+    if ((int64_t)std::abs(a.turn_steps[i]) * a.window >= a.heading_lattice)  // the kernel wraps psi + t h once
+      return bad(FMDP_E_ARG, "turn step x window beyond the lattice");
   if (a.n_acc < 1 || a.n_acc > fmdp::MAX_ACC || !a.acc_units) return bad(FMDP_E_ARG, "n_acc / acc_units");
   const bool wide = a.n_acc > 1 || a.acc_units[0] != 0 || a.speed_min > 0 || a.speed_max > 0;
   if (!a.climb_units || (wide ? !(a.n_climb == 3 || a.n_climb == 10)

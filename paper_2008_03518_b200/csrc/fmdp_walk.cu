@@ -33,6 +33,9 @@ namespace cg = cooperative_groups;
 namespace fmdp {
 
 // ----------------------------------------------------------------------------- PTX helpers
+#ifndef FMDP_MBAR_SUSPEND_NS
+#define FMDP_MBAR_SUSPEND_NS 1000000
+#endif
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -43,8 +46,12 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+// try_wait with a suspend-time hint: a waiting thread sleeps until the phase completes (or the hint
+// elapses) instead of re-polling, so warps that wait do not take issue slots from the warps of
+// their SM sub-partition that still work (the owner pass, the decision)
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
+#if FMDP_MBAR_SUSPEND_NS == 0
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -53,6 +60,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(addr),
       "r"(parity)
+      : "memory");
+  return;
+#endif
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity), "r"(FMDP_MBAR_SUSPEND_NS)
       : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -83,6 +101,18 @@ __device__ __forceinline__ void st_async_d2(uint32_t ra, double a, double b, uin
                "d"(b), "r"(rbar)
                : "memory");
 }
+// DSMEM bulk copy (sm_90+): one cp.async.bulk of a contiguous shared-memory run into a cluster CTA's
+// shared memory, completing its bytes on that CTA's mbarrier -- the reduce-scatter sends one copy
+// per owner CTA instead of one 16-byte st.async per float4 (the SM's remote-store issue rate, not
+// the bytes, was the exchange's cost).  Source reads complete per bulk group (wait_read before reuse).
+__device__ __forceinline__ void bulk_s2c(uint32_t dst_cluster, uint32_t src, uint32_t bytes, uint32_t bar_cluster) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   dst_cluster),
+               "r"(src), "r"(bytes), "r"(bar_cluster)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 // The same pushes for a one-CTA cluster (G = 1): DSMEM accesses (mapa / st.async) need a cluster
 // of at least two CTAs (compute-sanitizer memcheck, profiles/r02_sanitizer.md), so the value is a
 // plain shared store, released to the waiting threads by a CTA fence, and its bytes are completed
@@ -100,14 +130,7 @@ __device__ __forceinline__ void push_u32(bool solo, uint32_t a, unsigned dst, ui
     st_async_u32(mapa_u32(a, dst), v, mapa_u32(bar, dst));
   }
 }
-__device__ __forceinline__ void push_f4(bool solo, uint32_t a, unsigned dst, float4 v, uint32_t bar) {
-  if (solo) {
-    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
-    complete_tx_local(bar, 16);
-  } else {
-    st_async_f4(mapa_u32(a, dst), v, mapa_u32(bar, dst));
-  }
-}
+
 __device__ __forceinline__ void push_d2(bool solo, uint32_t a, unsigned dst, double x, double y, uint32_t bar) {
   if (solo) {
     asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(x), "d"(y) : "memory");
@@ -617,19 +640,18 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   int32_t* s_tc2 = reinterpret_cast<int32_t*>(smem + L.o_tc);
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + L.o_bar);
   Ctl* ctl = reinterpret_cast<Ctl*>(smem + L.o_ctl);
-  const int RAWW = L.RAWW, BLK = L.BLK, NOWN = L.NOWN;
+  const int RAWW = L.RAWW, WT = L.WT, BLK = L.BLK, NOWN = L.NOWN;
   const int4* tw = (w.n_tw <= TW_SMEM) ? s_tw : w.tw;
-  // reduce-scatter element of this thread (i = tid): action, float4 index, owner, offsets --
-  // fixed for the launch, so no integer divisions on the step's critical path
-  const int SC_NV = BLK / 4;
-  int sc_src = 0, sc_dst = 0;
-  unsigned sc_own = 0;
-  if (tid < A * SC_NV) {
-    const int a = tid / SC_NV, e = tid % SC_NV;
-    sc_own = (unsigned)(a % (int)G);
-    sc_src = a * BLK + 4 * e;
-    sc_dst = ((int)rank * NOWN + a / (int)G) * BLK + 4 * e;
-  }
+  // Per-thread step constants, fixed for the launch, so that no runtime integer division sits on
+  // the step's critical path: the owner pass-1 item i = tid + j*NT as (owned action oa, item r2 of
+  // its W*NTAU) and the goal/terrain item (owned action, substep) of the FIX loop, both advanced
+  // round by round without dividing.
+  const int p1_oa0 = tid / WT, p1_r20 = tid - p1_oa0 * WT;
+  const int p1_da = NT / WT, p1_dr = NT - p1_da * WT;
+  const int fx_i0 = (2 * NT - 33 - tid) % NT;  // the second-last warp first (see the FIX loop)
+  const int fx_oa0 = fx_i0 / W, fx_l0 = fx_i0 - fx_oa0 * W;
+  const int fx_da = NT / W, fx_dl = NT - fx_da * W;
+  const int col_l = col_t - 1;  // this column's substep index (col % W for col < NCOL)
   // plan-sharded multi-GPU step: xmode 1 exports this GPU's per-(state, tau)
   // minima and nearest-plan distance, xmode 2 imports their all-reduced minimum and decides
   // MODE 2: in-kernel exchange with the peer GPUs (xmode 3), no host round-trip per step;
@@ -786,11 +808,15 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
     cluster.sync();
 
     // ------------------------------------------------------------ step loop
+    int bK = (int)((rq.t0 + k) % 3);  // ring buffer of row K = t0 + k (advanced with k, no 64-bit modulo per step)
     for (;;) {
       if (prof) tmark = clock64();
       const int64_t K = rq.t0 + k;
       const int p = k & 1;
-      const int bK = (int)(K % 3), bK2 = (int)((K + 2) % 3);
+      const int bK2 = bK == 0 ? 2 : bK - 1;  // (K + 2) % 3
+      // the previous step's reduce-scatter copies (threads < G) must have read s_stage before this
+      // step stages into it again (long done: the owner pass and the V* exchange came in between)
+      if (!solo && tid < (int)G) bulk_wait_read();
       int4* s_pos = s_pos2 + p * AW;
       // fan origin of this step's projected states (hot-loop formulation)
       const int ox = (W >> 1) * s_dxy[psi].x, oy = (W >> 1) * s_dxy[psi].y;
@@ -956,7 +982,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
               FMDP_PAIR(e)
             }
           }
-          if ((ns & 1) && npf % NGW == grp) {  // odd tail: the partner slot is a well at infinity
+          if ((ns & 1) && (npf & (NGW - 1)) == grp) {  // odd tail (NGW a power of two): partner = a well at infinity
             const ulonglong2* t8 = cen2 + (PAIR_STRIDE / 4) * npf;
             ulonglong2 e[10];
 #pragma unroll
@@ -996,7 +1022,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           return npr;
         };
 
-        const int n_chunks = xmode != 2 ? (n + SC - 1) / SC : 0;
+        const int n_chunks = xmode == 2 ? 0 : (n <= SC ? (n > 0 ? 1 : 0) : (n + SC - 1) / SC);
         // the first chunk's well records are built BEFORE the projection: the build needs only q,
         // the fan origin and row K (staged two steps ahead), so it overlaps the projection's
         // table load, and the projection barrier also publishes the records (one CTA barrier less)
@@ -1045,8 +1071,8 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
             const int2 cum = __ldg(&w.proj[((size_t)psi * w.n_turn + it) * W + (t - 1)]);
             x = qx + cum.x;
             y = qy + cum.y;
-            ps = (psi + t * h) % w.HL;
-            ps += ps < 0 ? w.HL : 0;
+            ps = psi + t * h;  // |t h| < HL (checked by the host): one wrap at most
+            ps += ps < 0 ? w.HL : (ps >= w.HL ? -w.HL : 0);
           }
           // offsets from the fan origin o = q + (W/2) (DX, DY)[psi], doubled: the hot loop
           // evaluates |s - c|^2 - |s - o|^2 = Q + 2 (s - o).X with X = o - c, Q = |X|^2
@@ -1080,8 +1106,14 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           //      I/O thread's warp were the step's last arrivals)
           const int ntc = ctl->ntc[tcb];
           const int32_t* s_tc = s_tc2 + tcb * TC_MAX;
-          for (int i = (2 * NT - 33 - tid) % NT; i < n_own * W; i += NT) {
-            const int st = ((int)rank + (i / W) * (int)G) * W + i % W;
+          for (int i = fx_i0, foa = fx_oa0, fl_ = fx_l0; i < n_own * W; i += NT) {
+            const int st = ((int)rank + foa * (int)G) * W + fl_;
+            foa += fx_da;
+            fl_ += fx_dl;
+            if (fl_ >= W) {
+              fl_ -= W;
+              ++foa;
+            }
             const int4 q4 = s_pos[st];
             // fp64: exact integer d^2 < 2^52, correctly rounded sqrt, exp2 within an ulp
             // -- agrees with the oracle's pow to ~1e-15, so the level / climb near-ties of the goal
@@ -1124,7 +1156,8 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           }
           ctl->nsurv[((k + 1) & 1) * 2] = 0;  // step k+1, chunk 0 (last used in step k-1)
           const uint32_t bytesA = (xmode != 2 ? 4u * G : 0u) +
-                                  ((!fin && xmode != 2) ? (uint32_t)(4 * G * n_own * BLK) : 0u) + (args.stop ? 4u : 0u);
+                                  ((!fin && xmode != 2 && !solo) ? (uint32_t)(4 * G * n_own * BLK) : 0u) +
+                                  (args.stop ? 4u : 0u);
           mbar_arrive_tx(&s_bar[3 + p], bytesA);
           if (!fin) mbar_arrive_tx(&s_bar[5 + p], (uint32_t)(16 * A) + (XP ? 4u : 0u));
           if (args.stop && rank == 0) {  // one reading for the whole cluster
@@ -1178,8 +1211,8 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
 
       if (!fin) {
         // terrain / goal flags of every action's Delta_1 (the candidate next state)
-        if (grp == 0 && col < NCOL && col % W == 0) {
-          const int it = col / W;
+        if (grp == 0 && col < NCOL && col_l == 0) {
+          const int it = col_it;
           cp_async_wait_all();
           const int hgt = ctl->hgt[it];
 #pragma unroll
@@ -1190,8 +1223,8 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           }
         }
         FMDP_MARK(PH_FLAGS)
-        // group minimum inside the warp, then per-action blocks [t][tau] in s_stage
-        // (rounds over all C*NTAU values are unrolled so the shuffles overlap)
+        // group minimum inside the warp (rounds over all C*NTAU values are unrolled so the shuffles
+        // overlap), then the per-action blocks [t][tau] staged by owner CTA: s_stage[a mod G][a / G]
         if (CPW <= 8) {
 #pragma unroll
           for (int c = 0; c < C; ++c)
@@ -1205,11 +1238,14 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
             for (int t = 0; t < NTAU; ++t) m[c][t] = fminf(m[c][t], __shfl_xor_sync(0xffffffffu, m[c][t], 16));
         }
         if (grp == 0 && col < NCOL) {
-          const int it = col / W, t1 = col % W;
 #pragma unroll
-          for (int c = 0; c < C; ++c)
+          for (int c = 0; c < C; ++c) {
+            const int a = col_it * C + c;
+            float* dst = s_stage + ((a & (int)(G - 1)) * NOWN + (a >> lgG)) * BLK + col_l * NTAU;
 #pragma unroll
-            for (int t = 0; t < NTAU; ++t) s_stage[(it * C + c) * BLK + t1 * NTAU + t] = m[c][t];
+            for (int t = 0; t < NTAU; ++t) dst[t] = m[c][t];
+          }
+          if (!solo) fence_proxy_async();  // staged blocks -> the bulk copies' (async proxy) reads
         }
         FMDP_MARK(PH_STAGE)
       }
@@ -1219,25 +1255,21 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         ctl->stay_local[p ^ 1] = w.sat_d2;
         if (tc_free >= 0) ctl->ntc[tc_free] = 0;  // every thread has finished this step's FIX
       }
-      // slice separation minimum -> every CTA; reduce-scatter of the per-action blocks into the
-      // owner CTA (a mod G): DSMEM pushes completing on the receiver's mbarrier of this parity
+      // slice separation minimum -> every CTA; reduce-scatter: thread o sends the run of owner o's
+      // blocks as ONE bulk copy into s_recv[p][rank] of CTA o (completing on its mbarrier of this
+      // parity; G = 1: the owner pass reads s_stage in place)
       const uint32_t barA = smem_u32(&s_bar[3 + p]);
-      if (xmode != 2 && tid < (int)G)
+      if (xmode != 2 && tid < (int)G) {
         push_u32(solo, smem_u32(&s_stay[p * 16 + rank]), tid, ctl->stay_local[p], barA);
-      if (!fin && xmode != 2) {
-        const uint32_t recv_p = smem_u32(s_recv) + 4u * (uint32_t)(p * (int)G * NOWN * BLK);
-        for (int i = tid, j = 0; i < A * SC_NV; i += NT, ++j) {
-          int src = sc_src, dst = sc_dst;
-          unsigned own = sc_own;
-          if (j) {  // only when A * BLK / 4 > threads (A = 85)
-            const int a = i / SC_NV, e = i % SC_NV;
-            own = (unsigned)(a % (int)G);
-            src = a * BLK + 4 * e;
-            dst = ((int)rank * NOWN + a / (int)G) * BLK + 4 * e;
+        if (!fin && !solo) {
+          const int n_own_o = (A > tid) ? (A - tid + (int)G - 1) >> lgG : 0;
+          if (n_own_o > 0) {
+            const uint32_t src = smem_u32(s_stage + tid * NOWN * BLK);
+            const uint32_t dst = smem_u32(s_recv + ((p * (int)G + (int)rank) * NOWN) * BLK);
+            bulk_s2c(mapa_u32(dst, tid), src, (uint32_t)(4 * n_own_o * BLK), mapa_u32(barA, tid));
+            bulk_commit();
           }
-          push_f4(solo, recv_p + 4u * dst, own, *reinterpret_cast<const float4*>(s_stage + src), barA);
         }
-        FMDP_MARK(PH_SCATTER)
       }
       // (one-CTA cluster: the pushes were plain stores of this CTA, all issued before this barrier,
       // so a CTA barrier orders them -- the form compute-sanitizer racecheck can follow; the phase
@@ -1281,20 +1313,26 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       if (!fin) {
         // ---- owner epilogue (half-warp per owned action, lane = substep): G-way minimum of
         //      the partial blocks, exact in/out, values (Alg 8), V*(a)
-        const float* rcv = s_recv + p * (int)G * NOWN * BLK;
+        // this step's partial blocks: [source CTA][slot][BLK] (G = 1: the CTA's own staged blocks)
+        const float* rcv = solo ? s_stage : s_recv + p * (int)G * NOWN * BLK;
         // Pass 1 (whole CTA, one owned (action, substep, tau) per thread): G-way minimum of the
         // partial blocks (multi-GPU: export / import), |s - o|^2 added back, radius test ->
         // s_M = the in-radius d^2, FLT_MAX (outside), or -1 (inside the FP32 band: exact below).
-        // s_M has its own buffer (not s_stage, which other threads of this CTA may still be reading
-        // for their pushes to other owners: no CTA barrier needed before this pass).
+        // s_M has its own buffer (the CTA's own bulk copies may still be reading s_stage).
         float* s_M = reinterpret_cast<float*>(smem + L.o_M);
         const int nitem = n_own * W * NTAU;
         if (XP) {  // this GPU's minima of the owned items -> every peer (all sends
                    // before any poll); each thread keeps its own items' minima in s_M
-          for (int i = tid; i < nitem; i += NT) {
-            const int oa = i / (W * NTAU), r2 = i - oa * (W * NTAU);
-            const int io = (((int)rank + oa * (int)G) * W + r2 / NTAU) * NTAU + r2 % NTAU;
-            const float M = gway_min(rcv + oa * BLK + r2, (int)G, NOWN * BLK);
+          for (int i = tid, oa = p1_oa0, r2 = p1_r20; i < nitem; i += NT) {
+            const int io = ((int)rank + oa * (int)G) * WT + r2;  // (state, tau) index: st * NTAU + t
+            const int oa_i = oa, r2_i = r2;
+            oa += p1_da;
+            r2 += p1_dr;
+            if (r2 >= WT) {
+              r2 -= WT;
+              ++oa;
+            }
+            const float M = gway_min(rcv + oa_i * BLK + r2_i, (int)G, NOWN * BLK);
             s_M[i] = M;
             for (int q = 0; q < args.x_world; ++q)
               if (q != xme)
@@ -1307,10 +1345,16 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
                         xtag);
           }
         }
-        for (int i = tid; i < nitem; i += NT) {
-          const int oa = i / (W * NTAU), r2 = i - oa * (W * NTAU);
-          const int l = r2 / NTAU, t = r2 - l * NTAU;
+        for (int i = tid, oa = p1_oa0, r2 = p1_r20; i < nitem; i += NT) {
+          const int l = r2 / NTAU, t = r2 - l * NTAU;  // (constant divisor: multiply-shift)
           const int st = ((int)rank + oa * (int)G) * W + l;
+          const int oa_i = oa, r2_i = r2;
+          oa += p1_da;
+          r2 += p1_dr;
+          if (r2 >= WT) {
+            r2 -= WT;
+            ++oa;
+          }
           float M;
           if (xmode == 2) {
             M = __uint_as_float(args.xbuf[st * NTAU + t]);
@@ -1328,11 +1372,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
                               x_budget(xit), M);
             }
           } else {
-#ifdef FMDP_AB_P1FIRST  // A/B timing only (wrong values): no G-way minimum
-            M = rcv[oa * BLK + r2];
-#else
-            M = gway_min(rcv + oa * BLK + r2, (int)G, NOWN * BLK);
-#endif
+            M = gway_min(rcv + oa_i * BLK + r2_i, (int)G, NOWN * BLK);
             if (xmode == 1) args.xbuf[st * NTAU + t] = __float_as_uint(M);  // this GPU's minima
           }
           const int4 q4 = s_pos[st];
@@ -1388,6 +1428,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         const int hw = tid >> 4, hl = tid & 15;
         const int n_hw = NT >> 4;
         for (int oa0 = 0; oa0 < NOWN; oa0 += n_hw) {  // uniform trip count across the CTA
+          if (oa0 + 2 * warp >= n_own) continue;     // (warp-uniform) no owned action in this warp
           const int oa = oa0 + hw;
           const int a = (int)rank + oa * (int)G;
           const bool act = oa < n_own && hl < W && a < A_tile;
@@ -1602,6 +1643,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           n_near += near ? 1 : 0;
           steps_run += 1;
           k += 1;
+          bK = bK == 2 ? 0 : bK + 1;
           qx = p1.x; qy = p1.y; qz = p1.z;
           psi = npsi;
           if (WIDE) v = p1.w >> 16;

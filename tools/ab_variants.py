@@ -63,7 +63,8 @@ def run(reps=1):
     for _ in range(reps):
         for name in VARIANTS:
             env = dict(os.environ, FMDP_LIB_VARIANT=os.path.join(ROOT, "ab", f"libfmdp_{name}.so"))
-            out = subprocess.run([sys.executable, "-c", PROBE], env=env, capture_output=True, text=True)
+            extra = ["--batch"] if "--batch" in sys.argv else []
+            out = subprocess.run([sys.executable, "-c", PROBE, *extra], env=env, capture_output=True, text=True)
             print(f"== {name}\n{out.stdout}{out.stderr[-500:] if out.returncode else ''}", flush=True)
 
 
