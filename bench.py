@@ -33,7 +33,9 @@ WORKLOAD = ("configs[1]: batch of 100 FCFS requests against 3000 accepted plans 
             "grid, 16x16 km dense urban airspace, 9 headings x 3 climbs, W=10")
 OPS_PER_PAIR = 7.0  # algorithmic FP32 ops per (state, well) pair
 EXEC_OPS_PER_PAIR = 4.0 / 3.0  # FP32 lane-ops the kernel executes per pair at 3 climbs ((2 + C - 1)/C, level climb skipped)
-LOOP_CEILING_PAIRS_PER_CLK_SM = 35.0  # isolated hot loop, C = 3 (tools/hotbench, profiles/r01_hotbench.txt: 34-36)
+LOOP_CEILING_PAIRS_PER_CLK_SM = 40.0  # isolated hot loop as the walker runs it, C = 3 with the level-climb
+# skip (tools/hotbench/hotbench2.cu V0, profiles/r02s2_rates.txt: 38.3-39.6; round 1 measured 34-36
+# without the skip)
 
 
 def parse():
@@ -896,9 +898,10 @@ def run_native(args):
                      "exec_pipe_frac": exec_tops / peak_tops, "exec_ops_per_pair": EXEC_OPS_PER_PAIR,
                      "loop_ceiling_frac": (cpairs / (walk_ms / 1e3)) / loop_ceiling if walk_ms > 0 else 0.0,
                      "loop_ceiling_pairs_per_clk_sm": LOOP_CEILING_PAIRS_PER_CLK_SM,
-                     "loop_ceiling": "isolated hot loop saturates the FMA pipe at 34-36 pairs/clk/SM (register-"
-                                     "operand FFMA2 at half the nominal lane rate; tools/hotbench, "
-                                     "profiles/r01_hotbench.txt)",
+                     "loop_ceiling": "isolated hot loop (20 FFMA2 + 15 FMNMX3 + 10 LDS.128 per plan pair) "
+                                     "at 38-40 pairs/clk/SM: the 3-register FFMA2 and the 3-input FMNMX3 share "
+                                     "operand bandwidth (0.40 warp-instructions/clk/SMSP together; "
+                                     "tools/hotbench/rates.cu + hotbench2.cu, profiles/r02s2_rates.txt)",
                      "peak_basis": f"FP32 pipe: 148 SM x 128 lanes x {peak_clock:.0f} MHz (MEASURED_PEAKS sm_max_mhz)"},
         "e2e": {"value": e2e_value, "unit": "requests/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
@@ -913,6 +916,10 @@ def run_native(args):
             "pair_evals_per_step": Mc["pairs"] / args.steps, "gpu_launches": Mc["launches"],
             "committed_pairs_per_step": cpairs_c / args.steps,
             "roofline_frac": cpairs_c * OPS_PER_PAIR / (Mc["walk_ms"] / 1e3) / 1e12 / peak_tops,
+            "rounds": Mc["st_all"][-1]["rounds"], "reruns": Mc["st_all"][-1]["reruns"],
+            "reconverged": Mc["st_all"][-1]["reconverged"],
+            "reconverged_what": "rolled-back requests whose re-walk met their previous run and took it over "
+                                "(DESIGN.md §6; tests/test_gpu_reuse.py: identical to the sequential loop)",
             "same_results_as_full": same, "clocks": Mc["clocks"]},
         "f3_departures": Md,
         "f2_cosim": Mco,

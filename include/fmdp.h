@@ -191,7 +191,8 @@ typedef struct fmdp_stats {
                            /* row wait, hot loop, stage, reduce-scatter, barrier 1,         */
                            /* owner epilogue, barrier 2, decide                             */
   int32_t split;           /* clusters that shared the last single-request walk (launch.split) */
-  int32_t pad;
+  int32_t reconverged;     /* re-walks after a rollback that met the request's previous run */
+                           /* and took it over (schedule_batch)            */
 } fmdp_stats;
 
 /* Fill *a with the defaults of DESIGN.md Appendix A (the arrays point to static storage). */

@@ -84,14 +84,28 @@ struct Req {
   int32_t slot;                 // output slot
   int32_t head;                 // 1: the earliest pending FCFS request (never paused; sets *stop when done)
   int32_t speed0;               // departure speed, units per substep (0: the airspace's speed)
+  // re-convergence after a rollback (a10): the request's previous run, kept in the
+  // backup arrays (BakRec) over [rollback step, n_old), ended with old_status at state n_old - 1;
+  // no plan committed since can influence its states >= reuse_from.  A re-walk whose state k >=
+  // reuse_from equals the old state k takes the old run from k on.  n_old = 0: off.
+  int32_t reuse_from, n_old, old_status, old_fail;
   int32_t pad;
+};
+
+// One step of a request's previous run (re-convergence backup, Req::n_old): state, decision and
+// per-step records, 32 B (the first 16 B = the state, fetched with one 16-byte cp.async).
+struct BakRec {
+  int32_t x, y, z, heading;
+  int32_t astar, stepx;
+  uint32_t stepd2;
+  int32_t ntie;
 };
 
 struct Out {
   int32_t status, n_states, fail_step, n_near_ties;  // status -1: paused (resume at n_states-1)
   int32_t n_exact, steps_run;
   uint32_t min_sep_d2;
-  int32_t pad;
+  int32_t reconv;               // 1: the walk re-converged onto the request's previous run (Req::n_old)
 };
 
 struct XPeer;
@@ -126,6 +140,7 @@ struct WalkArgs {
   int32_t* dbg_astar;           // [1]
   unsigned long long* pairs;    // hot-loop pair counter (stats)
   int32_t* stepx;               // [slot][cap] exact-fallback count of step k (zeroed by the host)
+  const BakRec* bak;            // [slot][cap] previous runs (re-convergence; Req::n_old), or null
   double2* vtrace;              // [vtrace_n][cap][A] {V*(a), S(a)} per step (fmdp_set_trace), or null
   int32_t vtrace_n;
   unsigned long long* prof;     // [PH_N] per-phase cycles of rank 0 (nullptr = off)
@@ -217,6 +232,8 @@ struct AppendPlan {
 
 struct InflPair {
   int32_t i, j;                 // request slot i, plan from slot j
+  int32_t lo, hi;               // steps of i to test: [lo, hi) (hi < 0: [0, n_states[i]))
+  int32_t bak;                  // 1: i's states from the backup of its previous run (BakRec)
 };
 
 struct InflWells {              // exact-conservative influence criterion (a10)
@@ -237,7 +254,12 @@ cudaError_t walk_max_clusters(const World& w, int n_climb, int cluster, int thre
 size_t walk_smem_bytes(const World& w, int n_climb, int threads, int chunk, int rawcap, int cluster);
 cudaError_t launch_append(int32_t* rows, int32_t row_cap, int64_t horizon, const AppendPlan* plans, int n_plans,
                           int max_n, cudaStream_t s);
-cudaError_t launch_influence(const int32_t* traj, int32_t cap, const int32_t* n_states, const int64_t* t0,
-                             const InflPair* pairs, int n_pairs, const InflWells& iw, int32_t* kfirst, cudaStream_t s);
+cudaError_t launch_influence(const int32_t* traj, const BakRec* bak, int32_t cap, const int32_t* n_states,
+                             const int64_t* t0, const InflPair* pairs, int n_pairs, const InflWells& iw, int32_t* kfirst,
+                             cudaStream_t s);
+// Backup of request slot i's steps [lo, hi) (state, decision and per-step records) into bak.
+cudaError_t launch_backup(BakRec* bak, const int32_t* traj, const int32_t* heading, const int32_t* astar,
+                          const int32_t* stepx, const uint32_t* stepd2, const int8_t* ntie, int32_t cap, int slot, int lo,
+                          int hi, cudaStream_t s);
 
 }  // namespace fmdp

@@ -73,6 +73,7 @@ struct fmdp_ctx {
   uint32_t* d_stepd2 = nullptr;
   int8_t* d_ntie = nullptr;
   int32_t* d_stepx = nullptr;  // [slot][cap] exact-fallback count per step (zeroed per call / rollback)
+  fmdp::BakRec* d_bak = nullptr;  // [slot][cap] a rolled-back request's previous run (re-convergence)
   double2* d_vtrace = nullptr; // fmdp_set_trace: [vtrace_n][cap][A] {V*(a), S(a)} per step
   int vtrace_n = 0;
   int32_t* d_queue = nullptr;
@@ -266,7 +267,7 @@ fmdp_status ensure_slots(fmdp_ctx* ctx, int n) {
              {(void**)&ctx->d_traj, 12 * cap * m, nullptr},           {(void**)&ctx->d_heading, 4 * cap * m, nullptr},
              {(void**)&ctx->d_astar, 4 * cap * m, nullptr},           {(void**)&ctx->d_stepd2, 4 * cap * m, nullptr},
              {(void**)&ctx->d_ntie, cap * m, nullptr},                {(void**)&ctx->d_stepx, 4 * cap * m, nullptr},
-             {(void**)&ctx->d_speed, 4 * cap * m, nullptr},
+             {(void**)&ctx->d_speed, 4 * cap * m, nullptr},          {(void**)&ctx->d_bak, sizeof(fmdp::BakRec) * cap * m, nullptr},
              {(void**)&ctx->d_nstates, sizeof(int32_t) * m, nullptr}, {(void**)&ctx->d_t0s, sizeof(int64_t) * m, nullptr}};
     for (B& e : b) {
       e.p = dalloc(ctx, e.bytes);
@@ -433,6 +434,7 @@ fmdp::WalkArgs make_args(fmdp_ctx* ctx, const std::vector<Req>& run, bool eval, 
   a.pairs = ctx->d_pairctr;
   a.prof = ctx->launch.profile ? ctx->d_prof : nullptr;
   a.stepx = ctx->d_stepx;
+  a.bak = ctx->d_bak;  // used only by requests with Req::n_old > 0 (batch re-walks after a rollback)
   a.speed = ctx->d_speed;
   a.wb = ctx->d_wb;
   a.werr = ctx->d_wq ? ctx->d_wq + fmdp::XMAX * 4 : nullptr;
@@ -648,19 +650,20 @@ fmdp_status commit_slots(fmdp_ctx* ctx, const std::vector<int>& slots, const std
   return FMDP_OK;
 }
 
+// First and last step of each (request i, plan j) pair that could see the plan: kf[2q], kf[2q + 1]
 fmdp_status influence(fmdp_ctx* ctx, const std::vector<InflPair>& pairs, std::vector<int32_t>& kf) {
-  kf.assign(pairs.size(), INT_MAX);
+  kf.assign(2 * pairs.size(), INT_MAX);
   if (pairs.empty()) return FMDP_OK;
   if ((int)pairs.size() > ctx->pairs_cap) {
     fmdp_status s;
-    if ((s = grow(ctx, ctx->d_pairs, pairs.size())) || (s = grow(ctx, ctx->d_kfirst, pairs.size()))) return s;
+    if ((s = grow(ctx, ctx->d_pairs, pairs.size())) || (s = grow(ctx, ctx->d_kfirst, 2 * pairs.size()))) return s;
     ctx->pairs_cap = (int)pairs.size();
   }
   CK(cudaMemcpyAsync(ctx->d_pairs, pairs.data(), sizeof(InflPair) * pairs.size(), cudaMemcpyHostToDevice,
                      ctx->stream));
-  CK(fmdp::launch_influence(ctx->d_traj, ctx->cap_states, ctx->d_nstates, ctx->d_t0s, ctx->d_pairs, (int)pairs.size(),
-                            ctx->iw, ctx->d_kfirst, ctx->stream));
-  CK(cudaMemcpyAsync(kf.data(), ctx->d_kfirst, sizeof(int32_t) * pairs.size(), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(fmdp::launch_influence(ctx->d_traj, ctx->d_bak, ctx->cap_states, ctx->d_nstates, ctx->d_t0s, ctx->d_pairs,
+                            (int)pairs.size(), ctx->iw, ctx->d_kfirst, ctx->stream));
+  CK(cudaMemcpyAsync(kf.data(), ctx->d_kfirst, sizeof(int32_t) * 2 * pairs.size(), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->stats.kernels += 1;
   return FMDP_OK;
@@ -909,6 +912,23 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
     std::vector<char> fin(n, 0);
     std::vector<int> kdone(n, 0);
     int rollbacks = 0;
+    // Re-convergence: a finished request that a commit rolls back keeps its previous
+    // run in the backup arrays; the re-walk takes that run over as soon as its state equals the old
+    // one past every influenced step (ru.from).  Commits that can influence the backup's states
+    // raise ru.from (influence pairs against the backup).  Off for request sharding, and on the
+    // full path (only the culled walker carries the check: the full batches measured no gain).
+    struct Reuse {
+      bool on = false;
+      int n_old = 0, old_status = 0, old_fail = -1, bak_lo = 0, from = 0;
+    };
+    static const bool no_reuse = std::getenv("FMDP_NO_REUSE") != nullptr;  // A/B switch
+    const bool reuse_ok = !dist && !no_reuse && ctx->launch.cull;
+    std::vector<Reuse> ru(n);
+    auto backup = [&](int i, int lo, int hi) -> fmdp_status {
+      CK(fmdp::launch_backup(ctx->d_bak, ctx->d_traj, ctx->d_heading, ctx->d_astar, ctx->d_stepx, ctx->d_stepd2,
+                             ctx->d_ntie, ctx->cap_states, i, lo, hi, ctx->stream));
+      return FMDP_OK;
+    };
     int c = 0;
     while (c < n) {
       std::vector<Req> run;
@@ -916,6 +936,12 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
         if (!fin[i] && (!dist || i % g->world == g->rank)) {  // request sharding: rank i % world
           Req r = base[i];
           r.start_k = kdone[i];
+          if (ru[i].on) {
+            r.n_old = ru[i].n_old;
+            r.reuse_from = ru[i].from;
+            r.old_status = ru[i].old_status;
+            r.old_fail = ru[i].old_fail;
+          }
           run.push_back(r);
         }
       if (!run.empty()) {
@@ -940,10 +966,13 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
       for (const Req& r : run) {
         const Out& o = ctx->h_out[r.slot];
         ctx->stats.steps += o.steps_run;
+        ctx->stats.reconverged += o.reconv;
+        if (o.reconv) ru[r.slot].on = false;  // its records are one consistent run again
         if (o.status < 0) kdone[r.slot] = o.n_states - 1;
         else {
           fin[r.slot] = 1;
           mine.push_back(r.slot);
+          ru[r.slot].on = false;
         }
       }
       if (dist && (st = gather_finished(ctx, g, mine, fin, kdone))) return st;
@@ -957,17 +986,26 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
       for (int i = 0; i < n; ++i) ns[i] = ctx->h_out[i].n_states;
       for (int j = c; j < c_end; ++j)
         if (ctx->h_out[j].status == FMDP_ACCEPTED)
-          for (int i = j + 1; i < n; ++i)  // sharded: the trajectories this rank holds
-            if (!dist || fin[i] || i % g->world == g->rank) pairs.push_back({i, j});
+          for (int i = j + 1; i < n; ++i) {  // sharded: the trajectories this rank holds
+            if (!dist || fin[i] || i % g->world == g->rank) pairs.push_back({i, j, 0, -1, 0});
+            if (ru[i].on) pairs.push_back({i, j, ru[i].bak_lo, ru[i].n_old, 1});  // i's previous run
+          }
       std::vector<int32_t> kf;
       if (!pairs.empty()) {
         CK(cudaMemcpyAsync(ctx->d_nstates, ns.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
         if ((st = influence(ctx, pairs, kf))) return st;
       }
       // pairs by request i (first influenced step kf), and the plans committed so far
-      std::vector<std::vector<std::pair<int, int>>> by_i(n);
+      std::vector<std::vector<std::pair<int, int>>> by_i(n), by_last(n), by_bak(n);
       for (size_t q = 0; q < pairs.size(); ++q)
-        if (kf[q] != INT_MAX) by_i[pairs[q].i].push_back({pairs[q].j, kf[q]});
+        if (kf[2 * q] != INT_MAX) {
+          if (pairs[q].bak) {
+            by_bak[pairs[q].i].push_back({pairs[q].j, kf[2 * q + 1]});
+          } else {
+            by_i[pairs[q].i].push_back({pairs[q].j, kf[2 * q]});
+            by_last[pairs[q].i].push_back({pairs[q].j, kf[2 * q + 1]});
+          }
+        }
       std::vector<int> newly;
       std::vector<char> is_new(n, 0);
       auto first_influence = [&](int i) {
@@ -976,9 +1014,42 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
           if (is_new[e.first]) best = std::min(best, e.second);
         return best;
       };
+      auto last_influence = [&](const std::vector<std::pair<int, int>>& v) {
+        int kl = -1;
+        for (const auto& e : v)
+          if (is_new[e.first]) kl = std::max(kl, e.second);
+        return kl;
+      };
+      // rollback of request i to step k1: keep (fin: start) or extend its previous run's backup
+      auto note_rb = [&](int i, int k1, bool finished) -> fmdp_status {
+        if (!reuse_ok) return FMDP_OK;
+        Reuse& u = ru[i];
+        const int kl = last_influence(by_last[i]);
+        if (finished || !u.on) {  // keep the run computed so far (final, or paused at n_states - 1)
+          const Out& o = ctx->h_out[i];
+          u.on = true;
+          u.n_old = o.n_states;
+          u.old_status = o.status;  // (-1: paused)
+          u.old_fail = o.fail_step;
+          u.bak_lo = k1;
+          u.from = kl + 1;
+          fmdp_status e = backup(i, k1, u.n_old);
+          if (e) return e;
+        } else {
+          if (k1 < u.bak_lo) {  // states [k1, bak_lo) are still the previous run's
+            fmdp_status e = backup(i, k1, u.bak_lo);
+            if (e) return e;
+            u.bak_lo = k1;
+          }
+          u.from = std::max(u.from, kl + 1);
+        }
+        if (u.on && u.from >= u.n_old) u.on = false;
+        return FMDP_OK;
+      };
       while (c < n && fin[c]) {
         const int k1 = first_influence(c);
         if (k1 != INT_MAX) {
+          if ((st = note_rb(c, k1, true))) return st;
           fin[c] = 0;
           kdone[c] = k1;
           ++rollbacks;
@@ -992,15 +1063,29 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
         ++c;
       }
       if ((st = commit_slots(ctx, newly, base, aircraft, plan_id))) return st;
+      if (std::getenv("FMDP_DEBUG")) {
+        int pend = 0, prog = 0;
+        for (int i = c; i < n; ++i) pend += fin[i] ? 0 : 1;
+        for (const Req& r : run) prog += ctx->h_out[r.slot].steps_run > 0 ? 1 : 0;
+        std::fprintf(stderr, "fmdp: slice head=%d head_steps=%d committed=%zu next_head=%d pending=%d progressed=%d/%zu\n",
+                     run.empty() ? -1 : run[0].slot, run.empty() ? 0 : ctx->h_out[run[0].slot].steps_run, newly.size(), c,
+                     pend, prog, run.size());
+      }
       for (int i = c; i < n; ++i) {  // includes the unfinished head c
+        if (ru[i].on) {  // commits that can see the previous run's states
+          ru[i].from = std::max(ru[i].from, last_influence(by_bak[i]) + 1);
+          if (ru[i].from >= ru[i].n_old) ru[i].on = false;
+        }
         const int k1 = first_influence(i);
         if (k1 == INT_MAX) continue;
         if (fin[i]) {
+          if ((st = note_rb(i, k1, true))) return st;
           fin[i] = 0;
           kdone[i] = k1;
           ++rollbacks;
           if ((st = clear_stepx(ctx, i, k1))) return st;
         } else if (k1 < kdone[i]) {
+          if ((st = note_rb(i, k1, false))) return st;
           kdone[i] = k1;
           ++rollbacks;
           if ((st = clear_stepx(ctx, i, k1))) return st;

@@ -34,7 +34,7 @@ namespace fmdp {
 
 // ----------------------------------------------------------------------------- PTX helpers
 #ifndef FMDP_MBAR_SUSPEND_NS
-#define FMDP_MBAR_SUSPEND_NS 1000000
+#define FMDP_MBAR_SUSPEND_NS 0  // (A/B: a try_wait suspend hint measured no gain)
 #endif
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -232,6 +232,9 @@ struct Ctl {
   int32_t cs_ok;              // scratch of cs_idle
   int32_t stop[2];            // head-finished flag seen by rank 0 at the top of the step, by parity
   uint32_t xstay[2];          // multi-GPU: nearest-plan d^2 over the ranks (from CTA 0), by parity
+  int32_t rc_near, rc_exact;  // re-convergence: near-ties / exact counts of the reused steps (rank 0)
+  uint32_t rc_min;            //                 their nearest-plan minimum (rank 0)
+  int4 bakst[2];              // re-convergence: the previous run's state k + 1, by step parity
   unsigned long long* xp[XMAX];  // multi-GPU: every rank's receive area (loaded once per launch)
   unsigned long long* xip[XNODE];  // two-level exchange: cluster xcl's area on every GPU
 };
@@ -291,6 +294,9 @@ __device__ __forceinline__ int ground_height(const World& w, int x, int y) {
 // 4-byte asynchronous global -> shared copy (LDGSTS); completion by cp.async.wait_all.
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
@@ -576,6 +582,48 @@ __device__ __noinline__ void exact_fallback_call(float* s_M, const int32_t* s_am
   exact_fallback(s_M, s_amb, s_pos, namb, nitem, rowg, nK, row_cap, rank, G, W, tk, ctl, cs_pub_K, cs_n, self, stepx_k);
 }
 
+// Re-convergence (a10): the previous run's records of steps k .. n_old - 1 (BakRec backup) back into
+// the request's arrays, and their near-tie / exact-count sums and separation minimum into rank 0's
+// Ctl (c0).  All threads of every CTA of the lead cluster; out of line (keeps the step loop small).
+// (Plain pointers: a reference to the kernel parameters would force a local copy of them.)
+struct RecPtrs {
+  int32_t *traj, *heading, *astar, *stepx;
+  uint32_t* stepd2;
+  int8_t* ntie;
+};
+__device__ __noinline__ void reconv_copy(const BakRec* bak, RecPtrs args, size_t sbase, int k, int n_old, unsigned rank,
+                                         unsigned G, uint32_t sat, Ctl* c0) {
+  const int NT = blockDim.x, tid = threadIdx.x;
+  const BakRec* bb = bak + sbase;
+  int rn = 0, rx = 0;
+  uint32_t rm = sat;
+  for (int m = k + (int)rank * NT + tid; m < n_old; m += (int)G * NT) {
+    const BakRec e = bb[m];
+    if (m > k) {
+      int32_t* tq = args.traj + 3 * (sbase + m);
+      tq[0] = e.x; tq[1] = e.y; tq[2] = e.z;
+      args.heading[sbase + m] = e.heading;
+    }
+    args.stepd2[sbase + m] = e.stepd2;
+    rm = min(rm, e.stepd2);
+    if (m < n_old - 1) {  // decision steps
+      args.astar[sbase + m] = e.astar;
+      args.ntie[sbase + m] = (int8_t)e.ntie;
+      if (args.stepx) args.stepx[sbase + m] = e.stepx;
+      rn += e.ntie;
+      rx += e.stepx;
+    }
+  }
+  rn = __reduce_add_sync(0xffffffffu, rn);
+  rx = __reduce_add_sync(0xffffffffu, rx);
+  rm = __reduce_min_sync(0xffffffffu, rm);
+  if ((tid & 31) == 0) {
+    if (rn) atomicAdd(&c0->rc_near, rn);
+    if (rx) atomicAdd(&c0->rc_exact, rx);
+    if (rm < sat) atomicMin(&c0->rc_min, rm);
+  }
+}
+
 // Per-phase cycle accounting (rank 0, thread 0), enabled when args.prof != nullptr.
 enum Phase { PH_PROJ, PH_FIX, PH_WAIT, PH_HOT, PH_STAGE, PH_SCATTER, PH_BAR1, PH_OWNER, PH_BAR2, PH_DECIDE,
              PH_TOP, PH_SCAN, PH_PLOOP, PH_BUILD, PH_OWN1, PH_ARGMAX, PH_FLAGS, PH_N };
@@ -749,6 +797,13 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
     unsigned wit = 0;  // wide walker: decision-board steps of this request (tags 1, 2, ...)
     // per-request aggregates, kept by thread 0 of rank 0
     int n_near = 0, steps_run = 0, status = 0, fail_step = -1, nex0 = 0;
+    bool reconv = false;  // the re-walk met its previous run (Req::n_old): the rest is that run's
+    // re-convergence window: decisions k with reuse_from <= k + 1 < n_old compare their next state
+    // (only the culled FCFS walker and the reference instantiation carry it: measured, the full
+    // walker's batches gain nothing from it and its step loop would grow, +1.3 % per step)
+    constexpr bool REUSE = MODE == 4 || MODE == 3;
+    const int bk_lo = (REUSE && args.bak != nullptr && rq.n_old > 0 && !evalm) ? rq.reuse_from - 1 : INT_MAX;
+    const int bk_hi = rq.n_old - 1;
     uint32_t min_sep = w.sat_d2;
     if (tid == 0) {
       // terminal flags of the starting state (terrain, goal; timeout cannot apply: k < max_steps)
@@ -760,6 +815,8 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       ctl->stay_local[0] = ctl->stay_local[1] = w.sat_d2;
       ctl->nsurv[0] = ctl->nsurv[1] = ctl->nsurv[2] = ctl->nsurv[3] = 0;
       ctl->n_exact = 0;
+      ctl->rc_near = ctl->rc_exact = 0;
+      ctl->rc_min = w.sat_d2;
       if (rank == 0 && k > 0 && !evalm) {  // resume: aggregates of the kept prefix
         for (int kk = 0; kk < k; ++kk) {
           n_near += args.ntie[sbase + kk];
@@ -814,6 +871,10 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       const int64_t K = rq.t0 + k;
       const int p = k & 1;
       const int bK2 = bK == 0 ? 2 : bK - 1;  // (K + 2) % 3
+      // re-convergence window (a10): the previous run's state k + 1 -> shared memory (one 16-byte
+      // LDGSTS, waited before the post-stage barrier), compared with the decision's next state
+      const bool bak_act = REUSE && k >= bk_lo && k < bk_hi && !fin;
+      if (bak_act && tid == NT - 2) cp_async16(&ctl->bakst[p], &args.bak[sbase + k + 1]);
       // the previous step's reduce-scatter copies (threads < G) must have read s_stage before this
       // step stages into it again (long done: the owner pass and the V* exchange came in between)
       if (!solo && tid < (int)G) bulk_wait_read();
@@ -1249,6 +1310,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         }
         FMDP_MARK(PH_STAGE)
       }
+      if (bak_act && tid == NT - 2) cp_async_wait_all();
       __syncthreads();
       if (tid == 0) {  // step k+1's counters: every warp has left step k-1 (this barrier)
         ctl->namb[p ^ 1] = 0;
@@ -1655,6 +1717,19 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
             status = -1;
             done = true;
           }
+          // re-convergence: the new state k equals the previous run's, and no plan committed since
+          // that run can influence its states from here on -- its decisions, per-step records and
+          // verdict stand (copied in the request epilogue); a previous run that had paused (status
+          // -1) pauses this one at its last state (the host resumes it from there)
+          if (bak_act) {
+            const int4 o = ctl->bakst[p];
+            if (o.x == p1.x && o.y == p1.y && o.z == p1.z && o.w == npsi) {
+              reconv = true;
+              status = rq.old_status;
+              fail_step = rq.old_fail;
+              done = true;
+            }
+          }
         }
       }
       FMDP_MARK(PH_DECIDE)
@@ -1687,19 +1762,22 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
     }
 
     // ------------------------------------------------------------ request epilogue
+    if (REUSE && reconv && lead)  // the previous run's steps k .. n_old - 1 back into the request's records
+      reconv_copy(args.bak, RecPtrs{args.traj, args.heading, args.astar, args.stepx, args.stepd2, args.ntie}, sbase, k,
+                  rq.n_old, rank, G, w.sat_d2, solo ? ctl : cluster.map_shared_rank(ctl, 0));
     cluster.sync();  // n_exact contributions of every CTA have landed in rank 0
     if (XP && rank == 0 && tid == 0) args.x_seq[xcl] = xseq0 + xit;  // read by the next launch
-    if (lead && rank == 0 && tid == 0 && rq.head && args.stop && status >= 0) atomicExch(args.stop, 1);
+    if (lead && rank == 0 && tid == 0 && rq.head && args.stop && (status >= 0 || reconv)) atomicExch(args.stop, 1);
     if (lead && rank == 0 && tid == 0 && !evalm) {
       Out o;
       o.status = status;
-      o.n_states = k + 1;
+      o.n_states = reconv ? rq.n_old : k + 1;
       o.fail_step = fail_step;
-      o.n_near_ties = n_near;
-      o.n_exact = nex0 + ctl->n_exact;
+      o.n_near_ties = n_near + ctl->rc_near;
+      o.n_exact = nex0 + ctl->n_exact + ctl->rc_exact;
       o.steps_run = steps_run;
-      o.min_sep_d2 = min_sep;
-      o.pad = 0;
+      o.min_sep_d2 = min(min_sep, ctl->rc_min);
+      o.reconv = reconv ? 1 : 0;
       args.out[rq.slot] = o;
     }
     // drain prefetches still in flight before the ring buffers are reused
@@ -1752,20 +1830,24 @@ __global__ void append_kernel(int32_t* rows, int32_t cap, int64_t horizon, const
 // comes within R_tau + reach + 1 of q_i(k) (else it is >= R_tau + 1 from every projected
 // state: clearly outside the FP32 band, the same argument as f1 culling), or if p itself is
 // within the separation saturation radius R_max of q_i(k).  Exact-conservative (DESIGN.md a10).
-__global__ void influence_kernel(const int32_t* traj, int32_t cap, const int32_t* n_states, const int64_t* t0,
-                                 const InflPair* pairs, InflWells iw, int32_t* kfirst) {
-  __shared__ int32_t best;
+__global__ void influence_kernel(const int32_t* traj, const BakRec* bak, int32_t cap, const int32_t* n_states,
+                                 const int64_t* t0, const InflPair* pairs, InflWells iw, int32_t* kfirst) {
+  __shared__ int32_t best, last;
   const InflPair pr = pairs[blockIdx.x];
-  if (threadIdx.x == 0) best = INT_MAX;
+  if (threadIdx.x == 0) {
+    best = INT_MAX;
+    last = -1;
+  }
   __syncthreads();
-  const int ni = n_states[pr.i], nj = n_states[pr.j];
+  const int nj = n_states[pr.j];
+  const int ilo = pr.hi < 0 ? 0 : pr.lo, ihi = pr.hi < 0 ? n_states[pr.i] : pr.hi;
   const int64_t ti = t0[pr.i], tj = t0[pr.j];
   const int32_t* qi = traj + (size_t)pr.i * cap * 3;
+  const BakRec* bi = bak + (size_t)pr.i * cap;  // (pr.bak: the backup of i's previous run)
   const int32_t* pj = traj + (size_t)pr.j * cap * 3;
   // only rows where both are present can interact
-  const int64_t k_lo = max((int64_t)0, tj - ti), k_hi = min((int64_t)ni, tj + nj - ti);
+  const int64_t k_lo = max((int64_t)ilo, tj - ti), k_hi = min((int64_t)ihi, tj + nj - ti);
   for (int64_t k = k_lo + threadIdx.x; k < k_hi; k += blockDim.x) {
-    if (k >= best) break;
     const int64_t idx = ti + k - tj;
     const int32_t* p = pj + 3 * idx;
     int64_t vx = 0, vy = 0, vz = 0;  // forward difference (R11)
@@ -1773,16 +1855,47 @@ __global__ void influence_kernel(const int32_t* traj, int32_t cap, const int32_t
       const int32_t* a = idx < nj - 1 ? p : p - 3;
       vx = a[3] - a[0]; vy = a[4] - a[1]; vz = a[5] - a[2];
     }
-    const int64_t rx = (int64_t)p[0] - qi[3 * k], ry = (int64_t)p[1] - qi[3 * k + 1], rz = (int64_t)p[2] - qi[3 * k + 2];
+    int64_t qx, qy, qz;
+    if (pr.bak) {
+      qx = bi[k].x; qy = bi[k].y; qz = bi[k].z;
+    } else {
+      qx = qi[3 * k]; qy = qi[3 * k + 1]; qz = qi[3 * k + 2];
+    }
+    const int64_t rx = (int64_t)p[0] - qx, ry = (int64_t)p[1] - qy, rz = (int64_t)p[2] - qz;
     bool hit = rx * rx + ry * ry + rz * rz < iw.sat2;
     for (int t = 0; t < iw.n_tau && !hit; ++t) {
       const int64_t cx = rx + iw.k_tau[t] * vx, cy = ry + iw.k_tau[t] * vy, cz = rz + iw.k_tau[t] * vz;
       hit = cx * cx + cy * cy + cz * cz < iw.r2[t];
     }
-    if (hit) atomicMin(&best, (int32_t)k);
+    if (hit) {
+      atomicMin(&best, (int32_t)k);
+      atomicMax(&last, (int32_t)k);
+    }
   }
   __syncthreads();
-  if (threadIdx.x == 0) kfirst[blockIdx.x] = best;
+  if (threadIdx.x == 0) {  // [first, last] influenced step of request i (INT_MAX, -1: none)
+    kfirst[2 * blockIdx.x] = best;
+    kfirst[2 * blockIdx.x + 1] = last;
+  }
+}
+
+// Backup of slot i's steps [lo, hi) before a rollback overwrites them (re-convergence, a10).
+__global__ void backup_kernel(BakRec* bak, const int32_t* traj, const int32_t* heading, const int32_t* astar,
+                              const int32_t* stepx, const uint32_t* stepd2, const int8_t* ntie, int32_t cap, int slot,
+                              int lo, int hi) {
+  const size_t b = (size_t)slot * cap;
+  for (int m = lo + blockIdx.x * blockDim.x + threadIdx.x; m < hi; m += gridDim.x * blockDim.x) {
+    BakRec e;
+    e.x = traj[3 * (b + m)];
+    e.y = traj[3 * (b + m) + 1];
+    e.z = traj[3 * (b + m) + 2];
+    e.heading = heading[b + m];
+    e.astar = astar[b + m];
+    e.stepx = stepx[b + m];
+    e.stepd2 = stepd2[b + m];
+    e.ntie = ntie[b + m];
+    bak[b + m] = e;
+  }
 }
 
 // ----------------------------------------------------------------------------- launchers
@@ -1926,10 +2039,20 @@ cudaError_t launch_append(int32_t* rows, int32_t row_cap, int64_t horizon, const
   return cudaGetLastError();
 }
 
-cudaError_t launch_influence(const int32_t* traj, int32_t cap, const int32_t* n_states, const int64_t* t0,
-                             const InflPair* pairs, int n_pairs, const InflWells& iw, int32_t* kfirst, cudaStream_t s) {
+cudaError_t launch_influence(const int32_t* traj, const BakRec* bak, int32_t cap, const int32_t* n_states,
+                             const int64_t* t0, const InflPair* pairs, int n_pairs, const InflWells& iw, int32_t* kfirst,
+                             cudaStream_t s) {
   if (n_pairs <= 0) return cudaSuccess;
-  influence_kernel<<<n_pairs, 256, 0, s>>>(traj, cap, n_states, t0, pairs, iw, kfirst);
+  influence_kernel<<<n_pairs, 256, 0, s>>>(traj, bak, cap, n_states, t0, pairs, iw, kfirst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_backup(BakRec* bak, const int32_t* traj, const int32_t* heading, const int32_t* astar,
+                          const int32_t* stepx, const uint32_t* stepd2, const int8_t* ntie, int32_t cap, int slot, int lo,
+                          int hi, cudaStream_t s) {
+  if (hi <= lo) return cudaSuccess;
+  const int n = hi - lo;
+  backup_kernel<<<(n + 255) / 256, 256, 0, s>>>(bak, traj, heading, astar, stepx, stepd2, ntie, cap, slot, lo, hi);
   return cudaGetLastError();
 }
 

@@ -102,7 +102,7 @@ class Stats(C.Structure):
     _fields_ = [("steps", C.c_int64), ("pair_evals", C.c_int64), ("rounds", C.c_int32), ("reruns", C.c_int32),
                 ("cluster_size", C.c_int32), ("walkers", C.c_int32), ("kernels", C.c_int32),
                 ("device_ms", C.c_double), ("phase_cycles", C.c_int64 * 17), ("split", C.c_int32),
-                ("pad", C.c_int32)]
+                ("reconverged", C.c_int32)]
 
 PHASES = ("projection", "goal_terrain", "row_wait", "hot_loop", "stage", "reduce_scatter", "barrier1",
           "owner_epilogue", "barrier2", "decide", "top", "tscan", "proj_loop", "build", "own_classify", "argmax", "flags")

@@ -1,6 +1,9 @@
 """Sweep of the split-slice parameters of the FCFS batch (lanes at the head's cluster size, the
 others' cluster size, slice budget) on configs[1], full and culled; device ms per batch.
-Each setting in its own process (the overrides are read once per process)."""
+Each setting in its own process (the overrides are read once per process).
+
+    python tools/sweep_split.py [lanes,..] [Go,..] [budget,..]
+"""
 import os
 import subprocess
 import sys
@@ -25,9 +28,12 @@ for cull in (0, 1):
     out.append(f"cull={cull} {min(ms):.1f}")
 print(" ".join(out))
 ''' % ROOT
-for lanes in (1, 2, 3):
-    for go in (4, 8):
-        for budget in (1, 2, 4):
+LANES = [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "1,2,3").split(",")]
+GOS = [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "4,8").split(",")]
+BUDGETS = [int(x) for x in (sys.argv[3] if len(sys.argv) > 3 else "1,2,4").split(",")]
+for lanes in LANES:
+    for go in GOS:
+        for budget in BUDGETS:
             env = dict(os.environ, FMDP_TUNE_LANES=str(lanes), FMDP_TUNE_GO=str(go))
             r = subprocess.run([sys.executable, "-c", PROBE, str(budget)], env=env, capture_output=True, text=True)
             print(f"lanes={lanes} Go={go} budget={budget}: {r.stdout.strip()} {r.stderr[-200:] if r.returncode else ''}",
