@@ -15,7 +15,7 @@ sys.path.insert(0, ROOT)
 import tools.ab_variants as abv  # noqa: E402
 
 
-EXTRA = {"hint": ["FMDP_MBAR_SUSPEND_NS=1000000"]}  # working-tree variants (-D flags)
+EXTRA = {}  # working-tree variants (-D flags)
 
 
 def build(rev="HEAD"):
