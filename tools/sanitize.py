@@ -4,7 +4,8 @@ protocol relies on mbarriers / DSMEM st.async / cross-cluster words, meant to ru
     compute-sanitizer --tool {memcheck,racecheck,synccheck} python tools/sanitize.py CASE
 
 CASE: c1 (configs[0]: one request + eval_step, clusters 1 and 4), c2s (configs[1] city with 300
-plans, a 4-request FCFS batch full and culled, speculative slices), cosim (a 3-aircraft ring),
+plans, a 4-request FCFS batch full and culled, speculative slices), reuse (a compact 16-request
+culled batch whose rolled-back re-walks re-converge), cosim (a 3-aircraft ring),
 p2p (two exchange contexts in one process, a split request over 2 clusters).  Each case checks
 its result against a plain sequential run of the same context, so a race that changes an
 answer also fails the case, not only the tool.
@@ -52,6 +53,23 @@ def case_c2s():
     for key, res in out.items():
         assert all(_same(a, b) for a, b in zip(ref, res)), f"c2s mismatch {key}"
     print("c2s:", [r.status for r in ref], [r.n_states for r in ref])
+
+
+def case_reuse():
+    """Speculative culled batch with rollbacks whose re-walks re-converge (re-convergence check,
+    backup copy, reconv_copy epilogue), against the sequential loop."""
+    sc = fs.random_small(49, n_plans=60, n_requests=16, half_m=1200.0, n_buildings=20, max_steps=500, t0_max=60)
+    out = {}
+    for seq in (True, False):
+        ctx = FMDP(sc.airspace, sc.terrain, device=0, torch_alloc=False)
+        ctx.add_plans(sc.plans)
+        ctx.set_launch(cull=1, step_budget=7)
+        out[seq] = ctx.schedule_batch(sc.src, sc.dst, sc.t0, sequential=seq)
+        if not seq:
+            rc = ctx.stats()["reconverged"]
+        ctx.close()
+    assert all(_same(a, b) for a, b in zip(out[True], out[False])), "reuse mismatch"
+    print("reuse: reconverged", rc, [r.status for r in out[True]])
 
 
 def case_cosim():
