@@ -779,7 +779,7 @@ def run_native(args):
                          "algorithmic_ops_frac": pps * OPS_PER_PAIR / (148 * 128 * 1965e6),
                          "pipe_frac": pps * (2 + C5 - 1) / C5 / (148 * 128 * 1965e6),
                          "pairs_per_clk_per_sm_used": pps / (sms * 1965e6),
-                         "loop_ceiling_pairs_per_clk_per_sm": "34-36 (C = 3, profiles/r01_hotbench.txt)"}
+                         "loop_ceiling_pairs_per_clk_per_sm": "38-40 (C = 3 with the level-climb skip, tools/hotbench/hotbench2.cu, profiles/r02s2_rates.txt; C = 5 not measured in isolation)"}
             _log(f"c5: {name} {out[name]}")
         if world > 1:  # plan-sharded over the GPUs (fmdp_schedule_p2p); every rank takes part
             from paper_2008_03518_b200.fmdp import p2p_connect_group

@@ -502,8 +502,10 @@ fmdp_status run_split(fmdp_ctx* ctx, std::vector<Req>& run, int budget) {
   // (FMDP_TUNE_LANES / FMDP_TUNE_GO: tuning overrides for tools/sweep_split.py only)
   static const int lanes_env = std::getenv("FMDP_TUNE_LANES") ? std::atoi(std::getenv("FMDP_TUNE_LANES")) : 2;
   static const int go_env = std::getenv("FMDP_TUNE_GO") ? std::atoi(std::getenv("FMDP_TUNE_GO")) : 0;
+  static const int gl_env = std::getenv("FMDP_TUNE_GL") ? std::atoi(std::getenv("FMDP_TUNE_GL")) : 0;
+  const int Gl = gl_env > 0 ? gl_env : Gh;  // the lanes' cluster size
   int m = std::min(lanes_env, n - 2);
-  while (m > 0 && ctx->num_sms < (1 + m) * Gh + 16) --m;
+  while (m > 0 && ctx->num_sms < Gh + m * Gl + 16) --m;
   const bool lane2 = m > 0;
   const int nl = 1 + m;
   // the others: clusters of half the head's size on the SMs left -- fewer, faster walkers on the
@@ -511,7 +513,8 @@ fmdp_status run_split(fmdp_ctx* ctx, std::vector<Req>& run, int budget) {
   // choose_launch optimises the wrong objective here: configs[1] full batch 119.9 -> 111.7 ms,
   // culled 58.7 -> 58.5 ms, configs[2] unchanged)
   const int Go = go_env > 0 ? go_env : std::max(1, Gh / 2);
-  const int nco = std::max(1, std::min(n - nl, std::min(max_clusters(ctx, Go), (ctx->num_sms - nl * Gh) / Go)));
+  const int nco =
+      std::max(1, std::min(n - nl, std::min(max_clusters(ctx, Go), (ctx->num_sms - Gh - m * Gl) / Go)));
   CK(cudaMemcpyAsync(ctx->d_reqs, run.data(), sizeof(Req) * n, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemsetAsync(ctx->d_queue, 0, 2 * sizeof(int32_t), ctx->stream));  // [0] head, [1] others
   CK(cudaMemsetAsync(ctx->d_queue + 3, 0, sizeof(int32_t), ctx->stream));  // [3] second lane
@@ -534,7 +537,7 @@ fmdp_status run_split(fmdp_ctx* ctx, std::vector<Req>& run, int budget) {
     a2.n_reqs = m;
     a2.queue = ctx->d_queue + 3;
     CK(cudaStreamWaitEvent(ctx->stream3, ctx->ev0, 0));
-    CK(fmdp::launch_walk(ctx->w, a2, ctx->C, Gh, m, threads_for(ctx), chunk_for(ctx), rawcap_for(ctx), ctx->stream3));
+    CK(fmdp::launch_walk(ctx->w, a2, ctx->C, Gl, m, threads_for(ctx), chunk_for(ctx), rawcap_for(ctx), ctx->stream3));
     CK(cudaEventRecord(ctx->ev3, ctx->stream3));
   }
   CK(fmdp::launch_walk(ctx->w, ao, ctx->C, Go, nco, threads_for(ctx), chunk_for(ctx), rawcap_for(ctx), ctx->stream2));

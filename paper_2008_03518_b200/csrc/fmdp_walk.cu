@@ -764,6 +764,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   uint32_t parX = 0;     // next wait parity of the exchange mbarriers: bits 0-1 reduce-scatter, 2-3 V*
   uint32_t pending = 0;  // ring buffers issued and not yet waited
   int cnt2 = 0;          // (I/O thread NT-1) active count of row K+2, loaded one step ahead
+  uint32_t stop_f = 0;   // (I/O thread of rank 0) the head-finished flag, loaded one step ahead
 
   for (;;) {
     // ------------------------------------------------------------ next request
@@ -1222,9 +1223,11 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           mbar_arrive_tx(&s_bar[3 + p], bytesA);
           if (!fin) mbar_arrive_tx(&s_bar[5 + p], (uint32_t)(16 * A) + (XP ? 4u : 0u));
           if (args.stop && rank == 0) {  // one reading for the whole cluster
-            const uint32_t f = (uint32_t)*(volatile int32_t*)args.stop;
+            // the value loaded in the previous step: the L2 round trip of the volatile load stays
+            // off this warp's path (a walker may pause one step later -- speculation only)
             const uint32_t la = smem_u32(&ctl->stop[p]), lb = smem_u32(&s_bar[3 + p]);
-            for (unsigned b = 0; b < G; ++b) push_u32(solo, la, b, f, lb);
+            for (unsigned b = 0; b < G; ++b) push_u32(solo, la, b, stop_f, lb);
+            stop_f = (uint32_t)*(volatile int32_t*)args.stop;
           }
         }
 

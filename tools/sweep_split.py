@@ -2,7 +2,7 @@
 others' cluster size, slice budget) on configs[1], full and culled; device ms per batch.
 Each setting in its own process (the overrides are read once per process).
 
-    python tools/sweep_split.py [lanes,..] [Go,..] [budget,..]
+    python tools/sweep_split.py [lanes,..] [Go,..] [budget,..] [Gl,..]
 """
 import os
 import subprocess
@@ -31,10 +31,12 @@ print(" ".join(out))
 LANES = [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "1,2,3").split(",")]
 GOS = [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "4,8").split(",")]
 BUDGETS = [int(x) for x in (sys.argv[3] if len(sys.argv) > 3 else "1,2,4").split(",")]
+GLS = [int(x) for x in (sys.argv[4] if len(sys.argv) > 4 else "0").split(",")]  # lane cluster size (0: head's)
 for lanes in LANES:
     for go in GOS:
         for budget in BUDGETS:
-            env = dict(os.environ, FMDP_TUNE_LANES=str(lanes), FMDP_TUNE_GO=str(go))
+          for gl in GLS:
+            env = dict(os.environ, FMDP_TUNE_LANES=str(lanes), FMDP_TUNE_GO=str(go), FMDP_TUNE_GL=str(gl))
             r = subprocess.run([sys.executable, "-c", PROBE, str(budget)], env=env, capture_output=True, text=True)
-            print(f"lanes={lanes} Go={go} budget={budget}: {r.stdout.strip()} {r.stderr[-200:] if r.returncode else ''}",
+            print(f"lanes={lanes} Go={go} Gl={gl} budget={budget}: {r.stdout.strip()} {r.stderr[-200:] if r.returncode else ''}",
                   flush=True)
