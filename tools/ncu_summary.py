@@ -67,6 +67,7 @@ traffic = None
 import os
 for rep, kern, title in (('walk_batch', 'walk_kernel<3, 0>', 'configs[1] batch, first slice head (full path)'),
                          ('walk_cull16', 'walk_kernel<3, 4>', 'configs[1] request, f1 culling, G=16'),
+                         ('walk_cull8', 'walk_kernel<3, 4>', 'configs[1] request, f1 culling, G=8 (the culled head size)'),
                          ('walk_f4', 'walk_kernel<10, 5>', 'configs[1] request, A = 1350 (SURVEY f4), wide walker'),
                          ('walk_c5split', 'walk_kernel<5, 2>', 'configs[4] 1M plans, A = 85, split request (full path)')):
     rep = f'{rnd}_{rep}'
