@@ -1377,7 +1377,9 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   for (int c : ctx->climb) maxc = std::max(maxc, std::abs(c));
   w.reach_u = (int32_t)(a.window * ((int64_t)std::ceil(maxd) + maxc) + 1);
   w.step_reach_u = (int32_t)((int64_t)std::ceil(maxd) + maxc + 1);
-  w.cull_inf = (int32_t)(Rmax + w.reach_u + 1);
+  // f1 cull radius: the culled walker pre-culls a step's plans against the previous step's q, so
+  // the reach grows by one step: |s_{k+1} - q_k| <= reach + step_reach
+  w.cull_inf = (int32_t)(Rmax + w.reach_u + w.step_reach_u + 1);
   // Hot-loop filter band.  The kernel evaluates e = Q + 2(s-o).X, X = o - c,
   // Q = fl(|X|^2), with s - o bounded by S (the fan radius around o = q + (W/2)(DX,DY)[psi],
   // measured here over every heading, turn and substep, plus the climb).  First-order
@@ -1420,7 +1422,7 @@ fmdp_status fmdp_create(const fmdp_airspace* air, const fmdp_terrain* ter, const
   w.k_absmax = 0;
   for (int i = 0; i < a.n_tau; ++i) w.k_absmax = std::max(w.k_absmax, std::abs(w.k_tau[i]));
   for (int i = 0; i < fmdp::NTAU; ++i) {
-    const double rc = i < a.n_tau ? std::sqrt((double)w.R2_tau[i]) + w.reach_u + 1.0 : -1.0;
+    const double rc = i < a.n_tau ? std::sqrt((double)w.R2_tau[i]) + w.reach_u + w.step_reach_u + 1.0 : -1.0;
     w.cull2f_tau[i] = i < a.n_tau ? (float)(rc * rc * (1.0 + std::ldexp(1.0, -16))) : -1.0f;
   }
   ctx->iw.n_tau = a.n_tau;

@@ -274,6 +274,24 @@ __device__ __forceinline__ int row_count(const World& w, int64_t K) {
   return (K >= 0 && K < w.horizon) ? __ldg(&w.counts[K]) : 0;
 }
 
+// SURVEY f1 cull test of one plan (offsets r from the position the test is made against, forward
+// difference v): an exact L-inf prefilter on the whole plan (every well lies within kmax |v|_inf
+// of p), then a conservative FP32 test of each well against (R_tau + reach + step_reach + 1)^2.  A
+// culled well is farther than R_tau + 1 from every projected state of this step and the next (the
+// pre-cull tests against the previous step's q), i.e. clearly outside the FP32 band.
+__device__ __forceinline__ bool cull_keep(const World& w, int rx, int ry, int rz, int vx, int vy, int vz) {
+  const int vinf = max(abs(vx), max(abs(vy), abs(vz)));
+  const int dinf = max(abs(rx), max(abs(ry), abs(rz)));
+  if (dinf >= w.cull_inf + w.k_absmax * vinf) return false;
+  bool keep = false;
+#pragma unroll
+  for (int t = 0; t < NTAU; ++t) {
+    const float cx = (float)(rx + w.k_tau[t] * vx), cy = (float)(ry + w.k_tau[t] * vy), cz = (float)(rz + w.k_tau[t] * vz);
+    keep |= fmaf(cz, cz, fmaf(cy, cy, cx * cx)) < w.cull2f_tau[t];
+  }
+  return keep;
+}
+
 // Top-2 merge for the argmax (Alg 9): order by value, then lowest index (R13).
 __device__ __forceinline__ bool better(double v, int i, double bv, int bi) { return v > bv || (v == bv && i < bi); }
 
@@ -799,6 +817,10 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
     // per-request aggregates, kept by thread 0 of rank 0
     int n_near = 0, steps_run = 0, status = 0, fail_step = -1, nex0 = 0;
     bool reconv = false;  // the re-walk met its previous run (Req::n_old): the rest is that run's
+    // pre-cull (culled FCFS walker): this thread's survivors among its plans of the next step's
+    // first chunk, culled during this step's V* exchange (plan indices, -1: none); sv_n = their
+    // count (> 2: the thread re-culls its plans in the step; < 0: no pre-cull for the next step)
+    int sv0 = -1, sv1 = -1, sv_n = -1;
     // re-convergence window: decisions k with reuse_from <= k + 1 < n_old compare their next state
     // (only the culled FCFS walker and the reference instantiation carry it: measured, the full
     // walker's batches gain nothing from it and its step loop would grow, +1.3 % per step)
@@ -903,6 +925,8 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       }
       FMDP_MARK(PH_WAIT)
       uint32_t stay = w.sat_d2;
+      const int svn_now = sv_n;  // this step's first chunk was pre-culled in the previous step
+      sv_n = -1;
       {
         const int lo = ctl->sl_lo[bK], n = ctl->sl_n[bK];
         // plan j of the CTA slice: the first RAWCAP were staged by TMA, the rest are read from L2
@@ -937,22 +961,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
             }
             if (fin) continue;
             bool keep = valid;
-            if (valid && compact) {
-              // exact L-inf prefilter on the whole plan: every well lies within kmax*|v|_inf of p,
-              // so |p - q|_inf - kmax*|v|_inf >= R + reach + 1 culls all five wells
-              const int vinf = max(abs(vx), max(abs(vy), abs(vz)));
-              const int dinf = max(abs(rx), max(abs(ry), abs(rz)));
-              keep = dinf < w.cull_inf + w.k_absmax * vinf;
-            }
-            if (keep && compact) {
-              keep = false;
-#pragma unroll
-              for (int t = 0; t < NTAU; ++t) {
-                const float cx = (float)(rx + w.k_tau[t] * vx), cy = (float)(ry + w.k_tau[t] * vy),
-                            cz = (float)(rz + w.k_tau[t] * vz);
-                keep |= fmaf(cz, cz, fmaf(cy, cy, cx * cx)) < w.cull2f_tau[t];
-              }
-            }
+            if (valid && compact) keep = cull_keep(w, rx, ry, rz, vx, vy, vz);
             int slot = jj;
             if (compact && keep) slot = atomicAdd(counter, 1);  // survivors are rare: no warp round trip
             if (keep && slot < CH) {
@@ -1088,7 +1097,44 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         // the first chunk's well records are built BEFORE the projection: the build needs only q,
         // the fan origin and row K (staged two steps ahead), so it overlaps the projection's
         // table load, and the projection barrier also publishes the records (one CTA barrier less)
-        if (n_chunks > 0) build(0, min(SC, n), cullm, &ctl->nsurv[(k & 1) * 2]);
+        if (MODE == 4 && n_chunks > 0 && svn_now >= 0) {
+          // pre-culled first chunk (plans j < RAWCAP, staged): the separation minimum over every
+          // plan, records (with this step's anchor) of the thread's pre-culled survivors only
+          const int nc0 = min(SC, n);
+          for (int jj = tid; jj < nc0; jj += NT)
+            stay = min(stay, clamp_d2(rb[jj] - qx, rb[RAWW + jj] - qy, rb[2 * RAWW + jj] - qz, w.R_max, w.sat_d2));
+          if (!fin) {
+            int* counter = &ctl->nsurv[(k & 1) * 2];
+            auto rec = [&](int j, bool test) {
+              const int rx = rb[j] - qx, ry = rb[RAWW + j] - qy, rz = rb[2 * RAWW + j] - qz;
+              const uint32_t pv = (uint32_t)rb[3 * RAWW + j];
+              const int vx = sext(pv, 11), vy = sext(pv >> 11, 11), vz = sext(pv >> 22, 10);
+              if (test && !cull_keep(w, rx, ry, rz, vx, vy, vz)) return;
+              const int slot = atomicAdd(counter, 1);
+              if (slot < CH) {
+                float* cp = s_cen + PAIR_STRIDE * (slot >> 1) + (slot & 1);
+#pragma unroll
+                for (int t = 0; t < NTAU; ++t) {
+                  const float X = (float)(ox - (rx + w.k_tau[t] * vx));
+                  const float Y = (float)(oy - (ry + w.k_tau[t] * vy));
+                  const float Z = (float)(-(rz + w.k_tau[t] * vz));
+                  cp[8 * t + 0] = X;
+                  cp[8 * t + 2] = Y;
+                  cp[8 * t + 4] = Z;
+                  cp[8 * t + 6] = fmaf(Z, Z, fmaf(Y, Y, X * X));
+                }
+              }
+            };
+            if (svn_now > 2) {
+              for (int jj = NT - 1 - tid; jj < nc0; jj += NT) rec(jj, true);
+            } else {
+              if (sv0 >= 0) rec(sv0, false);
+              if (sv1 >= 0) rec(sv1, false);
+            }
+          }
+        } else if (n_chunks > 0) {
+          build(0, min(SC, n), cullm, &ctl->nsurv[(k & 1) * 2]);
+        }
         FMDP_MARK(PH_BUILD)
         if (!fin) {
           // ---- a5 candidates of steps k+1 .. k+1+TC_WIN when this list's window ends with step k
@@ -1542,6 +1588,34 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         if (tid == 0 && ctl->n_exact && rank != 0) {
           atomicAdd(&cluster.map_shared_rank(ctl, 0)->n_exact, ctl->n_exact);
           ctl->n_exact = 0;
+        }
+        // Pre-cull (culled FCFS walker): the f1 cull test of the next row's first chunk (row K + 1,
+        // staged two steps ahead) against this q, with the radius grown by one step's reach (host),
+        // while the V* exchange is in flight; each thread keeps its survivors (at most two) for the
+        // next step, which builds their records with its own anchor (no cross-thread dependence,
+        // so no barrier).  The highest threads take the plans (the owner pass-2 warps are the
+        // lowest).  Records of a superset of the relevant plans: results bit-identical.
+        if (MODE == 4) {
+          const int bK1 = bK == 2 ? 0 : bK + 1;
+          if (pending & (1u << bK1)) {
+            mbar_wait(&s_bar[bK1], (par >> bK1) & 1u);
+            par ^= 1u << bK1;
+            pending &= ~(1u << bK1);
+          }
+          const int nc1 = min(RAWCAP, ctl->sl_n[bK1]);
+          const int32_t* rb1 = s_raw + (size_t)bK1 * 4 * RAWW + ctl->sl_off[bK1];
+          int cnt = 0;
+          sv0 = sv1 = -1;
+          for (int jj = NT - 1 - tid; jj < nc1; jj += NT) {
+            const uint32_t pv = (uint32_t)rb1[3 * RAWW + jj];
+            if (cull_keep(w, rb1[jj] - qx, rb1[RAWW + jj] - qy, rb1[2 * RAWW + jj] - qz, sext(pv, 11), sext(pv >> 11, 11),
+                          sext(pv >> 22, 10))) {
+              if (cnt == 0) sv0 = jj;
+              else if (cnt == 1) sv1 = jj;
+              ++cnt;
+            }
+          }
+          sv_n = cnt;
         }
         FMDP_MARK(PH_OWNER)
         if (solo) __syncthreads();
