@@ -87,3 +87,26 @@ def test_reconverged_small_batches_equal_sequential_and_oracle(F, seed, budget):
     assert _replay_fcfs(sc, seq, b) == 0
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("G", [1, 2])
+def test_precull_dense_store_fallbacks(F, G):
+    """The culled walker's pre-cull in a dense store: 2000 plans in a 1.6 km box, so
+    one or two CTAs hold ~1000-2000 plans per row, most of them within reach -- threads keep more
+    than two survivors (they re-cull their plans in the step) and the survivors overflow the 256
+    well records (uncompacted rebuild).  The culled batch must equal the full one bit for bit."""
+    sc = fs.random_small(7, n_plans=2000, n_requests=6, half_m=800.0, max_steps=150, t0_max=40)
+    out = {}
+    for cull in (0, 1):
+        ctx = F.FMDP(sc.airspace, sc.terrain, device=0)
+        ctx.add_plans(sc.plans)
+        ctx.set_launch(cull=cull, cluster_size=G)
+        res = ctx.schedule_batch(sc.src, sc.dst, sc.t0)
+        out[cull] = (res, [ctx.steplog(i) for i in range(len(res))])
+        ctx.close()
+    (ra, la), (rb, lb) = out[0], out[1]
+    for i, (x, y) in enumerate(zip(ra, rb)):
+        assert x.status == y.status and x.n_states == y.n_states and (x.traj == y.traj).all(), i
+        assert x.n_exact == y.n_exact and x.n_near_ties == y.n_near_ties and x.min_sep_m == y.min_sep_m, i
+        for u, v in zip(la[i], lb[i]):
+            assert (u == v).all(), i
