@@ -257,6 +257,10 @@ cudaError_t launch_append(int32_t* rows, int32_t row_cap, int64_t horizon, const
 cudaError_t launch_influence(const int32_t* traj, const BakRec* bak, int32_t cap, const int32_t* n_states,
                              const int64_t* t0, const InflPair* pairs, int n_pairs, const InflWells& iw, int32_t* kfirst,
                              cudaStream_t s);
+// Trajectories of slots [0, n) packed back to back (slot i's states at off[i], n_states from out[i])
+// for one D2H copy of the whole batch's result.
+cudaError_t launch_pack_traj(const int32_t* traj, int32_t cap, const Out* out, const int64_t* off, int n, int32_t* pack,
+                             cudaStream_t s);
 // Backup of request slot i's steps [lo, hi) (state, decision and per-step records) into bak.
 cudaError_t launch_backup(BakRec* bak, const int32_t* traj, const int32_t* heading, const int32_t* astar,
                           const int32_t* stepx, const uint32_t* stepd2, const int8_t* ntie, int32_t cap, int slot, int lo,

@@ -89,6 +89,10 @@ struct fmdp_ctx {
   int app_cap = 0;
   int32_t* d_up = nullptr;  // upload scratch (states / slots)
   size_t up_cap = 0;
+  int32_t* d_pack = nullptr;    // batch result trajectories packed back to back (device) ...
+  int32_t* h_pack = nullptr;    // ... and their pinned host copy (one D2H per batch)
+  int64_t* d_packoff = nullptr;
+  size_t pack_cap = 0, packoff_cap = 0;
   int4* d_cspub = nullptr;     // co-simulation publish buffer [2][n][2]
   int32_t* d_csctr = nullptr;  // [0] arrivals, [1] barrier error
   int cs_cap = 0;
@@ -863,6 +867,48 @@ fmdp_status gather_finished(fmdp_ctx* ctx, const fmdp_gather* g, const std::vect
   return FMDP_OK;
 }
 
+// Result trajectories of slots [0, n) into the caller's buffer (traj_cap_each states per request):
+// packed on the device (pack_traj_kernel), one D2H copy into pinned memory, scattered on the host --
+// one copy per batch instead of one pageable copy per request (the e2e path's copy-out).
+fmdp_status copy_out_traj(fmdp_ctx* ctx, int n, fmdp_qpos* traj, int32_t traj_cap_each) {
+  std::vector<int64_t> off(n);
+  int64_t tot = 0;
+  for (int i = 0; i < n; ++i) {
+    off[i] = tot;
+    tot += ctx->h_out[i].n_states;
+  }
+  if (tot == 0) return FMDP_OK;
+  if ((size_t)tot * 3 > ctx->pack_cap) {
+    const size_t m = std::max((size_t)tot * 3, 2 * ctx->pack_cap);
+    int32_t* hp = nullptr;
+    if (cudaMallocHost(&hp, sizeof(int32_t) * m) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ctx, FMDP_E_NOMEM, "pinned host allocation failed (trajectory copy-out)");
+    }
+    fmdp_status s;
+    if ((s = grow(ctx, ctx->d_pack, m))) {
+      cudaFreeHost(hp);
+      return s;
+    }
+    if (ctx->h_pack) cudaFreeHost(ctx->h_pack);
+    ctx->h_pack = hp;
+    ctx->pack_cap = m;
+  }
+  if ((size_t)n > ctx->packoff_cap) {
+    fmdp_status s;
+    if ((s = grow(ctx, ctx->d_packoff, (size_t)n))) return s;
+    ctx->packoff_cap = (size_t)n;
+  }
+  CK(cudaMemcpyAsync(ctx->d_packoff, off.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(fmdp::launch_pack_traj(ctx->d_traj, ctx->cap_states, ctx->d_out, ctx->d_packoff, n, ctx->d_pack, ctx->stream));
+  ctx->stats.kernels += 1;
+  CK(cudaMemcpyAsync(ctx->h_pack, ctx->d_pack, sizeof(int32_t) * 3 * tot, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < n; ++i)
+    std::memcpy(traj + (size_t)i * traj_cap_each, ctx->h_pack + 3 * off[i], sizeof(fmdp_qpos) * ctx->h_out[i].n_states);
+  return FMDP_OK;
+}
+
 fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_result* res, fmdp_qpos* traj,
                           int32_t traj_cap_each, int32_t flags, const fmdp_gather* g = nullptr) {
   const bool dist = g && g->world > 1;
@@ -1117,13 +1163,7 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
     res[i].n_near_ties = o.n_near_ties;
     res[i].n_exact = o.n_exact;
   }
-  if (traj) {
-    for (int i = 0; i < n; ++i) {
-      CK(cudaMemcpyAsync(traj + (size_t)i * traj_cap_each, ctx->d_traj + (size_t)i * ctx->cap_states * 3,
-                         sizeof(fmdp_qpos) * ctx->h_out[i].n_states, cudaMemcpyDeviceToHost, ctx->stream));
-    }
-    CK(cudaStreamSynchronize(ctx->stream));
-  }
+  if (traj && (st = copy_out_traj(ctx, n, traj, traj_cap_each))) return st;
   ctx->last_n = n;
   return FMDP_OK;
 }
@@ -1538,6 +1578,7 @@ void fmdp_destroy(fmdp_ctx* ctx) {
   for (void* p : a) dfree(ctx, p);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->h_pack) cudaFreeHost(ctx->h_pack);
   if (ctx->ev2) cudaEventDestroy(ctx->ev2);
   if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
   if (ctx->ev3) cudaEventDestroy(ctx->ev3);

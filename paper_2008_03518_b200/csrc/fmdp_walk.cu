@@ -1956,6 +1956,15 @@ __global__ void influence_kernel(const int32_t* traj, const BakRec* bak, int32_t
   }
 }
 
+// Result trajectories of a batch packed back to back (one D2H copy instead of one per request).
+__global__ void pack_traj_kernel(const int32_t* traj, int32_t cap, const Out* out, const int64_t* off, int32_t* pack) {
+  const int i = blockIdx.x;
+  const int n3 = 3 * out[i].n_states;
+  const int32_t* src = traj + (size_t)i * cap * 3;
+  int32_t* dst = pack + 3 * off[i];
+  for (int e = threadIdx.x; e < n3; e += blockDim.x) dst[e] = src[e];
+}
+
 // Backup of slot i's steps [lo, hi) before a rollback overwrites them (re-convergence, a10).
 __global__ void backup_kernel(BakRec* bak, const int32_t* traj, const int32_t* heading, const int32_t* astar,
                               const int32_t* stepx, const uint32_t* stepd2, const int8_t* ntie, int32_t cap, int slot,
@@ -2121,6 +2130,13 @@ cudaError_t launch_influence(const int32_t* traj, const BakRec* bak, int32_t cap
                              cudaStream_t s) {
   if (n_pairs <= 0) return cudaSuccess;
   influence_kernel<<<n_pairs, 256, 0, s>>>(traj, bak, cap, n_states, t0, pairs, iw, kfirst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_traj(const int32_t* traj, int32_t cap, const Out* out, const int64_t* off, int n, int32_t* pack,
+                             cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  pack_traj_kernel<<<n, 256, 0, s>>>(traj, cap, out, off, pack);
   return cudaGetLastError();
 }
 
