@@ -229,7 +229,10 @@ fmdp_status fmdp_schedule(fmdp_ctx* ctx, uint64_t aircraft_id, fmdp_vec3 src, fm
 
 /* First-come-first-served batch: results identical to calling fmdp_schedule on each
  * request in array order.  Default implementation: speculative rounds against a store
- * snapshot + exact influence test + in-order commit.
+ * snapshot + exact influence test + in-order commit; with f1 culling
+ * (fmdp_launch.cull) a rolled-back request's re-walk takes over its previous run once its state
+ * meets it past every step a newly committed plan can influence (fmdp_stats.reconverged; DESIGN.md
+ * §6) -- same results.
  * flags: FMDP_BATCH_SEQUENTIAL forces the plain loop.
  * traj: n * traj_cap_each states (may be NULL to skip trajectory output). */
 #define FMDP_BATCH_SEQUENTIAL 1
