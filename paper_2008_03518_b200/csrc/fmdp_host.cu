@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -1010,7 +1011,9 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
         runs += (int)run.size();
         ctx->stats.rounds += 1;
       }
+      const auto th0 = std::chrono::steady_clock::now();  // (FMDP_DEBUG: host time between slices)
       if ((st = fetch_out(ctx, n))) return st;
+      const auto th1 = std::chrono::steady_clock::now();
       std::vector<int> mine;  // own requests that finished in this round
       for (const Req& r : run) {
         const Out& o = ctx->h_out[r.slot];
@@ -1040,6 +1043,7 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
             if (ru[i].on) pairs.push_back({i, j, ru[i].bak_lo, ru[i].n_old, 1});  // i's previous run
           }
       std::vector<int32_t> kf;
+      const auto th2 = std::chrono::steady_clock::now();
       if (!pairs.empty()) {
         CK(cudaMemcpyAsync(ctx->d_nstates, ns.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
         if ((st = influence(ctx, pairs, kf))) return st;
@@ -1111,8 +1115,13 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
         }
         ++c;
       }
+      const auto th3 = std::chrono::steady_clock::now();
       if ((st = commit_slots(ctx, newly, base, aircraft, plan_id))) return st;
+      const auto th4 = std::chrono::steady_clock::now();
       if (std::getenv("FMDP_DEBUG")) {
+        auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+        std::fprintf(stderr, "fmdp: host us fetch=%.0f pairs=%.0f influence+rollback=%.0f commit=%.0f\n", us(th0, th1),
+                     us(th1, th2), us(th2, th3), us(th3, th4));
         int pend = 0, prog = 0;
         for (int i = c; i < n; ++i) pend += fin[i] ? 0 : 1;
         for (const Req& r : run) prog += ctx->h_out[r.slot].steps_run > 0 ? 1 : 0;
