@@ -73,6 +73,14 @@ struct World {
   int32_t acc[MAX_ACC];         // speed increments, units per substep per substep
   int32_t vmin, vmax, v0;       // speed bounds / departure speed, units per substep
   const int2* spd;              // [vmax - vmin + 1][HL] displacement of one substep at (speed, heading)
+  // SURVEY f1 range query (culled FCFS walker): the plans loaded by fmdp_add_plans sit in each row
+  // sorted by x-y cell of side cell_l, slots [cstart[K][c], cstart[K][c+1]) in cell c (row-major,
+  // cell_ncx per row of cells), [cstart[K][cell_n], counts[K]) = plans appended since (unsorted).
+  // Every plan whose wells can reach a state of the next few steps lies in the 3x3 cells around
+  // the ownship (cell_l >= R_max + reach + the prefetch margin + max well offset).  cell_n = 0: off.
+  int32_t cell_n, cell_ncx, cell_ncy, cell_l;
+  int32_t cell_x0, cell_y0;
+  const int32_t* cstart;        // [horizon][cell_n + 1]
 };
 
 struct Req {
@@ -216,7 +224,7 @@ struct Layout {
     o_amb = o;  o = al(o + sizeof(int32_t) * AMB_MAX);
     o_tc = o;   o = al(o + sizeof(int32_t) * 2 * TC_MAX);  // candidate lists, by step parity
     o_bar = o;  o = al(o + sizeof(uint64_t) * 8);   // 3 TMA ring + 2 reduce-scatter + 2 V* mbarriers
-    o_ctl = o;  o = al(o + 512);
+    o_ctl = o;  o = al(o + 768);
     o_M = o;    o = al(o + sizeof(float) * (size_t)NOWN * WT);  // owner pass: in-radius minima of the owned items
     total = o;
   }
@@ -242,6 +250,14 @@ struct InflWells {              // exact-conservative influence criterion (a10)
   int64_t r2[NTAU];             // (R_tau + reach + 1)^2
   int64_t sat2;                 // R_max^2: separation saturation
 };
+
+// Range-query index build (fmdp_walk.cu): rows [K0, K0 + nrows) sorted by cell (see World),
+// cstart written; tmp = nrows * 4 * row_cap int32 scratch.
+cudaError_t launch_index(int32_t* rows, int32_t row_cap, const int32_t* counts, int64_t K0, int nrows, const World& w,
+                         int32_t* cstart, int32_t* tmp, cudaStream_t s);
+// Maximum |horizontal velocity|^2 (units^2 per substep^2) over every stored plan-step (index cell size).
+cudaError_t launch_vmax(const int32_t* rows, int32_t row_cap, const int32_t* counts, int64_t horizon,
+                        unsigned long long* out, cudaStream_t s);
 
 // Kernel launchers (fmdp_walk.cu).
 cudaError_t launch_walk(const World& w, const WalkArgs& a, int n_climb, int cluster, int n_clusters,

@@ -75,6 +75,14 @@ struct fmdp_ctx {
   int8_t* d_ntie = nullptr;
   int32_t* d_stepx = nullptr;  // [slot][cap] exact-fallback count per step (zeroed per call / rollback)
   fmdp::BakRec* d_bak = nullptr;  // [slot][cap] a rolled-back request's previous run (re-convergence)
+  // SURVEY f1 range query (culled walker): rows sorted by x-y cell, cstart offsets (fmdp::World)
+  int32_t* d_cstart = nullptr;
+  size_t cstart_cap = 0;
+  int32_t* d_itmp = nullptr;          // sort scratch
+  size_t itmp_cap = 0;
+  bool index_dirty = true;            // plans added since the last build (they are scanned, unsorted)
+  size_t n_indexed = 0;               // plans in the sorted regions (truncating below them reloads)
+  bool idx_cost = true;               // cost models may assume the range query (not for p2p walks)
   double2* d_vtrace = nullptr; // fmdp_set_trace: [vtrace_n][cap][A] {V*(a), S(a)} per step
   int vtrace_n = 0;
   int32_t* d_queue = nullptr;
@@ -354,7 +362,9 @@ double mean_plans(const fmdp_ctx* ctx) {
   int64_t tot = 0, nz = 0;
   for (int32_t c : ctx->counts)
     if (c) { tot += c; ++nz; }
-  return nz ? (double)tot / nz / ctx->shard_world : 0.0;  // plans per row this GPU evaluates
+  double m = nz ? (double)tot / nz / ctx->shard_world : 0.0;  // plans per row this GPU evaluates
+  if (ctx->launch.cull && ctx->w.cell_n > 0 && ctx->idx_cost) m *= std::min(1.0, 9.0 / ctx->w.cell_n);  // range query
+  return m;
 }
 
 // Cluster size for a round of n_run trajectories: the G minimising waves(G) * t(G) among the
@@ -701,9 +711,85 @@ fmdp_status prepare_requests(fmdp_ctx* ctx, const fmdp_request* reqs, int n, std
 // cost model t(G, k) = step_cycles(plans / k, G) + exchange, exchange = 2400 + 1150 (k - 1)
 // cycles (fit to tools/p2p_probe.py at 3000 / 30000 plans, profiles/r01_p2p_probe.txt), the
 // k clusters resident at once.  Returns k (1: no split) and the cluster size in *G_out.
+// SURVEY f1 range query: sort every row's plans by x-y cell of side L (World::cell_*), L covering a
+// plan's largest well offset k_max |v_h| (measured over the store), R_max, the projection reach and
+// four steps of ownship motion (the walker stages row K + 2 around q_{k-1}; the pre-cull tests row
+// K + 1 against q_k).  Appended plans go past the sorted regions and are scanned in full.  Rows are
+// identical on every rank of a plan-sharded exchange (stable, deterministic sort).
+constexpr int kIndexMinPlansPerRow = 10000;
+fmdp_status build_index(fmdp_ctx* ctx) {
+  fmdp::World& w = ctx->w;
+  w.cell_n = 0;
+  ctx->index_dirty = false;
+  ctx->n_indexed = 0;
+  static const bool off = std::getenv("FMDP_NO_INDEX") != nullptr;  // A/B switch
+  if (off || ctx->wide || ctx->plans.empty()) return FMDP_OK;
+  // only for large rows: at configs[1] scale (3000 plans per row) the staging of up to four pieces
+  // and the cell lookups of the I/O thread cost more per step than the scan of the whole slice
+  // (measured: culled step 5.05 -> 6.26 us), at configs[3] (100k) the range query wins (8.5 -> 6.7
+  // us/step on one 2-CTA cluster instead of 4 x 16 CTAs, batch of 100: 198 -> 61 ms)
+  {
+    int64_t tot = 0, nz = 0;
+    for (int32_t c : ctx->counts)
+      if (c) { tot += c; ++nz; }
+    if (nz == 0 || tot < (int64_t)kIndexMinPlansPerRow * nz) return FMDP_OK;
+  }
+  unsigned long long* d_v = nullptr;
+  if ((d_v = (unsigned long long*)dalloc(ctx, sizeof(unsigned long long))) == nullptr)
+    return fail(ctx, FMDP_E_NOMEM, "index scratch");
+  CK(cudaMemsetAsync(d_v, 0, sizeof(unsigned long long), ctx->stream));
+  CK(fmdp::launch_vmax(ctx->d_rows, w.row_cap, ctx->d_counts, w.horizon, d_v, ctx->stream));
+  unsigned long long v2 = 0;
+  CK(cudaMemcpyAsync(&v2, d_v, sizeof(v2), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  dfree(ctx, d_v);
+  const int64_t vh = (int64_t)std::ceil(std::sqrt((double)v2));
+  int64_t L = (int64_t)w.R_max + w.reach_u + 4LL * w.step_reach_u + (int64_t)w.k_absmax * vh + 2;
+  const int64_t sx = ctx->hi_u[0] - ctx->lo_u[0] + 1, sy = ctx->hi_u[1] - ctx->lo_u[1] + 1;
+  while ((sx + L - 1) / L * ((sy + L - 1) / L) > 16384) L += L / 8 + 1;
+  const int ncx = (int)((sx + L - 1) / L), ncy = (int)((sy + L - 1) / L);
+  if (ncx * ncy < 16) return FMDP_OK;  // too few cells to pay (a 4x4 grid reads 9/16 of a row)
+  const size_t cs_words = (size_t)w.horizon * (ncx * ncy + 1);
+  if (cs_words > ctx->cstart_cap) {
+    fmdp_status e;
+    if ((e = grow(ctx, ctx->d_cstart, cs_words))) return e;
+    ctx->cstart_cap = cs_words;
+  }
+  const int64_t per_row = (int64_t)4 * w.row_cap;
+  const int B = (int)std::max<int64_t>(1, std::min<int64_t>(1024, ((int64_t)1 << 28) / per_row));
+  if ((size_t)B * per_row > ctx->itmp_cap) {
+    fmdp_status e;
+    if ((e = grow(ctx, ctx->d_itmp, (size_t)B * per_row))) return e;
+    ctx->itmp_cap = (size_t)B * per_row;
+  }
+  fmdp::World wi = w;
+  wi.cell_n = ncx * ncy;
+  wi.cell_ncx = ncx;
+  wi.cell_ncy = ncy;
+  wi.cell_l = (int32_t)L;
+  wi.cell_x0 = (int32_t)ctx->lo_u[0];
+  wi.cell_y0 = (int32_t)ctx->lo_u[1];
+  wi.cstart = ctx->d_cstart;
+  for (int64_t K0 = 0; K0 < w.horizon; K0 += B) {
+    const int nr = (int)std::min<int64_t>(B, w.horizon - K0);
+    CK(fmdp::launch_index(ctx->d_rows, w.row_cap, ctx->d_counts, K0, nr, wi, ctx->d_cstart, ctx->d_itmp, ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  w = wi;
+  ctx->n_indexed = ctx->plans.size();
+  return FMDP_OK;
+}
+
+// Before a culled walk: (re)build the range-query index if plans were added since the last build.
+fmdp_status ensure_index(fmdp_ctx* ctx) {
+  if (!ctx->launch.cull || !ctx->index_dirty) return FMDP_OK;
+  return build_index(ctx);
+}
+
 int split_for(fmdp_ctx* ctx, int* G_out) {
   *G_out = 16;
   if (ctx->launch.split == 1) return 1;
+  if (ctx->launch.cull && ctx->w.cell_n > 0 && ctx->idx_cost && ctx->launch.split == 0) return 1;  // range query
   const double plans = mean_plans(ctx);
   int best = 1, bestG = 16;
   double tb = step_cycles(ctx, plans, solo_cluster_size(ctx));
@@ -923,6 +1009,10 @@ fmdp_status schedule_many(fmdp_ctx* ctx, const fmdp_request* reqs, int n, fmdp_r
     return fail(ctx, FMDP_E_BUFFER, "traj_cap must be >= max_steps + 1");
   std::memset(&ctx->stats, 0, sizeof(ctx->stats));
   if (n == 0) return FMDP_OK;
+  {
+    const fmdp_status e = ensure_index(ctx);
+    if (e) return e;
+  }
   std::vector<Req> base;
   fmdp_status st = prepare_requests(ctx, reqs, n, base);
   if (st) return st;
@@ -1682,6 +1772,7 @@ fmdp_status fmdp_add_plans(fmdp_ctx* ctx, int32_t n_plans, const uint64_t* aircr
     }
     p0 = p1;
   }
+  ctx->index_dirty = true;  // the range-query index is rebuilt before the next culled walk
   return FMDP_OK;
 }
 
@@ -1905,11 +1996,13 @@ fmdp_status fmdp_schedule_p2p(fmdp_ctx* ctx, uint64_t aircraft_id, fmdp_vec3 src
   const int N = ctx->x_world, me = ctx->x_me;
   ctx->shard_world = N;
   int G = 16;
+  ctx->idx_cost = false;  // the p2p walker scans its shard of every row (no range query)
   int k = split_for(ctx, &G);
   if (k <= 1) {
     k = 1;
     G = solo_cluster_size(ctx);
   }
+  ctx->idx_cost = true;
   ctx->shard_world = 1;
   unsigned long long* seq = ctx->d_xh_seq;
   int32_t* err = reinterpret_cast<int32_t*>(seq + fmdp::XMAX);
@@ -1991,6 +2084,10 @@ fmdp_status fmdp_schedule_departures(fmdp_ctx* ctx, uint64_t aircraft_id, fmdp_v
   if (ctx && ctx->wide) return fail(ctx, FMDP_E_ARG, "not available with acceleration actions (wide walker)");
   if (!ctx || n_delays < 1 || !delays || !res || !chosen) return fail(ctx, FMDP_E_ARG, "null argument");
   DevGuard dev_guard(ctx->device);  // the context's device for this call, the caller's restored after
+  {
+    const fmdp_status e = ensure_index(ctx);
+    if (e) return e;
+  }
   if (traj && traj_cap < ctx->w.max_steps + 1) return fail(ctx, FMDP_E_BUFFER, "traj_cap must be >= max_steps + 1");
   std::memset(&ctx->stats, 0, sizeof(ctx->stats));
   *chosen = -1;
@@ -2215,6 +2312,33 @@ fmdp_status fmdp_truncate(fmdp_ctx* ctx, uint32_t n_plans) {
   if (!ctx) return FMDP_E_ARG;
   DevGuard dev_guard(ctx->device);  // the context's device for this call, the caller's restored after
   if (n_plans >= ctx->plans.size()) return FMDP_OK;
+  if (n_plans < ctx->n_indexed) {
+    // rows below the range-query index's sorted regions: reload the kept plans from the host
+    // records (empty rows, re-append in id order) and rebuild the index before the next culled walk
+    std::vector<PlanRec> keep(ctx->plans.begin(), ctx->plans.begin() + n_plans);
+    std::fill(ctx->counts.begin(), ctx->counts.end(), 0);
+    CK(cudaMemsetAsync(ctx->d_counts, 0, sizeof(int32_t) * ctx->counts.size(), ctx->stream));
+    ctx->plans.clear();
+    ctx->w.cell_n = 0;
+    ctx->n_indexed = 0;
+    std::vector<uint64_t> ids;
+    std::vector<int64_t> t0;
+    std::vector<int32_t> n;
+    std::vector<int32_t> st;
+    for (const PlanRec& r : keep) {
+      ids.push_back(r.aircraft);
+      t0.push_back(r.t0);
+      n.push_back((int32_t)(r.states.size() / 3));
+      st.insert(st.end(), r.states.begin(), r.states.end());
+    }
+    if (keep.empty()) {
+      ctx->index_dirty = true;
+      CK(cudaStreamSynchronize(ctx->stream));
+      return FMDP_OK;
+    }
+    return fmdp_add_plans(ctx, (int32_t)keep.size(), ids.data(), t0.data(), n.data(),
+                          reinterpret_cast<const fmdp_qpos*>(st.data()), nullptr);
+  }
   // later plans occupy the top slots of each of their rows (appends are in id order)
   for (size_t i = n_plans; i < ctx->plans.size(); ++i) {
     const PlanRec& p = ctx->plans[i];

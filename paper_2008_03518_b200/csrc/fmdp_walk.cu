@@ -18,6 +18,7 @@
 //   a6-a8  every CTA redundantly: combine (Alg 8), max over t, argmax (Alg 9),
 //       advance (Alg 1), terminal tests (Sec IV.I)
 #include <cooperative_groups.h>
+#include <algorithm>
 #include <mutex>
 #include <type_traits>
 #include <cuda_runtime.h>
@@ -144,6 +145,14 @@ template <class T>
 __device__ __forceinline__ T* peer_ptr(cg::cluster_group& cl, T* p, unsigned r, bool solo) {
   return solo ? p : cl.map_shared_rank(p, r);
 }
+// 4-byte asynchronous global -> shared copy (LDGSTS); completion by cp.async.wait_all.
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
@@ -228,6 +237,13 @@ struct Ctl {
   int32_t nsurv[4];           // plans kept by the build, by (step parity, chunk parity)
   unsigned long long xmin;
   int32_t sl_lo[3], sl_n[3], sl_off[3];
+  // range-query staging (culled walker, World::cell_n > 0): ring buffer b holds this CTA's share of
+  // row K's candidate ranges as pn[b] pieces -- piece i = list entries [pst[b][i], pst[b][i+1]) of
+  // the CTA's share, global slots from pgl[b][i], staged at ring position poff[b][i] (-1: beyond the
+  // ring's capacity, read from L2)
+  int32_t pn[3];
+  int32_t pst[3][5], pgl[3][4], poff[3][4];
+  int32_t ilo[4], ihi[4];     // (I/O thread) candidate ranges of the next row to issue, loaded one step ahead
   int32_t hgt[MAX_TURN];      // ground height under Delta_1 of every turn (cp.async target)
   int32_t cs_ok;              // scratch of cs_idle
   int32_t stop[2];            // head-finished flag seen by rank 0 at the top of the step, by parity
@@ -238,7 +254,7 @@ struct Ctl {
   unsigned long long* xp[XMAX];  // multi-GPU: every rank's receive area (loaded once per launch)
   unsigned long long* xip[XNODE];  // two-level exchange: cluster xcl's area on every GPU
 };
-static_assert(sizeof(Ctl) <= 512, "Ctl exceeds its shared-memory slot (Layout::o_ctl)");
+static_assert(sizeof(Ctl) <= 768, "Ctl exceeds its shared-memory slot (Layout::o_ctl)");
 
 // Stage row K's slice for this CTA (slots [lo, lo+n) of n_row active slots): the first CH
 // plans go to ring buffer K % 3 with cp.async.bulk (TMA bulk copy), completion on its
@@ -268,6 +284,122 @@ __device__ __forceinline__ void issue_row(const World& w, int64_t K, int n_row, 
     for (int arr = 0; arr < 4; ++arr)
       bulk_g2s(dst + arr * RAWW, base + (size_t)arr * w.row_cap + lo4, bytes, &bars[b]);
   }
+}
+
+// Range query (culled walker, World::cell_n > 0): the candidate slot ranges of row K around (qx, qy):
+// the three cell rows of the 3x3 block (each one contiguous range: cells are row-major) and the
+// appended plans [cstart[K][cell_n], counts[K]).
+__device__ __forceinline__ void load_ranges(const World& w, int64_t K, int qx, int qy, int (&lo)[4], int (&hi)[4]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) lo[i] = hi[i] = 0;
+  if (K < 0 || K >= w.horizon) return;
+  const int32_t* cs = w.cstart + (size_t)K * (w.cell_n + 1);
+  const int cx = min(max((qx - w.cell_x0) / w.cell_l, 0), w.cell_ncx - 1);
+  const int cy = min(max((qy - w.cell_y0) / w.cell_l, 0), w.cell_ncy - 1);
+  const int xa = max(cx - 1, 0), xb = min(cx + 1, w.cell_ncx - 1);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const int yy = cy - 1 + i;
+    if (yy >= 0 && yy < w.cell_ncy) {
+      lo[i] = __ldg(cs + yy * w.cell_ncx + xa);
+      hi[i] = __ldg(cs + yy * w.cell_ncx + xb + 1);
+    }
+  }
+  lo[3] = __ldg(cs + w.cell_n);
+  hi[3] = __ldg(&w.counts[K]);
+}
+
+// The same ranges fetched asynchronously into shared memory (LDGSTS, no register and no stall for the
+// issuing thread; it waits with cp.async.wait_all before it reads them, a step later).
+__device__ __forceinline__ void fetch_ranges_async(const World& w, int64_t K, int qx, int qy, int32_t* lo, int32_t* hi) {
+  if (K < 0 || K >= w.horizon) {
+    for (int i = 0; i < 4; ++i) lo[i] = hi[i] = 0;
+    return;
+  }
+  const int32_t* cs = w.cstart + (size_t)K * (w.cell_n + 1);
+  const int cx = min(max((qx - w.cell_x0) / w.cell_l, 0), w.cell_ncx - 1);
+  const int cy = min(max((qy - w.cell_y0) / w.cell_l, 0), w.cell_ncy - 1);
+  const int xa = max(cx - 1, 0), xb = min(cx + 1, w.cell_ncx - 1);
+  for (int i = 0; i < 3; ++i) {
+    const int yy = cy - 1 + i;
+    if (yy >= 0 && yy < w.cell_ncy) {
+      cp_async4(&lo[i], cs + yy * w.cell_ncx + xa);
+      cp_async4(&hi[i], cs + yy * w.cell_ncx + xb + 1);
+    } else {
+      lo[i] = hi[i] = 0;
+    }
+  }
+  cp_async4(&lo[3], cs + w.cell_n);
+  cp_async4(&hi[3], &w.counts[K]);
+}
+
+// Stage this CTA's share of row K's candidate ranges (range query): the concatenation of the four
+// ranges is split evenly over the cluster; each intersected piece is copied with cp.async.bulk
+// (16-byte aligned, one copy per SoA array) to the next ring position, pieces past the ring's
+// capacity are read from L2 (poff = -1).  One thread.
+__device__ __forceinline__ void issue_row_idx(const World& w, int64_t K, const int (&lo)[4], const int (&hi)[4],
+                                              unsigned rank, unsigned lgG, int RAWCAP, int32_t* raw, int RAWW,
+                                              uint64_t* bars, Ctl* ctl) {
+  const int b = (int)(K % 3);
+  uint32_t T = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) T += (uint32_t)(hi[i] - lo[i]);
+  const int s0 = (int)((T * rank) >> lgG), s1 = (int)((T * (rank + 1)) >> lgG);
+  int np = 0, base = 0, rpos = 0;
+  uint32_t bytes = 0;
+  int cg4[4], cn4[4], cr[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int ni = hi[i] - lo[i];
+    const int a = max(s0, base), e = min(s1, base + ni);
+    cn4[i] = 0;
+    if (a < e) {
+      const int g = lo[i] + (a - base), cnt = e - a;
+      const int g4 = g & ~3, ge4 = (g + cnt + 3) & ~3;
+      ctl->pst[b][np] = a - s0;
+      ctl->pgl[b][np] = g;
+      if (rpos + (ge4 - g4) <= RAWCAP) {
+        ctl->poff[b][np] = rpos + (g - g4);
+        cg4[i] = g4;
+        cn4[i] = ge4 - g4;
+        cr[i] = rpos;
+        rpos += ge4 - g4;
+        bytes += (uint32_t)(ge4 - g4) * 4u;
+      } else {
+        ctl->poff[b][np] = -1;
+      }
+      ++np;
+    }
+    base += ni;
+  }
+  ctl->pst[b][np] = s1 - s0;
+  ctl->pn[b] = np;
+  ctl->sl_n[b] = s1 - s0;
+  fence_proxy_async();
+  mbar_arrive_tx(&bars[b], 4u * bytes);
+  const int32_t* row = w.rows + (size_t)K * 4 * w.row_cap;
+  int32_t* dst = raw + (size_t)b * 4 * RAWW;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (cn4[i] > 0)
+      for (int arr = 0; arr < 4; ++arr)
+        bulk_g2s(dst + arr * RAWW + cr[i], row + (size_t)arr * w.row_cap + cg4[i], (uint32_t)cn4[i] * 4u, &bars[b]);
+}
+
+// Plan jj of this CTA's share of the row in ring buffer b (range query): {x, y, z, packed v}.
+__device__ __forceinline__ int4 plan_at(const World& w, const Ctl* ctl, const int32_t* raw, int RAWW, int b, int64_t K,
+                                        int jj) {
+  const int np = ctl->pn[b];
+  int i = 0;
+  while (i + 1 < np && jj >= ctl->pst[b][i + 1]) ++i;
+  const int d = jj - ctl->pst[b][i];
+  const int q = ctl->poff[b][i];
+  if (q >= 0) {
+    const int32_t* r = raw + (size_t)b * 4 * RAWW + q + d;
+    return make_int4(r[0], r[RAWW], r[2 * RAWW], r[3 * RAWW]);
+  }
+  const int32_t* g = w.rows + (size_t)K * 4 * w.row_cap + ctl->pgl[b][i] + d;
+  return make_int4(__ldg(g), __ldg(g + w.row_cap), __ldg(g + 2 * w.row_cap), __ldg(g + 3 * w.row_cap));
 }
 
 __device__ __forceinline__ int row_count(const World& w, int64_t K) {
@@ -309,14 +441,7 @@ __device__ __forceinline__ int ground_height(const World& w, int x, int y) {
   const int32_t* p = ground_cell(w, x, y);
   return p ? __ldg(p) : INT_MIN;
 }
-// 4-byte asynchronous global -> shared copy (LDGSTS); completion by cp.async.wait_all.
-__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 
 // ----------------------------------------------------------------------------- co-simulation clock
 // SURVEY f2 (Alg 1: every aircraft decides from the states at clock K, then all
@@ -729,7 +854,12 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
   const bool evalm = (MODE == 3 || MODE == 5) && args.eval;
   // SURVEY f1 culling: MODE 4 is the culled FCFS walker, MODE 0 the full one (each carries only
   // its own build pass); the other instantiations decide at run time
-  const bool cullm = MODE == 4 ? true : (MODE == 0 ? false : args.cull != 0);
+  // MODE 6 = the culled FCFS walker with the range query (large rows; a separate instantiation so
+  // that MODE 4 carries none of its code: measured, its branches cost the 3000-plan step 10 %)
+  constexpr bool CULLW = MODE == 4 || MODE == 6;
+  const bool cullm = CULLW ? true : (MODE == 0 ? false : args.cull != 0);
+  // SURVEY f1 range query: the culled FCFS walker stages only the 3x3 cells around the ownship
+  constexpr bool IDX = MODE == 6;
   // SURVEY f2 co-simulated batch: a separate instantiation, so the FCFS walker carries no
   // co-simulation code at all (measured: any of it on the step path costs ~1.5 %)
   const int cosim = MODE == 1 ? 1 : 0;
@@ -824,7 +954,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
     // re-convergence window: decisions k with reuse_from <= k + 1 < n_old compare their next state
     // (only the culled FCFS walker and the reference instantiation carry it: measured, the full
     // walker's batches gain nothing from it and its step loop would grow, +1.3 % per step)
-    constexpr bool REUSE = MODE == 4 || MODE == 3;
+    constexpr bool REUSE = CULLW || MODE == 3;
     const int bk_lo = (REUSE && args.bak != nullptr && rq.n_old > 0 && !evalm) ? rq.reuse_from - 1 : INT_MAX;
     const int bk_hi = rq.n_old - 1;
     uint32_t min_sep = w.sat_d2;
@@ -856,14 +986,32 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           cs_publish(args, r, rq.t0, qx, qy, qz, CS_PRESENT, s_dxy[psi].x, s_dxy[psi].y, 0);
       }
       const int64_t K0 = rq.t0 + k;
-      const int n0 = row_count(w, K0), n1 = row_count(w, K0 + 1);
-      issue_row(w, K0, n0, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, srank, sworld);
-      issue_row(w, K0 + 1, n1, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, srank, sworld);
+      if (IDX) {
+        int lo[4], hi[4];
+        load_ranges(w, K0, qx, qy, lo, hi);
+        issue_row_idx(w, K0, lo, hi, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl);
+        load_ranges(w, K0 + 1, qx, qy, lo, hi);
+        issue_row_idx(w, K0 + 1, lo, hi, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl);
+      } else {
+        const int n0 = row_count(w, K0), n1 = row_count(w, K0 + 1);
+        issue_row(w, K0, n0, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, srank, sworld);
+        issue_row(w, K0 + 1, n1, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, srank, sworld);
+      }
     }
     {
       const int64_t K0 = rq.t0 + k;
       pending |= (1u << (K0 % 3)) | (1u << ((K0 + 1) % 3));
-      if (tid == NT - 1) cnt2 = row_count(w, K0 + 2);  // the I/O thread's row count, one step ahead
+      if (tid == NT - 1) {  // the I/O thread's row count (range query: candidate ranges), one step ahead
+        cnt2 = row_count(w, K0 + 2);
+        if (IDX) {
+          int lo[4], hi[4];
+          load_ranges(w, K0 + 2, qx, qy, lo, hi);
+          for (int i = 0; i < 4; ++i) {
+            ctl->ilo[i] = lo[i];
+            ctl->ihi[i] = hi[i];
+          }
+        }
+      }
     }
     __syncthreads();
     // terrain candidates (exact cull: the wells that can reach a projected state) of the next
@@ -949,7 +1097,11 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
             int rx = 0, ry = 0, rz = 0, vx = 0, vy = 0, vz = 0;
             if (valid) {
               uint32_t pv;
-              if (j < RAWCAP) {
+              if (IDX) {
+                const int4 P = plan_at(w, ctl, s_raw, RAWW, bK, K, j);
+                rx = P.x - qx; ry = P.y - qy; rz = P.z - qz;
+                pv = (uint32_t)P.w;
+              } else if (j < RAWCAP) {
                 rx = rb[j] - qx; ry = rb[RAWW + j] - qy; rz = rb[2 * RAWW + j] - qz;
                 pv = (uint32_t)rb[3 * RAWW + j];
               } else {
@@ -1097,17 +1249,21 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         // the first chunk's well records are built BEFORE the projection: the build needs only q,
         // the fan origin and row K (staged two steps ahead), so it overlaps the projection's
         // table load, and the projection barrier also publishes the records (one CTA barrier less)
-        if (MODE == 4 && n_chunks > 0 && svn_now >= 0) {
+        if (CULLW && n_chunks > 0 && svn_now >= 0) {
           // pre-culled first chunk (plans j < RAWCAP, staged): the separation minimum over every
           // plan, records (with this step's anchor) of the thread's pre-culled survivors only
           const int nc0 = min(SC, n);
-          for (int jj = tid; jj < nc0; jj += NT)
-            stay = min(stay, clamp_d2(rb[jj] - qx, rb[RAWW + jj] - qy, rb[2 * RAWW + jj] - qz, w.R_max, w.sat_d2));
+          for (int jj = tid; jj < nc0; jj += NT) {
+            const int4 P = IDX ? plan_at(w, ctl, s_raw, RAWW, bK, K, jj) : make_int4(rb[jj], rb[RAWW + jj], rb[2 * RAWW + jj], 0);
+            stay = min(stay, clamp_d2(P.x - qx, P.y - qy, P.z - qz, w.R_max, w.sat_d2));
+          }
           if (!fin) {
             int* counter = &ctl->nsurv[(k & 1) * 2];
             auto rec = [&](int j, bool test) {
-              const int rx = rb[j] - qx, ry = rb[RAWW + j] - qy, rz = rb[2 * RAWW + j] - qz;
-              const uint32_t pv = (uint32_t)rb[3 * RAWW + j];
+              const int4 P = IDX ? plan_at(w, ctl, s_raw, RAWW, bK, K, j)
+                                 : make_int4(rb[j], rb[RAWW + j], rb[2 * RAWW + j], rb[3 * RAWW + j]);
+              const int rx = P.x - qx, ry = P.y - qy, rz = P.z - qz;
+              const uint32_t pv = (uint32_t)P.w;
               const int vx = sext(pv, 11), vy = sext(pv >> 11, 11), vz = sext(pv >> 22, 10);
               if (test && !cull_keep(w, rx, ry, rz, vx, vy, vz)) return;
               const int slot = atomicAdd(counter, 1);
@@ -1259,8 +1415,20 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         //      blocks of the owned actions (from every CTA), the stop flag (from rank 0), V*(a)
         if (tid == NT - 1) {
           if (!evalm && !fin) {
-            issue_row(w, K + 2, cnt2, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, srank, sworld);
-            cnt2 = row_count(w, K + 3);  // consumed next step: latency hidden by this step
+            if (IDX) {  // candidates around q_{k-1} for row K+2 (cell side covers the steps in between)
+              cp_async_wait_all();  // the ranges fetched last step
+              int lo[4], hi[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                lo[i] = ctl->ilo[i];
+                hi[i] = ctl->ihi[i];
+              }
+              issue_row_idx(w, K + 2, lo, hi, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl);
+              fetch_ranges_async(w, K + 3, qx, qy, ctl->ilo, ctl->ihi);
+            } else {
+              issue_row(w, K + 2, cnt2, rank, lgG, RAWCAP, s_raw, RAWW, s_bar, ctl, srank, sworld);
+              cnt2 = row_count(w, K + 3);  // consumed next step: latency hidden by this step
+            }
           }
           ctl->nsurv[((k + 1) & 1) * 2] = 0;  // step k+1, chunk 0 (last used in step k-1)
           const uint32_t bytesA = (xmode != 2 ? 4u * G : 0u) +
@@ -1595,7 +1763,7 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
         // next step, which builds their records with its own anchor (no cross-thread dependence,
         // so no barrier).  The highest threads take the plans (the owner pass-2 warps are the
         // lowest).  Records of a superset of the relevant plans: results bit-identical.
-        if (MODE == 4) {
+        if (CULLW) {
           const int bK1 = bK == 2 ? 0 : bK + 1;
           if (pending & (1u << bK1)) {
             mbar_wait(&s_bar[bK1], (par >> bK1) & 1u);
@@ -1607,9 +1775,10 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           int cnt = 0;
           sv0 = sv1 = -1;
           for (int jj = NT - 1 - tid; jj < nc1; jj += NT) {
-            const uint32_t pv = (uint32_t)rb1[3 * RAWW + jj];
-            if (cull_keep(w, rb1[jj] - qx, rb1[RAWW + jj] - qy, rb1[2 * RAWW + jj] - qz, sext(pv, 11), sext(pv >> 11, 11),
-                          sext(pv >> 22, 10))) {
+            const int4 P = IDX ? plan_at(w, ctl, s_raw, RAWW, bK1, K + 1, jj)
+                               : make_int4(rb1[jj], rb1[RAWW + jj], rb1[2 * RAWW + jj], rb1[3 * RAWW + jj]);
+            const uint32_t pv = (uint32_t)P.w;
+            if (cull_keep(w, P.x - qx, P.y - qy, P.z - qz, sext(pv, 11), sext(pv >> 11, 11), sext(pv >> 22, 10))) {
               if (cnt == 0) sv0 = jj;
               else if (cnt == 1) sv1 = jj;
               ++cnt;
@@ -1984,6 +2153,110 @@ __global__ void backup_kernel(BakRec* bak, const int32_t* traj, const int32_t* h
   }
 }
 
+// ----------------------------------------------------------------------------- range-query index
+__device__ __forceinline__ int cell_of(const World& w, int x, int y) {
+  int cx = (x - w.cell_x0) / w.cell_l, cy = (y - w.cell_y0) / w.cell_l;  // (clamped: conservative, see World)
+  cx = min(max(cx, 0), w.cell_ncx - 1);
+  cy = min(max(cy, 0), w.cell_ncy - 1);
+  return cy * w.cell_ncx + cx;
+}
+
+// One CTA per row: counting sort of slots [0, counts[K]) by cell (histogram, block scan, scatter into
+// tmp, copy back); cstart[K][c] = first slot of cell c, cstart[K][cell_n] = counts[K].
+__global__ void index_kernel(int32_t* rows, int32_t row_cap, const int32_t* counts, int64_t K0, World w,
+                             int32_t* cstart, int32_t* tmp) {
+  extern __shared__ int32_t hist[];  // [cell_n] counts, then cursors
+  __shared__ int32_t part[1024];
+  const int64_t K = K0 + blockIdx.x;
+  const int n = counts[K];
+  const int C = w.cell_n, NT = blockDim.x, tid = threadIdx.x;
+  int32_t* row = rows + (size_t)K * 4 * row_cap;
+  int32_t* cs = cstart + (size_t)K * (C + 1);
+  for (int c = tid; c < C; c += NT) hist[c] = 0;
+  __syncthreads();
+  for (int j = tid; j < n; j += NT) atomicAdd(&hist[cell_of(w, row[j], row[row_cap + j])], 1);
+  __syncthreads();
+  // exclusive scan: thread t owns cells [t*per, (t+1)*per)
+  const int per = (C + NT - 1) / NT;
+  const int c0 = min(C, tid * per), c1 = min(C, c0 + per);
+  int sum = 0;
+  for (int c = c0; c < c1; ++c) sum += hist[c];
+  part[tid] = sum;
+  __syncthreads();
+  if (tid == 0) {
+    int acc = 0;
+    for (int t = 0; t < NT; ++t) {
+      const int v = part[t];
+      part[t] = acc;
+      acc += v;
+    }
+  }
+  __syncthreads();
+  int acc = part[tid];
+  for (int c = c0; c < c1; ++c) {
+    const int v = hist[c];
+    hist[c] = acc;
+    cs[c] = acc;
+    acc += v;
+  }
+  if (tid == 0) cs[C] = n;
+  __syncthreads();
+  // stable scatter (deterministic slot order: every rank of a plan-sharded exchange, which splits
+  // rows by slot ranges, must see the same row): warp 0 walks the row in order, 32 plans at a time,
+  // ranking equal cells within the warp by __match_any_sync
+  int32_t* t = tmp + (size_t)blockIdx.x * 4 * row_cap;
+  if (tid < 32) {
+    const unsigned lt = (1u << tid) - 1u;
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      const int j = j0 + tid;
+      const int c = j < n ? cell_of(w, row[j], row[row_cap + j]) : -1;
+      const unsigned m = __match_any_sync(0xffffffffu, c);
+      if (c >= 0) {
+        const int pos = hist[c] + __popc(m & lt);
+        for (int a = 0; a < 4; ++a) t[(size_t)a * row_cap + pos] = row[(size_t)a * row_cap + j];
+      }
+      __syncwarp();
+      if (c >= 0 && (m & lt) == 0) hist[c] += __popc(m);  // the group's first lane advances the cursor
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int a = 0; a < 4; ++a)
+    for (int j = tid; j < n; j += NT) row[(size_t)a * row_cap + j] = t[(size_t)a * row_cap + j];
+}
+
+__global__ void vmax_kernel(const int32_t* rows, int32_t row_cap, const int32_t* counts, int64_t horizon,
+                            unsigned long long* out) {
+  unsigned long long best = 0;
+  for (int64_t K = blockIdx.x; K < horizon; K += gridDim.x) {
+    const int n = counts[K];
+    const int32_t* vp = rows + (size_t)K * 4 * row_cap + 3 * (size_t)row_cap;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      const uint32_t pv = (uint32_t)vp[j];
+      const long long vx = sext(pv, 11), vy = sext(pv >> 11, 11);
+      best = max(best, (unsigned long long)(vx * vx + vy * vy));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0 && best) atomicMax(out, best);
+}
+
+cudaError_t launch_index(int32_t* rows, int32_t row_cap, const int32_t* counts, int64_t K0, int nrows, const World& w,
+                         int32_t* cstart, int32_t* tmp, cudaStream_t s) {
+  if (nrows <= 0) return cudaSuccess;
+  const int smem = (int)sizeof(int32_t) * w.cell_n;
+  cudaError_t e = cudaFuncSetAttribute(index_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  index_kernel<<<nrows, 1024, smem, s>>>(rows, row_cap, counts, K0, w, cstart, tmp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_vmax(const int32_t* rows, int32_t row_cap, const int32_t* counts, int64_t horizon,
+                        unsigned long long* out, cudaStream_t s) {
+  vmax_kernel<<<(int)std::min<int64_t>(horizon, 2048), 256, 0, s>>>(rows, row_cap, counts, horizon, out);
+  return cudaGetLastError();
+}
+
 // ----------------------------------------------------------------------------- launchers
 int walk_groups_per_warp(int ncol, int max_threads) {
   for (int ngw = 4; ngw > 1; ngw >>= 1)
@@ -2066,7 +2339,8 @@ static cudaError_t max_clusters_t(const World& w, int cluster, int threads, int 
 
 cudaError_t launch_walk(const World& w, const WalkArgs& a, int n_climb, int cluster, int n_clusters, int threads,
                         int chunk, int rawcap, cudaStream_t s) {
-  const int mode = w.wide ? 5 : (a.cosim ? 1 : (a.xmode == 3 ? 2 : ((a.xmode || a.eval || a.prof) ? 3 : (a.cull ? 4 : 0))));
+  const int mode =
+      w.wide ? 5 : (a.cosim ? 1 : (a.xmode == 3 ? 2 : ((a.xmode || a.eval || a.prof) ? 3 : (a.cull ? (w.cell_n > 0 ? 6 : 4) : 0))));
 #define FMDP_LW(c, m) launch_walk_t<c, m>(w, a, cluster, n_clusters, threads, chunk, rawcap, s)
   switch (n_climb * 8 + mode) {
     case 8: return FMDP_LW(1, 0);
@@ -2074,16 +2348,19 @@ cudaError_t launch_walk(const World& w, const WalkArgs& a, int n_climb, int clus
     case 10: return FMDP_LW(1, 2);
     case 11: return FMDP_LW(1, 3);
     case 12: return FMDP_LW(1, 4);
+    case 14: return FMDP_LW(1, 6);
     case 24: return FMDP_LW(3, 0);
     case 25: return FMDP_LW(3, 1);
     case 26: return FMDP_LW(3, 2);
     case 27: return FMDP_LW(3, 3);
     case 28: return FMDP_LW(3, 4);
+    case 30: return FMDP_LW(3, 6);
     case 40: return FMDP_LW(5, 0);
     case 41: return FMDP_LW(5, 1);
     case 42: return FMDP_LW(5, 2);
     case 43: return FMDP_LW(5, 3);
     case 44: return FMDP_LW(5, 4);
+    case 46: return FMDP_LW(5, 6);
     case 29: return FMDP_LW(3, 5);    // wide walker (acceleration actions)
     case 85: return FMDP_LW(10, 5);   // A = 15 x 9 x 10 = 1350
     default: return cudaErrorInvalidValue;
