@@ -746,7 +746,12 @@ fmdp_status build_index(fmdp_ctx* ctx) {
   const int64_t vh = (int64_t)std::ceil(std::sqrt((double)v2));
   int64_t L = (int64_t)w.R_max + w.reach_u + 4LL * w.step_reach_u + (int64_t)w.k_absmax * vh + 2;
   const int64_t sx = ctx->hi_u[0] - ctx->lo_u[0] + 1, sy = ctx->hi_u[1] - ctx->lo_u[1] + 1;
-  while ((sx + L - 1) / L * ((sy + L - 1) / L) > 16384) L += L / 8 + 1;
+  // at most 16384 cells (the sort's shared histogram) and 1 GB of cstart offsets
+  auto cells = [&](int64_t l) { return ((sx + l - 1) / l) * ((sy + l - 1) / l); };
+  while (cells(L) > 16384 || (double)w.horizon * (cells(L) + 1) * 4.0 > (double)(1LL << 30)) {
+    if (cells(L) < 16) return FMDP_OK;
+    L += L / 8 + 1;
+  }
   const int ncx = (int)((sx + L - 1) / L), ncy = (int)((sy + L - 1) / L);
   if (ncx * ncy < 16) return FMDP_OK;  // too few cells to pay (a 4x4 grid reads 9/16 of a row)
   const size_t cs_words = (size_t)w.horizon * (ncx * ncy + 1);
