@@ -301,7 +301,9 @@ fmdp_status fmdp_schedule_sharded(fmdp_ctx* ctx, const fmdp_shard* shard, uint64
  *      Resets this rank's area and tag sequence; every rank must connect before any rank
  *      schedules.
  * fmdp_schedule_p2p: collective -- every rank calls it with the same request, on identical
- * stores and launch settings (the cluster size must agree), concurrently (the walkers wait for
+ * stores (the same plans added in the same order; large rows are sorted by x-y cell the same
+ * deterministic way on every rank before a sharded call) and launch settings (the cluster size
+ * must agree), concurrently (the walkers wait for
  * each other every step).  A peer whose words do not arrive within ~2 s (~8 s for a launch's
  * first step) makes the call return FMDP_E_CUDA ("peer exchange timed out"); the store is not
  * changed; export and connect again before the next call.  world <= 8. */

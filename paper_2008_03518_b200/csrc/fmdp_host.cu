@@ -767,6 +767,7 @@ fmdp_status build_index(fmdp_ctx* ctx) {
     if ((e = grow(ctx, ctx->d_itmp, (size_t)B * per_row))) return e;
     ctx->itmp_cap = (size_t)B * per_row;
   }
+  ctx->n_indexed = ctx->plans.size();  // from here on the rows are permuted: truncating reloads
   fmdp::World wi = w;
   wi.cell_n = ncx * ncy;
   wi.cell_ncx = ncx;
@@ -781,13 +782,14 @@ fmdp_status build_index(fmdp_ctx* ctx) {
   }
   CK(cudaStreamSynchronize(ctx->stream));
   w = wi;
-  ctx->n_indexed = ctx->plans.size();
   return FMDP_OK;
 }
 
 // Before a culled walk: (re)build the range-query index if plans were added since the last build.
-fmdp_status ensure_index(fmdp_ctx* ctx) {
-  if (!ctx->launch.cull || !ctx->index_dirty) return FMDP_OK;
+// Plan-sharded calls (always: sharded = false -> true) sort too, culled or not, so that every rank --
+// same plans added in the same order -- holds the same row order (each evaluates a slot range).
+fmdp_status ensure_index(fmdp_ctx* ctx, bool sharded = false) {
+  if ((!ctx->launch.cull && !sharded) || !ctx->index_dirty) return FMDP_OK;
   return build_index(ctx);
 }
 
@@ -1830,6 +1832,10 @@ fmdp_status fmdp_schedule_sharded(fmdp_ctx* ctx, const fmdp_shard* shard, uint64
       shard->rank >= shard->world)
     return fail(ctx, FMDP_E_ARG, "invalid shard description");
   DevGuard dev_guard(ctx->device);  // the context's device for this call, the caller's restored after
+  {
+    const fmdp_status e = ensure_index(ctx, true);
+    if (e) return e;
+  }
   if (traj && traj_cap < ctx->w.max_steps + 1) return fail(ctx, FMDP_E_BUFFER, "traj_cap must be >= max_steps + 1");
   std::memset(&ctx->stats, 0, sizeof(ctx->stats));
   fmdp_request rq;
@@ -1983,6 +1989,10 @@ fmdp_status fmdp_schedule_p2p(fmdp_ctx* ctx, uint64_t aircraft_id, fmdp_vec3 src
   if (ctx->x_me < 0) return fail(ctx, FMDP_E_ARG, "fmdp_p2p_connect first");
   if (traj && traj_cap < ctx->w.max_steps + 1) return fail(ctx, FMDP_E_BUFFER, "traj_cap must be >= max_steps + 1");
   DevGuard dev_guard(ctx->device);  // the context's device for this call, the caller's restored after
+  {
+    const fmdp_status e = ensure_index(ctx, true);
+    if (e) return e;
+  }
   std::memset(&ctx->stats, 0, sizeof(ctx->stats));
   fmdp_request rq;
   rq.aircraft_id = aircraft_id;
