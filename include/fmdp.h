@@ -146,7 +146,7 @@ typedef struct fmdp_devices {
 typedef struct fmdp_launch {
   int32_t cluster_size;   /* CTAs cooperating on one trajectory (1..16), 0 = auto        */
   int32_t max_walkers;    /* concurrent trajectories in a batch round, 0 = auto          */
-  int32_t threads;        /* threads per CTA, 0 = auto                                   */
+  int32_t threads;        /* cap on threads per CTA (fewer plan groups per warp), 0 = auto */
   int32_t profile;        /* 1: per-phase cycles of CTA 0 (fmdp_stats), FCFS walks only;  */
                           /*    they then run in the reference kernel instantiation      */
   int32_t step_budget;    /* batch: steps the non-head walkers of a slice may run past the head's end, 0 = auto (2) */

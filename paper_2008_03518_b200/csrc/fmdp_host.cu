@@ -318,7 +318,8 @@ fmdp_status ensure_up(fmdp_ctx* ctx, size_t words) {
 }
 
 int threads_for(const fmdp_ctx* ctx) {
-  const int tmax = ctx->C == 1 ? 512 : 384;  // kernel __launch_bounds__
+  int tmax = ctx->C == 1 ? 512 : 384;  // kernel __launch_bounds__
+  if (ctx->launch.threads >= 32) tmax = std::min(tmax, ctx->launch.threads);  // fmdp_launch.threads: a cap
   return fmdp::walk_threads(ctx->w.n_turn * ctx->w.W, tmax);
 }
 
@@ -1699,9 +1700,14 @@ fmdp_status fmdp_set_launch(fmdp_ctx* ctx, const fmdp_launch* l) {
   if (l) n = *l;
   if (n.cluster_size < 0 || n.cluster_size > 16 || (n.cluster_size & (n.cluster_size - 1)))
     return fail(ctx, FMDP_E_ARG, "cluster_size must be 0 or a power of two <= 16");
-  if (n.threads && n.threads != threads_for(ctx))
-    return fail(ctx, FMDP_E_ARG, "threads is derived from the action lattice; pass 0");
+  if (n.threads && (n.threads < 32 || n.threads > (ctx->C == 1 ? 512 : 384)))
+    return fail(ctx, FMDP_E_ARG, "threads: 0 (auto) or a cap in [32, 384] (512 with one climb)");
+  const fmdp_launch prev = ctx->launch;
   ctx->launch = n;
+  if (threads_for(ctx) < 32) {
+    ctx->launch = prev;
+    return fail(ctx, FMDP_E_ARG, "threads cap below one warp of columns");
+  }
   std::memset(ctx->mc_cache, 0, sizeof(ctx->mc_cache));
   std::memset(ctx->mc_cache_cs, 0, sizeof(ctx->mc_cache_cs));
   if (fmdp::walk_smem_bytes(ctx->w, ctx->C, threads_for(ctx), chunk_for(ctx), rawcap_for(ctx), 16) > 227 * 1024)
