@@ -884,6 +884,7 @@ def run_native(args):
         "near_ties_per_batch": sum(r.n_near_ties for r in res_last),
         "exact_band_rescans_per_batch": sum(r.n_exact for r in res_last),
         "states_per_request": states / n, "device_steps_per_batch": steps_dev / args.steps,
+        "speculation_steps_ratio": steps_dev / args.steps / max(1, states),
         "action_plan_evals_per_s": pairs / 5.0 / sc.airspace.W / (tot_ms / 1e3) * world,
         "pair_evals_per_s": pairs / (tot_ms / 1e3) * world,
         "rounds": stats["rounds"], "reruns": stats["reruns"],
@@ -918,6 +919,8 @@ def run_native(args):
             "roofline_frac": cpairs_c * OPS_PER_PAIR / (Mc["walk_ms"] / 1e3) / 1e12 / peak_tops,
             "rounds": Mc["st_all"][-1]["rounds"], "reruns": Mc["st_all"][-1]["reruns"],
             "reconverged": Mc["st_all"][-1]["reconverged"],
+            "device_steps_per_batch": Mc["steps_dev"] / args.steps,
+            "speculation_steps_ratio": Mc["steps_dev"] / args.steps / max(1, sum(r.n_states for r in Mc["res_last"])),
             "reconverged_what": "rolled-back requests whose re-walk met their previous run and took it over "
                                 "(DESIGN.md §6; tests/test_gpu_reuse.py: identical to the sequential loop)",
             "same_results_as_full": same, "clocks": Mc["clocks"]},
