@@ -1462,7 +1462,9 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
           if (tid == 0) ctl->nsurv[(k & 1) * 2 + ((cidx + 1) & 1)] = 0;  // next pass's counter
           if (ns <= CH) {
             hot(ns);
-            __syncthreads();
+            // the next pass rebuilds the records; after the last one nothing writes them before
+            // the post-stage barrier, so a warp that is done goes on to its minima and staging
+            if (cidx + 1 < n_chunks + cosim) __syncthreads();
           } else {  // more survivors than well records (rare): exact fallback, uncompacted
             __syncthreads();
             for (int m0 = c0; m0 < c0 + nc; m0 += CH) {
