@@ -327,10 +327,22 @@ constexpr int kChunk = 512;      // well records / plans per build pass (brute f
 constexpr int kCullChunk = 256;  // well records with f1 culling (survivors only)
 // raw plans staged per row buffer: with culling as much of the slice as shared memory allows
 int rawcap_for(const fmdp_ctx* ctx);
-int chunk_for(const fmdp_ctx* ctx) { return ctx->launch.cull ? kCullChunk : kChunk; }
+// The full path's plans per build pass (= raw plans staged per row buffer): the largest of
+// 1024 / 768 / 512 that fits shared memory -- fewer passes (two CTA barriers and a build each)
+// per step at large stores (configs[3] split request: 30.0 -> 28.7 us/step at 1024; configs[4],
+// A = 85: 768 and 1024 exceed 220 KB, stays 512; tools/chunk_probe.py); one pass either way at
+// configs[1].  (FMDP_TUNE_CHUNK: an override for tools/chunk_probe.py only)
+int full_chunk(const fmdp_ctx* ctx) {
+  static const int env = std::getenv("FMDP_TUNE_CHUNK") ? std::atoi(std::getenv("FMDP_TUNE_CHUNK")) : 0;
+  if (env > 0) return env;
+  for (int c : {1024, 768})
+    if (fmdp::walk_smem_bytes(ctx->w, ctx->C, threads_for(ctx), c, c, 16) <= 220 * 1024) return c;
+  return kChunk;
+}
+int chunk_for(const fmdp_ctx* ctx) { return ctx->launch.cull ? kCullChunk : full_chunk(ctx); }
 
 int rawcap_for(const fmdp_ctx* ctx) {
-  if (!ctx->launch.cull) return kChunk;
+  if (!ctx->launch.cull) return full_chunk(ctx);
   int cap = 3072;
   while (cap > kCullChunk &&
          fmdp::walk_smem_bytes(ctx->w, ctx->C, threads_for(ctx), kCullChunk, cap, 16) > 220 * 1024)
