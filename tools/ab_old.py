@@ -15,7 +15,8 @@ sys.path.insert(0, ROOT)
 import tools.ab_variants as abv  # noqa: E402
 
 
-EXTRA = {}  # working-tree variants (-D flags)
+# working-tree variants (-D flags): FMDP_AB_EXTRA="name=DEFINE[;name=DEFINE...]" (build and run)
+EXTRA = {kv.split("=", 1)[0]: [kv.split("=", 1)[1]] for kv in os.environ.get("FMDP_AB_EXTRA", "").split(";") if "=" in kv}
 
 
 def build(rev="HEAD"):
