@@ -361,7 +361,8 @@ def run_native(args):
                     e2e_value=n * len(e2e_times) / (e2e_ms / 1e3), d2h=d2h,
                     st_all=st_all, res_last=res_last, clocks=clk.summary(), gpu_log=gpu_log,
                     walk_ms=sum(s["device_ms"] for s in st_all), pairs=sum(s["pair_evals"] for s in st_all),
-                    launches=sum(s["kernels"] for s in st_all), steps_dev=sum(s["steps"] for s in st_all))
+                    launches=sum(s["kernels"] for s in st_all),
+                    steps_dev=sum_over_ranks(sum(s["steps"] for s in st_all), world))  # every rank's walkers
 
     def measure_departures(n_req=8, delays=tuple(range(0, 400, 50))):
         # each request tried at len(delays) departures in one call, earliest accepted kept
