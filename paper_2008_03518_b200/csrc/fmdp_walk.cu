@@ -1490,18 +1490,6 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
       FMDP_MARK(PH_HOT)
 
       if (!fin) {
-        // terrain / goal flags of every action's Delta_1 (the candidate next state)
-        if (grp == 0 && col < NCOL && col_l == 0) {
-          const int it = col_it;
-          cp_async_wait_all();
-          const int hgt = ctl->hgt[it];
-#pragma unroll
-          for (int c = 0; c < C; ++c) {
-            const int z = qz + w.climb[c];
-            const int64_t gx = (int64_t)x1 - rq.dst[0], gy = (int64_t)y1 - rq.dst[1], gz = (int64_t)z - rq.dst[2];
-            s_flags[it * C + c] = ((z < 0 || z < hgt) ? 1 : 0) | ((gx * gx + gy * gy + gz * gz < w.cap2) ? 2 : 0);
-          }
-        }
         FMDP_MARK(PH_FLAGS)
         // group minimum inside the warp (rounds over all C*NTAU values are unrolled so the shuffles
         // overlap), then the per-action blocks [t][tau] staged by owner CTA: s_stage[a mod G][a / G]
@@ -1550,6 +1538,20 @@ __global__ void __launch_bounds__(C == 1 ? 512 : 384, 1)
             bulk_s2c(mapa_u32(dst, tid), src, (uint32_t)(4 * n_own_o * BLK), mapa_u32(barA, tid));
             bulk_commit();
           }
+        }
+      }
+      // terrain / goal flags of every action's Delta_1 (the candidate next state): read only after
+      // the V* exchange, so computed here, off the path to the post-stage barrier (published by
+      // the owner pass-1 barrier)
+      if (!fin && grp == 0 && col < NCOL && col_l == 0) {
+        const int it = col_it;
+        cp_async_wait_all();
+        const int hgt = ctl->hgt[it];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const int z = qz + w.climb[c];
+          const int64_t gx = (int64_t)x1 - rq.dst[0], gy = (int64_t)y1 - rq.dst[1], gz = (int64_t)z - rq.dst[2];
+          s_flags[it * C + c] = ((z < 0 || z < hgt) ? 1 : 0) | ((gx * gx + gy * gy + gz * gz < w.cap2) ? 2 : 0);
         }
       }
       // (one-CTA cluster: the pushes were plain stores of this CTA, all issued before this barrier,
